@@ -1,0 +1,238 @@
+/*
+ * fq_abi.h — C-ABI of the B200 (sm_100a) LightSeq inference hot path.
+ *
+ * This is the drop-in boundary under the reference's Python operator API
+ * (`fuseq`, /root/reference/pkg/src/fuseq). Every entry point below replaces
+ * one call site of the reference's kernel layer (`kernels.py`, numba) or GEMM
+ * layer (`tensor.py`, numpy->OpenBLAS); the comment on each names it. The
+ * Python package `paper_2010_13887_b200` binds these with ctypes exactly where
+ * the reference calls `kernels.*` / `np.matmul`.
+ *
+ * Conventions:
+ *  - plain device pointers, element counts and leading dimensions (in
+ *    elements), plus the CUDA stream (`fq_stream_t` = cudaStream_t);
+ *  - no allocation inside, no hidden global state, stream-ordered, reentrant;
+ *    every workspace comes from the caller's (torch-held) arena;
+ *  - return int: 0 = OK; < 0 = error (enum fq_status, message via
+ *    fq_last_error()); the softmax/bad-row count is reported through a device
+ *    int written by the kernel (kernels never raise, kernels.py:139).
+ *  - graph-capturable: entry points that depend on the decode position read it
+ *    from a device int (`d_cur`) so a captured step can be replayed.
+ */
+#ifndef FQ_ABI_H
+#define FQ_ABI_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef void* fq_stream_t;
+
+enum fq_status {
+  FQ_OK = 0,
+  FQ_ERR_DIMENSION = -1,   /* errors.py:8  DimensionError  */
+  FQ_ERR_PARAMETER = -2,   /* errors.py:36 ParameterError  */
+  FQ_ERR_ALIASING = -3,    /* errors.py:12 AliasingError   */
+  FQ_ERR_CAPACITY = -4,    /* errors.py:20 CapacityError   */
+  FQ_ERR_CUDA = -5,        /* launch / runtime failure      */
+  FQ_ERR_UNSUPPORTED = -6  /* dtype/shape combination not built */
+};
+
+enum fq_dtype { FQ_F32 = 0, FQ_BF16 = 1 };
+enum fq_act { FQ_ACT_NONE = 0, FQ_ACT_RELU = 1, FQ_ACT_GELU = 2 }; /* ops.py:61 */
+
+/* ---- library ---------------------------------------------------------- */
+int fq_abi_version(void);
+const char* fq_last_error(void);
+int fq_num_sms(void);
+/* Opt every kernel into the shared-memory sizes it may request, once, before
+ * any stream capture (cudaFuncSetAttribute is not a stream operation). */
+int fq_prepare(void);
+
+/* ---- fused elementwise passes (kernels.py) ---------------------------- */
+
+/* kernels.py:22 layer_norm_kernel. x fp32 [rows, d] (ldx); outputs optional:
+ * out (fp32, ldo) and/or out16 (bf16, ldo16; the next GEMM's operand). */
+int fq_layer_norm(const float* x, int64_t ldx, const float* gamma, const float* beta,
+                  double eps, int64_t rows, int64_t d, float* out, int64_t ldo,
+                  void* out16, int64_t ldo16, fq_stream_t stream);
+
+/* kernels.py:57 bias_residual_layer_norm_kernel: LN((x + bias) + residual). */
+int fq_bias_residual_layer_norm(const float* x, int64_t ldx, const float* bias,
+                                const float* residual, int64_t ldr, const float* gamma,
+                                const float* beta, double eps, int64_t rows, int64_t d,
+                                float* out, int64_t ldo, void* out16, int64_t ldo16,
+                                fq_stream_t stream);
+
+/* kernels.py:39 bias_residual_act_kernel: act(x + bias) (+ residual). In place
+ * allowed (out == x). act: enum fq_act. residual may be NULL. */
+int fq_bias_residual_act(const float* x, int64_t ldx, const float* bias,
+                         const float* residual, int64_t ldr, int act, int64_t rows,
+                         int64_t d, float* out, int64_t ldo, fq_stream_t stream);
+
+/* kernels.py:77 qkv_bias_reshape_kernel: [batch*seq, 3d] + bias -> q,k,v each
+ * contiguous [batch, heads, seq, head_dim]. */
+int fq_qkv_bias_reshape(const float* qkv, int64_t ldq, const float* bias, int64_t batch,
+                        int64_t seq, int64_t heads, int64_t head_dim, float* q, float* k,
+                        float* v, fq_stream_t stream);
+
+/* kernels.py:93 bias_reshape_heads_kernel: [batch*seq, d] + bias -> [batch, heads, seq, hd]. */
+int fq_bias_reshape_heads(const float* x, int64_t ldx, const float* bias, int64_t batch,
+                          int64_t seq, int64_t heads, int64_t head_dim, float* out,
+                          fq_stream_t stream);
+
+/* kernels.py:106 scale_mask_softmax_kernel over a [b, h, q, l] view whose
+ * rows (length l) are `ld` apart (the decoder's sscores[..., :cur] slice,
+ * model.py:574). mask: NULL or [b, l] of {0,-inf}. The number of fully masked
+ * rows is written to *d_bad (device int, may be NULL). In place allowed. */
+int fq_scale_mask_softmax(const float* scores, int64_t ld, float* out, int64_t ldo,
+                          int64_t b, int64_t h, int64_t q, int64_t l, float scale,
+                          const float* mask, int* d_bad, fq_stream_t stream);
+
+/* kernels.py:143 embed_scale_pos_kernel: out[i] = emb[tok[i]]*scale + pos[i%seq + off].
+ * If d_off != NULL the offset is read from device memory (graph replay).
+ * out (fp32) and/or out16 (bf16) may be NULL. */
+int fq_embed_scale_pos(const int64_t* tokens, int64_t n, const float* emb, int64_t d,
+                       float scale, const float* pos, int64_t pos_offset,
+                       const int32_t* d_off, int64_t seq, float* out, void* out16,
+                       fq_stream_t stream);
+
+/* kernels.py:205 kv_append_kernel: dst[r,:,cur,:] = new[r,:,0,:], dst [R,h,S,hd]. */
+int fq_kv_append(const float* new_k, const float* new_v, int64_t cur, int64_t rows,
+                 int64_t heads, int64_t max_seq, int64_t head_dim, float* dst_k,
+                 float* dst_v, fq_stream_t stream);
+
+/* kernels.py:189 kv_gather_append_kernel (ping-pong beam reorder):
+ * dst[r,:,:cur] = src[parents[r],:,:cur]; dst[r,:,cur] = new[r,:,0]. */
+int fq_kv_gather_append(const float* src_k, const float* src_v, const float* new_k,
+                        const float* new_v, const int64_t* parents, int64_t cur,
+                        int64_t rows, int64_t heads, int64_t max_seq, int64_t head_dim,
+                        float* dst_k, float* dst_v, fq_stream_t stream);
+
+/* ---- GEMM (tensor.py:179 gemm, :207 gemm_batched) --------------------- */
+
+/* C[M,N] = epilogue(A[M,K] @ op(B)); op(B) = B [K,N] (ldb) or B^T with B
+ * [N,K] when transpose_b. Epilogue (fused, fp32 math): t = acc (+ C if
+ * accumulate) (+ bias[N]); t = act(t); t = t + residual[M,N] (ldr).
+ * dtypes: a_dtype == b_dtype. FQ_F32 operands -> exact-mode SIMT FFMA kernel
+ * (sequential K order, M-independent). FQ_BF16 operands require transpose_b
+ * (weights pre-laid-out [N,K]) and run on tcgen05 tensor cores (TMEM
+ * accumulators, TMA-fed, fp32 accumulate). c_dtype: FQ_F32 or FQ_BF16. */
+int fq_gemm(const void* a, int a_dtype, int64_t lda, const void* b, int b_dtype, int64_t ldb,
+            int transpose_b, void* c, int c_dtype, int64_t ldc, int64_t M, int64_t N,
+            int64_t K, int accumulate, const float* bias, const float* residual, int64_t ldr,
+            int act, fq_stream_t stream);
+
+/* Strided batched fp32 GEMM over a two-level batch (i0 < n0, i1 < n1):
+ * operand X of batch (i0,i1) starts at X + i0*sX0 + i1*sX1 (elements).
+ * Covers every gemm_batched call site of model.py (QK^T, P.V into the
+ * merged-head strided view, the sscores[..., :cur] slice). */
+int fq_gemm_batched(const float* a, int64_t lda, int64_t sa0, int64_t sa1, const float* b,
+                    int64_t ldb, int64_t sb0, int64_t sb1, int transpose_b, float* c,
+                    int64_t ldc, int64_t sc0, int64_t sc1, int64_t n0, int64_t n1,
+                    int64_t M, int64_t N, int64_t K, fq_stream_t stream);
+
+/* ---- HARS output layer (decode.py) ------------------------------------ */
+
+/* Stage 1, decode.py:58 retrieve -> kernels.py:155 retrieve_kernel, one HBM
+ * sweep per row: strided group maxima (token j -> group j % k), threshold
+ * R = min_g m_g, lse = f64(row_max) + log(sum f64(expf(x - row_max))), and the
+ * candidates x >= R in ascending token order (cand_idx [rows, cand_ld]; rows
+ * whose count exceeds cand_ld are flagged by count > cand_ld and truncated).
+ * k per row: d_k[row] if d_k != NULL (0 = skip row) else k. */
+int fq_retrieve(const float* logits, int64_t ld, int64_t rows, int64_t vocab, int64_t k,
+                const int32_t* d_k, float* group_max, int64_t gm_ld, float* threshold,
+                double* lse, int32_t* cand_idx, int64_t cand_ld, int64_t* cand_count,
+                fq_stream_t stream);
+
+/* Device-resident beam state for `batch` items of beam K (decode.py:140). */
+typedef struct fq_beam_state {
+  int32_t* live;        /* [B] number of live beams (prefixes)            */
+  int32_t* step;        /* [B] BeamState.step                             */
+  int32_t* done;        /* [B] engine.py:154 done flags                    */
+  int32_t* prefix;      /* [B, K, max_len] live prefixes                  */
+  double* cum;          /* [B, K] cum_log_prob                            */
+  int32_t* fin_count;   /* [B]                                            */
+  int32_t* fin_tok;     /* [B, K, max_len] finished sequences             */
+  int32_t* fin_len;     /* [B, K]                                         */
+  double* fin_score;    /* [B, K]                                         */
+  int32_t* last_tok;    /* [B, K] last_tokens                             */
+  int32_t* parent;      /* [B, K] parents (item-local)                    */
+  int32_t* n_done;      /* [1] count of done items                        */
+} fq_beam_state;
+
+/* Stage 2, decode.py:217-240 beam_search_step + :192 _apply_selection +
+ * :186 _finished_insert + :160 should_stop, and the engine's per-item loop
+ * engine.py:148-169, for every item at once (one CTA per item):
+ * rerank score = cum + (f64(logit) - lse), order (-score, token, beam), walk.
+ * len_pow: NULL when the length penalty alpha is 0, else a device table
+ * len_pow[l] = l ** alpha (l = 0..max_len) computed by the host's libm, so the
+ * penalised scores are bit-identical to decode.py:203 / :170.
+ * Writes next-step row tokens/parents (int64 [B*K]) and, when hist != NULL,
+ * the copy-free KV history table hist [B*K, max_len] (positions 0..cur).
+ * The step t (= *d_cur, else the item's step) is the engine's last when
+ * t == max_steps-1 (engine.py:150). Workspace: unused, may be NULL. */
+int fq_hars_select(const float* logits, int64_t ld, const double* lse,
+                   const int32_t* cand_idx, int64_t cand_ld, const int64_t* cand_count,
+                   fq_beam_state st, int64_t batch, int64_t beam, int64_t vocab,
+                   int64_t max_len, int64_t eos, const double* len_pow, const int32_t* d_cur,
+                   int64_t max_steps, int64_t* row_tokens, int64_t* row_parents, int32_t* hist,
+                   void* workspace, int64_t ws_bytes, fq_stream_t stream);
+
+/* groups per row for stage 1: d_k[b*K+i] = i < live[b] && !done[b] ?
+ * min(K + live[b], V) : 0 (decode.py:230). exhaustive -> V. */
+int fq_hars_groups(fq_beam_state st, int64_t batch, int64_t beam, int64_t vocab,
+                   int exhaustive, int32_t* d_k, fq_stream_t stream);
+
+/* Reset beam state to BeamState() (decode.py:145-151) for every item. */
+int fq_beam_state_init(fq_beam_state st, int64_t batch, int64_t beam, int64_t max_len,
+                       fq_stream_t stream);
+
+/* *d_cur += 1 (KVCache.end_step, model.py:508-512). */
+int fq_step_advance(int32_t* d_cur, fq_stream_t stream);
+
+/* ---- fused attention for the device engine (model.py:329-336, :572-604) --- */
+
+/* Encoder self-attention, one pass per (item, head): q,k,v read from the packed
+ * [n, 3d] projection (bias already added), softmax(qk^T*scale + mask) with the
+ * kernels.py:106 numerics (exact mode: f64 exp/sum), ctx written merged-head
+ * [n, d] (ldo) as fp32 (out) and/or bf16 (out16). mask [batch, seq] or NULL.
+ * d_bad counts fully masked rows. exact: 1 = f64 softmax internals. */
+int fq_encoder_attention(const float* qkv, int64_t ldq, int64_t batch, int64_t seq,
+                         int64_t heads, int64_t head_dim, float scale, const float* mask,
+                         float* out, void* out16, int64_t ldo, int exact, int* d_bad,
+                         fq_stream_t stream);
+
+/* Decoder incremental self-attention with copy-free beam reorder: row r at
+ * step cur attends positions t < cur through cache slot (t, hist[r, t]) and
+ * position cur through its own new K/V (taken from the packed sqkv [R, 3d]
+ * projection, bias added), which this call also stores into slot (cur, r).
+ * Cache layout [max_len, R, d] (kv_dtype fp32 or bf16). */
+int fq_decoder_self_attention(const float* sqkv, int64_t ldq, void* kcache, void* vcache,
+                              int kv_dtype, const int32_t* hist, const int32_t* d_cur,
+                              int64_t rows, int64_t heads, int64_t head_dim, int64_t max_len,
+                              float scale, float* out, void* out16, int64_t ldo, int exact,
+                              fq_stream_t stream);
+
+/* Cross-attention: the K beam rows of item b attend to that item's encoder
+ * memory K/V (not replicated per beam, model.py:594-604). ck/cv rows are
+ * [batch*seq] with leading dim ldkv (bias added). mask [batch, seq] or NULL. */
+int fq_cross_attention(const float* cq, int64_t ldcq, const void* ck, const void* cv,
+                       int kv_dtype, int64_t ldkv, int64_t batch, int64_t beam, int64_t seq,
+                       int64_t heads, int64_t head_dim, float scale, const float* mask,
+                       float* out, void* out16, int64_t ldo, int exact, int* d_bad,
+                       fq_stream_t stream);
+
+/* ---- weight preparation (cast once at load) -------------- */
+
+/* dst16[N, K] (bf16, row-major) = src[K, N]^T (fp32) when transpose, else cast. */
+int fq_cast_bf16(const float* src, int64_t rows, int64_t cols, int transpose, void* dst16,
+                 fq_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FQ_ABI_H */

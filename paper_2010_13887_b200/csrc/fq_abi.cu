@@ -1,0 +1,95 @@
+// Library-level entry points: version, error reporting, SM count, weight cast.
+#include <stdarg.h>
+
+#include "fq_common.cuh"
+
+namespace fq {
+
+static thread_local char g_err[512] = "";
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+int launch_status(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_error("%s: %s", what, cudaGetErrorString(e));
+    return FQ_ERR_CUDA;
+  }
+  return FQ_OK;
+}
+
+// dst[N,K] bf16 = src[K,N]^T (transpose) or dst[rows,cols] = src (cast).
+__global__ void cast_bf16_kernel(const float* __restrict__ src, int64_t rows, int64_t cols,
+                                 int transpose, __nv_bfloat16* __restrict__ dst) {
+  __shared__ float tile[32][33];
+  if (!transpose) {
+    int64_t n = rows * cols;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x * blockDim.y +
+                     threadIdx.y * blockDim.x + threadIdx.x;
+         i < n; i += (int64_t)gridDim.x * blockDim.x * blockDim.y)
+      dst[i] = f2bf(src[i]);
+    return;
+  }
+  // 32x32 tiles: read src rows coalesced, write dst rows coalesced.
+  int64_t tiles_c = (cols + 31) / 32;
+  int64_t tiles = ((rows + 31) / 32) * tiles_c;
+  for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+    int64_t r0 = (t / tiles_c) * 32, c0 = (t % tiles_c) * 32;
+    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+      int64_t r = r0 + i, c = c0 + threadIdx.x;
+      tile[i][threadIdx.x] = (r < rows && c < cols) ? src[r * cols + c] : 0.0f;
+    }
+    __syncthreads();
+    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+      int64_t c = c0 + i, r = r0 + threadIdx.x;  // dst row = src col
+      if (c < cols && r < rows) dst[c * rows + r] = f2bf(tile[threadIdx.x][i]);
+    }
+    __syncthreads();
+  }
+}
+
+int attention_prepare();
+int gemm_tc_prepare();
+}  // namespace fq
+
+extern "C" {
+
+int fq_hars_prepare(void);
+
+int fq_prepare(void) {
+  int rc;
+  if ((rc = fq_hars_prepare()) != FQ_OK) return rc;
+  if ((rc = fq::attention_prepare()) != FQ_OK) return rc;
+  if ((rc = fq::gemm_tc_prepare()) != FQ_OK) return rc;
+  return fq::launch_status("fq_prepare");
+}
+
+
+int fq_abi_version(void) { return 1; }
+
+const char* fq_last_error(void) { return fq::g_err; }
+
+int fq_num_sms(void) {
+  int dev = 0, n = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return -1;
+  if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return -1;
+  return n;
+}
+
+int fq_cast_bf16(const float* src, int64_t rows, int64_t cols, int transpose, void* dst16,
+                 fq_stream_t stream) {
+  FQ_CHECK_ARG(src && dst16 && rows > 0 && cols > 0, FQ_ERR_DIMENSION, "fq_cast_bf16: bad args");
+  dim3 block(32, 8);
+  int64_t work = transpose ? ((rows + 31) / 32) * ((cols + 31) / 32) : (rows * cols + 255) / 256;
+  int grid = (int)(work < 148 * 16 ? work : 148 * 16);
+  fq::cast_bf16_kernel<<<grid, block, 0, fq::as_stream(stream)>>>(
+      src, rows, cols, transpose, reinterpret_cast<__nv_bfloat16*>(dst16));
+  return fq::launch_status("fq_cast_bf16");
+}
+
+}  // extern "C"

@@ -1,0 +1,89 @@
+// Shared helpers for the sm_100a kernels behind include/fq_abi.h.
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+#include <stdio.h>
+
+#include "../../include/fq_abi.h"
+
+namespace fq {
+
+// Thread-local last error message for fq_last_error().
+void set_error(const char* fmt, ...);
+
+inline cudaStream_t as_stream(fq_stream_t s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// Map the last launch status to an fq_status.
+int launch_status(const char* what);
+
+#define FQ_CHECK_ARG(cond, code, ...)      \
+  do {                                     \
+    if (!(cond)) {                         \
+      ::fq::set_error(__VA_ARGS__);        \
+      return (code);                       \
+    }                                      \
+  } while (0)
+
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ float warp_min(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fminf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ int warp_sum_i(int v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Block-wide sum of doubles; `red` needs blockDim/32 doubles of smem.
+__device__ __forceinline__ double block_sum(double v, double* red) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  v = warp_sum(v);
+  __syncthreads();
+  if (lane == 0) red[w] = v;
+  __syncthreads();
+  double t = 0.0;
+  for (int i = 0; i < nw; ++i) t += red[i];  // fixed order: deterministic
+  return t;
+}
+
+__device__ __forceinline__ float bf2f(__nv_bfloat16 x) { return __bfloat162float(x); }
+__device__ __forceinline__ __nv_bfloat16 f2bf(float x) { return __float2bfloat16_rn(x); }
+
+// fp32 ops with explicit rounding so nvcc never contracts them into FMA
+// (two separately rounded fp32 operations).
+__device__ __forceinline__ float fmul_rn(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ float fadd_rn(float a, float b) { return __fadd_rn(a, b); }
+
+// Activation on the fp32 pre-activation (kernels.py:45-50): ReLU by compare,
+// GELU = 0.5 t (1 + erf(t/sqrt 2)) evaluated in f64 and rounded to fp32.
+__device__ __forceinline__ float apply_act(float t, int act) {
+  if (act == FQ_ACT_RELU) return t < 0.0f ? 0.0f : t;
+  if (act == FQ_ACT_GELU) {
+    double td = (double)t;
+    return (float)(0.5 * td * (1.0 + erf(td * 0.70710678118654752440)));
+  }
+  return t;
+}
+
+inline int ceil_div(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
+
+}  // namespace fq

@@ -1,0 +1,296 @@
+// Fused single-pass elementwise kernels (reference: pkg/src/fuseq/kernels.py).
+//
+// Numerics follow SURVEY.md Appendix A (the numba-inferred types of the
+// reference kernels): f64 statistics for layer norm and softmax, fp32
+// two-rounding affine epilogues (no FMA contraction: __fmul_rn/__fadd_rn),
+// f64 erf for GELU. Reductions are warp/block trees in a fixed order, so the
+// results are deterministic run to run (the reference is deterministic too).
+//
+// All are HBM-bound: algorithmic bytes = inputs read + outputs written.
+#include "fq_common.cuh"
+
+namespace fq {
+
+// ---------------------------------------------------------------------------
+// layer norm / bias+residual+layer norm: one CTA per row, the row staged in
+// shared memory so the three sweeps of kernels.py:22-35 read HBM once.
+// ---------------------------------------------------------------------------
+template <bool kBiasRes>
+__global__ void __launch_bounds__(256) layer_norm_kernel(
+    const float* __restrict__ x, int64_t ldx, const float* __restrict__ bias,
+    const float* __restrict__ res, int64_t ldr, const float* __restrict__ gamma,
+    const float* __restrict__ beta, double eps, int d, float* __restrict__ out, int64_t ldo,
+    __nv_bfloat16* __restrict__ out16, int64_t ldo16) {
+  extern __shared__ float srow[];
+  __shared__ double red[8];
+  const int64_t row = blockIdx.x;
+  const float* xr = x + row * ldx;
+  double s = 0.0;
+  for (int j = threadIdx.x; j < d; j += blockDim.x) {
+    float u = xr[j];
+    if (kBiasRes) u = fadd_rn(fadd_rn(u, bias[j]), res[row * ldr + j]);  // kernels.py:64
+    srow[j] = u;
+    s += (double)u;
+  }
+  const double mean = block_sum(s, red) / d;
+  double v = 0.0;
+  for (int j = threadIdx.x; j < d; j += blockDim.x) {
+    double t = (double)srow[j] - mean;
+    v += t * t;
+  }
+  const double inv = 1.0 / sqrt(block_sum(v, red) / d + eps);
+  for (int j = threadIdx.x; j < d; j += blockDim.x) {
+    float n = (float)(((double)srow[j] - mean) * inv);
+    float o = fadd_rn(fmul_rn(n, gamma[j]), beta[j]);  // kernels.py:35
+    if (out) out[row * ldo + j] = o;
+    if (out16) out16[row * ldo16 + j] = f2bf(o);
+  }
+}
+
+// act(x + bias) (+ residual), kernels.py:39-53.
+__global__ void bias_residual_act_kernel(const float* __restrict__ x, int64_t ldx,
+                                         const float* __restrict__ bias,
+                                         const float* __restrict__ res, int64_t ldr, int act,
+                                         int64_t rows, int d, float* out, int64_t ldo) {
+  const int64_t n = rows * d;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r = i / d;
+    int j = (int)(i - r * d);
+    float t = apply_act(fadd_rn(x[r * ldx + j], bias[j]), act);
+    if (res) t = fadd_rn(t, res[r * ldr + j]);  // f64 sum of two fp32, rounded = RN fp32 add
+    out[r * ldo + j] = t;
+  }
+}
+
+// [batch*seq, parts*d] + bias -> parts x [batch, heads, seq, hd] (kernels.py:77-102).
+__global__ void bias_reshape_kernel(const float* __restrict__ x, int64_t ldx,
+                                    const float* __restrict__ bias, int64_t seq, int heads,
+                                    int hd, int parts, int64_t n_rows, float* __restrict__ o0,
+                                    float* __restrict__ o1, float* __restrict__ o2) {
+  const int d = heads * hd;
+  const int64_t per_part = n_rows * d;
+  const int64_t total = per_part * parts;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    int part = (int)(idx / per_part);
+    int64_t rem = idx - part * per_part;
+    int64_t i = rem / d;  // input row (b*seq + s)
+    int j = (int)(rem - i * d);
+    float v = fadd_rn(x[i * ldx + part * d + j], bias[part * d + j]);
+    int64_t b = i / seq, s = i - b * seq;
+    int h = j / hd, e = j - h * hd;
+    float* o = part == 0 ? o0 : (part == 1 ? o1 : o2);
+    o[((b * heads + h) * seq + s) * hd + e] = v;
+  }
+}
+
+// softmax(scores*scale + mask) per row, kernels.py:106-139: one warp per row.
+__global__ void scale_mask_softmax_kernel(const float* __restrict__ sc, int64_t ld, float* out,
+                                          int64_t ldo, int64_t rows, int64_t rows_per_b,
+                                          int l, float scale, const float* __restrict__ mask,
+                                          int* d_bad) {
+  const int lane = threadIdx.x & 31;
+  const int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (row >= rows) return;
+  const float* s = sc + row * ld;
+  const float* mk = mask ? mask + (row / rows_per_b) * l : nullptr;
+  float m = -INFINITY;
+  for (int j = lane; j < l; j += 32) {
+    float t = fmul_rn(s[j], scale);
+    if (mk) t = fadd_rn(t, mk[j]);
+    m = fmaxf(m, t);
+  }
+  m = warp_max(m);
+  if (m == -INFINITY) {  // kernels.py:121-123: counted, row left untouched
+    if (lane == 0 && d_bad) atomicAdd(d_bad, 1);
+    return;
+  }
+  double acc = 0.0;
+  for (int j = lane; j < l; j += 32) {
+    float t = fmul_rn(s[j], scale);
+    if (mk) t = fadd_rn(t, mk[j]);
+    acc += exp((double)t - (double)m);
+  }
+  const double inv = 1.0 / warp_sum(acc);
+  float* o = out + row * ldo;
+  for (int j = lane; j < l; j += 32) {
+    float t = fmul_rn(s[j], scale);
+    if (mk) t = fadd_rn(t, mk[j]);
+    o[j] = (t == -INFINITY) ? 0.0f : (float)(exp((double)t - (double)m) * inv);
+  }
+}
+
+// out[i] = emb[tok[i]] * scale + pos[i % seq + off], kernels.py:143-151.
+__global__ void embed_kernel(const int64_t* __restrict__ tok, int64_t n,
+                             const float* __restrict__ emb, int d, float scale,
+                             const float* __restrict__ pos, int64_t off,
+                             const int32_t* __restrict__ d_off, int64_t seq, float* out,
+                             __nv_bfloat16* out16) {
+  const int64_t base = d_off ? (int64_t)(*d_off) : off;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < n * d;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    int64_t i = idx / d;
+    int j = (int)(idx - i * d);
+    int64_t p = i % seq + base;
+    float v = fadd_rn(fmul_rn(emb[tok[i] * d + j], scale), pos[p * d + j]);
+    if (out) out[idx] = v;
+    if (out16) out16[idx] = f2bf(v);
+  }
+}
+
+// KV cache refresh, kernels.py:189-211: dst [R, h, S, hd].
+__global__ void kv_kernel(const float* __restrict__ sk, const float* __restrict__ sv,
+                          const float* __restrict__ nk, const float* __restrict__ nv,
+                          const int64_t* __restrict__ parents, int64_t cur, int64_t rows,
+                          int heads, int64_t S, int hd, float* dk, float* dv) {
+  const int64_t hist = parents ? cur + 1 : 1;  // positions written per (r, h)
+  const int64_t total = rows * heads * hist * hd;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    int e = (int)(idx % hd);
+    int64_t t = (idx / hd) % hist;
+    int64_t rh = idx / (hd * hist);
+    int h = (int)(rh % heads);
+    int64_t r = rh / heads;
+    int64_t pos = parents ? t : cur;
+    int64_t dst = ((r * heads + h) * S + pos) * hd + e;
+    if (pos == cur) {
+      int64_t src = (r * heads + h) * hd + e;  // new [R, h, 1, hd]
+      dk[dst] = nk[src];
+      dv[dst] = nv[src];
+    } else {
+      int64_t src = ((parents[r] * heads + h) * S + pos) * hd + e;
+      dk[dst] = sk[src];
+      dv[dst] = sv[src];
+    }
+  }
+}
+
+static inline int grid_for(int64_t n, int threads) {
+  int64_t g = (n + threads - 1) / threads;
+  const int64_t cap = 148LL * 32;
+  return (int)(g < 1 ? 1 : (g > cap ? cap : g));
+}
+
+}  // namespace fq
+
+using namespace fq;
+
+extern "C" {
+
+int fq_layer_norm(const float* x, int64_t ldx, const float* gamma, const float* beta,
+                  double eps, int64_t rows, int64_t d, float* out, int64_t ldo, void* out16,
+                  int64_t ldo16, fq_stream_t stream) {
+  FQ_CHECK_ARG(x && gamma && beta && rows >= 0 && d > 0 && d <= 12288 && (out || out16),
+               FQ_ERR_DIMENSION, "fq_layer_norm: bad shape rows=%lld d=%lld", (long long)rows,
+               (long long)d);
+  FQ_CHECK_ARG(eps >= 0, FQ_ERR_DIMENSION, "eps must be non-negative");
+  if (rows == 0) return FQ_OK;
+  int threads = d >= 1024 ? 256 : 128;
+  layer_norm_kernel<false><<<(unsigned)rows, threads, d * sizeof(float), as_stream(stream)>>>(
+      x, ldx, nullptr, nullptr, 0, gamma, beta, eps, (int)d, out, ldo,
+      reinterpret_cast<__nv_bfloat16*>(out16), ldo16);
+  return launch_status("fq_layer_norm");
+}
+
+int fq_bias_residual_layer_norm(const float* x, int64_t ldx, const float* bias,
+                                const float* residual, int64_t ldr, const float* gamma,
+                                const float* beta, double eps, int64_t rows, int64_t d,
+                                float* out, int64_t ldo, void* out16, int64_t ldo16,
+                                fq_stream_t stream) {
+  FQ_CHECK_ARG(x && bias && residual && gamma && beta && d > 0 && d <= 12288 && (out || out16),
+               FQ_ERR_DIMENSION, "fq_bias_residual_layer_norm: bad args");
+  if (rows == 0) return FQ_OK;
+  int threads = d >= 1024 ? 256 : 128;
+  layer_norm_kernel<true><<<(unsigned)rows, threads, d * sizeof(float), as_stream(stream)>>>(
+      x, ldx, bias, residual, ldr, gamma, beta, eps, (int)d, out, ldo,
+      reinterpret_cast<__nv_bfloat16*>(out16), ldo16);
+  return launch_status("fq_bias_residual_layer_norm");
+}
+
+int fq_bias_residual_act(const float* x, int64_t ldx, const float* bias, const float* residual,
+                         int64_t ldr, int act, int64_t rows, int64_t d, float* out, int64_t ldo,
+                         fq_stream_t stream) {
+  FQ_CHECK_ARG(x && bias && out && d > 0, FQ_ERR_DIMENSION, "fq_bias_residual_act: bad args");
+  FQ_CHECK_ARG(act >= 0 && act <= 2, FQ_ERR_PARAMETER, "unknown activation %d", act);
+  if (rows == 0) return FQ_OK;
+  bias_residual_act_kernel<<<grid_for(rows * d, 256), 256, 0, as_stream(stream)>>>(
+      x, ldx, bias, residual, ldr, act, rows, (int)d, out, ldo);
+  return launch_status("fq_bias_residual_act");
+}
+
+int fq_qkv_bias_reshape(const float* qkv, int64_t ldq, const float* bias, int64_t batch,
+                        int64_t seq, int64_t heads, int64_t head_dim, float* q, float* k,
+                        float* v, fq_stream_t stream) {
+  FQ_CHECK_ARG(qkv && bias && q && k && v && batch > 0 && seq > 0 && heads > 0 && head_dim > 0,
+               FQ_ERR_DIMENSION, "fq_qkv_bias_reshape: bad args");
+  int64_t n = batch * seq * heads * head_dim * 3;
+  bias_reshape_kernel<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(
+      qkv, ldq, bias, seq, (int)heads, (int)head_dim, 3, batch * seq, q, k, v);
+  return launch_status("fq_qkv_bias_reshape");
+}
+
+int fq_bias_reshape_heads(const float* x, int64_t ldx, const float* bias, int64_t batch,
+                          int64_t seq, int64_t heads, int64_t head_dim, float* out,
+                          fq_stream_t stream) {
+  FQ_CHECK_ARG(x && bias && out && batch > 0 && seq > 0 && heads > 0 && head_dim > 0,
+               FQ_ERR_DIMENSION, "fq_bias_reshape_heads: bad args");
+  int64_t n = batch * seq * heads * head_dim;
+  bias_reshape_kernel<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(
+      x, ldx, bias, seq, (int)heads, (int)head_dim, 1, batch * seq, out, nullptr, nullptr);
+  return launch_status("fq_bias_reshape_heads");
+}
+
+int fq_scale_mask_softmax(const float* scores, int64_t ld, float* out, int64_t ldo, int64_t b,
+                          int64_t h, int64_t q, int64_t l, float scale, const float* mask,
+                          int* d_bad, fq_stream_t stream) {
+  FQ_CHECK_ARG(scores && out && b > 0 && h > 0 && q > 0 && l > 0 && ld >= l && ldo >= l,
+               FQ_ERR_DIMENSION, "fq_scale_mask_softmax: bad shape");
+  int64_t rows = b * h * q;
+  int64_t threads = rows * 32;
+  scale_mask_softmax_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, as_stream(stream)>>>(
+      scores, ld, out, ldo, rows, h * q, (int)l, scale, mask, d_bad);
+  return launch_status("fq_scale_mask_softmax");
+}
+
+int fq_embed_scale_pos(const int64_t* tokens, int64_t n, const float* emb, int64_t d,
+                       float scale, const float* pos, int64_t pos_offset, const int32_t* d_off,
+                       int64_t seq, float* out, void* out16, fq_stream_t stream) {
+  FQ_CHECK_ARG(tokens && emb && pos && d > 0 && seq > 0 && (out || out16), FQ_ERR_DIMENSION,
+               "fq_embed_scale_pos: bad args");
+  if (n == 0) return FQ_OK;
+  embed_kernel<<<grid_for(n * d, 256), 256, 0, as_stream(stream)>>>(
+      tokens, n, emb, (int)d, scale, pos, pos_offset, d_off, seq, out,
+      reinterpret_cast<__nv_bfloat16*>(out16));
+  return launch_status("fq_embed_scale_pos");
+}
+
+int fq_kv_append(const float* new_k, const float* new_v, int64_t cur, int64_t rows,
+                 int64_t heads, int64_t max_seq, int64_t head_dim, float* dst_k, float* dst_v,
+                 fq_stream_t stream) {
+  FQ_CHECK_ARG(cur >= 0 && cur < max_seq, FQ_ERR_CAPACITY, "KV cache full at %lld positions",
+               (long long)cur);
+  int64_t n = rows * heads * head_dim;
+  kv_kernel<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(
+      nullptr, nullptr, new_k, new_v, nullptr, cur, rows, (int)heads, max_seq, (int)head_dim,
+      dst_k, dst_v);
+  return launch_status("fq_kv_append");
+}
+
+int fq_kv_gather_append(const float* src_k, const float* src_v, const float* new_k,
+                        const float* new_v, const int64_t* parents, int64_t cur, int64_t rows,
+                        int64_t heads, int64_t max_seq, int64_t head_dim, float* dst_k,
+                        float* dst_v, fq_stream_t stream) {
+  FQ_CHECK_ARG(cur >= 0 && cur < max_seq, FQ_ERR_CAPACITY, "KV cache full at %lld positions",
+               (long long)cur);
+  FQ_CHECK_ARG(src_k != dst_k && src_v != dst_v, FQ_ERR_ALIASING,
+               "ping-pong gather must not read and write the same slot");
+  int64_t n = rows * heads * (cur + 1) * head_dim;
+  kv_kernel<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(
+      src_k, src_v, new_k, new_v, parents, cur, rows, (int)heads, max_seq, (int)head_dim, dst_k,
+      dst_v);
+  return launch_status("fq_kv_gather_append");
+}
+
+}  // extern "C"

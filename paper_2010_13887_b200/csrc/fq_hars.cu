@@ -1,0 +1,550 @@
+// Hierarchical Auto-Regressive Search (HARS) output layer on sm_100a.
+//
+// Stage 1 (retrieve): reference decode.py:58-92 -> kernels.py:155-185. One CTA
+// per logit row. The row is read from HBM exactly once with 128-bit loads and
+// staged in shared memory (a 32k fp32 row is 128 KB; up to 51200 columns
+// fit); the group-maxima sweep runs on the loads, the logsumexp + candidate
+// sweep runs from shared memory. Grouping is the reference's deterministic
+// stride (token j -> group j % k): with a block width that is a multiple of
+// k, every thread's elements fall in fixed groups, so each thread keeps one
+// running maximum per vector lane and no atomics are needed.
+// Numerics: fp32 x - row_max, fp32 expf, f64 sum,
+// lse = f64(row_max) + log(sum); inclusive x >= R; candidates ascending.
+//
+// Stage 2 (select): decode.py:217-240 beam_search_step + :186-214 selection
+// + :160-171 should_stop + engine.py:148-169, one CTA per batch item, on the
+// device-resident beam state. Scores are f64 cum + (f64(logit) - lse) and the
+// order is (-score, token, beam), exactly the reference's sort key.
+#include "fq_common.cuh"
+
+namespace fq {
+
+constexpr int kRetrieveThreads = 1024;
+constexpr int kMaxStageCols = 51200;  // 200 KB of fp32 staged per row
+
+// block-wide exclusive scan of small ints (blockDim multiple of 32).
+__device__ __forceinline__ int block_excl_scan(int v, int* warp_tot, int* total) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  int incl = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  if (lane == 31) warp_tot[w] = incl;
+  __syncthreads();
+  if (w == 0) {
+    int x = lane < nw ? warp_tot[lane] : 0;
+    int ix = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int t = __shfl_up_sync(0xffffffffu, ix, o);
+      if (lane >= o) ix += t;
+    }
+    if (lane < nw) warp_tot[lane] = ix - x;
+    if (lane == 31) *total = ix;
+  }
+  __syncthreads();
+  return incl - v + warp_tot[w];
+}
+
+__global__ void __launch_bounds__(kRetrieveThreads) retrieve_kernel(
+    const float* __restrict__ logits, int64_t ld, int V, int k_fixed,
+    const int32_t* __restrict__ d_k, float* __restrict__ group_max, int64_t gm_ld,
+    float* __restrict__ threshold, double* __restrict__ lse, int32_t* __restrict__ cand_idx,
+    int64_t cand_ld, int64_t* __restrict__ cand_count, int stage) {
+  extern __shared__ __align__(16) float srow[];
+  __shared__ float part_max[kRetrieveThreads * 4];
+  __shared__ float gmax_s[32];
+  __shared__ float s_R, s_max;
+  __shared__ double red[32];
+  __shared__ int warp_tot[32];
+  __shared__ int s_total;
+
+  const int64_t row = blockIdx.x;
+  const int k = d_k ? d_k[row] : k_fixed;
+  if (k <= 0) {
+    if (threadIdx.x == 0) cand_count[row] = 0;
+    return;
+  }
+  const float* x = logits + row * ld;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, nw = blockDim.x >> 5;
+  const bool vec = ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
+  const bool small_k = k <= 32;
+
+  // ---------------- pass 1: group maxima (one HBM read, staged) -------------
+  if (small_k) {
+    // T threads, T % k == 0: thread t only ever sees groups (4t + c) % k.
+    const int T = blockDim.x - (blockDim.x % k);
+    float m[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+    if (tid < T) {
+      if (vec) {
+        const int nvec = V >> 2;
+        const float4* x4 = reinterpret_cast<const float4*>(x);
+#pragma unroll 4
+        for (int v = tid; v < nvec; v += T) {
+          float4 q = __ldcs(x4 + v);  // streaming: read once
+          m[0] = fmaxf(m[0], q.x); m[1] = fmaxf(m[1], q.y);
+          m[2] = fmaxf(m[2], q.z); m[3] = fmaxf(m[3], q.w);
+          if (stage) reinterpret_cast<float4*>(srow)[v] = q;
+        }
+        // tail (V % 4 elements): staged here, folded into its group after the reduction
+        if (stage)
+          for (int j = (nvec << 2) + tid; j < V; j += T) srow[j] = x[j];
+      } else {
+#pragma unroll 4
+        for (int j = tid; j < V; j += T) {
+          float q = __ldcs(x + j);
+          m[0] = fmaxf(m[0], q);
+          if (stage) srow[j] = q;
+        }
+      }
+    }
+    // partials: vec -> element index e = 4*tid + c (group e % k); scalar -> e = tid
+    const int per = vec ? 4 : 1;
+    const int nparts = T * per;
+    if (tid < T) {
+      for (int c = 0; c < per; ++c) part_max[tid * per + c] = m[c];
+    }
+    __syncthreads();
+    // warp g reduces entries e = g (mod k)
+    for (int g = w; g < k; g += nw) {
+      float mm = -INFINITY;
+      for (int e = g + lane * k; e < nparts; e += 32 * k) mm = fmaxf(mm, part_max[e]);
+      mm = warp_max(mm);
+      if (lane == 0) gmax_s[g] = mm;
+    }
+    __syncthreads();
+    // vec tail elements (j >= 4*nvec): fold into their group directly
+    if (vec && tid == 0) {
+      for (int j = (V >> 2) << 2; j < V; ++j) gmax_s[j % k] = fmaxf(gmax_s[j % k], x[j]);
+    }
+    __syncthreads();
+    if (tid == 0) {
+      float R = gmax_s[0], M = gmax_s[0];
+      for (int g = 0; g < k; ++g) {
+        R = fminf(R, gmax_s[g]);
+        M = fmaxf(M, gmax_s[g]);
+        if (group_max) group_max[row * gm_ld + g] = gmax_s[g];
+      }
+      s_R = R;
+      s_max = M;
+    }
+    __syncthreads();
+  } else {
+    // large k (up to V): thread per group, strided columns stay coalesced
+    float R = INFINITY, M = -INFINITY;
+    for (int g = tid; g < k; g += blockDim.x) {
+      float mm = -INFINITY;
+      for (int j = g; j < V; j += k) {
+        float q = x[j];
+        mm = fmaxf(mm, q);
+        if (stage) srow[j] = q;
+      }
+      if (group_max) group_max[row * gm_ld + g] = mm;
+      R = fminf(R, mm);
+      M = fmaxf(M, mm);
+    }
+    R = warp_min(R);
+    M = warp_max(M);
+    if (lane == 0) { part_max[w] = R; part_max[32 + w] = M; }
+    __syncthreads();
+    if (tid == 0) {
+      float r = part_max[0], mm = part_max[32];
+      for (int i = 1; i < nw; ++i) { r = fminf(r, part_max[i]); mm = fmaxf(mm, part_max[32 + i]); }
+      s_R = r;
+      s_max = mm;
+    }
+    __syncthreads();
+  }
+  const float R = s_R, M = s_max;
+  const float* src = stage ? srow : x;
+
+  // ---------------- pass 2: logsumexp + ordered candidate compaction ----------
+  double acc = 0.0;
+  int64_t base = 0;
+  int32_t* out_idx = cand_idx + row * cand_ld;
+  const int chunk = blockDim.x * 4;
+  for (int c0 = 0; c0 < V; c0 += chunk) {
+    int flags = 0;
+    float v4[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      int j = c0 + tid * 4 + c;
+      v4[c] = (j < V) ? src[j] : -INFINITY;
+      if (j < V) {
+        acc += (double)expf(__fsub_rn(v4[c], M));
+        if (v4[c] >= R) flags |= 1 << c;
+      }
+    }
+    if (!__syncthreads_or(flags)) continue;  // no survivors in this chunk
+    int cnt = __popc(flags);
+    int off = block_excl_scan(cnt, warp_tot, &s_total);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      if (flags & (1 << c)) {
+        int64_t pos = base + off;
+        if (pos < cand_ld) out_idx[pos] = c0 + tid * 4 + c;
+        ++off;
+      }
+    }
+    base += s_total;
+    __syncthreads();
+  }
+  const double s = block_sum(acc, red);
+  if (tid == 0) {
+    if (threshold) threshold[row] = R;
+    lse[row] = (double)M + log(s);
+    cand_count[row] = base;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// stage 2
+// ---------------------------------------------------------------------------
+constexpr int kSelThreads = 256;
+constexpr int kSelCap = 1024;  // candidates ranked in shared memory
+constexpr int kMaxBeam = 16;
+
+struct Cand {
+  double s;
+  int32_t tok;
+  int32_t beam;
+};
+
+__device__ __forceinline__ bool better(const Cand& a, const Cand& b) {
+  if (a.s != b.s) return a.s > b.s;
+  if (a.tok != b.tok) return a.tok < b.tok;
+  return a.beam < b.beam;
+}
+
+// python list order: lexicographic, a proper prefix sorts first
+__device__ bool seq_less(const int32_t* a, int la, const int32_t* b, int lb) {
+  int n = la < lb ? la : lb;
+  for (int i = 0; i < n; ++i)
+    if (a[i] != b[i]) return a[i] < b[i];
+  return la < lb;
+}
+
+__global__ void __launch_bounds__(kSelThreads) hars_select_kernel(
+    const float* __restrict__ logits, int64_t ld, const double* __restrict__ lse,
+    const int32_t* __restrict__ cand_idx, int64_t cand_ld,
+    const int64_t* __restrict__ cand_count, fq_beam_state st, int K, int max_len, int eos,
+    const double* __restrict__ len_pow, const int32_t* __restrict__ d_cur, int64_t max_steps, int64_t* row_tokens,
+    int64_t* row_parents, int32_t* hist) {
+  extern __shared__ int32_t sh[];  // old prefixes [K][max_len] then old hist [K][max_len]
+  __shared__ Cand cands[kSelCap];
+  __shared__ Cand picks[2 * kMaxBeam];
+  __shared__ int64_t offs[kMaxBeam + 1];
+  __shared__ int s_new_live, s_done, s_npick;
+  __shared__ int new_par[kMaxBeam], new_tok[kMaxBeam];
+  __shared__ double new_cum[kMaxBeam];
+  __shared__ double red_s[kSelThreads / 32];
+  __shared__ int red_t[kSelThreads / 32], red_b[kSelThreads / 32];
+
+  const int b = blockIdx.x, tid = threadIdx.x;
+  const int64_t row0 = (int64_t)b * K;
+  int32_t* old_pref = sh;
+  int32_t* old_hist = sh + K * max_len;
+
+  if (st.done[b]) {  // engine.py:148-155: dead rows get parent row0, token 0
+    if (tid < K) {
+      row_parents[row0 + tid] = row0;
+      row_tokens[row0 + tid] = 0;
+    }
+    return;
+  }
+  const int live = st.live[b];
+  const int step = st.step[b];
+  const int cur = d_cur ? *d_cur : step;
+  const bool last_step = (int64_t)cur == max_steps - 1;
+  if (tid == 0) {
+    offs[0] = 0;
+    for (int i = 0; i < live; ++i) offs[i + 1] = offs[i] + cand_count[row0 + i];
+  }
+  for (int i = tid; i < K * max_len; i += blockDim.x) {
+    old_pref[i] = st.prefix[(int64_t)b * K * max_len + i];
+  }
+  if (hist) {
+    for (int i = tid; i < K * (cur + 1); i += blockDim.x) {
+      int bi = i / (cur + 1), t = i % (cur + 1);
+      old_hist[bi * max_len + t] =
+          t == cur ? (int32_t)(row0 + bi) : hist[(row0 + bi) * max_len + t];
+    }
+  }
+  __syncthreads();
+  const int64_t n_total = offs[live];
+  const int need = (int)(((int64_t)K + live) < n_total ? ((int64_t)K + live) : n_total);
+
+  auto cand_at = [&](int64_t j) -> Cand {
+    int i = 0;
+    while (offs[i + 1] <= j) ++i;
+    const int64_t r = row0 + i;
+    const int32_t tok = cand_idx[r * cand_ld + (j - offs[i])];
+    const double lg = (double)logits[r * ld + tok];
+    Cand c;
+    c.s = st.cum[b * K + i] + (lg - lse[r]);  // decode.py:238
+    c.tok = tok;
+    c.beam = i;
+    return c;
+  };
+
+  if (n_total <= kSelCap) {
+    for (int64_t j = tid; j < n_total; j += blockDim.x) cands[j] = cand_at(j);
+    __syncthreads();
+    for (int64_t j = tid; j < n_total; j += blockDim.x) {
+      const Cand c = cands[j];
+      int rank = 0;
+      for (int64_t i = 0; i < n_total; ++i) rank += better(cands[i], c) ? 1 : 0;
+      if (rank < need) picks[rank] = c;
+    }
+  } else {
+    // overflow (tie-heavy rows, exhaustive mode): `need` block-wide arg-best sweeps
+    const int lane = tid & 31, w = tid >> 5;
+    for (int p = 0; p < need; ++p) {
+      Cand best;
+      best.s = -INFINITY; best.tok = 0x7fffffff; best.beam = 0x7fffffff;
+      bool have = false;
+      const Cand prev = p ? picks[p - 1] : best;
+      for (int64_t j = tid; j < n_total; j += blockDim.x) {
+        Cand c = cand_at(j);
+        if (p && !better(prev, c)) continue;  // already picked
+        if (!have || better(c, best)) { best = c; have = true; }
+      }
+      for (int o = 16; o > 0; o >>= 1) {
+        Cand other;
+        other.s = __shfl_xor_sync(0xffffffffu, best.s, o);
+        other.tok = __shfl_xor_sync(0xffffffffu, best.tok, o);
+        other.beam = __shfl_xor_sync(0xffffffffu, best.beam, o);
+        if (better(other, best)) best = other;
+      }
+      if (lane == 0) { red_s[w] = best.s; red_t[w] = best.tok; red_b[w] = best.beam; }
+      __syncthreads();
+      if (tid == 0) {
+        Cand bb; bb.s = red_s[0]; bb.tok = red_t[0]; bb.beam = red_b[0];
+        for (int i = 1; i < (int)(blockDim.x >> 5); ++i) {
+          Cand o; o.s = red_s[i]; o.tok = red_t[i]; o.beam = red_b[i];
+          if (better(o, bb)) bb = o;
+        }
+        picks[p] = bb;
+      }
+      __syncthreads();
+    }
+  }
+  __syncthreads();
+
+  // ---- selection walk, decode.py:192-214 (single thread; <= 2K picks) ----
+  if (tid == 0) {
+    int nl = 0;
+    const int length = step + 1;
+    int32_t* ftok = st.fin_tok + (int64_t)b * K * max_len;
+    int32_t* flen = st.fin_len + b * K;
+    double* fsc = st.fin_score + b * K;
+    int fc = st.fin_count[b];
+    for (int p = 0; p < need; ++p) {
+      const Cand c = picks[p];
+      if (c.tok == eos) {
+        const double sc = len_pow ? c.s / len_pow[length] : c.s;  // decode.py:203
+        const int32_t* par = old_pref + c.beam * max_len;  // seq = prefix + [eos]
+        // insertion point under key (-score, seq)
+        int pos = 0;
+        while (pos < fc) {
+          bool before;
+          if (fsc[pos] != sc) before = fsc[pos] > sc;
+          else {
+            // compare seq_pos with new seq (par[0:step] + eos)
+            const int32_t* e = ftok + pos * max_len;
+            int le = flen[pos], n = le < length ? le : length, i = 0;
+            before = false;
+            bool decided = false;
+            for (; i < n; ++i) {
+              int32_t nv = i < step ? par[i] : eos;
+              if (e[i] != nv) { before = e[i] < nv; decided = true; break; }
+            }
+            if (!decided) before = le < length;
+          }
+          if (!before) break;
+          ++pos;
+        }
+        if (pos < K) {
+          int last = fc < K ? fc : K - 1;  // shift [pos, last) down by one
+          for (int q = last; q > pos; --q) {
+            for (int i = 0; i < flen[q - 1]; ++i) ftok[q * max_len + i] = ftok[(q - 1) * max_len + i];
+            flen[q] = flen[q - 1];
+            fsc[q] = fsc[q - 1];
+          }
+          for (int i = 0; i < step; ++i) ftok[pos * max_len + i] = par[i];
+          ftok[pos * max_len + step] = eos;
+          flen[pos] = length;
+          fsc[pos] = sc;
+          if (fc < K) ++fc;
+        }
+      } else if (nl < K) {
+        new_par[nl] = c.beam;
+        new_tok[nl] = c.tok;
+        new_cum[nl] = c.s;
+        ++nl;
+      }
+      if (nl >= K) break;
+    }
+    st.fin_count[b] = fc;
+    // should_stop, decode.py:160-171, and the engine's stop rule (engine.py:164)
+    bool stop;
+    if (nl == 0) stop = true;
+    else if (fc < K) stop = false;
+    else {
+      double best = new_cum[0];
+      for (int i = 1; i < nl; ++i) best = fmax(best, new_cum[i]);
+      if (len_pow) best = best / len_pow[max(step + 1, 1)];  // decode.py:170
+      stop = best <= fsc[K - 1];
+    }
+    const int done = (stop || last_step || nl == 0) ? 1 : 0;
+    s_new_live = nl;
+    s_done = done;
+    st.live[b] = nl;
+    st.step[b] = step + 1;
+    st.done[b] = done;
+    if (done) atomicAdd(st.n_done, 1);
+  }
+  __syncthreads();
+  const int nl = s_new_live, done = s_done;
+  // new prefixes = parent prefix + token; cum / parents / last tokens
+  for (int i = tid; i < nl * (step + 1); i += blockDim.x) {
+    int bi = i / (step + 1), t = i % (step + 1);
+    st.prefix[((int64_t)b * K + bi) * max_len + t] =
+        t < step ? old_pref[new_par[bi] * max_len + t] : new_tok[bi];
+  }
+  if (tid < K) {
+    const bool on = tid < nl;
+    if (on) {
+      st.cum[b * K + tid] = new_cum[tid];
+      st.parent[b * K + tid] = new_par[tid];
+      st.last_tok[b * K + tid] = new_tok[tid];
+    }
+    const bool feed = on && !done;
+    row_parents[row0 + tid] = feed ? row0 + new_par[tid] : row0;
+    row_tokens[row0 + tid] = feed ? new_tok[tid] : 0;
+  }
+  // copy-free KV reorder: new history row i = old history of its parent
+  if (hist && !done) {
+    for (int i = tid; i < nl * (cur + 1); i += blockDim.x) {
+      int bi = i / (cur + 1), t = i % (cur + 1);
+      hist[(row0 + bi) * max_len + t] = old_hist[new_par[bi] * max_len + t];
+    }
+  }
+}
+
+__global__ void hars_groups_kernel(fq_beam_state st, int batch, int K, int V, int exhaustive,
+                                   int32_t* d_k) {
+  int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= batch * K) return;
+  int b = r / K, i = r % K;
+  int live = st.live[b];
+  int g = exhaustive ? V : min(K + live, V);
+  d_k[r] = (!st.done[b] && i < live) ? g : 0;
+}
+
+__global__ void beam_state_init_kernel(fq_beam_state st, int batch, int K, int max_len) {
+  int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= batch) return;
+  st.live[b] = 1;  // BeamState(): prefixes [[]], cum [0.0], parents [0]
+  st.step[b] = 0;
+  st.done[b] = 0;
+  st.fin_count[b] = 0;
+  for (int i = 0; i < K; ++i) {
+    st.cum[b * K + i] = 0.0;
+    st.parent[b * K + i] = 0;
+    st.last_tok[b * K + i] = 0;
+    st.fin_len[b * K + i] = 0;
+    st.fin_score[b * K + i] = 0.0;
+  }
+  if (b == 0) *st.n_done = 0;
+}
+
+__global__ void step_advance_kernel(int32_t* d_cur) { *d_cur += 1; }
+
+}  // namespace fq
+
+using namespace fq;
+
+extern "C" {
+
+int fq_retrieve(const float* logits, int64_t ld, int64_t rows, int64_t vocab, int64_t k,
+                const int32_t* d_k, float* group_max, int64_t gm_ld, float* threshold,
+                double* lse, int32_t* cand_idx, int64_t cand_ld, int64_t* cand_count,
+                fq_stream_t stream) {
+  FQ_CHECK_ARG(logits && lse && cand_idx && cand_count && rows >= 0 && vocab >= 1 &&
+                   ld >= vocab && cand_ld >= 1,
+               FQ_ERR_DIMENSION, "fq_retrieve: bad args");
+  FQ_CHECK_ARG(d_k || (k >= 1 && k <= vocab), FQ_ERR_PARAMETER,
+               "group count %lld outside [1, vocab=%lld]", (long long)k, (long long)vocab);
+  FQ_CHECK_ARG(!group_max || gm_ld >= (d_k ? vocab : k) || gm_ld >= k, FQ_ERR_DIMENSION,
+               "group_max leading dim too small");
+  if (rows == 0) return FQ_OK;
+  const int stage = vocab <= kMaxStageCols ? 1 : 0;
+  size_t smem = stage ? (size_t)((vocab + 3) & ~3LL) * sizeof(float) : 0;
+  retrieve_kernel<<<(unsigned)rows, kRetrieveThreads, smem, as_stream(stream)>>>(
+      logits, ld, (int)vocab, (int)k, d_k, group_max, gm_ld, threshold, lse, cand_idx, cand_ld,
+      cand_count, stage);
+  return launch_status("fq_retrieve");
+}
+
+int fq_hars_select(const float* logits, int64_t ld, const double* lse, const int32_t* cand_idx,
+                   int64_t cand_ld, const int64_t* cand_count, fq_beam_state st, int64_t batch,
+                   int64_t beam, int64_t vocab, int64_t max_len, int64_t eos,
+                   const double* len_pow, const int32_t* d_cur, int64_t max_steps, int64_t* row_tokens,
+                   int64_t* row_parents, int32_t* hist, void* workspace, int64_t ws_bytes,
+                   fq_stream_t stream) {
+  (void)workspace;
+  (void)ws_bytes;
+  FQ_CHECK_ARG(logits && lse && cand_idx && cand_count && row_tokens && row_parents &&
+                   batch > 0 && beam >= 1 && beam <= kMaxBeam && max_len >= 1,
+               FQ_ERR_DIMENSION, "fq_hars_select: bad args");
+  FQ_CHECK_ARG(cand_ld >= vocab, FQ_ERR_DIMENSION,
+               "fq_hars_select needs full candidate rows (cand_ld >= vocab)");
+  FQ_CHECK_ARG(eos >= 0 && eos < vocab, FQ_ERR_PARAMETER, "eos token outside vocabulary");
+  size_t smem = (size_t)2 * beam * max_len * sizeof(int32_t);
+  FQ_CHECK_ARG(smem <= 160 * 1024, FQ_ERR_CAPACITY, "fq_hars_select: max_len too large");
+  hars_select_kernel<<<(unsigned)batch, kSelThreads, smem, as_stream(stream)>>>(
+      logits, ld, lse, cand_idx, cand_ld, cand_count, st, (int)beam, (int)max_len, (int)eos,
+      len_pow, d_cur, max_steps, row_tokens, row_parents, hist);
+  return launch_status("fq_hars_select");
+}
+
+int fq_hars_groups(fq_beam_state st, int64_t batch, int64_t beam, int64_t vocab, int exhaustive,
+                   int32_t* d_k, fq_stream_t stream) {
+  FQ_CHECK_ARG(d_k && batch > 0 && beam > 0, FQ_ERR_DIMENSION, "fq_hars_groups: bad args");
+  int64_t n = batch * beam;
+  hars_groups_kernel<<<(unsigned)((n + 255) / 256), 256, 0, as_stream(stream)>>>(
+      st, (int)batch, (int)beam, (int)vocab, exhaustive, d_k);
+  return launch_status("fq_hars_groups");
+}
+
+int fq_beam_state_init(fq_beam_state st, int64_t batch, int64_t beam, int64_t max_len,
+                       fq_stream_t stream) {
+  FQ_CHECK_ARG(batch > 0 && beam > 0 && beam <= kMaxBeam, FQ_ERR_DIMENSION,
+               "fq_beam_state_init: bad args");
+  (void)max_len;
+  beam_state_init_kernel<<<(unsigned)((batch + 127) / 128), 128, 0, as_stream(stream)>>>(
+      st, (int)batch, (int)beam, (int)max_len);
+  return launch_status("fq_beam_state_init");
+}
+
+int fq_hars_prepare(void) {
+  if (cudaFuncSetAttribute(retrieve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)(kMaxStageCols * sizeof(float))) != cudaSuccess ||
+      cudaFuncSetAttribute(hars_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           160 * 1024) != cudaSuccess) {
+    set_error("fq_prepare: cannot opt in to large shared memory (hars)");
+    return FQ_ERR_CUDA;
+  }
+  return FQ_OK;
+}
+
+int fq_step_advance(int32_t* d_cur, fq_stream_t stream) {
+  FQ_CHECK_ARG(d_cur, FQ_ERR_DIMENSION, "fq_step_advance: null counter");
+  step_advance_kernel<<<1, 1, 0, as_stream(stream)>>>(d_cur);
+  return launch_status("fq_step_advance");
+}
+
+}  // extern "C"

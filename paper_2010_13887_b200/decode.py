@@ -1,0 +1,414 @@
+"""HARS output layer on the B200 (reference: pkg/src/fuseq/decode.py).
+
+Stage 1 (``retrieve``) and stage 2 (rerank + beam selection) run on the device
+(csrc/fq_hars.cu). The host-facing functions keep the reference's signatures
+and return types so callers and tests are unchanged:
+
+* ``retrieve(logits, k)`` -> ``RetrieveResult`` (group maxima, threshold,
+  candidates ascending, f64 full-vocabulary logsumexp), decode.py:58-92;
+* ``beam_search_step(state, logits, config)`` -> next ``BeamState``,
+  decode.py:217-240 (device stage 1 + device stage 2 on one item);
+* ``argmax_output``, ``sample_top_k``, ``sample_top_p`` use the device
+  retrieve and the reference's host-side draw (decode.py:378-492);
+* ``DeviceBeamState`` is the engine's batched, device-resident beam state.
+
+Tie-breaking everywhere: higher score first, then lower token id, then lower
+beam index (decode.py:19-20).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _abi
+from .errors import DimensionError, EngineError, ParameterError
+from .tensor import OpCounters, as_device, global_counters
+
+F32 = np.float32
+BIG_STEPS = 1 << 40  # "no last step" for the standalone beam step
+
+
+def _ctr(counters) -> OpCounters:
+    return counters if counters is not None else global_counters()
+
+
+def logsumexp(row) -> float:
+    """log(sum(exp(row))) via max shift (decode.py:40-44), host f64."""
+    r = np.asarray(row, dtype=np.float64)
+    m = r.max()
+    return float(m + np.log(np.exp(r - m).sum()))
+
+
+@dataclass
+class RetrieveResult:
+    """Survivors of the grouped-maximum threshold pass, one set per beam."""
+
+    group_maxima: np.ndarray            # [beams, k]
+    threshold: np.ndarray               # [beams]
+    candidate_tokens: list              # per beam, int32 token ids (ascending)
+    candidate_logits: list              # per beam, float32 logits
+    logsumexp_full: np.ndarray          # [beams], float64
+
+
+def retrieve_device(L: torch.Tensor, k: int, *, d_k=None, out=None, with_group_max=True):
+    """Launch stage 1 on a device fp32 [rows, V] view; returns device outputs
+    (group_max, threshold, lse, cand_idx, cand_count)."""
+    rows, V = L.shape
+    dev = L.device
+    if out is None:
+        gm = torch.empty((rows, max(k, 1)), dtype=torch.float32, device=dev) if with_group_max else None
+        th = torch.empty(rows, dtype=torch.float32, device=dev)
+        lse = torch.empty(rows, dtype=torch.float64, device=dev)
+        ci = torch.empty((rows, V), dtype=torch.int32, device=dev)
+        cc = torch.empty(rows, dtype=torch.int64, device=dev)
+    else:
+        gm, th, lse, ci, cc = out
+    _abi.call("fq_retrieve", L.data_ptr(), L.stride(0), rows, V, k, _abi.ptr(d_k), _abi.ptr(gm),
+              gm.stride(0) if gm is not None else 0, _abi.ptr(th), lse.data_ptr(), ci.data_ptr(),
+              ci.stride(0), cc.data_ptr(), _abi.stream_handle())
+    return gm, th, lse, ci, cc
+
+
+def retrieve(logits, k: int, *, counters: OpCounters | None = None,
+             bufs: dict | None = None) -> RetrieveResult:
+    """One kernel call: group maxima, threshold, full-vocabulary logsumexp and
+    candidate selection, with no vocabulary-sized intermediate (decode.py:58)."""
+    L = as_device(logits, torch.float32)
+    if L.dim() != 2:
+        raise DimensionError(f"logits must be [beams, vocab], got {tuple(L.shape)}")
+    beams, vocab = L.shape
+    if not 1 <= k <= vocab:
+        raise ParameterError(f"group count {k} outside [1, vocab={vocab}]")
+    if L.stride(1) != 1:
+        L = L.contiguous()
+    out = None
+    if bufs is not None:
+        out = (bufs["group_max"][:beams, :k], bufs["threshold"][:beams], bufs["lse"][:beams],
+               bufs["cand_idx"][:beams, :vocab], bufs["cand_count"][:beams])
+    gm, th, lse, ci, cc = retrieve_device(L, k, out=out)
+    _ctr(counters).count_fused("retrieve", beams * vocab * 4)
+    counts = cc.cpu().numpy()
+    cmax = int(counts.max()) if beams else 0
+    idx = ci[:, :max(cmax, 1)].cpu().numpy()
+    Lh = None
+    toks, lgs = [], []
+    for b in range(beams):
+        t = idx[b, :counts[b]].astype(np.int32).copy()
+        toks.append(t)
+        lgs.append(L[b, torch.from_numpy(t.astype(np.int64)).to(L.device)].cpu().numpy()
+                   if t.size else np.zeros(0, F32))
+    del Lh
+    return RetrieveResult(group_maxima=gm.cpu().numpy(), threshold=th.cpu().numpy(),
+                          candidate_tokens=toks, candidate_logits=lgs,
+                          logsumexp_full=lse.cpu().numpy())
+
+
+# ---------------------------------------------------------------------------
+# decoding configuration and beam state  (decode.py:99-183)
+# ---------------------------------------------------------------------------
+
+@dataclass(frozen=True)
+class DecodeConfig:
+    method: str = "beam"              # beam | diverse_beam | top_k | top_p | greedy
+    beam_size: int = 4
+    diversity_groups: int = 1
+    diversity_penalty: float = 0.0
+    sample_k: int = 1
+    sample_p: float = 1.0
+    length_penalty: float = 0.0
+    max_steps: int = 32
+    eos_token: int = 2
+    seed: int = 0
+
+    def validate(self, vocab_size: int, max_beam_size: int):
+        if self.method not in ("beam", "diverse_beam", "top_k", "top_p", "greedy"):
+            raise ParameterError(f"unknown decode method {self.method!r}")
+        k = self.effective_beam_size
+        if not 1 <= k <= max_beam_size:
+            raise ParameterError(f"beam size {k} outside [1, {max_beam_size}]")
+        if not 1 <= self.sample_k <= vocab_size:
+            raise ParameterError(f"sample_k {self.sample_k} outside [1, {vocab_size}]")
+        if not 0.0 < self.sample_p <= 1.0:
+            raise ParameterError(f"sample_p {self.sample_p} outside (0, 1]")
+        if self.diversity_penalty < 0:
+            raise ParameterError("diversity penalty must be >= 0")
+        if self.length_penalty < 0:
+            raise ParameterError("length penalty must be >= 0")
+        if self.method == "diverse_beam":
+            if self.diversity_groups < 1 or k % self.diversity_groups:
+                raise ParameterError(
+                    f"beam size {k} not divisible by {self.diversity_groups} groups")
+        if not 0 <= self.eos_token < vocab_size:
+            raise ParameterError(f"eos token {self.eos_token} outside vocabulary")
+        if self.max_steps < 1:
+            raise ParameterError("max_steps must be >= 1")
+
+    @property
+    def effective_beam_size(self) -> int:
+        return 1 if self.method in ("greedy", "top_k", "top_p") else self.beam_size
+
+
+@dataclass
+class BeamState:
+    """Live beams (score-sorted), finished hypotheses and reorder bookkeeping."""
+
+    prefixes: list = field(default_factory=lambda: [[]])
+    cum_log_prob: list = field(default_factory=lambda: [0.0])
+    finished: list = field(default_factory=list)
+    step: int = 0
+    parents: list = field(default_factory=lambda: [0])
+    last_tokens: list = field(default_factory=list)
+    chosen_tokens: list = field(default_factory=list)
+
+    @property
+    def live(self) -> int:
+        return len(self.prefixes)
+
+    def next_input_tokens(self, bos: int) -> list:
+        return [p[-1] if p else bos for p in self.prefixes]
+
+    def should_stop(self, config: DecodeConfig) -> bool:
+        """decode.py:160-171."""
+        if not self.prefixes:
+            return True
+        k = config.effective_beam_size
+        if len(self.finished) < k:
+            return False
+        alpha = config.length_penalty
+        best_live = max(self.cum_log_prob)
+        if alpha:
+            best_live = best_live / max(self.step, 1) ** alpha
+        return best_live <= self.finished[k - 1][1]
+
+    def finalize(self, config: DecodeConfig) -> list:
+        """Best-first hypotheses; unfinished live beams scored as-is (decode.py:173-183)."""
+        out = list(self.finished)
+        have = {tuple(seq) for seq, _ in out}
+        alpha = config.length_penalty
+        for p, c in zip(self.prefixes, self.cum_log_prob):
+            if p and tuple(p) not in have:
+                out.append((p, c / (len(p) ** alpha) if alpha else c))
+        out.sort(key=lambda h: (-h[1], h[0]))
+        return out[:config.effective_beam_size]
+
+
+class DeviceBeamState:
+    """Batched beam state in device memory (fq_beam_state, fq_abi.h)."""
+
+    FIELDS = (("live", torch.int32, "B"), ("step", torch.int32, "B"), ("done", torch.int32, "B"),
+              ("prefix", torch.int32, "BKS"), ("cum", torch.float64, "BK"),
+              ("fin_count", torch.int32, "B"), ("fin_tok", torch.int32, "BKS"),
+              ("fin_len", torch.int32, "BK"), ("fin_score", torch.float64, "BK"),
+              ("last_tok", torch.int32, "BK"), ("parent", torch.int32, "BK"),
+              ("n_done", torch.int32, "1"))
+
+    def __init__(self, batch: int, beam: int, max_len: int, buffers=None):
+        self.batch, self.beam, self.max_len = batch, beam, max_len
+        dims = {"B": batch, "K": beam, "S": max_len, "1": 1}
+        for name, dt, shape in self.FIELDS:
+            shp = tuple(dims[c] for c in shape)
+            t = (buffers.get(f"beam.{name}", shp, dt) if buffers is not None
+                 else torch.zeros(shp, dtype=dt, device=torch.device("cuda")))
+            setattr(self, name, t)
+        self.c = _abi.BeamStateC(*[getattr(self, n).data_ptr() for n, _, _ in self.FIELDS])
+
+    def init(self):
+        _abi.call("fq_beam_state_init", self.c, self.batch, self.beam, self.max_len,
+                  _abi.stream_handle())
+
+    @classmethod
+    def from_host(cls, state: BeamState, beam: int, max_len: int) -> "DeviceBeamState":
+        ds = cls(1, beam, max_len)
+        live = state.live
+        pre = np.zeros((1, beam, max_len), np.int32)
+        for i, p in enumerate(state.prefixes):
+            pre[0, i, :len(p)] = p
+        ds.prefix.copy_(torch.from_numpy(pre))
+        cum = np.zeros((1, beam)); cum[0, :live] = state.cum_log_prob
+        ds.cum.copy_(torch.from_numpy(cum))
+        ft = np.zeros((1, beam, max_len), np.int32)
+        fl = np.zeros((1, beam), np.int32)
+        fs = np.zeros((1, beam))
+        for i, (seq, sc) in enumerate(state.finished[:beam]):
+            ft[0, i, :len(seq)] = seq
+            fl[0, i] = len(seq)
+            fs[0, i] = sc
+        ds.fin_tok.copy_(torch.from_numpy(ft))
+        ds.fin_len.copy_(torch.from_numpy(fl))
+        ds.fin_score.copy_(torch.from_numpy(fs))
+        ds.fin_count.fill_(min(len(state.finished), beam))
+        ds.live.fill_(live)
+        ds.step.fill_(state.step)
+        ds.done.zero_()
+        ds.n_done.zero_()
+        return ds
+
+    def to_host(self, b: int) -> BeamState:
+        """Item b as a reference BeamState (prefixes, cum, finished, bookkeeping)."""
+        return self.host_items()[b]
+
+    def host_items(self) -> list:
+        live = self.live.cpu().numpy()
+        step = self.step.cpu().numpy()
+        pre = self.prefix.cpu().numpy()
+        cum = self.cum.cpu().numpy()
+        fc = self.fin_count.cpu().numpy()
+        ft = self.fin_tok.cpu().numpy()
+        fl = self.fin_len.cpu().numpy()
+        fs = self.fin_score.cpu().numpy()
+        lt = self.last_tok.cpu().numpy()
+        par = self.parent.cpu().numpy()
+        out = []
+        for b in range(self.batch):
+            nl, st = int(live[b]), int(step[b])
+            fin = [(ft[b, i, :fl[b, i]].tolist(), float(fs[b, i])) for i in range(int(fc[b]))]
+            out.append(BeamState(prefixes=[pre[b, i, :st].tolist() for i in range(nl)],
+                                 cum_log_prob=[float(cum[b, i]) for i in range(nl)],
+                                 finished=fin, step=st,
+                                 parents=[int(par[b, i]) for i in range(nl)],
+                                 last_tokens=[int(lt[b, i]) for i in range(nl)],
+                                 chosen_tokens=[int(lt[b, i]) for i in range(nl)]))
+        return out
+
+
+def length_penalty_table(alpha: float, max_len: int, device, out=None):
+    """[l ** alpha for l in 0..max_len] from the host's libm (None when alpha == 0),
+    so device scores divide by the same doubles as decode.py:170/:203."""
+    if not alpha:
+        return None
+    vals = torch.tensor([float(l) ** alpha for l in range(max_len + 1)], dtype=torch.float64)
+    if out is None:
+        return vals.to(device)
+    out[:max_len + 1].copy_(vals)
+    return out
+
+
+def _device_beam_step(state: BeamState, L: torch.Tensor, config: DecodeConfig, exhaustive: bool,
+                      counters=None) -> BeamState:
+    k = config.effective_beam_size
+    if L.shape[0] != state.live:
+        raise DimensionError(f"logits rows {L.shape[0]} != live beams {state.live}")
+    if state.live > k:
+        raise DimensionError(f"{state.live} live beams exceed beam size {k}")
+    V = L.shape[1]
+    max_len = state.step + 1
+    ds = DeviceBeamState.from_host(state, k, max_len)
+    rows = torch.zeros((k, V), dtype=torch.float32, device=L.device)
+    rows[:state.live] = L
+    dk = torch.empty(k, dtype=torch.int32, device=L.device)
+    _abi.call("fq_hars_groups", ds.c, 1, k, V, int(exhaustive), dk.data_ptr(), _abi.stream_handle())
+    _, _, lse, ci, cc = retrieve_device(rows, V if exhaustive else k + state.live, d_k=dk,
+                                        with_group_max=False)
+    _ctr(counters).count_fused("retrieve", state.live * V * 4)
+    rt = torch.empty(k, dtype=torch.int64, device=L.device)
+    rp = torch.empty(k, dtype=torch.int64, device=L.device)
+    lp = length_penalty_table(config.length_penalty, max_len, L.device)
+    _abi.call("fq_hars_select", rows.data_ptr(), rows.stride(0), lse.data_ptr(), ci.data_ptr(),
+              ci.stride(0), cc.data_ptr(), ds.c, 1, k, V, max_len, config.eos_token,
+              _abi.ptr(lp), None, BIG_STEPS, rt.data_ptr(), rp.data_ptr(), None,
+              None, 0, _abi.stream_handle())
+    return ds.to_host(0)
+
+
+def beam_search_step(state: BeamState, logits, config: DecodeConfig, *,
+                     counters: OpCounters | None = None, bufs: dict | None = None) -> BeamState:
+    """One hierarchical beam step (decode.py:217-240): device retrieve with
+    groups = min(k + live, V), device rerank/selection. Identical to
+    :func:`exhaustive_beam_search_step` on the same logits."""
+    return _device_beam_step(state, as_device(logits, torch.float32), config, False, counters)
+
+
+def exhaustive_beam_search_step(state: BeamState, logits, config: DecodeConfig, *,
+                                counters: OpCounters | None = None) -> BeamState:
+    """Exhaustive twin (decode.py:243-267): every token is a candidate (groups = V)."""
+    return _device_beam_step(state, as_device(logits, torch.float32), config, True, counters)
+
+
+# ---------------------------------------------------------------------------
+# sampling and argmax  (decode.py:378-513): device retrieve + reference draw
+# ---------------------------------------------------------------------------
+
+def _draw(tokens, probs, rng) -> int:
+    """Inverse-CDF draw over a small renormalised candidate set (decode.py:378-386)."""
+    r = rng.random() * probs.sum()
+    c = 0.0
+    for t, p in zip(tokens, probs):
+        c += p
+        if r <= c:
+            return int(t)
+    return int(tokens[-1])
+
+
+def _sorted_prefix(rr: RetrieveResult, beam: int = 0):
+    toks = rr.candidate_tokens[beam]
+    lgs = rr.candidate_logits[beam]
+    order = np.lexsort((toks, -lgs.astype(np.float64)))
+    return toks[order], lgs[order]
+
+
+def sample_top_k(logits_row, k: int, rng, *, counters=None, bufs=None) -> int:
+    """Draw from the renormalised true top-k set (decode.py:399-409)."""
+    row = as_device(logits_row, torch.float32).reshape(1, -1)
+    vocab = row.shape[1]
+    if not 1 <= k <= vocab:
+        raise ParameterError(f"top-k {k} outside [1, {vocab}]")
+    rr = retrieve(row, min(k, vocab), counters=counters)
+    toks, lgs = _sorted_prefix(rr)
+    toks, lgs = toks[:k], lgs[:k]
+    probs = np.exp(lgs.astype(np.float64) - rr.logsumexp_full[0])
+    return _draw(toks, probs, rng)
+
+
+def sample_top_p(logits_row, p: float, rng, *, counters=None, bufs=None) -> int:
+    """Nucleus draw with group-count escalation (decode.py:412-430)."""
+    if not 0.0 < p <= 1.0:
+        raise ParameterError(f"top-p {p} outside (0, 1]")
+    row = as_device(logits_row, torch.float32).reshape(1, -1)
+    vocab = row.shape[1]
+    groups = min(32, vocab)
+    while True:
+        rr = retrieve(row, groups, counters=counters)
+        toks, lgs = _sorted_prefix(rr)
+        probs = np.exp(lgs.astype(np.float64) - rr.logsumexp_full[0])
+        cum = np.cumsum(probs)
+        if cum.size and (cum[-1] >= p or groups == vocab):
+            cut = min(int(np.searchsorted(cum, p, side="left")), cum.size - 1)
+            return _draw(toks[:cut + 1], probs[:cut + 1], rng)
+        groups = min(groups * 8, vocab)
+
+
+def argmax_output(logits_row, *, counters=None, bufs=None) -> tuple:
+    """Highest-logit label and its exact probability from one retrieve pass (decode.py:485-492)."""
+    row = as_device(logits_row, torch.float32).reshape(1, -1)
+    rr = retrieve(row, 1, counters=counters)
+    label = int(rr.candidate_tokens[0].min())
+    prob = float(np.exp(float(rr.group_maxima[0, 0]) - rr.logsumexp_full[0]))
+    return label, prob
+
+
+def perplexity(per_step_logits, target_tokens) -> float:
+    """exp of the mean negative log-probability of the targets (decode.py:503-513);
+    the logsumexp comes from the device retrieve pass."""
+    L = as_device(per_step_logits, torch.float32)
+    T = np.asarray(target_tokens, dtype=np.int64).reshape(-1)
+    if L.dim() != 2 or L.shape[0] != T.shape[0]:
+        raise DimensionError(f"{L.shape[0] if L.dim() == 2 else tuple(L.shape)} logit rows "
+                             f"for {T.shape[0]} targets")
+    rr = retrieve(L, 1)
+    tgt = L[torch.arange(T.shape[0], device=L.device), torch.from_numpy(T).to(L.device)]
+    ll = tgt.double().cpu().numpy() - rr.logsumexp_full
+    return float(np.exp(-ll.mean()))
+
+
+def diverse_beam_search_step(state, logits, config, *, counters=None, bufs=None):
+    """Diverse beam search (decode.py:274-371) is ranked next in SURVEY §8(f)."""
+    raise EngineError("diverse beam search is not implemented on the B200 path yet")
+
+
+def top_k_set(logits_row, k: int) -> set:
+    row = np.asarray(logits_row, np.float64).reshape(-1)
+    order = np.lexsort((np.arange(row.size), -row))
+    return {int(t) for t in order[:k]}

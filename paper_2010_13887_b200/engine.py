@@ -1,0 +1,229 @@
+"""Inference sessions on the B200 (reference: pkg/src/fuseq/engine.py).
+
+A :class:`Session` owns one HBM arena, one counter set and one timer set
+(engine.py:36-59). ``generate`` keeps the reference's semantics
+(engine.py:81-173) but runs the whole decode loop on the device:
+
+* encoder + the one-GEMM cross-K/V setup run eagerly (a few dozen launches);
+* each decode step — embed, L decoder layers, logits GEMM, HARS stage 1 and
+  stage 2 (rerank, beam selection, finished list, stop rule, next-step tokens
+  and parents, copy-free KV history update) and the position advance — is
+  captured once into a CUDA graph and replayed; nothing in it touches the host;
+* the host only polls the "all items done" counter one step behind, through
+  pinned memory, to stop early (engine.py:170-171).
+
+``precision="fp32"`` is the exact mode (FFMA GEMMs, f64 softmax/LN
+statistics): token ids match the reference CPU implementation.
+``precision="bf16"`` is the throughput mode (tcgen05 GEMMs, bf16 weights,
+KV cache and GEMM operands, fp32 accumulation and residual stream).
+"""
+
+from __future__ import annotations
+
+import dataclasses
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _abi
+from . import decode as D
+from . import model as M
+from .errors import EngineError, FullMaskError, InputError
+from .memory_plan import Arena, build_plan
+from .tensor import OpCounters, Timers, gemm
+
+I64 = np.int64
+
+
+@dataclass(frozen=True)
+class Hypothesis:
+    tokens: list
+    score: float
+
+
+class Session:
+    def __init__(self, config: M.ModelConfig, weights: M.ModelWeights, engine: str = "fused",
+                 share_plan: bool = True, precision: str = "fp32", use_graphs: bool = True):
+        if engine != "fused":
+            raise InputError(f"unknown engine {engine!r} (the B200 product is the fused engine; "
+                             "the naive twin is the CPU baseline)")
+        if precision not in M.PRECISIONS:
+            raise InputError(f"unknown precision {precision!r}")
+        if not torch.cuda.is_available():
+            raise EngineError("a CUDA device is required (no CPU fallback)")
+        _abi.call("fq_prepare")
+        weights.validate(config)
+        self.config, self.weights, self.engine, self.precision = config, weights, engine, precision
+        self.use_graphs = use_graphs
+        self.counters = OpCounters()
+        self.timers = Timers()
+        self.dw = M.DeviceWeights.get(config, weights, precision)
+        specs = M.plan_intermediates(config, precision)
+        if not share_plan:
+            specs = [dataclasses.replace(s, first_use=0, last_use=1) for s in specs]
+        self.plan = build_plan(specs)
+        self.arena = Arena(self.plan)
+        self._buffers = M.ArenaBuffers(self.arena)
+        self._graphs: dict = {}
+        self._pinned_done = torch.zeros(max(config.max_seq_len, 1), dtype=torch.int32,
+                                        pin_memory=True)
+
+    # ------------------------------------------------------------------
+    def _encode_dev(self, src: np.ndarray, lengths=None):
+        return M.encode(src, self.dw, self.config, lengths, buffers=self._buffers,
+                        counters=self.counters, timers=self.timers, precision=self.precision,
+                        return_bf16=True)
+
+    def encode(self, tokens, lengths=None) -> np.ndarray:
+        """Encoder memory [batch*seq, d_model] (engine.py:62-66), copied to the host."""
+        x, _ = self._encode_dev(np.asarray(tokens, dtype=I64), lengths)
+        return x.cpu().numpy()
+
+    def _setup_decoder(self, src: np.ndarray, lengths, rows: int):
+        batch, seq = src.shape
+        memory, memory16 = self._encode_dev(src, lengths)
+        packed = M.build_cross_kv(memory, self.dw, self.config, batch, seq, buffers=self._buffers,
+                                  counters=self.counters, timers=self.timers,
+                                  precision=self.precision, memory16=memory16)
+        mask = self._buffers.get("enc.mask", (batch, seq)) if lengths is not None else None
+        cache = M.KVCache(self.config, rows, self._buffers, precision=self.precision)
+        return packed, mask, cache
+
+    # ------------------------------------------------------------------
+    def generate(self, src_tokens, decode_config: D.DecodeConfig, src_lengths=None,
+                 bos_token: int = 1, search: str | None = None) -> list:
+        """Encode, then auto-regressively decode every batch item on the device."""
+        cfg = decode_config
+        cfg.validate(self.config.vocab_size, self.config.max_beam_size)
+        src = np.asarray(src_tokens, dtype=I64)
+        if src.ndim != 2:
+            raise InputError(f"source tokens must be [batch, seq], got {src.shape}")
+        if self.config.num_decoder_layers < 1:
+            raise InputError("generation requires a decoder")
+        if cfg.method not in ("beam", "greedy"):
+            raise EngineError(f"decode method {cfg.method!r} is not on the B200 device path yet "
+                              "(SURVEY §8(f))")
+        if search is None:
+            search = "hierarchical"
+        if search not in ("hierarchical", "exhaustive"):
+            raise InputError(f"unknown search {search!r}")
+        if not 0 <= bos_token < self.config.vocab_size:
+            raise InputError("bos token outside vocabulary")
+        batch, seq = src.shape
+        K = cfg.effective_beam_size
+        rows = batch * K
+        max_steps = min(cfg.max_steps, self.config.max_seq_len)
+
+        packed, mask, cache = self._setup_decoder(src, src_lengths, rows)
+        step = M.DecoderStep(self.dw, self.config, batch, K, seq, cache, packed, mask,
+                             self._buffers, self.counters, self.timers)
+        st = D.DeviceBeamState(batch, K, self.config.max_seq_len, self._buffers)
+        st.init()
+        step.tokens.fill_(bos_token)
+        step.bad.zero_()
+        V = self.config.vocab_size
+        b = self._buffers
+        hk = b.get("hars.k", (rows,), torch.int32)
+        lse = b.get("hars.lse", (rows,), torch.float64)
+        ci = b.get("hars.cand_idx", (rows, V), torch.int32)
+        cc = b.get("hars.cand_count", (rows,), torch.int64)
+        parents = b.get("dec.parents", (rows,), torch.int64)
+        exhaustive = int(search == "exhaustive")
+        lp = D.length_penalty_table(cfg.length_penalty, self.config.max_seq_len, None,
+                                    out=b.get("hars.len_pow", (self.config.max_seq_len + 1,),
+                                              torch.float64))
+
+        def body():
+            logits = step.run()
+            stream = _abi.stream_handle()
+            _abi.call("fq_hars_groups", st.c, batch, K, V, exhaustive, hk.data_ptr(), stream)
+            D.retrieve_device(logits, K, d_k=hk, out=(None, None, lse, ci, cc))
+            self.counters.count_fused("retrieve", rows * V * 4)
+            _abi.call("fq_hars_select", logits.data_ptr(), logits.stride(0), lse.data_ptr(),
+                      ci.data_ptr(), ci.stride(0), cc.data_ptr(), st.c, batch, K, V,
+                      self.config.max_seq_len, cfg.eos_token, _abi.ptr(lp),
+                      cache.d_cur.data_ptr(), max_steps, step.tokens.data_ptr(),
+                      parents.data_ptr(), cache.hist.data_ptr(), None, 0, stream)
+            _abi.call("fq_step_advance", cache.d_cur.data_ptr(), stream)
+
+        key = (batch, seq, K, max_steps, mask is not None, exhaustive, cfg.eos_token,
+               float(cfg.length_penalty))
+        graph = None
+        if self.use_graphs:
+            graph = self._graphs.get(key)
+            if graph is None:
+                graph = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(graph):
+                    body()
+                self._graphs[key] = graph
+        pinned = self._pinned_done
+        events = []
+        for t in range(max_steps):
+            if graph is not None:
+                graph.replay()
+            else:
+                body()
+            pinned[t:t + 1].copy_(st.n_done, non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record()
+            events.append(ev)
+            if t >= 1:
+                events[t - 1].synchronize()
+                if int(pinned[t - 1]) >= batch:
+                    break
+        torch.cuda.synchronize()
+        if int(step.bad.item()):
+            raise FullMaskError("fully masked cross-attention row")
+        states = st.host_items()
+        return [[Hypothesis(tokens=s, score=sc) for s, sc in state.finalize(cfg)]
+                for state in states]
+
+    # ------------------------------------------------------------------
+    def forced_logits(self, src_tokens, tgt_tokens, src_lengths=None) -> np.ndarray:
+        """Teacher-forced per-position decoder logits [batch, tgt_len, vocab]
+        (engine.py:227-263)."""
+        src = np.asarray(src_tokens, dtype=I64)
+        tgt = np.asarray(tgt_tokens, dtype=I64)
+        batch, seq = src.shape
+        if tgt.ndim != 2 or tgt.shape[0] != batch:
+            raise InputError(f"target tokens must be [batch, steps], got {tgt.shape}")
+        M._check_tokens(tgt, self.config)
+        packed, mask, cache = self._setup_decoder(src, src_lengths, batch)
+        step = M.DecoderStep(self.dw, self.config, batch, 1, seq, cache, packed, mask,
+                             self._buffers, self.counters, self.timers)
+        step.bad.zero_()
+        out = np.empty((batch, tgt.shape[1], self.config.vocab_size), np.float32)
+        for t in range(tgt.shape[1]):
+            if cache.current_len >= cache.max_seq_len:
+                raise M.CapacityError(f"KV cache full at {cache.current_len} positions")
+            step.tokens.copy_(torch.from_numpy(tgt[:, t]))
+            logits = step.run()
+            out[:, t] = logits.cpu().numpy()
+            cache.end_step()
+        if int(step.bad.item()):
+            raise FullMaskError("fully masked cross-attention row")
+        return out
+
+    # ------------------------------------------------------------------
+    def classify(self, tokens, lengths=None) -> tuple:
+        """Encoder-only classification: first-position pooling, output
+        projection, argmax via the retrieve pass (engine.py:198-224)."""
+        T = np.asarray(tokens, dtype=I64)
+        batch, seq = T.shape
+        memory, memory16 = self._encode_dev(T, lengths)
+        d, V = self.config.d_model, self.config.vocab_size
+        pooled = memory.view(batch, seq, d)[:, 0, :].contiguous()
+        logits = torch.empty((batch, V), dtype=torch.float32, device=memory.device)
+        if self.dw.bf16:
+            gemm(pooled.to(torch.bfloat16), self.dw.out_proj, logits, transpose_b=True,
+                 counters=self.counters)
+        else:
+            gemm(pooled, self.dw.out_proj, logits, transpose_b=True, counters=self.counters)
+        gm, _, lse, ci, cc = D.retrieve_device(logits, 1)
+        labels = ci[:, 0].long().cpu().numpy().astype(I64)   # lowest index among ties
+        probs = np.exp(gm[:, 0].double().cpu().numpy() - lse.cpu().numpy())
+        return labels, probs
+
+    def plan_report(self) -> dict | None:
+        return self.plan.report()
