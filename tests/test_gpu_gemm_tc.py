@@ -1,0 +1,77 @@
+"""tcgen05 bf16 GEMM (fq_gemm_tc.cu) against a float64 reference of the same
+bf16-rounded operands. Tolerance: fp32 accumulation differences only, 1e-3
+relative (the north_star's bf16 bar)."""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def P(gpu):
+    import paper_2010_13887_b200 as pkg
+    return pkg
+
+
+def _ref(a16, b16, bias=None, act="none", res=None):
+    import torch
+    acc = a16.double() @ b16.double().T
+    if bias is not None:
+        acc = acc + bias.double()
+    if act == "relu":
+        acc = torch.relu(acc)
+    elif act == "gelu":
+        acc = torch.nn.functional.gelu(acc)
+    if res is not None:
+        acc = acc + res.double()
+    return acc
+
+
+def _rel(got, want):
+    return float((got.double() - want).abs().max() / max(want.abs().max().item(), 1e-6))
+
+
+@pytest.mark.parametrize("M,N,K", [
+    (128, 64, 64), (1, 8, 16), (32, 512, 512), (100, 100, 72), (512, 1024, 1024),
+    (512, 3072, 1024), (512, 1024, 4096), (300, 32000, 512), (8192, 3072, 1024),
+    (2048, 4096, 1024)])
+def test_tc_gemm_plain(P, M, N, K):
+    import torch
+    g = torch.Generator(device="cuda").manual_seed(M * 7 + N * 3 + K)
+    a = torch.randn(M, K, device="cuda", generator=g).to(torch.bfloat16)
+    b = torch.randn(N, K, device="cuda", generator=g).to(torch.bfloat16)
+    out = torch.empty(M, N, device="cuda")
+    P.gemm(a, b, out, transpose_b=True)
+    torch.cuda.synchronize()
+    assert _rel(out, _ref(a, b)) <= 1e-3, (M, N, K)
+
+
+@pytest.mark.parametrize("act", ["none", "relu", "gelu"])
+def test_tc_gemm_epilogue(P, act):
+    import torch
+    M, N, K = 384, 1536, 512
+    g = torch.Generator(device="cuda").manual_seed(5)
+    a = torch.randn(M, K, device="cuda", generator=g).to(torch.bfloat16)
+    b = torch.randn(N, K, device="cuda", generator=g).to(torch.bfloat16)
+    bias = torch.randn(N, device="cuda", generator=g)
+    res = torch.randn(M, N, device="cuda", generator=g)
+    out = torch.empty(M, N, device="cuda")
+    P.gemm(a, b, out, transpose_b=True, bias=bias, activation=act, residual=res)
+    assert _rel(out, _ref(a, b, bias, act, res)) <= 1e-3
+    out16 = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    P.gemm(a, b, out16, transpose_b=True, bias=bias, activation=act)
+    assert _rel(out16.float(), _ref(a, b, bias, act)) <= 8e-3  # bf16 output rounding
+
+
+def test_tc_gemm_strided_output_and_accumulate(P):
+    import torch
+    M, N, K = 256, 256, 256
+    a = torch.randn(M, K, device="cuda").to(torch.bfloat16)
+    b = torch.randn(N, K, device="cuda").to(torch.bfloat16)
+    big = torch.zeros(M, 2 * N, device="cuda")
+    view = big[:, N:]
+    view.fill_(1.0)
+    P.gemm(a, b, view, transpose_b=True, accumulate=True)
+    assert _rel(view, _ref(a, b) + 1.0) <= 1e-3
+    assert float(big[:, :N].abs().max()) == 0.0

@@ -165,8 +165,9 @@ def test_retrieve_large_vocab_vs_oracle(P, O, V):
             assert np.array_equal(rr.candidate_tokens[b], orr.candidate_tokens[b])
             assert rr.threshold[b] == orr.threshold[b]
             assert np.array_equal(rr.group_maxima[b], orr.group_maxima[b])
-            assert abs(rr.logsumexp_full[b] - orr.logsumexp_full[b]) <= 1e-9 * abs(
-                orr.logsumexp_full[b]) + 1e-9
+            # fp32 expf ulps + f64 summation order: the reference's own bar is 1e-6
+            assert abs(rr.logsumexp_full[b] - orr.logsumexp_full[b]) <= 1e-7 * abs(
+                orr.logsumexp_full[b]) + 1e-7
 
 
 def test_beam_streams_match_reference_fixture(P):
