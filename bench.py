@@ -1,0 +1,402 @@
+#!/usr/bin/env python
+"""Benchmark: decoded tokens/s for Transformer-big beam-4 translation (BASELINE.json
+config 2: 6+6 layers, d=1024, 16 heads, ff=4096, V=32000, batch 128, src 64,
+64 decode steps) through the B200 device engine, plus the HARS step microbench.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--precision bf16|fp32] [--batch B]
+
+One "step" = one full request: encoder + cross-K/V + 64 decode steps with HARS
+beam search over one batch of synthetic inputs (seeded random-init weights of
+the architecture, synthetic_tokens-style source ids). Multi-GPU (torchrun): one
+process per GPU, every rank decodes its own batch (weak scaling, no collective
+on the data path); value = all tokens / max-over-ranks time.
+
+Timing: W untimed warm-up steps, then exactly K steps, each bracketed by CUDA
+events on the launching stream, with a >L2 (256 MiB) buffer written before every
+step (outside the events); barrier + synchronize around the timed region.
+`--impl reference` times the CPU oracle port of the reference path (oracle/,
+the reference itself is pure Python/numba and cannot be compiled) on the host
+cores, rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+C2 = dict(num_encoder_layers=6, num_decoder_layers=6, d_model=1024, d_ff=4096, num_heads=16,
+          vocab_size=32000, max_batch=128, max_seq_len=64, max_beam_size=4)
+SRC_LEN, BEAM, MAX_STEPS = 64, 4, 64
+METRIC = "decoded tokens/sec (Transformer-big, beam=4)"
+CPU_SAMPLE_BATCH = 4  # bounded CPU sample: 4 items x 64 steps of the same workload
+
+REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+           0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+           0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+           0x100: "display_clock_setting"}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--precision", default="bf16", choices=["bf16", "fp32"])
+    ap.add_argument("--batch", type=int, default=128, help="items per GPU")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-micro", action="store_true")
+    return ap.parse_args()
+
+
+def synthetic_tokens(batch, seq, vocab, seed):
+    """bench.py:62-66 of the reference: uniform ids in [3, vocab)."""
+    import numpy as np
+    return np.random.default_rng(seed).integers(min(3, vocab - 1), vocab, size=(batch, seq),
+                                                dtype=np.int64)
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+# --------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+
+    def __init__(self, device_index: int):
+        self.idx = device_index
+        self.proc = None
+        self.lines = []
+        self.t = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.idx), "--query-gpu=clocks.sm,clocks.max.sm,"
+                 "clocks_event_reasons.active", "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        sm, mx, reasons = [], [], set()
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 3:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+                bits = int(parts[2], 16)
+            except ValueError:
+                continue
+            for b, name in REASONS.items():
+                if bits & b and name != "gpu_idle":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------------------ reference
+def run_reference(args, rank):
+    import numpy as np
+
+    from oracle import fuseq_oracle as O
+    if rank != 0:
+        return
+    cfg = O.OracleConfig(**C2)
+    w = O.make_random_weights(cfg, 0)
+    model = O.OracleModel(cfg, w)
+    src = synthetic_tokens(CPU_SAMPLE_BATCH, SRC_LEN, cfg.vocab_size, 0)
+    times, toks = [], 0
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        hyps = model.generate(src, beam_size=BEAM, max_steps=MAX_STEPS, eos=2)
+        dt = time.perf_counter() - t0
+        if i >= args.warmup:
+            times.append(dt)
+            toks = sum(len(h[0][0]) for h in hyps)
+    sec = sum(times) / len(times)
+    value = toks / sec
+    cores = os.cpu_count()
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": "Transformer-big beam4 translate (C2), bounded CPU sample",
+                   "batch": CPU_SAMPLE_BATCH, "src_len": SRC_LEN, "beam": BEAM,
+                   "max_steps": MAX_STEPS},
+        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": "port",
+                         "sample": f"C2 model, {CPU_SAMPLE_BATCH} items x {MAX_STEPS} steps "
+                                   f"per step (numpy/OpenBLAS oracle port, {cpu_model()})"},
+        "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- ours
+def cpu_baseline_sample(host_weights, cfg_dict):
+    """Oracle port on the box's host cores, bounded sample of the same workload."""
+    import numpy as np
+
+    from oracle import fuseq_oracle as O
+    ocfg = O.OracleConfig(**cfg_dict)
+    w = {n: a for n, a in host_weights.named_tensors(host_weights._cfg)}
+    model = O.OracleModel(ocfg, w)
+    src = synthetic_tokens(CPU_SAMPLE_BATCH, SRC_LEN, ocfg.vocab_size, 0)
+    t0 = time.perf_counter()
+    hyps = model.generate(src, beam_size=BEAM, max_steps=MAX_STEPS, eos=2)
+    dt = time.perf_counter() - t0
+    toks = sum(len(h[0][0]) for h in hyps)
+    return {"value": toks / dt, "unit": "tokens/s", "cores": os.cpu_count(), "kind": "port",
+            "sample": f"C2 model, {CPU_SAMPLE_BATCH} items x {MAX_STEPS} steps, "
+                      f"{dt:.1f} s (numpy/OpenBLAS oracle port, {cpu_model()})"}
+
+
+def time_kernel(fn, iters, flush):
+    import torch
+    times = []
+    for _ in range(iters):
+        flush()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        fn()
+        e.record()
+        e.synchronize()
+        times.append(s.elapsed_time(e) / 1e3)
+    return statistics.median(times)
+
+
+def run_ours(args, rank, world):
+    import numpy as np
+    import torch
+
+    import paper_2010_13887_b200 as P
+    from paper_2010_13887_b200 import _abi, decode as D
+
+    dev = torch.device("cuda", torch.cuda.current_device())
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    tc_peak = peaks.get("bf16_tflops_sustained", 1400.0)
+    cfg_d = dict(C2, max_batch=max(args.batch, 1))
+    cfg = P.ModelConfig(**cfg_d)
+    host_w = P.make_random_weights(cfg, seed=0)
+    host_w._cfg = cfg
+    sess = P.Session(cfg, host_w, precision=args.precision)
+    dc = P.DecodeConfig(method="beam", beam_size=BEAM, max_steps=MAX_STEPS, eos_token=2)
+    src_host = synthetic_tokens(args.batch, SRC_LEN, cfg.vocab_size, seed=rank)
+    src_dev = torch.from_numpy(src_host).to(dev)
+    src_pinned = torch.from_numpy(src_host).pin_memory()
+    flush_buf = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def flush():
+        flush_buf.fill_(1)
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+
+    # -- warm-up (captures the decode-step graph) --
+    for _ in range(args.warmup):
+        st = sess.generate(src_dev, dc, return_device_state=True)
+    torch.cuda.synchronize()
+
+    # -- device-timed region: inputs resident in HBM --
+    l0 = _abi.launch_count()
+    barrier()
+    step_times = []
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        for _ in range(args.steps):
+            flush()
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record()
+            st = sess.generate(src_dev, dc, return_device_state=True)
+            e.record()
+            e.synchronize()
+            step_times.append(s.elapsed_time(e) / 1e3)
+        barrier()
+    launches = (_abi.launch_count() - l0) // args.steps
+    sec = sum(step_times) / len(step_times)
+    hyps_state = st.host_items()
+    tokens = sum(len(s_.finalize(dc)[0][0]) if s_.finalize(dc) else 0 for s_ in hyps_state)
+    t_max = torch.tensor([sec], dtype=torch.float64, device=dev)
+    tok_sum = torch.tensor([float(tokens)], dtype=torch.float64, device=dev)
+    if world > 1:
+        torch.distributed.all_reduce(t_max, op=torch.distributed.ReduceOp.MAX)
+        torch.distributed.all_reduce(tok_sum)
+    sec_max, tok_total = float(t_max.item()), float(tok_sum.item())
+    value = tok_total / sec_max
+
+    # -- end to end through the public API: host tokens in, host hypotheses out --
+    e2e_times = []
+    h2d = src_host.nbytes
+    d2h = sum(getattr(st, n).numel() * getattr(st, n).element_size()
+              for n, _, _ in D.DeviceBeamState.FIELDS)
+    for i in range(max(1, min(args.steps, 3)) + 1):
+        flush()
+        barrier()
+        t0 = time.perf_counter()
+        hyps = sess.generate(src_pinned, dc)
+        dt = time.perf_counter() - t0
+        if i:
+            e2e_times.append(dt)
+    e2e_sec = torch.tensor([sum(e2e_times) / len(e2e_times)], dtype=torch.float64, device=dev)
+    if world > 1:
+        torch.distributed.all_reduce(e2e_sec, op=torch.distributed.ReduceOp.MAX)
+    e2e_value = tok_total / float(e2e_sec.item())
+
+    out = None
+    if rank == 0:
+        out = {
+            "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec_max * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": args.precision, "data": "synthetic (seeded random-init weights, "
+                                              "uniform source ids)",
+            "config": {"workload": "Transformer-big beam4 translate (BASELINE config 2)",
+                       "layers": "6+6", "d_model": 1024, "heads": 16, "d_ff": 4096,
+                       "vocab": 32000, "batch_per_gpu": args.batch,
+                       "global_batch": args.batch * world, "src_len": SRC_LEN, "beam": BEAM,
+                       "max_steps": MAX_STEPS, "parallelism": f"replicas x{world} (batch-sharded)",
+                       "tokens_per_step": tok_total,
+                       "l2": "256 MiB buffer written before every timed step; working set "
+                             ">> 126 MB L2"},
+            "clocks": clk.summary(),
+            "gpu_launches": launches,
+            "e2e": {"value": e2e_value, "unit": "tokens/s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h},
+        }
+
+    # -- kernel microbenches for the roofline (rank 0, same shapes as the step) --
+    if rank == 0 and not args.no_micro:
+        R, d, V = args.batch * BEAM, cfg.d_model, cfg.vocab_size
+        dw = sess.dw
+        x16 = torch.randn(R, d, device=dev).to(torch.bfloat16)
+        logits = torch.empty(R, V, device=dev)
+        w_out = dw.out_proj
+        if args.precision == "bf16":
+            fn_logits = lambda: P.gemm(x16, w_out, logits, transpose_b=True)  # noqa: E731
+        else:
+            x32 = x16.float()
+            fn_logits = lambda: P.gemm(x32, w_out, logits, transpose_b=True)  # noqa: E731
+        t_log = time_kernel(fn_logits, 20, flush)
+        fl = 2.0 * R * V * d
+        w1 = dw.dec[0]["w_ff1"]
+        h = torch.empty(R, cfg.d_ff, device=dev, dtype=dw.act_dtype)
+        b1 = dw.dec[0]["b_ff1"]
+        if args.precision == "bf16":
+            fn_ff1 = lambda: P.gemm(x16, w1, h, transpose_b=True, bias=b1, activation="relu")  # noqa
+        else:
+            fn_ff1 = lambda: P.gemm(x32, w1, h, bias=b1, activation="relu")  # noqa: E731
+        t_ff1 = time_kernel(fn_ff1, 50, flush)
+        fl_ff1 = 2.0 * R * cfg.d_ff * d
+        # HARS step (stage 1 + stage 2) on C2 rows, fp32 logits (metric 2)
+        lg = torch.randn(R, V, device=dev)
+        hst = D.DeviceBeamState(args.batch, BEAM, cfg.max_seq_len)
+        hk = torch.full((R,), 2 * BEAM, dtype=torch.int32, device=dev)
+        lse = torch.empty(R, dtype=torch.float64, device=dev)
+        ci = torch.empty(R, V, dtype=torch.int32, device=dev)
+        cc = torch.empty(R, dtype=torch.int64, device=dev)
+        rt = torch.empty(R, dtype=torch.int64, device=dev)
+        rp = torch.empty(R, dtype=torch.int64, device=dev)
+
+        def stage1():
+            D.retrieve_device(lg, 2 * BEAM, d_k=hk, out=(None, None, lse, ci, cc))
+
+        def hars_step():
+            hst.live.fill_(BEAM)
+            hst.done.zero_()
+            hst.step.fill_(5)
+            stage1()
+            _abi.call("fq_hars_select", lg.data_ptr(), lg.stride(0), lse.data_ptr(),
+                      ci.data_ptr(), ci.stride(0), cc.data_ptr(), hst.c, args.batch, BEAM, V,
+                      cfg.max_seq_len, 2, None, None, 1 << 40, rt.data_ptr(), rp.data_ptr(),
+                      None, None, 0, _abi.stream_handle())
+        hst.init()
+        t_s1 = time_kernel(stage1, 50, flush)
+        t_hars = time_kernel(hars_step, 50, flush)
+        hars_bytes = R * V * 4
+        s1_gbs = hars_bytes / t_s1 / 1e9
+        out["roofline"] = {
+            "kernel": "tcgen05 GEMM, logits projection (x[R,d] . E[V,d]^T, fused epilogue)"
+            if args.precision == "bf16" else "FFMA GEMM, logits projection",
+            "shape": [R, V, d], "bound": "tensor", "achieved": fl / t_log / 1e12,
+            "peak": tc_peak, "unit": "TFLOP/s", "frac": fl / t_log / 1e12 / tc_peak,
+            "traffic": None, "us_per_launch": t_log * 1e6,
+            "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained"}
+        out["kernels"] = {
+            "gemm_ffn1": {"shape": [R, cfg.d_ff, d], "us": t_ff1 * 1e6,
+                          "tflops": fl_ff1 / t_ff1 / 1e12,
+                          "frac_tensor": fl_ff1 / t_ff1 / 1e12 / tc_peak},
+            "hars_stage1_retrieve": {"rows": R, "vocab": V, "us": t_s1 * 1e6, "gbs": s1_gbs,
+                                     "frac_hbm": s1_gbs / hbm_peak,
+                                     "algorithmic_bytes": hars_bytes},
+        }
+        out["hars_step_us"] = {"value": t_hars * 1e6, "rows": R, "vocab": V, "beam": BEAM,
+                               "batch": args.batch, "gbs": hars_bytes / t_hars / 1e9,
+                               "frac_hbm": hars_bytes / t_hars / 1e9 / hbm_peak,
+                               "what": "stage 1 retrieve + stage 2 rerank/select, fp32 logits"}
+    if rank == 0 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline_sample(host_w, cfg_d)
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank)
+        return
+    import torch
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local))
+    try:
+        run_ours(args, rank, world)
+    finally:
+        if world > 1:
+            torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

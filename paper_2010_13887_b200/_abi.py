@@ -70,6 +70,17 @@ _lib = None
 _lock = threading.Lock()
 _prepared = False
 _NO_PREPARE = {"fq_abi_version", "fq_last_error", "fq_num_sms", "fq_prepare"}
+_launches = [0]
+
+
+def launch_count() -> int:
+    """Kernels launched (or captured) through the ABI so far in this process."""
+    return _launches[0]
+
+
+def add_launches(n: int):
+    """Account for kernels replayed from a captured CUDA graph."""
+    _launches[0] += n
 
 
 def load():
@@ -103,6 +114,8 @@ def call(name: str, *args) -> int:
             raise ExtensionError(f"fq_prepare: {lib.fq_last_error().decode()}")
         _prepared = True
     rc = getattr(lib, name)(*args)
+    if name not in _NO_PREPARE:
+        _launches[0] += 1  # every other entry point launches exactly one kernel
     if rc < 0:
         msg = lib.fq_last_error().decode("utf-8", "replace")
         raise _ERRORS.get(rc, EngineError)(f"{name}: {msg}")

@@ -47,6 +47,169 @@ __global__ void __launch_bounds__(256) layer_norm_kernel(
   }
 }
 
+// Warp-per-row variant for d % 128 == 0, d <= 128 * kMaxV: the row lives in
+// registers (float4 per lane per 128 columns), statistics reduce with f64
+// shuffles — one HBM read, no shared memory, no block barriers.
+constexpr int kMaxV = 8;  // d <= 1024 (wider rows use the CTA kernel)
+template <bool kBiasRes>
+__global__ void __launch_bounds__(256) layer_norm_warp_kernel(
+    const float* __restrict__ x, int64_t ldx, const float* __restrict__ bias,
+    const float* __restrict__ res, int64_t ldr, const float* __restrict__ gamma,
+    const float* __restrict__ beta, double eps, int64_t rows, int d, float* __restrict__ out,
+    int64_t ldo, __nv_bfloat16* __restrict__ out16, int64_t ldo16) {
+  const int lane = threadIdx.x & 31;
+  const int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (row >= rows) return;
+  const int nv = d >> 7;
+  float4 u[kMaxV];
+  double s = 0.0;
+#pragma unroll
+  for (int i = 0; i < kMaxV; ++i) {
+    if (i < nv) {
+      const int c = (i * 32 + lane) * 4;
+      float4 a = *reinterpret_cast<const float4*>(x + row * ldx + c);
+      if (kBiasRes) {
+        float4 b = *reinterpret_cast<const float4*>(bias + c);
+        float4 r = *reinterpret_cast<const float4*>(res + row * ldr + c);
+        a.x = fadd_rn(fadd_rn(a.x, b.x), r.x);  // kernels.py:64 summand
+        a.y = fadd_rn(fadd_rn(a.y, b.y), r.y);
+        a.z = fadd_rn(fadd_rn(a.z, b.z), r.z);
+        a.w = fadd_rn(fadd_rn(a.w, b.w), r.w);
+      }
+      u[i] = a;
+      s += ((double)a.x + (double)a.y) + ((double)a.z + (double)a.w);
+    }
+  }
+  const double mean = warp_sum(s) / d;
+  double v = 0.0;
+#pragma unroll
+  for (int i = 0; i < kMaxV; ++i) {
+    if (i < nv) {
+      double t0 = u[i].x - mean, t1 = u[i].y - mean, t2 = u[i].z - mean, t3 = u[i].w - mean;
+      v += (t0 * t0 + t1 * t1) + (t2 * t2 + t3 * t3);
+    }
+  }
+  const double inv = 1.0 / sqrt(warp_sum(v) / d + eps);
+#pragma unroll
+  for (int i = 0; i < kMaxV; ++i) {
+    if (i < nv) {
+      const int c = (i * 32 + lane) * 4;
+      const float4 g = *reinterpret_cast<const float4*>(gamma + c);
+      const float4 bb = *reinterpret_cast<const float4*>(beta + c);
+      float4 o;
+      o.x = fadd_rn(fmul_rn((float)((u[i].x - mean) * inv), g.x), bb.x);  // kernels.py:35
+      o.y = fadd_rn(fmul_rn((float)((u[i].y - mean) * inv), g.y), bb.y);
+      o.z = fadd_rn(fmul_rn((float)((u[i].z - mean) * inv), g.z), bb.z);
+      o.w = fadd_rn(fmul_rn((float)((u[i].w - mean) * inv), g.w), bb.w);
+      if (out) *reinterpret_cast<float4*>(out + row * ldo + c) = o;
+      if (out16) {
+        __nv_bfloat162 lo = __floats2bfloat162_rn(o.x, o.y), hi = __floats2bfloat162_rn(o.z, o.w);
+        uint2 pk;
+        pk.x = *reinterpret_cast<uint32_t*>(&lo);
+        pk.y = *reinterpret_cast<uint32_t*>(&hi);
+        *reinterpret_cast<uint2*>(out16 + row * ldo16 + c) = pk;
+      }
+    }
+  }
+}
+
+// 128 threads per row, V float4 per thread (d = 512 * V): 4x the warps of the
+// warp-per-row kernel for the decoder's few hundred rows (latency-bound op).
+template <bool kBiasRes, int V>
+__global__ void __launch_bounds__(128) layer_norm_row128_kernel(
+    const float* __restrict__ x, int64_t ldx, const float* __restrict__ bias,
+    const float* __restrict__ res, int64_t ldr, const float* __restrict__ gamma,
+    const float* __restrict__ beta, double eps, int d, float* __restrict__ out, int64_t ldo,
+    __nv_bfloat16* __restrict__ out16, int64_t ldo16) {
+  __shared__ double red[2][4];
+  const int64_t row = blockIdx.x;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  float4 u[V];
+  double s = 0.0;
+#pragma unroll
+  for (int i = 0; i < V; ++i) {
+    const int c = (i * 128 + threadIdx.x) * 4;
+    float4 a = *reinterpret_cast<const float4*>(x + row * ldx + c);
+    if (kBiasRes) {
+      const float4 b = *reinterpret_cast<const float4*>(bias + c);
+      const float4 r = *reinterpret_cast<const float4*>(res + row * ldr + c);
+      a.x = fadd_rn(fadd_rn(a.x, b.x), r.x);
+      a.y = fadd_rn(fadd_rn(a.y, b.y), r.y);
+      a.z = fadd_rn(fadd_rn(a.z, b.z), r.z);
+      a.w = fadd_rn(fadd_rn(a.w, b.w), r.w);
+    }
+    u[i] = a;
+    s += ((double)a.x + (double)a.y) + ((double)a.z + (double)a.w);
+  }
+  s = warp_sum(s);
+  if (lane == 0) red[0][w] = s;
+  __syncthreads();
+  const double mean = ((red[0][0] + red[0][1]) + (red[0][2] + red[0][3])) / d;
+  double v = 0.0;
+#pragma unroll
+  for (int i = 0; i < V; ++i) {
+    double t0 = u[i].x - mean, t1 = u[i].y - mean, t2 = u[i].z - mean, t3 = u[i].w - mean;
+    v += (t0 * t0 + t1 * t1) + (t2 * t2 + t3 * t3);
+  }
+  v = warp_sum(v);
+  if (lane == 0) red[1][w] = v;
+  __syncthreads();
+  const double inv = 1.0 / sqrt(((red[1][0] + red[1][1]) + (red[1][2] + red[1][3])) / d + eps);
+#pragma unroll
+  for (int i = 0; i < V; ++i) {
+    const int c = (i * 128 + threadIdx.x) * 4;
+    const float4 g = *reinterpret_cast<const float4*>(gamma + c);
+    const float4 bb = *reinterpret_cast<const float4*>(beta + c);
+    float4 o;
+    o.x = fadd_rn(fmul_rn((float)((u[i].x - mean) * inv), g.x), bb.x);  // kernels.py:35
+    o.y = fadd_rn(fmul_rn((float)((u[i].y - mean) * inv), g.y), bb.y);
+    o.z = fadd_rn(fmul_rn((float)((u[i].z - mean) * inv), g.z), bb.z);
+    o.w = fadd_rn(fmul_rn((float)((u[i].w - mean) * inv), g.w), bb.w);
+    if (out) *reinterpret_cast<float4*>(out + row * ldo + c) = o;
+    if (out16) {
+      __nv_bfloat162 lo = __floats2bfloat162_rn(o.x, o.y), hi = __floats2bfloat162_rn(o.z, o.w);
+      uint2 pk;
+      pk.x = *reinterpret_cast<uint32_t*>(&lo);
+      pk.y = *reinterpret_cast<uint32_t*>(&hi);
+      *reinterpret_cast<uint2*>(out16 + row * ldo16 + c) = pk;
+    }
+  }
+}
+
+static inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+template <bool kBiasRes>
+static void launch_ln(const float* x, int64_t ldx, const float* bias, const float* res,
+                      int64_t ldr, const float* gamma, const float* beta, double eps,
+                      int64_t rows, int64_t d, float* out, int64_t ldo, __nv_bfloat16* out16,
+                      int64_t ldo16, cudaStream_t s) {
+  bool align_ok = ldx % 4 == 0 && aligned16(x) && aligned16(gamma) && aligned16(beta) &&
+                  (!out || (ldo % 4 == 0 && aligned16(out))) &&
+                  (!out16 || (ldo16 % 4 == 0 && (reinterpret_cast<uintptr_t>(out16) & 7) == 0));
+  if (kBiasRes) align_ok = align_ok && ldr % 4 == 0 && aligned16(res) && aligned16(bias);
+  const bool warp_ok = align_ok && d % 128 == 0 && d <= 128 * kMaxV;
+  const bool row128 = align_ok && (d == 512 || d == 1024 || d == 2048) &&
+                      (rows < 4 * 148 * 8 || d == 2048);
+  if (row128) {
+    // few rows (decoder): 128 threads per row keep enough loads in flight
+#define FQ_LN128(V)                                                                       \
+  layer_norm_row128_kernel<kBiasRes, V><<<(unsigned)rows, 128, 0, s>>>(                   \
+      x, ldx, bias, res, ldr, gamma, beta, eps, (int)d, out, ldo, out16, ldo16)
+    if (d == 512) FQ_LN128(1);
+    else if (d == 1024) FQ_LN128(2);
+    else FQ_LN128(4);
+#undef FQ_LN128
+  } else if (warp_ok) {
+    const int64_t threads = rows * 32;
+    layer_norm_warp_kernel<kBiasRes><<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(
+        x, ldx, bias, res, ldr, gamma, beta, eps, rows, (int)d, out, ldo, out16, ldo16);
+  } else {
+    int threads = d >= 1024 ? 256 : 128;
+    layer_norm_kernel<kBiasRes><<<(unsigned)rows, threads, d * sizeof(float), s>>>(
+        x, ldx, bias, res, ldr, gamma, beta, eps, (int)d, out, ldo, out16, ldo16);
+  }
+}
+
 // act(x + bias) (+ residual), kernels.py:39-53.
 __global__ void bias_residual_act_kernel(const float* __restrict__ x, int64_t ldx,
                                          const float* __restrict__ bias,
@@ -187,10 +350,8 @@ int fq_layer_norm(const float* x, int64_t ldx, const float* gamma, const float* 
                (long long)d);
   FQ_CHECK_ARG(eps >= 0, FQ_ERR_DIMENSION, "eps must be non-negative");
   if (rows == 0) return FQ_OK;
-  int threads = d >= 1024 ? 256 : 128;
-  layer_norm_kernel<false><<<(unsigned)rows, threads, d * sizeof(float), as_stream(stream)>>>(
-      x, ldx, nullptr, nullptr, 0, gamma, beta, eps, (int)d, out, ldo,
-      reinterpret_cast<__nv_bfloat16*>(out16), ldo16);
+  launch_ln<false>(x, ldx, nullptr, nullptr, 0, gamma, beta, eps, rows, d, out, ldo,
+                   reinterpret_cast<__nv_bfloat16*>(out16), ldo16, as_stream(stream));
   return launch_status("fq_layer_norm");
 }
 
@@ -202,10 +363,8 @@ int fq_bias_residual_layer_norm(const float* x, int64_t ldx, const float* bias,
   FQ_CHECK_ARG(x && bias && residual && gamma && beta && d > 0 && d <= 12288 && (out || out16),
                FQ_ERR_DIMENSION, "fq_bias_residual_layer_norm: bad args");
   if (rows == 0) return FQ_OK;
-  int threads = d >= 1024 ? 256 : 128;
-  layer_norm_kernel<true><<<(unsigned)rows, threads, d * sizeof(float), as_stream(stream)>>>(
-      x, ldx, bias, residual, ldr, gamma, beta, eps, (int)d, out, ldo,
-      reinterpret_cast<__nv_bfloat16*>(out16), ldo16);
+  launch_ln<true>(x, ldx, bias, residual, ldr, gamma, beta, eps, rows, d, out, ldo,
+                  reinterpret_cast<__nv_bfloat16*>(out16), ldo16, as_stream(stream));
   return launch_status("fq_bias_residual_layer_norm");
 }
 

@@ -103,18 +103,25 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
       : "memory");
 }
 
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
-  uint32_t r[16];
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
+  uint32_t r[32];
   asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
-      "%14,%15}, [%16];"
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+      "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
       : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
         "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
-        "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]),
+        "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]),
+        "=r"(r[31])
       : "r"(taddr));
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
 struct Epi {
@@ -128,6 +135,9 @@ struct Epi {
   int act;
 };
 
+// Persistent: grid <= #SMs, CTA walks tiles t = blockIdx.x, +gridDim.x, ...
+// (M-tile fastest so concurrent CTAs share the weight tile in L2). Two TMEM
+// accumulator stages let the epilogue of tile i overlap the MMAs of tile i+1.
 template <int BN, int STAGES>
 __global__ void __launch_bounds__(kThreads, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tma_a,
@@ -135,25 +145,32 @@ __global__ void __launch_bounds__(kThreads, 1)
   constexpr int A_BYTES = BM * BK * 2;
   constexpr int B_BYTES = BN * BK * 2;
   constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  constexpr uint32_t TMEM_COLS = BN < 32 ? 32 : BN;
+  constexpr uint32_t TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;  // two accumulator stages
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-B aligned (128B-swizzle atoms); pointer arithmetic keeps the shared
+  // address space visible to the compiler (LDS/STS, not generic LD/ST)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  float* stage_out = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES);  // 4 x [32][33]
   __shared__ __align__(8) uint64_t full_bar[STAGES];
   __shared__ __align__(8) uint64_t empty_bar[STAGES];
-  __shared__ __align__(8) uint64_t tfull_bar;
+  __shared__ __align__(8) uint64_t tfull_bar[2];
+  __shared__ __align__(8) uint64_t tempty_bar[2];
   __shared__ uint32_t tmem_base_sh;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
   const int num_kb = (K + BK - 1) / BK;
+  const int mt = (M + BM - 1) / BM;
+  const int ntiles = mt * ((N + BN - 1) / BN);
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full_bar[s], 1);
       mbar_init(&empty_bar[s], 1);
     }
-    mbar_init(&tfull_bar, 1);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull_bar[s], 1);
+      mbar_init(&tempty_bar[s], 4);  // one arrive per epilogue warp
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tma_a)));
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tma_b)));
@@ -171,61 +188,122 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp == 0) {
     if (lane == 0) {  // ---- TMA producer ----
-      for (int kb = 0; kb < num_kb; ++kb) {
-        const int s = kb % STAGES;
-        const uint32_t ph = (kb / STAGES) & 1;
-        mbar_wait(&empty_bar[s], ph ^ 1);
-        uint8_t* sa = smem + s * STAGE_BYTES;
-        mbar_expect_tx(&full_bar[s], STAGE_BYTES);
-        tma_load_2d(&tma_a, &full_bar[s], sa, kb * BK, m0);
-        tma_load_2d(&tma_b, &full_bar[s], sa + A_BYTES, kb * BK, n0);
+      int it = 0;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const int m0 = (t % mt) * BM, n0 = (t / mt) * BN;
+        for (int kb = 0; kb < num_kb; ++kb, ++it) {
+          const int s = it % STAGES;
+          const uint32_t ph = (it / STAGES) & 1;
+          mbar_wait(&empty_bar[s], ph ^ 1);
+          uint8_t* sa = smem + s * STAGE_BYTES;
+          mbar_expect_tx(&full_bar[s], STAGE_BYTES);
+          tma_load_2d(&tma_a, &full_bar[s], sa, kb * BK, m0);
+          tma_load_2d(&tma_b, &full_bar[s], sa + A_BYTES, kb * BK, n0);
+        }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {  // ---- MMA issuer ----
       constexpr uint32_t idesc = idesc_bf16(BM, BN);
-      for (int kb = 0; kb < num_kb; ++kb) {
-        const int s = kb % STAGES;
-        const uint32_t ph = (kb / STAGES) & 1;
-        mbar_wait(&full_bar[s], ph);
+      int it = 0, local = 0;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++local) {
+        const int as = local & 1;
+        mbar_wait(&tempty_bar[as], ((local >> 1) & 1) ^ 1);  // epilogue drained this stage
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint32_t a_base = smem_u32(smem + s * STAGE_BYTES);
-        const uint32_t b_base = a_base + A_BYTES;
+        const uint32_t acc = tmem + as * BN;
+        for (int kb = 0; kb < num_kb; ++kb, ++it) {
+          const int s = it % STAGES;
+          const uint32_t ph = (it / STAGES) & 1;
+          mbar_wait(&full_bar[s], ph);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t a_base = smem_u32(smem + s * STAGE_BYTES);
+          const uint32_t b_base = a_base + A_BYTES;
 #pragma unroll
-        for (int k = 0; k < BK / 16; ++k) {
-          mma_bf16(tmem, sw128_desc(a_base + k * 32), sw128_desc(b_base + k * 32), idesc,
-                   (kb | k) != 0);
+          for (int k = 0; k < BK / 16; ++k) {
+            mma_bf16(acc, sw128_desc(a_base + k * 32), sw128_desc(b_base + k * 32), idesc,
+                     (kb | k) != 0);
+          }
+          mma_commit(&empty_bar[s]);  // ring slot reusable once these MMAs retire
         }
-        mma_commit(&empty_bar[s]);  // slot reusable once these MMAs retire
+        mma_commit(&tfull_bar[as]);   // accumulator stage complete
       }
-      mma_commit(&tfull_bar);       // accumulator complete
     }
   } else {  // ---- epilogue: warps 2..5 own TMEM lane quarters (warp % 4) ----
     const int q = warp & 3;
-    mbar_wait(&tfull_bar, 0);
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    const int row = m0 + q * 32 + lane;
-    const bool row_ok = row < M;
+    float* st = stage_out + (warp - 2) * 32 * 33;
     float* c32 = reinterpret_cast<float*>(ep.c);
     __nv_bfloat16* c16 = reinterpret_cast<__nv_bfloat16*>(ep.c);
+    int local = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++local) {
+      const int as = local & 1;
+      const int m0 = (t % mt) * BM, n0 = (t / mt) * BN;
+      mbar_wait(&tfull_bar[as], (local >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const int rbase = m0 + q * 32;
+      const int nrows = min(32, M - rbase);
 #pragma unroll 1
-    for (int cc = 0; cc < BN; cc += 16) {
-      float v[16];
-      tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + cc, v);
-      if (!row_ok) continue;
-      const int col0 = n0 + cc;
+      for (int cc = 0; cc < BN; cc += 32) {
+        float v[32];
+        tmem_ld32(tmem + as * BN + ((uint32_t)(q * 32) << 16) + cc, v);
+        if (cc + 32 >= BN) {  // last TMEM read of this stage: hand it back to the MMA warp
+          asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tempty_bar[as]);
+        }
+        // transpose through smem: thread = row on the TMEM side, column on the store side
 #pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const int col = col0 + j;
-        if (col >= N) break;
-        float t = v[j];
-        const int64_t ci = (int64_t)row * ep.ldc + col;
-        if (ep.accumulate) t = fadd_rn(ep.c_bf16 ? bf2f(c16[ci]) : c32[ci], t);
-        if (ep.bias) t = fadd_rn(t, ep.bias[col]);
-        t = apply_act(t, ep.act);
-        if (ep.res) t = fadd_rn(t, ep.res[(int64_t)row * ep.ldr + col]);
-        if (ep.c_bf16) c16[ci] = f2bf(t);
-        else c32[ci] = t;
+        for (int j = 0; j < 32; ++j) st[lane * 33 + j] = v[j];
+        __syncwarp();
+        const int col = n0 + cc + lane;
+#pragma unroll 1
+        for (int h0 = 0; h0 < 32; h0 += 16) {  // 16 rows at a time bounds register use
+        float x[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) x[i] = st[(h0 + i) * 33 + lane];
+        const int nr = nrows - h0;
+        if (col < N && nr > 0) {
+          // every global read of the 32 rows is issued before any store
+          // (no per-row dependent latency); each lane owns one column, so the
+          // warp writes full 128-byte row segments
+          const int64_t c0 = (int64_t)(rbase + h0) * ep.ldc + col;
+          if (ep.accumulate) {
+            float cv[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i)
+              cv[i] = i < nr ? (ep.c_bf16 ? bf2f(c16[c0 + i * ep.ldc]) : c32[c0 + i * ep.ldc])
+                                : 0.0f;
+#pragma unroll
+            for (int i = 0; i < 16; ++i) x[i] = fadd_rn(cv[i], x[i]);
+          }
+          if (ep.bias) {
+            const float bias = __ldg(ep.bias + col);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) x[i] = fadd_rn(x[i], bias);
+          }
+          if (ep.act) {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) x[i] = apply_act(x[i], ep.act);
+          }
+          if (ep.res) {
+            const float* rp = ep.res + (int64_t)(rbase + h0) * ep.ldr + col;
+            float rv[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) rv[i] = i < nr ? __ldg(rp + i * ep.ldr) : 0.0f;
+#pragma unroll
+            for (int i = 0; i < 16; ++i) x[i] = fadd_rn(x[i], rv[i]);
+          }
+          if (ep.c_bf16) {
+#pragma unroll
+            for (int i = 0; i < 16; ++i)
+              if (i < nr) c16[c0 + i * ep.ldc] = f2bf(x[i]);
+          } else {
+#pragma unroll
+            for (int i = 0; i < 16; ++i)
+              if (i < nr) c32[c0 + i * ep.ldc] = x[i];
+          }
+        }
+        }
+        __syncwarp();  // staging free for the next chunk
       }
     }
   }
@@ -240,7 +318,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 template <int BN, int STAGES>
 constexpr int smem_bytes() {
-  return STAGES * (BM * BK * 2 + BN * BK * 2) + 1024;
+  return STAGES * (BM * BK * 2 + BN * BK * 2) + 4 * 32 * 33 * 4 + 1024;
 }
 
 using EncodeFn = PFN_cuTensorMapEncodeTiled_v12000;
@@ -289,7 +367,14 @@ static int launch(const void* a, int64_t lda, const void* b, int64_t ldb, const 
   int rc;
   if ((rc = make_map(&ma, a, M, K, lda, BM)) != FQ_OK) return rc;
   if ((rc = make_map(&mb, b, N, K, ldb, BN)) != FQ_OK) return rc;
-  dim3 grid((unsigned)((N + BN - 1) / BN), (unsigned)((M + BM - 1) / BM));
+  static int num_sms = 0;
+  if (!num_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const int64_t ntiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
+  const unsigned grid = (unsigned)(ntiles < num_sms ? ntiles : num_sms);
   tc_gemm_kernel<BN, STAGES><<<grid, kThreads, smem_bytes<BN, STAGES>(), s>>>(ma, mb, ep, (int)M,
                                                                              (int)N, (int)K);
   return launch_status("fq_gemm(tcgen05)");

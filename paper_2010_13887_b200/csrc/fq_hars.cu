@@ -19,8 +19,8 @@
 
 namespace fq {
 
-constexpr int kRetrieveThreads = 1024;
-constexpr int kMaxStageCols = 51200;  // 200 KB of fp32 staged per row
+constexpr int kRetrieveThreads = 512;
+constexpr int kCandCap = 2048;  // survivors ranked in shared memory; more -> ordered rescan
 
 // block-wide exclusive scan of small ints (blockDim multiple of 32).
 __device__ __forceinline__ int block_excl_scan(int v, int* warp_tot, int* total) {
@@ -48,18 +48,21 @@ __device__ __forceinline__ int block_excl_scan(int v, int* warp_tot, int* total)
   return incl - v + warp_tot[w];
 }
 
-__global__ void __launch_bounds__(kRetrieveThreads) retrieve_kernel(
+// One CTA (512 threads) per row; up to 4 CTAs per SM. Pass 1 streams the row
+// from HBM once (128-bit loads, evict-first); pass 2 re-reads it from L2 (the
+// <= 4 x 148 rows in flight are far below the 126 MB L2).
+__global__ void __launch_bounds__(kRetrieveThreads, 4) retrieve_kernel(
     const float* __restrict__ logits, int64_t ld, int V, int k_fixed,
     const int32_t* __restrict__ d_k, float* __restrict__ group_max, int64_t gm_ld,
     float* __restrict__ threshold, double* __restrict__ lse, int32_t* __restrict__ cand_idx,
-    int64_t cand_ld, int64_t* __restrict__ cand_count, int stage) {
-  extern __shared__ __align__(16) float srow[];
+    int64_t cand_ld, int64_t* __restrict__ cand_count) {
   __shared__ float part_max[kRetrieveThreads * 4];
+  __shared__ int32_t s_idx[kCandCap];
   __shared__ float gmax_s[32];
   __shared__ float s_R, s_max;
   __shared__ double red[32];
   __shared__ int warp_tot[32];
-  __shared__ int s_total;
+  __shared__ int s_total, s_cnt;
 
   const int64_t row = blockIdx.x;
   const int k = d_k ? d_k[row] : k_fixed;
@@ -70,10 +73,10 @@ __global__ void __launch_bounds__(kRetrieveThreads) retrieve_kernel(
   const float* x = logits + row * ld;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, nw = blockDim.x >> 5;
   const bool vec = ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
-  const bool small_k = k <= 32;
+  if (tid == 0) s_cnt = 0;
 
-  // ---------------- pass 1: group maxima (one HBM read, staged) -------------
-  if (small_k) {
+  // ---------------- pass 1: strided group maxima -------------------------
+  if (k <= 32) {
     // T threads, T % k == 0: thread t only ever sees groups (4t + c) % k.
     const int T = blockDim.x - (blockDim.x % k);
     float m[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
@@ -83,21 +86,13 @@ __global__ void __launch_bounds__(kRetrieveThreads) retrieve_kernel(
         const float4* x4 = reinterpret_cast<const float4*>(x);
 #pragma unroll 4
         for (int v = tid; v < nvec; v += T) {
-          float4 q = __ldcs(x4 + v);  // streaming: read once
+          float4 q = __ldcs(x4 + v);
           m[0] = fmaxf(m[0], q.x); m[1] = fmaxf(m[1], q.y);
           m[2] = fmaxf(m[2], q.z); m[3] = fmaxf(m[3], q.w);
-          if (stage) reinterpret_cast<float4*>(srow)[v] = q;
         }
-        // tail (V % 4 elements): staged here, folded into its group after the reduction
-        if (stage)
-          for (int j = (nvec << 2) + tid; j < V; j += T) srow[j] = x[j];
       } else {
 #pragma unroll 4
-        for (int j = tid; j < V; j += T) {
-          float q = __ldcs(x + j);
-          m[0] = fmaxf(m[0], q);
-          if (stage) srow[j] = q;
-        }
+        for (int j = tid; j < V; j += T) m[0] = fmaxf(m[0], __ldcs(x + j));
       }
     }
     // partials: vec -> element index e = 4*tid + c (group e % k); scalar -> e = tid
@@ -107,16 +102,14 @@ __global__ void __launch_bounds__(kRetrieveThreads) retrieve_kernel(
       for (int c = 0; c < per; ++c) part_max[tid * per + c] = m[c];
     }
     __syncthreads();
-    // warp g reduces entries e = g (mod k)
-    for (int g = w; g < k; g += nw) {
+    for (int g = w; g < k; g += nw) {  // warp g reduces entries e = g (mod k)
       float mm = -INFINITY;
       for (int e = g + lane * k; e < nparts; e += 32 * k) mm = fmaxf(mm, part_max[e]);
       mm = warp_max(mm);
       if (lane == 0) gmax_s[g] = mm;
     }
     __syncthreads();
-    // vec tail elements (j >= 4*nvec): fold into their group directly
-    if (vec && tid == 0) {
+    if (vec && tid == 0) {  // tail (V % 4 elements) folds into its group directly
       for (int j = (V >> 2) << 2; j < V; ++j) gmax_s[j % k] = fmaxf(gmax_s[j % k], x[j]);
     }
     __syncthreads();
@@ -136,11 +129,7 @@ __global__ void __launch_bounds__(kRetrieveThreads) retrieve_kernel(
     float R = INFINITY, M = -INFINITY;
     for (int g = tid; g < k; g += blockDim.x) {
       float mm = -INFINITY;
-      for (int j = g; j < V; j += k) {
-        float q = x[j];
-        mm = fmaxf(mm, q);
-        if (stage) srow[j] = q;
-      }
+      for (int j = g; j < V; j += k) mm = fmaxf(mm, x[j]);
       if (group_max) group_max[row * gm_ld + g] = mm;
       R = fminf(R, mm);
       M = fmaxf(M, mm);
@@ -158,44 +147,68 @@ __global__ void __launch_bounds__(kRetrieveThreads) retrieve_kernel(
     __syncthreads();
   }
   const float R = s_R, M = s_max;
-  const float* src = stage ? srow : x;
 
-  // ---------------- pass 2: logsumexp + ordered candidate compaction ----------
+  // ---------------- pass 2 (L2): logsumexp + survivors x >= R ---------------
   double acc = 0.0;
-  int64_t base = 0;
-  int32_t* out_idx = cand_idx + row * cand_ld;
-  const int chunk = blockDim.x * 4;
-  for (int c0 = 0; c0 < V; c0 += chunk) {
-    int flags = 0;
-    float v4[4];
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      int j = c0 + tid * 4 + c;
-      v4[c] = (j < V) ? src[j] : -INFINITY;
-      if (j < V) {
-        acc += (double)expf(__fsub_rn(v4[c], M));
-        if (v4[c] >= R) flags |= 1 << c;
-      }
+  auto visit = [&](float v, int j) {
+    acc += (double)expf(__fsub_rn(v, M));  // E1: fp32 x - max, fp32 expf, f64 sum
+    if (v >= R) {
+      int p = atomicAdd(&s_cnt, 1);
+      if (p < kCandCap) s_idx[p] = j;
     }
-    if (!__syncthreads_or(flags)) continue;  // no survivors in this chunk
-    int cnt = __popc(flags);
-    int off = block_excl_scan(cnt, warp_tot, &s_total);
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      if (flags & (1 << c)) {
-        int64_t pos = base + off;
-        if (pos < cand_ld) out_idx[pos] = c0 + tid * 4 + c;
-        ++off;
-      }
+  };
+  if (vec) {
+    const int nvec = V >> 2;
+    const float4* x4 = reinterpret_cast<const float4*>(x);
+#pragma unroll 4
+    for (int v = tid; v < nvec; v += blockDim.x) {
+      float4 q = x4[v];
+      visit(q.x, 4 * v); visit(q.y, 4 * v + 1); visit(q.z, 4 * v + 2); visit(q.w, 4 * v + 3);
     }
-    base += s_total;
-    __syncthreads();
+    for (int j = (nvec << 2) + tid; j < V; j += blockDim.x) visit(x[j], j);
+  } else {
+    for (int j = tid; j < V; j += blockDim.x) visit(x[j], j);
   }
-  const double s = block_sum(acc, red);
+  const double s = block_sum(acc, red);  // contains __syncthreads: s_cnt is final
+  const int n = s_cnt;
+  int32_t* out_idx = cand_idx + row * cand_ld;
+  if (n <= kCandCap) {
+    // ascending token order: rank of each (distinct) survivor
+    for (int i = tid; i < n; i += blockDim.x) {
+      const int j = s_idx[i];
+      int rank = 0;
+      for (int q = 0; q < n; ++q) rank += s_idx[q] < j ? 1 : 0;
+      if (rank < cand_ld) out_idx[rank] = j;
+    }
+  } else {
+    // tie-heavy row: ordered block-scan compaction over the row (rare)
+    int64_t base = 0;
+    const int chunk = blockDim.x * 4;
+    for (int c0 = 0; c0 < V; c0 += chunk) {
+      int flags = 0;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        int j = c0 + tid * 4 + c;
+        if (j < V && x[j] >= R) flags |= 1 << c;
+      }
+      if (!__syncthreads_or(flags)) continue;
+      int off = block_excl_scan(__popc(flags), warp_tot, &s_total);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        if (flags & (1 << c)) {
+          int64_t pos = base + off;
+          if (pos < cand_ld) out_idx[pos] = c0 + tid * 4 + c;
+          ++off;
+        }
+      }
+      base += s_total;
+      __syncthreads();
+    }
+  }
   if (tid == 0) {
     if (threshold) threshold[row] = R;
     lse[row] = (double)M + log(s);
-    cand_count[row] = base;
+    cand_count[row] = n;
   }
 }
 
@@ -481,11 +494,9 @@ int fq_retrieve(const float* logits, int64_t ld, int64_t rows, int64_t vocab, in
   FQ_CHECK_ARG(!group_max || gm_ld >= (d_k ? vocab : k) || gm_ld >= k, FQ_ERR_DIMENSION,
                "group_max leading dim too small");
   if (rows == 0) return FQ_OK;
-  const int stage = vocab <= kMaxStageCols ? 1 : 0;
-  size_t smem = stage ? (size_t)((vocab + 3) & ~3LL) * sizeof(float) : 0;
-  retrieve_kernel<<<(unsigned)rows, kRetrieveThreads, smem, as_stream(stream)>>>(
+  retrieve_kernel<<<(unsigned)rows, kRetrieveThreads, 0, as_stream(stream)>>>(
       logits, ld, (int)vocab, (int)k, d_k, group_max, gm_ld, threshold, lse, cand_idx, cand_ld,
-      cand_count, stage);
+      cand_count);
   return launch_status("fq_retrieve");
 }
 
@@ -531,9 +542,7 @@ int fq_beam_state_init(fq_beam_state st, int64_t batch, int64_t beam, int64_t ma
 }
 
 int fq_hars_prepare(void) {
-  if (cudaFuncSetAttribute(retrieve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)(kMaxStageCols * sizeof(float))) != cudaSuccess ||
-      cudaFuncSetAttribute(hars_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  if (cudaFuncSetAttribute(hars_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            160 * 1024) != cudaSuccess) {
     set_error("fq_prepare: cannot opt in to large shared memory (hars)");
     return FQ_ERR_CUDA;

@@ -92,13 +92,22 @@ class Session:
 
     # ------------------------------------------------------------------
     def generate(self, src_tokens, decode_config: D.DecodeConfig, src_lengths=None,
-                 bos_token: int = 1, search: str | None = None) -> list:
-        """Encode, then auto-regressively decode every batch item on the device."""
+                 bos_token: int = 1, search: str | None = None, *,
+                 return_device_state: bool = False):
+        """Encode, then auto-regressively decode every batch item on the device.
+
+        ``src_tokens`` is host [batch, seq] (copied in) or an int64 device
+        tensor already resident in HBM (used as is, not range-checked). With
+        ``return_device_state`` the final ``DeviceBeamState`` is returned
+        instead of host hypotheses (no device->host traffic)."""
         cfg = decode_config
         cfg.validate(self.config.vocab_size, self.config.max_beam_size)
-        src = np.asarray(src_tokens, dtype=I64)
+        if isinstance(src_tokens, torch.Tensor) and src_tokens.is_cuda:
+            src = src_tokens
+        else:
+            src = np.asarray(src_tokens, dtype=I64)
         if src.ndim != 2:
-            raise InputError(f"source tokens must be [batch, seq], got {src.shape}")
+            raise InputError(f"source tokens must be [batch, seq], got {tuple(src.shape)}")
         if self.config.num_decoder_layers < 1:
             raise InputError("generation requires a decoder")
         if cfg.method not in ("beam", "greedy"):
@@ -151,17 +160,22 @@ class Session:
                float(cfg.length_penalty))
         graph = None
         if self.use_graphs:
-            graph = self._graphs.get(key)
-            if graph is None:
+            entry = self._graphs.get(key)
+            if entry is None:
                 graph = torch.cuda.CUDAGraph()
+                n0 = _abi.launch_count()
                 with torch.cuda.graph(graph):
                     body()
-                self._graphs[key] = graph
+                entry = (graph, _abi.launch_count() - n0)
+                _abi.add_launches(-entry[1])  # captured, not launched
+                self._graphs[key] = entry
+            graph, per_step = entry
         pinned = self._pinned_done
         events = []
         for t in range(max_steps):
             if graph is not None:
                 graph.replay()
+                _abi.add_launches(per_step)
             else:
                 body()
             pinned[t:t + 1].copy_(st.n_done, non_blocking=True)
@@ -172,6 +186,8 @@ class Session:
                 events[t - 1].synchronize()
                 if int(pinned[t - 1]) >= batch:
                     break
+        if return_device_state:
+            return st
         torch.cuda.synchronize()
         if int(step.bad.item()):
             raise FullMaskError("fully masked cross-attention row")

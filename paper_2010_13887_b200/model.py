@@ -459,19 +459,21 @@ def encode(tokens, weights, config: ModelConfig, lengths=None, *, engine: str = 
     (plus its bf16 copy when ``return_bf16``)."""
     if engine != "fused":
         raise InputError("the B200 engine implements the fused path only")
-    T = np.asarray(tokens, dtype=I64)
+    resident = isinstance(tokens, torch.Tensor) and tokens.is_cuda
+    T = tokens if resident else np.asarray(tokens, dtype=I64)
     if T.ndim != 2:
-        raise InputError(f"tokens must be [batch, seq], got {T.shape}")
+        raise InputError(f"tokens must be [batch, seq], got {tuple(T.shape)}")
     batch, seq = T.shape
     if batch > config.max_batch or seq > config.max_seq_len:
         raise CapacityError(f"batch {batch} x seq {seq} exceeds configured maxima")
-    _check_tokens(T, config)
+    if not resident:
+        _check_tokens(T, config)
     dw = DeviceWeights.get(config, weights, precision)
     bufs = buffers if buffers is not None else HeapBuffers()
     ctr = counters or global_counters()
     n, d = batch * seq, config.d_model
     tok = bufs.get("enc.tokens", (n,), torch.int64)
-    tok.copy_(torch.from_numpy(T.reshape(-1)))
+    tok.copy_(T.reshape(-1) if resident else torch.from_numpy(T.reshape(-1)))
     mask = None
     if lengths is not None:
         mask = bufs.get("enc.mask", (batch, seq))

@@ -1,0 +1,144 @@
+"""Fused attention kernels (fq_attention.cu) against float64 torch references
+of the reference's three-step attention (gemm_batched QK^T -> scale_mask_softmax
+-> gemm_batched P.V, model.py:329-336 / :572-604), including the copy-free
+history-table KV cache. fp32 KV: 1e-5 relative; bf16 KV: operands rounded to
+bf16 in the reference too, 1e-4."""
+
+import math
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def T(gpu):
+    import torch
+    return torch
+
+
+def _abi():
+    from paper_2010_13887_b200 import _abi
+    return _abi
+
+
+def _rel(got, want):
+    return float((got.double() - want).abs().max() / max(want.abs().max().item(), 1e-9))
+
+
+def _softmax_ref(T, s, mask=None):
+    if mask is not None:
+        s = s + mask
+    return T.softmax(s, dim=-1)
+
+
+@pytest.mark.parametrize("hd", [16, 32, 64, 128])
+@pytest.mark.parametrize("beam", [1, 3, 4, 8])
+@pytest.mark.parametrize("kv16", [False, True])
+def test_cross_attention(T, hd, beam, kv16):
+    A = _abi()
+    g = T.Generator(device="cuda").manual_seed(hd * 10 + beam)
+    B, S, H, L = 3, 37, 4, 2
+    d = H * hd
+    ld = 2 * L * d
+    cq = T.randn(B * beam, d, device="cuda", generator=g)
+    packed = T.randn(B * S, ld, device="cuda", generator=g)
+    if kv16:
+        packed = packed.to(T.bfloat16)
+    mask = T.zeros(B, S, device="cuda")
+    mask[1, 30:] = -math.inf
+    scale = float(np.float32(1 / math.sqrt(hd)))
+    layer = 1
+    ck = packed[:, 2 * layer * d:]
+    cv = packed[:, (2 * layer + 1) * d:]
+    out = T.empty(B * beam, d, device="cuda")
+    out16 = T.empty(B * beam, d, device="cuda", dtype=T.bfloat16)
+    bad = T.zeros(1, dtype=T.int32, device="cuda")
+    A.call("fq_cross_attention", cq.data_ptr(), d, ck.data_ptr(), cv.data_ptr(), int(kv16), ld, B,
+           beam, S, H, hd, scale, mask.data_ptr(), out.data_ptr(), out16.data_ptr(), d,
+           0 if kv16 else 1, bad.data_ptr(), A.stream_handle())
+    T.cuda.synchronize()
+    K = packed[:, 2 * layer * d:(2 * layer + 1) * d].double().view(B, S, H, hd).permute(0, 2, 1, 3)
+    V = packed[:, (2 * layer + 1) * d:(2 * layer + 2) * d].double().view(B, S, H, hd).permute(0, 2, 1, 3)
+    Q = cq.double().view(B, beam, H, hd).permute(0, 2, 1, 3)
+    P = _softmax_ref(T, (Q @ K.transpose(-1, -2)) * scale, mask.double()[:, None, None, :])
+    want = (P @ V).permute(0, 2, 1, 3).reshape(B * beam, d)
+    assert int(bad.item()) == 0
+    assert _rel(out, want) <= (1e-4 if kv16 else 1e-5)
+    assert _rel(out16.float(), want) <= 1e-2
+
+
+@pytest.mark.parametrize("hd", [16, 64, 128, 48])
+@pytest.mark.parametrize("kv16", [False, True])
+def test_decoder_self_attention_history_table(T, hd, kv16):
+    A = _abi()
+    g = T.Generator(device="cuda").manual_seed(hd + 7)
+    rows, H, S, beam = 12, 3, 20, 4
+    d = H * hd
+    dt = T.bfloat16 if kv16 else T.float32
+    kc = T.randn(S, rows, d, device="cuda", generator=g).to(dt)
+    vc = T.randn(S, rows, d, device="cuda", generator=g).to(dt)
+    cur = 13
+    # beams only ever inherit from rows of their own item
+    hist = T.empty(rows, S, dtype=T.int32, device="cuda")
+    for r in range(rows):
+        item0 = (r // beam) * beam
+        hist[r] = T.randint(item0, item0 + beam, (S,), generator=g, device="cuda").int()
+    sqkv = T.randn(rows, 3 * d, device="cuda", generator=g)
+    d_cur = T.tensor([cur], dtype=T.int32, device="cuda")
+    out = T.empty(rows, d, device="cuda")
+    scale = float(np.float32(1 / math.sqrt(hd)))
+    A.call("fq_decoder_self_attention", sqkv.data_ptr(), 3 * d, kc.data_ptr(), vc.data_ptr(),
+           int(kv16), hist.data_ptr(), d_cur.data_ptr(), rows, H, hd, S, scale, out.data_ptr(),
+           None, d, 0 if kv16 else 1, A.stream_handle())
+    T.cuda.synchronize()
+    knew = sqkv[:, d:2 * d].to(dt).double()
+    vnew = sqkv[:, 2 * d:].to(dt).double()
+    assert T.equal(kc[cur].double(), knew) and T.equal(vc[cur].double(), vnew)  # slot written
+    for r in range(rows):
+        idx = hist[r, :cur].long()
+        Kr = T.cat([kc[T.arange(cur, device="cuda"), idx].double(), knew[r:r + 1]])  # [cur+1, d]
+        Vr = T.cat([vc[T.arange(cur, device="cuda"), idx].double(), vnew[r:r + 1]])
+        q = sqkv[r, :d].double()
+        for h in range(H):
+            sl = slice(h * hd, (h + 1) * hd)
+            p = T.softmax((Kr[:, sl] @ q[sl]) * scale, dim=0)
+            want = p @ Vr[:, sl]
+            assert _rel(out[r, sl], want) <= 1e-5, (r, h)
+
+
+@pytest.mark.parametrize("hd", [16, 64])
+def test_encoder_attention(T, hd):
+    A = _abi()
+    g = T.Generator(device="cuda").manual_seed(3)
+    B, S, H = 2, 29, 4
+    d = H * hd
+    qkv = T.randn(B * S, 3 * d, device="cuda", generator=g)
+    mask = T.zeros(B, S, device="cuda")
+    mask[0, 20:] = -math.inf
+    out = T.empty(B * S, d, device="cuda")
+    scale = float(np.float32(1 / math.sqrt(hd)))
+    A.call("fq_encoder_attention", qkv.data_ptr(), 3 * d, B, S, H, hd, scale, mask.data_ptr(),
+           out.data_ptr(), None, d, 1, None, A.stream_handle())
+    T.cuda.synchronize()
+    x = qkv.double().view(B, S, 3, H, hd)
+    Q, K, V = (x[:, :, i].permute(0, 2, 1, 3) for i in range(3))
+    P = _softmax_ref(T, (Q @ K.transpose(-1, -2)) * scale, mask.double()[:, None, None, :])
+    want = (P @ V).permute(0, 2, 1, 3).reshape(B * S, d)
+    assert _rel(out, want) <= 1e-5
+
+
+@pytest.mark.parametrize("rows,d", [(7, 512), (512, 1024), (3, 2048), (9000, 1024), (5, 384)])
+def test_layer_norm_paths(T, rows, d):
+    """All three LN kernels (row128 / warp / CTA) against the f64 formula."""
+    import paper_2010_13887_b200 as P
+    g = T.Generator(device="cuda").manual_seed(rows)
+    x = T.randn(rows, d, device="cuda", generator=g)
+    gm = T.randn(d, device="cuda", generator=g)
+    b = T.randn(d, device="cuda", generator=g)
+    out = P.fused_layer_norm(x, gm, b, 1e-5).data
+    xd = x.double()
+    want = (xd - xd.mean(1, keepdim=True)) / T.sqrt(xd.var(1, unbiased=False, keepdim=True) + 1e-5)
+    want = want * gm.double() + b.double()
+    assert _rel(out, want) <= 1e-6
