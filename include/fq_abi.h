@@ -126,6 +126,10 @@ int fq_gemm(const void* a, int a_dtype, int64_t lda, const void* b, int b_dtype,
             int64_t K, int accumulate, const float* bias, const float* residual, int64_t ldr,
             int act, fq_stream_t stream);
 
+/* Tile width and thread-block-cluster shape (cm x cn CTAs sharing A/B tiles
+ * through TMA multicast) the bf16 dispatcher picks for an M x N x K GEMM. */
+int fq_gemm_plan(int64_t M, int64_t N, int64_t K, int* bn, int* cm, int* cn, int* split);
+
 /* Strided batched fp32 GEMM over a two-level batch (i0 < n0, i1 < n1):
  * operand X of batch (i0,i1) starts at X + i0*sX0 + i1*sX1 (elements).
  * Covers every gemm_batched call site of model.py (QK^T, P.V into the

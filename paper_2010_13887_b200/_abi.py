@@ -47,6 +47,7 @@ SIGNATURES = {
     "fq_kv_gather_append": ([P, P, P, P, P, I64, I64, I64, I64, I64, P, P, P], I32),
     "fq_gemm": ([P, I32, I64, P, I32, I64, I32, P, I32, I64, I64, I64, I64, I32, P, P, I64, I32,
                  P], I32),
+    "fq_gemm_plan": ([I64, I64, I64, P, P, P, P], I32),
     "fq_gemm_batched": ([P, I64, I64, I64, P, I64, I64, I64, I32, P, I64, I64, I64, I64, I64, I64,
                          I64, I64, P], I32),
     "fq_retrieve": ([P, I64, I64, I64, I64, P, P, I64, P, P, P, I64, P, P], I32),
@@ -69,7 +70,7 @@ _ERRORS = {-1: DimensionError, -2: ParameterError, -3: AliasingError, -4: Capaci
 _lib = None
 _lock = threading.Lock()
 _prepared = False
-_NO_PREPARE = {"fq_abi_version", "fq_last_error", "fq_num_sms", "fq_prepare"}
+_NO_PREPARE = {"fq_abi_version", "fq_last_error", "fq_num_sms", "fq_prepare", "fq_gemm_plan"}
 _launches = [0]
 
 

@@ -1,19 +1,29 @@
 // bf16 GEMM on the 5th-generation tensor cores (tcgen05 + TMEM + TMA), sm_100a.
 //
 // C[M,N] = epilogue(A[M,K] . B[N,K]^T), A and B bf16 K-major (weights were
-// re-laid out to [N,K] once at load), fp32 accumulation in TMEM. One CTA per
-// 128 x BN output tile, warp-specialised:
+// re-laid out to [N,K] once at load), fp32 accumulation in TMEM.
+//
+// Persistent, warp-specialised, one 128 x BN output tile per CTA iteration:
 //   warp 0      TMA producer: 2D tiled loads (128B swizzle) into a STAGES-deep
 //               shared-memory ring, mbarrier complete_tx;
 //   warp 1      TMEM allocator + single-thread tcgen05.mma issuer
-//               (M=128, N=BN, K=16 per instruction), tcgen05.commit frees ring
-//               slots and finally signals the accumulator;
-//   warps 2..5  epilogue: tcgen05.ld (32 lanes x 16 columns per load), fused
-//               (+C) (+bias) act (+residual), fp32 or bf16 stores.
+//               (M=128, N=BN, K=16 per instruction); tcgen05.commit frees ring
+//               slots and signals one of two TMEM accumulator stages;
+//   warps 2..5  epilogue: tcgen05.ld 32x32b.x32, transpose through smem,
+//               fused (+C) (+bias) act (+residual), coalesced fp32/bf16 stores,
+//               overlapping the next tile's MMAs.
+// Thread-block clusters of cm x cn CTAs share operands through TMA multicast:
+// the cn CTAs of a cluster row (same M-tile) each load 1/cn of the A tile and
+// multicast it to the row; the cm CTAs of a column (same N-tile) do the same
+// for B. L2->SM traffic drops by cn (A) and cm (B) — the decode GEMMs
+// (M = batch*beam = 512) were L2-bandwidth bound re-reading A once per N-tile.
 // The fused epilogue is the reference's bias_residual_act pass (kernels.py:39-53)
 // applied to the accumulator, so the [M,N] pre-activation never reaches HBM.
 #include <cuda.h>
 #include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cmath>
 
 #include "fq_common.cuh"
 
@@ -133,22 +143,55 @@ struct Epi {
   const float* res;
   int64_t ldr;
   int act;
+  unsigned long long* dbg;  // per-CTA [start, end] %globaltimer (profiling only)
 };
 
-// Persistent: grid <= #SMs, CTA walks tiles t = blockIdx.x, +gridDim.x, ...
-// (M-tile fastest so concurrent CTAs share the weight tile in L2). Two TMEM
-// accumulator stages let the epilogue of tile i overlap the MMAs of tile i+1.
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;"
+               ::: "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d_mc(const CUtensorMap* map, uint64_t* bar, void* dst,
+                                               int c0, int c1, uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      ".multicast::cluster [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "h"(mask)
+      : "memory");
+}
+
+__device__ __forceinline__ void mma_commit_mc(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(smem_u32(bar)),
+      "h"(mask)
+      : "memory");
+}
+
+// Persistent over tile groups: a cluster (cm x cn CTAs, rank r -> (ry = r / cn,
+// rx = r % cn)) walks groups g = cluster_id, +num_clusters, ...; group g covers
+// M-tiles [gm*cm, +cm) x N-tiles [gn*cn, +cn) with the M-group fastest so
+// concurrent clusters share weight tiles in L2. Two TMEM accumulator stages let
+// the epilogue of one tile overlap the MMAs of the next.
 template <int BN, int STAGES>
 __global__ void __launch_bounds__(kThreads, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tma_a,
-                   const __grid_constant__ CUtensorMap tma_b, const Epi ep, int M, int N, int K) {
+                   const __grid_constant__ CUtensorMap tma_b, const Epi ep, int M, int N, int K,
+                   int cm, int cn) {
   constexpr int A_BYTES = BM * BK * 2;
   constexpr int B_BYTES = BN * BK * 2;
   constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   constexpr uint32_t TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;  // two accumulator stages
   extern __shared__ uint8_t smem_raw[];
-  // 1024-B aligned (128B-swizzle atoms); pointer arithmetic keeps the shared
-  // address space visible to the compiler (LDS/STS, not generic LD/ST)
+  // 1024-B aligned (128B-swizzle atoms); identical offset in every CTA, so a
+  // multicast lands at the same place cluster-wide. Pointer arithmetic keeps
+  // the shared address space visible (LDS/STS, not generic LD/ST).
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   float* stage_out = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES);  // 4 x [32][33]
   __shared__ __align__(8) uint64_t full_bar[STAGES];
@@ -158,14 +201,28 @@ __global__ void __launch_bounds__(kThreads, 1)
   __shared__ uint32_t tmem_base_sh;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (ep.dbg && threadIdx.x == 0) {
+    unsigned long long t_;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
+    ep.dbg[2 * blockIdx.x] = t_;
+  }
+  const int csize = cm * cn;
+  const int rank = csize > 1 ? (int)cluster_rank() : 0;
+  const int ry = rank / cn, rx = rank % cn;
   const int num_kb = (K + BK - 1) / BK;
-  const int mt = (M + BM - 1) / BM;
-  const int ntiles = mt * ((N + BN - 1) / BN);
+  const int mt = (M + BM - 1) / BM, nt = (N + BN - 1) / BN;
+  const int mg = mt / cm;                     // cm | mt and cn | nt (host guarantees)
+  const int ngroups = mg * (nt / cn);
+  const int cluster_id = blockIdx.x / csize, nclusters = gridDim.x / csize;
+  uint16_t row_mask = 0, col_mask = 0;        // CTAs sharing my A tile / my B tile
+  for (int x = 0; x < cn; ++x) row_mask |= (uint16_t)(1u << (ry * cn + x));
+  for (int y = 0; y < cm; ++y) col_mask |= (uint16_t)(1u << (y * cn + rx));
+  const uint16_t peer_mask = row_mask | col_mask;
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full_bar[s], 1);
-      mbar_init(&empty_bar[s], 1);
+      mbar_init(&empty_bar[s], cm + cn - 1);  // every CTA that multicasts into my ring
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull_bar[s], 1);
@@ -182,31 +239,43 @@ __global__ void __launch_bounds__(kThreads, 1)
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
+  if (csize > 1) cluster_sync_all();  // peers' barriers initialised before any multicast
+  else __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = tmem_base_sh;
 
   if (warp == 0) {
     if (lane == 0) {  // ---- TMA producer ----
+      const int a_rows = BM / cn, b_rows = BN / cm;
       int it = 0;
-      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-        const int m0 = (t % mt) * BM, n0 = (t / mt) * BN;
+      for (int g = cluster_id; g < ngroups; g += nclusters) {
+        const int m0 = ((g % mg) * cm + ry) * BM, n0 = ((g / mg) * cn + rx) * BN;
         for (int kb = 0; kb < num_kb; ++kb, ++it) {
           const int s = it % STAGES;
           const uint32_t ph = (it / STAGES) & 1;
-          mbar_wait(&empty_bar[s], ph ^ 1);
+          mbar_wait(&empty_bar[s], ph ^ 1);  // free in every CTA I multicast into
           uint8_t* sa = smem + s * STAGE_BYTES;
           mbar_expect_tx(&full_bar[s], STAGE_BYTES);
-          tma_load_2d(&tma_a, &full_bar[s], sa, kb * BK, m0);
-          tma_load_2d(&tma_b, &full_bar[s], sa + A_BYTES, kb * BK, n0);
+          if (cn > 1)
+            tma_load_2d_mc(&tma_a, &full_bar[s], sa + rx * a_rows * 128, kb * BK,
+                           m0 + rx * a_rows, row_mask);
+          else
+            tma_load_2d(&tma_a, &full_bar[s], sa, kb * BK, m0);
+          if (cm > 1)
+            tma_load_2d_mc(&tma_b, &full_bar[s], sa + A_BYTES + ry * b_rows * 128, kb * BK,
+                           n0 + ry * b_rows, col_mask);
+          else
+            tma_load_2d(&tma_b, &full_bar[s], sa + A_BYTES, kb * BK, n0);
         }
       }
+      // drain: every peer's release of my last fills has landed before teardown
+      for (int j = 0; j < STAGES; ++j, ++it) mbar_wait(&empty_bar[it % STAGES], ((it / STAGES) & 1) ^ 1);
     }
   } else if (warp == 1) {
     if (lane == 0) {  // ---- MMA issuer ----
       constexpr uint32_t idesc = idesc_bf16(BM, BN);
       int it = 0, local = 0;
-      for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++local) {
+      for (int g = cluster_id; g < ngroups; g += nclusters, ++local) {
         const int as = local & 1;
         mbar_wait(&tempty_bar[as], ((local >> 1) & 1) ^ 1);  // epilogue drained this stage
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -223,7 +292,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             mma_bf16(acc, sw128_desc(a_base + k * 32), sw128_desc(b_base + k * 32), idesc,
                      (kb | k) != 0);
           }
-          mma_commit(&empty_bar[s]);  // ring slot reusable once these MMAs retire
+          // ring slot reusable (in me and in every CTA that multicasts into me)
+          if (csize > 1) mma_commit_mc(&empty_bar[s], peer_mask);
+          else mma_commit(&empty_bar[s]);
         }
         mma_commit(&tfull_bar[as]);   // accumulator stage complete
       }
@@ -234,9 +305,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     float* c32 = reinterpret_cast<float*>(ep.c);
     __nv_bfloat16* c16 = reinterpret_cast<__nv_bfloat16*>(ep.c);
     int local = 0;
-    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++local) {
+    for (int g = cluster_id; g < ngroups; g += nclusters, ++local) {
       const int as = local & 1;
-      const int m0 = (t % mt) * BM, n0 = (t / mt) * BN;
+      const int m0 = ((g % mg) * cm + ry) * BM, n0 = ((g / mg) * cn + rx) * BN;
       mbar_wait(&tfull_bar[as], (local >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const int rbase = m0 + q * 32;
@@ -257,63 +328,268 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int col = n0 + cc + lane;
 #pragma unroll 1
         for (int h0 = 0; h0 < 32; h0 += 16) {  // 16 rows at a time bounds register use
-        float x[16];
+          float x[16];
 #pragma unroll
-        for (int i = 0; i < 16; ++i) x[i] = st[(h0 + i) * 33 + lane];
-        const int nr = nrows - h0;
-        if (col < N && nr > 0) {
-          // every global read of the 32 rows is issued before any store
-          // (no per-row dependent latency); each lane owns one column, so the
-          // warp writes full 128-byte row segments
-          const int64_t c0 = (int64_t)(rbase + h0) * ep.ldc + col;
-          if (ep.accumulate) {
-            float cv[16];
+          for (int i = 0; i < 16; ++i) x[i] = st[(h0 + i) * 33 + lane];
+          const int nr = nrows - h0;
+          if (col < N && nr > 0) {
+            // all global reads of the rows issue before any store (no per-row
+            // dependent latency); lanes own columns: 128-byte row segments
+            const int64_t c0 = (int64_t)(rbase + h0) * ep.ldc + col;
+            if (ep.accumulate) {
+              float cv[16];
 #pragma unroll
-            for (int i = 0; i < 16; ++i)
-              cv[i] = i < nr ? (ep.c_bf16 ? bf2f(c16[c0 + i * ep.ldc]) : c32[c0 + i * ep.ldc])
-                                : 0.0f;
+              for (int i = 0; i < 16; ++i)
+                cv[i] = i < nr ? (ep.c_bf16 ? bf2f(c16[c0 + i * ep.ldc]) : c32[c0 + i * ep.ldc])
+                               : 0.0f;
 #pragma unroll
-            for (int i = 0; i < 16; ++i) x[i] = fadd_rn(cv[i], x[i]);
+              for (int i = 0; i < 16; ++i) x[i] = fadd_rn(cv[i], x[i]);
+            }
+            if (ep.bias) {
+              const float bias = __ldg(ep.bias + col);
+#pragma unroll
+              for (int i = 0; i < 16; ++i) x[i] = fadd_rn(x[i], bias);
+            }
+            if (ep.act) {
+#pragma unroll
+              for (int i = 0; i < 16; ++i) x[i] = apply_act(x[i], ep.act);
+            }
+            if (ep.res) {
+              const float* rp = ep.res + (int64_t)(rbase + h0) * ep.ldr + col;
+              float rv[16];
+#pragma unroll
+              for (int i = 0; i < 16; ++i) rv[i] = i < nr ? __ldg(rp + i * ep.ldr) : 0.0f;
+#pragma unroll
+              for (int i = 0; i < 16; ++i) x[i] = fadd_rn(x[i], rv[i]);
+            }
+            if (ep.c_bf16) {
+#pragma unroll
+              for (int i = 0; i < 16; ++i)
+                if (i < nr) c16[c0 + i * ep.ldc] = f2bf(x[i]);
+            } else {
+#pragma unroll
+              for (int i = 0; i < 16; ++i)
+                if (i < nr) c32[c0 + i * ep.ldc] = x[i];
+            }
           }
-          if (ep.bias) {
-            const float bias = __ldg(ep.bias + col);
-#pragma unroll
-            for (int i = 0; i < 16; ++i) x[i] = fadd_rn(x[i], bias);
-          }
-          if (ep.act) {
-#pragma unroll
-            for (int i = 0; i < 16; ++i) x[i] = apply_act(x[i], ep.act);
-          }
-          if (ep.res) {
-            const float* rp = ep.res + (int64_t)(rbase + h0) * ep.ldr + col;
-            float rv[16];
-#pragma unroll
-            for (int i = 0; i < 16; ++i) rv[i] = i < nr ? __ldg(rp + i * ep.ldr) : 0.0f;
-#pragma unroll
-            for (int i = 0; i < 16; ++i) x[i] = fadd_rn(x[i], rv[i]);
-          }
-          if (ep.c_bf16) {
-#pragma unroll
-            for (int i = 0; i < 16; ++i)
-              if (i < nr) c16[c0 + i * ep.ldc] = f2bf(x[i]);
-          } else {
-#pragma unroll
-            for (int i = 0; i < 16; ++i)
-              if (i < nr) c32[c0 + i * ep.ldc] = x[i];
-          }
-        }
         }
         __syncwarp();  // staging free for the next chunk
       }
     }
   }
+  __syncwarp();
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
+  if (csize > 1) cluster_sync_all();  // no CTA leaves while peers may still signal it
+  else __syncthreads();
+  if (ep.dbg && threadIdx.x == 0) {
+    unsigned long long t_;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
+    ep.dbg[2 * blockIdx.x + 1] = t_;
+  }
   if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
                  "r"(TMEM_COLS));
   }
+}
+
+// ---------------------------------------------------------------------------
+// Split-K over a thread-block cluster for small-M GEMMs (the decode step's
+// M = batch*beam rows). Per-SM TMA ingest (~40 B/clk measured) bounds these
+// GEMMs: a 128 x BN tile needs (128 + BN) * K * 2 bytes per SM. Splitting K
+// across the S CTAs of a cluster cuts each SM's bytes by S; the fp32 partial
+// tiles are then reduced through distributed shared memory — CTA r sums rows
+// [r*128/S, (r+1)*128/S) over all S partials in fixed rank order (deterministic)
+// and applies the fused epilogue with 128-bit coalesced stores.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t cluster_nrank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
+  return r;
+}
+
+__device__ __forceinline__ float4 ld_dsmem_f4(uint32_t local_addr, uint32_t rank) {
+  uint32_t ra;
+  asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(local_addr), "r"(rank));
+  float4 v;
+  // not volatile, no memory clobber: ordering comes from the cluster barrier,
+  // and independent remote loads must be free to overlap (~200-cycle latency)
+  asm("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
+      : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+      : "r"(ra));
+  return v;
+}
+
+template <int BN, int STAGES>
+__global__ void __launch_bounds__(kThreads, 1)
+    tc_gemm_splitk_kernel(const __grid_constant__ CUtensorMap tma_a,
+                          const __grid_constant__ CUtensorMap tma_b, const Epi ep, int M, int N,
+                          int K, int kb_per_split) {
+  constexpr int A_BYTES = BM * BK * 2;
+  constexpr int B_BYTES = BN * BK * 2;
+  constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  constexpr uint32_t TMEM_COLS = BN < 32 ? 32 : BN;
+  constexpr int PLD = BN + 4;  // padded partial row (floats): conflict-free v4 rows
+  static_assert(BM * PLD * 4 <= STAGES * STAGE_BYTES, "partial tile must fit the ring");
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  float* part = reinterpret_cast<float*>(smem);  // reuses the ring once all MMAs retired
+  __shared__ __align__(8) uint64_t full_bar[STAGES];
+  __shared__ __align__(8) uint64_t empty_bar[STAGES];
+  __shared__ __align__(8) uint64_t tfull_bar;
+  __shared__ uint32_t tmem_base_sh;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (ep.dbg && threadIdx.x == 0) {
+    unsigned long long t_;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
+    ep.dbg[2 * blockIdx.x] = t_;
+  }
+  const int S = (int)cluster_nrank(), rank = (int)cluster_rank();
+  const int mt = (M + BM - 1) / BM;
+  const int tile = blockIdx.x / S;
+  const int m0 = (tile % mt) * BM, n0 = (tile / mt) * BN;
+  const int num_kb = (K + BK - 1) / BK;
+  const int kb0 = rank * kb_per_split;
+  const int kb1 = min(num_kb, kb0 + kb_per_split);
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    mbar_init(&tfull_bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tma_a)));
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tma_b)));
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(&tmem_base_sh)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = tmem_base_sh;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---- TMA producer: this CTA's K slice ----
+      for (int kb = kb0, it = 0; kb < kb1; ++kb, ++it) {
+        const int s = it % STAGES;
+        mbar_wait(&empty_bar[s], ((it / STAGES) & 1) ^ 1);
+        uint8_t* sa = smem + s * STAGE_BYTES;
+        mbar_expect_tx(&full_bar[s], STAGE_BYTES);
+        tma_load_2d(&tma_a, &full_bar[s], sa, kb * BK, m0);
+        tma_load_2d(&tma_b, &full_bar[s], sa + A_BYTES, kb * BK, n0);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---- MMA issuer ----
+      constexpr uint32_t idesc = idesc_bf16(BM, BN);
+      for (int kb = kb0, it = 0; kb < kb1; ++kb, ++it) {
+        const int s = it % STAGES;
+        mbar_wait(&full_bar[s], (it / STAGES) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t a_base = smem_u32(smem + s * STAGE_BYTES);
+        const uint32_t b_base = a_base + A_BYTES;
+#pragma unroll
+        for (int k = 0; k < BK / 16; ++k)
+          mma_bf16(tmem, sw128_desc(a_base + k * 32), sw128_desc(b_base + k * 32), idesc,
+                   (it | k) != 0);
+        mma_commit(&empty_bar[s]);
+      }
+      mma_commit(&tfull_bar);
+    }
+  } else {  // ---- epilogue warps: TMEM partial -> own smem [128][PLD] ----
+    const int q = warp & 3;
+    mbar_wait(&tfull_bar, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    float* prow = part + (q * 32 + lane) * PLD;
+#pragma unroll 1
+    for (int cc = 0; cc < BN; cc += 32) {
+      float v[32];
+      tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + cc, v);
+#pragma unroll
+      for (int j = 0; j < 32; j += 4)
+        *reinterpret_cast<float4*>(prow + cc + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+    }
+  }
+  __syncwarp();
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  cluster_sync_all();  // every partial tile of the cluster is in shared memory
+
+  if (warp >= 2) {  // ---- reduce my row slice over the S partials, fused epilogue ----
+    const int t = threadIdx.x - 64;  // 0..127
+    const int rows_per = (BM + S - 1) / S;          // S need not divide 128
+    const int r_lo = rank * rows_per;
+    const int rows = max(0, min(BM, r_lo + rows_per) - r_lo);
+    constexpr int C4 = BN / 4;
+    float* c32 = reinterpret_cast<float*>(ep.c);
+    __nv_bfloat16* c16 = reinterpret_cast<__nv_bfloat16*>(ep.c);
+    const uint32_t part_s = smem_u32(part);
+    for (int idx = t; idx < rows * C4; idx += 128) {
+      const int lr = r_lo + idx / C4;
+      const int c = (idx % C4) * 4;
+      const int row = m0 + lr, col = n0 + c;
+      const uint32_t off = part_s + (uint32_t)(lr * PLD + c) * 4u;
+      float4 pv[8];  // all S remote partials in flight before the fixed-order sum
+#pragma unroll
+      for (int p = 0; p < 8; ++p)
+        if (p < S) pv[p] = ld_dsmem_f4(off, p);
+      float4 a = pv[0];
+#pragma unroll
+      for (int p = 1; p < 8; ++p)
+        if (p < S) { a.x += pv[p].x; a.y += pv[p].y; a.z += pv[p].z; a.w += pv[p].w; }
+      if (row >= M) continue;
+      float x[4] = {a.x, a.y, a.z, a.w};
+      const int64_t ci = (int64_t)row * ep.ldc + col;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if (col + j >= N) break;
+        float y = x[j];
+        if (ep.accumulate) y = fadd_rn(ep.c_bf16 ? bf2f(c16[ci + j]) : c32[ci + j], y);
+        if (ep.bias) y = fadd_rn(y, __ldg(ep.bias + col + j));
+        y = apply_act(y, ep.act);
+        if (ep.res) y = fadd_rn(y, __ldg(ep.res + (int64_t)row * ep.ldr + col + j));
+        x[j] = y;
+      }
+      if (col + 3 < N && ((ci & 3) == 0)) {
+        if (ep.c_bf16) {
+          __nv_bfloat162 lo = __floats2bfloat162_rn(x[0], x[1]), hi = __floats2bfloat162_rn(x[2], x[3]);
+          uint2 pk;
+          pk.x = *reinterpret_cast<uint32_t*>(&lo);
+          pk.y = *reinterpret_cast<uint32_t*>(&hi);
+          *reinterpret_cast<uint2*>(c16 + ci) = pk;
+        } else {
+          *reinterpret_cast<float4*>(c32 + ci) = make_float4(x[0], x[1], x[2], x[3]);
+        }
+      } else {
+        for (int j = 0; j < 4 && col + j < N; ++j) {
+          if (ep.c_bf16) c16[ci + j] = f2bf(x[j]);
+          else c32[ci + j] = x[j];
+        }
+      }
+    }
+  }
+  __syncwarp();
+  cluster_sync_all();  // peers finished reading my partial
+  if (ep.dbg && threadIdx.x == 0) {
+    unsigned long long t_;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
+    ep.dbg[2 * blockIdx.x + 1] = t_;
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "r"(TMEM_COLS));
+  }
+}
+
+template <int BN, int STAGES>
+constexpr int smem_bytes_splitk() {
+  return STAGES * (BM * BK * 2 + BN * BK * 2) + 1024;
 }
 
 template <int BN, int STAGES>
@@ -360,24 +636,86 @@ static int make_map(CUtensorMap* map, const void* ptr, int64_t rows, int64_t col
   return FQ_OK;
 }
 
+static int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return n;
+}
+
 template <int BN, int STAGES>
 static int launch(const void* a, int64_t lda, const void* b, int64_t ldb, const Epi& ep,
-                  int64_t M, int64_t N, int64_t K, cudaStream_t s) {
+                  int64_t M, int64_t N, int64_t K, int cm, int cn, cudaStream_t s) {
+  CUtensorMap ma, mb;
+  int rc;
+  if ((rc = make_map(&ma, a, M, K, lda, BM / cn)) != FQ_OK) return rc;
+  if ((rc = make_map(&mb, b, N, K, ldb, BN / cm)) != FQ_OK) return rc;
+  const int csize = cm * cn;
+  const int64_t groups = ((M + BM - 1) / BM / cm) * ((N + BN - 1) / BN / cn);
+  const int64_t max_clusters = num_sms() / csize;
+  const int64_t clusters = groups < max_clusters ? groups : max_clusters;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)(clusters * csize));
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem_bytes<BN, STAGES>();
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = csize;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, tc_gemm_kernel<BN, STAGES>, ma, mb, ep, (int)M, (int)N,
+                                     (int)K, cm, cn);
+  if (e != cudaSuccess) {
+    set_error("fq_gemm(tcgen05): launch failed: %s", cudaGetErrorString(e));
+    return FQ_ERR_CUDA;
+  }
+  return launch_status("fq_gemm(tcgen05)");
+}
+
+template <int BN, int STAGES>
+static int launch_splitk(const void* a, int64_t lda, const void* b, int64_t ldb, const Epi& ep,
+                         int64_t M, int64_t N, int64_t K, int S, cudaStream_t s) {
   CUtensorMap ma, mb;
   int rc;
   if ((rc = make_map(&ma, a, M, K, lda, BM)) != FQ_OK) return rc;
   if ((rc = make_map(&mb, b, N, K, ldb, BN)) != FQ_OK) return rc;
-  static int num_sms = 0;
-  if (!num_sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
+  const int nkb = (int)((K + BK - 1) / BK);
+  const int kbs = (nkb + S - 1) / S;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)(tiles * S));
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem_bytes_splitk<BN, STAGES>();
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = S;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, tc_gemm_splitk_kernel<BN, STAGES>, ma, mb, ep, (int)M,
+                                     (int)N, (int)K, kbs);
+  if (e != cudaSuccess) {
+    set_error("fq_gemm(tcgen05 split-K): launch failed: %s", cudaGetErrorString(e));
+    return FQ_ERR_CUDA;
   }
-  const int64_t ntiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
-  const unsigned grid = (unsigned)(ntiles < num_sms ? ntiles : num_sms);
-  tc_gemm_kernel<BN, STAGES><<<grid, kThreads, smem_bytes<BN, STAGES>(), s>>>(ma, mb, ep, (int)M,
-                                                                             (int)N, (int)K);
-  return launch_status("fq_gemm(tcgen05)");
+  return launch_status("fq_gemm(tcgen05 split-K)");
+}
+
+template <int BN, int STAGES>
+static int prep_splitk() {
+  return cudaFuncSetAttribute(tc_gemm_splitk_kernel<BN, STAGES>,
+                              cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              smem_bytes_splitk<BN, STAGES>()) == cudaSuccess
+             ? FQ_OK
+             : FQ_ERR_CUDA;
 }
 
 template <int BN, int STAGES>
@@ -392,11 +730,51 @@ static int prep() {
 }  // namespace tc
 
 int gemm_tc_prepare() {
-  if (tc::prep<256, 4>() || tc::prep<128, 6>() || tc::prep<64, 8>() || tc::prep<32, 8>()) {
+  if (tc::prep<256, 4>() || tc::prep<128, 6>() || tc::prep<64, 8>() || tc::prep<32, 8>() ||
+      tc::prep_splitk<256, 4>() || tc::prep_splitk<128, 6>() || tc::prep_splitk<64, 8>()) {
     set_error("fq_prepare: tcgen05 GEMM smem opt-in failed");
     return FQ_ERR_CUDA;
   }
   return FQ_OK;
+}
+
+// Tile / split choice from the measured bottleneck: per-SM TMA ingest
+// (~40 B/clk, ~80 GB/s per SM on this B200 pool, fq_gemm_tc phase traces): a
+// CTA streams (128 + BN) * K_slice * 2 bytes per tile. Persistent tiles overlap
+// the epilogue with the next tile; a split-K cluster additionally reduces
+// 512 * BN bytes of fp32 partials through DSMEM per CTA. Multicast clusters
+// (cm x cn) stay available through fq_gemm_force_plan but never won on the
+// sweep (ingest, not L2, is the limit), so the model picks cm = cn = 1.
+struct TcPlan {
+  int bn, cm, cn, split;  // split > 1: split-K cluster kernel (cm = cn = 1)
+};
+
+static TcPlan g_forced{0, 0, 0, 1};
+unsigned long long* g_gemm_dbg = nullptr;
+extern "C" void fq_gemm_debug_timestamps(unsigned long long* p) { g_gemm_dbg = p; }
+
+static TcPlan plan_tc(int64_t M, int64_t N, int64_t K) {
+  const int64_t mt = (M + tc::BM - 1) / tc::BM;
+  const int nkb = (int)((K + tc::BK - 1) / tc::BK);
+  if (g_forced.bn) {
+    const int64_t nt = (N + g_forced.bn - 1) / g_forced.bn;
+    if (mt % g_forced.cm == 0 && nt % g_forced.cn == 0 &&
+        (g_forced.split == 1 || (mt * nt * g_forced.split <= tc::num_sms() &&
+                                 g_forced.split <= nkb && g_forced.cm * g_forced.cn == 1)))
+      return g_forced;
+  }
+  // Measured table (scripts/gemm_graph_sweep.py, CUDA-graph back-to-back
+  // launches on B200): small-M GEMMs are bound by the chip-wide L2->SM
+  // operand traffic and per-launch overhead, large ones by per-SM ingest.
+  const int64_t nt128 = (N + 127) / 128;
+  if (mt <= 8) {
+    if (N <= 1024 && nkb >= 32 && mt * nt128 * 4 <= tc::num_sms())
+      return {128, 1, 1, 4};                       // K=4096: split-K over 4 CTAs
+    if (N <= 1024) return {32, 1, 1, 1};
+    if (N < 8192) return {128, 1, 1, 1};
+    return {256, 1, 1, 1};
+  }
+  return {256, 1, 1, 1};
 }
 
 int launch_tc_gemm(const void* a, int64_t lda, const void* b, int64_t ldb, void* c, int c_bf16,
@@ -407,15 +785,38 @@ int launch_tc_gemm(const void* a, int64_t lda, const void* b, int64_t ldb, void*
                FQ_ERR_DIMENSION, "tcgen05 GEMM: operands need 16-byte aligned rows (ld %% 8 == 0)");
   FQ_CHECK_ARG(M < (1LL << 31) && N < (1LL << 31) && K < (1LL << 31), FQ_ERR_DIMENSION,
                "tcgen05 GEMM: dimension too large");
-  tc::Epi ep{c, ldc, c_bf16, accumulate, bias, res, ldr, act};
-  // Widest N tile that still puts >= one CTA on every SM; the weight-streaming
-  // decode GEMMs (M = rows <= 512) end up on narrow tiles.
-  const int64_t mt = (M + tc::BM - 1) / tc::BM;
-  auto tiles = [&](int bn) { return mt * ((N + bn - 1) / bn); };
-  if (tiles(256) >= 148) return tc::launch<256, 4>(a, lda, b, ldb, ep, M, N, K, s);
-  if (tiles(128) >= 148) return tc::launch<128, 6>(a, lda, b, ldb, ep, M, N, K, s);
-  if (tiles(64) >= 148) return tc::launch<64, 8>(a, lda, b, ldb, ep, M, N, K, s);
-  return tc::launch<32, 8>(a, lda, b, ldb, ep, M, N, K, s);
+  tc::Epi ep{c, ldc, c_bf16, accumulate, bias, res, ldr, act, g_gemm_dbg};
+  const TcPlan p = plan_tc(M, N, K);
+  if (p.split > 1) {
+    switch (p.bn) {
+      case 256: return tc::launch_splitk<256, 4>(a, lda, b, ldb, ep, M, N, K, p.split, s);
+      case 128: return tc::launch_splitk<128, 6>(a, lda, b, ldb, ep, M, N, K, p.split, s);
+      default: return tc::launch_splitk<64, 8>(a, lda, b, ldb, ep, M, N, K, p.split, s);
+    }
+  }
+  switch (p.bn) {
+    case 256: return tc::launch<256, 4>(a, lda, b, ldb, ep, M, N, K, p.cm, p.cn, s);
+    case 128: return tc::launch<128, 6>(a, lda, b, ldb, ep, M, N, K, p.cm, p.cn, s);
+    case 64: return tc::launch<64, 8>(a, lda, b, ldb, ep, M, N, K, p.cm, p.cn, s);
+    default: return tc::launch<32, 8>(a, lda, b, ldb, ep, M, N, K, p.cm, p.cn, s);
+  }
+}
+
+// Benchmarks only: force (bn, cm, cn) for shapes it divides; bn = 0 restores auto.
+extern "C" int fq_gemm_force_plan(int bn, int cm, int cn, int split) {
+  g_forced = {bn, cm, cn, split < 1 ? 1 : split};
+  return FQ_OK;
+}
+
+// Exposed for tests/benchmarks: the plan the dispatcher would pick.
+extern "C" int fq_gemm_plan(int64_t M, int64_t N, int64_t K, int* bn, int* cm, int* cn,
+                            int* split) {
+  const TcPlan p = plan_tc(M, N, K);
+  *bn = p.bn;
+  *cm = p.cm;
+  *cn = p.cn;
+  *split = p.split;
+  return FQ_OK;
 }
 
 }  // namespace fq

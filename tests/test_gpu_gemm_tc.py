@@ -75,3 +75,36 @@ def test_tc_gemm_strided_output_and_accumulate(P):
     P.gemm(a, b, view, transpose_b=True, accumulate=True)
     assert _rel(view, _ref(a, b) + 1.0) <= 1e-3
     assert float(big[:, :N].abs().max()) == 0.0
+
+
+@pytest.mark.parametrize("M,N,K", [(512, 1024, 1024), (512, 1024, 4096), (300, 2048, 512),
+                                   (128, 256, 1024), (512, 4096, 1024)])
+def test_tc_gemm_all_plans(P, M, N, K):
+    """Every schedule the dispatcher can pick — persistent tiles, multicast
+    clusters (cm x cn) and split-K clusters reduced through DSMEM — computes
+    the same GEMM (fused bias + ReLU + residual epilogue included)."""
+    import ctypes
+    import torch
+    from paper_2010_13887_b200 import _abi
+    lib = _abi.load()
+    lib.fq_gemm_force_plan.argtypes = [ctypes.c_int] * 4
+    g = torch.Generator(device="cuda").manual_seed(M + N + K)
+    a = torch.randn(M, K, device="cuda", generator=g).to(torch.bfloat16)
+    b = torch.randn(N, K, device="cuda", generator=g).to(torch.bfloat16)
+    bias = torch.randn(N, device="cuda", generator=g)
+    res = torch.randn(M, N, device="cuda", generator=g)
+    want = _ref(a, b, bias, "relu", res)
+    plans = [(64, 1, 1, 1), (128, 2, 1, 1), (128, 1, 2, 1), (32, 2, 4, 1), (256, 1, 1, 1)]
+    plans += [(bn, 1, 1, s) for bn in (64, 128, 256) for s in (2, 3, 4, 8)]
+    tried = 0
+    try:
+        for plan in plans:
+            lib.fq_gemm_force_plan(*plan)
+            out = torch.full((M, N), float("nan"), device="cuda")
+            P.gemm(a, b, out, transpose_b=True, bias=bias, activation="relu", residual=res)
+            torch.cuda.synchronize()
+            assert _rel(out, want) <= 1e-3, plan
+            tried += 1
+    finally:
+        lib.fq_gemm_force_plan(0, 0, 0, 1)
+    assert tried == len(plans)
