@@ -150,6 +150,7 @@ __global__ void __launch_bounds__(256) encoder_attention_kernel(
     const float* __restrict__ qkv, int64_t ldq, int seq, int heads, int hd, float scale,
     const float* __restrict__ mask, float* __restrict__ out, __nv_bfloat16* __restrict__ out16,
     int64_t ldo, int exact, int* d_bad) {
+  pdl_enter();
   extern __shared__ float sm[];
   const int b = blockIdx.x / heads, h = blockIdx.x % heads;
   const int d = heads * hd;
@@ -185,6 +186,7 @@ __global__ void __launch_bounds__(128) decoder_self_attention_fast(
     const int32_t* __restrict__ hist, const int32_t* __restrict__ d_cur, int rows, int heads,
     int max_len, float scale, float* __restrict__ out, __nv_bfloat16* __restrict__ out16,
     int64_t ldo, int exact) {
+  pdl_enter();
   extern __shared__ float sm[];
   constexpr int EV = 16 / sizeof(KV);  // elements per 128-bit load
   constexpr int EPL = (HD + 31) / 32;  // output elements per lane in P.V
@@ -282,6 +284,7 @@ __global__ void __launch_bounds__(256) cross_attention_kernel(
     const KV* __restrict__ cv, int64_t ldkv, int beam, int seq, int heads, int hd, float scale,
     const float* __restrict__ mask, float* __restrict__ out, __nv_bfloat16* __restrict__ out16,
     int64_t ldo, int exact, int* d_bad) {
+  pdl_enter();
   extern __shared__ float sm[];
   const int b = blockIdx.x / heads, h = blockIdx.x % heads;
   const int hp = hd + 1;
@@ -314,6 +317,7 @@ __global__ void __launch_bounds__(128) cross_attention_fast(
     const KV* __restrict__ cv, int64_t ldkv, int beam, int seq, int heads, float scale,
     const float* __restrict__ mask, float* __restrict__ out, __nv_bfloat16* __restrict__ out16,
     int64_t ldo, int exact, int* d_bad) {
+  pdl_enter();
   constexpr int EV = 16 / sizeof(KV);
   constexpr int KP = HD + EV;  // padded K row (elements)
   extern __shared__ __align__(16) uint8_t smraw[];
@@ -427,6 +431,7 @@ __global__ void __launch_bounds__(128) decoder_self_attention_kernel(
     const int32_t* __restrict__ hist, const int32_t* __restrict__ d_cur, int rows, int heads,
     int hd, int max_len, float scale, float* __restrict__ out,
     __nv_bfloat16* __restrict__ out16, int64_t ldo, int exact) {
+  pdl_enter();
   extern __shared__ float sm[];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int r = blockIdx.x * (blockDim.x >> 5) + w;
@@ -518,7 +523,7 @@ static void launch_self_fast(dim3 grid, size_t smem, cudaStream_t s, const float
                              int64_t ldq, void* kc, void* vc, const int32_t* hist,
                              const int32_t* d_cur, int64_t rows, int64_t heads, int64_t max_len,
                              float scale, float* out, void* out16, int64_t ldo, int exact) {
-  decoder_self_attention_fast<KV, HD><<<grid, 128, smem, s>>>(
+  launch_kernel(decoder_self_attention_fast<KV, HD>, grid, 128, smem, s, 1u, 
       sqkv, ldq, (KV*)kc, (KV*)vc, hist, d_cur, (int)rows, (int)heads, (int)max_len, scale, out,
       reinterpret_cast<__nv_bfloat16*>(out16), ldo, exact);
 }
@@ -540,7 +545,7 @@ int fq_encoder_attention(const float* qkv, int64_t ldq, int64_t batch, int64_t s
   size_t smem = (size_t)(2 * seq * (head_dim + 1) + seq * head_dim + (threads / 32) * seq) * 4;
   FQ_CHECK_ARG(smem <= 227 * 1024, FQ_ERR_CAPACITY, "encoder attention: seq %lld too long",
                (long long)seq);
-  encoder_attention_kernel<<<(unsigned)(batch * heads), threads, smem, as_stream(stream)>>>(
+  launch_kernel(encoder_attention_kernel, (unsigned)(batch * heads), threads, smem, as_stream(stream), 1u, 
       qkv, ldq, (int)seq, (int)heads, (int)head_dim, scale, mask, out,
       reinterpret_cast<__nv_bfloat16*>(out16), ldo, exact, d_bad);
   return launch_status("fq_encoder_attention");
@@ -581,12 +586,12 @@ int fq_decoder_self_attention(const float* sqkv, int64_t ldq, void* kcache, void
   }
   size_t smem = (size_t)wpb * (max_len + 1) * 4;
   if (kv_dtype == FQ_F32) {
-    decoder_self_attention_kernel<float><<<grid, wpb * 32, smem, s>>>(
+    launch_kernel(decoder_self_attention_kernel<float>, grid, wpb * 32, smem, s, 1u, 
         sqkv, ldq, (float*)kcache, (float*)vcache, hist, d_cur, (int)rows, (int)heads,
         (int)head_dim, (int)max_len, scale, out, reinterpret_cast<__nv_bfloat16*>(out16), ldo,
         exact);
   } else {
-    decoder_self_attention_kernel<__nv_bfloat16><<<grid, wpb * 32, smem, s>>>(
+    launch_kernel(decoder_self_attention_kernel<__nv_bfloat16>, grid, wpb * 32, smem, s, 1u, 
         sqkv, ldq, (__nv_bfloat16*)kcache, (__nv_bfloat16*)vcache, hist, d_cur, (int)rows,
         (int)heads, (int)head_dim, (int)max_len, scale, out,
         reinterpret_cast<__nv_bfloat16*>(out16), ldo, exact);
@@ -613,7 +618,7 @@ int fq_cross_attention(const float* cq, int64_t ldcq, const void* ck, const void
   if (fast_ok) {
     cudaStream_t s = as_stream(stream);
 #define FQ_CROSS(KV, HD)                                                                   \
-  cross_attention_fast<KV, HD><<<grid, 128, fast_smem, s>>>(                               \
+  launch_kernel(cross_attention_fast<KV, HD>, grid, 128, fast_smem, s, 1u,                                \
       cq, ldcq, (const KV*)ck, (const KV*)cv, ldkv, (int)beam, (int)seq, (int)heads, scale, \
       mask, out, reinterpret_cast<__nv_bfloat16*>(out16), ldo, exact, d_bad)
     if (kv_dtype == FQ_F32) {
@@ -632,12 +637,12 @@ int fq_cross_attention(const float* cq, int64_t ldcq, const void* ck, const void
   size_t smem = (size_t)(2 * seq * (head_dim + 1) + (threads / 32) * (seq + head_dim)) * 4;
   FQ_CHECK_ARG(smem <= 227 * 1024, FQ_ERR_CAPACITY, "cross attention: seq too long");
   if (kv_dtype == FQ_F32) {
-    cross_attention_kernel<float><<<grid, threads, smem, as_stream(stream)>>>(
+    launch_kernel(cross_attention_kernel<float>, grid, threads, smem, as_stream(stream), 1u, 
         cq, ldcq, (const float*)ck, (const float*)cv, ldkv, (int)beam, (int)seq, (int)heads,
         (int)head_dim, scale, mask, out, reinterpret_cast<__nv_bfloat16*>(out16), ldo, exact,
         d_bad);
   } else {
-    cross_attention_kernel<__nv_bfloat16><<<grid, threads, smem, as_stream(stream)>>>(
+    launch_kernel(cross_attention_kernel<__nv_bfloat16>, grid, threads, smem, as_stream(stream), 1u, 
         cq, ldcq, (const __nv_bfloat16*)ck, (const __nv_bfloat16*)cv, ldkv, (int)beam,
         (int)seq, (int)heads, (int)head_dim, scale, mask, out,
         reinterpret_cast<__nv_bfloat16*>(out16), ldo, exact, d_bad);

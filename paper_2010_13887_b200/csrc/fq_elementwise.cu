@@ -21,6 +21,7 @@ __global__ void __launch_bounds__(256) layer_norm_kernel(
     const float* __restrict__ res, int64_t ldr, const float* __restrict__ gamma,
     const float* __restrict__ beta, double eps, int d, float* __restrict__ out, int64_t ldo,
     __nv_bfloat16* __restrict__ out16, int64_t ldo16) {
+  pdl_enter();
   extern __shared__ float srow[];
   __shared__ double red[8];
   const int64_t row = blockIdx.x;
@@ -57,6 +58,7 @@ __global__ void __launch_bounds__(256) layer_norm_warp_kernel(
     const float* __restrict__ res, int64_t ldr, const float* __restrict__ gamma,
     const float* __restrict__ beta, double eps, int64_t rows, int d, float* __restrict__ out,
     int64_t ldo, __nv_bfloat16* __restrict__ out16, int64_t ldo16) {
+  pdl_enter();
   const int lane = threadIdx.x & 31;
   const int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   if (row >= rows) return;
@@ -121,6 +123,7 @@ __global__ void __launch_bounds__(128) layer_norm_row128_kernel(
     const float* __restrict__ res, int64_t ldr, const float* __restrict__ gamma,
     const float* __restrict__ beta, double eps, int d, float* __restrict__ out, int64_t ldo,
     __nv_bfloat16* __restrict__ out16, int64_t ldo16) {
+  pdl_enter();
   __shared__ double red[2][4];
   const int64_t row = blockIdx.x;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -193,7 +196,7 @@ static void launch_ln(const float* x, int64_t ldx, const float* bias, const floa
   if (row128) {
     // few rows (decoder): 128 threads per row keep enough loads in flight
 #define FQ_LN128(V)                                                                       \
-  layer_norm_row128_kernel<kBiasRes, V><<<(unsigned)rows, 128, 0, s>>>(                   \
+  launch_kernel(layer_norm_row128_kernel<kBiasRes, V>, (unsigned)rows, 128, 0, s, 1u,                    \
       x, ldx, bias, res, ldr, gamma, beta, eps, (int)d, out, ldo, out16, ldo16)
     if (d == 512) FQ_LN128(1);
     else if (d == 1024) FQ_LN128(2);
@@ -201,11 +204,11 @@ static void launch_ln(const float* x, int64_t ldx, const float* bias, const floa
 #undef FQ_LN128
   } else if (warp_ok) {
     const int64_t threads = rows * 32;
-    layer_norm_warp_kernel<kBiasRes><<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(
+    launch_kernel(layer_norm_warp_kernel<kBiasRes>, (unsigned)((threads + 255) / 256), 256, 0, s, 1u, 
         x, ldx, bias, res, ldr, gamma, beta, eps, rows, (int)d, out, ldo, out16, ldo16);
   } else {
     int threads = d >= 1024 ? 256 : 128;
-    layer_norm_kernel<kBiasRes><<<(unsigned)rows, threads, d * sizeof(float), s>>>(
+    launch_kernel(layer_norm_kernel<kBiasRes>, (unsigned)rows, threads, d * sizeof(float), s, 1u, 
         x, ldx, bias, res, ldr, gamma, beta, eps, (int)d, out, ldo, out16, ldo16);
   }
 }
@@ -215,6 +218,7 @@ __global__ void bias_residual_act_kernel(const float* __restrict__ x, int64_t ld
                                          const float* __restrict__ bias,
                                          const float* __restrict__ res, int64_t ldr, int act,
                                          int64_t rows, int d, float* out, int64_t ldo) {
+  pdl_enter();
   const int64_t n = rows * d;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -231,6 +235,7 @@ __global__ void bias_reshape_kernel(const float* __restrict__ x, int64_t ldx,
                                     const float* __restrict__ bias, int64_t seq, int heads,
                                     int hd, int parts, int64_t n_rows, float* __restrict__ o0,
                                     float* __restrict__ o1, float* __restrict__ o2) {
+  pdl_enter();
   const int d = heads * hd;
   const int64_t per_part = n_rows * d;
   const int64_t total = per_part * parts;
@@ -253,6 +258,7 @@ __global__ void scale_mask_softmax_kernel(const float* __restrict__ sc, int64_t 
                                           int64_t ldo, int64_t rows, int64_t rows_per_b,
                                           int l, float scale, const float* __restrict__ mask,
                                           int* d_bad) {
+  pdl_enter();
   const int lane = threadIdx.x & 31;
   const int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   if (row >= rows) return;
@@ -290,6 +296,7 @@ __global__ void embed_kernel(const int64_t* __restrict__ tok, int64_t n,
                              const float* __restrict__ pos, int64_t off,
                              const int32_t* __restrict__ d_off, int64_t seq, float* out,
                              __nv_bfloat16* out16) {
+  pdl_enter();
   const int64_t base = d_off ? (int64_t)(*d_off) : off;
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < n * d;
        idx += (int64_t)gridDim.x * blockDim.x) {
@@ -307,6 +314,7 @@ __global__ void kv_kernel(const float* __restrict__ sk, const float* __restrict_
                           const float* __restrict__ nk, const float* __restrict__ nv,
                           const int64_t* __restrict__ parents, int64_t cur, int64_t rows,
                           int heads, int64_t S, int hd, float* dk, float* dv) {
+  pdl_enter();
   const int64_t hist = parents ? cur + 1 : 1;  // positions written per (r, h)
   const int64_t total = rows * heads * hist * hd;
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
@@ -374,7 +382,7 @@ int fq_bias_residual_act(const float* x, int64_t ldx, const float* bias, const f
   FQ_CHECK_ARG(x && bias && out && d > 0, FQ_ERR_DIMENSION, "fq_bias_residual_act: bad args");
   FQ_CHECK_ARG(act >= 0 && act <= 2, FQ_ERR_PARAMETER, "unknown activation %d", act);
   if (rows == 0) return FQ_OK;
-  bias_residual_act_kernel<<<grid_for(rows * d, 256), 256, 0, as_stream(stream)>>>(
+  launch_kernel(bias_residual_act_kernel, grid_for(rows * d, 256), 256, 0, as_stream(stream), 1u, 
       x, ldx, bias, residual, ldr, act, rows, (int)d, out, ldo);
   return launch_status("fq_bias_residual_act");
 }
@@ -385,7 +393,7 @@ int fq_qkv_bias_reshape(const float* qkv, int64_t ldq, const float* bias, int64_
   FQ_CHECK_ARG(qkv && bias && q && k && v && batch > 0 && seq > 0 && heads > 0 && head_dim > 0,
                FQ_ERR_DIMENSION, "fq_qkv_bias_reshape: bad args");
   int64_t n = batch * seq * heads * head_dim * 3;
-  bias_reshape_kernel<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(
+  launch_kernel(bias_reshape_kernel, grid_for(n, 256), 256, 0, as_stream(stream), 1u, 
       qkv, ldq, bias, seq, (int)heads, (int)head_dim, 3, batch * seq, q, k, v);
   return launch_status("fq_qkv_bias_reshape");
 }
@@ -396,7 +404,7 @@ int fq_bias_reshape_heads(const float* x, int64_t ldx, const float* bias, int64_
   FQ_CHECK_ARG(x && bias && out && batch > 0 && seq > 0 && heads > 0 && head_dim > 0,
                FQ_ERR_DIMENSION, "fq_bias_reshape_heads: bad args");
   int64_t n = batch * seq * heads * head_dim;
-  bias_reshape_kernel<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(
+  launch_kernel(bias_reshape_kernel, grid_for(n, 256), 256, 0, as_stream(stream), 1u, 
       x, ldx, bias, seq, (int)heads, (int)head_dim, 1, batch * seq, out, nullptr, nullptr);
   return launch_status("fq_bias_reshape_heads");
 }
@@ -408,7 +416,7 @@ int fq_scale_mask_softmax(const float* scores, int64_t ld, float* out, int64_t l
                FQ_ERR_DIMENSION, "fq_scale_mask_softmax: bad shape");
   int64_t rows = b * h * q;
   int64_t threads = rows * 32;
-  scale_mask_softmax_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, as_stream(stream)>>>(
+  launch_kernel(scale_mask_softmax_kernel, (unsigned)((threads + 255) / 256), 256, 0, as_stream(stream), 1u, 
       scores, ld, out, ldo, rows, h * q, (int)l, scale, mask, d_bad);
   return launch_status("fq_scale_mask_softmax");
 }
@@ -419,7 +427,7 @@ int fq_embed_scale_pos(const int64_t* tokens, int64_t n, const float* emb, int64
   FQ_CHECK_ARG(tokens && emb && pos && d > 0 && seq > 0 && (out || out16), FQ_ERR_DIMENSION,
                "fq_embed_scale_pos: bad args");
   if (n == 0) return FQ_OK;
-  embed_kernel<<<grid_for(n * d, 256), 256, 0, as_stream(stream)>>>(
+  launch_kernel(embed_kernel, grid_for(n * d, 256), 256, 0, as_stream(stream), 1u, 
       tokens, n, emb, (int)d, scale, pos, pos_offset, d_off, seq, out,
       reinterpret_cast<__nv_bfloat16*>(out16));
   return launch_status("fq_embed_scale_pos");
@@ -431,7 +439,7 @@ int fq_kv_append(const float* new_k, const float* new_v, int64_t cur, int64_t ro
   FQ_CHECK_ARG(cur >= 0 && cur < max_seq, FQ_ERR_CAPACITY, "KV cache full at %lld positions",
                (long long)cur);
   int64_t n = rows * heads * head_dim;
-  kv_kernel<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(
+  launch_kernel(kv_kernel, grid_for(n, 256), 256, 0, as_stream(stream), 1u, 
       nullptr, nullptr, new_k, new_v, nullptr, cur, rows, (int)heads, max_seq, (int)head_dim,
       dst_k, dst_v);
   return launch_status("fq_kv_append");
@@ -446,7 +454,7 @@ int fq_kv_gather_append(const float* src_k, const float* src_v, const float* new
   FQ_CHECK_ARG(src_k != dst_k && src_v != dst_v, FQ_ERR_ALIASING,
                "ping-pong gather must not read and write the same slot");
   int64_t n = rows * heads * (cur + 1) * head_dim;
-  kv_kernel<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(
+  launch_kernel(kv_kernel, grid_for(n, 256), 256, 0, as_stream(stream), 1u, 
       src_k, src_v, new_k, new_v, parents, cur, rows, (int)heads, max_seq, (int)head_dim, dst_k,
       dst_v);
   return launch_status("fq_kv_gather_append");

@@ -33,6 +33,7 @@ struct GemmArgs {
 template <int BM, int BN, int BK, int TM, int TN>
 __global__ void __launch_bounds__((BM / TM) * (BN / TN))
     sgemm_kernel(const GemmArgs p) {
+  pdl_enter();
   constexpr int NT = (BM / TM) * (BN / TN);
   __shared__ float As[2][BK][BM + 4];
   __shared__ float Bs[2][BK][BN + 4];
@@ -148,13 +149,13 @@ int launch_sgemm(const GemmArgs& p, int64_t nbatch, cudaStream_t s) {
   int64_t big_tiles = ((p.M + 127) / 128) * ((p.N + 127) / 128) * nbatch;
   if (big_tiles >= 2 * 148) {
     dim3 grid((unsigned)((p.N + 127) / 128), (unsigned)((p.M + 127) / 128), (unsigned)nbatch);
-    sgemm_kernel<128, 128, 8, 8, 8><<<grid, 256, 0, s>>>(p);
+    launch_kernel(sgemm_kernel<128, 128, 8, 8, 8>, grid, 256, 0, s, 1u, p);
   } else if (p.M <= 16 || p.N <= 16) {
     dim3 grid((unsigned)((p.N + 31) / 32), (unsigned)((p.M + 31) / 32), (unsigned)nbatch);
-    sgemm_kernel<32, 32, 16, 2, 2><<<grid, 256, 0, s>>>(p);
+    launch_kernel(sgemm_kernel<32, 32, 16, 2, 2>, grid, 256, 0, s, 1u, p);
   } else {
     dim3 grid((unsigned)((p.N + 63) / 64), (unsigned)((p.M + 63) / 64), (unsigned)nbatch);
-    sgemm_kernel<64, 64, 16, 4, 4><<<grid, 256, 0, s>>>(p);
+    launch_kernel(sgemm_kernel<64, 64, 16, 4, 4>, grid, 256, 0, s, 1u, p);
   }
   return launch_status("fq_gemm(simt)");
 }

@@ -243,6 +243,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   else __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = tmem_base_sh;
+  pdl_enter();  // prologue above overlapped the previous kernel's tail
 
   if (warp == 0) {
     if (lane == 0) {  // ---- TMA producer ----
@@ -473,6 +474,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = tmem_base_sh;
+  pdl_enter();  // prologue above overlapped the previous kernel's tail
 
   if (warp == 0) {
     if (lane == 0) {  // ---- TMA producer: this CTA's K slice ----
@@ -657,20 +659,9 @@ static int launch(const void* a, int64_t lda, const void* b, int64_t ldb, const 
   const int64_t groups = ((M + BM - 1) / BM / cm) * ((N + BN - 1) / BN / cn);
   const int64_t max_clusters = num_sms() / csize;
   const int64_t clusters = groups < max_clusters ? groups : max_clusters;
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3((unsigned)(clusters * csize));
-  cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = smem_bytes<BN, STAGES>();
-  cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = csize;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, tc_gemm_kernel<BN, STAGES>, ma, mb, ep, (int)M, (int)N,
-                                     (int)K, cm, cn);
+  cudaError_t e = launch_kernel(tc_gemm_kernel<BN, STAGES>, dim3((unsigned)(clusters * csize)),
+                                dim3(kThreads), smem_bytes<BN, STAGES>(), s, (unsigned)csize, ma,
+                                mb, ep, (int)M, (int)N, (int)K, cm, cn);
   if (e != cudaSuccess) {
     set_error("fq_gemm(tcgen05): launch failed: %s", cudaGetErrorString(e));
     return FQ_ERR_CUDA;
@@ -688,20 +679,9 @@ static int launch_splitk(const void* a, int64_t lda, const void* b, int64_t ldb,
   const int64_t tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
   const int nkb = (int)((K + BK - 1) / BK);
   const int kbs = (nkb + S - 1) / S;
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3((unsigned)(tiles * S));
-  cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = smem_bytes_splitk<BN, STAGES>();
-  cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = S;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, tc_gemm_splitk_kernel<BN, STAGES>, ma, mb, ep, (int)M,
-                                     (int)N, (int)K, kbs);
+  cudaError_t e = launch_kernel(tc_gemm_splitk_kernel<BN, STAGES>, dim3((unsigned)(tiles * S)),
+                                dim3(kThreads), smem_bytes_splitk<BN, STAGES>(), s, (unsigned)S,
+                                ma, mb, ep, (int)M, (int)N, (int)K, kbs);
   if (e != cudaSuccess) {
     set_error("fq_gemm(tcgen05 split-K): launch failed: %s", cudaGetErrorString(e));
     return FQ_ERR_CUDA;

@@ -56,6 +56,7 @@ __global__ void __launch_bounds__(kRetrieveThreads, 4) retrieve_kernel(
     const int32_t* __restrict__ d_k, float* __restrict__ group_max, int64_t gm_ld,
     float* __restrict__ threshold, double* __restrict__ lse, int32_t* __restrict__ cand_idx,
     int64_t cand_ld, int64_t* __restrict__ cand_count) {
+  pdl_enter();
   __shared__ float part_max[kRetrieveThreads * 4];
   __shared__ int32_t s_idx[kCandCap];
   __shared__ float gmax_s[32];
@@ -245,6 +246,7 @@ __global__ void __launch_bounds__(kSelThreads) hars_select_kernel(
     const int64_t* __restrict__ cand_count, fq_beam_state st, int K, int max_len, int eos,
     const double* __restrict__ len_pow, const int32_t* __restrict__ d_cur, int64_t max_steps, int64_t* row_tokens,
     int64_t* row_parents, int32_t* hist) {
+  pdl_enter();
   extern __shared__ int32_t sh[];  // old prefixes [K][max_len] then old hist [K][max_len]
   __shared__ Cand cands[kSelCap];
   __shared__ Cand picks[2 * kMaxBeam];
@@ -449,6 +451,7 @@ __global__ void __launch_bounds__(kSelThreads) hars_select_kernel(
 
 __global__ void hars_groups_kernel(fq_beam_state st, int batch, int K, int V, int exhaustive,
                                    int32_t* d_k) {
+  pdl_enter();
   int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= batch * K) return;
   int b = r / K, i = r % K;
@@ -458,6 +461,7 @@ __global__ void hars_groups_kernel(fq_beam_state st, int batch, int K, int V, in
 }
 
 __global__ void beam_state_init_kernel(fq_beam_state st, int batch, int K, int max_len) {
+  pdl_enter();
   int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= batch) return;
   st.live[b] = 1;  // BeamState(): prefixes [[]], cum [0.0], parents [0]
@@ -474,7 +478,8 @@ __global__ void beam_state_init_kernel(fq_beam_state st, int batch, int K, int m
   if (b == 0) *st.n_done = 0;
 }
 
-__global__ void step_advance_kernel(int32_t* d_cur) { *d_cur += 1; }
+__global__ void step_advance_kernel(int32_t* d_cur) {
+  pdl_enter(); *d_cur += 1; }
 
 }  // namespace fq
 
@@ -494,7 +499,7 @@ int fq_retrieve(const float* logits, int64_t ld, int64_t rows, int64_t vocab, in
   FQ_CHECK_ARG(!group_max || gm_ld >= (d_k ? vocab : k) || gm_ld >= k, FQ_ERR_DIMENSION,
                "group_max leading dim too small");
   if (rows == 0) return FQ_OK;
-  retrieve_kernel<<<(unsigned)rows, kRetrieveThreads, 0, as_stream(stream)>>>(
+  launch_kernel(retrieve_kernel, (unsigned)rows, kRetrieveThreads, 0, as_stream(stream), 1u, 
       logits, ld, (int)vocab, (int)k, d_k, group_max, gm_ld, threshold, lse, cand_idx, cand_ld,
       cand_count);
   return launch_status("fq_retrieve");
@@ -516,7 +521,7 @@ int fq_hars_select(const float* logits, int64_t ld, const double* lse, const int
   FQ_CHECK_ARG(eos >= 0 && eos < vocab, FQ_ERR_PARAMETER, "eos token outside vocabulary");
   size_t smem = (size_t)2 * beam * max_len * sizeof(int32_t);
   FQ_CHECK_ARG(smem <= 160 * 1024, FQ_ERR_CAPACITY, "fq_hars_select: max_len too large");
-  hars_select_kernel<<<(unsigned)batch, kSelThreads, smem, as_stream(stream)>>>(
+  launch_kernel(hars_select_kernel, (unsigned)batch, kSelThreads, smem, as_stream(stream), 1u, 
       logits, ld, lse, cand_idx, cand_ld, cand_count, st, (int)beam, (int)max_len, (int)eos,
       len_pow, d_cur, max_steps, row_tokens, row_parents, hist);
   return launch_status("fq_hars_select");
@@ -526,7 +531,7 @@ int fq_hars_groups(fq_beam_state st, int64_t batch, int64_t beam, int64_t vocab,
                    int32_t* d_k, fq_stream_t stream) {
   FQ_CHECK_ARG(d_k && batch > 0 && beam > 0, FQ_ERR_DIMENSION, "fq_hars_groups: bad args");
   int64_t n = batch * beam;
-  hars_groups_kernel<<<(unsigned)((n + 255) / 256), 256, 0, as_stream(stream)>>>(
+  launch_kernel(hars_groups_kernel, (unsigned)((n + 255) / 256), 256, 0, as_stream(stream), 1u, 
       st, (int)batch, (int)beam, (int)vocab, exhaustive, d_k);
   return launch_status("fq_hars_groups");
 }
@@ -536,7 +541,7 @@ int fq_beam_state_init(fq_beam_state st, int64_t batch, int64_t beam, int64_t ma
   FQ_CHECK_ARG(batch > 0 && beam > 0 && beam <= kMaxBeam, FQ_ERR_DIMENSION,
                "fq_beam_state_init: bad args");
   (void)max_len;
-  beam_state_init_kernel<<<(unsigned)((batch + 127) / 128), 128, 0, as_stream(stream)>>>(
+  launch_kernel(beam_state_init_kernel, (unsigned)((batch + 127) / 128), 128, 0, as_stream(stream), 1u, 
       st, (int)batch, (int)beam, (int)max_len);
   return launch_status("fq_beam_state_init");
 }
@@ -552,7 +557,7 @@ int fq_hars_prepare(void) {
 
 int fq_step_advance(int32_t* d_cur, fq_stream_t stream) {
   FQ_CHECK_ARG(d_cur, FQ_ERR_DIMENSION, "fq_step_advance: null counter");
-  step_advance_kernel<<<1, 1, 0, as_stream(stream)>>>(d_cur);
+  launch_kernel(step_advance_kernel, 1, 1, 0, as_stream(stream), 1u, d_cur);
   return launch_status("fq_step_advance");
 }
 
