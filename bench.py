@@ -207,7 +207,7 @@ def run_ours(args, rank, world):
     import torch
 
     import paper_2010_13887_b200 as P
-    from paper_2010_13887_b200 import _abi, decode as D
+    from paper_2010_13887_b200 import _abi, decode as D, replicas
 
     dev = torch.device("cuda", torch.cuda.current_device())
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
@@ -256,12 +256,7 @@ def run_ours(args, rank, world):
     sec = sum(step_times) / len(step_times)
     hyps_state = st.host_items()
     tokens = sum(len(s_.finalize(dc)[0][0]) if s_.finalize(dc) else 0 for s_ in hyps_state)
-    t_max = torch.tensor([sec], dtype=torch.float64, device=dev)
-    tok_sum = torch.tensor([float(tokens)], dtype=torch.float64, device=dev)
-    if world > 1:
-        torch.distributed.all_reduce(t_max, op=torch.distributed.ReduceOp.MAX)
-        torch.distributed.all_reduce(tok_sum)
-    sec_max, tok_total = float(t_max.item()), float(tok_sum.item())
+    sec_max, tok_total = replicas.reduce_step_stats(sec, float(tokens), dev)
     value = tok_total / sec_max
 
     # -- end to end through the public API: host tokens in, host hypotheses out --
@@ -277,10 +272,8 @@ def run_ours(args, rank, world):
         dt = time.perf_counter() - t0
         if i:
             e2e_times.append(dt)
-    e2e_sec = torch.tensor([sum(e2e_times) / len(e2e_times)], dtype=torch.float64, device=dev)
-    if world > 1:
-        torch.distributed.all_reduce(e2e_sec, op=torch.distributed.ReduceOp.MAX)
-    e2e_value = tok_total / float(e2e_sec.item())
+    e2e_sec, _ = replicas.reduce_step_stats(sum(e2e_times) / len(e2e_times), 0.0, dev)
+    e2e_value = tok_total / e2e_sec
 
     out = None
     if rank == 0:
