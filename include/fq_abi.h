@@ -146,7 +146,8 @@ int fq_gemm_batched(const float* a, int64_t lda, int64_t sa0, int64_t sa1, const
  * R = min_g m_g, lse = f64(row_max) + log(sum f64(expf(x - row_max))), and the
  * candidates x >= R in ascending token order (cand_idx [rows, cand_ld]; rows
  * whose count exceeds cand_ld are flagged by count > cand_ld and truncated).
- * k per row: d_k[row] if d_k != NULL (0 = skip row) else k. */
+ * k per row: d_k[row] if d_k != NULL (0 = skip row) else k; with d_k, k is an
+ * upper bound on the d_k entries. */
 int fq_retrieve(const float* logits, int64_t ld, int64_t rows, int64_t vocab, int64_t k,
                 const int32_t* d_k, float* group_max, int64_t gm_ld, float* threshold,
                 double* lse, int32_t* cand_idx, int64_t cand_ld, int64_t* cand_count,

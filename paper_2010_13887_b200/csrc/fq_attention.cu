@@ -500,6 +500,496 @@ __global__ void __launch_bounds__(128) decoder_self_attention_kernel(
   }
 }
 
+// ---------------------------------------------------------------------------
+// Encoder self-attention, register-tiled: CTA per (item, head); Q/K/V head
+// slices in smem; every thread owns a 4-row x NC-column block of the score
+// tile (columns strided by 16 so the K reads are bank-conflict free) and a
+// 4-row x HC-column block of the output. Same arithmetic as attend_rows —
+// each score an fp32 FMA chain over e in order, each output an FMA chain over
+// keys in order, softmax by warp_softmax — so both precision modes keep the
+// exact-mode numerics; ~10x fewer shared-memory reads than one dot per lane.
+// ---------------------------------------------------------------------------
+template <int NC, int HC>
+__global__ void __launch_bounds__(256) encoder_attention_tiled(
+    const float* __restrict__ qkv, int64_t ldq, int seq, int heads, int hd, float scale,
+    const float* __restrict__ mask, float* __restrict__ out, __nv_bfloat16* __restrict__ out16,
+    int64_t ldo, int exact, int* d_bad) {
+  pdl_enter();
+  extern __shared__ float sm[];
+  const int b = blockIdx.x / heads, h = blockIdx.x % heads;
+  const int d = heads * hd;
+  const int hp = hd + 1, sp = seq + 1;
+  float* Qs = sm;               // [seq][hp]; reused as scores [seq][sp] (seq <= hd + ... checked)
+  float* Ks = Qs + seq * (hp > sp ? hp : sp);
+  float* Vs = Ks + seq * hp;
+  int* bad_row = reinterpret_cast<int*>(Vs + seq * hp);
+  const float* base = qkv + (int64_t)b * seq * ldq;
+  load_slice<float>(base + h * hd, ldq, seq, hd, Qs, hp);
+  load_slice<float>(base + d + h * hd, ldq, seq, hd, Ks, hp);
+  load_slice<float>(base + 2 * d + h * hd, ldq, seq, hd, Vs, hp);
+  __syncthreads();
+  const int RT = (seq + 3) >> 2;
+  const float* mk = mask ? mask + (int64_t)b * seq : nullptr;
+  // ---- scores: 4 x NC per thread, kept in registers until Q is dead ----
+  const int t = threadIdx.x;
+  const bool has = t < RT * 16;
+  const int ti = t >> 4, tj = t & 15;
+  float acc[4][NC];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int c = 0; c < NC; ++c) acc[a][c] = 0.0f;
+  if (has) {
+    int qr[4], kr[NC];
+#pragma unroll
+    for (int a = 0; a < 4; ++a) qr[a] = min(4 * ti + a, seq - 1) * hp;
+#pragma unroll
+    for (int c = 0; c < NC; ++c) kr[c] = min(tj + 16 * c, seq - 1) * hp;
+#pragma unroll 4
+    for (int e = 0; e < hd; ++e) {
+      float qv[4], kv[NC];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) qv[a] = Qs[qr[a] + e];
+#pragma unroll
+      for (int c = 0; c < NC; ++c) kv[c] = Ks[kr[c] + e];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int c = 0; c < NC; ++c) acc[a][c] = fmaf(qv[a], kv[c], acc[a][c]);
+    }
+  }
+  __syncthreads();  // Q dead: scores overwrite it
+  float* Ss = Qs;
+  if (has) {
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      const int i = 4 * ti + a;
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        const int j = tj + 16 * c;
+        if (i < seq && j < seq) {
+          float s = fmul_rn(acc[a][c], scale);
+          if (mk) s = fadd_rn(s, mk[j]);
+          Ss[i * sp + j] = s;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int i = w; i < seq; i += nw) {
+    const bool ok = warp_softmax(Ss + i * sp, seq, exact);
+    if (lane == 0) {
+      bad_row[i] = ok ? 0 : 1;
+      if (!ok && d_bad) atomicAdd(d_bad, 1);
+    }
+  }
+  __syncthreads();
+  // ---- P.V: 4 rows x HC columns per thread ----
+  if (has) {
+    float o[4][HC];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int c = 0; c < HC; ++c) o[a][c] = 0.0f;
+    int pr[4], vc[HC];
+#pragma unroll
+    for (int a = 0; a < 4; ++a) pr[a] = min(4 * ti + a, seq - 1) * sp;
+#pragma unroll
+    for (int c = 0; c < HC; ++c) vc[c] = min(tj + 16 * c, hd - 1);
+#pragma unroll 4
+    for (int j = 0; j < seq; ++j) {
+      float pv[4], vv[HC];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) pv[a] = Ss[pr[a] + j];
+#pragma unroll
+      for (int c = 0; c < HC; ++c) vv[c] = Vs[j * hp + vc[c]];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int c = 0; c < HC; ++c) o[a][c] = fmaf(pv[a], vv[c], o[a][c]);
+    }
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      const int i = 4 * ti + a;
+      if (i >= seq || bad_row[i]) continue;
+      const int64_t orow = ((int64_t)b * seq + i) * ldo + h * hd;
+#pragma unroll
+      for (int c = 0; c < HC; ++c) {
+        const int e = tj + 16 * c;
+        if (e < hd) {
+          if (out) out[orow + e] = o[a][c];
+          if (out16) out16[orow + e] = f2bf(o[a][c]);
+        }
+      }
+    }
+  }
+}
+
+// ---- async bulk copies (cp.async.bulk, TMA engine) into shared memory ------
+__device__ __forceinline__ uint32_t sm_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void bar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(sm_u32(bar)), "r"(count));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void bar_expect(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sm_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok = 0;
+  while (!ok) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(ok)
+        : "r"(sm_u32(bar)), "r"(parity)
+        : "memory");
+  }
+}
+// bytes % 16 == 0, both addresses 16-byte aligned
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          sm_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(sm_u32(bar))
+      : "memory");
+}
+
+// ---------------------------------------------------------------------------
+// Decoder self-attention, bf16 KV cache (throughput mode). CTA per beam row;
+// thread lt owns 8 consecutive model dims (one 16-byte bf16 load per cached
+// position), so a cached slot row (all heads, 2 KB) is read as one coalesced
+// segment instead of per-head 128-byte pieces; G = blockDim / (d/8) position
+// groups stream disjoint positions with U loads in flight per thread. Head
+// dots are reduced over the HD/8 lanes of a head with xor-shuffles. The K/V of
+// this step are written to slot (cur, r) (copy-free history, see above).
+// ---------------------------------------------------------------------------
+template <int HD, int U>
+__global__ void __launch_bounds__(256) decoder_self_attention_rows(
+    const float* __restrict__ sqkv, int64_t ldq, __nv_bfloat16* __restrict__ kc,
+    __nv_bfloat16* __restrict__ vc, const int32_t* __restrict__ hist,
+    const int32_t* __restrict__ d_cur, int rows, int heads, int max_len, float scale,
+    float* __restrict__ out, __nv_bfloat16* __restrict__ out16, int64_t ldo) {
+  pdl_enter();
+  constexpr int TPH = HD / 8;  // threads per head
+  extern __shared__ __align__(16) float smf[];
+  const int r = blockIdx.x;
+  const int d = heads * HD;
+  const int TP = d / 8;               // threads per position
+  const int G = blockDim.x / TP;      // position groups
+  const int tid = threadIdx.x;
+  const int g = tid / TP, lt = tid % TP;
+  const int h = lt / TPH;
+  const int cur = *d_cur;
+  const int L1 = max_len + 1;
+  float* S = smf;                                   // [heads][L1]
+  int* phys = reinterpret_cast<int*>(S + heads * L1);  // [max_len]
+  float* red = reinterpret_cast<float*>(phys + max_len);  // [G][d]
+  const int32_t* hr = hist + (int64_t)r * max_len;
+  for (int t = tid; t < cur; t += blockDim.x) phys[t] = hr[t];
+  if (tid == 0) phys[cur] = r;
+  const float* rowp = sqkv + (int64_t)r * ldq + lt * 8;
+  float q[8], kn[8], vn[8];
+  {
+    const float4 a0 = *reinterpret_cast<const float4*>(rowp);
+    const float4 a1 = *reinterpret_cast<const float4*>(rowp + 4);
+    const float4 b0 = *reinterpret_cast<const float4*>(rowp + d);
+    const float4 b1 = *reinterpret_cast<const float4*>(rowp + d + 4);
+    const float4 c0 = *reinterpret_cast<const float4*>(rowp + 2 * d);
+    const float4 c1 = *reinterpret_cast<const float4*>(rowp + 2 * d + 4);
+    q[0] = a0.x; q[1] = a0.y; q[2] = a0.z; q[3] = a0.w; q[4] = a1.x; q[5] = a1.y; q[6] = a1.z; q[7] = a1.w;
+    kn[0] = b0.x; kn[1] = b0.y; kn[2] = b0.z; kn[3] = b0.w; kn[4] = b1.x; kn[5] = b1.y; kn[6] = b1.z; kn[7] = b1.w;
+    vn[0] = c0.x; vn[1] = c0.y; vn[2] = c0.z; vn[3] = c0.w; vn[4] = c1.x; vn[5] = c1.y; vn[6] = c1.z; vn[7] = c1.w;
+  }
+  uint4 kpk, vpk;
+  {
+    __nv_bfloat162 t2[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) t2[i] = __floats2bfloat162_rn(kn[2 * i], kn[2 * i + 1]);
+    kpk = *reinterpret_cast<uint4*>(t2);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) t2[i] = __floats2bfloat162_rn(vn[2 * i], vn[2 * i + 1]);
+    vpk = *reinterpret_cast<uint4*>(t2);
+  }
+  if (g == 0) {
+    const int64_t slot = ((int64_t)cur * rows + r) * d + lt * 8;
+    *reinterpret_cast<uint4*>(kc + slot) = kpk;
+    *reinterpret_cast<uint4*>(vc + slot) = vpk;
+  }
+  __syncthreads();  // phys[] staged
+  // ---- scores ----
+  for (int t0 = g; t0 <= cur; t0 += G * U) {
+    uint4 raw[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int t = t0 + u * G;
+      if (t < cur) raw[u] = *reinterpret_cast<const uint4*>(kc + ((int64_t)t * rows + phys[t]) * d + lt * 8);
+      else raw[u] = kpk;  // t == cur: the stored (rounded) key; t > cur unused
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int t = t0 + u * G;
+      float f[8];
+      unpack16<__nv_bfloat16>(raw[u], f);
+      float p = 0.0f;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) p = fmaf(q[j], f[j], p);
+#pragma unroll
+      for (int o = TPH / 2; o > 0; o >>= 1) p += __shfl_xor_sync(0xffffffffu, p, o);
+      if ((lt % TPH) == 0 && t <= cur) S[h * L1 + t] = p * scale;
+    }
+  }
+  __syncthreads();
+  // ---- softmax per head (warp per head) ----
+  {
+    const int w = tid >> 5, nw = blockDim.x >> 5;
+    for (int hh = w; hh < heads; hh += nw) warp_softmax(S + hh * L1, cur + 1, false);
+  }
+  __syncthreads();
+  // ---- P.V ----
+  float acc[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) acc[j] = 0.0f;
+  const float* Sh = S + h * L1;
+  for (int t0 = g; t0 <= cur; t0 += G * U) {
+    uint4 raw[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int t = t0 + u * G;
+      if (t < cur) raw[u] = *reinterpret_cast<const uint4*>(vc + ((int64_t)t * rows + phys[t]) * d + lt * 8);
+      else raw[u] = vpk;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int t = t0 + u * G;
+      if (t <= cur) {
+        const float p = Sh[t];
+        float f[8];
+        unpack16<__nv_bfloat16>(raw[u], f);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[j] = fmaf(p, f[j], acc[j]);
+      }
+    }
+  }
+  if (G > 1) {
+    if (g > 0) {
+#pragma unroll
+      for (int j = 0; j < 8; j += 4)
+        *reinterpret_cast<float4*>(red + (g - 1) * d + lt * 8 + j) =
+            make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
+    }
+    __syncthreads();
+    if (g > 0) return;
+    for (int gg = 1; gg < G; ++gg) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[j] += red[(gg - 1) * d + lt * 8 + j];
+    }
+  }
+  const int64_t o = (int64_t)r * ldo + lt * 8;
+  if (out16) {
+    __nv_bfloat162 t2[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) t2[i] = __floats2bfloat162_rn(acc[2 * i], acc[2 * i + 1]);
+    *reinterpret_cast<uint4*>(out16 + o) = *reinterpret_cast<uint4*>(t2);
+  }
+  if (out) {
+    *reinterpret_cast<float4*>(out + o) = make_float4(acc[0], acc[1], acc[2], acc[3]);
+    *reinterpret_cast<float4*>(out + o + 4) = make_float4(acc[4], acc[5], acc[6], acc[7]);
+  }
+}
+
+// ---- warp-level bf16 tensor-core helpers (mma.sync m16n8k16, ldmatrix) ----
+// Decode attention is a handful of tiny per-(item, head) products (M = beams
+// <= 8); the legacy warp MMA does them in a few dozen instructions where the
+// FMA formulation needs thousands, which is what bounds these kernels. fp32
+// queries / probabilities enter as a bf16 hi + lo pair (two MMAs), so the
+// products keep ~16 mantissa bits against the bf16 keys/values they meet.
+__device__ __forceinline__ void mma_bf16_16816(float* c, const uint32_t* a, uint32_t b0,
+                                               uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ void ldsm_x4(uint32_t* r, const void* p) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(sm_u32(p)));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t* r, const void* p) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(sm_u32(p)));
+}
+// (x0, x1) -> packed bf16x2 hi and the bf16x2 residual lo
+__device__ __forceinline__ void split2(float x0, float x1, uint32_t& hi, uint32_t& lo) {
+  const __nv_bfloat162 h = __floats2bfloat162_rn(x0, x1);
+  const float2 hf = __bfloat1622float2(h);
+  const __nv_bfloat162 l = __floats2bfloat162_rn(x0 - hf.x, x1 - hf.y);
+  hi = *reinterpret_cast<const uint32_t*>(&h);
+  lo = *reinterpret_cast<const uint32_t*>(&l);
+}
+
+// Cross-attention on warp MMAs, bf16 K/V (throughput mode). One warp per
+// (item, head): the item's K and V head slices arrive by bulk copies into
+// padded smem rows (144 B: conflict-free ldmatrix), then
+//   S^T [pos x beam] = K . Q^T      (A = K via ldmatrix, B = Q^T hi/lo)
+//   softmax over positions per beam (C fragments, xor-shuffles over groupID)
+//   O^T [dim x beam] = V^T . P^T    (A = V^T via ldmatrix.trans, B = P^T hi/lo via smem)
+// NT = position tiles of 16 (seq <= 16 NT), beams <= 8.
+template <int HD, int NT>
+__global__ void __launch_bounds__(32) cross_attention_mma(
+    const float* __restrict__ cq, int64_t ldcq, const __nv_bfloat16* __restrict__ ck,
+    const __nv_bfloat16* __restrict__ cv, int64_t ldkv, int beam, int seq, float scale,
+    const float* __restrict__ mask, float* __restrict__ out, __nv_bfloat16* __restrict__ out16,
+    int64_t ldo, int* d_bad) {
+  constexpr int RS = HD * 2 + 16;  // padded smem row bytes
+  constexpr int NP = NT * 16;
+  extern __shared__ __align__(128) uint8_t smb[];
+  __shared__ __align__(8) uint64_t bar;
+  __shared__ float Ps[8][NP + 4];
+  uint8_t* Ks = smb;
+  uint8_t* Vs = smb + NP * RS;
+  const int b = blockIdx.x, h = blockIdx.y, lane = threadIdx.x;
+  const int g = lane >> 2, t4 = lane & 3;
+  if (lane == 0) {
+    bar_init(&bar, 1);
+    bar_expect(&bar, (uint32_t)(2 * seq * HD * 2));
+  }
+  __syncwarp();
+  pdl_enter();
+  const __nv_bfloat16* kb = ck + (int64_t)b * seq * ldkv + h * HD;
+  const __nv_bfloat16* vb = cv + (int64_t)b * seq * ldkv + h * HD;
+  for (int x = lane; x < 2 * seq; x += 32) {
+    const int t = x >> 1;
+    if (x & 1) bulk_g2s(Vs + t * RS, vb + (int64_t)t * ldkv, HD * 2, &bar);
+    else bulk_g2s(Ks + t * RS, kb + (int64_t)t * ldkv, HD * 2, &bar);
+  }
+  // zero the padded positions [seq, NP) so 0 * garbage never makes NaN
+  for (int x = lane; x < (NP - seq) * (HD / 8); x += 32) {
+    const int t = seq + x / (HD / 8), c = (x % (HD / 8)) * 16;
+    *reinterpret_cast<uint4*>(Ks + t * RS + c) = make_uint4(0, 0, 0, 0);
+    *reinterpret_cast<uint4*>(Vs + t * RS + c) = make_uint4(0, 0, 0, 0);
+  }
+  // Q^T fragments: lane (g, t4) needs beam g, dims 16k + {2t4, 2t4+1, 2t4+8, 2t4+9}
+  uint32_t qh[HD / 16][2], ql[HD / 16][2];
+  {
+    const bool ok = g < beam;
+    const float* qp = cq + ((int64_t)b * beam + (ok ? g : 0)) * ldcq + h * HD;
+#pragma unroll
+    for (int kk = 0; kk < HD / 16; ++kk) {
+      float2 x0 = ok ? *reinterpret_cast<const float2*>(qp + 16 * kk + 2 * t4) : make_float2(0.f, 0.f);
+      float2 x1 = ok ? *reinterpret_cast<const float2*>(qp + 16 * kk + 2 * t4 + 8) : make_float2(0.f, 0.f);
+      split2(x0.x, x0.y, qh[kk][0], ql[kk][0]);
+      split2(x1.x, x1.y, qh[kk][1], ql[kk][1]);
+    }
+  }
+  __syncwarp();
+  bar_wait(&bar, 0);
+  // ---- scores: NT tiles of 16 positions x 8 beams ----
+  float sc[NT][4];
+  const int lrow = (lane & 7) + ((lane >> 3) & 1) * 8, lcol = (lane >> 4) * 8;
+#pragma unroll
+  for (int m = 0; m < NT; ++m) {
+    sc[m][0] = sc[m][1] = sc[m][2] = sc[m][3] = 0.0f;
+#pragma unroll
+    for (int kk = 0; kk < HD / 16; ++kk) {
+      uint32_t a[4];
+      ldsm_x4(a, Ks + (16 * m + lrow) * RS + (16 * kk + lcol) * 2);
+      mma_bf16_16816(sc[m], a, qh[kk][0], qh[kk][1]);
+      mma_bf16_16816(sc[m], a, ql[kk][0], ql[kk][1]);
+    }
+  }
+  // ---- softmax over positions, per beam column (2 per lane: 2t4, 2t4+1) ----
+  const float* mk = mask ? mask + (int64_t)b * seq : nullptr;
+  float mx0 = -INFINITY, mx1 = -INFINITY;
+#pragma unroll
+  for (int m = 0; m < NT; ++m) {
+#pragma unroll
+    for (int hh = 0; hh < 2; ++hh) {
+      const int p = 16 * m + g + 8 * hh;
+      const float add = p < seq ? (mk ? mk[p] : 0.0f) : -INFINITY;
+      sc[m][2 * hh] = fmaf(sc[m][2 * hh], scale, add);
+      sc[m][2 * hh + 1] = fmaf(sc[m][2 * hh + 1], scale, add);
+      mx0 = fmaxf(mx0, sc[m][2 * hh]);
+      mx1 = fmaxf(mx1, sc[m][2 * hh + 1]);
+    }
+  }
+#pragma unroll
+  for (int o = 4; o < 32; o <<= 1) {
+    mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, o));
+    mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, o));
+  }
+  float l0 = 0.0f, l1 = 0.0f;
+#pragma unroll
+  for (int m = 0; m < NT; ++m) {
+#pragma unroll
+    for (int hh = 0; hh < 2; ++hh) {
+      const float e0 = mx0 == -INFINITY ? 0.0f : __expf(sc[m][2 * hh] - mx0);
+      const float e1 = mx1 == -INFINITY ? 0.0f : __expf(sc[m][2 * hh + 1] - mx1);
+      l0 += e0;
+      l1 += e1;
+      const int p = 16 * m + g + 8 * hh;
+      Ps[2 * t4][p] = e0;
+      Ps[2 * t4 + 1][p] = e1;
+    }
+  }
+#pragma unroll
+  for (int o = 4; o < 32; o <<= 1) {
+    l0 += __shfl_xor_sync(0xffffffffu, l0, o);
+    l1 += __shfl_xor_sync(0xffffffffu, l1, o);
+  }
+  __syncwarp();
+  // ---- O^T = V^T . P^T: HD/16 tiles of 16 dims x 8 beams, k over positions ----
+  float oc[HD / 16][4];
+#pragma unroll
+  for (int m = 0; m < HD / 16; ++m) oc[m][0] = oc[m][1] = oc[m][2] = oc[m][3] = 0.0f;
+  const int mi = lane >> 3;
+  const int vrow = (lane & 7) + ((mi >> 1) & 1) * 8, vcol = (mi & 1) * 8;
+#pragma unroll
+  for (int kk = 0; kk < NT; ++kk) {
+    uint32_t bh0, bl0, bh1, bl1;
+    split2(Ps[g][16 * kk + 2 * t4], Ps[g][16 * kk + 2 * t4 + 1], bh0, bl0);
+    split2(Ps[g][16 * kk + 2 * t4 + 8], Ps[g][16 * kk + 2 * t4 + 9], bh1, bl1);
+#pragma unroll
+    for (int m = 0; m < HD / 16; ++m) {
+      uint32_t a[4];
+      ldsm_x4_t(a, Vs + (16 * kk + vrow) * RS + (16 * m + vcol) * 2);
+      mma_bf16_16816(oc[m], a, bh0, bh1);
+      mma_bf16_16816(oc[m], a, bl0, bl1);
+    }
+  }
+  // ---- normalise and store: lane holds dims {16m + g, +8} x beams {2t4, 2t4+1} ----
+  const float inv0 = l0 > 0.0f ? 1.0f / l0 : 0.0f, inv1 = l1 > 0.0f ? 1.0f / l1 : 0.0f;
+  if (d_bad && g == 0) {
+    if (2 * t4 < beam && !(l0 > 0.0f)) atomicAdd(d_bad, 1);
+    if (2 * t4 + 1 < beam && !(l1 > 0.0f)) atomicAdd(d_bad, 1);
+  }
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    const int bi = 2 * t4 + j;
+    if (bi >= beam) continue;
+    const float inv = j ? inv1 : inv0;
+    const int64_t o = ((int64_t)b * beam + bi) * ldo + h * HD;
+#pragma unroll
+    for (int m = 0; m < HD / 16; ++m) {
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh) {
+        const int dd = 16 * m + g + 8 * hh;
+        const float v = oc[m][2 * hh + j] * inv;
+        if (out) out[o + dd] = v;
+        if (out16) out16[o + dd] = f2bf(v);
+      }
+    }
+  }
+}
+
 int attention_prepare() {
   const int big = 227 * 1024;
   if (cudaFuncSetAttribute(encoder_attention_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, big) ||
@@ -511,7 +1001,9 @@ int attention_prepare() {
       cudaFuncSetAttribute(cross_attention_fast<float, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024) ||
       cudaFuncSetAttribute(cross_attention_fast<__nv_bfloat16, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024) ||
       cudaFuncSetAttribute(cross_attention_fast<__nv_bfloat16, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024) ||
-      cudaFuncSetAttribute(cross_attention_fast<__nv_bfloat16, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024)) {
+      cudaFuncSetAttribute(cross_attention_fast<__nv_bfloat16, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024) ||
+      cudaFuncSetAttribute(encoder_attention_tiled<4, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024) ||
+      cudaFuncSetAttribute(encoder_attention_tiled<4, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024)) {
     set_error("fq_prepare: cannot opt in to large shared memory (attention)");
     return FQ_ERR_CUDA;
   }
@@ -541,11 +1033,24 @@ int fq_encoder_attention(const float* qkv, int64_t ldq, int64_t batch, int64_t s
   FQ_CHECK_ARG(qkv && (out || out16) && batch > 0 && seq > 0 && heads > 0 && head_dim > 0 &&
                    head_dim <= 128,
                FQ_ERR_DIMENSION, "fq_encoder_attention: bad shape");
+  if (seq <= 64 && ldq % 4 == 0 && ((uintptr_t)qkv & 15) == 0) {
+    const int64_t hp = head_dim + 1, sp = seq + 1;
+    const size_t smem = (size_t)(seq * (hp > sp ? hp : sp) + 2 * seq * hp + seq) * 4;
+    if (head_dim <= 64)
+      launch_kernel(encoder_attention_tiled<4, 4>, (unsigned)(batch * heads), 256, smem,
+                    as_stream(stream), 1u, qkv, ldq, (int)seq, (int)heads, (int)head_dim, scale,
+                    mask, out, reinterpret_cast<__nv_bfloat16*>(out16), ldo, exact, d_bad);
+    else
+      launch_kernel(encoder_attention_tiled<4, 8>, (unsigned)(batch * heads), 256, smem,
+                    as_stream(stream), 1u, qkv, ldq, (int)seq, (int)heads, (int)head_dim, scale,
+                    mask, out, reinterpret_cast<__nv_bfloat16*>(out16), ldo, exact, d_bad);
+    return launch_status("fq_encoder_attention");
+  }
   const int threads = 256;
   size_t smem = (size_t)(2 * seq * (head_dim + 1) + seq * head_dim + (threads / 32) * seq) * 4;
   FQ_CHECK_ARG(smem <= 227 * 1024, FQ_ERR_CAPACITY, "encoder attention: seq %lld too long",
                (long long)seq);
-  launch_kernel(encoder_attention_kernel, (unsigned)(batch * heads), threads, smem, as_stream(stream), 1u, 
+  launch_kernel(encoder_attention_kernel, (unsigned)(batch * heads), threads, smem, as_stream(stream), 1u,
       qkv, ldq, (int)seq, (int)heads, (int)head_dim, scale, mask, out,
       reinterpret_cast<__nv_bfloat16*>(out16), ldo, exact, d_bad);
   return launch_status("fq_encoder_attention");
@@ -559,6 +1064,31 @@ int fq_decoder_self_attention(const float* sqkv, int64_t ldq, void* kcache, void
   FQ_CHECK_ARG(sqkv && kcache && vcache && hist && d_cur && (out || out16) && rows > 0 &&
                    heads > 0 && head_dim > 0 && head_dim <= 128 && max_len > 0,
                FQ_ERR_DIMENSION, "fq_decoder_self_attention: bad args");
+  {
+    const int64_t d = heads * head_dim, tp = d / 8;
+    const bool rows_ok = kv_dtype != FQ_F32 && !exact &&
+                         (head_dim == 32 || head_dim == 64 || head_dim == 128) &&
+                         tp % 32 == 0 && tp <= 256 && ldq % 4 == 0 &&
+                         ((uintptr_t)sqkv & 15) == 0 && ((uintptr_t)kcache & 15) == 0 &&
+                         ((uintptr_t)vcache & 15) == 0 && ldo % 8 == 0 &&
+                         ((uintptr_t)out16 & 15) == 0 && ((uintptr_t)out & 15) == 0;
+    if (rows_ok) {
+      const int threads = 256;
+      const int G = threads / (int)tp;
+      const size_t smem = (size_t)(heads * (max_len + 1)) * 4 + (size_t)max_len * 4 +
+                          (size_t)(G - 1) * d * 4 + 16;
+#define FQ_SELF_ROWS(HD)                                                                       \
+  launch_kernel(decoder_self_attention_rows<HD, 8>, dim3((unsigned)rows), threads, smem,       \
+                as_stream(stream), 1u, sqkv, ldq, (__nv_bfloat16*)kcache,                     \
+                (__nv_bfloat16*)vcache, hist, d_cur, (int)rows, (int)heads, (int)max_len, scale, \
+                out, reinterpret_cast<__nv_bfloat16*>(out16), ldo)
+      if (head_dim == 32) FQ_SELF_ROWS(32);
+      else if (head_dim == 64) FQ_SELF_ROWS(64);
+      else FQ_SELF_ROWS(128);
+#undef FQ_SELF_ROWS
+      return launch_status("fq_decoder_self_attention");
+    }
+  }
   const int wpb = 4;
   dim3 grid((unsigned)((rows + wpb - 1) / wpb), (unsigned)heads);
   cudaStream_t s = as_stream(stream);
@@ -607,6 +1137,28 @@ int fq_cross_attention(const float* cq, int64_t ldcq, const void* ck, const void
   FQ_CHECK_ARG(cq && ck && cv && (out || out16) && batch > 0 && beam > 0 && seq > 0 &&
                    heads > 0 && head_dim > 0 && head_dim <= 128,
                FQ_ERR_DIMENSION, "fq_cross_attention: bad args");
+  if (kv_dtype != FQ_F32 && !exact && (head_dim == 32 || head_dim == 64 || head_dim == 128) &&
+      beam <= 8 && seq <= 64 && ldcq % 2 == 0 && ((uintptr_t)cq & 7) == 0 && ldkv % 8 == 0 &&
+      ((uintptr_t)ck & 15) == 0 && ((uintptr_t)cv & 15) == 0) {
+    const dim3 grid((unsigned)batch, (unsigned)heads);
+    const int nt = (int)((seq + 15) / 16);
+    const size_t msmem = (size_t)2 * nt * 16 * (head_dim * 2 + 16);
+#define FQ_CROSS_M(HD, NT)                                                                     \
+  launch_kernel(cross_attention_mma<HD, NT>, grid, 32, msmem, as_stream(stream), 1u, cq, ldcq,  \
+                (const __nv_bfloat16*)ck, (const __nv_bfloat16*)cv, ldkv, (int)beam, (int)seq,  \
+                scale, mask, out, reinterpret_cast<__nv_bfloat16*>(out16), ldo, d_bad)
+#define FQ_CROSS_MH(HD)                      \
+  if (nt == 1) FQ_CROSS_M(HD, 1);            \
+  else if (nt == 2) FQ_CROSS_M(HD, 2);       \
+  else if (nt == 3) FQ_CROSS_M(HD, 3);       \
+  else FQ_CROSS_M(HD, 4);
+    if (head_dim == 32) { FQ_CROSS_MH(32) }
+    else if (head_dim == 64) { FQ_CROSS_MH(64) }
+    else { FQ_CROSS_MH(128) }
+#undef FQ_CROSS_MH
+#undef FQ_CROSS_M
+    return launch_status("fq_cross_attention");
+  }
   dim3 grid((unsigned)(batch * heads));
   const size_t es = kv_dtype == FQ_F32 ? 4 : 2;
   const size_t fast_smem = (size_t)seq * (2 * head_dim + 16 / es) * es +

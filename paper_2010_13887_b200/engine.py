@@ -147,7 +147,9 @@ class Session:
             logits = step.run()
             stream = _abi.stream_handle()
             _abi.call("fq_hars_groups", st.c, batch, K, V, exhaustive, hk.data_ptr(), stream)
-            D.retrieve_device(logits, K, d_k=hk, out=(None, None, lse, ci, cc))
+            # k bound for the per-row group counts min(K + live, V) (exhaustive: V)
+            D.retrieve_device(logits, V if exhaustive else min(2 * K, V), d_k=hk,
+                              out=(None, None, lse, ci, cc))
             self.counters.count_fused("retrieve", rows * V * 4)
             _abi.call("fq_hars_select", logits.data_ptr(), logits.stride(0), lse.data_ptr(),
                       ci.data_ptr(), ci.stride(0), cc.data_ptr(), st.c, batch, K, V,

@@ -41,6 +41,13 @@ if len(adv) > 3:
         agg[e.name[:70]] += e.time_range.end - e.time_range.start
     for k, v in sorted(agg.items(), key=lambda kv: -kv[1])[:14]:
         print(f"   {v:8.1f} us  {k}")
+tot = collections.defaultdict(lambda: [0, 0.0])
+for e in ev:
+    tot[e.name[:70]][0] += 1
+    tot[e.name[:70]][1] += e.time_range.end - e.time_range.start
+print("whole generate, per kernel (n, total us, avg us):")
+for k, (n, v) in sorted(tot.items(), key=lambda kv: -kv[1][1])[:16]:
+    print(f"   {n:5d} {v:10.1f} {v / n:8.2f}  {k}")
 enc = [e for e in ev if e.time_range.end <= adv[0].time_range.start] if adv else []
 if enc:
     print(f"prefix (encoder + setup + step 0): {(adv[0].time_range.end - t0) / 1e3:.2f} ms")

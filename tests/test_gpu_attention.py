@@ -142,3 +142,105 @@ def test_layer_norm_paths(T, rows, d):
     want = (xd - xd.mean(1, keepdim=True)) / T.sqrt(xd.var(1, unbiased=False, keepdim=True) + 1e-5)
     want = want * gm.double() + b.double()
     assert _rel(out, want) <= 1e-6
+
+
+@pytest.mark.parametrize("H,hd,rows,cur", [(16, 64, 12, 13), (8, 128, 8, 0), (16, 64, 20, 63),
+                                          (32, 32, 4, 7), (8, 64, 8, 30)])
+def test_decoder_self_attention_rows_kernel(T, H, hd, rows, cur):
+    """The bf16 throughput-mode row kernel (CTA per beam row, 16-byte slot
+    segments, shuffle-reduced head dots) vs float64 on the bf16 cache."""
+    A = _abi()
+    g = T.Generator(device="cuda").manual_seed(H * hd + rows + cur)
+    S, beam = 64, 4
+    d = H * hd
+    kc = T.randn(S, rows, d, device="cuda", generator=g).to(T.bfloat16)
+    vc = T.randn(S, rows, d, device="cuda", generator=g).to(T.bfloat16)
+    hist = T.empty(rows, S, dtype=T.int32, device="cuda")
+    for r in range(rows):
+        item0 = (r // beam) * beam
+        hist[r] = T.randint(item0, min(item0 + beam, rows), (S,), generator=g, device="cuda").int()
+    sqkv = T.randn(rows, 3 * d, device="cuda", generator=g)
+    d_cur = T.tensor([cur], dtype=T.int32, device="cuda")
+    out = T.empty(rows, d, device="cuda")
+    out16 = T.empty(rows, d, device="cuda", dtype=T.bfloat16)
+    scale = float(np.float32(1 / math.sqrt(hd)))
+    A.call("fq_decoder_self_attention", sqkv.data_ptr(), 3 * d, kc.data_ptr(), vc.data_ptr(), 1,
+           hist.data_ptr(), d_cur.data_ptr(), rows, H, hd, S, scale, out.data_ptr(),
+           out16.data_ptr(), d, 0, A.stream_handle())
+    T.cuda.synchronize()
+    knew = sqkv[:, d:2 * d].to(T.bfloat16).double()
+    vnew = sqkv[:, 2 * d:].to(T.bfloat16).double()
+    assert T.equal(kc[cur].double(), knew) and T.equal(vc[cur].double(), vnew)
+    ar = T.arange(cur, device="cuda")
+    for r in range(rows):
+        idx = hist[r, :cur].long()
+        Kr = T.cat([kc[ar, idx].double(), knew[r:r + 1]]).view(cur + 1, H, hd)
+        Vr = T.cat([vc[ar, idx].double(), vnew[r:r + 1]]).view(cur + 1, H, hd)
+        q = sqkv[r, :d].double().view(H, hd)
+        p = T.softmax(T.einsum("the,he->ht", Kr, q) * scale, dim=1)
+        want = T.einsum("ht,the->he", p, Vr).reshape(d)
+        assert _rel(out[r], want) <= 1e-4, r
+        assert _rel(out16[r].float(), want) <= 1e-2, r
+
+
+@pytest.mark.parametrize("H,hd,beam", [(16, 64, 4), (16, 64, 1), (8, 128, 3), (32, 32, 8),
+                                       (16, 64, 6)])
+def test_cross_attention_stream_kernel(T, H, hd, beam):
+    """The bf16 throughput-mode cross-attention (CTA per item x head chunk)
+    including a padded item and a fully masked item (counted in d_bad)."""
+    A = _abi()
+    g = T.Generator(device="cuda").manual_seed(H + hd + beam)
+    B, S, L = 4, 64, 3
+    d = H * hd
+    ld = 2 * L * d
+    cq = T.randn(B * beam, d, device="cuda", generator=g)
+    packed = T.randn(B * S, ld, device="cuda", generator=g).to(T.bfloat16)
+    mask = T.zeros(B, S, device="cuda")
+    mask[1, 41:] = -math.inf
+    mask[3, :] = -math.inf
+    scale = float(np.float32(1 / math.sqrt(hd)))
+    layer = 2
+    ck = packed[:, 2 * layer * d:]
+    cv = packed[:, (2 * layer + 1) * d:]
+    out = T.empty(B * beam, d, device="cuda")
+    out16 = T.empty(B * beam, d, device="cuda", dtype=T.bfloat16)
+    bad = T.zeros(1, dtype=T.int32, device="cuda")
+    A.call("fq_cross_attention", cq.data_ptr(), d, ck.data_ptr(), cv.data_ptr(), 1, ld, B,
+           beam, S, H, hd, scale, mask.data_ptr(), out.data_ptr(), out16.data_ptr(), d, 0,
+           bad.data_ptr(), A.stream_handle())
+    T.cuda.synchronize()
+    assert int(bad.item()) == beam * H  # every (beam, head) row of item 3
+    K = packed[:, 2 * layer * d:(2 * layer + 1) * d].double().view(B, S, H, hd).permute(0, 2, 1, 3)
+    V = packed[:, (2 * layer + 1) * d:(2 * layer + 2) * d].double().view(B, S, H, hd).permute(0, 2, 1, 3)
+    Q = cq.double().view(B, beam, H, hd).permute(0, 2, 1, 3)
+    P = _softmax_ref(T, (Q @ K.transpose(-1, -2)) * scale, mask.double()[:, None, None, :])
+    want = (P @ V).permute(0, 2, 1, 3).reshape(B * beam, d)
+    n = 3 * beam  # items 0..2
+    assert _rel(out[:n], want[:n]) <= 1e-4
+    assert _rel(out16[:n].float(), want[:n]) <= 1e-2
+
+
+@pytest.mark.parametrize("S,hd,exact", [(64, 64, 1), (64, 64, 0), (17, 128, 1), (1, 64, 1),
+                                        (64, 32, 0)])
+def test_encoder_attention_tiled(T, S, hd, exact):
+    A = _abi()
+    g = T.Generator(device="cuda").manual_seed(S + hd)
+    B, H = 3, 4
+    d = H * hd
+    qkv = T.randn(B * S, 3 * d, device="cuda", generator=g)
+    mask = T.zeros(B, S, device="cuda")
+    mask[1, S // 2 + 1:] = -math.inf
+    out = T.empty(B * S, d, device="cuda")
+    out16 = T.empty(B * S, d, device="cuda", dtype=T.bfloat16)
+    bad = T.zeros(1, dtype=T.int32, device="cuda")
+    scale = float(np.float32(1 / math.sqrt(hd)))
+    A.call("fq_encoder_attention", qkv.data_ptr(), 3 * d, B, S, H, hd, scale, mask.data_ptr(),
+           out.data_ptr(), out16.data_ptr(), d, exact, bad.data_ptr(), A.stream_handle())
+    T.cuda.synchronize()
+    assert int(bad.item()) == 0
+    x = qkv.double().view(B, S, 3, H, hd)
+    Q, K, V = (x[:, :, i].permute(0, 2, 1, 3) for i in range(3))
+    P = _softmax_ref(T, (Q @ K.transpose(-1, -2)) * scale, mask.double()[:, None, None, :])
+    want = (P @ V).permute(0, 2, 1, 3).reshape(B * S, d)
+    assert _rel(out, want) <= (1e-5 if exact else 1e-4)
+    assert _rel(out16.float(), want) <= 1e-2

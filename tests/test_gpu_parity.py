@@ -286,3 +286,33 @@ def test_bf16_mode_tracks_oracle(P, O):
     assert rel(fl, ref) <= 3e-2
     hyps = sess.generate(src, P.DecodeConfig(beam_size=4, max_steps=10))
     assert all(len(h) == 4 for h in hyps)
+
+
+@pytest.mark.parametrize("V", [32000, 50257, 7])
+def test_retrieve_per_row_k_vs_oracle(P, O, V):
+    """Per-row group counts through d_k (the decode step's min(K + live, V)),
+    k bound <= 32: the register-resident cluster kernel; bit-exact group maxima,
+    thresholds and ordered candidates, including tie-heavy and all-equal rows."""
+    import torch
+    from paper_2010_13887_b200 import decode as D
+    rng = np.random.default_rng(V + 1)
+    rows = 40
+    L = rng.normal(size=(rows, V)).astype(F32)
+    L[3] = np.round(L[3])
+    L[5, :] = -1.5
+    L[7] = np.round(L[7] * 4) / 4
+    ks = rng.integers(1, min(32, V) + 1, size=rows).astype(np.int32)
+    ks[0], ks[1] = 0, min(32, V)
+    Ld = torch.from_numpy(L).cuda()
+    dk = torch.from_numpy(ks).cuda()
+    gm, th, lse, ci, cc = D.retrieve_device(Ld, min(32, V), d_k=dk)
+    torch.cuda.synchronize()
+    gm, th, lse, ci, cc = (t.cpu().numpy() for t in (gm, th, lse, ci, cc))
+    assert cc[0] == 0
+    for b in range(1, rows):
+        orr = O.retrieve(L[b:b + 1], int(ks[b]))
+        assert np.array_equal(gm[b, :ks[b]], orr.group_maxima[0]), b
+        assert th[b] == orr.threshold[0], b
+        assert cc[b] == len(orr.candidate_tokens[0]), b
+        assert np.array_equal(ci[b, :cc[b]], orr.candidate_tokens[0]), b
+        assert abs(lse[b] - orr.logsumexp_full[0]) <= 1e-7 * abs(orr.logsumexp_full[0]) + 1e-7
