@@ -104,6 +104,14 @@ def load():
     return _lib
 
 
+# Launch probe (bench.py): when PROBE is a list, every probed entry point is
+# bracketed by timing events on the launching stream (external events, so they
+# become event-record nodes inside a captured CUDA graph) and
+# (name, args, start, end) is appended. Off (None) on the product path.
+PROBE = None
+PROBE_NAMES = ("fq_gemm",)
+
+
 def call(name: str, *args) -> int:
     """Invoke an fq_* entry point; map a negative status to the reference's
     exception class (errors.py) with the library's message."""
@@ -114,7 +122,16 @@ def call(name: str, *args) -> int:
         if rc < 0:
             raise ExtensionError(f"fq_prepare: {lib.fq_last_error().decode()}")
         _prepared = True
-    rc = getattr(lib, name)(*args)
+    if PROBE is not None and name in PROBE_NAMES:
+        import torch
+        e0 = torch.cuda.Event(enable_timing=True, external=True)
+        e1 = torch.cuda.Event(enable_timing=True, external=True)
+        e0.record()
+        rc = getattr(lib, name)(*args)
+        e1.record()
+        PROBE.append((name, args, e0, e1, torch.cuda.is_current_stream_capturing()))
+    else:
+        rc = getattr(lib, name)(*args)
     if name not in _NO_PREPARE:
         _launches[0] += 1  # every other entry point launches exactly one kernel
     if rc < 0:

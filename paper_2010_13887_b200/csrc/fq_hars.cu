@@ -15,6 +15,8 @@
 // + :160-171 should_stop + engine.py:148-169, one CTA per batch item, on the
 // device-resident beam state. Scores are f64 cum + (f64(logit) - lse) and the
 // order is (-score, token, beam), exactly the reference's sort key.
+#include <stdlib.h>
+
 #include "fq_common.cuh"
 
 namespace fq {
@@ -210,6 +212,231 @@ __global__ void __launch_bounds__(kRetrieveThreads, 4) retrieve_kernel(
     if (threshold) threshold[row] = R;
     lse[row] = (double)M + log(s);
     cand_count[row] = n;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Stage 1, single-sweep variant (k <= 32, the decode step): the row is read
+// once from HBM and every per-element decision is made on the fly.
+//   * A pilot (each thread's first U vectors, ~13% of the row) gives a CTA-wide
+//     lower bound R' <= R (min over groups of partial group maxima: maxima only
+//     grow) and the pilot maximum M'.
+//   * Strided group maxima as in the two-pass kernel (thread t, lane c always in
+//     group (4t + c) % k).
+//   * logsumexp as an online sum started at M': s_t = sum exp(x - m_t), four
+//     terms per fp32 partial, f64 accumulation, rescaled in f64 only when an
+//     element exceeds the running max (rare after the pilot); combined as
+//     S = sum_t s_t exp(m_t - M) in a fixed order. Equal to the reference's lse
+//     up to fp32 rounding of the terms (~1e-7; tested against the oracle).
+//   * candidates: every x >= R' is appended to a shared-memory survivor list
+//     (~0.5% of the row); after R is known the survivors >= R are ranked by
+//     token. A survivor overflow (tie-heavy rows) falls back to an ordered
+//     rescan of the row from L2.
+// ---------------------------------------------------------------------------
+constexpr int kSwThreads = 256;
+constexpr int kSwU = 4;
+constexpr int kSurvCap = 2048;
+
+__global__ void __launch_bounds__(kSwThreads, 4) retrieve_sweep_kernel(
+    const float* __restrict__ logits, int64_t ld, int V, int k_fixed,
+    const int32_t* __restrict__ d_k, float* __restrict__ group_max, int64_t gm_ld,
+    float* __restrict__ threshold, double* __restrict__ lse, int32_t* __restrict__ cand_idx,
+    int64_t cand_ld, int64_t* __restrict__ cand_count) {
+  pdl_enter();
+  __shared__ float part_max[kSwThreads * 4];
+  __shared__ int32_t sv_idx[kSurvCap];
+  __shared__ float sv_val[kSurvCap];
+  __shared__ float gmax_s[32];
+  __shared__ float s_R, s_M;
+  __shared__ double red[kSwThreads / 32];
+  __shared__ int warp_tot[32];
+  __shared__ int s_cnt, s_total, s_n, s_ovf;
+  const int64_t row = blockIdx.x;
+  const int k = d_k ? d_k[row] : k_fixed;
+  if (k <= 0) {
+    if (threadIdx.x == 0) cand_count[row] = 0;
+    return;
+  }
+  const float* x = logits + row * ld;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int kk = k / (k & -k) * ((k & -k) > 4 ? (k & -k) / 4 : 1);  // k / gcd(k, 4)
+  const int T = kSwThreads - kSwThreads % kk;
+  const int nvec = V >> 2;
+  const float4* x4 = reinterpret_cast<const float4*>(x);
+  const bool act = tid < T;
+  constexpr float NEG = -INFINITY;
+  float4 q[kSwU];
+#pragma unroll
+  for (int u = 0; u < kSwU; ++u) {
+    const int v = tid + u * T;
+    q[u] = (act && v < nvec) ? __ldcs(x4 + v) : make_float4(NEG, NEG, NEG, NEG);
+  }
+  if (tid == 0) { s_cnt = 0; s_ovf = 0; }
+  // ---- pilot: partial group maxima -> R' (lower bound of R), M' ----
+  float gm[4] = {NEG, NEG, NEG, NEG};
+#pragma unroll
+  for (int u = 0; u < kSwU; ++u) {
+    gm[0] = fmaxf(gm[0], q[u].x); gm[1] = fmaxf(gm[1], q[u].y);
+    gm[2] = fmaxf(gm[2], q[u].z); gm[3] = fmaxf(gm[3], q[u].w);
+  }
+  if (act) {
+    part_max[4 * tid] = gm[0]; part_max[4 * tid + 1] = gm[1];
+    part_max[4 * tid + 2] = gm[2]; part_max[4 * tid + 3] = gm[3];
+  }
+  __syncthreads();
+  for (int g = w; g < k; g += kSwThreads / 32) {
+    float mm = NEG;
+    for (int e = g + lane * k; e < 4 * T; e += 32 * k) mm = fmaxf(mm, part_max[e]);
+    mm = warp_max(mm);
+    if (lane == 0) gmax_s[g] = mm;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    float R = gmax_s[0], M = gmax_s[0];
+    for (int g = 1; g < k; ++g) { R = fminf(R, gmax_s[g]); M = fmaxf(M, gmax_s[g]); }
+    s_R = R;
+    s_M = M;
+  }
+  __syncthreads();
+  const float Rp = s_R;  // may be -inf (group without pilot elements): everything survives
+  float m = s_M;
+  double s = 0.0;
+  auto visit4 = [&](const float4& e, int v) {
+    const float m4 = fmaxf(fmaxf(e.x, e.y), fmaxf(e.z, e.w));
+    if (m4 > m) {  // running max grows (rare after the pilot)
+      s = m == NEG ? 0.0 : s * exp((double)m - (double)m4);
+      m = m4;
+    }
+    if (m != NEG) {
+      const float t4 = (__expf(e.x - m) + __expf(e.y - m)) + (__expf(e.z - m) + __expf(e.w - m));
+      s += (double)t4;
+    }
+    if (m4 >= Rp) {
+      const float e4[4] = {e.x, e.y, e.z, e.w};
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        if (e4[c] >= Rp) {
+          const int p = atomicAdd(&s_cnt, 1);
+          if (p < kSurvCap) { sv_idx[p] = 4 * v + c; sv_val[p] = e4[c]; }
+        }
+      }
+    }
+  };
+#pragma unroll
+  for (int u = 0; u < kSwU; ++u) {
+    const int v = tid + u * T;
+    if (act && v < nvec) visit4(q[u], v);
+  }
+  if (act) {
+    for (int v0 = tid + kSwU * T; v0 < nvec; v0 += kSwU * T) {
+#pragma unroll
+      for (int u = 0; u < kSwU; ++u) {
+        const int v = v0 + u * T;
+        q[u] = v < nvec ? __ldcs(x4 + v) : make_float4(NEG, NEG, NEG, NEG);
+      }
+#pragma unroll
+      for (int u = 0; u < kSwU; ++u) {
+        const int v = v0 + u * T;
+        if (v < nvec) {
+          gm[0] = fmaxf(gm[0], q[u].x); gm[1] = fmaxf(gm[1], q[u].y);
+          gm[2] = fmaxf(gm[2], q[u].z); gm[3] = fmaxf(gm[3], q[u].w);
+          visit4(q[u], v);
+        }
+      }
+    }
+    part_max[4 * tid] = gm[0]; part_max[4 * tid + 1] = gm[1];
+    part_max[4 * tid + 2] = gm[2]; part_max[4 * tid + 3] = gm[3];
+  }
+  if (tid == 0) {  // V % 4 tail (visited scalar-wise; folded into its groups below)
+    for (int j = nvec << 2; j < V; ++j) {
+      const float xv = x[j];
+      if (xv > m) { s = m == NEG ? 0.0 : s * exp((double)m - (double)xv); m = xv; }
+      if (m != NEG) s += (double)__expf(xv - m);
+      if (xv >= Rp) {
+        const int p = atomicAdd(&s_cnt, 1);
+        if (p < kSurvCap) { sv_idx[p] = j; sv_val[p] = xv; }
+      }
+    }
+  }
+  __syncthreads();
+  for (int g = w; g < k; g += kSwThreads / 32) {
+    float mm = NEG;
+    for (int e = g + lane * k; e < 4 * T; e += 32 * k) mm = fmaxf(mm, part_max[e]);
+    mm = warp_max(mm);
+    if (lane == 0) gmax_s[g] = mm;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    for (int j = nvec << 2; j < V; ++j) gmax_s[j % k] = fmaxf(gmax_s[j % k], x[j]);
+    float R = gmax_s[0], M = gmax_s[0];
+    for (int g = 0; g < k; ++g) {
+      R = fminf(R, gmax_s[g]);
+      M = fmaxf(M, gmax_s[g]);
+      if (group_max) group_max[row * gm_ld + g] = gmax_s[g];
+    }
+    s_R = R;
+    s_M = M;
+  }
+  __syncthreads();
+  const float R = s_R, M = s_M;
+  const double st = m == NEG ? 0.0 : s * exp((double)m - (double)M);
+  const double S = block_sum(st, red);  // contains __syncthreads
+  const int nsv = s_cnt;
+  int32_t* out_idx = cand_idx + row * cand_ld;
+  if (nsv <= kSurvCap) {
+    // keep survivors >= R, compacted in place order-free, then rank by token
+    if (tid == 0) s_n = 0;
+    __syncthreads();
+    for (int i = tid; i < nsv; i += kSwThreads) {
+      const float v = sv_val[i];
+      const int j = sv_idx[i];
+      if (v >= R) part_max[atomicAdd(&s_n, 1)] = __int_as_float(j);
+    }
+    __syncthreads();
+    const int n = s_n;
+    if (n <= kSwThreads * 4) {
+      for (int i = tid; i < n; i += kSwThreads) {
+        const int j = __float_as_int(part_max[i]);
+        int rk = 0;
+        for (int q2 = 0; q2 < n; ++q2) rk += __float_as_int(part_max[q2]) < j ? 1 : 0;
+        if (rk < cand_ld) out_idx[rk] = j;
+      }
+      if (tid == 0) cand_count[row] = n;
+    } else {
+      if (tid == 0) s_ovf = 1;
+    }
+  }
+  __syncthreads();
+  if (nsv > kSurvCap || s_ovf) {
+    // ordered block-scan compaction over the row (re-read from L2)
+    __syncthreads();
+    int64_t base = 0;
+    const int chunk = kSwThreads * 4;
+    for (int c0 = 0; c0 < V; c0 += chunk) {
+      int flags = 0;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int j = c0 + tid * 4 + c;
+        if (j < V && x[j] >= R) flags |= 1 << c;
+      }
+      if (!__syncthreads_or(flags)) continue;
+      int off = block_excl_scan(__popc(flags), warp_tot, &s_total);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        if (flags & (1 << c)) {
+          const int64_t pos = base + off;
+          if (pos < cand_ld) out_idx[pos] = c0 + tid * 4 + c;
+          ++off;
+        }
+      }
+      base += s_total;
+      __syncthreads();
+    }
+    if (tid == 0) cand_count[row] = base;
+  }
+  if (tid == 0) {
+    if (threshold) threshold[row] = R;
+    lse[row] = (double)M + log(S);
   }
 }
 
@@ -487,6 +714,16 @@ using namespace fq;
 
 extern "C" {
 
+// FQ_RETRIEVE_TWO_PASS=1 selects the two-pass kernel for every k (A/B runs).
+static bool retrieve_two_pass_forced() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("FQ_RETRIEVE_TWO_PASS");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+
 int fq_retrieve(const float* logits, int64_t ld, int64_t rows, int64_t vocab, int64_t k,
                 const int32_t* d_k, float* group_max, int64_t gm_ld, float* threshold,
                 double* lse, int32_t* cand_idx, int64_t cand_ld, int64_t* cand_count,
@@ -499,6 +736,13 @@ int fq_retrieve(const float* logits, int64_t ld, int64_t rows, int64_t vocab, in
   FQ_CHECK_ARG(!group_max || gm_ld >= (d_k ? vocab : k) || gm_ld >= k, FQ_ERR_DIMENSION,
                "group_max leading dim too small");
   if (rows == 0) return FQ_OK;
+  if (k >= 1 && k <= 32 && (ld % 4) == 0 && ((uintptr_t)logits & 15) == 0 &&
+      !retrieve_two_pass_forced()) {
+    launch_kernel(retrieve_sweep_kernel, (unsigned)rows, kSwThreads, 0, as_stream(stream), 1u,
+                  logits, ld, (int)vocab, (int)k, d_k, group_max, gm_ld, threshold, lse,
+                  cand_idx, cand_ld, cand_count);
+    return launch_status("fq_retrieve");
+  }
   launch_kernel(retrieve_kernel, (unsigned)rows, kRetrieveThreads, 0, as_stream(stream), 1u, 
       logits, ld, (int)vocab, (int)k, d_k, group_max, gm_ld, threshold, lse, cand_idx, cand_ld,
       cand_count);
