@@ -16,10 +16,9 @@ void set_error(const char* fmt, ...) {
 
 bool pdl_enabled() {
   static const bool on = [] {
-    // opt-in: measured neutral on the graph-captured decode step (B200,
-    // C2 bf16: 121k vs 122k tok/s with/without), so the default is off
+    // default on; FQ_PDL=0 launches without programmatic serialization
     const char* e = getenv("FQ_PDL");
-    return e && e[0] == '1';
+    return !(e && e[0] == '0');
   }();
   return on;
 }

@@ -88,16 +88,21 @@ inline int ceil_div(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
 
 // ---- programmatic dependent launch (PDL) ---------------------------------
 // Every kernel is launched with programmatic stream serialization and starts
-// with pdl_enter(): griddepcontrol.wait blocks until the stream predecessor has
-// completed and its writes are visible (so nothing below it may touch global
-// memory earlier), then launch_dependents lets the NEXT kernel's CTAs launch
-// and run their prologue while this grid drains. In a captured decode step
-// this can hide per-kernel launch/ramp latency.
-// Opt-in with FQ_PDL=1 (measured neutral on the captured decode step).
+// with pdl_enter(): launch_dependents lets the NEXT kernel's CTAs launch and
+// run their prologue while this grid drains, then griddepcontrol.wait blocks
+// until the stream predecessor has completed and its writes are visible (so
+// nothing below it may touch dependent global memory earlier). The tcgen05
+// GEMMs go further: their TMA producer streams the first stages of the
+// (constant) weight operand before the wait, so weight fetch latency overlaps
+// the previous kernel. FQ_PDL=0 disables it.
 __device__ __forceinline__ void pdl_enter() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_launch_dependents() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 bool pdl_enabled();
 

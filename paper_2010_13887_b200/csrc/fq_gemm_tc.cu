@@ -201,6 +201,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __shared__ uint32_t tmem_base_sh;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  pdl_launch_dependents();
   if (ep.dbg && threadIdx.x == 0) {
     unsigned long long t_;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
@@ -243,19 +244,35 @@ __global__ void __launch_bounds__(kThreads, 1)
   else __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = tmem_base_sh;
-  pdl_enter();  // prologue above overlapped the previous kernel's tail
 
   if (warp == 0) {
     if (lane == 0) {  // ---- TMA producer ----
       const int a_rows = BM / cn, b_rows = BN / cm;
+      // Weights (B) do not depend on the previous kernel: stream the first
+      // tile's first stages of B before the grid-dependency wait.
+      int npre = 0;
+      if (csize == 1 && cluster_id < ngroups) {
+        const int n0 = (cluster_id / mg) * BN;
+        npre = num_kb < STAGES ? num_kb : STAGES;
+        for (int kb = 0; kb < npre; ++kb) {
+          uint8_t* sa = smem + kb * STAGE_BYTES;
+          mbar_expect_tx(&full_bar[kb], STAGE_BYTES);
+          tma_load_2d(&tma_b, &full_bar[kb], sa + A_BYTES, kb * BK, n0);
+        }
+      }
+      pdl_wait();  // activations (A) are written by the previous kernel
       int it = 0;
       for (int g = cluster_id; g < ngroups; g += nclusters) {
         const int m0 = ((g % mg) * cm + ry) * BM, n0 = ((g / mg) * cn + rx) * BN;
         for (int kb = 0; kb < num_kb; ++kb, ++it) {
           const int s = it % STAGES;
           const uint32_t ph = (it / STAGES) & 1;
-          mbar_wait(&empty_bar[s], ph ^ 1);  // free in every CTA I multicast into
           uint8_t* sa = smem + s * STAGE_BYTES;
+          if (it < npre) {  // B already in flight
+            tma_load_2d(&tma_a, &full_bar[s], sa, kb * BK, m0);
+            continue;
+          }
+          mbar_wait(&empty_bar[s], ph ^ 1);  // free in every CTA I multicast into
           mbar_expect_tx(&full_bar[s], STAGE_BYTES);
           if (cn > 1)
             tma_load_2d_mc(&tma_a, &full_bar[s], sa + rx * a_rows * 128, kb * BK,
@@ -301,6 +318,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else {  // ---- epilogue: warps 2..5 own TMEM lane quarters (warp % 4) ----
+    pdl_wait();  // C / residual / bias may be touched by the previous kernel
     const int q = warp & 3;
     float* st = stage_out + (warp - 2) * 32 * 33;
     float* c32 = reinterpret_cast<float*>(ep.c);
@@ -441,6 +459,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __shared__ uint32_t tmem_base_sh;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  pdl_launch_dependents();
   if (ep.dbg && threadIdx.x == 0) {
     unsigned long long t_;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
@@ -474,14 +493,25 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = tmem_base_sh;
-  pdl_enter();  // prologue above overlapped the previous kernel's tail
 
   if (warp == 0) {
     if (lane == 0) {  // ---- TMA producer: this CTA's K slice ----
+      // weight stages first (independent of the previous kernel), then wait
+      const int npre = (kb1 - kb0) < STAGES ? (kb1 - kb0) : STAGES;
+      for (int it = 0; it < npre; ++it) {
+        uint8_t* sa = smem + it * STAGE_BYTES;
+        mbar_expect_tx(&full_bar[it], STAGE_BYTES);
+        tma_load_2d(&tma_b, &full_bar[it], sa + A_BYTES, (kb0 + it) * BK, n0);
+      }
+      pdl_wait();
       for (int kb = kb0, it = 0; kb < kb1; ++kb, ++it) {
         const int s = it % STAGES;
-        mbar_wait(&empty_bar[s], ((it / STAGES) & 1) ^ 1);
         uint8_t* sa = smem + s * STAGE_BYTES;
+        if (it < npre) {
+          tma_load_2d(&tma_a, &full_bar[s], sa, kb * BK, m0);
+          continue;
+        }
+        mbar_wait(&empty_bar[s], ((it / STAGES) & 1) ^ 1);
         mbar_expect_tx(&full_bar[s], STAGE_BYTES);
         tma_load_2d(&tma_a, &full_bar[s], sa, kb * BK, m0);
         tma_load_2d(&tma_b, &full_bar[s], sa + A_BYTES, kb * BK, n0);
@@ -505,6 +535,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mma_commit(&tfull_bar);
     }
   } else {  // ---- epilogue warps: TMEM partial -> own smem [128][PLD] ----
+    pdl_wait();
     const int q = warp & 3;
     mbar_wait(&tfull_bar, 0);
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
