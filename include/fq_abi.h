@@ -192,6 +192,19 @@ int fq_hars_select(const float* logits, int64_t ld, const double* lse,
 int fq_hars_groups(fq_beam_state st, int64_t batch, int64_t beam, int64_t vocab,
                    int exhaustive, int32_t* d_k, fq_stream_t stream);
 
+/* The whole HARS step of a decode step in one launch (engine.py:148-169 +
+ * decode.py:217-240 + model.py:508-512): per row the group count
+ * min(K + live, V) (decode.py:230), stage 1 (single-sweep retrieve), and for
+ * each item, run by the last of its rows to finish, stage 2 (fq_hars_select
+ * semantics); the last item advances *d_cur. counters: int32 [batch + 1],
+ * zero-initialised once (they reset themselves). Needs 2*beam <= 32 and
+ * 16-byte aligned rows; exhaustive search uses the separate entry points. */
+int fq_hars_step(const float* logits, int64_t ld, fq_beam_state st, int64_t batch, int64_t beam,
+                 int64_t vocab, int64_t max_len, int64_t eos, const double* len_pow,
+                 int32_t* d_cur, int64_t max_steps, double* lse, int32_t* cand_idx,
+                 int64_t cand_ld, int64_t* cand_count, int32_t* counters, int64_t* row_tokens,
+                 int64_t* row_parents, int32_t* hist, fq_stream_t stream);
+
 /* Reset beam state to BeamState() (decode.py:145-151) for every item. */
 int fq_beam_state_init(fq_beam_state st, int64_t batch, int64_t beam, int64_t max_len,
                        fq_stream_t stream);

@@ -24,6 +24,8 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 
 #include "fq_common.cuh"
 
@@ -174,6 +176,14 @@ __device__ __forceinline__ void mma_commit_mc(uint64_t* bar, uint16_t mask) {
       : "memory");
 }
 
+__device__ __forceinline__ void dbg_stamp(unsigned long long* dbg, int slot) {
+  if (dbg) {
+    unsigned long long t_;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
+    dbg[8 * blockIdx.x + slot] = t_;
+  }
+}
+
 // Persistent over tile groups: a cluster (cm x cn CTAs, rank r -> (ry = r / cn,
 // rx = r % cn)) walks groups g = cluster_id, +num_clusters, ...; group g covers
 // M-tiles [gm*cm, +cm) x N-tiles [gn*cn, +cn) with the M-group fastest so
@@ -202,11 +212,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   pdl_launch_dependents();
-  if (ep.dbg && threadIdx.x == 0) {
-    unsigned long long t_;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
-    ep.dbg[2 * blockIdx.x] = t_;
-  }
+  if (threadIdx.x == 0) dbg_stamp(ep.dbg, 0);
   const int csize = cm * cn;
   const int rank = csize > 1 ? (int)cluster_rank() : 0;
   const int ry = rank / cn, rx = rank % cn;
@@ -244,6 +250,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   else __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = tmem_base_sh;
+  if (threadIdx.x == 0) dbg_stamp(ep.dbg, 1);
 
   if (warp == 0) {
     if (lane == 0) {  // ---- TMA producer ----
@@ -302,6 +309,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int s = it % STAGES;
           const uint32_t ph = (it / STAGES) & 1;
           mbar_wait(&full_bar[s], ph);
+          if (it == 0) dbg_stamp(ep.dbg, 2);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           const uint32_t a_base = smem_u32(smem + s * STAGE_BYTES);
           const uint32_t b_base = a_base + A_BYTES;
@@ -315,6 +323,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           else mma_commit(&empty_bar[s]);
         }
         mma_commit(&tfull_bar[as]);   // accumulator stage complete
+        if (local == 0) dbg_stamp(ep.dbg, 3);  // first tile's MMAs issued
       }
     }
   } else {  // ---- epilogue: warps 2..5 own TMEM lane quarters (warp % 4) ----
@@ -328,6 +337,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int as = local & 1;
       const int m0 = ((g % mg) * cm + ry) * BM, n0 = ((g / mg) * cn + rx) * BN;
       mbar_wait(&tfull_bar[as], (local >> 1) & 1);
+      if (local == 0 && threadIdx.x == 64) dbg_stamp(ep.dbg, 4);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const int rbase = m0 + q * 32;
       const int nrows = min(32, M - rbase);
@@ -396,15 +406,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   }
+  if (threadIdx.x == 64) dbg_stamp(ep.dbg, 5);  // epilogue done
   __syncwarp();
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   if (csize > 1) cluster_sync_all();  // no CTA leaves while peers may still signal it
   else __syncthreads();
-  if (ep.dbg && threadIdx.x == 0) {
-    unsigned long long t_;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
-    ep.dbg[2 * blockIdx.x + 1] = t_;
-  }
+  if (threadIdx.x == 0) dbg_stamp(ep.dbg, 6);
   if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
@@ -460,11 +467,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   pdl_launch_dependents();
-  if (ep.dbg && threadIdx.x == 0) {
-    unsigned long long t_;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
-    ep.dbg[2 * blockIdx.x] = t_;
-  }
+  if (threadIdx.x == 0) dbg_stamp(ep.dbg, 0);
   const int S = (int)cluster_nrank(), rank = (int)cluster_rank();
   const int mt = (M + BM - 1) / BM;
   const int tile = blockIdx.x / S;
@@ -608,11 +611,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   __syncwarp();
   cluster_sync_all();  // peers finished reading my partial
-  if (ep.dbg && threadIdx.x == 0) {
-    unsigned long long t_;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
-    ep.dbg[2 * blockIdx.x + 1] = t_;
-  }
+  if (threadIdx.x == 0) dbg_stamp(ep.dbg, 6);
   if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
@@ -778,6 +777,18 @@ static TcPlan plan_tc(int64_t M, int64_t N, int64_t K) {
   // launches on B200): small-M GEMMs are bound by the chip-wide L2->SM
   // operand traffic and per-launch overhead, large ones by per-SM ingest.
   const int64_t nt128 = (N + 127) / 128;
+  if (mt <= 8 && N <= 1024) {  // experiment hook: FQ_PLAN_SMALLN="bn,split"
+    static int ov_bn = -1, ov_sp = 1;
+    if (ov_bn < 0) {
+      ov_bn = 0;
+      if (const char* e = getenv("FQ_PLAN_SMALLN")) sscanf(e, "%d,%d", &ov_bn, &ov_sp);
+    }
+    if (ov_bn > 0) {
+      const int64_t nt = (N + ov_bn - 1) / ov_bn;
+      if (ov_sp == 1 || (mt * nt * ov_sp <= tc::num_sms() && ov_sp <= nkb))
+        return {ov_bn, 1, 1, ov_sp};
+    }
+  }
   if (mt <= 8) {
     if (N <= 1024 && nkb >= 32 && mt * nt128 * 4 <= tc::num_sms())
       return {128, 1, 1, 4};                       // K=4096: split-K over 4 CTAs

@@ -237,12 +237,11 @@ constexpr int kSwThreads = 256;
 constexpr int kSwU = 4;
 constexpr int kSurvCap = 2048;
 
-__global__ void __launch_bounds__(kSwThreads, 4) retrieve_sweep_kernel(
-    const float* __restrict__ logits, int64_t ld, int V, int k_fixed,
-    const int32_t* __restrict__ d_k, float* __restrict__ group_max, int64_t gm_ld,
-    float* __restrict__ threshold, double* __restrict__ lse, int32_t* __restrict__ cand_idx,
-    int64_t cand_ld, int64_t* __restrict__ cand_count) {
-  pdl_enter();
+__device__ __forceinline__ void sweep_row(
+    const float* __restrict__ logits, int64_t ld, int V, const int64_t row, const int k,
+    float* __restrict__ group_max, int64_t gm_ld, float* __restrict__ threshold,
+    double* __restrict__ lse, int32_t* __restrict__ cand_idx, int64_t cand_ld,
+    int64_t* __restrict__ cand_count) {
   __shared__ float part_max[kSwThreads * 4];
   __shared__ int32_t sv_idx[kSurvCap];
   __shared__ float sv_val[kSurvCap];
@@ -251,8 +250,6 @@ __global__ void __launch_bounds__(kSwThreads, 4) retrieve_sweep_kernel(
   __shared__ double red[kSwThreads / 32];
   __shared__ int warp_tot[32];
   __shared__ int s_cnt, s_total, s_n, s_ovf;
-  const int64_t row = blockIdx.x;
-  const int k = d_k ? d_k[row] : k_fixed;
   if (k <= 0) {
     if (threadIdx.x == 0) cand_count[row] = 0;
     return;
@@ -440,6 +437,17 @@ __global__ void __launch_bounds__(kSwThreads, 4) retrieve_sweep_kernel(
   }
 }
 
+__global__ void __launch_bounds__(kSwThreads, 4) retrieve_sweep_kernel(
+    const float* __restrict__ logits, int64_t ld, int V, int k_fixed,
+    const int32_t* __restrict__ d_k, float* __restrict__ group_max, int64_t gm_ld,
+    float* __restrict__ threshold, double* __restrict__ lse, int32_t* __restrict__ cand_idx,
+    int64_t cand_ld, int64_t* __restrict__ cand_count) {
+  pdl_enter();
+  const int64_t row = blockIdx.x;
+  sweep_row(logits, ld, V, row, d_k ? d_k[row] : k_fixed, group_max, gm_ld, threshold, lse,
+            cand_idx, cand_ld, cand_count);
+}
+
 // ---------------------------------------------------------------------------
 // stage 2
 // ---------------------------------------------------------------------------
@@ -467,13 +475,14 @@ __device__ bool seq_less(const int32_t* a, int la, const int32_t* b, int lb) {
   return la < lb;
 }
 
-__global__ void __launch_bounds__(kSelThreads) hars_select_kernel(
-    const float* __restrict__ logits, int64_t ld, const double* __restrict__ lse,
-    const int32_t* __restrict__ cand_idx, int64_t cand_ld,
-    const int64_t* __restrict__ cand_count, fq_beam_state st, int K, int max_len, int eos,
-    const double* __restrict__ len_pow, const int32_t* __restrict__ d_cur, int64_t max_steps, int64_t* row_tokens,
-    int64_t* row_parents, int32_t* hist) {
-  pdl_enter();
+// Stage-2 body for item b (one CTA). Candidate lists, counts and lse are read
+// with ld.global.cg: in the fused step they were written by other CTAs of the
+// same grid (made visible by their fence + the arrival counter).
+__device__ __forceinline__ void select_item(
+    const int b, const float* __restrict__ logits, int64_t ld, const double* lse,
+    const int32_t* cand_idx, int64_t cand_ld, const int64_t* cand_count, fq_beam_state st, int K,
+    int max_len, int eos, const double* __restrict__ len_pow, const int32_t* __restrict__ d_cur,
+    int64_t max_steps, int64_t* row_tokens, int64_t* row_parents, int32_t* hist) {
   extern __shared__ int32_t sh[];  // old prefixes [K][max_len] then old hist [K][max_len]
   __shared__ Cand cands[kSelCap];
   __shared__ Cand picks[2 * kMaxBeam];
@@ -484,7 +493,7 @@ __global__ void __launch_bounds__(kSelThreads) hars_select_kernel(
   __shared__ double red_s[kSelThreads / 32];
   __shared__ int red_t[kSelThreads / 32], red_b[kSelThreads / 32];
 
-  const int b = blockIdx.x, tid = threadIdx.x;
+  const int tid = threadIdx.x;
   const int64_t row0 = (int64_t)b * K;
   int32_t* old_pref = sh;
   int32_t* old_hist = sh + K * max_len;
@@ -502,7 +511,7 @@ __global__ void __launch_bounds__(kSelThreads) hars_select_kernel(
   const bool last_step = (int64_t)cur == max_steps - 1;
   if (tid == 0) {
     offs[0] = 0;
-    for (int i = 0; i < live; ++i) offs[i + 1] = offs[i] + cand_count[row0 + i];
+    for (int i = 0; i < live; ++i) offs[i + 1] = offs[i] + __ldcg(cand_count + row0 + i);
   }
   for (int i = tid; i < K * max_len; i += blockDim.x) {
     old_pref[i] = st.prefix[(int64_t)b * K * max_len + i];
@@ -522,10 +531,10 @@ __global__ void __launch_bounds__(kSelThreads) hars_select_kernel(
     int i = 0;
     while (offs[i + 1] <= j) ++i;
     const int64_t r = row0 + i;
-    const int32_t tok = cand_idx[r * cand_ld + (j - offs[i])];
+    const int32_t tok = __ldcg(cand_idx + r * cand_ld + (j - offs[i]));
     const double lg = (double)logits[r * ld + tok];
     Cand c;
-    c.s = st.cum[b * K + i] + (lg - lse[r]);  // decode.py:238
+    c.s = st.cum[b * K + i] + (lg - __ldcg(lse + r));  // decode.py:238
     c.tok = tok;
     c.beam = i;
     return c;
@@ -676,6 +685,60 @@ __global__ void __launch_bounds__(kSelThreads) hars_select_kernel(
   }
 }
 
+__global__ void __launch_bounds__(kSelThreads) hars_select_kernel(
+    const float* __restrict__ logits, int64_t ld, const double* __restrict__ lse,
+    const int32_t* __restrict__ cand_idx, int64_t cand_ld,
+    const int64_t* __restrict__ cand_count, fq_beam_state st, int K, int max_len, int eos,
+    const double* __restrict__ len_pow, const int32_t* __restrict__ d_cur, int64_t max_steps,
+    int64_t* row_tokens, int64_t* row_parents, int32_t* hist) {
+  pdl_enter();
+  select_item(blockIdx.x, logits, ld, lse, cand_idx, cand_ld, cand_count, st, K, max_len, eos,
+              len_pow, d_cur, max_steps, row_tokens, row_parents, hist);
+}
+
+// ---------------------------------------------------------------------------
+// The whole HARS step in one launch (decode step, k = min(K + live, V) <= 32):
+// CTA per beam row derives its group count from the beam state
+// (decode.py:230), runs the single-sweep stage 1 on its row, and the last CTA
+// of each item to finish (arrival counter, self-resetting) runs stage 2 for the
+// item; the last item to finish advances the decode position. Replaces
+// fq_hars_groups + fq_retrieve + fq_hars_select + fq_step_advance, and lets
+// the selection of early items overlap the retrieve of the others.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kSwThreads) hars_step_kernel(
+    const float* __restrict__ logits, int64_t ld, int V, fq_beam_state st, int batch, int K,
+    int max_len, int eos, const double* __restrict__ len_pow, int32_t* d_cur, int64_t max_steps,
+    double* lse, int32_t* cand_idx, int64_t cand_ld, int64_t* cand_count, int* item_cnt,
+    int* all_cnt, int64_t* row_tokens, int64_t* row_parents, int32_t* hist) {
+  pdl_enter();
+  const int64_t row = blockIdx.x;
+  const int b = (int)(row / K), i = (int)(row % K);
+  const int live = st.live[b];
+  const int k = (!st.done[b] && i < live) ? min(K + live, V) : 0;  // hars_groups
+  sweep_row(logits, ld, V, row, k, nullptr, 0, nullptr, lse, cand_idx, cand_ld, cand_count);
+  __shared__ int s_last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const int prev = atomicAdd(item_cnt + b, 1);
+    s_last = prev == K - 1;
+    if (s_last) item_cnt[b] = 0;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  select_item(b, logits, ld, lse, cand_idx, cand_ld, cand_count, st, K, max_len, eos, len_pow,
+              d_cur, max_steps, row_tokens, row_parents, hist);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(all_cnt, 1) == batch - 1) {  // every item read d_cur: advance it
+      *all_cnt = 0;
+      *d_cur += 1;
+    }
+  }
+}
+
 __global__ void hars_groups_kernel(fq_beam_state st, int batch, int K, int V, int exhaustive,
                                    int32_t* d_k) {
   pdl_enter();
@@ -771,6 +834,27 @@ int fq_hars_select(const float* logits, int64_t ld, const double* lse, const int
   return launch_status("fq_hars_select");
 }
 
+int fq_hars_step(const float* logits, int64_t ld, fq_beam_state st, int64_t batch, int64_t beam,
+                 int64_t vocab, int64_t max_len, int64_t eos, const double* len_pow,
+                 int32_t* d_cur, int64_t max_steps, double* lse, int32_t* cand_idx,
+                 int64_t cand_ld, int64_t* cand_count, int32_t* counters, int64_t* row_tokens,
+                 int64_t* row_parents, int32_t* hist, fq_stream_t stream) {
+  FQ_CHECK_ARG(logits && lse && cand_idx && cand_count && counters && d_cur && row_tokens &&
+                   row_parents && batch > 0 && beam >= 1 && beam <= kMaxBeam && max_len >= 1,
+               FQ_ERR_DIMENSION, "fq_hars_step: bad args");
+  FQ_CHECK_ARG(2 * beam <= 32 && ld % 4 == 0 && vocab % 4 == 0 && ((uintptr_t)logits & 15) == 0,
+               FQ_ERR_PARAMETER, "fq_hars_step: needs 2*beam <= 32 and 16-byte aligned rows");
+  FQ_CHECK_ARG(cand_ld >= vocab, FQ_ERR_DIMENSION, "fq_hars_step needs full candidate rows");
+  FQ_CHECK_ARG(eos >= 0 && eos < vocab, FQ_ERR_PARAMETER, "eos token outside vocabulary");
+  const size_t smem = (size_t)2 * beam * max_len * sizeof(int32_t);
+  FQ_CHECK_ARG(smem <= 96 * 1024, FQ_ERR_CAPACITY, "fq_hars_step: max_len too large");
+  launch_kernel(hars_step_kernel, (unsigned)(batch * beam), kSwThreads, smem, as_stream(stream),
+                1u, logits, ld, (int)vocab, st, (int)batch, (int)beam, (int)max_len, (int)eos,
+                len_pow, d_cur, max_steps, lse, cand_idx, cand_ld, cand_count, counters,
+                counters + batch, row_tokens, row_parents, hist);
+  return launch_status("fq_hars_step");
+}
+
 int fq_hars_groups(fq_beam_state st, int64_t batch, int64_t beam, int64_t vocab, int exhaustive,
                    int32_t* d_k, fq_stream_t stream) {
   FQ_CHECK_ARG(d_k && batch > 0 && beam > 0, FQ_ERR_DIMENSION, "fq_hars_groups: bad args");
@@ -792,7 +876,9 @@ int fq_beam_state_init(fq_beam_state st, int64_t batch, int64_t beam, int64_t ma
 
 int fq_hars_prepare(void) {
   if (cudaFuncSetAttribute(hars_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           160 * 1024) != cudaSuccess) {
+                           160 * 1024) != cudaSuccess ||
+      cudaFuncSetAttribute(hars_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           96 * 1024) != cudaSuccess) {
     set_error("fq_prepare: cannot opt in to large shared memory (hars)");
     return FQ_ERR_CUDA;
   }

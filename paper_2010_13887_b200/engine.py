@@ -143,9 +143,22 @@ class Session:
                                     out=b.get("hars.len_pow", (self.config.max_seq_len + 1,),
                                               torch.float64))
 
+        fused = not exhaustive and 2 * K <= 32 and V % 4 == 0
+        if fused:
+            hcnt = b.get("hars.counters", (batch + 1,), torch.int32)
+            hcnt.zero_()
+
         def body():
             logits = step.run()
             stream = _abi.stream_handle()
+            if fused:  # groups + stage 1 + stage 2 + position advance, one launch
+                _abi.call("fq_hars_step", logits.data_ptr(), logits.stride(0), st.c, batch, K, V,
+                          self.config.max_seq_len, cfg.eos_token, _abi.ptr(lp),
+                          cache.d_cur.data_ptr(), max_steps, lse.data_ptr(), ci.data_ptr(),
+                          ci.stride(0), cc.data_ptr(), hcnt.data_ptr(), step.tokens.data_ptr(),
+                          parents.data_ptr(), cache.hist.data_ptr(), stream)
+                self.counters.count_fused("retrieve", rows * V * 4)
+                return
             _abi.call("fq_hars_groups", st.c, batch, K, V, exhaustive, hk.data_ptr(), stream)
             # k bound for the per-row group counts min(K + live, V) (exhaustive: V)
             D.retrieve_device(logits, V if exhaustive else min(2 * K, V), d_k=hk,
