@@ -197,7 +197,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   constexpr int A_BYTES = BM * BK * 2;
   constexpr int B_BYTES = BN * BK * 2;
   constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  constexpr uint32_t TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;  // two accumulator stages
+  // two accumulator stages; the allocation is a power of two >= 32 columns
+  constexpr uint32_t TMEM_COLS = 2 * BN <= 32 ? 32 : 2 * BN <= 64 ? 64 : 2 * BN <= 128 ? 128
+                                 : 2 * BN <= 256 ? 256 : 512;
   extern __shared__ uint8_t smem_raw[];
   // 1024-B aligned (128B-swizzle atoms); identical offset in every CTA, so a
   // multicast lands at the same place cluster-wide. Pointer arithmetic keeps
@@ -740,7 +742,8 @@ static int prep() {
 }  // namespace tc
 
 int gemm_tc_prepare() {
-  if (tc::prep<256, 4>() || tc::prep<128, 6>() || tc::prep<64, 8>() || tc::prep<32, 8>() ||
+  if (tc::prep<256, 4>() || tc::prep<224, 4>() || tc::prep<192, 4>() || tc::prep<128, 6>() ||
+      tc::prep<64, 8>() || tc::prep<32, 8>() ||
       tc::prep_splitk<256, 4>() || tc::prep_splitk<128, 6>() || tc::prep_splitk<64, 8>()) {
     set_error("fq_prepare: tcgen05 GEMM smem opt-in failed");
     return FQ_ERR_CUDA;
@@ -794,9 +797,17 @@ static TcPlan plan_tc(int64_t M, int64_t N, int64_t K) {
       return {128, 1, 1, 4};                       // K=4096: split-K over 4 CTAs
     if (N <= 1024) return {32, 1, 1, 1};
     if (N < 8192) return {128, 1, 1, 1};
-    return {256, 1, 1, 1};
   }
-  return {256, 1, 1, 1};
+  // Large GEMMs are tensor-bound: pick the tile width minimising the busiest
+  // CTA's work, ceil(tiles / SMs) * BN (wave quantisation over 148 SMs).
+  int best = 256;
+  int64_t best_cost = -1;
+  for (int bn : {256, 224, 192}) {
+    const int64_t tiles = mt * ((N + bn - 1) / bn);
+    const int64_t cost = (tiles + tc::num_sms() - 1) / tc::num_sms() * bn;
+    if (best_cost < 0 || cost < best_cost) { best = bn; best_cost = cost; }
+  }
+  return {best, 1, 1, 1};
 }
 
 int launch_tc_gemm(const void* a, int64_t lda, const void* b, int64_t ldb, void* c, int c_bf16,
@@ -818,6 +829,8 @@ int launch_tc_gemm(const void* a, int64_t lda, const void* b, int64_t ldb, void*
   }
   switch (p.bn) {
     case 256: return tc::launch<256, 4>(a, lda, b, ldb, ep, M, N, K, p.cm, p.cn, s);
+    case 224: return tc::launch<224, 4>(a, lda, b, ldb, ep, M, N, K, p.cm, p.cn, s);
+    case 192: return tc::launch<192, 4>(a, lda, b, ldb, ep, M, N, K, p.cm, p.cn, s);
     case 128: return tc::launch<128, 6>(a, lda, b, ldb, ep, M, N, K, p.cm, p.cn, s);
     case 64: return tc::launch<64, 8>(a, lda, b, ldb, ep, M, N, K, p.cm, p.cn, s);
     default: return tc::launch<32, 8>(a, lda, b, ldb, ep, M, N, K, p.cm, p.cn, s);

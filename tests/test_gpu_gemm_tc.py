@@ -35,7 +35,7 @@ def _rel(got, want):
 @pytest.mark.parametrize("M,N,K", [
     (128, 64, 64), (1, 8, 16), (32, 512, 512), (100, 100, 72), (512, 1024, 1024),
     (512, 3072, 1024), (512, 1024, 4096), (300, 32000, 512), (8192, 3072, 1024),
-    (2048, 4096, 1024)])
+    (2048, 4096, 1024), (512, 32000, 1024), (8192, 1024, 4096), (1000, 4000, 256)])
 def test_tc_gemm_plain(P, M, N, K):
     import torch
     g = torch.Generator(device="cuda").manual_seed(M * 7 + N * 3 + K)
@@ -108,3 +108,18 @@ def test_tc_gemm_all_plans(P, M, N, K):
     finally:
         lib.fq_gemm_force_plan(0, 0, 0, 1)
     assert tried == len(plans)
+
+
+@pytest.mark.parametrize("M,N,K", [(8192, 3072, 1024), (512, 32000, 1024)])
+def test_tc_gemm_wide_tile_epilogue(P, M, N, K):
+    """Tile widths 192/224 (wave-quantisation plan) with the fused epilogue."""
+    import torch
+    g = torch.Generator(device="cuda").manual_seed(N + K)
+    a = torch.randn(M, K, device="cuda", generator=g).to(torch.bfloat16)
+    b = torch.randn(N, K, device="cuda", generator=g).to(torch.bfloat16)
+    bias = torch.randn(N, device="cuda", generator=g)
+    res = torch.randn(M, N, device="cuda", generator=g)
+    out = torch.empty(M, N, device="cuda")
+    P.gemm(a, b, out, transpose_b=True, bias=bias, activation="relu", residual=res)
+    torch.cuda.synchronize()
+    assert _rel(out, _ref(a, b, bias, "relu", res)) <= 1e-3
