@@ -1,0 +1,34 @@
+#!/bin/bash
+# ncu evidence for profiles/: launch list of one C2 generate, full captures of
+# one decode step's GEMMs (traffic) and of the other hot kernels (one launch
+# each, steady state). Usage: bash scripts/ncu_round.sh <tag>
+set -u
+T=${1:-r1}
+mkdir -p gpurun_out
+ncu --metrics gpu__time_duration.sum --clock-control none --profile-from-start off --csv \
+  --log-file gpurun_out/${T}_launches.csv python scripts/profile_step.py > /dev/null 2>&1
+echo "launches rc=$?"
+# one decode step's GEMMs (skip the 25 encoder/cross GEMMs + 10 decode steps x 37)
+timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed,lts__t_bytes.sum,launch__grid_size \
+  --clock-control none --profile-from-start off -k regex:tc_gemm --csv \
+  -s 395 -c 37 python scripts/profile_step.py --steps 12 > gpurun_out/${T}_step_gemms.csv 2> gpurun_out/${T}_step_gemms.log
+echo "gemms rc=$?"
+cap() {  # name regex skip
+  timeout 600 ncu --set full --clock-control none --import-source on --profile-from-start off \
+    -k regex:"$2" -s "$3" -c 1 -o gpurun_out/${T}_$1 -f python scripts/profile_step.py --steps 40 \
+    > gpurun_out/${T}_$1.log 2>&1
+  echo "$1 rc=$?"
+}
+cap hars "hars_step" 32
+cap selfattn "decoder_self_attention" 190
+cap crossattn "cross_attention" 190
+cap ln "layer_norm_row128" 570
+cap logits "tc_gemm_kernel" 1000
+cap encattn "encoder_attention" 3
+for f in hars selfattn crossattn ln logits encattn; do
+  python scripts/ncu_summary.py gpurun_out/${T}_$f.ncu-rep 12 > gpurun_out/${T}_${f}_summary.txt 2>&1
+  python scripts/ncu_ops.py gpurun_out/${T}_$f.ncu-rep 12 >> gpurun_out/${T}_${f}_summary.txt 2>&1
+done
+python scripts/launch_summary.py gpurun_out/${T}_launches.csv 30 > gpurun_out/${T}_launches_summary.txt 2>&1
+rm -f gpurun_out/${T}_launches.csv gpurun_out/${T}_encattn.ncu-rep gpurun_out/${T}_crossattn.ncu-rep
+ls -la gpurun_out | grep $T
