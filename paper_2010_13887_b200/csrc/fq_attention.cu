@@ -510,7 +510,7 @@ __global__ void __launch_bounds__(128) decoder_self_attention_kernel(
 // exact-mode numerics; ~10x fewer shared-memory reads than one dot per lane.
 // ---------------------------------------------------------------------------
 template <int NC, int HC>
-__global__ void __launch_bounds__(256) encoder_attention_tiled(
+__global__ void __launch_bounds__(256, 4) encoder_attention_tiled(
     const float* __restrict__ qkv, int64_t ldq, int seq, int heads, int hd, float scale,
     const float* __restrict__ mask, float* __restrict__ out, __nv_bfloat16* __restrict__ out16,
     int64_t ldo, int exact, int* d_bad) {
@@ -670,7 +670,7 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 // this step are written to slot (cur, r) (copy-free history, see above).
 // ---------------------------------------------------------------------------
 template <int HD, int U>
-__global__ void __launch_bounds__(256) decoder_self_attention_rows(
+__global__ void __launch_bounds__(256, 4) decoder_self_attention_rows(
     const float* __restrict__ sqkv, int64_t ldq, __nv_bfloat16* __restrict__ kc,
     __nv_bfloat16* __restrict__ vc, const int32_t* __restrict__ hist,
     const int32_t* __restrict__ d_cur, int rows, int heads, int max_len, float scale,
