@@ -298,8 +298,13 @@ def run_ours(args, rank, world):
     # -- end to end through the public API: host tokens in, host hypotheses out --
     e2e_times = []
     h2d = src_host.nbytes
-    d2h = sum(getattr(st, n).numel() * getattr(st, n).element_size()
-              for n, _, _ in D.DeviceBeamState.FIELDS)
+    dims = {"B": args.batch, "K": BEAM, "S": cfg.max_seq_len, "1": 1}
+    d2h = 0
+    for _, dt, shape in D.DeviceBeamState.FIELDS:
+        n = 1
+        for c in shape:
+            n *= dims[c]
+        d2h += n * torch.empty((), dtype=dt).element_size()
     for i in range(max(1, min(args.steps, 3)) + 1):
         flush()
         barrier()

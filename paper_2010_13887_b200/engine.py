@@ -42,9 +42,23 @@ class Hypothesis:
     score: float
 
 
+class _GroupedBeamState:
+    """The device beam states of the item groups of one generate, in item order."""
+
+    def __init__(self, states):
+        self.states = states
+
+    def host_items(self) -> list:
+        out = []
+        for st in self.states:
+            out.extend(st.host_items())
+        return out
+
+
 class Session:
     def __init__(self, config: M.ModelConfig, weights: M.ModelWeights, engine: str = "fused",
-                 share_plan: bool = True, precision: str = "fp32", use_graphs: bool = True):
+                 share_plan: bool = True, precision: str = "fp32", use_graphs: bool = True,
+                 streams: int = 1):
         if engine != "fused":
             raise InputError(f"unknown engine {engine!r} (the B200 product is the fused engine; "
                              "the naive twin is the CPU baseline)")
@@ -56,6 +70,9 @@ class Session:
         weights.validate(config)
         self.config, self.weights, self.engine, self.precision = config, weights, engine, precision
         self.use_graphs = use_graphs
+        if streams not in (1, 2):
+            raise InputError("streams must be 1 or 2")
+        self.streams = streams
         self.counters = OpCounters()
         self.timers = Timers()
         self.dw = M.DeviceWeights.get(config, weights, precision)
@@ -66,8 +83,17 @@ class Session:
         self.arena = Arena(self.plan)
         self._buffers = M.ArenaBuffers(self.arena)
         self._graphs: dict = {}
-        self._pinned_done = torch.zeros(max(config.max_seq_len, 1), dtype=torch.int32,
+        self._pinned_done = torch.zeros((max(config.max_seq_len, 1), 2), dtype=torch.int32,
                                         pin_memory=True)
+        self._side_stream = torch.cuda.Stream()
+        self._buffers2 = None
+
+    def _group_buffers(self):
+        """Decode buffers of the second item group (its own arena, same plan)."""
+        if self._buffers2 is None:
+            self._arena2 = Arena(self.plan)
+            self._buffers2 = M.ArenaBuffers(self._arena2)
+        return self._buffers2
 
     # ------------------------------------------------------------------
     def _encode_dev(self, src: np.ndarray, lengths=None):
@@ -124,55 +150,90 @@ class Session:
         rows = batch * K
         max_steps = min(cfg.max_steps, self.config.max_seq_len)
 
-        packed, mask, cache = self._setup_decoder(src, src_lengths, rows)
-        step = M.DecoderStep(self.dw, self.config, batch, K, seq, cache, packed, mask,
-                             self._buffers, self.counters, self.timers)
-        st = D.DeviceBeamState(batch, K, self.config.max_seq_len, self._buffers)
-        st.init()
-        step.tokens.fill_(bos_token)
-        step.bad.zero_()
+        packed, mask, cache0 = self._setup_decoder(src, src_lengths, rows)
         V = self.config.vocab_size
-        b = self._buffers
-        hk = b.get("hars.k", (rows,), torch.int32)
-        lse = b.get("hars.lse", (rows,), torch.float64)
-        ci = b.get("hars.cand_idx", (rows, V), torch.int32)
-        cc = b.get("hars.cand_count", (rows,), torch.int64)
-        parents = b.get("dec.parents", (rows,), torch.int64)
         exhaustive = int(search == "exhaustive")
-        lp = D.length_penalty_table(cfg.length_penalty, self.config.max_seq_len, None,
-                                    out=b.get("hars.len_pow", (self.config.max_seq_len + 1,),
-                                              torch.float64))
-
         fused = not exhaustive and 2 * K <= 32 and V % 4 == 0
-        if fused:
-            hcnt = b.get("hars.counters", (batch + 1,), torch.int32)
-            hcnt.zero_()
+        # Two-group overlap (streams=2, opt-in): the items are split in two
+        # halves decoded by two independent chains on two streams inside the
+        # step graph (every op is per row / per item, so results are
+        # unchanged). Measured on C2: no gain over one chain (the halves'
+        # GEMMs keep the same per-SM ingest and double the launches), so the
+        # default is one chain.
+        ngroups = 2 if (self.streams == 2 and fused and self.use_graphs and batch >= 2) else 1
+        bounds = [0, batch] if ngroups == 1 else [0, (batch + 1) // 2, batch]
+        groups = []
+        for g in range(ngroups):
+            i0, i1 = bounds[g], bounds[g + 1]
+            nb, nr = i1 - i0, (i1 - i0) * K
+            bufs = self._buffers if g == 0 else self._group_buffers()
+            cache = cache0 if ngroups == 1 else M.KVCache(self.config, nr, bufs,
+                                                          precision=self.precision)
+            gp = packed[i0 * seq:i1 * seq]
+            gm = mask[i0:i1] if mask is not None else None
+            step = M.DecoderStep(self.dw, self.config, nb, K, seq, cache, gp, gm, bufs,
+                                 self.counters, self.timers)
+            st = D.DeviceBeamState(nb, K, self.config.max_seq_len, bufs)
+            st.init()
+            step.tokens.fill_(bos_token)
+            step.bad.zero_()
+            grp = dict(batch=nb, rows=nr, cache=cache, step=step, st=st,
+                       hk=bufs.get("hars.k", (nr,), torch.int32),
+                       lse=bufs.get("hars.lse", (nr,), torch.float64),
+                       ci=bufs.get("hars.cand_idx", (nr, V), torch.int32),
+                       cc=bufs.get("hars.cand_count", (nr,), torch.int64),
+                       parents=bufs.get("dec.parents", (nr,), torch.int64),
+                       lp=D.length_penalty_table(
+                           cfg.length_penalty, self.config.max_seq_len, None,
+                           out=bufs.get("hars.len_pow", (self.config.max_seq_len + 1,),
+                                        torch.float64)))
+            if fused:
+                grp["hcnt"] = bufs.get("hars.counters", (nb + 1,), torch.int32)
+                grp["hcnt"].zero_()
+            groups.append(grp)
 
-        def body():
+        def body(gr):
+            step, st, cache = gr["step"], gr["st"], gr["cache"]
+            nb, nr = gr["batch"], gr["rows"]
+            lse, ci, cc, hk, parents, lp = (gr[k] for k in ("lse", "ci", "cc", "hk", "parents",
+                                                           "lp"))
             logits = step.run()
             stream = _abi.stream_handle()
             if fused:  # groups + stage 1 + stage 2 + position advance, one launch
-                _abi.call("fq_hars_step", logits.data_ptr(), logits.stride(0), st.c, batch, K, V,
+                _abi.call("fq_hars_step", logits.data_ptr(), logits.stride(0), st.c, nb, K, V,
                           self.config.max_seq_len, cfg.eos_token, _abi.ptr(lp),
                           cache.d_cur.data_ptr(), max_steps, lse.data_ptr(), ci.data_ptr(),
-                          ci.stride(0), cc.data_ptr(), hcnt.data_ptr(), step.tokens.data_ptr(),
-                          parents.data_ptr(), cache.hist.data_ptr(), stream)
-                self.counters.count_fused("retrieve", rows * V * 4)
+                          ci.stride(0), cc.data_ptr(), gr["hcnt"].data_ptr(),
+                          step.tokens.data_ptr(), parents.data_ptr(), cache.hist.data_ptr(),
+                          stream)
+                self.counters.count_fused("retrieve", nr * V * 4)
                 return
-            _abi.call("fq_hars_groups", st.c, batch, K, V, exhaustive, hk.data_ptr(), stream)
+            _abi.call("fq_hars_groups", st.c, nb, K, V, exhaustive, hk.data_ptr(), stream)
             # k bound for the per-row group counts min(K + live, V) (exhaustive: V)
             D.retrieve_device(logits, V if exhaustive else min(2 * K, V), d_k=hk,
                               out=(None, None, lse, ci, cc))
-            self.counters.count_fused("retrieve", rows * V * 4)
+            self.counters.count_fused("retrieve", nr * V * 4)
             _abi.call("fq_hars_select", logits.data_ptr(), logits.stride(0), lse.data_ptr(),
-                      ci.data_ptr(), ci.stride(0), cc.data_ptr(), st.c, batch, K, V,
+                      ci.data_ptr(), ci.stride(0), cc.data_ptr(), st.c, nb, K, V,
                       self.config.max_seq_len, cfg.eos_token, _abi.ptr(lp),
                       cache.d_cur.data_ptr(), max_steps, step.tokens.data_ptr(),
                       parents.data_ptr(), cache.hist.data_ptr(), None, 0, stream)
             _abi.call("fq_step_advance", cache.d_cur.data_ptr(), stream)
 
+        def body_all():
+            if ngroups == 1:
+                body(groups[0])
+                return
+            main = torch.cuda.current_stream()
+            side = self._side_stream
+            side.wait_stream(main)
+            body(groups[0])
+            with torch.cuda.stream(side):
+                body(groups[1])
+            main.wait_stream(side)
+
         key = (batch, seq, K, max_steps, mask is not None, exhaustive, cfg.eos_token,
-               float(cfg.length_penalty))
+               float(cfg.length_penalty), ngroups)
         graph = None
         if self.use_graphs:
             entry = self._graphs.get(key)
@@ -180,7 +241,7 @@ class Session:
                 graph = torch.cuda.CUDAGraph()
                 n0 = _abi.launch_count()
                 with torch.cuda.graph(graph):
-                    body()
+                    body_all()
                 entry = (graph, _abi.launch_count() - n0)
                 _abi.add_launches(-entry[1])  # captured, not launched
                 self._graphs[key] = entry
@@ -192,21 +253,23 @@ class Session:
                 graph.replay()
                 _abi.add_launches(per_step)
             else:
-                body()
-            pinned[t:t + 1].copy_(st.n_done, non_blocking=True)
+                body_all()
+            for g, gr in enumerate(groups):
+                pinned[t, g:g + 1].copy_(gr["st"].n_done, non_blocking=True)
             ev = torch.cuda.Event()
             ev.record()
             events.append(ev)
             if t >= 1:
                 events[t - 1].synchronize()
-                if int(pinned[t - 1]) >= batch:
+                if int(pinned[t - 1, :ngroups].sum()) >= batch:
                     break
+        result = groups[0]["st"] if ngroups == 1 else _GroupedBeamState([g["st"] for g in groups])
         if return_device_state:
-            return st
+            return result
         torch.cuda.synchronize()
-        if int(step.bad.item()):
+        if any(int(g["step"].bad.item()) for g in groups):
             raise FullMaskError("fully masked cross-attention row")
-        states = st.host_items()
+        states = result.host_items()
         return [[Hypothesis(tokens=s, score=sc) for s, sc in state.finalize(cfg)]
                 for state in states]
 

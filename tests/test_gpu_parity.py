@@ -257,6 +257,26 @@ def test_graph_and_eager_paths_identical(P):
         [[h.tokens for h in x] for x in s.generate(src, dc)]
 
 
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
+def test_two_group_overlap_identical(P, precision):
+    """streams=2 (two item groups decoded on two streams inside the step
+    graph) gives exactly the single-chain hypotheses and scores: every op is
+    per row or per item."""
+    cfg = P.ModelConfig(num_encoder_layers=2, num_decoder_layers=2, d_model=128, d_ff=256,
+                        num_heads=4, vocab_size=2000, max_batch=9, max_seq_len=20,
+                        max_beam_size=4)
+    w = P.make_random_weights(cfg, seed=3)
+    src = np.random.default_rng(5).integers(3, cfg.vocab_size, size=(9, 11))
+    lengths = [11, 7, 11, 3, 11, 11, 9, 11, 1]
+    dc = P.DecodeConfig(beam_size=4, max_steps=16, length_penalty=0.6)
+    a = P.Session(cfg, w, precision=precision, streams=1).generate(src, dc, src_lengths=lengths)
+    s2 = P.Session(cfg, w, precision=precision, streams=2)
+    for _ in range(2):  # capture, then replay
+        b = s2.generate(src, dc, src_lengths=lengths)
+        assert [[h.tokens for h in x] for x in a] == [[h.tokens for h in x] for x in b]
+        assert [[h.score for h in x] for x in a] == [[h.score for h in x] for x in b]
+
+
 def test_c1_transformer_base_exact_mode_token_identical(P):
     """BASELINE config 1 (Transformer-base, B=8, S=32, beam 4, 32 steps):
     token ids bit-exact against the reference CPU implementation."""
