@@ -567,46 +567,83 @@ __global__ void __launch_bounds__(kThreads, 1)
     float* c32 = reinterpret_cast<float*>(ep.c);
     __nv_bfloat16* c16 = reinterpret_cast<__nv_bfloat16*>(ep.c);
     const uint32_t part_s = smem_u32(part);
-    for (int idx = t; idx < rows * C4; idx += 128) {
-      const int lr = r_lo + idx / C4;
-      const int c = (idx % C4) * 4;
-      const int row = m0 + lr, col = n0 + c;
-      const uint32_t off = part_s + (uint32_t)(lr * PLD + c) * 4u;
-      float4 pv[8];  // all S remote partials in flight before the fixed-order sum
+    // Two output float4 per thread per pass; every remote partial and the
+    // residual / bias vectors of both are requested before the first use, so
+    // a pass costs one DSMEM + one global round trip, not one per element.
+    const bool vec_io = (ep.ldc % 4) == 0 && (!ep.res || (ep.ldr % 4) == 0) &&
+                        !ep.accumulate && (N % 4) == 0;
+    constexpr int U = 2;
+    for (int idx0 = t; idx0 < rows * C4; idx0 += U * 128) {
+      float4 pv[U][8];
+      float4 rv[U], bv[U];
 #pragma unroll
-      for (int p = 0; p < 8; ++p)
-        if (p < S) pv[p] = ld_dsmem_f4(off, p);
-      float4 a = pv[0];
+      for (int u = 0; u < U; ++u) {
+        const int idx = idx0 + u * 128;
+        rv[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+        bv[u] = rv[u];
+        if (idx >= rows * C4) continue;
+        const int lr = r_lo + idx / C4, c = (idx % C4) * 4;
+        const uint32_t off = part_s + (uint32_t)(lr * PLD + c) * 4u;
 #pragma unroll
-      for (int p = 1; p < 8; ++p)
-        if (p < S) { a.x += pv[p].x; a.y += pv[p].y; a.z += pv[p].z; a.w += pv[p].w; }
-      if (row >= M) continue;
-      float x[4] = {a.x, a.y, a.z, a.w};
-      const int64_t ci = (int64_t)row * ep.ldc + col;
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        if (col + j >= N) break;
-        float y = x[j];
-        if (ep.accumulate) y = fadd_rn(ep.c_bf16 ? bf2f(c16[ci + j]) : c32[ci + j], y);
-        if (ep.bias) y = fadd_rn(y, __ldg(ep.bias + col + j));
-        y = apply_act(y, ep.act);
-        if (ep.res) y = fadd_rn(y, __ldg(ep.res + (int64_t)row * ep.ldr + col + j));
-        x[j] = y;
-      }
-      if (col + 3 < N && ((ci & 3) == 0)) {
-        if (ep.c_bf16) {
-          __nv_bfloat162 lo = __floats2bfloat162_rn(x[0], x[1]), hi = __floats2bfloat162_rn(x[2], x[3]);
-          uint2 pk;
-          pk.x = *reinterpret_cast<uint32_t*>(&lo);
-          pk.y = *reinterpret_cast<uint32_t*>(&hi);
-          *reinterpret_cast<uint2*>(c16 + ci) = pk;
-        } else {
-          *reinterpret_cast<float4*>(c32 + ci) = make_float4(x[0], x[1], x[2], x[3]);
+        for (int p = 0; p < 8; ++p)
+          if (p < S) pv[u][p] = ld_dsmem_f4(off, p);
+        const int row = m0 + lr, col = n0 + c;
+        if (vec_io && row < M && col < N) {
+          if (ep.res) rv[u] = __ldg(reinterpret_cast<const float4*>(ep.res + (int64_t)row * ep.ldr + col));
+          if (ep.bias) bv[u] = __ldg(reinterpret_cast<const float4*>(ep.bias + col));
         }
-      } else {
-        for (int j = 0; j < 4 && col + j < N; ++j) {
-          if (ep.c_bf16) c16[ci + j] = f2bf(x[j]);
-          else c32[ci + j] = x[j];
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int idx = idx0 + u * 128;
+        if (idx >= rows * C4) continue;
+        const int lr = r_lo + idx / C4, c = (idx % C4) * 4;
+        const int row = m0 + lr, col = n0 + c;
+        float4 a = pv[u][0];
+#pragma unroll
+        for (int p = 1; p < 8; ++p)
+          if (p < S) { a.x += pv[u][p].x; a.y += pv[u][p].y; a.z += pv[u][p].z; a.w += pv[u][p].w; }
+        if (row >= M) continue;
+        float x[4] = {a.x, a.y, a.z, a.w};
+        const int64_t ci = (int64_t)row * ep.ldc + col;
+        if (vec_io) {
+          const float bb[4] = {bv[u].x, bv[u].y, bv[u].z, bv[u].w};
+          const float rr[4] = {rv[u].x, rv[u].y, rv[u].z, rv[u].w};
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            float y = x[j];
+            if (ep.bias) y = fadd_rn(y, bb[j]);
+            y = apply_act(y, ep.act);
+            if (ep.res) y = fadd_rn(y, rr[j]);
+            x[j] = y;
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            if (col + j >= N) break;
+            float y = x[j];
+            if (ep.accumulate) y = fadd_rn(ep.c_bf16 ? bf2f(c16[ci + j]) : c32[ci + j], y);
+            if (ep.bias) y = fadd_rn(y, __ldg(ep.bias + col + j));
+            y = apply_act(y, ep.act);
+            if (ep.res) y = fadd_rn(y, __ldg(ep.res + (int64_t)row * ep.ldr + col + j));
+            x[j] = y;
+          }
+        }
+        if (col + 3 < N && ((ci & 3) == 0)) {
+          if (ep.c_bf16) {
+            __nv_bfloat162 lo = __floats2bfloat162_rn(x[0], x[1]), hi = __floats2bfloat162_rn(x[2], x[3]);
+            uint2 pk;
+            pk.x = *reinterpret_cast<uint32_t*>(&lo);
+            pk.y = *reinterpret_cast<uint32_t*>(&hi);
+            *reinterpret_cast<uint2*>(c16 + ci) = pk;
+          } else {
+            *reinterpret_cast<float4*>(c32 + ci) = make_float4(x[0], x[1], x[2], x[3]);
+          }
+        } else {
+          for (int j = 0; j < 4 && col + j < N; ++j) {
+            if (ep.c_bf16) c16[ci + j] = f2bf(x[j]);
+            else c32[ci + j] = x[j];
+          }
         }
       }
     }
@@ -743,7 +780,7 @@ static int prep() {
 
 int gemm_tc_prepare() {
   if (tc::prep<256, 4>() || tc::prep<224, 4>() || tc::prep<192, 4>() || tc::prep<128, 6>() ||
-      tc::prep<64, 8>() || tc::prep<32, 8>() ||
+      tc::prep<64, 8>() || tc::prep<32, 8>() || tc::prep<32, 4>() || tc::prep<32, 2>() ||
       tc::prep_splitk<256, 4>() || tc::prep_splitk<128, 6>() || tc::prep_splitk<64, 8>()) {
     set_error("fq_prepare: tcgen05 GEMM smem opt-in failed");
     return FQ_ERR_CUDA;
@@ -793,8 +830,8 @@ static TcPlan plan_tc(int64_t M, int64_t N, int64_t K) {
     }
   }
   if (mt <= 8) {
-    if (N <= 1024 && nkb >= 32 && mt * nt128 * 4 <= tc::num_sms())
-      return {128, 1, 1, 4};                       // K=4096: split-K over 4 CTAs
+    if (N <= 1024 && nkb >= 16 && mt * nt128 * 4 <= tc::num_sms())
+      return {128, 1, 1, 4};                       // K >= 1024: split-K over 4 CTAs
     if (N <= 1024) return {32, 1, 1, 1};
     if (N < 8192) return {128, 1, 1, 1};
   }
@@ -833,7 +870,16 @@ int launch_tc_gemm(const void* a, int64_t lda, const void* b, int64_t ldb, void*
     case 192: return tc::launch<192, 4>(a, lda, b, ldb, ep, M, N, K, p.cm, p.cn, s);
     case 128: return tc::launch<128, 6>(a, lda, b, ldb, ep, M, N, K, p.cm, p.cn, s);
     case 64: return tc::launch<64, 8>(a, lda, b, ldb, ep, M, N, K, p.cm, p.cn, s);
-    default: return tc::launch<32, 8>(a, lda, b, ldb, ep, M, N, K, p.cm, p.cn, s);
+    default: {
+      static int st32 = -1;  // experiment hook: FQ_STAGES32 = 2 | 4 | 8
+      if (st32 < 0) {
+        const char* e = getenv("FQ_STAGES32");
+        st32 = e ? atoi(e) : 8;
+      }
+      if (st32 == 2) return tc::launch<32, 2>(a, lda, b, ldb, ep, M, N, K, p.cm, p.cn, s);
+      if (st32 == 4) return tc::launch<32, 4>(a, lda, b, ldb, ep, M, N, K, p.cm, p.cn, s);
+      return tc::launch<32, 8>(a, lda, b, ldb, ep, M, N, K, p.cm, p.cn, s);
+    }
   }
 }
 
