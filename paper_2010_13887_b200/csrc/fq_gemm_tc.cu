@@ -833,7 +833,19 @@ static TcPlan plan_tc(int64_t M, int64_t N, int64_t K) {
     if (N <= 1024 && nkb >= 16 && mt * nt128 * 4 <= tc::num_sms())
       return {128, 1, 1, 4};                       // K >= 1024: split-K over 4 CTAs
     if (N <= 1024) return {32, 1, 1, 1};
-    if (N < 8192) return {128, 1, 1, 1};
+    if (N < 8192) {
+      static int ov_bn = -1, ov_sp = 1;  // experiment hook: FQ_PLAN_MIDN="bn,split"
+      if (ov_bn < 0) {
+        ov_bn = 0;
+        if (const char* e = getenv("FQ_PLAN_MIDN")) sscanf(e, "%d,%d", &ov_bn, &ov_sp);
+      }
+      if (ov_bn > 0) {
+        const int64_t nt = (N + ov_bn - 1) / ov_bn;
+        if (ov_sp == 1 || (mt * nt * ov_sp <= tc::num_sms() && ov_sp <= nkb))
+          return {ov_bn, 1, 1, ov_sp};
+      }
+      return {128, 1, 1, 1};
+    }
   }
   // Large GEMMs are tensor-bound: pick the tile width minimising the busiest
   // CTA's work, ceil(tiles / SMs) * BN (wave quantisation over 148 SMs).

@@ -17,6 +17,8 @@
 // order is (-score, token, beam), exactly the reference's sort key.
 #include <stdlib.h>
 
+#include <algorithm>
+
 #include "fq_common.cuh"
 
 namespace fq {
@@ -234,24 +236,79 @@ __global__ void __launch_bounds__(kRetrieveThreads, 4) retrieve_kernel(
 //     rescan of the row from L2.
 // ---------------------------------------------------------------------------
 constexpr int kSwThreads = 256;
-constexpr int kSwU = 4;
+__device__ unsigned long long* g_sw_dbg = nullptr;  // phase stamps (profiling only)
+__device__ __forceinline__ void sw_stamp(int64_t row, int slot) {
+  if (g_sw_dbg && threadIdx.x == 0) {
+    unsigned long long t_;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
+    g_sw_dbg[row * 8 + slot] = t_;
+  }
+}
+constexpr int kSwU = 4;   // pilot vectors per thread
+constexpr int kSwP = 8;   // async ring depth (vectors in flight per thread)
+// CTAs (cluster) per row. 2 balances rows over SMs but needs 7 resident CTAs
+// per SM for one wave, which the ring + survivor smem does not allow: measured
+// slower (two waves), so one CTA per row.
+constexpr int kSwSplit = 1;
 constexpr int kSurvCap = 2048;
 
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                   static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
+               "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// ring: kSwP x kSwThreads float4 of dynamic shared memory (per-thread slots:
+// each thread only ever reads back its own async copies, so the ring needs no
+// block barrier, only per-thread cp.async groups).
+__device__ __forceinline__ uint32_t cl_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t cl_nrank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cl_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+template <typename T>
+__device__ __forceinline__ T* peer_ptr(T* p, int rank) {
+  return reinterpret_cast<T*>(__cluster_map_shared_rank(reinterpret_cast<void*>(p), rank));
+}
+
+// C CTAs (a thread-block cluster, C = 1 or 2) share one row: rank r sweeps the
+// vector iterations [r*I0, (r+1)*I0) (I0 a multiple-free split of the per-thread
+// iteration count, so the strided group mapping is unchanged); group maxima,
+// the logsumexp partial and the survivor counts are exchanged through
+// distributed shared memory. Half rows balance the 512 decode rows over 148
+// SMs (a row per CTA leaves a 4-vs-3 rows-per-SM tail).
 __device__ __forceinline__ void sweep_row(
     const float* __restrict__ logits, int64_t ld, int V, const int64_t row, const int k,
     float* __restrict__ group_max, int64_t gm_ld, float* __restrict__ threshold,
     double* __restrict__ lse, int32_t* __restrict__ cand_idx, int64_t cand_ld,
-    int64_t* __restrict__ cand_count) {
+    int64_t* __restrict__ cand_count, float4* __restrict__ ring, const int C, const int rank) {
   __shared__ float part_max[kSwThreads * 4];
   __shared__ int32_t sv_idx[kSurvCap];
   __shared__ float sv_val[kSurvCap];
   __shared__ float gmax_s[32];
   __shared__ float s_R, s_M;
   __shared__ double red[kSwThreads / 32];
+  __shared__ double s_S;
   __shared__ int warp_tot[32];
   __shared__ int s_cnt, s_total, s_n, s_ovf;
-  if (k <= 0) {
-    if (threadIdx.x == 0) cand_count[row] = 0;
+  if (k <= 0) {  // uniform across the cluster
+    if (threadIdx.x == 0 && rank == 0) cand_count[row] = 0;
     return;
   }
   const float* x = logits + row * ld;
@@ -262,19 +319,29 @@ __device__ __forceinline__ void sweep_row(
   const float4* x4 = reinterpret_cast<const float4*>(x);
   const bool act = tid < T;
   constexpr float NEG = -INFINITY;
-  float4 q[kSwU];
+  const int itmax = (nvec + T - 1) / T;      // iterations of thread 0
+  const int I0 = (itmax + C - 1) / C;
+  const int i_lo = rank * I0;
+  const int nit_thr = act && tid < nvec ? (nvec - tid + T - 1) / T : 0;
+  const int nit = max(0, min(nit_thr, i_lo + I0) - i_lo);  // this CTA's iterations
+  const float4* xb = x4 + tid + (int64_t)i_lo * T;
+  // async prologue: this thread's first kSwP vectors in flight at once
 #pragma unroll
-  for (int u = 0; u < kSwU; ++u) {
-    const int v = tid + u * T;
-    q[u] = (act && v < nvec) ? __ldcs(x4 + v) : make_float4(NEG, NEG, NEG, NEG);
+  for (int i = 0; i < kSwP; ++i) {
+    if (i < nit) cp_async16(ring + i * kSwThreads + tid, xb + i * T);
+    cp_async_commit();
   }
   if (tid == 0) { s_cnt = 0; s_ovf = 0; }
-  // ---- pilot: partial group maxima -> R' (lower bound of R), M' ----
+  // ---- pilot (first kSwU vectors): partial group maxima -> R' <= R, M' ----
   float gm[4] = {NEG, NEG, NEG, NEG};
+  cp_async_wait<kSwP - kSwU>();
 #pragma unroll
   for (int u = 0; u < kSwU; ++u) {
-    gm[0] = fmaxf(gm[0], q[u].x); gm[1] = fmaxf(gm[1], q[u].y);
-    gm[2] = fmaxf(gm[2], q[u].z); gm[3] = fmaxf(gm[3], q[u].w);
+    if (u < nit) {
+      const float4 e = ring[u * kSwThreads + tid];
+      gm[0] = fmaxf(gm[0], e.x); gm[1] = fmaxf(gm[1], e.y);
+      gm[2] = fmaxf(gm[2], e.z); gm[3] = fmaxf(gm[3], e.w);
+    }
   }
   if (act) {
     part_max[4 * tid] = gm[0]; part_max[4 * tid + 1] = gm[1];
@@ -288,14 +355,15 @@ __device__ __forceinline__ void sweep_row(
     if (lane == 0) gmax_s[g] = mm;
   }
   __syncthreads();
-  if (tid == 0) {
-    float R = gmax_s[0], M = gmax_s[0];
-    for (int g = 1; g < k; ++g) { R = fminf(R, gmax_s[g]); M = fmaxf(M, gmax_s[g]); }
-    s_R = R;
-    s_M = M;
+  if (w == 0) {
+    const float gv = lane < k ? gmax_s[lane] : INFINITY;
+    const float R = warp_min(gv);
+    const float M = warp_max(lane < k ? gv : NEG);
+    if (lane == 0) { s_R = R; s_M = M; }
   }
   __syncthreads();
   const float Rp = s_R;  // may be -inf (group without pilot elements): everything survives
+  sw_stamp(row, 1);
   float m = s_M;
   double s = 0.0;
   auto visit4 = [&](const float4& e, int v) {
@@ -319,32 +387,26 @@ __device__ __forceinline__ void sweep_row(
       }
     }
   };
-#pragma unroll
-  for (int u = 0; u < kSwU; ++u) {
-    const int v = tid + u * T;
-    if (act && v < nvec) visit4(q[u], v);
-  }
-  if (act) {
-    for (int v0 = tid + kSwU * T; v0 < nvec; v0 += kSwU * T) {
-#pragma unroll
-      for (int u = 0; u < kSwU; ++u) {
-        const int v = v0 + u * T;
-        q[u] = v < nvec ? __ldcs(x4 + v) : make_float4(NEG, NEG, NEG, NEG);
-      }
-#pragma unroll
-      for (int u = 0; u < kSwU; ++u) {
-        const int v = v0 + u * T;
-        if (v < nvec) {
-          gm[0] = fmaxf(gm[0], q[u].x); gm[1] = fmaxf(gm[1], q[u].y);
-          gm[2] = fmaxf(gm[2], q[u].z); gm[3] = fmaxf(gm[3], q[u].w);
-          visit4(q[u], v);
-        }
-      }
+  // ---- sweep: consume slot i, refill it with vector i + kSwP ----
+  for (int i = 0; i < nit; ++i) {
+    cp_async_wait<kSwP - 1>();
+    float4* slot = ring + (i % kSwP) * kSwThreads + tid;
+    const float4 e = *slot;
+    if (i + kSwP < nit) cp_async16(slot, xb + (i + kSwP) * T);
+    cp_async_commit();
+    if (i >= kSwU) {
+      gm[0] = fmaxf(gm[0], e.x); gm[1] = fmaxf(gm[1], e.y);
+      gm[2] = fmaxf(gm[2], e.z); gm[3] = fmaxf(gm[3], e.w);
     }
+    visit4(e, tid + (i_lo + i) * T);
+  }
+  cp_async_wait<0>();
+  sw_stamp(row, 2);
+  if (act) {
     part_max[4 * tid] = gm[0]; part_max[4 * tid + 1] = gm[1];
     part_max[4 * tid + 2] = gm[2]; part_max[4 * tid + 3] = gm[3];
   }
-  if (tid == 0) {  // V % 4 tail (visited scalar-wise; folded into its groups below)
+  if (tid == 0 && rank == C - 1) {  // V % 4 tail (the last rank)
     for (int j = nvec << 2; j < V; ++j) {
       const float xv = x[j];
       if (xv > m) { s = m == NEG ? 0.0 : s * exp((double)m - (double)xv); m = xv; }
@@ -363,51 +425,63 @@ __device__ __forceinline__ void sweep_row(
     if (lane == 0) gmax_s[g] = mm;
   }
   __syncthreads();
-  if (tid == 0) {
+  if (tid == 0 && rank == C - 1)
     for (int j = nvec << 2; j < V; ++j) gmax_s[j % k] = fmaxf(gmax_s[j % k], x[j]);
-    float R = gmax_s[0], M = gmax_s[0];
-    for (int g = 0; g < k; ++g) {
-      R = fminf(R, gmax_s[g]);
-      M = fmaxf(M, gmax_s[g]);
-      if (group_max) group_max[row * gm_ld + g] = gmax_s[g];
+  if (C > 1) cl_sync_all();  // both halves' group maxima complete
+  if (w == 0) {
+    float gv = NEG;
+    if (lane < k) {
+      gv = gmax_s[lane];
+      for (int r2 = 0; r2 < C; ++r2)
+        if (r2 != rank) gv = fmaxf(gv, *peer_ptr(&gmax_s[lane], r2));
+      if (rank == 0 && group_max) group_max[row * gm_ld + lane] = gv;
     }
-    s_R = R;
-    s_M = M;
+    const float R = warp_min(lane < k ? gv : INFINITY);
+    const float M = warp_max(gv);
+    if (lane == 0) { s_R = R; s_M = M; }
   }
   __syncthreads();
   const float R = s_R, M = s_M;
   const double st = m == NEG ? 0.0 : s * exp((double)m - (double)M);
-  const double S = block_sum(st, red);  // contains __syncthreads
+  const double Sl = block_sum(st, red);  // contains __syncthreads
+  sw_stamp(row, 3);
   const int nsv = s_cnt;
   int32_t* out_idx = cand_idx + row * cand_ld;
+  // survivors >= R of this CTA, compacted, then ranked by token below
+  if (tid == 0) { s_n = 0; s_S = Sl; }
+  __syncthreads();
   if (nsv <= kSurvCap) {
-    // keep survivors >= R, compacted in place order-free, then rank by token
-    if (tid == 0) s_n = 0;
-    __syncthreads();
     for (int i = tid; i < nsv; i += kSwThreads) {
       const float v = sv_val[i];
       const int j = sv_idx[i];
       if (v >= R) part_max[atomicAdd(&s_n, 1)] = __int_as_float(j);
     }
-    __syncthreads();
-    const int n = s_n;
-    if (n <= kSwThreads * 4) {
-      for (int i = tid; i < n; i += kSwThreads) {
-        const int j = __float_as_int(part_max[i]);
-        int rk = 0;
-        for (int q2 = 0; q2 < n; ++q2) rk += __float_as_int(part_max[q2]) < j ? 1 : 0;
-        if (rk < cand_ld) out_idx[rk] = j;
-      }
-      if (tid == 0) cand_count[row] = n;
-    } else {
-      if (tid == 0) s_ovf = 1;
-    }
   }
   __syncthreads();
-  if (nsv > kSurvCap || s_ovf) {
-    // ordered block-scan compaction over the row (re-read from L2)
-    __syncthreads();
-    int64_t base = 0;
+  if (tid == 0) s_ovf = (nsv > kSurvCap || s_n > kSwThreads * 4) ? 1 : 0;
+  if (C > 1) cl_sync_all();  // counts, overflow flags and partial sums visible
+  else __syncthreads();
+  int ovf = 0, base = 0, total = 0;
+  double S = 0.0;
+  for (int r2 = 0; r2 < C; ++r2) {
+    const int n2 = r2 == rank ? s_n : *peer_ptr(&s_n, r2);
+    ovf |= r2 == rank ? s_ovf : *peer_ptr(&s_ovf, r2);
+    if (r2 < rank) base += n2;
+    total += n2;
+    S += r2 == rank ? s_S : *peer_ptr(&s_S, r2);  // fixed rank order
+  }
+  if (!ovf) {
+    const int n = s_n;
+    for (int i = tid; i < n; i += kSwThreads) {
+      const int j = __float_as_int(part_max[i]);
+      int rk = 0;
+      for (int q2 = 0; q2 < n; ++q2) rk += __float_as_int(part_max[q2]) < j ? 1 : 0;
+      if (base + rk < cand_ld) out_idx[base + rk] = j;
+    }
+    if (tid == 0 && rank == 0) cand_count[row] = total;
+  } else if (rank == 0) {
+    // ordered block-scan compaction over the whole row (tie-heavy rows)
+    int64_t cb = 0;
     const int chunk = kSwThreads * 4;
     for (int c0 = 0; c0 < V; c0 += chunk) {
       int flags = 0;
@@ -421,20 +495,22 @@ __device__ __forceinline__ void sweep_row(
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         if (flags & (1 << c)) {
-          const int64_t pos = base + off;
+          const int64_t pos = cb + off;
           if (pos < cand_ld) out_idx[pos] = c0 + tid * 4 + c;
           ++off;
         }
       }
-      base += s_total;
+      cb += s_total;
       __syncthreads();
     }
-    if (tid == 0) cand_count[row] = base;
+    if (tid == 0) cand_count[row] = cb;
   }
-  if (tid == 0) {
+  if (tid == 0 && rank == 0) {
     if (threshold) threshold[row] = R;
     lse[row] = (double)M + log(S);
+    sw_stamp(row, 4);
   }
+  if (C > 1) cl_sync_all();  // peers done reading my shared memory
 }
 
 __global__ void __launch_bounds__(kSwThreads, 4) retrieve_sweep_kernel(
@@ -443,9 +519,12 @@ __global__ void __launch_bounds__(kSwThreads, 4) retrieve_sweep_kernel(
     float* __restrict__ threshold, double* __restrict__ lse, int32_t* __restrict__ cand_idx,
     int64_t cand_ld, int64_t* __restrict__ cand_count) {
   pdl_enter();
-  const int64_t row = blockIdx.x;
+  extern __shared__ __align__(16) float4 sw_ring[];
+  const int C = (int)cl_nrank(), rank = (int)cl_rank();
+  const int64_t row = blockIdx.x / C;
+  if (rank == 0) sw_stamp(row, 0);
   sweep_row(logits, ld, V, row, d_k ? d_k[row] : k_fixed, group_max, gm_ld, threshold, lse,
-            cand_idx, cand_ld, cand_count);
+            cand_idx, cand_ld, cand_count, sw_ring, C, rank);
 }
 
 // ---------------------------------------------------------------------------
@@ -483,8 +562,10 @@ __device__ __forceinline__ void select_item(
     const int32_t* cand_idx, int64_t cand_ld, const int64_t* cand_count, fq_beam_state st, int K,
     int max_len, int eos, const double* __restrict__ len_pow, const int32_t* __restrict__ d_cur,
     int64_t max_steps, int64_t* row_tokens, int64_t* row_parents, int32_t* hist) {
-  extern __shared__ int32_t sh[];  // old prefixes [K][max_len] then old hist [K][max_len]
-  __shared__ Cand cands[kSelCap];
+  // dynamic smem: old prefixes [K][max_len], old hist [K][max_len], then the
+  // candidate array (16-byte aligned)
+  extern __shared__ int32_t sh[];
+  Cand* cands = reinterpret_cast<Cand*>(sh + ((2 * K * max_len + 3) & ~3));
   __shared__ Cand picks[2 * kMaxBeam];
   __shared__ int64_t offs[kMaxBeam + 1];
   __shared__ int s_new_live, s_done, s_npick;
@@ -711,17 +792,20 @@ __global__ void __launch_bounds__(kSwThreads) hars_step_kernel(
     double* lse, int32_t* cand_idx, int64_t cand_ld, int64_t* cand_count, int* item_cnt,
     int* all_cnt, int64_t* row_tokens, int64_t* row_parents, int32_t* hist) {
   pdl_enter();
-  const int64_t row = blockIdx.x;
+  const int C = (int)cl_nrank(), rank = (int)cl_rank();
+  const int64_t row = blockIdx.x / C;
   const int b = (int)(row / K), i = (int)(row % K);
   const int live = st.live[b];
   const int k = (!st.done[b] && i < live) ? min(K + live, V) : 0;  // hars_groups
-  sweep_row(logits, ld, V, row, k, nullptr, 0, nullptr, lse, cand_idx, cand_ld, cand_count);
+  extern __shared__ __align__(16) float4 sw_ring[];  // aliases stage 2's dynamic smem
+  sweep_row(logits, ld, V, row, k, nullptr, 0, nullptr, lse, cand_idx, cand_ld, cand_count,
+            sw_ring, C, rank);
   __shared__ int s_last;
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
     const int prev = atomicAdd(item_cnt + b, 1);
-    s_last = prev == K - 1;
+    s_last = prev == K * C - 1;  // every CTA of the item's rows has arrived
     if (s_last) item_cnt[b] = 0;
   }
   __syncthreads();
@@ -777,6 +861,10 @@ using namespace fq;
 
 extern "C" {
 
+static size_t sel_smem(int64_t beam, int64_t max_len) {
+  return (size_t)((2 * beam * max_len + 3) & ~3) * sizeof(int32_t) + kSelCap * sizeof(Cand);
+}
+
 // FQ_RETRIEVE_TWO_PASS=1 selects the two-pass kernel for every k (A/B runs).
 static bool retrieve_two_pass_forced() {
   static int v = -1;
@@ -785,6 +873,10 @@ static bool retrieve_two_pass_forced() {
     v = (e && e[0] == '1') ? 1 : 0;
   }
   return v == 1;
+}
+
+extern "C" int fq_retrieve_debug_timestamps(unsigned long long* p) {
+  return cudaMemcpyToSymbol(g_sw_dbg, &p, sizeof(p)) == cudaSuccess ? FQ_OK : FQ_ERR_CUDA;
 }
 
 int fq_retrieve(const float* logits, int64_t ld, int64_t rows, int64_t vocab, int64_t k,
@@ -801,7 +893,9 @@ int fq_retrieve(const float* logits, int64_t ld, int64_t rows, int64_t vocab, in
   if (rows == 0) return FQ_OK;
   if (k >= 1 && k <= 32 && (ld % 4) == 0 && ((uintptr_t)logits & 15) == 0 &&
       !retrieve_two_pass_forced()) {
-    launch_kernel(retrieve_sweep_kernel, (unsigned)rows, kSwThreads, 0, as_stream(stream), 1u,
+    launch_kernel(retrieve_sweep_kernel, (unsigned)(rows * kSwSplit), kSwThreads,
+                  (size_t)kSwP * kSwThreads * sizeof(float4), as_stream(stream),
+                  (unsigned)kSwSplit,
                   logits, ld, (int)vocab, (int)k, d_k, group_max, gm_ld, threshold, lse,
                   cand_idx, cand_ld, cand_count);
     return launch_status("fq_retrieve");
@@ -826,7 +920,7 @@ int fq_hars_select(const float* logits, int64_t ld, const double* lse, const int
   FQ_CHECK_ARG(cand_ld >= vocab, FQ_ERR_DIMENSION,
                "fq_hars_select needs full candidate rows (cand_ld >= vocab)");
   FQ_CHECK_ARG(eos >= 0 && eos < vocab, FQ_ERR_PARAMETER, "eos token outside vocabulary");
-  size_t smem = (size_t)2 * beam * max_len * sizeof(int32_t);
+  size_t smem = sel_smem(beam, max_len);
   FQ_CHECK_ARG(smem <= 160 * 1024, FQ_ERR_CAPACITY, "fq_hars_select: max_len too large");
   launch_kernel(hars_select_kernel, (unsigned)batch, kSelThreads, smem, as_stream(stream), 1u, 
       logits, ld, lse, cand_idx, cand_ld, cand_count, st, (int)beam, (int)max_len, (int)eos,
@@ -846,10 +940,11 @@ int fq_hars_step(const float* logits, int64_t ld, fq_beam_state st, int64_t batc
                FQ_ERR_PARAMETER, "fq_hars_step: needs 2*beam <= 32 and 16-byte aligned rows");
   FQ_CHECK_ARG(cand_ld >= vocab, FQ_ERR_DIMENSION, "fq_hars_step needs full candidate rows");
   FQ_CHECK_ARG(eos >= 0 && eos < vocab, FQ_ERR_PARAMETER, "eos token outside vocabulary");
-  const size_t smem = (size_t)2 * beam * max_len * sizeof(int32_t);
+  const size_t smem = std::max(sel_smem(beam, max_len),
+                               (size_t)kSwP * kSwThreads * sizeof(float4));
   FQ_CHECK_ARG(smem <= 96 * 1024, FQ_ERR_CAPACITY, "fq_hars_step: max_len too large");
-  launch_kernel(hars_step_kernel, (unsigned)(batch * beam), kSwThreads, smem, as_stream(stream),
-                1u, logits, ld, (int)vocab, st, (int)batch, (int)beam, (int)max_len, (int)eos,
+  launch_kernel(hars_step_kernel, (unsigned)(batch * beam * kSwSplit), kSwThreads, smem,
+                as_stream(stream), (unsigned)kSwSplit, logits, ld, (int)vocab, st, (int)batch, (int)beam, (int)max_len, (int)eos,
                 len_pow, d_cur, max_steps, lse, cand_idx, cand_ld, cand_count, counters,
                 counters + batch, row_tokens, row_parents, hist);
   return launch_status("fq_hars_step");
@@ -878,7 +973,9 @@ int fq_hars_prepare(void) {
   if (cudaFuncSetAttribute(hars_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            160 * 1024) != cudaSuccess ||
       cudaFuncSetAttribute(hars_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           96 * 1024) != cudaSuccess) {
+                           96 * 1024) != cudaSuccess ||
+      cudaFuncSetAttribute(retrieve_sweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           64 * 1024) != cudaSuccess) {
     set_error("fq_prepare: cannot opt in to large shared memory (hars)");
     return FQ_ERR_CUDA;
   }

@@ -15,10 +15,11 @@ lib.fq_gemm_debug_timestamps.argtypes = [ctypes.c_void_p]
 for M, N, K in [(512, 1024, 1024), (512, 4096, 1024), (512, 3072, 1024), (512, 1024, 4096),
                 (512, 32000, 1024)]:
     a = torch.randn(M, K, device="cuda").bfloat16()
-    bs = [torch.randn(N, K, device="cuda").bfloat16() for _ in range(4)]
+    nb = int(os.environ.get("NBUF", "4"))
+    bs = [torch.randn(N, K, device="cuda").bfloat16() for _ in range(nb)]
     c = torch.empty(M, N, device="cuda")
     dbg = torch.zeros(8 * 1024, dtype=torch.int64, device="cuda")
-    for i in range(4):
+    for i in range(nb):
         P.gemm(a, bs[i], c, transpose_b=True)
     torch.cuda.synchronize()
     lib.fq_gemm_debug_timestamps(dbg.data_ptr())
