@@ -17,6 +17,8 @@
 //
 // All three kernels are bandwidth/latency bound: head slices are staged with
 // 128-bit loads (8 bf16 or 4 fp32 per load), all issued before first use.
+#include <cuda.h>
+
 #include "fq_common.cuh"
 
 namespace fq {
@@ -990,6 +992,160 @@ __global__ void __launch_bounds__(32) cross_attention_mma(
   }
 }
 
+
+int make_tmap_bf16_sw128(CUtensorMap* map, const void* ptr, int64_t rows, int64_t cols,
+                         int64_t ld, int box_cols, int box_rows);
+
+// Cross-attention on warp MMAs, TMA variant (head_dim 64, seq <= 64): the K
+// and V head slices of (item, head) arrive as two 64x64 bf16 TMA boxes with
+// the 128-byte swizzle (no smem padding, conflict-free ldmatrix), and the
+// probabilities reuse the K buffer once the scores are done, so a CTA needs
+// 16 KB and all (item, head) CTAs are resident in one wave.
+__device__ __forceinline__ uint32_t sw128(int row, int chunk) {
+  return (uint32_t)(row * 128 + ((chunk ^ (row & 7)) << 4));
+}
+
+__global__ void __launch_bounds__(32) cross_attention_tma(
+    const __grid_constant__ CUtensorMap tk, const __grid_constant__ CUtensorMap tv,
+    const float* __restrict__ cq, int64_t ldcq, int beam, int seq, float scale,
+    const float* __restrict__ mask, float* __restrict__ out, __nv_bfloat16* __restrict__ out16,
+    int64_t ldo, int* d_bad) {
+  constexpr int HD = 64, NT = 4, NP = 64;
+  extern __shared__ __align__(1024) uint8_t smraw[];
+  uint8_t* Ks = smraw + ((1024u - (sm_u32(smraw) & 1023u)) & 1023u);
+  uint8_t* Vs = Ks + NP * 128;
+  float (*Ps)[NP + 4] = reinterpret_cast<float (*)[NP + 4]>(Ks);  // after the scores
+  __shared__ __align__(8) uint64_t bar;
+  const int b = blockIdx.x, h = blockIdx.y, lane = threadIdx.x;
+  const int g = lane >> 2, t4 = lane & 3;
+  if (lane == 0) {
+    bar_init(&bar, 1);
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tk)));
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tv)));
+  }
+  __syncwarp();
+  pdl_enter();
+  if (lane == 0) {
+    bar_expect(&bar, 2 * NP * 128);
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3}], [%4];" ::"r"(sm_u32(Ks)),
+        "l"(reinterpret_cast<uint64_t>(&tk)), "r"(h * HD), "r"(b * seq), "r"(sm_u32(&bar))
+        : "memory");
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3}], [%4];" ::"r"(sm_u32(Vs)),
+        "l"(reinterpret_cast<uint64_t>(&tv)), "r"(h * HD), "r"(b * seq), "r"(sm_u32(&bar))
+        : "memory");
+  }
+  uint32_t qh[HD / 16][2], ql[HD / 16][2];
+  {
+    const bool ok = g < beam;
+    const float* qp = cq + ((int64_t)b * beam + (ok ? g : 0)) * ldcq + h * HD;
+#pragma unroll
+    for (int kk = 0; kk < HD / 16; ++kk) {
+      float2 x0 = ok ? *reinterpret_cast<const float2*>(qp + 16 * kk + 2 * t4) : make_float2(0.f, 0.f);
+      float2 x1 = ok ? *reinterpret_cast<const float2*>(qp + 16 * kk + 2 * t4 + 8) : make_float2(0.f, 0.f);
+      split2(x0.x, x0.y, qh[kk][0], ql[kk][0]);
+      split2(x1.x, x1.y, qh[kk][1], ql[kk][1]);
+    }
+  }
+  bar_wait(&bar, 0);
+  float sc[NT][4];
+  const int lrow = (lane & 7) + ((lane >> 3) & 1) * 8, lch = lane >> 4;
+#pragma unroll
+  for (int m = 0; m < NT; ++m) {
+    sc[m][0] = sc[m][1] = sc[m][2] = sc[m][3] = 0.0f;
+#pragma unroll
+    for (int kk = 0; kk < HD / 16; ++kk) {
+      uint32_t a[4];
+      ldsm_x4(a, Ks + sw128(16 * m + lrow, 2 * kk + lch));
+      mma_bf16_16816(sc[m], a, qh[kk][0], qh[kk][1]);
+      mma_bf16_16816(sc[m], a, ql[kk][0], ql[kk][1]);
+    }
+  }
+  __syncwarp();  // K is dead: Ps may overwrite it
+  const float* mk = mask ? mask + (int64_t)b * seq : nullptr;
+  float mx0 = -INFINITY, mx1 = -INFINITY;
+#pragma unroll
+  for (int m = 0; m < NT; ++m) {
+#pragma unroll
+    for (int hh = 0; hh < 2; ++hh) {
+      const int p = 16 * m + g + 8 * hh;
+      const float add = p < seq ? (mk ? mk[p] : 0.0f) : -INFINITY;
+      sc[m][2 * hh] = fmaf(sc[m][2 * hh], scale, add);
+      sc[m][2 * hh + 1] = fmaf(sc[m][2 * hh + 1], scale, add);
+      mx0 = fmaxf(mx0, sc[m][2 * hh]);
+      mx1 = fmaxf(mx1, sc[m][2 * hh + 1]);
+    }
+  }
+#pragma unroll
+  for (int o = 4; o < 32; o <<= 1) {
+    mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, o));
+    mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, o));
+  }
+  float l0 = 0.0f, l1 = 0.0f;
+#pragma unroll
+  for (int m = 0; m < NT; ++m) {
+#pragma unroll
+    for (int hh = 0; hh < 2; ++hh) {
+      const float e0 = mx0 == -INFINITY ? 0.0f : __expf(sc[m][2 * hh] - mx0);
+      const float e1 = mx1 == -INFINITY ? 0.0f : __expf(sc[m][2 * hh + 1] - mx1);
+      l0 += e0;
+      l1 += e1;
+      const int p = 16 * m + g + 8 * hh;
+      Ps[2 * t4][p] = e0;
+      Ps[2 * t4 + 1][p] = e1;
+    }
+  }
+#pragma unroll
+  for (int o = 4; o < 32; o <<= 1) {
+    l0 += __shfl_xor_sync(0xffffffffu, l0, o);
+    l1 += __shfl_xor_sync(0xffffffffu, l1, o);
+  }
+  __syncwarp();
+  float oc[HD / 16][4];
+#pragma unroll
+  for (int m = 0; m < HD / 16; ++m) oc[m][0] = oc[m][1] = oc[m][2] = oc[m][3] = 0.0f;
+  const int mi = lane >> 3;
+  const int vrow = (lane & 7) + ((mi >> 1) & 1) * 8, vch = mi & 1;
+#pragma unroll
+  for (int kk = 0; kk < NT; ++kk) {
+    uint32_t bh0, bl0, bh1, bl1;
+    split2(Ps[g][16 * kk + 2 * t4], Ps[g][16 * kk + 2 * t4 + 1], bh0, bl0);
+    split2(Ps[g][16 * kk + 2 * t4 + 8], Ps[g][16 * kk + 2 * t4 + 9], bh1, bl1);
+#pragma unroll
+    for (int m = 0; m < HD / 16; ++m) {
+      uint32_t a[4];
+      ldsm_x4_t(a, Vs + sw128(16 * kk + vrow, 2 * m + vch));
+      mma_bf16_16816(oc[m], a, bh0, bh1);
+      mma_bf16_16816(oc[m], a, bl0, bl1);
+    }
+  }
+  const float inv0 = l0 > 0.0f ? 1.0f / l0 : 0.0f, inv1 = l1 > 0.0f ? 1.0f / l1 : 0.0f;
+  if (d_bad && g == 0) {
+    if (2 * t4 < beam && !(l0 > 0.0f)) atomicAdd(d_bad, 1);
+    if (2 * t4 + 1 < beam && !(l1 > 0.0f)) atomicAdd(d_bad, 1);
+  }
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    const int bi = 2 * t4 + j;
+    if (bi >= beam) continue;
+    const float inv = j ? inv1 : inv0;
+    const int64_t o = ((int64_t)b * beam + bi) * ldo + h * HD;
+#pragma unroll
+    for (int m = 0; m < HD / 16; ++m) {
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh) {
+        const int dd = 16 * m + g + 8 * hh;
+        const float v = oc[m][2 * hh + j] * inv;
+        if (out) out[o + dd] = v;
+        if (out16) out16[o + dd] = f2bf(v);
+      }
+    }
+  }
+}
+
 int attention_prepare() {
   const int big = 227 * 1024;
   if (cudaFuncSetAttribute(encoder_attention_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, big) ||
@@ -1137,6 +1293,20 @@ int fq_cross_attention(const float* cq, int64_t ldcq, const void* ck, const void
   FQ_CHECK_ARG(cq && ck && cv && (out || out16) && batch > 0 && beam > 0 && seq > 0 &&
                    heads > 0 && head_dim > 0 && head_dim <= 128,
                FQ_ERR_DIMENSION, "fq_cross_attention: bad args");
+  if (kv_dtype != FQ_F32 && !exact && head_dim == 64 && beam <= 8 && seq <= 64 &&
+      ldcq % 2 == 0 && ((uintptr_t)cq & 7) == 0 && ldkv % 8 == 0 && ((uintptr_t)ck & 15) == 0 &&
+      ((uintptr_t)cv & 15) == 0) {
+    CUtensorMap tk, tv;
+    const int64_t nrows = batch * seq, ncols = heads * head_dim;
+    if (make_tmap_bf16_sw128(&tk, ck, nrows, ncols, ldkv, 64, 64) == FQ_OK &&
+        make_tmap_bf16_sw128(&tv, cv, nrows, ncols, ldkv, 64, 64) == FQ_OK) {
+      launch_kernel(cross_attention_tma, dim3((unsigned)batch, (unsigned)heads), 32,
+                    (size_t)2 * 64 * 128 + 1024, as_stream(stream), 1u, tk, tv, cq, ldcq,
+                    (int)beam, (int)seq, scale, mask, out,
+                    reinterpret_cast<__nv_bfloat16*>(out16), ldo, d_bad);
+      return launch_status("fq_cross_attention");
+    }
+  }
   if (kv_dtype != FQ_F32 && !exact && (head_dim == 32 || head_dim == 64 || head_dim == 128) &&
       beam <= 8 && seq <= 64 && ldcq % 2 == 0 && ((uintptr_t)cq & 7) == 0 && ldkv % 8 == 0 &&
       ((uintptr_t)ck & 15) == 0 && ((uintptr_t)cv & 15) == 0) {

@@ -707,6 +707,34 @@ static int make_map(CUtensorMap* map, const void* ptr, int64_t rows, int64_t col
   return FQ_OK;
 }
 
+}  // namespace tc
+
+// 2D bf16 tensor map with 128-byte swizzle for other kernels (attention):
+// [rows, cols] row-major with leading dimension ld elements, box
+// [box_rows, box_cols] (box_cols * 2 == 128 bytes for the swizzle).
+int make_tmap_bf16_sw128(CUtensorMap* map, const void* ptr, int64_t rows, int64_t cols,
+                         int64_t ld, int box_cols, int box_rows) {
+  tc::EncodeFn enc = tc::get_encode();
+  if (!enc) {
+    set_error("cuTensorMapEncodeTiled unavailable");
+    return FQ_ERR_CUDA;
+  }
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * 2)};
+  cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled failed (%d)", (int)r);
+    return FQ_ERR_CUDA;
+  }
+  return FQ_OK;
+}
+
+namespace tc {
+
 static int num_sms() {
   static int n = 0;
   if (!n) {
