@@ -18,6 +18,7 @@
 // All three kernels are bandwidth/latency bound: head slices are staged with
 // 128-bit loads (8 bf16 or 4 fp32 per load), all issued before first use.
 #include <cuda.h>
+#include <stdlib.h>
 
 #include "fq_common.cuh"
 
@@ -1146,6 +1147,172 @@ __global__ void __launch_bounds__(32) cross_attention_tma(
   }
 }
 
+// Decoder self-attention on warp MMAs (bf16 cache, head_dim 64): warp per
+// (beam row, head). Cached positions stream through a 2-stage shared-memory
+// ring in chunks of 16 (cp.async 16-byte pieces of the hist-gathered slot rows,
+// 128-byte rows with an XOR chunk swizzle, so ldmatrix is conflict-free); this
+// step's K/V (position cur) are written to their cache slot and placed in the
+// ring from registers. Per chunk: S^T[16 pos x 8] = K . q^T on the tensor core
+// (column 0 is this row's query, fp32 split hi + lo), an online-softmax update,
+// and O^T[64 x 8] += V^T . p^T (p split hi + lo). The FMA formulation needs
+// ~16 instructions per cached element; this needs one MMA per 2048 MACs.
+__device__ __forceinline__ uint32_t swz(int row, int chunk) {
+  return (uint32_t)(row * 128 + ((chunk ^ (row & 7)) << 4));
+}
+
+__device__ __forceinline__ void cp16(uint32_t dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+
+__global__ void __launch_bounds__(32) decoder_self_attention_mma(
+    const float* __restrict__ sqkv, int64_t ldq, __nv_bfloat16* __restrict__ kc,
+    __nv_bfloat16* __restrict__ vc, const int32_t* __restrict__ hist,
+    const int32_t* __restrict__ d_cur, int rows, int heads, int max_len, float scale,
+    float* __restrict__ out, __nv_bfloat16* __restrict__ out16, int64_t ldo) {
+  constexpr int HD = 64;
+  __shared__ __align__(128) uint8_t ring[2][2][16 * 128];  // [stage][K|V][16 rows x 128 B]
+  __shared__ int phys_s[128];
+  pdl_enter();
+  const int r = blockIdx.x, h = blockIdx.y, lane = threadIdx.x;
+  const int g = lane >> 2, t4 = lane & 3;
+  const int d = heads * HD;
+  const int cur = *d_cur;
+  for (int t = lane; t < cur; t += 32) phys_s[t] = hist[(int64_t)r * max_len + t];
+  // this step's q, k, v (fp32 from the QKV GEMM); lane owns 2 dims for k/v
+  const float* rowp = sqkv + (int64_t)r * ldq + h * HD;
+  const float2 kn = *reinterpret_cast<const float2*>(rowp + d + 2 * lane);
+  const float2 vn = *reinterpret_cast<const float2*>(rowp + 2 * d + 2 * lane);
+  const __nv_bfloat162 kb2 = __floats2bfloat162_rn(kn.x, kn.y);
+  const __nv_bfloat162 vb2 = __floats2bfloat162_rn(vn.x, vn.y);
+  {
+    const int64_t slot = ((int64_t)cur * rows + r) * d + h * HD + 2 * lane;
+    *reinterpret_cast<__nv_bfloat162*>(kc + slot) = kb2;
+    *reinterpret_cast<__nv_bfloat162*>(vc + slot) = vb2;
+  }
+  // q^T fragments (column 0 = this row; other columns zero)
+  uint32_t qh[4][2], ql[4][2];
+#pragma unroll
+  for (int kk = 0; kk < 4; ++kk) {
+    float2 x0 = make_float2(0.f, 0.f), x1 = x0;
+    if (g == 0) {
+      x0 = *reinterpret_cast<const float2*>(rowp + 16 * kk + 2 * t4);
+      x1 = *reinterpret_cast<const float2*>(rowp + 16 * kk + 2 * t4 + 8);
+    }
+    split2(x0.x, x0.y, qh[kk][0], ql[kk][0]);
+    split2(x1.x, x1.y, qh[kk][1], ql[kk][1]);
+  }
+  __syncwarp();
+  const int npos = cur + 1;                 // positions 0..cur
+  const int nchunk = (npos + 15) / 16;
+  // issue chunk c into stage s: lane -> (16-byte chunk lane & 7, rows lane >> 3 + 4i)
+  auto issue = [&](int c, int s) {
+    const int ch = lane & 7;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int rr = (lane >> 3) + 4 * i;
+      const int t = 16 * c + rr;
+      const uint32_t kd = sm_u32(&ring[s][0][0]) + swz(rr, ch);
+      const uint32_t vd = sm_u32(&ring[s][1][0]) + swz(rr, ch);
+      if (t < cur) {
+        const int64_t off = ((int64_t)t * rows + phys_s[t]) * d + h * HD + ch * 8;
+        cp16(kd, kc + off);
+        cp16(vd, vc + off);
+      } else if (t > cur) {  // beyond the sequence: zeros (masked, 0 * 0)
+        *reinterpret_cast<uint4*>(&ring[s][0][0] + swz(rr, ch)) = make_uint4(0, 0, 0, 0);
+        *reinterpret_cast<uint4*>(&ring[s][1][0] + swz(rr, ch)) = make_uint4(0, 0, 0, 0);
+      }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  issue(0, 0);
+  if (nchunk > 1) issue(1, 1);
+  float m_run = -INFINITY, l_run = 0.0f;
+  float oc[4][4];
+#pragma unroll
+  for (int m = 0; m < 4; ++m) oc[m][0] = oc[m][1] = oc[m][2] = oc[m][3] = 0.0f;
+  const int lrow = (lane & 7) + ((lane >> 3) & 1) * 8, lch = lane >> 4;
+  const int mi = lane >> 3;
+  const int vrow = (lane & 7) + ((mi >> 1) & 1) * 8, vch = mi & 1;
+  for (int c = 0; c < nchunk; ++c) {
+    const int s = c & 1;
+    if (c + 1 < nchunk) asm volatile("cp.async.wait_group 1;" ::: "memory");
+    else asm volatile("cp.async.wait_group 0;" ::: "memory");
+    if (cur / 16 == c) {  // this step's k / v (row cur % 16) from registers
+      const int rr = cur % 16;
+      const int ch = (2 * lane) / 8, within = (2 * lane) % 8;
+      *reinterpret_cast<__nv_bfloat162*>(&ring[s][0][0] + swz(rr, ch) + within * 2) = kb2;
+      *reinterpret_cast<__nv_bfloat162*>(&ring[s][1][0] + swz(rr, ch) + within * 2) = vb2;
+    }
+    __syncwarp();
+    const uint8_t* Ks = &ring[s][0][0];
+    const uint8_t* Vs = &ring[s][1][0];
+    float sc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk) {
+      uint32_t a[4];
+      ldsm_x4(a, Ks + swz(lrow, 2 * kk + lch));
+      mma_bf16_16816(sc, a, qh[kk][0], qh[kk][1]);
+      mma_bf16_16816(sc, a, ql[kk][0], ql[kk][1]);
+    }
+    // column 0 lives in lanes with t4 == 0: positions 16c + g (sc[0]) and + 8 (sc[2])
+    const int p0 = 16 * c + g, p1 = p0 + 8;
+    const float s0 = p0 <= cur ? sc[0] * scale : -INFINITY;
+    const float s1 = p1 <= cur ? sc[2] * scale : -INFINITY;
+    float cm = fmaxf(s0, s1);
+#pragma unroll
+    for (int o = 4; o < 32; o <<= 1) cm = fmaxf(cm, __shfl_xor_sync(0xffffffffu, cm, o));
+    cm = __shfl_sync(0xffffffffu, cm, 0);
+    const float mn = fmaxf(m_run, cm);
+    const float corr = __expf(m_run - mn);  // m_run = -inf: 0
+    const float e0 = __expf(s0 - mn), e1 = __expf(s1 - mn);
+    float cs = e0 + e1;
+#pragma unroll
+    for (int o = 4; o < 32; o <<= 1) cs += __shfl_xor_sync(0xffffffffu, cs, o);
+    cs = __shfl_sync(0xffffffffu, cs, 0);
+    l_run = fmaf(l_run, corr, cs);
+    m_run = mn;
+    // p^T fragment: lanes 0-3 need positions 2t4, 2t4+1, 2t4+8, 2t4+9 of the chunk
+    const float pa = __shfl_sync(0xffffffffu, e0, 4 * (2 * t4));
+    const float pb = __shfl_sync(0xffffffffu, e0, 4 * (2 * t4 + 1));
+    const float pc = __shfl_sync(0xffffffffu, e1, 4 * (2 * t4));
+    const float pd = __shfl_sync(0xffffffffu, e1, 4 * (2 * t4 + 1));
+    uint32_t bh0, bl0, bh1, bl1;
+    split2(g == 0 ? pa : 0.f, g == 0 ? pb : 0.f, bh0, bl0);
+    split2(g == 0 ? pc : 0.f, g == 0 ? pd : 0.f, bh1, bl1);
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+      oc[m][0] *= corr; oc[m][1] *= corr; oc[m][2] *= corr; oc[m][3] *= corr;
+      uint32_t a[4];
+      ldsm_x4_t(a, Vs + swz(vrow, 2 * m + vch));
+      mma_bf16_16816(oc[m], a, bh0, bh1);
+      mma_bf16_16816(oc[m], a, bl0, bl1);
+    }
+    __syncwarp();  // stage s consumed
+    if (c + 2 < nchunk) issue(c + 2, s);
+  }
+  // column 0 of O^T: lanes t4 == 0 hold dims 16m + g (oc[m][0]) and 16m + g + 8 (oc[m][2])
+  if (t4 == 0) {
+    const float inv = 1.0f / l_run;
+    const int64_t o = (int64_t)r * ldo + h * HD;
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+      const float v0 = oc[m][0] * inv, v1 = oc[m][2] * inv;
+      if (out) { out[o + 16 * m + g] = v0; out[o + 16 * m + g + 8] = v1; }
+      if (out16) { out16[o + 16 * m + g] = f2bf(v0); out16[o + 16 * m + g + 8] = f2bf(v1); }
+    }
+  }
+}
+
+// FQ_SELF_MMA=0 selects the FMA row kernel (A/B runs).
+static bool mma_self_disabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("FQ_SELF_MMA");
+    v = (e && e[0] == '0') ? 1 : 0;
+  }
+  return v == 1;
+}
+
 int attention_prepare() {
   const int big = 227 * 1024;
   if (cudaFuncSetAttribute(encoder_attention_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, big) ||
@@ -1220,6 +1387,15 @@ int fq_decoder_self_attention(const float* sqkv, int64_t ldq, void* kcache, void
   FQ_CHECK_ARG(sqkv && kcache && vcache && hist && d_cur && (out || out16) && rows > 0 &&
                    heads > 0 && head_dim > 0 && head_dim <= 128 && max_len > 0,
                FQ_ERR_DIMENSION, "fq_decoder_self_attention: bad args");
+  if (kv_dtype != FQ_F32 && !exact && head_dim == 64 && max_len <= 128 && ldq % 2 == 0 &&
+      ((uintptr_t)sqkv & 7) == 0 && ((uintptr_t)kcache & 15) == 0 &&
+      ((uintptr_t)vcache & 15) == 0 && !mma_self_disabled()) {
+    launch_kernel(decoder_self_attention_mma, dim3((unsigned)rows, (unsigned)heads), 32, 0,
+                  as_stream(stream), 1u, sqkv, ldq, (__nv_bfloat16*)kcache,
+                  (__nv_bfloat16*)vcache, hist, d_cur, (int)rows, (int)heads, (int)max_len,
+                  scale, out, reinterpret_cast<__nv_bfloat16*>(out16), ldo);
+    return launch_status("fq_decoder_self_attention");
+  }
   {
     const int64_t d = heads * head_dim, tp = d / 8;
     const bool rows_ok = kv_dtype != FQ_F32 && !exact &&
