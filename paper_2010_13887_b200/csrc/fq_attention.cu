@@ -1164,13 +1164,14 @@ __device__ __forceinline__ void cp16(uint32_t dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
 }
 
+template <int NS>
 __global__ void __launch_bounds__(32) decoder_self_attention_mma(
     const float* __restrict__ sqkv, int64_t ldq, __nv_bfloat16* __restrict__ kc,
     __nv_bfloat16* __restrict__ vc, const int32_t* __restrict__ hist,
     const int32_t* __restrict__ d_cur, int rows, int heads, int max_len, float scale,
     float* __restrict__ out, __nv_bfloat16* __restrict__ out16, int64_t ldo) {
   constexpr int HD = 64;
-  __shared__ __align__(128) uint8_t ring[2][2][16 * 128];  // [stage][K|V][16 rows x 128 B]
+  __shared__ __align__(128) uint8_t ring[NS][2][16 * 128];  // [stage][K|V][16 rows x 128 B]
   __shared__ int phys_s[128];
   pdl_enter();
   const int r = blockIdx.x, h = blockIdx.y, lane = threadIdx.x;
@@ -1224,8 +1225,11 @@ __global__ void __launch_bounds__(32) decoder_self_attention_mma(
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
-  issue(0, 0);
-  if (nchunk > 1) issue(1, 1);
+#pragma unroll
+  for (int c = 0; c < NS - 1; ++c) {
+    if (c < nchunk) issue(c, c);
+    else asm volatile("cp.async.commit_group;" ::: "memory");
+  }
   float m_run = -INFINITY, l_run = 0.0f;
   float oc[4][4];
 #pragma unroll
@@ -1234,9 +1238,9 @@ __global__ void __launch_bounds__(32) decoder_self_attention_mma(
   const int mi = lane >> 3;
   const int vrow = (lane & 7) + ((mi >> 1) & 1) * 8, vch = mi & 1;
   for (int c = 0; c < nchunk; ++c) {
-    const int s = c & 1;
-    if (c + 1 < nchunk) asm volatile("cp.async.wait_group 1;" ::: "memory");
-    else asm volatile("cp.async.wait_group 0;" ::: "memory");
+    const int s = c % NS;
+    // NS - 1 groups were committed ahead of chunk c: wait for the oldest
+    asm volatile("cp.async.wait_group %0;" ::"n"(NS - 2) : "memory");
     if (cur / 16 == c) {  // this step's k / v (row cur % 16) from registers
       const int rr = cur % 16;
       const int ch = (2 * lane) / 8, within = (2 * lane) % 8;
@@ -1246,14 +1250,16 @@ __global__ void __launch_bounds__(32) decoder_self_attention_mma(
     __syncwarp();
     const uint8_t* Ks = &ring[s][0][0];
     const uint8_t* Vs = &ring[s][1][0];
-    float sc[4] = {0.f, 0.f, 0.f, 0.f};
+    float sc[4] = {0.f, 0.f, 0.f, 0.f}, sl[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-    for (int kk = 0; kk < 4; ++kk) {
+    for (int kk = 0; kk < 4; ++kk) {  // hi and lo products in separate chains
       uint32_t a[4];
       ldsm_x4(a, Ks + swz(lrow, 2 * kk + lch));
       mma_bf16_16816(sc, a, qh[kk][0], qh[kk][1]);
-      mma_bf16_16816(sc, a, ql[kk][0], ql[kk][1]);
+      mma_bf16_16816(sl, a, ql[kk][0], ql[kk][1]);
     }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) sc[j] += sl[j];
     // column 0 lives in lanes with t4 == 0: positions 16c + g (sc[0]) and + 8 (sc[2])
     const int p0 = 16 * c + g, p1 = p0 + 8;
     const float s0 = p0 <= cur ? sc[0] * scale : -INFINITY;
@@ -1288,7 +1294,8 @@ __global__ void __launch_bounds__(32) decoder_self_attention_mma(
       mma_bf16_16816(oc[m], a, bl0, bl1);
     }
     __syncwarp();  // stage s consumed
-    if (c + 2 < nchunk) issue(c + 2, s);
+    if (c + NS - 1 < nchunk) issue(c + NS - 1, (c + NS - 1) % NS);
+    else asm volatile("cp.async.commit_group;" ::: "memory");
   }
   // column 0 of O^T: lanes t4 == 0 hold dims 16m + g (oc[m][0]) and 16m + g + 8 (oc[m][2])
   if (t4 == 0) {
@@ -1390,7 +1397,14 @@ int fq_decoder_self_attention(const float* sqkv, int64_t ldq, void* kcache, void
   if (kv_dtype != FQ_F32 && !exact && head_dim == 64 && max_len <= 128 && ldq % 2 == 0 &&
       ((uintptr_t)sqkv & 7) == 0 && ((uintptr_t)kcache & 15) == 0 &&
       ((uintptr_t)vcache & 15) == 0 && !mma_self_disabled()) {
-    launch_kernel(decoder_self_attention_mma, dim3((unsigned)rows, (unsigned)heads), 32, 0,
+    static int ns = -1;  // ring depth (FQ_SELF_STAGES = 2 | 3 | 4)
+    if (ns < 0) {
+      const char* e = getenv("FQ_SELF_STAGES");
+      ns = e ? atoi(e) : 2;
+    }
+    auto kern = ns == 2 ? decoder_self_attention_mma<2>
+              : ns == 4 ? decoder_self_attention_mma<4> : decoder_self_attention_mma<3>;
+    launch_kernel(kern, dim3((unsigned)rows, (unsigned)heads), 32, 0,
                   as_stream(stream), 1u, sqkv, ldq, (__nv_bfloat16*)kcache,
                   (__nv_bfloat16*)vcache, hist, d_cur, (int)rows, (int)heads, (int)max_len,
                   scale, out, reinterpret_cast<__nv_bfloat16*>(out16), ldo);
