@@ -1310,6 +1310,150 @@ __global__ void __launch_bounds__(32) decoder_self_attention_mma(
   }
 }
 
+// Encoder self-attention on warp MMAs (throughput mode, head_dim 64, seq <= 64):
+// CTA per (item, head), warp per 16 queries. Q, K, V (fp32 from the QKV GEMM)
+// are split into bf16 hi + lo halves in XOR-swizzled shared memory; scores
+// S = Q K^T take three MMA products (hi.hi + hi.lo + lo.hi), the softmax runs
+// on the accumulator fragments (FlashAttention-2 register layout), and P V
+// reuses the probability fragments as A operands (P and V split likewise).
+__global__ void __launch_bounds__(128) encoder_attention_mma(
+    const float* __restrict__ qkv, int64_t ldq, int seq, int heads, float scale,
+    const float* __restrict__ mask, float* __restrict__ out, __nv_bfloat16* __restrict__ out16,
+    int64_t ldo, int* d_bad) {
+  constexpr int HD = 64, NP = 64;
+  __shared__ __align__(128) uint8_t sm[6][NP * 128];  // Qh Ql Kh Kl Vh Vl, rows of 128 B
+  pdl_enter();
+  const int b = blockIdx.x / heads, h = blockIdx.x % heads;
+  const int d = heads * HD;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int g = lane >> 2, t4 = lane & 3;
+  // load + split: 64 rows x 16 float4 per tensor; thread -> (row, float4)
+  for (int x = tid; x < 3 * NP * (HD / 4); x += 128) {
+    const int tsr = x / (NP * (HD / 4)), rem = x % (NP * (HD / 4));
+    const int row = rem / (HD / 4), c4 = rem % (HD / 4);
+    float4 f = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (row < seq)
+      f = *reinterpret_cast<const float4*>(qkv + ((int64_t)b * seq + row) * ldq + tsr * d +
+                                           h * HD + 4 * c4);
+    uint32_t h0, l0, h1, l1;
+    split2(f.x, f.y, h0, l0);
+    split2(f.z, f.w, h1, l1);
+    // element offset 4*c4 -> byte 8*c4 within the 128-byte row: chunk c4/2, half c4&1
+    const uint32_t off = (uint32_t)(row * 128 + (((c4 >> 1) ^ (row & 7)) << 4) + (c4 & 1) * 8);
+    *reinterpret_cast<uint2*>(&sm[2 * tsr][0] + off) = make_uint2(h0, h1);
+    *reinterpret_cast<uint2*>(&sm[2 * tsr + 1][0] + off) = make_uint2(l0, l1);
+  }
+  __syncthreads();
+  const int q0 = 16 * w;  // this warp's queries
+  const int lrow = (lane & 7) + ((lane >> 3) & 1) * 8, lch = lane >> 4;
+  // scores: 8 key tiles x 4 k-steps, three products
+  float sc[8][4];
+#pragma unroll
+  for (int n = 0; n < 8; ++n) sc[n][0] = sc[n][1] = sc[n][2] = sc[n][3] = 0.0f;
+#pragma unroll
+  for (int kk = 0; kk < 4; ++kk) {
+    uint32_t qa[4], qb[4];
+    ldsm_x4(qa, &sm[0][0] + swz(q0 + lrow, 2 * kk + lch));
+    ldsm_x4(qb, &sm[1][0] + swz(q0 + lrow, 2 * kk + lch));
+#pragma unroll
+    for (int n = 0; n < 8; ++n) {
+      // B = K^T: keys 8n..8n+7 (rows), dims 16kk..16kk+15 -> x2 ldmatrix: two 8x8 matrices
+      uint32_t kh[2], kl[2];
+      const int krow = 8 * n + (lane & 7), kch = 2 * kk + ((lane >> 3) & 1);
+      asm volatile("ldmatrix.sync.aligned.m8n8.x2.shared.b16 {%0,%1}, [%2];"
+                   : "=r"(kh[0]), "=r"(kh[1])
+                   : "r"(sm_u32(&sm[2][0] + swz(krow, kch))));
+      asm volatile("ldmatrix.sync.aligned.m8n8.x2.shared.b16 {%0,%1}, [%2];"
+                   : "=r"(kl[0]), "=r"(kl[1])
+                   : "r"(sm_u32(&sm[3][0] + swz(krow, kch))));
+      mma_bf16_16816(sc[n], qa, kh[0], kh[1]);
+      mma_bf16_16816(sc[n], qa, kl[0], kl[1]);
+      mma_bf16_16816(sc[n], qb, kh[0], kh[1]);
+    }
+  }
+  // softmax per query row (rows g and g + 8 of the warp's tile)
+  const float* mk = mask ? mask + (int64_t)b * seq : nullptr;
+  float mx[2] = {-INFINITY, -INFINITY};
+#pragma unroll
+  for (int n = 0; n < 8; ++n) {
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int key = 8 * n + 2 * t4 + j;
+      const float add = key < seq ? (mk ? mk[key] : 0.0f) : -INFINITY;
+      sc[n][j] = fmaf(sc[n][j], scale, add);
+      sc[n][2 + j] = fmaf(sc[n][2 + j], scale, add);
+      mx[0] = fmaxf(mx[0], sc[n][j]);
+      mx[1] = fmaxf(mx[1], sc[n][2 + j]);
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffffu, mx[r], 1));
+    mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffffu, mx[r], 2));
+  }
+  float sum[2] = {0.f, 0.f};
+#pragma unroll
+  for (int n = 0; n < 8; ++n) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int r = j >> 1;
+      const float e = mx[r] == -INFINITY ? 0.0f : __expf(sc[n][j] - mx[r]);
+      sc[n][j] = e;
+      sum[r] += e;
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    sum[r] += __shfl_xor_sync(0xffffffffu, sum[r], 1);
+    sum[r] += __shfl_xor_sync(0xffffffffu, sum[r], 2);
+  }
+  // O = P V: k over keys (4 steps of 16), n over dims (8 tiles of 8)
+  float oc[8][4];
+#pragma unroll
+  for (int n = 0; n < 8; ++n) oc[n][0] = oc[n][1] = oc[n][2] = oc[n][3] = 0.0f;
+#pragma unroll
+  for (int kk = 0; kk < 4; ++kk) {
+    uint32_t ph[4], pl[4];
+    split2(sc[2 * kk][0], sc[2 * kk][1], ph[0], pl[0]);
+    split2(sc[2 * kk][2], sc[2 * kk][3], ph[1], pl[1]);
+    split2(sc[2 * kk + 1][0], sc[2 * kk + 1][1], ph[2], pl[2]);
+    split2(sc[2 * kk + 1][2], sc[2 * kk + 1][3], ph[3], pl[3]);
+#pragma unroll
+    for (int n = 0; n < 8; ++n) {
+      // B = V: keys 16kk.. (k), dims 8n.. (n) -> ldmatrix.trans of V rows, x2
+      uint32_t vh[2], vl[2];
+      const int vrow = 16 * kk + (lane & 7) + ((lane >> 3) & 1) * 8, vch = n;
+      asm volatile("ldmatrix.sync.aligned.m8n8.x2.trans.shared.b16 {%0,%1}, [%2];"
+                   : "=r"(vh[0]), "=r"(vh[1])
+                   : "r"(sm_u32(&sm[4][0] + swz(vrow, vch))));
+      asm volatile("ldmatrix.sync.aligned.m8n8.x2.trans.shared.b16 {%0,%1}, [%2];"
+                   : "=r"(vl[0]), "=r"(vl[1])
+                   : "r"(sm_u32(&sm[5][0] + swz(vrow, vch))));
+      mma_bf16_16816(oc[n], ph, vh[0], vh[1]);
+      mma_bf16_16816(oc[n], ph, vl[0], vl[1]);
+      mma_bf16_16816(oc[n], pl, vh[0], vh[1]);
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    const int q = q0 + g + 8 * r;
+    if (q >= seq) continue;
+    if (!(sum[r] > 0.0f)) {
+      if (t4 == 0 && d_bad) atomicAdd(d_bad, 1);
+      continue;
+    }
+    const float inv = 1.0f / sum[r];
+    const int64_t o = ((int64_t)b * seq + q) * ldo + h * HD;
+#pragma unroll
+    for (int n = 0; n < 8; ++n) {
+      const float v0 = oc[n][2 * r] * inv, v1 = oc[n][2 * r + 1] * inv;
+      const int dd = 8 * n + 2 * t4;
+      if (out) *reinterpret_cast<float2*>(out + o + dd) = make_float2(v0, v1);
+      if (out16) *reinterpret_cast<__nv_bfloat162*>(out16 + o + dd) = __floats2bfloat162_rn(v0, v1);
+    }
+  }
+}
+
 // FQ_SELF_MMA=0 selects the FMA row kernel (A/B runs).
 static bool mma_self_disabled() {
   static int v = -1;
@@ -1363,6 +1507,13 @@ int fq_encoder_attention(const float* qkv, int64_t ldq, int64_t batch, int64_t s
   FQ_CHECK_ARG(qkv && (out || out16) && batch > 0 && seq > 0 && heads > 0 && head_dim > 0 &&
                    head_dim <= 128,
                FQ_ERR_DIMENSION, "fq_encoder_attention: bad shape");
+  if (!exact && head_dim == 64 && seq <= 64 && ldq % 4 == 0 && ((uintptr_t)qkv & 15) == 0 &&
+      ldo % 2 == 0) {
+    launch_kernel(encoder_attention_mma, (unsigned)(batch * heads), 128, 0, as_stream(stream), 1u,
+                  qkv, ldq, (int)seq, (int)heads, scale, mask, out,
+                  reinterpret_cast<__nv_bfloat16*>(out16), ldo, d_bad);
+    return launch_status("fq_encoder_attention");
+  }
   if (seq <= 64 && ldq % 4 == 0 && ((uintptr_t)qkv & 15) == 0) {
     const int64_t hp = head_dim + 1, sp = seq + 1;
     const size_t smem = (size_t)(seq * (hp > sp ? hp : sp) + 2 * seq * hp + seq) * 4;

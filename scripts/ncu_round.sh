@@ -15,20 +15,22 @@ timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__byte
 echo "gemms rc=$?"
 cap() {  # name regex skip
   timeout 600 ncu --set full --clock-control none --import-source on --profile-from-start off \
-    -k regex:"$2" -s "$3" -c 1 -o gpurun_out/${T}_$1 -f python scripts/profile_step.py --steps 40 \
-    > gpurun_out/${T}_$1.log 2>&1
+    --kernel-name-base demangled -k regex:"$2" -s "$3" -c 1 -o gpurun_out/${T}_$1 -f \
+    python scripts/profile_step.py --steps 40 > gpurun_out/${T}_$1.log 2>&1
   echo "$1 rc=$?"
 }
 cap hars "hars_step" 32
 cap selfattn "decoder_self_attention" 190
 cap crossattn "cross_attention" 190
 cap ln "layer_norm_row128" 570
-cap logits "tc_gemm_kernel" 1000
+cap logits "tc_gemm_kernel<224" 30
+cap ffn1 "tc_gemm_kernel<128" 380
+cap splitk "tc_gemm_splitk" 760
 cap encattn "encoder_attention" 3
-for f in hars selfattn crossattn ln logits encattn; do
+for f in hars selfattn crossattn ln logits ffn1 splitk encattn; do
   python scripts/ncu_summary.py gpurun_out/${T}_$f.ncu-rep 12 > gpurun_out/${T}_${f}_summary.txt 2>&1
   python scripts/ncu_ops.py gpurun_out/${T}_$f.ncu-rep 12 >> gpurun_out/${T}_${f}_summary.txt 2>&1
 done
 python scripts/launch_summary.py gpurun_out/${T}_launches.csv 30 > gpurun_out/${T}_launches_summary.txt 2>&1
-rm -f gpurun_out/${T}_launches.csv gpurun_out/${T}_encattn.ncu-rep gpurun_out/${T}_crossattn.ncu-rep
+rm -f gpurun_out/${T}_launches.csv gpurun_out/${T}_*.ncu-rep
 ls -la gpurun_out | grep $T
