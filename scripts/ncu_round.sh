@@ -23,8 +23,8 @@ cap hars "hars_step" 32
 cap selfattn "decoder_self_attention" 190
 cap crossattn "cross_attention" 190
 cap ln "layer_norm_row128" 570
-cap logits "tc_gemm_kernel<224" 30
-cap ffn1 "tc_gemm_kernel<128" 380
+cap logits "tc_gemm_kernel<.int.224" 30
+cap ffn1 "tc_gemm_kernel<.int.128" 380
 cap splitk "tc_gemm_splitk" 760
 cap encattn "encoder_attention" 3
 for f in hars selfattn crossattn ln logits ffn1 splitk encattn; do
