@@ -406,7 +406,8 @@ def run_ours(args, rank, world):
             _abi.call("fq_hars_step", lg.data_ptr(), lg.stride(0), hst.c, args.batch, BEAM, V,
                       cfg.max_seq_len, 2, None, dcur.data_ptr(), 1 << 40, lse.data_ptr(),
                       ci.data_ptr(), ci.stride(0), cc.data_ptr(), hcnt.data_ptr(),
-                      rt.data_ptr(), rp.data_ptr(), hist.data_ptr(), _abi.stream_handle())
+                      rt.data_ptr(), rp.data_ptr(), hist.data_ptr(), None, 0, 0.0, None, None,
+                      None, _abi.stream_handle())
         hst.init()
         t_s1 = graph_time(stage1)
         t_sep = graph_time(hars_step)

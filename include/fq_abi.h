@@ -198,12 +198,18 @@ int fq_hars_groups(fq_beam_state st, int64_t batch, int64_t beam, int64_t vocab,
  * each item, run by the last of its rows to finish, stage 2 (fq_hars_select
  * semantics); the last item advances *d_cur. counters: int32 [batch + 1],
  * zero-initialised once (they reset themselves). Needs 2*beam <= 32 and
- * 16-byte aligned rows; exhaustive search uses the separate entry points. */
+ * 16-byte aligned rows; exhaustive search uses the separate entry points.
+ * With x_next != NULL the item's rows of the next step's decoder input are
+ * also written (embed_scale_pos at position *d_cur + 1, kernels.py:143-151:
+ * fp32 emb[token] * emb_scale + pos[position], row-major [rows, d_model],
+ * x16_next an optional bf16 copy), replacing the next step's embedding launch. */
 int fq_hars_step(const float* logits, int64_t ld, fq_beam_state st, int64_t batch, int64_t beam,
                  int64_t vocab, int64_t max_len, int64_t eos, const double* len_pow,
                  int32_t* d_cur, int64_t max_steps, double* lse, int32_t* cand_idx,
                  int64_t cand_ld, int64_t* cand_count, int32_t* counters, int64_t* row_tokens,
-                 int64_t* row_parents, int32_t* hist, fq_stream_t stream);
+                 int64_t* row_parents, int32_t* hist, const float* emb, int64_t d_model,
+                 float emb_scale, const float* pos, float* x_next, void* x16_next,
+                 fq_stream_t stream);
 
 /* Reset beam state to BeamState() (decode.py:145-151) for every item. */
 int fq_beam_state_init(fq_beam_state st, int64_t batch, int64_t beam, int64_t max_len,

@@ -790,7 +790,9 @@ __global__ void __launch_bounds__(kSwThreads) hars_step_kernel(
     const float* __restrict__ logits, int64_t ld, int V, fq_beam_state st, int batch, int K,
     int max_len, int eos, const double* __restrict__ len_pow, int32_t* d_cur, int64_t max_steps,
     double* lse, int32_t* cand_idx, int64_t cand_ld, int64_t* cand_count, int* item_cnt,
-    int* all_cnt, int64_t* row_tokens, int64_t* row_parents, int32_t* hist) {
+    int* all_cnt, int64_t* row_tokens, int64_t* row_parents, int32_t* hist,
+    const float* __restrict__ emb, int d, float emb_scale, const float* __restrict__ pos,
+    float* __restrict__ x_next, __nv_bfloat16* __restrict__ x16_next) {
   pdl_enter();
   const int C = (int)cl_nrank(), rank = (int)cl_rank();
   const int64_t row = blockIdx.x / C;
@@ -813,6 +815,33 @@ __global__ void __launch_bounds__(kSwThreads) hars_step_kernel(
   __threadfence();
   select_item(b, logits, ld, lse, cand_idx, cand_ld, cand_count, st, K, max_len, eos, len_pow,
               d_cur, max_steps, row_tokens, row_parents, hist);
+  __syncthreads();
+  // next step's embedding of the item's rows (embed_scale_pos, kernels.py:143-151:
+  // fp32 emb * sqrt(d), then + PE[cur + 1], two roundings), so the decode step
+  // needs no separate embedding launch
+  const int nxt = *d_cur + 1;
+  if (x_next && nxt < max_len) {
+    const int d4 = d >> 2;  // d % 4 == 0 (checked on the host)
+    for (int idx = threadIdx.x; idx < K * d4; idx += blockDim.x) {
+      const int ri = idx / d4, j = 4 * (idx - ri * d4);
+      const int64_t r = (int64_t)b * K + ri;
+      const float4 e = *reinterpret_cast<const float4*>(emb + row_tokens[r] * d + j);
+      const float4 p = *reinterpret_cast<const float4*>(pos + (int64_t)nxt * d + j);
+      float4 v;
+      v.x = fadd_rn(fmul_rn(e.x, emb_scale), p.x);
+      v.y = fadd_rn(fmul_rn(e.y, emb_scale), p.y);
+      v.z = fadd_rn(fmul_rn(e.z, emb_scale), p.z);
+      v.w = fadd_rn(fmul_rn(e.w, emb_scale), p.w);
+      *reinterpret_cast<float4*>(x_next + r * d + j) = v;
+      if (x16_next) {
+        __nv_bfloat162 lo = __floats2bfloat162_rn(v.x, v.y), hi = __floats2bfloat162_rn(v.z, v.w);
+        uint2 pk;
+        pk.x = *reinterpret_cast<uint32_t*>(&lo);
+        pk.y = *reinterpret_cast<uint32_t*>(&hi);
+        *reinterpret_cast<uint2*>(x16_next + r * d + j) = pk;
+      }
+    }
+  }
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
@@ -932,13 +961,21 @@ int fq_hars_step(const float* logits, int64_t ld, fq_beam_state st, int64_t batc
                  int64_t vocab, int64_t max_len, int64_t eos, const double* len_pow,
                  int32_t* d_cur, int64_t max_steps, double* lse, int32_t* cand_idx,
                  int64_t cand_ld, int64_t* cand_count, int32_t* counters, int64_t* row_tokens,
-                 int64_t* row_parents, int32_t* hist, fq_stream_t stream) {
+                 int64_t* row_parents, int32_t* hist, const float* emb, int64_t d_model,
+                 float emb_scale, const float* pos, float* x_next, void* x16_next,
+                 fq_stream_t stream) {
   FQ_CHECK_ARG(logits && lse && cand_idx && cand_count && counters && d_cur && row_tokens &&
                    row_parents && batch > 0 && beam >= 1 && beam <= kMaxBeam && max_len >= 1,
                FQ_ERR_DIMENSION, "fq_hars_step: bad args");
   FQ_CHECK_ARG(2 * beam <= 32 && ld % 4 == 0 && vocab % 4 == 0 && ((uintptr_t)logits & 15) == 0,
                FQ_ERR_PARAMETER, "fq_hars_step: needs 2*beam <= 32 and 16-byte aligned rows");
   FQ_CHECK_ARG(cand_ld >= vocab, FQ_ERR_DIMENSION, "fq_hars_step needs full candidate rows");
+  FQ_CHECK_ARG(!x_next || (emb && pos && d_model > 0 && d_model % 4 == 0 &&
+                            ((uintptr_t)emb & 15) == 0 && ((uintptr_t)pos & 15) == 0 &&
+                            ((uintptr_t)x_next & 15) == 0 &&
+                            ((uintptr_t)x16_next & 7) == 0),
+               FQ_ERR_DIMENSION,
+               "fq_hars_step: next-step embedding needs aligned emb/pos/x and d_model % 4 == 0");
   FQ_CHECK_ARG(eos >= 0 && eos < vocab, FQ_ERR_PARAMETER, "eos token outside vocabulary");
   const size_t smem = std::max(sel_smem(beam, max_len),
                                (size_t)kSwP * kSwThreads * sizeof(float4));
@@ -946,7 +983,9 @@ int fq_hars_step(const float* logits, int64_t ld, fq_beam_state st, int64_t batc
   launch_kernel(hars_step_kernel, (unsigned)(batch * beam * kSwSplit), kSwThreads, smem,
                 as_stream(stream), (unsigned)kSwSplit, logits, ld, (int)vocab, st, (int)batch, (int)beam, (int)max_len, (int)eos,
                 len_pow, d_cur, max_steps, lse, cand_idx, cand_ld, cand_count, counters,
-                counters + batch, row_tokens, row_parents, hist);
+                counters + batch, row_tokens, row_parents, hist, x_next ? emb : nullptr,
+                (int)d_model, emb_scale, pos, x_next,
+                reinterpret_cast<__nv_bfloat16*>(x16_next));
   return launch_status("fq_hars_step");
 }
 

@@ -21,6 +21,7 @@ KV cache and GEMM operands, fp32 accumulation and residual stream).
 from __future__ import annotations
 
 import dataclasses
+import math
 from dataclasses import dataclass
 
 import numpy as np
@@ -153,7 +154,8 @@ class Session:
         packed, mask, cache0 = self._setup_decoder(src, src_lengths, rows)
         V = self.config.vocab_size
         exhaustive = int(search == "exhaustive")
-        fused = not exhaustive and 2 * K <= 32 and V % 4 == 0
+        fused = (not exhaustive and 2 * K <= 32 and V % 4 == 0
+                 and self.config.d_model % 4 == 0)
         # Two-group overlap (streams=2, opt-in): the items are split in two
         # halves decoded by two independent chains on two streams inside the
         # step graph (every op is per row / per item, so results are
@@ -177,6 +179,8 @@ class Session:
             st.init()
             step.tokens.fill_(bos_token)
             step.bad.zero_()
+            if fused:
+                step.embed()  # step 0's input; later steps' come from fq_hars_step
             grp = dict(batch=nb, rows=nr, cache=cache, step=step, st=st,
                        hk=bufs.get("hars.k", (nr,), torch.int32),
                        lse=bufs.get("hars.lse", (nr,), torch.float64),
@@ -197,15 +201,18 @@ class Session:
             nb, nr = gr["batch"], gr["rows"]
             lse, ci, cc, hk, parents, lp = (gr[k] for k in ("lse", "ci", "cc", "hk", "parents",
                                                            "lp"))
-            logits = step.run()
+            logits = step.run(embed=not fused)
             stream = _abi.stream_handle()
-            if fused:  # groups + stage 1 + stage 2 + position advance, one launch
+            if fused:  # groups + stage 1 + stage 2 + position advance + next embedding
                 _abi.call("fq_hars_step", logits.data_ptr(), logits.stride(0), st.c, nb, K, V,
                           self.config.max_seq_len, cfg.eos_token, _abi.ptr(lp),
                           cache.d_cur.data_ptr(), max_steps, lse.data_ptr(), ci.data_ptr(),
                           ci.stride(0), cc.data_ptr(), gr["hcnt"].data_ptr(),
                           step.tokens.data_ptr(), parents.data_ptr(), cache.hist.data_ptr(),
-                          stream)
+                          self.dw.embedding.data_ptr(), self.config.d_model,
+                          float(np.float32(math.sqrt(self.config.d_model))),
+                          self.dw.positions.data_ptr(), step.x.data_ptr(),
+                          _abi.ptr(step.x16), stream)
                 self.counters.count_fused("retrieve", nr * V * 4)
                 return
             _abi.call("fq_hars_groups", st.c, nb, K, V, exhaustive, hk.data_ptr(), stream)

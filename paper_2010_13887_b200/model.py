@@ -627,18 +627,28 @@ class DecoderStep:
         self.logits = b.get("dec.logits", (R, V))
         self.bad = b.get("dec.bad", (1,), torch.int32)
 
-    def run(self):
-        """Embed -> L decoder layers -> logits. Position comes from cache.d_cur."""
+    def embed(self):
+        """Decoder input of the current position (model.py:559)."""
+        c, dw = self.config, self.dw
+        R, d = self.rows, c.d_model
+        _abi.call("fq_embed_scale_pos", self.tokens.data_ptr(), R, dw.embedding.data_ptr(), d,
+                  float(np.float32(math.sqrt(d))), dw.positions.data_ptr(), 0,
+                  self.cache.d_cur.data_ptr(), 1, self.x.data_ptr(), _abi.ptr(self.x16),
+                  _abi.stream_handle())
+        self.counters.count_fused("embed_scale_pos", R * d * 8)
+
+    def run(self, embed: bool = True):
+        """Embed -> L decoder layers -> logits. Position comes from cache.d_cur.
+        ``embed=False``: the input rows were already written (by the previous
+        step's fused HARS launch, fq_hars_step)."""
         c, dw, ctr, tm = self.config, self.dw, self.counters, self.timers
         R, d, h, hd, L = self.rows, c.d_model, c.num_heads, c.head_dim, c.num_decoder_layers
         stream = _abi.stream_handle()
         scale = attention_scale(hd)
         kvdt = 1 if dw.bf16 else 0
         exact = 0 if dw.bf16 else 1
-        _abi.call("fq_embed_scale_pos", self.tokens.data_ptr(), R, dw.embedding.data_ptr(), d,
-                  float(np.float32(math.sqrt(d))), dw.positions.data_ptr(), 0,
-                  self.cache.d_cur.data_ptr(), 1, self.x.data_ptr(), _abi.ptr(self.x16), stream)
-        ctr.count_fused("embed_scale_pos", R * d * 8)
+        if embed:
+            self.embed()
         x, x16 = self.x, self.x16
         for i, lw in enumerate(dw.dec):
             _lin(dw, x, x16, lw["w_qkv"], self.sqkv, bias=lw["b_qkv"], counters=ctr, timers=tm)
