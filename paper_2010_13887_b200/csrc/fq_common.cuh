@@ -75,12 +75,15 @@ __device__ __forceinline__ float fadd_rn(float a, float b) { return __fadd_rn(a,
 
 // Activation on the fp32 pre-activation (kernels.py:45-50): ReLU by compare,
 // GELU = 0.5 t (1 + erf(t/sqrt 2)) evaluated in f64 and rounded to fp32.
+// The f64 GELU is out of line: inlined into every unrolled epilogue it grew
+// the GEMM kernels' code past the instruction cache (ReLU stays inline).
+static __device__ __noinline__ float gelu_f64(float t) {
+  double td = (double)t;
+  return (float)(0.5 * td * (1.0 + erf(td * 0.70710678118654752440)));
+}
 __device__ __forceinline__ float apply_act(float t, int act) {
   if (act == FQ_ACT_RELU) return t < 0.0f ? 0.0f : t;
-  if (act == FQ_ACT_GELU) {
-    double td = (double)t;
-    return (float)(0.5 * td * (1.0 + erf(td * 0.70710678118654752440)));
-  }
+  if (act == FQ_ACT_GELU) return gelu_f64(t);
   return t;
 }
 
