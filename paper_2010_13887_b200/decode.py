@@ -195,6 +195,9 @@ class BeamState:
         return out[:config.effective_beam_size]
 
 
+_PINNED: dict = {}  # pinned host staging buffers for DeviceBeamState.host_items, by size
+
+
 class DeviceBeamState:
     """Batched beam state in device memory (fq_beam_state, fq_abi.h)."""
 
@@ -250,27 +253,41 @@ class DeviceBeamState:
         """Item b as a reference BeamState (prefixes, cum, finished, bookkeeping)."""
         return self.host_items()[b]
 
+    def _to_host(self) -> dict:
+        """Every field in one pinned staging buffer: async copies, one sync."""
+        sizes = [getattr(self, n).numel() * getattr(self, n).element_size()
+                 for n, _, _ in self.FIELDS]
+        total = sum((z + 63) // 64 * 64 for z in sizes)
+        buf = _PINNED.get(total)
+        if buf is None:
+            buf = _PINNED[total] = torch.empty(total, dtype=torch.uint8, pin_memory=True)
+        out, off = {}, 0
+        for (n, dt, _), z in zip(self.FIELDS, sizes):
+            t = getattr(self, n)
+            view = buf[off:off + z].view(dt).view(t.shape)
+            view.copy_(t, non_blocking=True)
+            out[n] = view
+            off += (z + 63) // 64 * 64
+        torch.cuda.current_stream().synchronize()
+        return {n: v.numpy() for n, v in out.items()}
+
     def host_items(self) -> list:
-        live = self.live.cpu().numpy()
-        step = self.step.cpu().numpy()
-        pre = self.prefix.cpu().numpy()
-        cum = self.cum.cpu().numpy()
-        fc = self.fin_count.cpu().numpy()
-        ft = self.fin_tok.cpu().numpy()
-        fl = self.fin_len.cpu().numpy()
-        fs = self.fin_score.cpu().numpy()
-        lt = self.last_tok.cpu().numpy()
-        par = self.parent.cpu().numpy()
+        h = self._to_host()
+        live, step, pre, cum = h["live"], h["step"], h["prefix"], h["cum"]
+        fc, ft, fl, fs = h["fin_count"], h["fin_tok"], h["fin_len"], h["fin_score"]
+        lt, par = h["last_tok"], h["parent"]
         out = []
+        live_l, step_l, fc_l = live.tolist(), step.tolist(), fc.tolist()
         for b in range(self.batch):
-            nl, st = int(live[b]), int(step[b])
-            fin = [(ft[b, i, :fl[b, i]].tolist(), float(fs[b, i])) for i in range(int(fc[b]))]
-            out.append(BeamState(prefixes=[pre[b, i, :st].tolist() for i in range(nl)],
-                                 cum_log_prob=[float(cum[b, i]) for i in range(nl)],
-                                 finished=fin, step=st,
-                                 parents=[int(par[b, i]) for i in range(nl)],
-                                 last_tokens=[int(lt[b, i]) for i in range(nl)],
-                                 chosen_tokens=[int(lt[b, i]) for i in range(nl)]))
+            nl, st, nf = live_l[b], step_l[b], fc_l[b]
+            lens = fl[b, :nf].tolist()
+            toks = ft[b, :nf].tolist()
+            fin = [(toks[i][:lens[i]], sc) for i, sc in enumerate(fs[b, :nf].tolist())]
+            last = lt[b, :nl].tolist()
+            out.append(BeamState(prefixes=pre[b, :nl, :st].tolist(),
+                                 cum_log_prob=cum[b, :nl].tolist(), finished=fin, step=st,
+                                 parents=par[b, :nl].tolist(), last_tokens=last,
+                                 chosen_tokens=list(last)))
         return out
 
 
