@@ -297,7 +297,8 @@ __device__ __forceinline__ void sweep_row(
     const float* __restrict__ logits, int64_t ld, int V, const int64_t row, const int k,
     float* __restrict__ group_max, int64_t gm_ld, float* __restrict__ threshold,
     double* __restrict__ lse, int32_t* __restrict__ cand_idx, int64_t cand_ld,
-    int64_t* __restrict__ cand_count, float4* __restrict__ ring, const int C, const int rank) {
+    int64_t* __restrict__ cand_count, float4* __restrict__ ring, const int C, const int rank,
+    const int64_t vals_off = 0) {
   __shared__ float part_max[kSwThreads * 4];
   __shared__ int32_t sv_idx[kSurvCap];
   __shared__ float sv_val[kSurvCap];
@@ -454,11 +455,17 @@ __device__ __forceinline__ void sweep_row(
     for (int i = tid; i < nsv; i += kSwThreads) {
       const float v = sv_val[i];
       const int j = sv_idx[i];
-      if (v >= R) part_max[atomicAdd(&s_n, 1)] = __int_as_float(j);
+      if (v >= R) {
+        const int p = atomicAdd(&s_n, 1);
+        if (p < kSwThreads * 2) {  // (index, value) pairs
+          part_max[2 * p] = __int_as_float(j);
+          part_max[2 * p + 1] = v;
+        }
+      }
     }
   }
   __syncthreads();
-  if (tid == 0) s_ovf = (nsv > kSurvCap || s_n > kSwThreads * 4) ? 1 : 0;
+  if (tid == 0) s_ovf = (nsv > kSurvCap || s_n > kSwThreads * 2) ? 1 : 0;
   if (C > 1) cl_sync_all();  // counts, overflow flags and partial sums visible
   else __syncthreads();
   int ovf = 0, base = 0, total = 0;
@@ -473,10 +480,12 @@ __device__ __forceinline__ void sweep_row(
   if (!ovf) {
     const int n = s_n;
     for (int i = tid; i < n; i += kSwThreads) {
-      const int j = __float_as_int(part_max[i]);
+      const int j = __float_as_int(part_max[2 * i]);
       int rk = 0;
-      for (int q2 = 0; q2 < n; ++q2) rk += __float_as_int(part_max[q2]) < j ? 1 : 0;
+      for (int q2 = 0; q2 < n; ++q2) rk += __float_as_int(part_max[2 * q2]) < j ? 1 : 0;
       if (base + rk < cand_ld) out_idx[base + rk] = j;
+      if (vals_off && base + rk < vals_off)  // candidate logit beside its index (stage 2)
+        out_idx[vals_off + base + rk] = __float_as_int(part_max[2 * i + 1]);
     }
     if (tid == 0 && rank == 0) cand_count[row] = total;
   } else if (rank == 0) {
@@ -496,7 +505,9 @@ __device__ __forceinline__ void sweep_row(
       for (int c = 0; c < 4; ++c) {
         if (flags & (1 << c)) {
           const int64_t pos = cb + off;
-          if (pos < cand_ld) out_idx[pos] = c0 + tid * 4 + c;
+          const int j = c0 + tid * 4 + c;
+          if (pos < cand_ld) out_idx[pos] = j;
+          if (vals_off && pos < vals_off) out_idx[vals_off + pos] = __float_as_int(x[j]);
           ++off;
         }
       }
@@ -561,7 +572,8 @@ __device__ __forceinline__ void select_item(
     const int b, const float* __restrict__ logits, int64_t ld, const double* lse,
     const int32_t* cand_idx, int64_t cand_ld, const int64_t* cand_count, fq_beam_state st, int K,
     int max_len, int eos, const double* __restrict__ len_pow, const int32_t* __restrict__ d_cur,
-    int64_t max_steps, int64_t* row_tokens, int64_t* row_parents, int32_t* hist) {
+    int64_t max_steps, int64_t* row_tokens, int64_t* row_parents, int32_t* hist,
+    const int64_t vals_off = 0) {
   // dynamic smem: old prefixes [K][max_len], old hist [K][max_len], then the
   // candidate array (16-byte aligned)
   extern __shared__ int32_t sh[];
@@ -590,9 +602,11 @@ __device__ __forceinline__ void select_item(
   const int step = st.step[b];
   const int cur = d_cur ? *d_cur : step;
   const bool last_step = (int64_t)cur == max_steps - 1;
-  if (tid == 0) {
-    offs[0] = 0;
-    for (int i = 0; i < live; ++i) offs[i + 1] = offs[i] + __ldcg(cand_count + row0 + i);
+  __shared__ int64_t cnt_s[kMaxBeam];
+  __shared__ double lse_s[kMaxBeam];
+  if (tid < live) {  // one round trip for every row's count and lse
+    cnt_s[tid] = __ldcg(cand_count + row0 + tid);
+    lse_s[tid] = __ldcg(lse + row0 + tid);
   }
   for (int i = tid; i < K * max_len; i += blockDim.x) {
     old_pref[i] = st.prefix[(int64_t)b * K * max_len + i];
@@ -605,6 +619,11 @@ __device__ __forceinline__ void select_item(
     }
   }
   __syncthreads();
+  if (tid == 0) {
+    offs[0] = 0;
+    for (int i = 0; i < live; ++i) offs[i + 1] = offs[i] + cnt_s[i];
+  }
+  __syncthreads();
   const int64_t n_total = offs[live];
   const int need = (int)(((int64_t)K + live) < n_total ? ((int64_t)K + live) : n_total);
 
@@ -612,10 +631,14 @@ __device__ __forceinline__ void select_item(
     int i = 0;
     while (offs[i + 1] <= j) ++i;
     const int64_t r = row0 + i;
-    const int32_t tok = __ldcg(cand_idx + r * cand_ld + (j - offs[i]));
-    const double lg = (double)logits[r * ld + tok];
+    const int64_t jj = j - offs[i];
+    const int32_t tok = __ldcg(cand_idx + r * cand_ld + jj);
+    // candidate logit stored beside the index by the fused stage 1 (one round trip)
+    const double lg = (vals_off && cnt_s[i] <= vals_off)
+                          ? (double)__int_as_float(__ldcg(cand_idx + r * cand_ld + vals_off + jj))
+                          : (double)logits[r * ld + tok];
     Cand c;
-    c.s = st.cum[b * K + i] + (lg - __ldcg(lse + r));  // decode.py:238
+    c.s = st.cum[b * K + i] + (lg - lse_s[i]);  // decode.py:238
     c.tok = tok;
     c.beam = i;
     return c;
@@ -800,8 +823,9 @@ __global__ void __launch_bounds__(kSwThreads) hars_step_kernel(
   const int live = st.live[b];
   const int k = (!st.done[b] && i < live) ? min(K + live, V) : 0;  // hars_groups
   extern __shared__ __align__(16) float4 sw_ring[];  // aliases stage 2's dynamic smem
+  const int64_t vals_off = cand_ld / 2 >= kSwThreads * 2 ? cand_ld / 2 : 0;
   sweep_row(logits, ld, V, row, k, nullptr, 0, nullptr, lse, cand_idx, cand_ld, cand_count,
-            sw_ring, C, rank);
+            sw_ring, C, rank, vals_off);
   __shared__ int s_last;
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -814,7 +838,7 @@ __global__ void __launch_bounds__(kSwThreads) hars_step_kernel(
   if (!s_last) return;
   __threadfence();
   select_item(b, logits, ld, lse, cand_idx, cand_ld, cand_count, st, K, max_len, eos, len_pow,
-              d_cur, max_steps, row_tokens, row_parents, hist);
+              d_cur, max_steps, row_tokens, row_parents, hist, vals_off);
   __syncthreads();
   // next step's embedding of the item's rows (embed_scale_pos, kernels.py:143-151:
   // fp32 emb * sqrt(d), then + PE[cur + 1], two roundings), so the decode step
