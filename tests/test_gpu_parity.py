@@ -336,3 +336,57 @@ def test_retrieve_per_row_k_vs_oracle(P, O, V):
         assert cc[b] == len(orr.candidate_tokens[0]), b
         assert np.array_equal(ci[b, :cc[b]], orr.candidate_tokens[0]), b
         assert abs(lse[b] - orr.logsumexp_full[0]) <= 1e-7 * abs(orr.logsumexp_full[0]) + 1e-7
+
+
+def test_fused_hars_step_equals_separate_launches(P):
+    """fq_hars_step (groups + stage 1 + stage 2 + advance + next embedding in
+    one launch) reproduces fq_hars_groups + fq_retrieve + fq_hars_select +
+    fq_step_advance step for step, including EOS picks and a length penalty."""
+    import torch
+    from paper_2010_13887_b200 import _abi, decode as D
+    B, K, V, S, d, eos = 6, 4, 32000, 16, 64, 7
+    R = B * K
+    g = torch.Generator(device="cuda").manual_seed(0)
+    lp = D.length_penalty_table(0.6, S, "cuda")
+    emb = torch.randn(V, d, device="cuda", generator=g)
+    pos = torch.randn(S, d, device="cuda", generator=g)
+
+    def mk():
+        st = D.DeviceBeamState(B, K, S)
+        st.init()
+        return dict(st=st, cur=torch.zeros(1, dtype=torch.int32, device="cuda"),
+                    hist=torch.arange(R, dtype=torch.int32, device="cuda")[:, None].repeat(1, S).contiguous(),
+                    tok=torch.zeros(R, dtype=torch.int64, device="cuda"),
+                    par=torch.zeros(R, dtype=torch.int64, device="cuda"),
+                    lse=torch.zeros(R, dtype=torch.float64, device="cuda"),
+                    ci=torch.zeros(R, V, dtype=torch.int32, device="cuda"),
+                    cc=torch.zeros(R, dtype=torch.int64, device="cuda"),
+                    cnt=torch.zeros(B + 1 + R, dtype=torch.int32, device="cuda"),
+                    dk=torch.zeros(R, dtype=torch.int32, device="cuda"),
+                    x=torch.zeros(R, d, device="cuda"))
+    a, b = mk(), mk()
+    hs = _abi.stream_handle
+    for t in range(S - 1):
+        L = torch.randn(R, V, device="cuda", generator=g) * 3
+        L[:, eos] += 4.0 * (t % 3 == 2)  # EOS becomes competitive every third step
+        _abi.call("fq_hars_groups", a["st"].c, B, K, V, 0, a["dk"].data_ptr(), hs())
+        D.retrieve_device(L, 2 * K, d_k=a["dk"], out=(None, None, a["lse"], a["ci"], a["cc"]))
+        _abi.call("fq_hars_select", L.data_ptr(), V, a["lse"].data_ptr(), a["ci"].data_ptr(), V,
+                  a["cc"].data_ptr(), a["st"].c, B, K, V, S, eos, lp.data_ptr(),
+                  a["cur"].data_ptr(), S, a["tok"].data_ptr(), a["par"].data_ptr(),
+                  a["hist"].data_ptr(), None, 0, hs())
+        _abi.call("fq_step_advance", a["cur"].data_ptr(), hs())
+        _abi.call("fq_hars_step", L.data_ptr(), V, b["st"].c, B, K, V, S, eos, lp.data_ptr(),
+                  b["cur"].data_ptr(), S, b["lse"].data_ptr(), b["ci"].data_ptr(), V,
+                  b["cc"].data_ptr(), b["cnt"].data_ptr(), b["tok"].data_ptr(),
+                  b["par"].data_ptr(), b["hist"].data_ptr(), emb.data_ptr(), d,
+                  float(np.float32(8.0)), pos.data_ptr(), b["x"].data_ptr(), None, hs())
+        torch.cuda.synchronize()
+        for key in ("tok", "par", "hist", "cur", "cc"):
+            assert torch.equal(a[key], b[key]), (t, key)
+        assert torch.equal(a["lse"], b["lse"]) or float((a["lse"] - b["lse"]).abs().max()) < 1e-6
+        for n, _, _ in D.DeviceBeamState.FIELDS:
+            assert torch.equal(getattr(a["st"], n), getattr(b["st"], n)), (t, n)
+        if t + 1 < S:
+            want = emb[b["tok"]] * np.float32(8.0) + pos[t + 1]
+            assert torch.equal(b["x"], want), t
