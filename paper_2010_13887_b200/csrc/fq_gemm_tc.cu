@@ -808,7 +808,7 @@ static int prep() {
 
 int gemm_tc_prepare() {
   if (tc::prep<256, 4>() || tc::prep<224, 4>() || tc::prep<192, 4>() || tc::prep<128, 6>() ||
-      tc::prep<64, 8>() || tc::prep<32, 8>() || tc::prep<32, 4>() || tc::prep<32, 2>() ||
+      tc::prep<64, 8>() || tc::prep<32, 8>() ||
       tc::prep_splitk<256, 4>() || tc::prep_splitk<128, 6>() || tc::prep_splitk<64, 8>()) {
     set_error("fq_prepare: tcgen05 GEMM smem opt-in failed");
     return FQ_ERR_CUDA;
@@ -845,35 +845,11 @@ static TcPlan plan_tc(int64_t M, int64_t N, int64_t K) {
   // launches on B200): small-M GEMMs are bound by the chip-wide L2->SM
   // operand traffic and per-launch overhead, large ones by per-SM ingest.
   const int64_t nt128 = (N + 127) / 128;
-  if (mt <= 8 && N <= 1024) {  // experiment hook: FQ_PLAN_SMALLN="bn,split"
-    static int ov_bn = -1, ov_sp = 1;
-    if (ov_bn < 0) {
-      ov_bn = 0;
-      if (const char* e = getenv("FQ_PLAN_SMALLN")) sscanf(e, "%d,%d", &ov_bn, &ov_sp);
-    }
-    if (ov_bn > 0) {
-      const int64_t nt = (N + ov_bn - 1) / ov_bn;
-      if (ov_sp == 1 || (mt * nt * ov_sp <= tc::num_sms() && ov_sp <= nkb))
-        return {ov_bn, 1, 1, ov_sp};
-    }
-  }
   if (mt <= 8) {
     if (N <= 1024 && nkb >= 16 && mt * nt128 * 4 <= tc::num_sms())
       return {128, 1, 1, 4};                       // K >= 1024: split-K over 4 CTAs
     if (N <= 1024) return {32, 1, 1, 1};
-    if (N < 8192) {
-      static int ov_bn = -1, ov_sp = 1;  // experiment hook: FQ_PLAN_MIDN="bn,split"
-      if (ov_bn < 0) {
-        ov_bn = 0;
-        if (const char* e = getenv("FQ_PLAN_MIDN")) sscanf(e, "%d,%d", &ov_bn, &ov_sp);
-      }
-      if (ov_bn > 0) {
-        const int64_t nt = (N + ov_bn - 1) / ov_bn;
-        if (ov_sp == 1 || (mt * nt * ov_sp <= tc::num_sms() && ov_sp <= nkb))
-          return {ov_bn, 1, 1, ov_sp};
-      }
-      return {128, 1, 1, 1};
-    }
+    if (N < 8192) return {128, 1, 1, 1};
   }
   // Large GEMMs are tensor-bound: pick the tile width minimising the busiest
   // CTA's work, ceil(tiles / SMs) * BN (wave quantisation over 148 SMs).
@@ -910,16 +886,7 @@ int launch_tc_gemm(const void* a, int64_t lda, const void* b, int64_t ldb, void*
     case 192: return tc::launch<192, 4>(a, lda, b, ldb, ep, M, N, K, p.cm, p.cn, s);
     case 128: return tc::launch<128, 6>(a, lda, b, ldb, ep, M, N, K, p.cm, p.cn, s);
     case 64: return tc::launch<64, 8>(a, lda, b, ldb, ep, M, N, K, p.cm, p.cn, s);
-    default: {
-      static int st32 = -1;  // experiment hook: FQ_STAGES32 = 2 | 4 | 8
-      if (st32 < 0) {
-        const char* e = getenv("FQ_STAGES32");
-        st32 = e ? atoi(e) : 8;
-      }
-      if (st32 == 2) return tc::launch<32, 2>(a, lda, b, ldb, ep, M, N, K, p.cm, p.cn, s);
-      if (st32 == 4) return tc::launch<32, 4>(a, lda, b, ldb, ep, M, N, K, p.cm, p.cn, s);
-      return tc::launch<32, 8>(a, lda, b, ldb, ep, M, N, K, p.cm, p.cn, s);
-    }
+    default: return tc::launch<32, 8>(a, lda, b, ldb, ep, M, N, K, p.cm, p.cn, s);
   }
 }
 
