@@ -145,13 +145,14 @@ def test_layer_norm_paths(T, rows, d):
 
 
 @pytest.mark.parametrize("H,hd,rows,cur", [(16, 64, 12, 13), (8, 128, 8, 0), (16, 64, 20, 63),
-                                          (32, 32, 4, 7), (8, 64, 8, 30)])
+                                          (32, 32, 4, 7), (8, 64, 8, 30), (4, 64, 6, 97),
+                                          (16, 64, 5, 15), (16, 64, 5, 16)])
 def test_decoder_self_attention_rows_kernel(T, H, hd, rows, cur):
     """The bf16 throughput-mode row kernel (CTA per beam row, 16-byte slot
     segments, shuffle-reduced head dots) vs float64 on the bf16 cache."""
     A = _abi()
     g = T.Generator(device="cuda").manual_seed(H * hd + rows + cur)
-    S, beam = 64, 4
+    S, beam = (64 if cur < 64 else 128), 4
     d = H * hd
     kc = T.randn(S, rows, d, device="cuda", generator=g).to(T.bfloat16)
     vc = T.randn(S, rows, d, device="cuda", generator=g).to(T.bfloat16)
