@@ -244,6 +244,11 @@ __device__ __forceinline__ void sw_stamp(int64_t row, int slot) {
     g_sw_dbg[row * 8 + slot] = t_;
   }
 }
+__device__ __forceinline__ float ex2_ftz(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 constexpr int kSwU = 4;   // pilot vectors per thread
 constexpr int kSwP = 8;   // async ring depth (vectors in flight per thread)
 // CTAs (cluster) per row. 2 balances rows over SMs but needs 7 resident CTAs
@@ -365,16 +370,32 @@ __device__ __forceinline__ void sweep_row(
   __syncthreads();
   const float Rp = s_R;  // may be -inf (group without pilot elements): everything survives
   sw_stamp(row, 1);
+  // logsumexp reference point: the pilot maximum, kept fixed (terms exp(x - m)
+  // up to e^64 are exact enough in fp32/f64): moving it with every new
+  // running maximum costs a divergent f64 exp per record (measured +20% on a
+  // streaming sweep, scripts/micro/streamprobe.cu)
+  constexpr float L2E = 1.4426950408889634f;
+  constexpr float L2E_LO = 1.925963033500011e-08f;  // log2(e) - L2E
+  constexpr double L2E_D = 1.4426950408889634;
   float m = s_M;
+  float mL = m * L2E;
   double s = 0.0;
   auto visit4 = [&](const float4& e, int v) {
     const float m4 = fmaxf(fmaxf(e.x, e.y), fmaxf(e.z, e.w));
-    if (m4 > m) {  // running max grows (rare after the pilot)
-      s = m == NEG ? 0.0 : s * exp((double)m - (double)m4);
-      m = m4;
+    if (m4 > m + 64.f || m == NEG) {  // (practically never for logits)
+      if (m4 != NEG) {
+        s = m == NEG ? 0.0 : s * exp2((double)mL - (double)m4 * L2E_D);
+        m = m4;
+        mL = m * L2E;
+      }
     }
+    // exp(x - m_eff) = 2^(x log2e - mL), m_eff = mL / log2e, log2e as hi + lo
+    // fp32 parts (argument exact to ~1 ulp); terms below 2^-126 flush to 0
     if (m != NEG) {
-      const float t4 = (__expf(e.x - m) + __expf(e.y - m)) + (__expf(e.z - m) + __expf(e.w - m));
+      const float t4 = (ex2_ftz(fmaf(e.x, L2E_LO, fmaf(e.x, L2E, -mL))) +
+                        ex2_ftz(fmaf(e.y, L2E_LO, fmaf(e.y, L2E, -mL)))) +
+                       (ex2_ftz(fmaf(e.z, L2E_LO, fmaf(e.z, L2E, -mL))) +
+                        ex2_ftz(fmaf(e.w, L2E_LO, fmaf(e.w, L2E, -mL))));
       s += (double)t4;
     }
     if (m4 >= Rp) {
@@ -410,8 +431,14 @@ __device__ __forceinline__ void sweep_row(
   if (tid == 0 && rank == C - 1) {  // V % 4 tail (the last rank)
     for (int j = nvec << 2; j < V; ++j) {
       const float xv = x[j];
-      if (xv > m) { s = m == NEG ? 0.0 : s * exp((double)m - (double)xv); m = xv; }
-      if (m != NEG) s += (double)__expf(xv - m);
+      if (xv > m + 64.f || m == NEG) {
+        if (xv != NEG) {
+          s = m == NEG ? 0.0 : s * exp2((double)mL - (double)xv * L2E_D);
+          m = xv;
+          mL = m * L2E;
+        }
+      }
+      if (m != NEG) s += (double)ex2_ftz(fmaf(xv, L2E_LO, fmaf(xv, L2E, -mL)));
       if (xv >= Rp) {
         const int p = atomicAdd(&s_cnt, 1);
         if (p < kSurvCap) { sv_idx[p] = j; sv_val[p] = xv; }
@@ -443,7 +470,7 @@ __device__ __forceinline__ void sweep_row(
   }
   __syncthreads();
   const float R = s_R, M = s_M;
-  const double st = m == NEG ? 0.0 : s * exp((double)m - (double)M);
+  const double st = m == NEG ? 0.0 : s * exp2((double)mL - (double)M * L2E_D);
   const double Sl = block_sum(st, red);  // contains __syncthreads
   sw_stamp(row, 3);
   const int nsv = s_cnt;
@@ -573,7 +600,7 @@ __device__ __forceinline__ void select_item(
     const int32_t* cand_idx, int64_t cand_ld, const int64_t* cand_count, fq_beam_state st, int K,
     int max_len, int eos, const double* __restrict__ len_pow, const int32_t* __restrict__ d_cur,
     int64_t max_steps, int64_t* row_tokens, int64_t* row_parents, int32_t* hist,
-    const int64_t vals_off = 0) {
+    const int64_t vals_off = 0, int64_t* tok_sh = nullptr) {
   // dynamic smem: old prefixes [K][max_len], old hist [K][max_len], then the
   // candidate array (16-byte aligned)
   extern __shared__ int32_t sh[];
@@ -591,34 +618,43 @@ __device__ __forceinline__ void select_item(
   int32_t* old_pref = sh;
   int32_t* old_hist = sh + K * max_len;
 
-  if (st.done[b]) {  // engine.py:148-155: dead rows get parent row0, token 0
-    if (tid < K) {
-      row_parents[row0 + tid] = row0;
-      row_tokens[row0 + tid] = 0;
-    }
-    return;
-  }
-  const int live = st.live[b];
-  const int step = st.step[b];
-  const int cur = d_cur ? *d_cur : step;
-  const bool last_step = (int64_t)cur == max_steps - 1;
+  // every input of the item in one round trip: state scalars, per-row counts
+  // and lse, old prefixes and whole history rows (no dependency on cur)
+  __shared__ int s_in[5];
   __shared__ int64_t cnt_s[kMaxBeam];
-  __shared__ double lse_s[kMaxBeam];
-  if (tid < live) {  // one round trip for every row's count and lse
+  __shared__ double lse_s[kMaxBeam], cum_s[kMaxBeam];
+  __shared__ double s_fsc_last;
+  if (tid == 0) {
+    s_in[0] = st.done[b];
+    s_in[1] = st.live[b];
+    s_in[2] = st.step[b];
+    s_in[3] = d_cur ? *d_cur : -1;
+    s_in[4] = st.fin_count[b];
+    s_fsc_last = st.fin_score[b * K + K - 1];
+  }
+  if (tid < K) {
     cnt_s[tid] = __ldcg(cand_count + row0 + tid);
     lse_s[tid] = __ldcg(lse + row0 + tid);
+    cum_s[tid] = st.cum[b * K + tid];
   }
   for (int i = tid; i < K * max_len; i += blockDim.x) {
     old_pref[i] = st.prefix[(int64_t)b * K * max_len + i];
-  }
-  if (hist) {
-    for (int i = tid; i < K * (cur + 1); i += blockDim.x) {
-      int bi = i / (cur + 1), t = i % (cur + 1);
-      old_hist[bi * max_len + t] =
-          t == cur ? (int32_t)(row0 + bi) : hist[(row0 + bi) * max_len + t];
-    }
+    if (hist) old_hist[i] = hist[row0 * max_len + i];
   }
   __syncthreads();
+  if (s_in[0]) {  // engine.py:148-155: dead rows get parent row0, token 0
+    if (tid < K) {
+      row_parents[row0 + tid] = row0;
+      row_tokens[row0 + tid] = 0;
+      if (tok_sh) tok_sh[tid] = 0;
+    }
+    return;
+  }
+  const int live = s_in[1];
+  const int step = s_in[2];
+  const int cur = d_cur ? s_in[3] : step;
+  const bool last_step = (int64_t)cur == max_steps - 1;
+  if (hist && tid < K && cur < max_len) old_hist[tid * max_len + cur] = (int32_t)(row0 + tid);
   if (tid == 0) {
     offs[0] = 0;
     for (int i = 0; i < live; ++i) offs[i + 1] = offs[i] + cnt_s[i];
@@ -638,7 +674,7 @@ __device__ __forceinline__ void select_item(
                           ? (double)__int_as_float(__ldcg(cand_idx + r * cand_ld + vals_off + jj))
                           : (double)logits[r * ld + tok];
     Cand c;
-    c.s = st.cum[b * K + i] + (lg - lse_s[i]);  // decode.py:238
+    c.s = cum_s[i] + (lg - lse_s[i]);  // decode.py:238
     c.tok = tok;
     c.beam = i;
     return c;
@@ -695,7 +731,8 @@ __device__ __forceinline__ void select_item(
     int32_t* ftok = st.fin_tok + (int64_t)b * K * max_len;
     int32_t* flen = st.fin_len + b * K;
     double* fsc = st.fin_score + b * K;
-    int fc = st.fin_count[b];
+    int fc = s_in[4];
+    bool eos_in = false;  // finished list changed this step (else fsc[K-1] preloaded)
     for (int p = 0; p < need; ++p) {
       const Cand c = picks[p];
       if (c.tok == eos) {
@@ -732,6 +769,7 @@ __device__ __forceinline__ void select_item(
           ftok[pos * max_len + step] = eos;
           flen[pos] = length;
           fsc[pos] = sc;
+          eos_in = true;
           if (fc < K) ++fc;
         }
       } else if (nl < K) {
@@ -751,7 +789,7 @@ __device__ __forceinline__ void select_item(
       double best = new_cum[0];
       for (int i = 1; i < nl; ++i) best = fmax(best, new_cum[i]);
       if (len_pow) best = best / len_pow[max(step + 1, 1)];  // decode.py:170
-      stop = best <= fsc[K - 1];
+      stop = best <= (eos_in ? fsc[K - 1] : s_fsc_last);
     }
     const int done = (stop || last_step || nl == 0) ? 1 : 0;
     s_new_live = nl;
@@ -779,6 +817,7 @@ __device__ __forceinline__ void select_item(
     const bool feed = on && !done;
     row_parents[row0 + tid] = feed ? row0 + new_par[tid] : row0;
     row_tokens[row0 + tid] = feed ? new_tok[tid] : 0;
+    if (tok_sh) tok_sh[tid] = feed ? new_tok[tid] : 0;
   }
   // copy-free KV reorder: new history row i = old history of its parent
   if (hist && !done) {
@@ -820,6 +859,8 @@ __global__ void __launch_bounds__(kSwThreads) hars_step_kernel(
   const int C = (int)cl_nrank(), rank = (int)cl_rank();
   const int64_t row = blockIdx.x / C;
   const int b = (int)(row / K), i = (int)(row % K);
+  // the position is only advanced after every item has passed its read below
+  const int cur0 = *d_cur;
   const int live = st.live[b];
   const int k = (!st.done[b] && i < live) ? min(K + live, V) : 0;  // hars_groups
   extern __shared__ __align__(16) float4 sw_ring[];  // aliases stage 2's dynamic smem
@@ -837,19 +878,20 @@ __global__ void __launch_bounds__(kSwThreads) hars_step_kernel(
   __syncthreads();
   if (!s_last) return;
   __threadfence();
+  __shared__ int64_t s_tok[kMaxBeam];
   select_item(b, logits, ld, lse, cand_idx, cand_ld, cand_count, st, K, max_len, eos, len_pow,
-              d_cur, max_steps, row_tokens, row_parents, hist, vals_off);
+              d_cur, max_steps, row_tokens, row_parents, hist, vals_off, s_tok);
   __syncthreads();
   // next step's embedding of the item's rows (embed_scale_pos, kernels.py:143-151:
   // fp32 emb * sqrt(d), then + PE[cur + 1], two roundings), so the decode step
   // needs no separate embedding launch
-  const int nxt = *d_cur + 1;
+  const int nxt = cur0 + 1;
   if (x_next && nxt < max_len) {
     const int d4 = d >> 2;  // d % 4 == 0 (checked on the host)
     for (int idx = threadIdx.x; idx < K * d4; idx += blockDim.x) {
       const int ri = idx / d4, j = 4 * (idx - ri * d4);
       const int64_t r = (int64_t)b * K + ri;
-      const float4 e = *reinterpret_cast<const float4*>(emb + row_tokens[r] * d + j);
+      const float4 e = *reinterpret_cast<const float4*>(emb + s_tok[ri] * d + j);
       const float4 p = *reinterpret_cast<const float4*>(pos + (int64_t)nxt * d + j);
       float4 v;
       v.x = fadd_rn(fmul_rn(e.x, emb_scale), p.x);

@@ -338,6 +338,38 @@ def test_retrieve_per_row_k_vs_oracle(P, O, V):
         assert abs(lse[b] - orr.logsumexp_full[0]) <= 1e-7 * abs(orr.logsumexp_full[0]) + 1e-7
 
 
+@pytest.mark.parametrize("rows,V", [(1, 250000), (3, 32000), (7, 2048), (512, 32000),
+                                    (1200, 32000), (64, 128000)])
+def test_retrieve_shapes_per_row_k_vs_oracle(P, O, rows, V):
+    """Stage 1 through d_k at the HARS microbench's shape range (single long
+    rows to more rows than resident CTAs), per-row k including 0, tie-heavy
+    and all-equal rows: bit-exact maxima, thresholds and ordered candidates."""
+    import torch
+    from paper_2010_13887_b200 import decode as D
+    rng = np.random.default_rng(rows * 7 + V)
+    L = (rng.normal(size=(rows, V)) * 3).astype(F32)
+    if rows > 5:
+        L[2] = np.round(L[2])
+        L[4, :] = 0.25
+    ks = rng.integers(1, 17, size=rows).astype(np.int32)
+    if rows > 2:
+        ks[1] = 0
+    gm, th, lse, ci, cc = D.retrieve_device(torch.from_numpy(L).cuda(), 16,
+                                            d_k=torch.from_numpy(ks).cuda())
+    torch.cuda.synchronize()
+    gm, th, lse, ci, cc = (t.cpu().numpy() for t in (gm, th, lse, ci, cc))
+    check = [i for i in range(rows) if i < 8 or i % 97 == 0]
+    for b in check:
+        if ks[b] == 0:
+            assert cc[b] == 0
+            continue
+        orr = O.retrieve(L[b:b + 1], int(ks[b]))
+        assert np.array_equal(gm[b, :ks[b]], orr.group_maxima[0]), b
+        assert th[b] == orr.threshold[0], b
+        assert np.array_equal(ci[b, :cc[b]], orr.candidate_tokens[0]), b
+        assert abs(lse[b] - orr.logsumexp_full[0]) <= 1e-7 * abs(orr.logsumexp_full[0]) + 1e-7
+
+
 def test_fused_hars_step_equals_separate_launches(P):
     """fq_hars_step (groups + stage 1 + stage 2 + advance + next embedding in
     one launch) reproduces fq_hars_groups + fq_retrieve + fq_hars_select +
