@@ -196,8 +196,11 @@ int fq_hars_groups(fq_beam_state st, int64_t batch, int64_t beam, int64_t vocab,
  * decode.py:217-240 + model.py:508-512): per row the group count
  * min(K + live, V) (decode.py:230), stage 1 (single-sweep retrieve), and for
  * each item, run by the last of its rows to finish, stage 2 (fq_hars_select
- * semantics); the last item advances *d_cur. counters: int32 [batch + 1],
- * zero-initialised once (they reset themselves). Needs 2*beam <= 32 and
+ * semantics); the last item advances *d_cur. counters: int32
+ * [batch + 1 + batch*beam] (item, all-items and row arrival counters),
+ * zero-initialised once (they reset themselves). For long rows (V >= 64k) or
+ * <= 8 rows stage 1 runs on the balanced split (every CTA of one wave streams
+ * an equal share of the [rows, V] block; the CTA completing a row merges it). Needs 2*beam <= 32 and
  * 16-byte aligned rows; exhaustive search uses the separate entry points.
  * With x_next != NULL the item's rows of the next step's decoder input are
  * also written (embed_scale_pos at position *d_cur + 1, kernels.py:143-151:

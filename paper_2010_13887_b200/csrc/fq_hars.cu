@@ -566,6 +566,482 @@ __global__ void __launch_bounds__(kSwThreads, 4) retrieve_sweep_kernel(
 }
 
 // ---------------------------------------------------------------------------
+// Stage 1, balanced split (k <= 32, V % 4 == 0, V >= 2048; the default).
+// The [rows, V/4] float4 space is cut into G equal contiguous ranges, one per
+// CTA of a single resident wave (G = SMs x resident CTAs, fewer for small
+// problems); a boundary within kMinPortion vectors of a row start/end snaps
+// to it, so every row portion holds >= kMinPortion vectors. So every SM
+// streams the same number of bytes whatever rows vs SMs is (a CTA per row
+// leaves 4-vs-3 rows per SM at 512 rows and idles most SMs at few rows).
+//   * A CTA sweeps each row portion in its range exactly like sweep_row
+//     (pilot bound, strided group maxima, online logsumexp, survivor list)
+//     and leaves a partial inside the row's own candidate row (cand_ld >= V):
+//     its survivors >= its local bound min_g(portion group max) <= R at the
+//     portion's first slots, and a header in its last kHdr slots.
+//   * It then adds its portion length to the row's arrival counter; the CTA
+//     that completes the row merges the partials in column order (group
+//     maxima -> R and M, S = sum_p S_p exp(M_p - M) in fixed order, survivors
+//     >= R ranked by token) into the row's outputs, overwriting the partials.
+// Same results as retrieve_kernel / sweep_row (candidates and group maxima
+// exact, lse to fp32 rounding of the terms).
+// ---------------------------------------------------------------------------
+constexpr int kHdr = 40;           // header slots: [0,32) group maxima, 32 M_p, 33-34 S_p, 35 n, 36 ovf
+constexpr int kMinPortion = 256;   // float4 per row portion (>= kSwThreads: every thread works)
+constexpr int kMaxPortions = 160;   // per row (G <= (kMaxPortions - 2) * rows)
+
+struct SplitGeom {
+  int64_t Q;     // rows * nvec
+  int64_t nvec;  // V / 4
+  int G;         // CTAs
+};
+// Q = rows * nvec < 2^31 (checked on the host): 32-bit row arithmetic; c*Q/G
+// in double is exact (c*Q < 2^53; a non-integer quotient is >= 1/G away from
+// the next integer, far above the double ulp at < 2^31).
+__host__ __device__ __forceinline__ int64_t split_bound(const SplitGeom& g, int64_t c) {
+  if (c <= 0) return 0;
+  if (c >= g.G) return g.Q;
+  const uint32_t x = (uint32_t)(((double)c * (double)g.Q) / (double)g.G);
+  const uint32_t nv = (uint32_t)g.nvec;
+  const uint32_t r = x / nv;
+  uint32_t off = x - r * nv;
+  if (off < (uint32_t)kMinPortion) off = 0;
+  else if (nv - off < (uint32_t)kMinPortion) off = nv;
+  return (int64_t)r * nv + off;
+}
+// the CTA whose range holds float4 position p (0 <= p < Q)
+__device__ __forceinline__ int split_find(const SplitGeom& g, int64_t p) {
+  int c = (int)(((double)p * (double)g.G) / (double)g.Q) - 2;
+  if (c < 0) c = 0;
+  while (c + 1 < g.G && split_bound(g, c + 1) <= p) ++c;
+  return c;
+}
+
+__device__ __forceinline__ int f2ord(float f) {
+  const int i = __float_as_int(f);
+  return i >= 0 ? i : i ^ 0x7fffffff;
+}
+__device__ __forceinline__ float ord2f(int i) { return __int_as_float(i >= 0 ? i : i ^ 0x7fffffff); }
+
+
+struct __align__(16) SplitSmem {
+  float wsc[kSwThreads / 32][128];  // per-warp group-maxima scratch
+  int32_t sv_idx[kSurvCap];
+  float sv_val[kSurvCap];
+  float gmax[32];
+  int gmax_ord[32];                 // CTA group maxima (ordered ints, atomicMax)
+  double red[kSwThreads / 32];
+  int warp_tot[32];
+  int cnt, n, total, ovf, c_first, np;
+  float R, M;
+  double S;
+};
+
+__device__ __forceinline__ int lattice_T(int k) {
+  const int kk = k / (k & -k) * ((k & -k) > 4 ? (k & -k) / 4 : 1);  // k / gcd(k, 4)
+  return kSwThreads - kSwThreads % kk;
+}
+
+// Sweep float4 columns [a, b) of one row (x = row base) with k groups; write
+// the partial into crow (the row's candidate slots). As sweep_row: a
+// per-thread cp.async ring, a CTA pilot (the first kSwU vectors per thread)
+// for the survivor bound R' <= R and the logsumexp reference m, which stays
+// fixed (terms exp(x - m) up to e^64 are exact enough in fp32/f64; moving it
+// with every new maximum costs a divergent f64 exp per record, measured +20%
+// on the sweep in scripts/micro/streamprobe.cu).
+__device__ __forceinline__ void sweep_portion(const float* __restrict__ x, const int a, const int b,
+                                              const int k, int32_t* __restrict__ crow,
+                                              float4* __restrict__ ring, SplitSmem& sm) {
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int T = lattice_T(k);
+  const bool act = tid < T;
+  constexpr float NEG = -INFINITY;
+  constexpr float L2E = 1.4426950408889634f;
+  constexpr float L2E_LO = 1.925963033500011e-08f;  // log2(e) - L2E
+  constexpr double L2E_D = 1.4426950408889634;
+  float* part_max = &sm.wsc[0][0];
+  // thread t owns float4 columns t + T*i (the row-global lattice): lane c of
+  // its vectors is always in group (4t + c) % k
+  int nit = 0, v0 = 0;
+  if (act) {
+    const int i0 = a > tid ? (a - tid + T - 1) / T : 0;
+    v0 = tid + i0 * T;
+    nit = v0 < b ? (b - 1 - v0) / T + 1 : 0;
+  }
+  const float4* xb = reinterpret_cast<const float4*>(x) + v0;
+#pragma unroll
+  for (int i = 0; i < kSwP; ++i) {
+    if (i < nit) cp_async16(ring + i * kSwThreads + tid, xb + i * T);
+    cp_async_commit();
+  }
+  if (tid == 0) { sm.cnt = 0; sm.n = 0; }
+  // ---- pilot: partial group maxima of the first kSwU vectors -> R', m ----
+  float gm[4] = {NEG, NEG, NEG, NEG};
+  cp_async_wait<kSwP - kSwU>();
+#pragma unroll
+  for (int u = 0; u < kSwU; ++u) {
+    if (u < nit) {
+      const float4 e = ring[u * kSwThreads + tid];
+      gm[0] = fmaxf(gm[0], e.x); gm[1] = fmaxf(gm[1], e.y);
+      gm[2] = fmaxf(gm[2], e.z); gm[3] = fmaxf(gm[3], e.w);
+    }
+  }
+  if (act) {
+    part_max[4 * tid] = gm[0]; part_max[4 * tid + 1] = gm[1];
+    part_max[4 * tid + 2] = gm[2]; part_max[4 * tid + 3] = gm[3];
+  }
+  __syncthreads();
+  for (int gg = w; gg < k; gg += kSwThreads / 32) {
+    float mm = NEG;
+    for (int e = gg + lane * k; e < 4 * T; e += 32 * k) mm = fmaxf(mm, part_max[e]);
+    mm = warp_max(mm);
+    if (lane == 0) sm.gmax[gg] = mm;
+  }
+  __syncthreads();
+  if (w == 0) {
+    const float gv = lane < k ? sm.gmax[lane] : INFINITY;
+    const float R = warp_min(gv);
+    const float M = warp_max(lane < k ? gv : NEG);
+    if (lane == 0) { sm.R = R; sm.M = M; }
+  }
+  __syncthreads();
+  const float Rp = sm.R;
+  float m = sm.M;
+  float mL = m * L2E;
+  double s = 0.0;
+  for (int i = 0; i < nit; ++i) {
+    cp_async_wait<kSwP - 1>();
+    float4* slot = ring + (i % kSwP) * kSwThreads + tid;
+    const float4 e = *slot;
+    if (i + kSwP < nit) cp_async16(slot, xb + (i + kSwP) * T);
+    cp_async_commit();
+    if (i >= kSwU) {
+      gm[0] = fmaxf(gm[0], e.x); gm[1] = fmaxf(gm[1], e.y);
+      gm[2] = fmaxf(gm[2], e.z); gm[3] = fmaxf(gm[3], e.w);
+    }
+    const float m4 = fmaxf(fmaxf(e.x, e.y), fmaxf(e.z, e.w));
+    if (m4 > m + 64.f || m == NEG) {  // (practically never for logits)
+      if (m4 != NEG) {
+        s = m == NEG ? 0.0 : s * exp2((double)mL - (double)m4 * L2E_D);
+        m = m4;
+        mL = m * L2E;
+      }
+    }
+    // exp(x - m_eff) = 2^(x log2e - mL), m_eff = mL / log2e, log2e as hi + lo
+    // fp32 parts (argument exact to ~1 ulp); terms below 2^-126 flush to 0
+    if (m != NEG) {
+      const float t4 = (ex2_ftz(fmaf(e.x, L2E_LO, fmaf(e.x, L2E, -mL))) +
+                        ex2_ftz(fmaf(e.y, L2E_LO, fmaf(e.y, L2E, -mL)))) +
+                       (ex2_ftz(fmaf(e.z, L2E_LO, fmaf(e.z, L2E, -mL))) +
+                        ex2_ftz(fmaf(e.w, L2E_LO, fmaf(e.w, L2E, -mL))));
+      s += (double)t4;
+    }
+    if (m4 >= Rp) {
+      const int v = v0 + i * T;
+      const float e4[4] = {e.x, e.y, e.z, e.w};
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        if (e4[c] >= Rp) {
+          const int p = atomicAdd(&sm.cnt, 1);
+          if (p < kSurvCap) { sm.sv_idx[p] = 4 * v + c; sm.sv_val[p] = e4[c]; }
+        }
+      }
+    }
+  }
+  cp_async_wait<0>();
+  if (act) {
+    part_max[4 * tid] = gm[0]; part_max[4 * tid + 1] = gm[1];
+    part_max[4 * tid + 2] = gm[2]; part_max[4 * tid + 3] = gm[3];
+  }
+  __syncthreads();
+  for (int gg = w; gg < k; gg += kSwThreads / 32) {
+    float mm = NEG;
+    for (int e = gg + lane * k; e < 4 * T; e += 32 * k) mm = fmaxf(mm, part_max[e]);
+    mm = warp_max(mm);
+    if (lane == 0) sm.gmax[gg] = mm;
+  }
+  __syncthreads();
+  if (w == 0) {
+    const float gv = lane < k ? sm.gmax[lane] : INFINITY;
+    const float R = warp_min(gv);
+    const float M = warp_max(lane < k ? gv : NEG);
+    if (lane == 0) { sm.R = R; sm.M = M; }
+  }
+  __syncthreads();
+  const float Rl = sm.R, Mp = sm.M;  // local bound Rl <= R (maxima only grow)
+  const double Sp =
+      block_sum(m == NEG ? 0.0 : s * exp2((double)mL - (double)Mp * L2E_D), sm.red);
+  const int nsv = sm.cnt;
+  const int cap = (4 * (b - a) - kHdr) / 2;
+  int32_t* sidx = crow + 4 * a;
+  int32_t* sval = sidx + cap;
+  if (nsv <= kSurvCap) {
+    for (int i = tid; i < nsv; i += kSwThreads) {
+      const float v = sm.sv_val[i];
+      if (v >= Rl) {
+        const int p = atomicAdd(&sm.n, 1);
+        if (p < cap) { sidx[p] = sm.sv_idx[i]; sval[p] = __float_as_int(v); }
+      }
+    }
+  }
+  __syncthreads();
+  int32_t* hdr = crow + 4 * b - kHdr;
+  if (tid < k) hdr[tid] = __float_as_int(sm.gmax[tid]);
+  if (tid == 0) {
+    hdr[32] = __float_as_int(Mp);
+    const long long sb = __double_as_longlong(Sp);
+    hdr[33] = (int32_t)(sb & 0xffffffffll);
+    hdr[34] = (int32_t)(sb >> 32);
+    hdr[35] = min(sm.n, cap);
+    hdr[36] = (nsv > kSurvCap || sm.n > cap) ? 1 : 0;
+  }
+}
+
+// Merge the partials of row `row` (all portions arrived). x = row base.
+__device__ __forceinline__ void finalize_split_row(
+    const SplitGeom& g, const int64_t row, const int k, const float* __restrict__ x,
+    int32_t* __restrict__ crow, float* __restrict__ group_max, int64_t gm_ld,
+    float* __restrict__ threshold, double* __restrict__ lse, int64_t* __restrict__ cand_count,
+    int64_t cand_ld, int64_t vals_off, void* dyn, SplitSmem& sm) {
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int V = (int)(g.nvec * 4);
+  if (k <= 0) {
+    if (tid == 0) cand_count[row] = 0;
+    return;
+  }
+  const int64_t rs = row * g.nvec, re = rs + g.nvec;
+  // portion table in the warp scratch (the ring may be streaming the CTA's
+  // next portion): S as double, a, b, n as int, M as float
+  (void)dyn;
+  double* pS = reinterpret_cast<double*>(&sm.wsc[0][0]);
+  int* pa = reinterpret_cast<int*>(pS + kMaxPortions);
+  int* pb = pa + kMaxPortions;
+  int* pn = pb + kMaxPortions;
+  float* pM = reinterpret_cast<float*>(pn + kMaxPortions);
+  if (tid == 0) {
+    const int c0 = split_find(g, rs), c1 = split_find(g, re - 1);
+    sm.c_first = c0;
+    sm.np = min(c1 - c0 + 1, kMaxPortions);
+    sm.ovf = c1 - c0 + 1 > kMaxPortions ? 1 : 0;
+    sm.cnt = 0;
+  }
+  if (tid < 32) sm.gmax_ord[tid] = f2ord(-INFINITY);
+  __syncthreads();
+  const int np = sm.np;
+  for (int j = tid; j < np; j += kSwThreads) {
+    const int64_t c = sm.c_first + j;
+    pa[j] = (int)(max(split_bound(g, c), rs) - rs);
+    pb[j] = (int)(min(split_bound(g, c + 1), re) - rs);
+  }
+  __syncthreads();
+  // per-portion group maxima table in the (idle) survivor lists (sv_idx and
+  // sv_val are adjacent: 2 * kSurvCap floats; the host keeps np * k within it)
+  float* pgm = reinterpret_cast<float*>(sm.sv_idx);
+  // every header word of every portion in one round trip: word w of a portion
+  // is group maximum w (< k) or one of M, S lo, S hi, n, ovf; the loads of a
+  // thread's words are all issued before any is used
+  {
+    const int nw = k + 5, total = np * nw;
+    for (int e0 = tid; e0 < total; e0 += 4 * kSwThreads) {
+      int v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int e = e0 + u * kSwThreads;
+        if (e < total) {
+          const int j = e / nw, wq = e - j * nw;
+          v[u] = __ldcg(crow + 4 * pb[j] - kHdr + (wq < k ? wq : 32 + (wq - k)));
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int e = e0 + u * kSwThreads;
+        if (e >= total) continue;
+        const int j = e / nw, wq = e - j * nw;
+        if (wq < k) pgm[j * k + wq] = __int_as_float(v[u]);  // reduced per group below
+        else if (wq == k) pM[j] = __int_as_float(v[u]);
+        else if (wq == k + 1) reinterpret_cast<int*>(pS + j)[0] = v[u];
+        else if (wq == k + 2) reinterpret_cast<int*>(pS + j)[1] = v[u];
+        else if (wq == k + 3) pn[j] = v[u];
+        else if (v[u]) sm.ovf = 1;
+      }
+    }
+  }
+  __syncthreads();
+  for (int gq = w; gq < k; gq += kSwThreads / 32) {  // warp per group: max over portions
+    float mm = -INFINITY;
+    for (int j = lane; j < np; j += 32) mm = fmaxf(mm, pgm[j * k + gq]);
+    mm = warp_max(mm);
+    if (lane == 0) sm.gmax[gq] = mm;
+  }
+  __syncthreads();
+  if (w == 0) {
+    const float gv = lane < k ? sm.gmax[lane] : INFINITY;
+    if (lane < k && group_max) group_max[row * gm_ld + lane] = gv;
+    const float R = warp_min(gv);
+    const float M = warp_max(lane < k ? gv : -INFINITY);
+    if (lane == 0) { sm.R = R; sm.M = M; }
+  }
+  __syncthreads();
+  // exclusive prefix of the portions' survivor counts (np <= kMaxPortions <=
+  // kSwThreads: one per thread) for the flattened gather below; a portion whose
+  // maximum is below R holds no survivor >= R and is skipped
+  const int my_n = tid < np && pM[tid] >= sm.R ? pn[tid] : 0;
+  const int my_off = block_excl_scan(my_n, sm.warp_tot, &sm.total);  // contains syncs
+  const int n_all = sm.total;
+  __shared__ int s_cap[kMaxPortions], s_base[kMaxPortions];
+  if (tid < np) {
+    s_cap[tid] = (4 * (pb[tid] - pa[tid]) - kHdr) / 2;
+    s_base[tid] = 4 * pa[tid];
+  }
+  __syncthreads();
+  if (tid < np) pn[tid] = my_off;  // pn now holds the exclusive prefix
+  __syncthreads();
+  const float R = sm.R, M = sm.M;
+  double acc = 0.0;
+  for (int j = tid; j < np; j += kSwThreads)  // fixed assignment + fixed tree: deterministic
+    acc += pS[j] == 0.0 ? 0.0 : pS[j] * exp((double)pM[j] - (double)M);
+  const double S = block_sum(acc, sm.red);
+  sw_stamp(blockIdx.x, 6);
+  // survivors >= R of every portion, flattened over all threads (binary search
+  // of the portion in the prefix), loads issued ahead of use
+  if (!sm.ovf) {
+    for (int e0 = tid; e0 < n_all; e0 += 2 * kSwThreads) {
+      float v[2];
+      int ix[2];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int e = e0 + u * kSwThreads;
+        v[u] = -INFINITY;
+        if (e < n_all) {
+          int lo = 0, hi = np - 1;  // last j with pn[j] <= e
+          while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (pn[mid] <= e) lo = mid; else hi = mid - 1;
+          }
+          const int i = e - pn[lo];
+          const int32_t* sidx = crow + s_base[lo];
+          v[u] = __int_as_float(__ldcg(sidx + s_cap[lo] + i));
+          ix[u] = __ldcg(sidx + i);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        if (e0 + u * kSwThreads < n_all && v[u] >= R) {
+          const int p = atomicAdd(&sm.cnt, 1);
+          if (p < kSurvCap) { sm.sv_idx[p] = ix[u]; sm.sv_val[p] = v[u]; }
+        }
+      }
+    }
+  }
+  __syncthreads();  // every partial read before the row is overwritten below
+  sw_stamp(blockIdx.x, 7);
+  const int n = sm.cnt;
+  if (!sm.ovf && n <= kSurvCap) {
+    for (int i = tid; i < n; i += kSwThreads) {
+      const int j = sm.sv_idx[i];
+      int rk = 0;
+      for (int q = 0; q < n; ++q) rk += sm.sv_idx[q] < j ? 1 : 0;
+      if (rk < cand_ld) crow[rk] = j;
+      if (vals_off && rk < vals_off) crow[vals_off + rk] = __float_as_int(sm.sv_val[i]);
+    }
+    if (tid == 0) cand_count[row] = n;
+  } else {
+    // ordered block-scan compaction over the whole row (tie-heavy rows)
+    int64_t cb = 0;
+    const int chunk = kSwThreads * 4;
+    for (int c0 = 0; c0 < V; c0 += chunk) {
+      int flags = 0;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int j = c0 + tid * 4 + c;
+        if (j < V && x[j] >= R) flags |= 1 << c;
+      }
+      if (!__syncthreads_or(flags)) continue;
+      int off = block_excl_scan(__popc(flags), sm.warp_tot, &sm.total);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        if (flags & (1 << c)) {
+          const int64_t pos = cb + off;
+          const int j = c0 + tid * 4 + c;
+          if (pos < cand_ld) crow[pos] = j;
+          if (vals_off && pos < vals_off) crow[vals_off + pos] = __float_as_int(x[j]);
+          ++off;
+        }
+      }
+      cb += sm.total;
+      __syncthreads();
+    }
+    if (tid == 0) cand_count[row] = cb;
+  }
+  if (tid == 0) {
+    if (threshold) threshold[row] = R;
+    lse[row] = (double)M + log(S);
+  }
+}
+
+// Walk this CTA's range; for each row portion: sweep, arrive, and (if it
+// completed the row) finalize + on_row(row).
+template <typename OnRow, typename KOf>
+__device__ __forceinline__ void split_walk(const SplitGeom& g, const float* __restrict__ logits,
+                                           int64_t ld, int32_t* __restrict__ cand_idx,
+                                           int64_t cand_ld, int* row_ctr, int ctr_stride,
+                                           bool self_reset, float4* ring, SplitSmem& sm,
+                                           KOf k_of, OnRow on_row) {
+  __shared__ int s_last;
+  const int64_t A = split_bound(g, blockIdx.x), B = split_bound(g, blockIdx.x + 1);
+  int64_t p = A;
+  int nport = 0;
+  sw_stamp(blockIdx.x, 0);
+  while (p < B) {
+    const int64_t row = p / g.nvec;
+    const int64_t rs = row * g.nvec;
+    const int a = (int)(p - rs);
+    const int b = (int)(min(B, rs + g.nvec) - rs);
+    const int k = k_of(row);
+    const float* x = logits + row * ld;
+    int32_t* crow = cand_idx + row * cand_ld;
+    if (k > 0) sweep_portion(x, a, b, k, crow, ring, sm);
+    sw_stamp(blockIdx.x, 1 + min(nport++, 1));
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      int* ctr = row_ctr + row * ctr_stride;
+      const int prev = atomicAdd(ctr, b - a);
+      s_last = prev + (b - a) == (int)g.nvec;
+      if (s_last && self_reset) *ctr = 0;
+    }
+    __syncthreads();
+    if (s_last) {
+      __threadfence();
+      sw_stamp(blockIdx.x, 3);
+      on_row(row, k, x, crow);
+      sw_stamp(blockIdx.x, 4);
+    }
+    __syncthreads();
+    p = rs + b;
+  }
+  sw_stamp(blockIdx.x, 5);
+}
+
+__global__ void __launch_bounds__(kSwThreads, 4) retrieve_split_kernel(
+    const float* __restrict__ logits, int64_t ld, SplitGeom g, int k_fixed,
+    const int32_t* __restrict__ d_k, float* __restrict__ group_max, int64_t gm_ld,
+    float* __restrict__ threshold, double* __restrict__ lse, int32_t* __restrict__ cand_idx,
+    int64_t cand_ld, int64_t* __restrict__ cand_count) {
+  pdl_enter();
+  extern __shared__ __align__(16) float4 sw_ring[];
+  __shared__ SplitSmem sm;
+  // arrival counters: the low words of cand_count (zeroed by the launcher)
+  split_walk(
+      g, logits, ld, cand_idx, cand_ld, reinterpret_cast<int*>(cand_count), 2, false, sw_ring, sm,
+      [&](int64_t row) { return d_k ? d_k[row] : k_fixed; },
+      [&](int64_t row, int k, const float* x, int32_t* crow) {
+        finalize_split_row(g, row, k, x, crow, group_max, gm_ld, threshold, lse, cand_count,
+                           cand_ld, 0, sw_ring, sm);
+      });
+}
+
+
+// ---------------------------------------------------------------------------
 // stage 2
 // ---------------------------------------------------------------------------
 constexpr int kSelThreads = 256;
@@ -839,6 +1315,59 @@ __global__ void __launch_bounds__(kSelThreads) hars_select_kernel(
               len_pow, d_cur, max_steps, row_tokens, row_parents, hist);
 }
 
+// Stage 2 of item b (whole CTA), then the item's rows of the next step's
+// decoder input (embed_scale_pos, kernels.py:143-151: fp32 emb * sqrt(d), then
+// + PE[cur + 1], two roundings), so the decode step needs no separate
+// embedding launch; the last item advances the position. cur0: *d_cur as read
+// at kernel start (advanced only after every item passed here).
+__device__ __forceinline__ void stage2_and_next(
+    const int b, const float* __restrict__ logits, int64_t ld, const double* lse,
+    const int32_t* cand_idx, int64_t cand_ld, const int64_t* cand_count, fq_beam_state st,
+    int K, int max_len, int eos, const double* __restrict__ len_pow, int32_t* d_cur,
+    int64_t max_steps, int64_t* row_tokens, int64_t* row_parents, int32_t* hist,
+    const int64_t vals_off, const int cur0, const float* __restrict__ emb, int d,
+    float emb_scale, const float* __restrict__ pos, float* __restrict__ x_next,
+    __nv_bfloat16* __restrict__ x16_next, int batch, int* all_cnt) {
+  __shared__ int64_t s_tok[kMaxBeam];
+  select_item(b, logits, ld, lse, cand_idx, cand_ld, cand_count, st, K, max_len, eos, len_pow,
+              d_cur, max_steps, row_tokens, row_parents, hist, vals_off, s_tok);
+  __syncthreads();
+  // next step's embedding of the item's rows (embed_scale_pos, kernels.py:143-151:
+  // fp32 emb * sqrt(d), then + PE[cur + 1], two roundings), so the decode step
+  // needs no separate embedding launch
+  const int nxt = cur0 + 1;
+  if (x_next && nxt < max_len) {
+    const int d4 = d >> 2;  // d % 4 == 0 (checked on the host)
+    for (int idx = threadIdx.x; idx < K * d4; idx += blockDim.x) {
+      const int ri = idx / d4, j = 4 * (idx - ri * d4);
+      const int64_t r = (int64_t)b * K + ri;
+      const float4 e = *reinterpret_cast<const float4*>(emb + s_tok[ri] * d + j);
+      const float4 p = *reinterpret_cast<const float4*>(pos + (int64_t)nxt * d + j);
+      float4 v;
+      v.x = fadd_rn(fmul_rn(e.x, emb_scale), p.x);
+      v.y = fadd_rn(fmul_rn(e.y, emb_scale), p.y);
+      v.z = fadd_rn(fmul_rn(e.z, emb_scale), p.z);
+      v.w = fadd_rn(fmul_rn(e.w, emb_scale), p.w);
+      *reinterpret_cast<float4*>(x_next + r * d + j) = v;
+      if (x16_next) {
+        __nv_bfloat162 lo = __floats2bfloat162_rn(v.x, v.y), hi = __floats2bfloat162_rn(v.z, v.w);
+        uint2 pk;
+        pk.x = *reinterpret_cast<uint32_t*>(&lo);
+        pk.y = *reinterpret_cast<uint32_t*>(&hi);
+        *reinterpret_cast<uint2*>(x16_next + r * d + j) = pk;
+      }
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(all_cnt, 1) == batch - 1) {  // every item read d_cur: advance it
+      *all_cnt = 0;
+      *d_cur += 1;
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // The whole HARS step in one launch (decode step, k = min(K + live, V) <= 32):
 // CTA per beam row derives its group count from the beam state
@@ -878,44 +1407,58 @@ __global__ void __launch_bounds__(kSwThreads) hars_step_kernel(
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  __shared__ int64_t s_tok[kMaxBeam];
-  select_item(b, logits, ld, lse, cand_idx, cand_ld, cand_count, st, K, max_len, eos, len_pow,
-              d_cur, max_steps, row_tokens, row_parents, hist, vals_off, s_tok);
-  __syncthreads();
-  // next step's embedding of the item's rows (embed_scale_pos, kernels.py:143-151:
-  // fp32 emb * sqrt(d), then + PE[cur + 1], two roundings), so the decode step
-  // needs no separate embedding launch
-  const int nxt = cur0 + 1;
-  if (x_next && nxt < max_len) {
-    const int d4 = d >> 2;  // d % 4 == 0 (checked on the host)
-    for (int idx = threadIdx.x; idx < K * d4; idx += blockDim.x) {
-      const int ri = idx / d4, j = 4 * (idx - ri * d4);
-      const int64_t r = (int64_t)b * K + ri;
-      const float4 e = *reinterpret_cast<const float4*>(emb + s_tok[ri] * d + j);
-      const float4 p = *reinterpret_cast<const float4*>(pos + (int64_t)nxt * d + j);
-      float4 v;
-      v.x = fadd_rn(fmul_rn(e.x, emb_scale), p.x);
-      v.y = fadd_rn(fmul_rn(e.y, emb_scale), p.y);
-      v.z = fadd_rn(fmul_rn(e.z, emb_scale), p.z);
-      v.w = fadd_rn(fmul_rn(e.w, emb_scale), p.w);
-      *reinterpret_cast<float4*>(x_next + r * d + j) = v;
-      if (x16_next) {
-        __nv_bfloat162 lo = __floats2bfloat162_rn(v.x, v.y), hi = __floats2bfloat162_rn(v.z, v.w);
-        uint2 pk;
-        pk.x = *reinterpret_cast<uint32_t*>(&lo);
-        pk.y = *reinterpret_cast<uint32_t*>(&hi);
-        *reinterpret_cast<uint2*>(x16_next + r * d + j) = pk;
-      }
-    }
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    if (atomicAdd(all_cnt, 1) == batch - 1) {  // every item read d_cur: advance it
-      *all_cnt = 0;
-      *d_cur += 1;
-    }
-  }
+  stage2_and_next(b, logits, ld, lse, cand_idx, cand_ld, cand_count, st, K, max_len, eos,
+                  len_pow, d_cur, max_steps, row_tokens, row_parents, hist, vals_off, cur0, emb,
+                  d, emb_scale, pos, x_next, x16_next, batch, all_cnt);
+}
+
+// The fused HARS step on the balanced split (few rows: rows < 2 x SMs): as
+// hars_step_kernel, but stage 1 runs on split_walk; the CTA that completes a
+// row arrives at its item, the one completing the item runs stage 2 + the
+// next-step embedding. counters: [batch] item, [1] all, [rows] row arrivals.
+__global__ void __launch_bounds__(kSwThreads, 4) hars_step_split_kernel(
+    const float* __restrict__ logits, int64_t ld, SplitGeom g, fq_beam_state st, int batch, int K,
+    int max_len, int eos, const double* __restrict__ len_pow, int32_t* d_cur, int64_t max_steps,
+    double* lse, int32_t* cand_idx, int64_t cand_ld, int64_t* cand_count, int* counters,
+    int64_t* row_tokens, int64_t* row_parents, int32_t* hist, const float* __restrict__ emb,
+    int d, float emb_scale, const float* __restrict__ pos, float* __restrict__ x_next,
+    __nv_bfloat16* __restrict__ x16_next) {
+  pdl_enter();
+  extern __shared__ __align__(16) float4 sw_ring[];  // also stage 2's dynamic smem
+  __shared__ SplitSmem sm;
+  __shared__ int s_item_last;
+  const int V = (int)(g.nvec * 4);
+  const int64_t vals_off = cand_ld / 2 >= kSwThreads * 2 ? cand_ld / 2 : 0;
+  const int cur0 = *d_cur;
+  int* item_cnt = counters;
+  int* all_cnt = counters + batch;
+  int* row_ctr = counters + batch + 1;
+  split_walk(
+      g, logits, ld, cand_idx, cand_ld, row_ctr, 1, true, sw_ring, sm,
+      [&](int64_t row) {
+        const int b = (int)(row / K), i = (int)(row % K);
+        const int live = st.live[b];
+        return (!st.done[b] && i < live) ? min(K + live, V) : 0;  // hars_groups
+      },
+      [&](int64_t row, int k, const float* x, int32_t* crow) {
+        finalize_split_row(g, row, k, x, crow, nullptr, 0, nullptr, lse, cand_count, cand_ld,
+                           vals_off, sw_ring, sm);
+        const int b = (int)(row / K);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          __threadfence();
+          const int prev = atomicAdd(item_cnt + b, 1);
+          s_item_last = prev == K - 1;
+          if (s_item_last) item_cnt[b] = 0;
+        }
+        __syncthreads();
+        if (s_item_last) {
+          __threadfence();
+          stage2_and_next(b, logits, ld, lse, cand_idx, cand_ld, cand_count, st, K, max_len, eos,
+                          len_pow, d_cur, max_steps, row_tokens, row_parents, hist, vals_off,
+                          cur0, emb, d, emb_scale, pos, x_next, x16_next, batch, all_cnt);
+        }
+      });
 }
 
 __global__ void hars_groups_kernel(fq_beam_state st, int batch, int K, int V, int exhaustive,
@@ -970,6 +1513,59 @@ static bool retrieve_two_pass_forced() {
   return v == 1;
 }
 
+static int hars_num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return n;
+}
+
+// Stage 1 on the balanced split when a CTA per row would stream very long rows
+// with few CTAs: V >= 64k, or <= 8 rows (scripts/hars_split_ab.py, graph-timed
+// us, CTA-per-row vs split: 250k x 64 rows 201 vs 39, 250k x 1 row 52 vs 19,
+// 128k x 128 rows 54 vs 39; but 32k x 32..512 rows 14..28 vs 23..39: the
+// split's row merge costs a few dependent L2 round trips per row).
+// FQ_HARS_SPLIT=0/1 forces either (A/B runs and tests).
+static bool use_split(int64_t rows, int64_t vocab, int64_t cand_ld) {
+  if (vocab % 4 != 0 || vocab < 8 * kMinPortion || cand_ld < vocab ||
+      rows * (vocab / 4) >= (1ll << 31))
+    return false;
+  const char* e = getenv("FQ_HARS_SPLIT");
+  if (e && e[0] == '0') return false;
+  if (e && e[0] == '1') return true;
+  return vocab >= 65536 || rows <= 8;
+}
+
+// Grid of the balanced split: one resident wave, every portion >= kMinPortion.
+static SplitGeom split_geom(const void* kernel, size_t smem, int64_t rows, int64_t vocab,
+                            int64_t kmax) {
+  static thread_local const void* c_kernel = nullptr;
+  static thread_local size_t c_smem = 0;
+  static thread_local int c_slots = 0;
+  if (c_kernel != kernel || c_smem != smem) {
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, kSwThreads, smem);
+    c_kernel = kernel;
+    c_smem = smem;
+    c_slots = std::max(1, hars_num_sms()) * std::max(1, occ);
+  }
+  SplitGeom g;
+  g.nvec = vocab / 4;
+  g.Q = rows * g.nvec;
+  int64_t G = c_slots;
+  G = std::min<int64_t>(G, g.Q / (kMinPortion + 1));
+  G = std::min<int64_t>(G, (int64_t)(kMaxPortions - 2) * rows);
+  G = std::min<int64_t>(G, (int64_t)(2 * kSurvCap / kmax - 2) * rows);  // finalize's table
+  G = std::max<int64_t>(1, G);
+  g.G = (int)G;
+  return g;
+}
+
+static size_t split_smem() { return (size_t)kSwP * kSwThreads * sizeof(float4); }
+
 extern "C" int fq_retrieve_debug_timestamps(unsigned long long* p) {
   return cudaMemcpyToSymbol(g_sw_dbg, &p, sizeof(p)) == cudaSuccess ? FQ_OK : FQ_ERR_CUDA;
 }
@@ -986,6 +1582,20 @@ int fq_retrieve(const float* logits, int64_t ld, int64_t rows, int64_t vocab, in
   FQ_CHECK_ARG(!group_max || gm_ld >= (d_k ? vocab : k) || gm_ld >= k, FQ_ERR_DIMENSION,
                "group_max leading dim too small");
   if (rows == 0) return FQ_OK;
+  if (k >= 1 && k <= 32 && (ld % 4) == 0 && ((uintptr_t)logits & 15) == 0 &&
+      !retrieve_two_pass_forced() && use_split(rows, vocab, cand_ld)) {
+    const size_t smem = split_smem();
+    const SplitGeom g = split_geom(reinterpret_cast<const void*>(retrieve_split_kernel), smem,
+                                   rows, vocab, k);
+    // the low words of cand_count are the rows' arrival counters
+    if (cudaMemsetAsync(cand_count, 0, (size_t)rows * sizeof(int64_t), as_stream(stream)) !=
+        cudaSuccess)
+      return launch_status("fq_retrieve");
+    launch_kernel(retrieve_split_kernel, (unsigned)g.G, kSwThreads, smem, as_stream(stream), 1u,
+                  logits, ld, g, (int)k, d_k, group_max, gm_ld, threshold, lse, cand_idx, cand_ld,
+                  cand_count);
+    return launch_status("fq_retrieve");
+  }
   if (k >= 1 && k <= 32 && (ld % 4) == 0 && ((uintptr_t)logits & 15) == 0 &&
       !retrieve_two_pass_forced()) {
     launch_kernel(retrieve_sweep_kernel, (unsigned)(rows * kSwSplit), kSwThreads,
@@ -1043,6 +1653,18 @@ int fq_hars_step(const float* logits, int64_t ld, fq_beam_state st, int64_t batc
                FQ_ERR_DIMENSION,
                "fq_hars_step: next-step embedding needs aligned emb/pos/x and d_model % 4 == 0");
   FQ_CHECK_ARG(eos >= 0 && eos < vocab, FQ_ERR_PARAMETER, "eos token outside vocabulary");
+  if (use_split(batch * beam, vocab, cand_ld)) {
+    const size_t smem = std::max(sel_smem(beam, max_len), split_smem());
+    FQ_CHECK_ARG(smem <= 96 * 1024, FQ_ERR_CAPACITY, "fq_hars_step: max_len too large");
+    const SplitGeom g = split_geom(reinterpret_cast<const void*>(hars_step_split_kernel), smem,
+                                   batch * beam, vocab, std::min<int64_t>(2 * beam, vocab));
+    launch_kernel(hars_step_split_kernel, (unsigned)g.G, kSwThreads, smem, as_stream(stream), 1u,
+                  logits, ld, g, st, (int)batch, (int)beam, (int)max_len, (int)eos, len_pow, d_cur,
+                  max_steps, lse, cand_idx, cand_ld, cand_count, counters, row_tokens,
+                  row_parents, hist, x_next ? emb : nullptr, (int)d_model, emb_scale, pos, x_next,
+                  reinterpret_cast<__nv_bfloat16*>(x16_next));
+    return launch_status("fq_hars_step");
+  }
   const size_t smem = std::max(sel_smem(beam, max_len),
                                (size_t)kSwP * kSwThreads * sizeof(float4));
   FQ_CHECK_ARG(smem <= 96 * 1024, FQ_ERR_CAPACITY, "fq_hars_step: max_len too large");
@@ -1080,7 +1702,11 @@ int fq_hars_prepare(void) {
       cudaFuncSetAttribute(hars_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            96 * 1024) != cudaSuccess ||
       cudaFuncSetAttribute(retrieve_sweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           64 * 1024) != cudaSuccess) {
+                           64 * 1024) != cudaSuccess ||
+      cudaFuncSetAttribute(retrieve_split_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           64 * 1024) != cudaSuccess ||
+      cudaFuncSetAttribute(hars_step_split_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           96 * 1024) != cudaSuccess) {
     set_error("fq_prepare: cannot opt in to large shared memory (hars)");
     return FQ_ERR_CUDA;
   }

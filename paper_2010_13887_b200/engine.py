@@ -192,7 +192,7 @@ class Session:
                            out=bufs.get("hars.len_pow", (self.config.max_seq_len + 1,),
                                         torch.float64)))
             if fused:
-                grp["hcnt"] = bufs.get("hars.counters", (nb + 1,), torch.int32)
+                grp["hcnt"] = bufs.get("hars.counters", (nb + 1 + nr,), torch.int32)
                 grp["hcnt"].zero_()
             groups.append(grp)
 

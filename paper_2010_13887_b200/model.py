@@ -787,7 +787,7 @@ def plan_intermediates(config: ModelConfig, precision: str = "fp32") -> list[Int
         # HARS stage 1 / 2 and the device beam state (whole request)
         add("hars.k", R * 4, end - 2, end)
         add("hars.len_pow", (S + 1) * 8, setup, end)
-        add("hars.counters", (B + 1) * 4, setup, end)
+        add("hars.counters", (B + 1 + R) * 4, setup, end)
         add("hars.lse", R * 8, end - 2, end)
         add("hars.cand_idx", R * V * 4, end - 2, end)
         add("hars.cand_count", R * 8, end - 2, end)

@@ -13,7 +13,7 @@ from paper_2010_13887_b200 import _abi, decode as D
 
 lib = _abi.load()
 lib.fq_retrieve_debug_timestamps.argtypes = [ctypes.c_void_p]
-B, K, V, S = 128, 4, 32000, 64
+B, K, V, S = (int(x) for x in os.environ.get("SHAPE", "128,4,32000,64").split(","))
 R = B * K
 lgs = [torch.randn(R, V, device="cuda") for _ in range(3)]
 hk = torch.full((R,), 8, dtype=torch.int32, device="cuda")
@@ -22,14 +22,14 @@ dbg = torch.zeros(NC * 8, dtype=torch.int64, device="cuda")
 
 
 def report(tag):
-    t = dbg.view(NC, 8)[:, :6].cpu().numpy().astype(np.float64)
+    t = dbg.view(NC, 8)[:, :8].cpu().numpy().astype(np.float64)
     used = t[:, 0] > 0
     t = t[used]
     t0 = t[:, 0].min()
     rel = np.where(t > 0, (t - t0) / 1e3, np.nan)
     print(f"[{tag}] CTAs {used.sum()}: start skew max {np.nanmax(rel[:, 0]):.2f} us, "
           f"end max {np.nanmax(rel[:, 5]):.2f} us")
-    for i, n in enumerate(["start", "portion1", "portion2", "final0", "final1", "end"]):
+    for i, n in enumerate(["start", "portion1", "portion2", "final0", "final1", "end", "fin_sums", "fin_surv"]):
         c = rel[:, i]
         c = c[~np.isnan(c)]
         if len(c):

@@ -370,11 +370,41 @@ def test_retrieve_shapes_per_row_k_vs_oracle(P, O, rows, V):
         assert abs(lse[b] - orr.logsumexp_full[0]) <= 1e-7 * abs(orr.logsumexp_full[0]) + 1e-7
 
 
-def test_fused_hars_step_equals_separate_launches(P):
+@pytest.mark.parametrize("split", ["0", "1"])
+@pytest.mark.parametrize("rows,V", [(24, 32000), (600, 32000)])
+def test_retrieve_split_and_per_row_paths_agree(P, O, rows, V, split, monkeypatch):
+    """Both stage-1 layouts (balanced split across every CTA / a CTA per row)
+    forced on the same rows: identical candidates and maxima, lse to fp32
+    rounding of the terms, and the oracle on a sample."""
+    import torch
+    from paper_2010_13887_b200 import decode as D
+    monkeypatch.setenv("FQ_HARS_SPLIT", split)
+    rng = np.random.default_rng(rows + V)
+    L = (rng.normal(size=(rows, V)) * 2).astype(F32)
+    L[3] = np.round(L[3])
+    ks = rng.integers(1, 17, size=rows).astype(np.int32)
+    ks[1] = 0
+    gm, th, lse, ci, cc = D.retrieve_device(torch.from_numpy(L).cuda(), 16,
+                                            d_k=torch.from_numpy(ks).cuda())
+    torch.cuda.synchronize()
+    gm, th, lse, ci, cc = (t.cpu().numpy() for t in (gm, th, lse, ci, cc))
+    assert cc[1] == 0
+    for b in [0, 2, 3, 5, rows // 2, rows - 1]:
+        orr = O.retrieve(L[b:b + 1], int(ks[b]))
+        assert np.array_equal(gm[b, :ks[b]], orr.group_maxima[0]), b
+        assert th[b] == orr.threshold[0], b
+        assert np.array_equal(ci[b, :cc[b]], orr.candidate_tokens[0]), b
+        assert abs(lse[b] - orr.logsumexp_full[0]) <= 1e-7 * abs(orr.logsumexp_full[0]) + 1e-7
+
+
+@pytest.mark.parametrize("split", ["1", "0"])
+def test_fused_hars_step_equals_separate_launches(P, split, monkeypatch):
     """fq_hars_step (groups + stage 1 + stage 2 + advance + next embedding in
     one launch) reproduces fq_hars_groups + fq_retrieve + fq_hars_select +
-    fq_step_advance step for step, including EOS picks and a length penalty."""
+    fq_step_advance step for step, including EOS picks and a length penalty
+    (both stage-1 layouts forced: "1" balanced split, "0" CTA per row)."""
     import torch
+    monkeypatch.setenv("FQ_HARS_SPLIT", split)
     from paper_2010_13887_b200 import _abi, decode as D
     B, K, V, S, d, eos = 6, 4, 32000, 16, 64, 7
     R = B * K
