@@ -238,6 +238,53 @@ def retrieve(logits, k):
 
 
 # ---------------------------------------------------------------------------
+# sampling output layer  (decode.py:378-430)
+# ---------------------------------------------------------------------------
+
+def draw(tokens, probs, rng):
+    """decode.py:378-386: r = U * sum(probs) (numpy sum), first prefix with
+    cumulative mass >= r (sequential Python float sum)."""
+    r = rng.random() * probs.sum()
+    c = 0.0
+    for t, p in zip(tokens, probs):
+        c += p
+        if r <= c:
+            return int(t)
+    return int(tokens[-1])
+
+
+def _sorted_survivors(rr, b=0):
+    toks, lgs = rr.candidate_tokens[b], rr.candidate_logits[b]
+    order = np.lexsort((toks, -lgs.astype(F64)))   # (-logit, token)
+    return toks[order], lgs[order]
+
+
+def sample_top_k(row, k, rng):
+    """decode.py:399-409: the true top-k from one retrieve with k groups."""
+    rr = retrieve(np.atleast_2d(row), min(k, np.shape(row)[-1]))
+    toks, lgs = _sorted_survivors(rr)
+    toks, lgs = toks[:k], lgs[:k]
+    return draw(toks, np.exp(lgs.astype(F64) - rr.logsumexp_full[0]), rng)
+
+
+def sample_top_p(row, p, rng):
+    """decode.py:412-430: survivors of min(32, V) groups, escalated x8 until
+    their cumulative mass reaches p; nucleus = shortest sorted prefix >= p."""
+    row = np.atleast_2d(row)
+    V = row.shape[1]
+    groups = min(32, V)
+    while True:
+        rr = retrieve(row, groups)
+        toks, lgs = _sorted_survivors(rr)
+        probs = np.exp(lgs.astype(F64) - rr.logsumexp_full[0])
+        cum = np.cumsum(probs)
+        if cum.size and (cum[-1] >= p or groups == V):
+            cut = min(int(np.searchsorted(cum, p, side="left")), cum.size - 1)
+            return draw(toks[:cut + 1], probs[:cut + 1], rng)
+        groups = min(groups * 8, V)
+
+
+# ---------------------------------------------------------------------------
 # beam state + HARS selection  (decode.py:99-240)
 # ---------------------------------------------------------------------------
 
@@ -450,12 +497,16 @@ class OracleModel:
         return out
 
     def generate(self, src, beam_size=4, max_steps=32, eos=2, alpha=0.0, lengths=None,
-                 bos=1, method="beam", exhaustive=False):
-        """engine.py:81-173 (beam / greedy): returns per item a list of
+                 bos=1, method="beam", exhaustive=False, sample_k=1, sample_p=1.0, seed=0):
+        """engine.py:81-173 (beam / greedy; top_k / top_p through
+        _sampling_step, engine.py:197-216, one PCG64 stream seeded with
+        ``seed`` consumed item by item): returns per item a list of
         (tokens, score), best first."""
         src = np.asarray(src, I64)
         batch, seq = src.shape
-        K = 1 if method == "greedy" else beam_size
+        sampling = method in ("top_k", "top_p")
+        K = 1 if method in ("greedy", "top_k", "top_p") else beam_size
+        rng = np.random.default_rng(seed)
         rows = batch * K
         mem = self.encode(src, lengths)
         mask = lengths_mask(lengths, seq) if lengths is not None else None
@@ -477,7 +528,18 @@ class OracleModel:
                 parents[r0:r0 + K] = r0
                 if done[b]:
                     continue
-                st = step_fn(states[b], logits[r0:r0 + states[b].live], K, eos, alpha)
+                if sampling:
+                    old = states[b]
+                    tok = (sample_top_k(logits[r0], sample_k, rng) if method == "top_k"
+                           else sample_top_p(logits[r0], sample_p, rng))
+                    st = OBeamState(prefixes=[old.prefixes[0] + [tok]], cum_log_prob=[0.0],
+                                    finished=list(old.finished), step=old.step + 1,
+                                    parents=[0], last_tokens=[tok])
+                    if tok == eos:
+                        st.finished.append((st.prefixes[0], 0.0))
+                        st.prefixes = []
+                else:
+                    st = step_fn(states[b], logits[r0:r0 + states[b].live], K, eos, alpha)
                 states[b] = st
                 if st.should_stop(K, alpha) or last or not st.prefixes:
                     done[b] = True

@@ -137,6 +137,10 @@ class Session:
             raise InputError(f"source tokens must be [batch, seq], got {tuple(src.shape)}")
         if self.config.num_decoder_layers < 1:
             raise InputError("generation requires a decoder")
+        if cfg.method in ("top_k", "top_p"):
+            if return_device_state:
+                raise EngineError("sampling returns host hypotheses only")
+            return self._generate_sampling(src, src_lengths, cfg, bos_token)
         if cfg.method not in ("beam", "greedy"):
             raise EngineError(f"decode method {cfg.method!r} is not on the B200 device path yet "
                               "(SURVEY §8(f))")
@@ -279,6 +283,98 @@ class Session:
         states = result.host_items()
         return [[Hypothesis(tokens=s, score=sc) for s, sc in state.finalize(cfg)]
                 for state in states]
+
+    # ------------------------------------------------------------------
+    def _generate_sampling(self, src, src_lengths, cfg: D.DecodeConfig, bos_token: int):
+        """Top-k / top-p sampling generate (engine.py:175-195 + _sampling_step
+        :197-216, decode.py:378-430). Every step: the device decoder step over
+        all rows, ONE batched device retrieve (per-row group counts: done rows
+        0), the candidates (a few per row) copied to the host, and the
+        reference's own draw there: one seeded PCG64 stream consumed item by
+        item in order, sorted prefix (-logit, token), probs exp(logit - lse)
+        in f64, inverse-CDF walk. Top-p rows whose survivors miss the nucleus
+        escalate their group count x8 with a per-row retrieve (:420-430)."""
+        if isinstance(src, torch.Tensor):
+            src = src.cpu().numpy()
+        batch, seq = src.shape
+        V = self.config.vocab_size
+        max_steps = min(cfg.max_steps, self.config.max_seq_len)
+        packed, mask, cache = self._setup_decoder(src, src_lengths, batch)
+        step = M.DecoderStep(self.dw, self.config, batch, 1, seq, cache, packed, mask,
+                             self._buffers, self.counters, self.timers)
+        step.bad.zero_()
+        rng = np.random.default_rng(cfg.seed)
+        states = [D.BeamState() for _ in range(batch)]
+        done = [False] * batch
+        tokens = np.full(batch, bos_token, dtype=I64)
+        dk = torch.empty(batch, dtype=torch.int32, device="cuda")
+        stream = _abi.stream_handle()
+        for t in range(max_steps):
+            step.tokens.copy_(torch.from_numpy(tokens))
+            logits = step.run()
+            live = [b for b in range(batch) if not done[b]]
+            g0 = min(cfg.sample_k, V) if cfg.method == "top_k" else min(32, V)
+            kv = np.zeros(batch, np.int32)
+            kv[live] = g0
+            dk.copy_(torch.from_numpy(kv))
+            _, _, lse, ci, cc = D.retrieve_device(logits, g0, d_k=dk, with_group_max=False)
+            self.counters.count_fused("retrieve", batch * V * 4)
+            cnt = cc.cpu().numpy()
+            w = int(min(cnt.max(initial=0), V))
+            toks_h = ci[:, :max(w, 1)].cpu().numpy()
+            lg_h = logits.gather(1, ci[:, :max(w, 1)].long().clamp(0, V - 1)).cpu().numpy()
+            lse_h = lse.cpu().numpy()
+            _abi.call("fq_step_advance", cache.d_cur.data_ptr(), stream)
+            last = t == max_steps - 1
+            tokens = np.zeros(batch, dtype=I64)
+            for b in live:
+                n = int(cnt[b])
+                toks, lgs = toks_h[b, :n].astype(np.int64), lg_h[b, :n]
+                if cfg.method == "top_k":
+                    order = np.lexsort((toks, -lgs.astype(np.float64)))
+                    toks, lgs = toks[order][:cfg.sample_k], lgs[order][:cfg.sample_k]
+                    probs = np.exp(lgs.astype(np.float64) - lse_h[b])
+                    tok = D._draw(toks, probs, rng)
+                else:
+                    tok = self._top_p_row(logits[b:b + 1], toks, lgs, float(lse_h[b]), g0, cfg,
+                                          rng)
+                st = states[b]
+                new = D.BeamState(prefixes=[st.prefixes[0] + [tok]], cum_log_prob=[0.0],
+                                  finished=list(st.finished), step=st.step + 1, parents=[0],
+                                  last_tokens=[tok], chosen_tokens=[tok])
+                if tok == cfg.eos_token:
+                    new.finished.append((new.prefixes[0], 0.0))
+                    new.prefixes = []
+                states[b] = new
+                if new.should_stop(cfg) or last or not new.prefixes:
+                    done[b] = True
+                    continue
+                tokens[b] = tok
+            if all(done):
+                break
+        torch.cuda.synchronize()
+        if int(step.bad.item()):
+            raise FullMaskError("fully masked cross-attention row")
+        return [[Hypothesis(tokens=s_, score=sc) for s_, sc in st.finalize(cfg)]
+                for st in states]
+
+    def _top_p_row(self, row, toks, lgs, lse, groups, cfg, rng) -> int:
+        """decode.py:412-430 on one row: survivors of `groups` groups sorted by
+        (-logit, token); escalate x8 until they hold the nucleus mass."""
+        V = self.config.vocab_size
+        while True:
+            order = np.lexsort((toks, -lgs.astype(np.float64)))
+            toks, lgs = toks[order], lgs[order]
+            probs = np.exp(lgs.astype(np.float64) - lse)
+            cum = np.cumsum(probs)
+            if cum.size and (cum[-1] >= cfg.sample_p or groups == V):
+                cut = min(int(np.searchsorted(cum, cfg.sample_p, side="left")), cum.size - 1)
+                return D._draw(toks[:cut + 1], probs[:cut + 1], rng)
+            groups = min(groups * 8, V)
+            rr = D.retrieve(row, groups, counters=self.counters)
+            toks = rr.candidate_tokens[0].astype(np.int64)
+            lgs = rr.candidate_logits[0]
+            lse = float(rr.logsumexp_full[0])
 
     # ------------------------------------------------------------------
     def forced_logits(self, src_tokens, tgt_tokens, src_lengths=None) -> np.ndarray:

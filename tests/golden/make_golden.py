@@ -19,6 +19,8 @@ Fixture inventory (all seeds fixed):
 * ``tiny_golden.npz``     tiny seq2seq models: generate / forced_logits / encode
 * ``c1_golden.npz``       Transformer-base C1 generate (BASELINE config 1)
 * ``c2_golden.npz``       Transformer-big C2 generate (BASELINE config 2), --big only
+* ``sampling_golden.npz`` tiny models: top-k / top-p sampling generate (engine.py:175-195,
+                          decode.py:378-430), seeded PCG64 draws
 """
 
 from __future__ import annotations
@@ -243,6 +245,43 @@ def make_tiny():
     np.savez_compressed(os.path.join(HERE, "tiny_golden.npz"), **out)
 
 
+def make_sampling():
+    """Sampling generate on the tiny models (only_sampling: python make_golden.py --sampling)."""
+    out = {}
+    runs = []
+    rng = np.random.default_rng(5)
+    for ci, kw in enumerate(TINY_CFGS[:2]):
+        cfg = M.ModelConfig(**kw)
+        w = M.make_random_weights(cfg, seed=10 + ci)
+        sess = Session(cfg, w, engine="fused")
+        batch = cfg.max_batch
+        seq = int(min(cfg.max_seq_len, 6))
+        src = rng.integers(3, cfg.vocab_size, size=(batch, seq)).astype(np.int64)
+        lengths = np.array([seq - (b % 2) for b in range(batch)], np.int64)
+        out[f"m{ci}_src"], out[f"m{ci}_len"] = src, lengths
+        for si, (method, kk, pp, seed, eos) in enumerate(
+                [("top_k", 5, 1.0, 7, 2), ("top_k", 1, 1.0, 3, 2), ("top_p", 1, 0.9, 11, 2),
+                 ("top_p", 1, 0.5, 13, 5), ("top_k", 40, 1.0, 17, 7), ("top_k", 5, 1.0, 7, -1),
+                 ("top_p", 1, 0.9, 11, -1)]):
+            if eos < 0:  # EOS = a token the eos=2 run samples early for item 1: finished path
+                probe = sess.generate(src, D.DecodeConfig(method=method, sample_k=kk,
+                                                          sample_p=pp, seed=seed, max_steps=12,
+                                                          eos_token=2))
+                eos = int(probe[1][0].tokens[3])
+            for use_len in (False, True):
+                dc = D.DecodeConfig(method=method, sample_k=kk, sample_p=pp, seed=seed,
+                                    max_steps=12, eos_token=eos)
+                hyps = sess.generate(src, dc, src_lengths=lengths if use_len else None)
+                t, l, s, n = pack_hyps(hyps, 1, cfg.max_seq_len + 1)
+                p = f"m{ci}_s{si}{int(use_len)}_"
+                out[p + "tok"], out[p + "len"], out[p + "score"], out[p + "n"] = t, l, s, n
+                runs.append(dict(model=ci, key=p, method=method, sample_k=kk, sample_p=pp,
+                                 seed=seed, eos=eos, lengths=use_len))
+    out["cfgs"] = np.array(json.dumps(TINY_CFGS[:2]))
+    out["runs"] = np.array(json.dumps(runs))
+    np.savez_compressed(os.path.join(HERE, "sampling_golden.npz"), **out)
+
+
 BASE = dict(num_encoder_layers=6, num_decoder_layers=6, d_model=512, d_ff=2048, num_heads=8,
             vocab_size=32000, max_batch=8, max_seq_len=64, max_beam_size=4)
 BIG = dict(num_encoder_layers=6, num_decoder_layers=6, d_model=1024, d_ff=4096, num_heads=16,
@@ -272,6 +311,11 @@ def make_generate(name, kw, batch, seq, steps):
 
 
 if __name__ == "__main__":
+    if "--sampling" in sys.argv:
+        make_sampling()
+        print("done")
+        sys.exit(0)
+    make_sampling()
     make_ops()
     make_retrieve()
     make_beam()

@@ -244,6 +244,35 @@ def test_tiny_models_exact_mode_match_reference_fixture(P, ci):
                 assert abs(h.score - g[p + "score"][b, i]) <= 1e-4
 
 
+@pytest.mark.parametrize("ci", [0, 1])
+def test_sampling_generate_matches_reference_fixture(P, ci):
+    """Top-k / top-p sampling generate (engine.py:175-216, decode.py:378-430):
+    token-identical to the reference run with the same seed, including EOS
+    finishes, length masks, top-k 1/5/40 and top-p 0.5/0.9 (fp32 mode)."""
+    g = np.load(golden_path("sampling_golden.npz"))
+    kw = json.loads(str(g["cfgs"]))[ci]
+    cfg = P.ModelConfig(**kw)
+    w = P.make_random_weights(cfg, seed=10 + ci)
+    sess = P.Session(cfg, w, precision="fp32")
+    src, lens = g[f"m{ci}_src"], g[f"m{ci}_len"]
+    nrun = 0
+    for run in json.loads(str(g["runs"])):
+        if run["model"] != ci:
+            continue
+        p = run["key"]
+        dc = P.DecodeConfig(method=run["method"], sample_k=run["sample_k"],
+                            sample_p=run["sample_p"], seed=run["seed"], max_steps=12,
+                            eos_token=run["eos"])
+        hyps = sess.generate(src, dc, src_lengths=lens if run["lengths"] else None)
+        for b, hs in enumerate(hyps):
+            assert len(hs) == g[p + "n"][b], (p, b)
+            for i, h in enumerate(hs):
+                assert h.tokens == g[p + "tok"][b, i][:g[p + "len"][b, i]].tolist(), (p, b, i)
+                assert h.score == g[p + "score"][b, i]
+        nrun += 1
+    assert nrun == 14
+
+
 def test_graph_and_eager_paths_identical(P):
     g, cfg, w = _tiny(P, 0)
     src = g["m0_src"]
