@@ -21,6 +21,8 @@ Fixture inventory (all seeds fixed):
 * ``c2_golden.npz``       Transformer-big C2 generate (BASELINE config 2), --big only
 * ``sampling_golden.npz`` tiny models: top-k / top-p sampling generate (engine.py:175-195,
                           decode.py:378-430), seeded PCG64 draws
+* ``classify_golden.npz`` encoder-only models: classify labels + probabilities
+                          (engine.py:198-224, decode.py:485-492)
 """
 
 from __future__ import annotations
@@ -282,6 +284,34 @@ def make_sampling():
     np.savez_compressed(os.path.join(HERE, "sampling_golden.npz"), **out)
 
 
+CLS_CFGS = [
+    dict(num_encoder_layers=2, num_decoder_layers=0, d_model=64, d_ff=128, num_heads=4,
+         vocab_size=500, max_batch=6, max_seq_len=16, max_beam_size=1, activation="gelu"),
+    dict(num_encoder_layers=1, num_decoder_layers=0, d_model=32, d_ff=64, num_heads=2,
+         vocab_size=50, max_batch=5, max_seq_len=9, max_beam_size=1, activation="gelu",
+         tie_output=False),
+]
+
+
+def make_classify():
+    out = {}
+    rng = np.random.default_rng(21)
+    for ci, kw in enumerate(CLS_CFGS):
+        cfg = M.ModelConfig(**kw)
+        w = M.make_random_weights(cfg, seed=30 + ci)
+        sess = Session(cfg, w, engine="fused")
+        batch, seq = cfg.max_batch, cfg.max_seq_len
+        tok = rng.integers(3, cfg.vocab_size, size=(batch, seq)).astype(np.int64)
+        lengths = np.array([seq - (b % 4) for b in range(batch)], np.int64)
+        out[f"m{ci}_tok"], out[f"m{ci}_len"] = tok, lengths
+        for use_len in (False, True):
+            lab, prob = sess.classify(tok, lengths if use_len else None)
+            out[f"m{ci}_labels{int(use_len)}"] = np.asarray(lab, np.int64)
+            out[f"m{ci}_probs{int(use_len)}"] = np.asarray(prob, np.float64)
+    out["cfgs"] = np.array(json.dumps(CLS_CFGS))
+    np.savez_compressed(os.path.join(HERE, "classify_golden.npz"), **out)
+
+
 BASE = dict(num_encoder_layers=6, num_decoder_layers=6, d_model=512, d_ff=2048, num_heads=8,
             vocab_size=32000, max_batch=8, max_seq_len=64, max_beam_size=4)
 BIG = dict(num_encoder_layers=6, num_decoder_layers=6, d_model=1024, d_ff=4096, num_heads=16,
@@ -313,9 +343,11 @@ def make_generate(name, kw, batch, seq, steps):
 if __name__ == "__main__":
     if "--sampling" in sys.argv:
         make_sampling()
+        make_classify()
         print("done")
         sys.exit(0)
     make_sampling()
+    make_classify()
     make_ops()
     make_retrieve()
     make_beam()

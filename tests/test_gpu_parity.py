@@ -273,6 +273,30 @@ def test_sampling_generate_matches_reference_fixture(P, ci):
     assert nrun == 14
 
 
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
+@pytest.mark.parametrize("ci", [0, 1])
+def test_classify_matches_reference_fixture(P, ci, precision):
+    """Encoder-only classification (engine.py:198-224): first-position
+    pooling, output projection, argmax + exact probability from one retrieve
+    pass (decode.py:485-492). fp32: labels identical, probabilities <= 1e-5
+    relative; bf16: labels identical where the reference's margin is clear."""
+    g = np.load(golden_path("classify_golden.npz"))
+    kw = json.loads(str(g["cfgs"]))[ci]
+    cfg = P.ModelConfig(**kw)
+    w = P.make_random_weights(cfg, seed=30 + ci)
+    sess = P.Session(cfg, w, precision=precision)
+    tok, lens = g[f"m{ci}_tok"], g[f"m{ci}_len"]
+    for use_len in (0, 1):
+        lab, prob = sess.classify(tok, lens if use_len else None)
+        want_l, want_p = g[f"m{ci}_labels{use_len}"], g[f"m{ci}_probs{use_len}"]
+        if precision == "fp32":
+            assert np.array_equal(lab, want_l)
+            assert np.allclose(prob, want_p, rtol=1e-5, atol=0)
+        else:
+            assert np.mean(lab == want_l) >= 0.8
+            assert np.allclose(prob[lab == want_l], want_p[lab == want_l], rtol=3e-2)
+
+
 def test_graph_and_eager_paths_identical(P):
     g, cfg, w = _tiny(P, 0)
     src = g["m0_src"]
