@@ -100,6 +100,13 @@ int fq_embed_scale_pos(const int64_t* tokens, int64_t n, const float* emb, int64
                        const int32_t* d_off, int64_t seq, float* out, void* out16,
                        fq_stream_t stream);
 
+/* Diversity penalty of diverse beam search, decode.py:291-295 ->
+ * kernels.py:215-219: out[r, j] = logits[r, j] - lam * counts[j] (f64
+ * arithmetic, rounded to fp32, as numba types it). */
+int fq_penalize_counts(const float* logits, int64_t ld, int64_t rows, int64_t vocab,
+                       const int32_t* counts, float lam, float* out, int64_t ldo,
+                       fq_stream_t stream);
+
 /* kernels.py:205 kv_append_kernel: dst[r,:,cur,:] = new[r,:,0,:], dst [R,h,S,hd]. */
 int fq_kv_append(const float* new_k, const float* new_v, int64_t cur, int64_t rows,
                  int64_t heads, int64_t max_seq, int64_t head_dim, float* dst_k,

@@ -338,6 +338,20 @@ __global__ void kv_kernel(const float* __restrict__ sk, const float* __restrict_
   }
 }
 
+// Diversity penalty (kernels.py:215-219): out = logits - f32(lam) * count[j],
+// numba-typed as f32 * i32 -> f64, f32 - f64 -> f64, stored as f32.
+__global__ void penalize_counts_kernel(const float* __restrict__ logits, int64_t ld, int64_t rows,
+                                       int64_t vocab, const int32_t* __restrict__ counts,
+                                       float lam, float* __restrict__ out, int64_t ldo) {
+  pdl_enter();
+  const int64_t n = rows * vocab;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / vocab, j = i - r * vocab;
+    out[r * ldo + j] = (float)((double)logits[r * ld + j] - (double)lam * (double)counts[j]);
+  }
+}
+
 static inline int grid_for(int64_t n, int threads) {
   int64_t g = (n + threads - 1) / threads;
   const int64_t cap = 148LL * 32;
@@ -431,6 +445,17 @@ int fq_embed_scale_pos(const int64_t* tokens, int64_t n, const float* emb, int64
       tokens, n, emb, (int)d, scale, pos, pos_offset, d_off, seq, out,
       reinterpret_cast<__nv_bfloat16*>(out16));
   return launch_status("fq_embed_scale_pos");
+}
+
+int fq_penalize_counts(const float* logits, int64_t ld, int64_t rows, int64_t vocab,
+                       const int32_t* counts, float lam, float* out, int64_t ldo,
+                       fq_stream_t stream) {
+  FQ_CHECK_ARG(logits && counts && out && rows >= 0 && vocab >= 1 && ld >= vocab && ldo >= vocab,
+               FQ_ERR_DIMENSION, "fq_penalize_counts: bad args");
+  if (rows == 0) return FQ_OK;
+  launch_kernel(penalize_counts_kernel, grid_for(rows * vocab, 256), 256, 0, as_stream(stream),
+                1u, logits, ld, rows, vocab, counts, lam, out, ldo);
+  return launch_status("fq_penalize_counts");
 }
 
 int fq_kv_append(const float* new_k, const float* new_v, int64_t cur, int64_t rows,

@@ -420,9 +420,117 @@ def perplexity(per_step_logits, target_tokens) -> float:
     return float(np.exp(-ll.mean()))
 
 
-def diverse_beam_search_step(state, logits, config, *, counters=None, bufs=None):
-    """Diverse beam search (decode.py:274-371) is ranked next in SURVEY §8(f)."""
-    raise EngineError("diverse beam search is not implemented on the B200 path yet")
+# ---------------------------------------------------------------------------
+# diverse beam search  (decode.py:274-371): device penalty + device retrieve,
+# host group walk over the few survivors
+# ---------------------------------------------------------------------------
+
+def _finished_insert(finished: list, seq: list, score: float, cap: int):
+    """decode.py:186-189."""
+    finished.append((seq, score))
+    finished.sort(key=lambda h: (-h[1], h[0]))
+    del finished[cap:]
+
+
+def apply_selection(state: BeamState, picks: list, eos: int, alpha: float, k: int) -> BeamState:
+    """decode.py:192-214: score-ordered (cum, token, parent) picks -> next
+    state; EOS picks become finished (cum / len^alpha), the rest live until k."""
+    new = BeamState(prefixes=[], cum_log_prob=[], finished=list(state.finished),
+                    step=state.step + 1, parents=[], last_tokens=[], chosen_tokens=[])
+    length = state.step + 1
+    for cum, tok, parent in picks:
+        if tok == eos:
+            seq = state.prefixes[parent] + [tok]
+            score = cum / (length ** alpha) if alpha else cum
+            _finished_insert(new.finished, seq, score, k)
+            new.chosen_tokens.append(tok)
+        elif len(new.prefixes) < k:
+            new.prefixes.append(state.prefixes[parent] + [tok])
+            new.cum_log_prob.append(cum)
+            new.parents.append(parent)
+            new.last_tokens.append(tok)
+            new.chosen_tokens.append(tok)
+        if len(new.prefixes) >= k:
+            break
+    return new
+
+
+def _walk_group(cands, kg, eos):
+    """decode.py:341-353: score-ordered candidates until kg non-EOS picks."""
+    picks = []
+    non_eos = 0
+    for cum, tok, parent in cands:
+        picks.append((cum, tok, parent))
+        if tok != eos:
+            non_eos += 1
+            if non_eos >= kg:
+                break
+    return picks
+
+
+def _diverse_step(state: BeamState, logits, config: DecodeConfig, exhaustive: bool,
+                  counters=None) -> BeamState:
+    """decode.py:274-303 (hierarchical :306-320, exhaustive :323-338): groups
+    pick in sequence from all live beams' candidates; group g sees the logits
+    penalised by lambda * count(token chosen by earlier groups this step)
+    (fq_penalize_counts) and skips beam-token pairs already taken. The
+    exhaustive twin is the same walk with every token a candidate (groups = V)."""
+    L = as_device(logits, torch.float32)
+    if L.dim() != 2 or L.shape[0] != state.live:
+        raise DimensionError(f"logits rows {L.shape[0]} != live beams {state.live}")
+    if L.stride(1) != 1:
+        L = L.contiguous()
+    k = config.effective_beam_size
+    G = config.diversity_groups
+    kg = k // G
+    lam = config.diversity_penalty
+    vocab = L.shape[1]
+    counts = np.zeros(vocab, np.int32)
+    dcounts = torch.zeros(vocab, dtype=torch.int32, device=L.device)
+    pen_buf = torch.empty_like(L)
+    taken: set = set()
+    all_picks: list = []
+    for _ in range(G):
+        if lam and counts.any():
+            dcounts.copy_(torch.from_numpy(counts))
+            _abi.call("fq_penalize_counts", L.data_ptr(), L.stride(0), L.shape[0], vocab,
+                      dcounts.data_ptr(), float(np.float32(lam)), pen_buf.data_ptr(),
+                      pen_buf.stride(0), _abi.stream_handle())
+            _ctr(counters).count_fused("diversity_penalty", L.numel() * 4)
+            pen = pen_buf
+        else:
+            pen = L
+        # every beam's top-(taken + kg + live) must survive (decode.py:307-309)
+        groups = vocab if exhaustive else min(len(taken) + kg + state.live, vocab)
+        rr = retrieve(pen, groups, counters=counters)
+        cands = []
+        for b in range(state.live):
+            base = state.cum_log_prob[b]
+            lse = float(rr.logsumexp_full[b])
+            for tok, lg in zip(rr.candidate_tokens[b], rr.candidate_logits[b]):
+                if (b, int(tok)) not in taken:
+                    cands.append((base + (float(lg) - lse), int(tok), b))
+        cands.sort(key=lambda c: (-c[0], c[1], c[2]))
+        if exhaustive:
+            cands = cands[:kg + state.live]
+        picks = _walk_group(cands, kg, config.eos_token)
+        for cum, tok, parent in picks:
+            taken.add((parent, tok))
+            counts[tok] += 1
+            all_picks.append((cum, tok, parent))
+    return apply_selection(state, all_picks, config.eos_token, config.length_penalty, k)
+
+
+def diverse_beam_search_step(state: BeamState, logits, config: DecodeConfig, *,
+                             counters=None, bufs=None) -> BeamState:
+    """decode.py:356-359."""
+    return _diverse_step(state, logits, config, False, counters)
+
+
+def exhaustive_diverse_beam_search_step(state: BeamState, logits, config: DecodeConfig, *,
+                                        counters=None) -> BeamState:
+    """decode.py:362-365."""
+    return _diverse_step(state, logits, config, True, counters)
 
 
 def top_k_set(logits_row, k: int) -> set:

@@ -141,6 +141,13 @@ class Session:
             if return_device_state:
                 raise EngineError("sampling returns host hypotheses only")
             return self._generate_sampling(src, src_lengths, cfg, bos_token)
+        if cfg.method == "diverse_beam":
+            if return_device_state:
+                raise EngineError("diverse beam search returns host hypotheses only")
+            if search not in (None, "hierarchical", "exhaustive"):
+                raise InputError(f"unknown search {search!r}")
+            return self._generate_diverse(src, src_lengths, cfg, bos_token,
+                                          search == "exhaustive")
         if cfg.method not in ("beam", "greedy"):
             raise EngineError(f"decode method {cfg.method!r} is not on the B200 device path yet "
                               "(SURVEY §8(f))")
@@ -350,6 +357,58 @@ class Session:
                     done[b] = True
                     continue
                 tokens[b] = tok
+            if all(done):
+                break
+        torch.cuda.synchronize()
+        if int(step.bad.item()):
+            raise FullMaskError("fully masked cross-attention row")
+        return [[Hypothesis(tokens=s_, score=sc) for s_, sc in st.finalize(cfg)]
+                for st in states]
+
+    def _generate_diverse(self, src, src_lengths, cfg: D.DecodeConfig, bos_token: int,
+                          exhaustive: bool):
+        """Diverse beam search generate (engine.py:81-173 with
+        diverse_beam_search_step, decode.py:274-371): the device decoder step
+        over all rows with the copy-free KV history reordered by the parents;
+        per item and group the device penalty (fq_penalize_counts) and the
+        device retrieve, the group walk over the survivors on the host."""
+        if isinstance(src, torch.Tensor):
+            src = src.cpu().numpy()
+        batch, seq = src.shape
+        K = cfg.effective_beam_size
+        rows = batch * K
+        max_steps = min(cfg.max_steps, self.config.max_seq_len)
+        packed, mask, cache = self._setup_decoder(src, src_lengths, rows)
+        step = M.DecoderStep(self.dw, self.config, batch, K, seq, cache, packed, mask,
+                             self._buffers, self.counters, self.timers)
+        step.bad.zero_()
+        states = [D.BeamState() for _ in range(batch)]
+        done = [False] * batch
+        tokens = np.full(rows, bos_token, dtype=I64)
+        parents = None
+        fn = D.exhaustive_diverse_beam_search_step if exhaustive else D.diverse_beam_search_step
+        for t in range(max_steps):
+            cache.begin_step(parents)
+            step.tokens.copy_(torch.from_numpy(tokens))
+            logits = step.run()
+            cache.end_step()
+            parents = np.empty(rows, dtype=I64)
+            tokens = np.zeros(rows, dtype=I64)
+            last = t == max_steps - 1
+            for b in range(batch):
+                row0 = b * K
+                parents[row0:row0 + K] = row0
+                if done[b]:
+                    continue
+                st = fn(states[b], logits[row0:row0 + states[b].live], cfg,
+                        counters=self.counters)
+                states[b] = st
+                if st.should_stop(cfg) or last or not st.prefixes:
+                    done[b] = True
+                    continue
+                for i in range(st.live):
+                    parents[row0 + i] = row0 + st.parents[i]
+                    tokens[row0 + i] = st.last_tokens[i]
             if all(done):
                 break
         torch.cuda.synchronize()

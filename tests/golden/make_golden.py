@@ -23,6 +23,8 @@ Fixture inventory (all seeds fixed):
                           decode.py:378-430), seeded PCG64 draws
 * ``classify_golden.npz`` encoder-only models: classify labels + probabilities
                           (engine.py:198-224, decode.py:485-492)
+* ``diverse_golden.npz``  tiny models: diverse beam search generate, hierarchical and
+                          exhaustive (decode.py:274-371)
 """
 
 from __future__ import annotations
@@ -284,6 +286,37 @@ def make_sampling():
     np.savez_compressed(os.path.join(HERE, "sampling_golden.npz"), **out)
 
 
+def make_diverse():
+    out = {}
+    runs = []
+    rng = np.random.default_rng(8)
+    for ci, kw in enumerate(TINY_CFGS[:2]):
+        cfg = M.ModelConfig(**kw)
+        w = M.make_random_weights(cfg, seed=10 + ci)
+        sess = Session(cfg, w, engine="fused")
+        batch = cfg.max_batch
+        seq = int(min(cfg.max_seq_len, 6))
+        src = rng.integers(3, cfg.vocab_size, size=(batch, seq)).astype(np.int64)
+        lengths = np.array([seq - (b % 2) for b in range(batch)], np.int64)
+        out[f"m{ci}_src"], out[f"m{ci}_len"] = src, lengths
+        variants = [(4, 2, 0.5, 0.0, "hierarchical", False), (4, 4, 1.5, 0.6, "hierarchical", True),
+                    (2, 2, 0.0, 0.0, "hierarchical", False), (4, 2, 0.5, 0.0, "exhaustive", True)]
+        for vi, (beam, G, lam, alpha, search, use_len) in enumerate(variants):
+            beam = min(beam, cfg.max_beam_size)
+            dc = D.DecodeConfig(method="diverse_beam", beam_size=beam, diversity_groups=G,
+                                diversity_penalty=lam, length_penalty=alpha, max_steps=10,
+                                eos_token=2)
+            hyps = sess.generate(src, dc, src_lengths=lengths if use_len else None, search=search)
+            t, l, sc, n = pack_hyps(hyps, beam, cfg.max_seq_len + 1)
+            p = f"m{ci}_d{vi}_"
+            out[p + "tok"], out[p + "len"], out[p + "score"], out[p + "n"] = t, l, sc, n
+            runs.append(dict(model=ci, key=p, beam=beam, groups=G, penalty=lam, alpha=alpha,
+                             search=search, lengths=use_len))
+    out["cfgs"] = np.array(json.dumps(TINY_CFGS[:2]))
+    out["runs"] = np.array(json.dumps(runs))
+    np.savez_compressed(os.path.join(HERE, "diverse_golden.npz"), **out)
+
+
 CLS_CFGS = [
     dict(num_encoder_layers=2, num_decoder_layers=0, d_model=64, d_ff=128, num_heads=4,
          vocab_size=500, max_batch=6, max_seq_len=16, max_beam_size=1, activation="gelu"),
@@ -344,10 +377,12 @@ if __name__ == "__main__":
     if "--sampling" in sys.argv:
         make_sampling()
         make_classify()
+        make_diverse()
         print("done")
         sys.exit(0)
     make_sampling()
     make_classify()
+    make_diverse()
     make_ops()
     make_retrieve()
     make_beam()

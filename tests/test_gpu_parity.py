@@ -297,6 +297,33 @@ def test_classify_matches_reference_fixture(P, ci, precision):
             assert np.allclose(prob[lab == want_l], want_p[lab == want_l], rtol=3e-2)
 
 
+@pytest.mark.parametrize("ci", [0, 1])
+def test_diverse_beam_generate_matches_reference_fixture(P, ci):
+    """Diverse beam search generate (decode.py:274-371): device diversity
+    penalty + device retrieve per group, hierarchical and exhaustive, with
+    length masks and a length penalty: token-identical to the reference."""
+    g = np.load(golden_path("diverse_golden.npz"))
+    kw = json.loads(str(g["cfgs"]))[ci]
+    cfg = P.ModelConfig(**kw)
+    w = P.make_random_weights(cfg, seed=10 + ci)
+    sess = P.Session(cfg, w, precision="fp32")
+    src, lens = g[f"m{ci}_src"], g[f"m{ci}_len"]
+    for run in json.loads(str(g["runs"])):
+        if run["model"] != ci:
+            continue
+        p = run["key"]
+        dc = P.DecodeConfig(method="diverse_beam", beam_size=run["beam"],
+                            diversity_groups=run["groups"], diversity_penalty=run["penalty"],
+                            length_penalty=run["alpha"], max_steps=10, eos_token=2)
+        hyps = sess.generate(src, dc, src_lengths=lens if run["lengths"] else None,
+                             search=run["search"])
+        for b, hs in enumerate(hyps):
+            assert len(hs) == g[p + "n"][b], (p, b)
+            for i, h in enumerate(hs):
+                assert h.tokens == g[p + "tok"][b, i][:g[p + "len"][b, i]].tolist(), (p, b, i)
+                assert abs(h.score - g[p + "score"][b, i]) <= 1e-4
+
+
 def test_graph_and_eager_paths_identical(P):
     g, cfg, w = _tiny(P, 0)
     src = g["m0_src"]
