@@ -1006,18 +1006,29 @@ __device__ __forceinline__ uint32_t sw128(int row, int chunk) {
   return (uint32_t)(row * 128 + ((chunk ^ (row & 7)) << 4));
 }
 
-__global__ void __launch_bounds__(32) cross_attention_tma(
+// kCrossWarps warps per CTA, each an independent (item, head) with its own
+// 16 KB of K/V boxes: one CTA of 14 warps per SM fills the SM's shared memory
+// in a single wave (32-thread CTAs left a second, partial wave at C2).
+constexpr int kCrossWarps = 14;
+__global__ void __launch_bounds__(32 * kCrossWarps) cross_attention_tma(
     const __grid_constant__ CUtensorMap tk, const __grid_constant__ CUtensorMap tv,
     const float* __restrict__ cq, int64_t ldcq, int beam, int seq, float scale,
     const float* __restrict__ mask, float* __restrict__ out, __nv_bfloat16* __restrict__ out16,
-    int64_t ldo, int* d_bad) {
+    int64_t ldo, int* d_bad, int heads, int npairs) {
   constexpr int HD = 64, NT = 4, NP = 64;
   extern __shared__ __align__(1024) uint8_t smraw[];
-  uint8_t* Ks = smraw + ((1024u - (sm_u32(smraw) & 1023u)) & 1023u);
+  const int wid = threadIdx.x >> 5;
+  const int pair = blockIdx.x * kCrossWarps + wid;
+  if (pair >= npairs) {
+    pdl_enter();
+    return;
+  }
+  uint8_t* Ks = smraw + ((1024u - (sm_u32(smraw) & 1023u)) & 1023u) + wid * (2 * NP * 128);
   uint8_t* Vs = Ks + NP * 128;
   float (*Ps)[NP + 4] = reinterpret_cast<float (*)[NP + 4]>(Ks);  // after the scores
-  __shared__ __align__(8) uint64_t bar;
-  const int b = blockIdx.x, h = blockIdx.y, lane = threadIdx.x;
+  __shared__ __align__(8) uint64_t bars[kCrossWarps];
+  uint64_t& bar = bars[wid];
+  const int b = pair / heads, h = pair - b * heads, lane = threadIdx.x & 31;
   const int g = lane >> 2, t4 = lane & 3;
   if (lane == 0) {
     bar_init(&bar, 1);
@@ -1477,6 +1488,8 @@ int attention_prepare() {
       cudaFuncSetAttribute(cross_attention_fast<__nv_bfloat16, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024) ||
       cudaFuncSetAttribute(cross_attention_fast<__nv_bfloat16, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024) ||
       cudaFuncSetAttribute(encoder_attention_tiled<4, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024) ||
+      cudaFuncSetAttribute(cross_attention_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           kCrossWarps * 2 * 64 * 128 + 1024) ||
       cudaFuncSetAttribute(encoder_attention_tiled<4, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024)) {
     set_error("fq_prepare: cannot opt in to large shared memory (attention)");
     return FQ_ERR_CUDA;
@@ -1641,10 +1654,12 @@ int fq_cross_attention(const float* cq, int64_t ldcq, const void* ck, const void
     const int64_t nrows = batch * seq, ncols = heads * head_dim;
     if (make_tmap_bf16_sw128(&tk, ck, nrows, ncols, ldkv, 64, 64) == FQ_OK &&
         make_tmap_bf16_sw128(&tv, cv, nrows, ncols, ldkv, 64, 64) == FQ_OK) {
-      launch_kernel(cross_attention_tma, dim3((unsigned)batch, (unsigned)heads), 32,
-                    (size_t)2 * 64 * 128 + 1024, as_stream(stream), 1u, tk, tv, cq, ldcq,
-                    (int)beam, (int)seq, scale, mask, out,
-                    reinterpret_cast<__nv_bfloat16*>(out16), ldo, d_bad);
+      const int npairs = (int)(batch * heads);
+      launch_kernel(cross_attention_tma, (unsigned)((npairs + kCrossWarps - 1) / kCrossWarps),
+                    32 * kCrossWarps, (size_t)kCrossWarps * 2 * 64 * 128 + 1024,
+                    as_stream(stream), 1u, tk, tv, cq, ldcq, (int)beam, (int)seq, scale, mask,
+                    out, reinterpret_cast<__nv_bfloat16*>(out16), ldo, d_bad, (int)heads,
+                    npairs);
       return launch_status("fq_cross_attention");
     }
   }
