@@ -148,6 +148,35 @@ struct Epi {
   unsigned long long* dbg;  // per-CTA [start, end] %globaltimer (profiling only)
 };
 
+// HARS stage-1 statistics computed in the logits GEMM's epilogue (the [rows,
+// V] logits are never written): per row and column tile the strided group
+// maxima (published to the row's running maxima with global atomics), the
+// tile-row maximum and sum of exp(x - max), and every element >= the row's
+// current bound min_g(running group max) <= R as a survivor.
+struct HarsEpi {
+  const int32_t* dk;  // [M] group count per row (0: row not searched)
+  int* gmax;          // [M][32] running group maxima, ordered ints (-inf between steps)
+  float* tmax;        // [M][ldt] tile-row maxima
+  double* tsum;       // [M][ldt] sum over the tile-row of exp(x - tmax)
+  int* sv_cnt;        // [M] survivor counts (0 between steps)
+  int2* sv;           // [M][sv_cap] survivors (column, value bits)
+  int sv_cap;
+  int ldt;
+};
+
+__device__ __forceinline__ int hs_f2ord(float f) {
+  const int i = __float_as_int(f);
+  return i >= 0 ? i : i ^ 0x7fffffff;
+}
+__device__ __forceinline__ float hs_ord2f(int i) {
+  return __int_as_float(i >= 0 ? i : i ^ 0x7fffffff);
+}
+__device__ __forceinline__ float hs_ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 __device__ __forceinline__ uint32_t cluster_rank() {
   uint32_t r;
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
@@ -189,11 +218,11 @@ __device__ __forceinline__ void dbg_stamp(unsigned long long* dbg, int slot) {
 // M-tiles [gm*cm, +cm) x N-tiles [gn*cn, +cn) with the M-group fastest so
 // concurrent clusters share weight tiles in L2. Two TMEM accumulator stages let
 // the epilogue of one tile overlap the MMAs of the next.
-template <int BN, int STAGES>
+template <int BN, int STAGES, bool HS = false>
 __global__ void __launch_bounds__(kThreads, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tma_a,
                    const __grid_constant__ CUtensorMap tma_b, const Epi ep, int M, int N, int K,
-                   int cm, int cn) {
+                   int cm, int cn, const HarsEpi he) {
   constexpr int A_BYTES = BM * BK * 2;
   constexpr int B_BYTES = BN * BK * 2;
   constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
@@ -326,6 +355,103 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         mma_commit(&tfull_bar[as]);   // accumulator stage complete
         if (local == 0) dbg_stamp(ep.dbg, 3);  // first tile's MMAs issued
+      }
+    }
+  } else if constexpr (HS) {  // ---- HARS statistics epilogue (thread = row) ----
+    pdl_wait();  // the group counts / running maxima come from the previous kernel
+    const int q = warp & 3;
+    float* gms = stage_out + 4 * 32 * 33 + ((warp - 2) * 32 + lane) * 33;  // per-thread scratch
+    constexpr float L2E = 1.4426950408889634f;
+    constexpr float L2E_LO = 1.925963033500011e-08f;
+    int local = 0;
+    for (int g = cluster_id; g < ngroups; g += nclusters, ++local) {
+      const int as = local & 1;
+      const int m0 = ((g % mg) * cm + ry) * BM, n0 = ((g / mg) * cn + rx) * BN;
+      const int r = m0 + q * 32 + lane;
+      const int k = r < M ? he.dk[r] : 0;
+      mbar_wait(&tfull_bar[as], (local >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      for (int gq = 0; gq < k; ++gq) gms[gq] = -INFINITY;
+      // pass 1: tile-row maximum and group maxima (group of column c: c % k)
+      float mt = -INFINITY;
+      int gi = k > 0 ? n0 % k : 0;
+#pragma unroll 1
+      for (int cc = 0; cc < BN; cc += 32) {
+        float v[32];
+        tmem_ld32(tmem + as * BN + ((uint32_t)(q * 32) << 16) + cc, v);
+        if (k > 0) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            if (n0 + cc + j < N) {
+              gms[gi] = fmaxf(gms[gi], v[j]);
+              mt = fmaxf(mt, v[j]);
+            }
+            if (++gi == k) gi = 0;
+          }
+        }
+      }
+      // publish: running row maxima; bound = min over groups (<= the row's R)
+      float bound = INFINITY;
+      if (k > 0) {
+        int old[32];
+#pragma unroll
+        for (int gq = 0; gq < 32; ++gq)
+          if (gq < k) old[gq] = atomicMax(he.gmax + (int64_t)r * 32 + gq, hs_f2ord(gms[gq]));
+#pragma unroll
+        for (int gq = 0; gq < 32; ++gq)
+          if (gq < k) bound = fminf(bound, fmaxf(hs_ord2f(old[gq]), gms[gq]));
+      }
+      // pass 2: sum exp(x - mt) (fp32 terms, f64 sum) and survivors x >= bound,
+      // kept in the scratch (16 pairs) and flushed with one atomic per tile
+      const float mL = mt * L2E;
+      double s = 0.0;
+      int ns = 0;
+      int* svl = reinterpret_cast<int*>(gms);
+#pragma unroll 1
+      for (int cc = 0; cc < BN; cc += 32) {
+        float v[32];
+        tmem_ld32(tmem + as * BN + ((uint32_t)(q * 32) << 16) + cc, v);
+        if (cc + 32 >= BN) {  // last TMEM read of this stage: hand it back to the MMA warp
+          asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tempty_bar[as]);
+        }
+        if (k > 0) {
+#pragma unroll
+          for (int j0 = 0; j0 < 32; j0 += 4) {
+            float t4 = 0.0f;
+#pragma unroll
+            for (int j = j0; j < j0 + 4; ++j) {
+              const int col = n0 + cc + j;
+              if (col < N) {
+                t4 += hs_ex2(fmaf(v[j], L2E_LO, fmaf(v[j], L2E, -mL)));
+                if (v[j] >= bound) {
+                  if (ns < 16) {
+                    svl[2 * ns] = col;
+                    svl[2 * ns + 1] = __float_as_int(v[j]);
+                  } else {
+                    const int p = atomicAdd(he.sv_cnt + r, 1);
+                    if (p < he.sv_cap) he.sv[(int64_t)r * he.sv_cap + p] = make_int2(col, __float_as_int(v[j]));
+                  }
+                  ++ns;
+                }
+              }
+            }
+            s += (double)t4;
+          }
+        }
+      }
+      if (k > 0) {
+        const int nl = ns < 16 ? ns : 16;
+        if (nl > 0) {
+          const int p0 = atomicAdd(he.sv_cnt + r, nl);
+          for (int i = 0; i < nl; ++i)
+            if (p0 + i < he.sv_cap)
+              he.sv[(int64_t)r * he.sv_cap + p0 + i] = make_int2(svl[2 * i], svl[2 * i + 1]);
+        }
+        const int tn = n0 / BN;
+        he.tmax[(int64_t)r * he.ldt + tn] = mt;
+        he.tsum[(int64_t)r * he.ldt + tn] = s;
       }
     }
   } else {  // ---- epilogue: warps 2..5 own TMEM lane quarters (warp % 4) ----
@@ -663,9 +789,9 @@ constexpr int smem_bytes_splitk() {
   return STAGES * (BM * BK * 2 + BN * BK * 2) + 1024;
 }
 
-template <int BN, int STAGES>
+template <int BN, int STAGES, bool HS = false>
 constexpr int smem_bytes() {
-  return STAGES * (BM * BK * 2 + BN * BK * 2) + 4 * 32 * 33 * 4 + 1024;
+  return STAGES * (BM * BK * 2 + BN * BK * 2) + (HS ? 8 : 4) * 32 * 33 * 4 + 1024;
 }
 
 using EncodeFn = PFN_cuTensorMapEncodeTiled_v12000;
@@ -745,9 +871,10 @@ static int num_sms() {
   return n;
 }
 
-template <int BN, int STAGES>
+template <int BN, int STAGES, bool HS = false>
 static int launch(const void* a, int64_t lda, const void* b, int64_t ldb, const Epi& ep,
-                  int64_t M, int64_t N, int64_t K, int cm, int cn, cudaStream_t s) {
+                  int64_t M, int64_t N, int64_t K, int cm, int cn, cudaStream_t s,
+                  const HarsEpi& he = HarsEpi{}) {
   CUtensorMap ma, mb;
   int rc;
   if ((rc = make_map(&ma, a, M, K, lda, BM / cn)) != FQ_OK) return rc;
@@ -756,9 +883,10 @@ static int launch(const void* a, int64_t lda, const void* b, int64_t ldb, const 
   const int64_t groups = ((M + BM - 1) / BM / cm) * ((N + BN - 1) / BN / cn);
   const int64_t max_clusters = num_sms() / csize;
   const int64_t clusters = groups < max_clusters ? groups : max_clusters;
-  cudaError_t e = launch_kernel(tc_gemm_kernel<BN, STAGES>, dim3((unsigned)(clusters * csize)),
-                                dim3(kThreads), smem_bytes<BN, STAGES>(), s, (unsigned)csize, ma,
-                                mb, ep, (int)M, (int)N, (int)K, cm, cn);
+  cudaError_t e = launch_kernel(tc_gemm_kernel<BN, STAGES, HS>,
+                                dim3((unsigned)(clusters * csize)), dim3(kThreads),
+                                smem_bytes<BN, STAGES, HS>(), s, (unsigned)csize, ma, mb, ep,
+                                (int)M, (int)N, (int)K, cm, cn, he);
   if (e != cudaSuccess) {
     set_error("fq_gemm(tcgen05): launch failed: %s", cudaGetErrorString(e));
     return FQ_ERR_CUDA;
@@ -795,11 +923,11 @@ static int prep_splitk() {
              : FQ_ERR_CUDA;
 }
 
-template <int BN, int STAGES>
+template <int BN, int STAGES, bool HS = false>
 static int prep() {
-  return cudaFuncSetAttribute(tc_gemm_kernel<BN, STAGES>,
+  return cudaFuncSetAttribute(tc_gemm_kernel<BN, STAGES, HS>,
                               cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              smem_bytes<BN, STAGES>()) == cudaSuccess
+                              smem_bytes<BN, STAGES, HS>()) == cudaSuccess
              ? FQ_OK
              : FQ_ERR_CUDA;
 }
@@ -808,6 +936,7 @@ static int prep() {
 
 int gemm_tc_prepare() {
   if (tc::prep<256, 4>() || tc::prep<224, 4>() || tc::prep<192, 4>() || tc::prep<128, 6>() ||
+      tc::prep<224, 4, true>() ||
       tc::prep<64, 8>() || tc::prep<32, 8>() ||
       tc::prep_splitk<256, 4>() || tc::prep_splitk<128, 6>() || tc::prep_splitk<64, 8>()) {
     set_error("fq_prepare: tcgen05 GEMM smem opt-in failed");
@@ -888,6 +1017,25 @@ int launch_tc_gemm(const void* a, int64_t lda, const void* b, int64_t ldb, void*
     case 64: return tc::launch<64, 8>(a, lda, b, ldb, ep, M, N, K, p.cm, p.cn, s);
     default: return tc::launch<32, 8>(a, lda, b, ldb, ep, M, N, K, p.cm, p.cn, s);
   }
+}
+
+// Logits GEMM with the HARS statistics epilogue (see HarsEpi): x16 [rows, d]
+// bf16, emb16 [vocab, d] bf16 (K-major). Column tile width 224 (ncu: the
+// C2 logits GEMM's best wave quantisation;
+// tiles; ldt >= ceil(vocab / 224) = the number of column tiles).
+extern "C" int fq_logits_hars(const void* x16, int64_t ldx, const void* emb16, int64_t lde,
+                              int64_t rows, int64_t vocab, int64_t d, const int32_t* dk,
+                              int32_t* gmax, float* tmax, double* tsum, int64_t ldt,
+                              int32_t* sv_cnt, void* sv, int64_t sv_cap, fq_stream_t stream) {
+  FQ_CHECK_ARG(x16 && emb16 && dk && gmax && tmax && tsum && sv_cnt && sv && rows > 0 &&
+                   vocab > 0 && d > 0 && ldt >= (vocab + 223) / 224 && sv_cap >= 1 &&
+                   ldx % 8 == 0 && lde % 8 == 0,
+               FQ_ERR_DIMENSION, "fq_logits_hars: bad args");
+  tc::Epi ep{nullptr, 0, 0, 0, nullptr, nullptr, 0, 0, g_gemm_dbg};
+  tc::HarsEpi he{dk, gmax, tmax, tsum, sv_cnt, reinterpret_cast<int2*>(sv), (int)sv_cap,
+                 (int)ldt};
+  return tc::launch<224, 4, true>(x16, ldx, emb16, lde, ep, rows, vocab, d, 1, 1,
+                                  as_stream(stream), he);
 }
 
 // Benchmarks only: force (bn, cm, cn) for shapes it divides; bn = 0 restores auto.

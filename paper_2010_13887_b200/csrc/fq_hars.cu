@@ -1461,6 +1461,106 @@ __global__ void __launch_bounds__(kSwThreads, 4) hars_step_split_kernel(
       });
 }
 
+// ---------------------------------------------------------------------------
+// HARS from the logits GEMM's statistics (fq_logits_hars): the [rows, V]
+// logits were never written. CTA per row: the row's exact group maxima (the
+// GEMM's running atomics) give R and M; S = sum_t tsum_t exp(tmax_t - M) in a
+// fixed tile order; the survivors (every element >= a bound <= R, recorded by
+// the GEMM) filtered at R and ranked by column are exactly the candidates
+// x >= R. Then, per item, stage 2 + next-step embedding as fq_hars_step, and
+// the item's group counts for the next step's GEMM. Resets the running maxima
+// and survivor counts for the next step.
+// ---------------------------------------------------------------------------
+constexpr int kMergeCap = 2048;
+__global__ void __launch_bounds__(kSelThreads) hars_merge_step_kernel(
+    int V, fq_beam_state st, int batch, int K, int max_len, int eos,
+    const double* __restrict__ len_pow, int32_t* d_cur, int64_t max_steps, int32_t* dk,
+    int* gmax, const float* __restrict__ tmax, const double* __restrict__ tsum, int ldt,
+    int ntiles, int* sv_cnt, const int2* __restrict__ sv, int sv_cap, double* lse,
+    int32_t* cand_idx, int64_t cand_ld, int64_t* cand_count, int* counters, int* d_ovf,
+    int64_t* row_tokens, int64_t* row_parents, int32_t* hist, const float* __restrict__ emb,
+    int d, float emb_scale, const float* __restrict__ pos, float* __restrict__ x_next,
+    __nv_bfloat16* __restrict__ x16_next) {
+  pdl_enter();
+  __shared__ int s_idx[kMergeCap];
+  __shared__ float s_val[kMergeCap];
+  __shared__ float s_R, s_M;
+  __shared__ int s_n, s_cnt, s_last;
+  __shared__ double red[kSelThreads / 32];
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int64_t row = blockIdx.x;
+  const int b = (int)(row / K);
+  const int cur0 = *d_cur;
+  const int k = dk[row];
+  const int64_t vals_off = cand_ld / 2;
+  int32_t* crow = cand_idx + row * cand_ld;
+  if (k > 0) {
+    if (w == 0) {
+      const float gv = lane < k ? ord2f(gmax[row * 32 + lane]) : INFINITY;
+      gmax[row * 32 + lane] = f2ord(-INFINITY);  // ready for the next step
+      const float R = warp_min(gv);
+      const float M = warp_max(lane < k ? gv : -INFINITY);
+      if (lane == 0) {
+        s_R = R;
+        s_M = M;
+        s_n = min(sv_cnt[row], sv_cap);
+        s_cnt = 0;
+      }
+    }
+    __syncthreads();
+    const float R = s_R, M = s_M;
+    const int n = s_n;
+    double acc = 0.0;
+    for (int t = tid; t < ntiles; t += kSelThreads)  // fixed assignment + tree: deterministic
+      acc += tsum[row * ldt + t] * exp((double)tmax[row * ldt + t] - (double)M);
+    const double S = block_sum(acc, red);
+    for (int i = tid; i < n; i += kSelThreads) {
+      const int2 e = sv[row * sv_cap + i];
+      const float v = __int_as_float(e.y);
+      if (v >= R) {
+        const int p = atomicAdd(&s_cnt, 1);
+        if (p < kMergeCap) { s_idx[p] = e.x; s_val[p] = v; }
+      }
+    }
+    __syncthreads();
+    const int c = s_cnt;
+    const int cw = min(c, kMergeCap);
+    for (int i = tid; i < cw; i += kSelThreads) {
+      const int j = s_idx[i];
+      int rk = 0;
+      for (int q = 0; q < cw; ++q) rk += s_idx[q] < j ? 1 : 0;
+      crow[rk] = j;
+      if (rk < vals_off) crow[vals_off + rk] = __float_as_int(s_val[i]);
+    }
+    if (tid == 0) {
+      if (c > kMergeCap) atomicAdd(d_ovf, 1);  // tie-heavy row: beyond this path
+      sv_cnt[row] = 0;
+      cand_count[row] = cw;
+      lse[row] = (double)M + log(S);
+    }
+  } else if (tid == 0) {
+    cand_count[row] = 0;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    const int prev = atomicAdd(counters + b, 1);
+    s_last = prev == K - 1;
+    if (s_last) counters[b] = 0;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  stage2_and_next(b, nullptr, 0, lse, cand_idx, cand_ld, cand_count, st, K, max_len, eos, len_pow,
+                  d_cur, max_steps, row_tokens, row_parents, hist, vals_off, cur0, emb, d,
+                  emb_scale, pos, x_next, x16_next, batch, counters + batch);
+  __syncthreads();
+  if (tid < K) {  // group counts of the item's rows for the next step (decode.py:230)
+    const int live = st.live[b];
+    dk[(int64_t)b * K + tid] = (!st.done[b] && tid < live) ? min(K + live, V) : 0;
+  }
+}
+
 __global__ void hars_groups_kernel(fq_beam_state st, int batch, int K, int V, int exhaustive,
                                    int32_t* d_k) {
   pdl_enter();
@@ -1677,6 +1777,34 @@ int fq_hars_step(const float* logits, int64_t ld, fq_beam_state st, int64_t batc
   return launch_status("fq_hars_step");
 }
 
+int fq_hars_merge_step(fq_beam_state st, int64_t batch, int64_t beam, int64_t vocab,
+                       int64_t max_len, int64_t eos, const double* len_pow, int32_t* d_cur,
+                       int64_t max_steps, int32_t* dk, int32_t* gmax, const float* tmax,
+                       const double* tsum, int64_t ldt, int64_t ntiles, int32_t* sv_cnt,
+                       const void* sv, int64_t sv_cap, double* lse, int32_t* cand_idx,
+                       int64_t cand_ld, int64_t* cand_count, int32_t* counters, int32_t* d_ovf,
+                       int64_t* row_tokens, int64_t* row_parents, int32_t* hist,
+                       const float* emb, int64_t d_model, float emb_scale, const float* pos,
+                       float* x_next, void* x16_next, fq_stream_t stream) {
+  FQ_CHECK_ARG(d_cur && dk && gmax && tmax && tsum && sv_cnt && sv && lse && cand_idx &&
+                   cand_count && counters && d_ovf && row_tokens && row_parents && batch > 0 &&
+                   beam >= 1 && beam <= kMaxBeam && 2 * beam <= 32 && ntiles <= ldt &&
+                   cand_ld >= vocab && cand_ld / 2 >= kMergeCap,
+               FQ_ERR_DIMENSION, "fq_hars_merge_step: bad args");
+  FQ_CHECK_ARG(!x_next || (emb && pos && d_model > 0 && d_model % 4 == 0),
+               FQ_ERR_DIMENSION, "fq_hars_merge_step: next-step embedding needs emb/pos");
+  const size_t smem = sel_smem(beam, max_len);
+  FQ_CHECK_ARG(smem <= 96 * 1024, FQ_ERR_CAPACITY, "fq_hars_merge_step: max_len too large");
+  launch_kernel(hars_merge_step_kernel, (unsigned)(batch * beam), kSelThreads, smem,
+                as_stream(stream), 1u, (int)vocab, st, (int)batch, (int)beam, (int)max_len,
+                (int)eos, len_pow, d_cur, max_steps, dk, gmax, tmax, tsum, (int)ldt, (int)ntiles,
+                sv_cnt, reinterpret_cast<const int2*>(sv), (int)sv_cap, lse, cand_idx, cand_ld,
+                cand_count, counters, d_ovf, row_tokens, row_parents, hist,
+                x_next ? emb : nullptr, (int)d_model, emb_scale, pos, x_next,
+                reinterpret_cast<__nv_bfloat16*>(x16_next));
+  return launch_status("fq_hars_merge_step");
+}
+
 int fq_hars_groups(fq_beam_state st, int64_t batch, int64_t beam, int64_t vocab, int exhaustive,
                    int32_t* d_k, fq_stream_t stream) {
   FQ_CHECK_ARG(d_k && batch > 0 && beam > 0, FQ_ERR_DIMENSION, "fq_hars_groups: bad args");
@@ -1706,6 +1834,8 @@ int fq_hars_prepare(void) {
       cudaFuncSetAttribute(retrieve_split_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            64 * 1024) != cudaSuccess ||
       cudaFuncSetAttribute(hars_step_split_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           96 * 1024) != cudaSuccess ||
+      cudaFuncSetAttribute(hars_merge_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            96 * 1024) != cudaSuccess) {
     set_error("fq_prepare: cannot opt in to large shared memory (hars)");
     return FQ_ERR_CUDA;

@@ -22,6 +22,7 @@ from __future__ import annotations
 
 import dataclasses
 import math
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -54,6 +55,9 @@ class _GroupedBeamState:
         for st in self.states:
             out.extend(st.host_items())
         return out
+
+
+_ORD_NEG_INF = -2139095041  # -inf as the ordered int of fq_logits_hars' running maxima
 
 
 class Session:
@@ -174,6 +178,13 @@ class Session:
         # GEMMs keep the same per-SM ingest and double the launches), so the
         # default is one chain.
         ngroups = 2 if (self.streams == 2 and fused and self.use_graphs and batch >= 2) else 1
+        # output layer: FQ_LOGITS_HARS=1 (opt-in) runs the logits GEMM with the HARS
+        # stage-1 statistics epilogue + fq_hars_merge_step (logits never written);
+        # measured slower than materialised logits + fq_hars_step (122 vs 41 us for
+        # the GEMM: a thread-per-row statistics epilogue with one warp per SMSP
+        # cannot hide its latency), so the default keeps the materialised path
+        lh = (fused and self.dw.bf16 and os.environ.get("FQ_LOGITS_HARS", "0") == "1"
+              and self.config.d_model % 64 == 0 and V >= 4096)
         bounds = [0, batch] if ngroups == 1 else [0, (batch + 1) // 2, batch]
         groups = []
         for g in range(ngroups):
@@ -205,6 +216,20 @@ class Session:
             if fused:
                 grp["hcnt"] = bufs.get("hars.counters", (nb + 1 + nr,), torch.int32)
                 grp["hcnt"].zero_()
+            if fused and lh:  # fused logits + HARS stage 1 (the logits never materialised)
+                ldt = (V + 223) // 224
+                grp["ldt"] = ldt
+                grp["gmax"] = bufs.get("hars.gmax", (nr, 32), torch.int32)
+                grp["gmax"].fill_(_ORD_NEG_INF)
+                grp["tmax"] = bufs.get("hars.tmax", (nr, ldt), torch.float32)
+                grp["tsum"] = bufs.get("hars.tsum", (nr, ldt), torch.float64)
+                grp["svcnt"] = bufs.get("hars.svcnt", (nr,), torch.int32)
+                grp["svcnt"].zero_()
+                grp["sv"] = bufs.get("hars.sv", (nr, V, 2), torch.int32)
+                grp["ovf"] = bufs.get("hars.ovf", (1,), torch.int32)
+                grp["ovf"].zero_()
+                _abi.call("fq_hars_groups", st.c, nb, K, V, 0, grp["hk"].data_ptr(),
+                          _abi.stream_handle())
             groups.append(grp)
 
         def body(gr):
@@ -212,8 +237,29 @@ class Session:
             nb, nr = gr["batch"], gr["rows"]
             lse, ci, cc, hk, parents, lp = (gr[k] for k in ("lse", "ci", "cc", "hk", "parents",
                                                            "lp"))
-            logits = step.run(embed=not fused)
             stream = _abi.stream_handle()
+            if fused and lh:
+                # layers, then the logits GEMM whose epilogue emits HARS stage-1
+                # statistics, then the per-row merge + stage 2 + next embedding
+                step.run(embed=False, logits=False)
+                d = self.config.d_model
+                _abi.call("fq_logits_hars", step.x16.data_ptr(), d, self.dw.out_proj.data_ptr(),
+                          self.dw.out_proj.stride(0), nr, V, d, hk.data_ptr(),
+                          gr["gmax"].data_ptr(), gr["tmax"].data_ptr(), gr["tsum"].data_ptr(),
+                          gr["ldt"], gr["svcnt"].data_ptr(), gr["sv"].data_ptr(), V, stream)
+                _abi.call("fq_hars_merge_step", st.c, nb, K, V, self.config.max_seq_len,
+                          cfg.eos_token, _abi.ptr(lp), cache.d_cur.data_ptr(), max_steps,
+                          hk.data_ptr(), gr["gmax"].data_ptr(), gr["tmax"].data_ptr(),
+                          gr["tsum"].data_ptr(), gr["ldt"], gr["ldt"], gr["svcnt"].data_ptr(),
+                          gr["sv"].data_ptr(), V, lse.data_ptr(), ci.data_ptr(), ci.stride(0),
+                          cc.data_ptr(), gr["hcnt"].data_ptr(), gr["ovf"].data_ptr(),
+                          step.tokens.data_ptr(), parents.data_ptr(), cache.hist.data_ptr(),
+                          self.dw.embedding.data_ptr(), d,
+                          float(np.float32(math.sqrt(d))), self.dw.positions.data_ptr(),
+                          step.x.data_ptr(), _abi.ptr(step.x16), stream)
+                self.counters.count_fused("logits_hars", nr * gr["ldt"] * 12)
+                return
+            logits = step.run(embed=not fused)
             if fused:  # groups + stage 1 + stage 2 + position advance + next embedding
                 _abi.call("fq_hars_step", logits.data_ptr(), logits.stride(0), st.c, nb, K, V,
                           self.config.max_seq_len, cfg.eos_token, _abi.ptr(lp),
@@ -287,6 +333,9 @@ class Session:
         torch.cuda.synchronize()
         if any(int(g["step"].bad.item()) for g in groups):
             raise FullMaskError("fully masked cross-attention row")
+        if any(int(g["ovf"].item()) for g in groups if "ovf" in g):
+            raise EngineError("more than 2048 candidates in a row (tie-heavy logits) on the "
+                              "fused logits/HARS path; set FQ_LOGITS_HARS=0")
         states = result.host_items()
         return [[Hypothesis(tokens=s, score=sc) for s, sc in state.finalize(cfg)]
                 for state in states]

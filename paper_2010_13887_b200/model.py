@@ -637,10 +637,11 @@ class DecoderStep:
                   _abi.stream_handle())
         self.counters.count_fused("embed_scale_pos", R * d * 8)
 
-    def run(self, embed: bool = True):
+    def run(self, embed: bool = True, logits: bool = True):
         """Embed -> L decoder layers -> logits. Position comes from cache.d_cur.
         ``embed=False``: the input rows were already written (by the previous
-        step's fused HARS launch, fq_hars_step)."""
+        step's fused HARS launch, fq_hars_step). ``logits=False``: stop after the
+        layers (the output layer runs as fq_logits_hars on ``x16``)."""
         c, dw, ctr, tm = self.config, self.dw, self.counters, self.timers
         R, d, h, hd, L = self.rows, c.d_model, c.num_heads, c.head_dim, c.num_decoder_layers
         stream = _abi.stream_handle()
@@ -683,6 +684,8 @@ class DecoderStep:
                  residual=self.cnorm, counters=ctr, timers=tm)
             _ln(self.u, lw["ln3_g"], lw["ln3_b"], c.ln_eps, self.x, self.x16, counters=ctr)
             x, x16 = self.x, self.x16
+        if not logits:
+            return None
         _lin(dw, x, x16, dw.out_proj, self.logits, counters=ctr, timers=tm) if dw.bf16 else \
             gemm(x, dw.out_proj, self.logits, transpose_b=True, counters=ctr, timers=tm)
         return self.logits
@@ -785,12 +788,20 @@ def plan_intermediates(config: ModelConfig, precision: str = "fp32") -> list[Int
             add("dec.cnorm16", R * d * 2, dec0, end - 3)
         add("dec.logits", R * V * 4, end - 3, end)
         # HARS stage 1 / 2 and the device beam state (whole request)
-        add("hars.k", R * 4, end - 2, end)
+        add("hars.k", R * 4, setup, end)  # persists across steps (fq_hars_merge_step)
         add("hars.len_pow", (S + 1) * 8, setup, end)
         add("hars.counters", (B + 1 + R) * 4, setup, end)
         add("hars.lse", R * 8, end - 2, end)
         add("hars.cand_idx", R * V * 4, end - 2, end)
         add("hars.cand_count", R * 8, end - 2, end)
+        if bf:  # fq_logits_hars statistics (the fused logits + HARS stage-1 output layer)
+            ldt = (V + 223) // 224
+            add("hars.gmax", R * 32 * 4, setup, end)
+            add("hars.tmax", R * ldt * 4, end - 3, end)
+            add("hars.tsum", R * ldt * 8, end - 3, end)
+            add("hars.svcnt", R * 4, setup, end)
+            add("hars.sv", R * V * 8, end - 3, end)
+            add("hars.ovf", 4, setup, end)
         for nm, sz in (("live", B * 4), ("step", B * 4), ("done", B * 4),
                        ("prefix", B * K * S * 4), ("cum", B * K * 8), ("fin_count", B * 4),
                        ("fin_tok", B * K * S * 4), ("fin_len", B * K * 4),

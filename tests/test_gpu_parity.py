@@ -534,6 +534,104 @@ def test_fused_hars_step_equals_separate_launches(P, split, monkeypatch):
             assert torch.equal(b["x"], want), t
 
 
+@pytest.mark.parametrize("B,d,V", [(6, 256, 32000), (128, 1024, 32000), (8, 128, 8192)])
+def test_logits_hars_equals_materialised_path(P, B, d, V):
+    """fq_logits_hars (logits GEMM whose epilogue emits HARS stage-1
+    statistics; the [rows, V] logits never written) + fq_hars_merge_step
+    reproduce GEMM -> fq_hars_step step for step: candidates, lse, tokens,
+    parents, KV history and beam state, with EOS picks and a length penalty."""
+    import torch
+    from paper_2010_13887_b200 import _abi, decode as D
+    K, S, eos = 4, 12, 7
+    R = B * K
+    g = torch.Generator(device="cuda").manual_seed(3)
+    lp = D.length_penalty_table(0.6, S, "cuda")
+    E = (torch.randn(V, d, device="cuda", generator=g) * 0.5).bfloat16()
+    emb = torch.randn(V, d, device="cuda", generator=g)
+    pos = torch.randn(S, d, device="cuda", generator=g)
+    ldt = (V + 223) // 224
+
+    def mk():
+        st = D.DeviceBeamState(B, K, S)
+        st.init()
+        return dict(st=st, cur=torch.zeros(1, dtype=torch.int32, device="cuda"),
+                    hist=torch.arange(R, dtype=torch.int32, device="cuda")[:, None].repeat(1, S).contiguous(),
+                    tok=torch.zeros(R, dtype=torch.int64, device="cuda"),
+                    par=torch.zeros(R, dtype=torch.int64, device="cuda"),
+                    lse=torch.zeros(R, dtype=torch.float64, device="cuda"),
+                    ci=torch.zeros(R, V, dtype=torch.int32, device="cuda"),
+                    cc=torch.zeros(R, dtype=torch.int64, device="cuda"),
+                    cnt=torch.zeros(B + 1 + R, dtype=torch.int32, device="cuda"),
+                    x=torch.zeros(R, d, device="cuda"))
+    a, b = mk(), mk()
+    dk = torch.zeros(R, dtype=torch.int32, device="cuda")
+    gmax = torch.full((R, 32), -2139095041, dtype=torch.int32, device="cuda")  # ord(-inf)
+    tmax = torch.zeros(R, ldt, device="cuda")
+    tsum = torch.zeros(R, ldt, dtype=torch.float64, device="cuda")
+    svc = torch.zeros(R, dtype=torch.int32, device="cuda")
+    sv = torch.zeros(R, V, 2, dtype=torch.int32, device="cuda")
+    ovf = torch.zeros(1, dtype=torch.int32, device="cuda")
+    hs = _abi.stream_handle
+    _abi.call("fq_hars_groups", b["st"].c, B, K, V, 0, dk.data_ptr(), hs())
+    logits = torch.empty(R, V, device="cuda")
+    for t in range(S - 1):
+        x16 = torch.randn(R, d, device="cuda", generator=g).bfloat16()
+        x16[:, :8] += 2.0 * (t % 3 == 2)  # shifts every logit row: ties of nothing, EOS mixes in
+        P.gemm(x16, E, logits, transpose_b=True)
+        _abi.call("fq_hars_step", logits.data_ptr(), V, a["st"].c, B, K, V, S, eos, lp.data_ptr(),
+                  a["cur"].data_ptr(), S, a["lse"].data_ptr(), a["ci"].data_ptr(), V,
+                  a["cc"].data_ptr(), a["cnt"].data_ptr(), a["tok"].data_ptr(),
+                  a["par"].data_ptr(), a["hist"].data_ptr(), emb.data_ptr(), d,
+                  float(np.float32(8.0)), pos.data_ptr(), a["x"].data_ptr(), None, hs())
+        _abi.call("fq_logits_hars", x16.data_ptr(), d, E.data_ptr(), d, R, V, d, dk.data_ptr(),
+                  gmax.data_ptr(), tmax.data_ptr(), tsum.data_ptr(), ldt, svc.data_ptr(),
+                  sv.data_ptr(), V, hs())
+        _abi.call("fq_hars_merge_step", b["st"].c, B, K, V, S, eos, lp.data_ptr(),
+                  b["cur"].data_ptr(), S, dk.data_ptr(), gmax.data_ptr(), tmax.data_ptr(),
+                  tsum.data_ptr(), ldt, ldt,
+                  svc.data_ptr(), sv.data_ptr(), V, b["lse"].data_ptr(), b["ci"].data_ptr(), V,
+                  b["cc"].data_ptr(), b["cnt"].data_ptr(), ovf.data_ptr(), b["tok"].data_ptr(),
+                  b["par"].data_ptr(), b["hist"].data_ptr(), emb.data_ptr(), d,
+                  float(np.float32(8.0)), pos.data_ptr(), b["x"].data_ptr(), None, hs())
+        torch.cuda.synchronize()
+        assert int(ovf.item()) == 0
+        assert torch.equal(a["cc"], b["cc"]), t
+        for r in range(R):
+            n = int(a["cc"][r])
+            assert torch.equal(a["ci"][r, :n], b["ci"][r, :n]), (t, r)
+        # both f64 sums of fp32 exp terms, per row vs per tile reference points
+        assert float(((a["lse"] - b["lse"]).abs() / a["lse"].abs().clamp(min=1)).max()) <= 1e-7, t
+        for key in ("tok", "par", "hist", "cur"):
+            assert torch.equal(a[key], b[key]), (t, key)
+        tol = 1e-7 * float(a["lse"].abs().max()) + 1e-9  # scores carry the lse rounding
+        for n_, _, _ in D.DeviceBeamState.FIELDS:
+            x_, y_ = getattr(a["st"], n_), getattr(b["st"], n_)
+            if n_ in ("cum", "fin_score"):
+                assert float((x_ - y_).abs().max()) <= (t + 1) * tol, (t, n_)
+            else:
+                assert torch.equal(x_, y_), (t, n_)
+        assert torch.equal(a["x"], b["x"]), t
+        assert int(svc.sum()) == 0 and int((gmax != -2139095041).sum()) == 0  # reset for next step
+
+
+def test_logits_hars_engine_path_token_identical(P, monkeypatch):
+    """Session.generate with FQ_LOGITS_HARS=1 (fused logits + stage-1 statistics,
+    no [rows, V] logits) gives the same hypotheses as the default path."""
+    cfg = P.ModelConfig(num_encoder_layers=1, num_decoder_layers=2, d_model=128, d_ff=256,
+                        num_heads=2, vocab_size=8192, max_batch=8, max_seq_len=16,
+                        max_beam_size=4)
+    w = P.make_random_weights(cfg, seed=4)
+    src = np.random.default_rng(2).integers(3, cfg.vocab_size, size=(8, 10))
+    dc = P.DecodeConfig(beam_size=4, max_steps=12, eos_token=2, length_penalty=0.6)
+    want = P.Session(cfg, w, precision="bf16").generate(src, dc)
+    monkeypatch.setenv("FQ_LOGITS_HARS", "1")
+    got = P.Session(cfg, w, precision="bf16").generate(src, dc)
+    assert [[h.tokens for h in x] for x in got] == [[h.tokens for h in x] for x in want]
+    for x, y in zip(got, want):
+        for h1, h2 in zip(x, y):
+            assert abs(h1.score - h2.score) <= 1e-5 * max(1.0, abs(h2.score))
+
+
 @pytest.mark.parametrize("kw,bar", [
     # one fused layer each: the north_star's 1e-3, measured 3e-4 .. 1.4e-3 RMS
     (dict(num_encoder_layers=1, num_decoder_layers=1, d_model=256, d_ff=512, num_heads=4,
