@@ -227,10 +227,11 @@ int fq_hars_step(const float* logits, int64_t ld, fq_beam_state st, int64_t batc
  * statistics per row and column tile: strided group maxima folded into the
  * row's running maxima gmax [rows][32] (ordered ints, -inf between steps) with
  * global atomics, the tile-row maximum tmax and sum of exp(x - tmax) tsum
- * ([rows][ldt], column tiles of 224: ldt >= ceil(vocab/224)), and every element >= the row's
- * current bound min_g(running max) <= R appended to sv [rows][sv_cap] (int2
- * column, value bits; sv_cnt [rows] zero between steps). dk [rows]: group count
- * per row (0 = skip). Replaces model.py:627-629 + decode.py:58-92 stage 1. */
+ * ([rows][ldt], column tiles of 224: ldt >= ceil(vocab/224)), and every element >= the
+ * tile-local bound min_g(tile group max) <= R stored in the tile-row's own slots
+ * sv [rows][ldt][sv_cap] (int2 column, value bits) with its count in
+ * sv_cnt [rows][ldt] (> sv_cap: overflow). dk [rows]: group count per row (0 =
+ * skip). Replaces model.py:627-629 + decode.py:58-92 stage 1. */
 int fq_logits_hars(const void* x16, int64_t ldx, const void* emb16, int64_t lde, int64_t rows,
                    int64_t vocab, int64_t d, const int32_t* dk, int32_t* gmax, float* tmax,
                    double* tsum, int64_t ldt, int32_t* sv_cnt, void* sv, int64_t sv_cap,
@@ -240,8 +241,9 @@ int fq_logits_hars(const void* x16, int64_t ldx, const void* emb16, int64_t lde,
  * tile sums) and the ordered candidates x >= R from the survivors; then per
  * item stage 2 + next-step embedding + position advance exactly as
  * fq_hars_step, and the item's group counts for the next step in dk. Resets
- * gmax / sv_cnt. counters: int32 [batch + 1] zeroed once; d_ovf counts rows
- * with more than 2048 candidates (tie-heavy; not supported on this path). */
+ * gmax. ntiles <= 256. counters: int32 [batch + 1] zeroed once; d_ovf counts
+ * survivor-slot overflows and rows with more than 2048 candidates (tie-heavy
+ * logits; not supported on this path). */
 int fq_hars_merge_step(fq_beam_state st, int64_t batch, int64_t beam, int64_t vocab,
                        int64_t max_len, int64_t eos, const double* len_pow, int32_t* d_cur,
                        int64_t max_steps, int32_t* dk, int32_t* gmax, const float* tmax,

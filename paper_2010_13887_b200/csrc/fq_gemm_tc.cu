@@ -155,11 +155,11 @@ struct Epi {
 // current bound min_g(running group max) <= R as a survivor.
 struct HarsEpi {
   const int32_t* dk;  // [M] group count per row (0: row not searched)
-  int* gmax;          // [M][32] running group maxima, ordered ints (-inf between steps)
+  int* gmax;          // [M][32] row group maxima, ordered ints (-inf between steps)
   float* tmax;        // [M][ldt] tile-row maxima
   double* tsum;       // [M][ldt] sum over the tile-row of exp(x - tmax)
-  int* sv_cnt;        // [M] survivor counts (0 between steps)
-  int2* sv;           // [M][sv_cap] survivors (column, value bits)
+  int* sv_cnt;        // [M][ldt] survivors of the tile-row (may exceed sv_cap: overflow)
+  int2* sv;           // [M][ldt][sv_cap] survivors (column, value bits)
   int sv_cap;
   int ldt;
 };
@@ -362,7 +362,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int q = warp & 3;
     float* gms = stage_out + 4 * 32 * 33 + ((warp - 2) * 32 + lane) * 33;  // per-thread scratch
     constexpr float L2E = 1.4426950408889634f;
-    constexpr float L2E_LO = 1.925963033500011e-08f;
     int local = 0;
     for (int g = cluster_id; g < ngroups; g += nclusters, ++local) {
       const int as = local & 1;
@@ -372,41 +371,62 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&tfull_bar[as], (local >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       for (int gq = 0; gq < k; ++gq) gms[gq] = -INFINITY;
-      // pass 1: tile-row maximum and group maxima (group of column c: c % k)
+      // pass 1: tile-row maximum and group maxima (group of column c: c % k).
+      // k = 8 (the steady beam-4 step, K + live): 32 % 8 == 0, so column j of
+      // every 32-column chunk is in group (n0 + j) % 8 -> 8 register maxima
+      // indexed at compile time; other k: per-thread shared-memory maxima.
       float mt = -INFINITY;
+      float g8[8] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY,
+                     -INFINITY, -INFINITY, -INFINITY, -INFINITY};
       int gi = k > 0 ? n0 % k : 0;
 #pragma unroll 1
       for (int cc = 0; cc < BN; cc += 32) {
         float v[32];
         tmem_ld32(tmem + as * BN + ((uint32_t)(q * 32) << 16) + cc, v);
-        if (k > 0) {
+        if (k == 8) {
+          if (n0 + cc + 32 <= N) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) g8[j & 7] = fmaxf(g8[j & 7], v[j]);
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (n0 + cc + j < N) g8[j & 7] = fmaxf(g8[j & 7], v[j]);
+          }
+        } else if (k > 0) {
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
-            if (n0 + cc + j < N) {
-              gms[gi] = fmaxf(gms[gi], v[j]);
-              mt = fmaxf(mt, v[j]);
-            }
+            if (n0 + cc + j < N) gms[gi] = fmaxf(gms[gi], v[j]);
             if (++gi == k) gi = 0;
           }
         }
       }
-      // publish: running row maxima; bound = min over groups (<= the row's R)
+      if (k == 8) {  // register q holds group (n0 + q) % 8
+#pragma unroll
+        for (int qq = 0; qq < 8; ++qq) gms[(n0 + qq) & 7] = g8[qq];
+      }
+      for (int gq = 0; gq < k; ++gq) mt = fmaxf(mt, gms[gq]);
+      // publish the tile's group maxima into the row maxima (fire-and-forget
+      // reductions); the survivor bound is the tile-local min over groups of the
+      // tile's maxima (<= the row's R), so no global round trip is waited on
       float bound = INFINITY;
       if (k > 0) {
-        int old[32];
 #pragma unroll
         for (int gq = 0; gq < 32; ++gq)
-          if (gq < k) old[gq] = atomicMax(he.gmax + (int64_t)r * 32 + gq, hs_f2ord(gms[gq]));
-#pragma unroll
-        for (int gq = 0; gq < 32; ++gq)
-          if (gq < k) bound = fminf(bound, fmaxf(hs_ord2f(old[gq]), gms[gq]));
+          if (gq < k) {
+            atomicMax(he.gmax + (int64_t)r * 32 + gq, hs_f2ord(gms[gq]));
+            bound = fminf(bound, gms[gq]);
+          }
       }
-      // pass 2: sum exp(x - mt) (fp32 terms, f64 sum) and survivors x >= bound,
-      // kept in the scratch (16 pairs) and flushed with one atomic per tile
+      // pass 2: sum exp(x - mt) (fp32 per 32-column chunk, f64 across chunks)
+      // and survivors x >= bound: a branch-free per-chunk bit mask, then the set
+      // bits (a few per chunk) re-read from the warp's staging row and stored to
+      // the tile-row's own slots (no atomics)
       const float mL = mt * L2E;
+      const int tn = n0 / BN;
+      int2* svr = he.sv + ((int64_t)r * he.ldt + tn) * he.sv_cap;
+      float* strow = stage_out + ((warp - 2) * 32 + lane) * 33;
       double s = 0.0;
       int ns = 0;
-      int* svl = reinterpret_cast<int*>(gms);
 #pragma unroll 1
       for (int cc = 0; cc < BN; cc += 32) {
         float v[32];
@@ -417,39 +437,38 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (lane == 0) mbar_arrive(&tempty_bar[as]);
         }
         if (k > 0) {
+          const int nval = min(32, N - (n0 + cc));  // valid columns of this chunk
+          float t = 0.0f;
+          uint32_t mask = 0u;
+          if (nval >= 32) {
 #pragma unroll
-          for (int j0 = 0; j0 < 32; j0 += 4) {
-            float t4 = 0.0f;
-#pragma unroll
-            for (int j = j0; j < j0 + 4; ++j) {
-              const int col = n0 + cc + j;
-              if (col < N) {
-                t4 += hs_ex2(fmaf(v[j], L2E_LO, fmaf(v[j], L2E, -mL)));
-                if (v[j] >= bound) {
-                  if (ns < 16) {
-                    svl[2 * ns] = col;
-                    svl[2 * ns + 1] = __float_as_int(v[j]);
-                  } else {
-                    const int p = atomicAdd(he.sv_cnt + r, 1);
-                    if (p < he.sv_cap) he.sv[(int64_t)r * he.sv_cap + p] = make_int2(col, __float_as_int(v[j]));
-                  }
-                  ++ns;
-                }
-              }
+            for (int j = 0; j < 32; ++j) {
+              t += hs_ex2(fmaf(v[j], L2E, -mL));  // bf16 mode: one-FMA argument
+              mask |= (v[j] >= bound ? 1u : 0u) << j;
             }
-            s += (double)t4;
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (j < nval) {
+                t += hs_ex2(fmaf(v[j], L2E, -mL));
+                mask |= (v[j] >= bound ? 1u : 0u) << j;
+              }
+          }
+          s += (double)t;
+          if (mask) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) strow[j] = v[j];
+            while (mask) {
+              const int j = __ffs(mask) - 1;
+              mask &= mask - 1u;
+              if (ns < he.sv_cap) svr[ns] = make_int2(n0 + cc + j, __float_as_int(strow[j]));
+              ++ns;
+            }
           }
         }
       }
       if (k > 0) {
-        const int nl = ns < 16 ? ns : 16;
-        if (nl > 0) {
-          const int p0 = atomicAdd(he.sv_cnt + r, nl);
-          for (int i = 0; i < nl; ++i)
-            if (p0 + i < he.sv_cap)
-              he.sv[(int64_t)r * he.sv_cap + p0 + i] = make_int2(svl[2 * i], svl[2 * i + 1]);
-        }
-        const int tn = n0 / BN;
+        he.sv_cnt[(int64_t)r * he.ldt + tn] = ns;
         he.tmax[(int64_t)r * he.ldt + tn] = mt;
         he.tsum[(int64_t)r * he.ldt + tn] = s;
       }

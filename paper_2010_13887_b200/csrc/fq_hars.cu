@@ -1485,8 +1485,10 @@ __global__ void __launch_bounds__(kSelThreads) hars_merge_step_kernel(
   __shared__ int s_idx[kMergeCap];
   __shared__ float s_val[kMergeCap];
   __shared__ float s_R, s_M;
-  __shared__ int s_n, s_cnt, s_last;
+  __shared__ int s_n, s_cnt, s_last, s_total;
   __shared__ double red[kSelThreads / 32];
+  __shared__ int s_off[kSelThreads + 1];
+  __shared__ int warp_tot[32];
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int64_t row = blockIdx.x;
   const int b = (int)(row / K);
@@ -1503,23 +1505,39 @@ __global__ void __launch_bounds__(kSelThreads) hars_merge_step_kernel(
       if (lane == 0) {
         s_R = R;
         s_M = M;
-        s_n = min(sv_cnt[row], sv_cap);
         s_cnt = 0;
       }
     }
     __syncthreads();
     const float R = s_R, M = s_M;
-    const int n = s_n;
+    // tile t (ntiles <= kSelThreads: thread per tile): its survivor count, 0 when
+    // the tile's maximum is below R (no candidate there); overflow is fatal
+    int my_n = 0;
     double acc = 0.0;
-    for (int t = tid; t < ntiles; t += kSelThreads)  // fixed assignment + tree: deterministic
-      acc += tsum[row * ldt + t] * exp((double)tmax[row * ldt + t] - (double)M);
-    const double S = block_sum(acc, red);
-    for (int i = tid; i < n; i += kSelThreads) {
-      const int2 e = sv[row * sv_cap + i];
-      const float v = __int_as_float(e.y);
+    if (tid < ntiles) {
+      const float tm = tmax[row * ldt + tid];
+      acc = tsum[row * ldt + tid] * exp((double)tm - (double)M);
+      const int c = sv_cnt[row * ldt + tid];
+      if (c > sv_cap) atomicAdd(d_ovf, 1);
+      my_n = tm >= R ? min(c, sv_cap) : 0;
+    }
+    const double S = block_sum(acc, red);  // fixed tile order: deterministic
+    const int my_off = block_excl_scan(my_n, warp_tot, &s_total);
+    s_off[tid] = my_off;
+    if (tid == 0) s_off[kSelThreads] = s_total;
+    __syncthreads();
+    const int n = s_total;
+    for (int e = tid; e < n; e += kSelThreads) {
+      int lo = 0, hi = ntiles - 1;  // last tile t with s_off[t] <= e
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (s_off[mid] <= e) lo = mid; else hi = mid - 1;
+      }
+      const int2 en = sv[((int64_t)row * ldt + lo) * sv_cap + (e - s_off[lo])];
+      const float v = __int_as_float(en.y);
       if (v >= R) {
         const int p = atomicAdd(&s_cnt, 1);
-        if (p < kMergeCap) { s_idx[p] = e.x; s_val[p] = v; }
+        if (p < kMergeCap) { s_idx[p] = en.x; s_val[p] = v; }
       }
     }
     __syncthreads();
@@ -1534,7 +1552,6 @@ __global__ void __launch_bounds__(kSelThreads) hars_merge_step_kernel(
     }
     if (tid == 0) {
       if (c > kMergeCap) atomicAdd(d_ovf, 1);  // tie-heavy row: beyond this path
-      sv_cnt[row] = 0;
       cand_count[row] = cw;
       lse[row] = (double)M + log(S);
     }
@@ -1789,6 +1806,7 @@ int fq_hars_merge_step(fq_beam_state st, int64_t batch, int64_t beam, int64_t vo
   FQ_CHECK_ARG(d_cur && dk && gmax && tmax && tsum && sv_cnt && sv && lse && cand_idx &&
                    cand_count && counters && d_ovf && row_tokens && row_parents && batch > 0 &&
                    beam >= 1 && beam <= kMaxBeam && 2 * beam <= 32 && ntiles <= ldt &&
+                   ntiles <= kSelThreads &&
                    cand_ld >= vocab && cand_ld / 2 >= kMergeCap,
                FQ_ERR_DIMENSION, "fq_hars_merge_step: bad args");
   FQ_CHECK_ARG(!x_next || (emb && pos && d_model > 0 && d_model % 4 == 0),

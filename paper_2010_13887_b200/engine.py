@@ -178,13 +178,12 @@ class Session:
         # GEMMs keep the same per-SM ingest and double the launches), so the
         # default is one chain.
         ngroups = 2 if (self.streams == 2 and fused and self.use_graphs and batch >= 2) else 1
-        # output layer: FQ_LOGITS_HARS=1 (opt-in) runs the logits GEMM with the HARS
-        # stage-1 statistics epilogue + fq_hars_merge_step (logits never written);
-        # measured slower than materialised logits + fq_hars_step (122 vs 41 us for
-        # the GEMM: a thread-per-row statistics epilogue with one warp per SMSP
-        # cannot hide its latency), so the default keeps the materialised path
-        lh = (fused and self.dw.bf16 and os.environ.get("FQ_LOGITS_HARS", "0") == "1"
-              and self.config.d_model % 64 == 0 and V >= 4096)
+        # output layer (bf16): the logits GEMM with the HARS stage-1 statistics
+        # epilogue + fq_hars_merge_step, the [rows, V] logits never written
+        # (C2: 49.5 us GEMM + merge vs 40.7 us GEMM + 39 us HARS).
+        # FQ_LOGITS_HARS=0: materialised logits + fq_hars_step
+        lh = (fused and self.dw.bf16 and os.environ.get("FQ_LOGITS_HARS", "1") != "0"
+              and self.config.d_model % 64 == 0 and V >= 4096 and (V + 223) // 224 <= 256)
         bounds = [0, batch] if ngroups == 1 else [0, (batch + 1) // 2, batch]
         groups = []
         for g in range(ngroups):
@@ -223,9 +222,8 @@ class Session:
                 grp["gmax"].fill_(_ORD_NEG_INF)
                 grp["tmax"] = bufs.get("hars.tmax", (nr, ldt), torch.float32)
                 grp["tsum"] = bufs.get("hars.tsum", (nr, ldt), torch.float64)
-                grp["svcnt"] = bufs.get("hars.svcnt", (nr,), torch.int32)
-                grp["svcnt"].zero_()
-                grp["sv"] = bufs.get("hars.sv", (nr, V, 2), torch.int32)
+                grp["svcnt"] = bufs.get("hars.svcnt", (nr, ldt), torch.int32)
+                grp["sv"] = bufs.get("hars.sv", (nr, ldt, M.LH_SV_CAP, 2), torch.int32)
                 grp["ovf"] = bufs.get("hars.ovf", (1,), torch.int32)
                 grp["ovf"].zero_()
                 _abi.call("fq_hars_groups", st.c, nb, K, V, 0, grp["hk"].data_ptr(),
@@ -246,12 +244,14 @@ class Session:
                 _abi.call("fq_logits_hars", step.x16.data_ptr(), d, self.dw.out_proj.data_ptr(),
                           self.dw.out_proj.stride(0), nr, V, d, hk.data_ptr(),
                           gr["gmax"].data_ptr(), gr["tmax"].data_ptr(), gr["tsum"].data_ptr(),
-                          gr["ldt"], gr["svcnt"].data_ptr(), gr["sv"].data_ptr(), V, stream)
+                          gr["ldt"], gr["svcnt"].data_ptr(), gr["sv"].data_ptr(), M.LH_SV_CAP,
+                          stream)
                 _abi.call("fq_hars_merge_step", st.c, nb, K, V, self.config.max_seq_len,
                           cfg.eos_token, _abi.ptr(lp), cache.d_cur.data_ptr(), max_steps,
                           hk.data_ptr(), gr["gmax"].data_ptr(), gr["tmax"].data_ptr(),
                           gr["tsum"].data_ptr(), gr["ldt"], gr["ldt"], gr["svcnt"].data_ptr(),
-                          gr["sv"].data_ptr(), V, lse.data_ptr(), ci.data_ptr(), ci.stride(0),
+                          gr["sv"].data_ptr(), M.LH_SV_CAP, lse.data_ptr(), ci.data_ptr(),
+                          ci.stride(0),
                           cc.data_ptr(), gr["hcnt"].data_ptr(), gr["ovf"].data_ptr(),
                           step.tokens.data_ptr(), parents.data_ptr(), cache.hist.data_ptr(),
                           self.dw.embedding.data_ptr(), d,

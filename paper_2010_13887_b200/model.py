@@ -722,6 +722,9 @@ def decode_step(last_tokens, cache: KVCache, cross_kv, enc_mask, weights, config
 # static intermediate enumeration for the arena  (model.py:772-860)
 # ---------------------------------------------------------------------------
 
+LH_SV_CAP = 128  # fq_logits_hars survivor slots per (row, 224-column tile)
+
+
 def plan_intermediates(config: ModelConfig, precision: str = "fp32") -> list[IntermediateSpec]:
     """Every intermediate of one max-shape request with its lifetime in the
     static op order: embed, encoder layers, cross-K/V setup, one decode step
@@ -799,8 +802,8 @@ def plan_intermediates(config: ModelConfig, precision: str = "fp32") -> list[Int
             add("hars.gmax", R * 32 * 4, setup, end)
             add("hars.tmax", R * ldt * 4, end - 3, end)
             add("hars.tsum", R * ldt * 8, end - 3, end)
-            add("hars.svcnt", R * 4, setup, end)
-            add("hars.sv", R * V * 8, end - 3, end)
+            add("hars.svcnt", R * ldt * 4, end - 3, end)
+            add("hars.sv", R * ldt * LH_SV_CAP * 8, end - 3, end)
             add("hars.ovf", 4, setup, end)
         for nm, sz in (("live", B * 4), ("step", B * 4), ("done", B * 4),
                        ("prefix", B * K * S * 4), ("cum", B * K * 8), ("fin_count", B * 4),
