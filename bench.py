@@ -233,7 +233,10 @@ def probe_step_gemms(sess, src_dev, dc):
     for name, a, e0, e1, captured in probe:
         if not captured:
             continue
-        M, N, K = int(a[10]), int(a[11]), int(a[12])
+        if name == "fq_logits_hars":  # (x16, ldx, emb16, lde, rows, vocab, d, ...)
+            M, N, K = int(a[4]), int(a[5]), int(a[6])
+        else:
+            M, N, K = int(a[10]), int(a[11]), int(a[12])
         rows.append((M, N, K, e0.elapsed_time(e1) / 1e3))
     return rows
 
@@ -356,7 +359,8 @@ def run_ours(args, rank, world):
         out["roofline"] = {
             "kernel": "tc_gemm (tcgen05/TMEM/TMA bf16 GEMM with fused epilogue): every GEMM "
                       "launch of one decode step (QKV, self-out, cross-q, cross-out, FFN1, FFN2 "
-                      "x 6 layers + logits), timed with events inside the step graph",
+                      "x 6 layers + the logits GEMM, whose epilogue computes HARS stage 1), "
+                      "timed with events inside the step graph",
             "bound": "tensor", "achieved": g_flops / g_time / 1e12, "peak": tc_peak,
             "unit": "TFLOP/s", "frac": g_flops / g_time / 1e12 / tc_peak, "traffic": traffic,
             "launches_per_step": len(gemms), "flops_per_launch_mean": g_flops / max(len(gemms), 1),
@@ -458,6 +462,64 @@ def run_ours(args, rank, world):
                                "in the same graph setup (5.0-5.7 TB/s, scripts/micro/streamprobe.cu)",
             "stage1_sweep": sweep,
             "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)"}
+        # the decode step's whole output layer as the engine runs it:
+        # fused = logits GEMM with the HARS stage-1 statistics epilogue + per-row
+        # merge/stage 2 (logits never written); materialised = GEMM + fq_hars_step
+        d_m = cfg.d_model
+        E16 = sess.dw.out_proj
+        x16s = [torch.randn(R, d_m, device=dev).bfloat16() for _ in range(3)]
+        ldt = (V + 223) // 224
+        cap = 128
+        dk = torch.zeros(R, dtype=torch.int32, device=dev)
+        gmx = torch.full((R, 32), -2139095041, dtype=torch.int32, device=dev)
+        tmx = torch.zeros(R, ldt, device=dev)
+        tsm = torch.zeros(R, ldt, dtype=torch.float64, device=dev)
+        svc = torch.zeros(R, ldt, dtype=torch.int32, device=dev)
+        svb = torch.zeros(R, ldt, cap, 2, dtype=torch.int32, device=dev)
+        ovf = torch.zeros(1, dtype=torch.int32, device=dev)
+        mcnt = torch.zeros(args.batch + 1, dtype=torch.int32, device=dev)
+        lg1 = torch.empty(R, V, device=dev)
+
+        def out_fused():
+            resets()
+            x = x16s[it[0] % 3]
+            it[0] += 1
+            _abi.call("fq_logits_hars", x.data_ptr(), d_m, E16.data_ptr(), d_m, R, V, d_m,
+                      dk.data_ptr(), gmx.data_ptr(), tmx.data_ptr(), tsm.data_ptr(), ldt,
+                      svc.data_ptr(), svb.data_ptr(), cap, _abi.stream_handle())
+            _abi.call("fq_hars_merge_step", hst.c, args.batch, BEAM, V, cfg.max_seq_len, 2, None,
+                      dcur.data_ptr(), 1 << 40, dk.data_ptr(), gmx.data_ptr(), tmx.data_ptr(),
+                      tsm.data_ptr(), ldt, ldt, svc.data_ptr(), svb.data_ptr(), cap,
+                      lse.data_ptr(), ci.data_ptr(), ci.stride(0), cc.data_ptr(), mcnt.data_ptr(),
+                      ovf.data_ptr(), rt.data_ptr(), rp.data_ptr(), hist.data_ptr(), None, 0, 0.0,
+                      None, None, None, _abi.stream_handle())
+
+        def out_mat():
+            resets()
+            x = x16s[it[0] % 3]
+            it[0] += 1
+            P.gemm(x, E16, lg1, transpose_b=True)
+            _abi.call("fq_hars_step", lg1.data_ptr(), V, hst.c, args.batch, BEAM, V,
+                      cfg.max_seq_len, 2, None, dcur.data_ptr(), 1 << 40, lse.data_ptr(),
+                      ci.data_ptr(), ci.stride(0), cc.data_ptr(), hcnt.data_ptr(),
+                      rt.data_ptr(), rp.data_ptr(), hist.data_ptr(), None, 0, 0.0, None, None,
+                      None, _abi.stream_handle())
+        hst.init()
+        _abi.call("fq_hars_groups", hst.c, args.batch, BEAM, V, 0, dk.data_ptr(),
+                  _abi.stream_handle())
+        t_of = graph_time(out_fused) - t_reset
+        hst.init()
+        t_om = graph_time(out_mat) - t_reset
+        out["output_layer"] = {
+            "what": "the decode step's output layer at C2 (512 x 1024 -> 32000 logits, HARS "
+                    "stages 1+2, next embedding off): graph-timed us, state-reset fills "
+                    "subtracted",
+            "fused_us": t_of * 1e6, "materialised_us": t_om * 1e6,
+            "fused": "fq_logits_hars (tcgen05 logits GEMM, epilogue emits per-tile group "
+                     "maxima, sum exp and survivors; [rows, V] never written) + "
+                     "fq_hars_merge_step",
+            "materialised": "fq_gemm (65.5 MB fp32 logits) + fq_hars_step",
+            "hbm_bytes_avoided_per_step": 2 * R * V * 4}
     if rank == 0 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline_sample(host_w, cfg_d)
     if rank == 0:

@@ -116,7 +116,7 @@ def load():
 # become event-record nodes inside a captured CUDA graph) and
 # (name, args, start, end) is appended. Off (None) on the product path.
 PROBE = None
-PROBE_NAMES = ("fq_gemm",)
+PROBE_NAMES = ("fq_gemm", "fq_logits_hars")
 
 
 def call(name: str, *args) -> int:
