@@ -19,7 +19,11 @@ cap() {  # name regex skip
     python scripts/profile_step.py --steps 40 > gpurun_out/${T}_$1.log 2>&1
   echo "$1 rc=$?"
 }
-cap hars "hars_step" 32
+cap hars "hars_merge_step" 32
+timeout 600 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
+  -k regex:"hars_step_kernel" -s 4 -c 1 -o gpurun_out/${T}_harsstep -f python scripts/hars_step_once.py \
+  > gpurun_out/${T}_harsstep.log 2>&1
+echo "harsstep rc=$?"
 cap selfattn "decoder_self_attention" 190
 cap crossattn "cross_attention" 190
 cap ln "layer_norm_row128" 570
@@ -27,7 +31,7 @@ cap logits "tc_gemm_kernel<.int.224" 30
 cap ffn1 "tc_gemm_kernel<.int.128" 380
 cap splitk "tc_gemm_splitk" 760
 cap encattn "encoder_attention" 3
-for f in hars selfattn crossattn ln logits ffn1 splitk encattn; do
+for f in hars harsstep selfattn crossattn ln logits ffn1 splitk encattn; do
   python scripts/ncu_summary.py gpurun_out/${T}_$f.ncu-rep 12 > gpurun_out/${T}_${f}_summary.txt 2>&1
   python scripts/ncu_ops.py gpurun_out/${T}_$f.ncu-rep 12 >> gpurun_out/${T}_${f}_summary.txt 2>&1
 done
