@@ -1138,6 +1138,7 @@ __device__ __forceinline__ void select_item(
   __syncthreads();
   const int64_t n_total = offs[live];
   const int need = (int)(((int64_t)K + live) < n_total ? ((int64_t)K + live) : n_total);
+  sw_stamp(blockIdx.x, 5);
 
   auto cand_at = [&](int64_t j) -> Cand {
     int i = 0;
@@ -1159,11 +1160,22 @@ __device__ __forceinline__ void select_item(
   if (n_total <= kSelCap) {
     for (int64_t j = tid; j < n_total; j += blockDim.x) cands[j] = cand_at(j);
     __syncthreads();
-    for (int64_t j = tid; j < n_total; j += blockDim.x) {
-      const Cand c = cands[j];
+    // rank of each candidate under (-score, token, beam): 4 threads per
+    // candidate, each counting the better ones among a quarter of the list
+    // (the quarter counts summed over the 4 lanes); the top `need` are picks
+    const int n = (int)n_total;
+    const int sub = tid & 3;
+    for (int j0 = 0; j0 < n; j0 += (int)(blockDim.x >> 2)) {
+      const int j = j0 + (tid >> 2);
       int rank = 0;
-      for (int64_t i = 0; i < n_total; ++i) rank += better(cands[i], c) ? 1 : 0;
-      if (rank < need) picks[rank] = c;
+      Cand c;
+      if (j < n) {
+        c = cands[j];
+        for (int i = sub; i < n; i += 4) rank += better(cands[i], c) ? 1 : 0;
+      }
+      rank += __shfl_xor_sync(0xffffffffu, rank, 1);
+      rank += __shfl_xor_sync(0xffffffffu, rank, 2);
+      if (j < n && sub == 0 && rank < need) picks[rank] = c;
     }
   } else {
     // overflow (tie-heavy rows, exhaustive mode): `need` block-wide arg-best sweeps
@@ -1199,6 +1211,7 @@ __device__ __forceinline__ void select_item(
     }
   }
   __syncthreads();
+  sw_stamp(blockIdx.x, 6);
 
   // ---- selection walk, decode.py:192-214 (single thread; <= 2K picks) ----
   if (tid == 0) {
@@ -1276,6 +1289,7 @@ __device__ __forceinline__ void select_item(
     if (done) atomicAdd(st.n_done, 1);
   }
   __syncthreads();
+  sw_stamp(blockIdx.x, 7);
   const int nl = s_new_live, done = s_done;
   // new prefixes = parent prefix + token; cum / parents / last tokens
   for (int i = tid; i < nl * (step + 1); i += blockDim.x) {
@@ -1332,6 +1346,7 @@ __device__ __forceinline__ void stage2_and_next(
   select_item(b, logits, ld, lse, cand_idx, cand_ld, cand_count, st, K, max_len, eos, len_pow,
               d_cur, max_steps, row_tokens, row_parents, hist, vals_off, s_tok);
   __syncthreads();
+  sw_stamp(blockIdx.x, 3);
   // next step's embedding of the item's rows (embed_scale_pos, kernels.py:143-151:
   // fp32 emb * sqrt(d), then + PE[cur + 1], two roundings), so the decode step
   // needs no separate embedding launch
@@ -1492,6 +1507,7 @@ __global__ void __launch_bounds__(kSelThreads) hars_merge_step_kernel(
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int64_t row = blockIdx.x;
   const int b = (int)(row / K);
+  sw_stamp(row, 0);
   const int cur0 = *d_cur;
   const int k = dk[row];
   const int64_t vals_off = cand_ld / 2;
@@ -1559,6 +1575,7 @@ __global__ void __launch_bounds__(kSelThreads) hars_merge_step_kernel(
     cand_count[row] = 0;
   }
   __syncthreads();
+  sw_stamp(row, 1);
   if (tid == 0) {
     __threadfence();
     const int prev = atomicAdd(counters + b, 1);
@@ -1568,10 +1585,12 @@ __global__ void __launch_bounds__(kSelThreads) hars_merge_step_kernel(
   __syncthreads();
   if (!s_last) return;
   __threadfence();
+  sw_stamp(row, 2);
   stage2_and_next(b, nullptr, 0, lse, cand_idx, cand_ld, cand_count, st, K, max_len, eos, len_pow,
                   d_cur, max_steps, row_tokens, row_parents, hist, vals_off, cur0, emb, d,
                   emb_scale, pos, x_next, x16_next, batch, counters + batch);
   __syncthreads();
+  sw_stamp(row, 4);
   if (tid < K) {  // group counts of the item's rows for the next step (decode.py:230)
     const int live = st.live[b];
     dk[(int64_t)b * K + tid] = (!st.done[b] && tid < live) ? min(K + live, V) : 0;
