@@ -121,6 +121,18 @@ int fq_kv_gather_append(const float* src_k, const float* src_v, const float* new
 
 /* ---- GEMM (tensor.py:179 gemm, :207 gemm_batched) --------------------- */
 
+/* out = LN(a . w^T + bias + residual) (bf16 operands, fp32 out, optional bf16
+ * copy): model.py:596-627's GEMM + fused_bias_residual_layer_norm pairs
+ * (kernels.py:57-73) in one launch when the GEMM runs split-K over 128-column
+ * tiles and all its clusters fit on the GPU at once (the LN statistics of a
+ * row block are exchanged between its CTAs through ws); otherwise the GEMM then
+ * fq_layer_norm. ws: M * (N/128) * 16 + ceil(M/128) * 8 bytes, zeroed once
+ * (the counters reset themselves); one launch per stream at a time. */
+int fq_gemm_ln(const void* a, int64_t lda, const void* w, int64_t ldw, const float* bias,
+               const float* res, int64_t ldr, const float* gamma, const float* beta, double eps,
+               float* out, int64_t ldo, void* out16, int64_t ldo16, void* ws, int64_t ws_bytes,
+               int64_t M, int64_t N, int64_t K, fq_stream_t stream);
+
 /* C[M,N] = epilogue(A[M,K] @ op(B)); op(B) = B [K,N] (ldb) or B^T with B
  * [N,K] when transpose_b. Epilogue (fused, fp32 math): t = acc (+ C if
  * accumulate) (+ bias[N]); t = act(t); t = t + residual[M,N] (ldr).

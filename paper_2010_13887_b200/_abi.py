@@ -46,6 +46,8 @@ SIGNATURES = {
     "fq_kv_append": ([P, P, I64, I64, I64, I64, I64, P, P, P], I32),
     "fq_kv_gather_append": ([P, P, P, P, P, I64, I64, I64, I64, I64, P, P, P], I32),
     "fq_penalize_counts": ([P, I64, I64, I64, P, F32, P, I64, P], I32),
+    "fq_gemm_ln": ([P, I64, P, I64, P, P, I64, P, P, F64, P, I64, P, I64, P, I64, I64, I64, I64,
+                    P], I32),
     "fq_gemm": ([P, I32, I64, P, I32, I64, I32, P, I32, I64, I64, I64, I64, I32, P, P, I64, I32,
                  P], I32),
     "fq_gemm_plan": ([I64, I64, I64, P, P, P, P], I32),

@@ -164,6 +164,26 @@ struct HarsEpi {
   int ldt;
 };
 
+// LayerNorm of the split-K GEMM's output rows folded into its epilogue
+// (bias + residual + LN, kernels.py:57-73): every CTA of the row block
+// publishes per-row partial statistics of its 32 x BN slice (sum and the sum
+// of squared deviations from the slice mean), the row block's CTAs meet at a
+// global counter (all CTAs of the launch are co-resident: checked at launch),
+// combine the N/BN partials (parallel-variance formula, f64) and normalise
+// their own slice. ctr [mt][2] int32, zero between launches (self-resetting).
+struct LnEpi {
+  const float* gamma;
+  const float* beta;
+  double eps;
+  float* out;
+  int64_t ldo;
+  __nv_bfloat16* out16;
+  int64_t ldo16;
+  double2* stats;  // [M][nt]
+  int* ctr;
+  int nt;
+};
+
 __device__ __forceinline__ int hs_f2ord(float f) {
   const int i = __float_as_int(f);
   return i >= 0 ? i : i ^ 0x7fffffff;
@@ -593,11 +613,11 @@ __device__ __forceinline__ float4 ld_dsmem_f4(uint32_t local_addr, uint32_t rank
   return v;
 }
 
-template <int BN, int STAGES>
+template <int BN, int STAGES, bool LNF = false>
 __global__ void __launch_bounds__(kThreads, 1)
     tc_gemm_splitk_kernel(const __grid_constant__ CUtensorMap tma_a,
                           const __grid_constant__ CUtensorMap tma_b, const Epi ep, int M, int N,
-                          int K, int kb_per_split) {
+                          int K, int kb_per_split, const LnEpi ln) {
   constexpr int A_BYTES = BM * BK * 2;
   constexpr int B_BYTES = BN * BK * 2;
   constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
@@ -774,7 +794,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             x[j] = y;
           }
         }
-        if (col + 3 < N && ((ci & 3) == 0)) {
+        if constexpr (LNF) {  // keep the pre-LN row slice (my own rows of my partial)
+          *reinterpret_cast<float4*>(part + lr * PLD + c) = make_float4(x[0], x[1], x[2], x[3]);
+        } else if (col + 3 < N && ((ci & 3) == 0)) {
           if (ep.c_bf16) {
             __nv_bfloat162 lo = __floats2bfloat162_rn(x[0], x[1]), hi = __floats2bfloat162_rn(x[2], x[3]);
             uint2 pk;
@@ -789,6 +811,89 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (ep.c_bf16) c16[ci + j] = f2bf(x[j]);
             else c32[ci + j] = x[j];
           }
+        }
+      }
+    }
+  }
+  if constexpr (LNF) {
+    if (warp >= 2) {  // ---- LayerNorm of my 32 x BN slice (thread = row quarter) ----
+      const int t = threadIdx.x - 64;
+      const int rows_per = (BM + S - 1) / S;
+      const int r_lo = rank * rows_per;
+      const int rows = max(0, min(BM, r_lo + rows_per) - r_lo);
+      asm volatile("bar.sync 1, 128;" ::: "memory");  // the slice is complete in smem
+      constexpr int QW = BN / 4;                      // columns per thread
+      const int lrl = t >> 2, qd = t & 3;
+      const int lr = r_lo + lrl, row = m0 + lr;
+      const bool rv = lrl < rows && row < M;
+      const float* prow = part + lr * PLD + qd * QW;
+      double sm = 0.0;
+      if (rv)
+        for (int j = 0; j < QW; ++j) sm += (double)prow[j];
+      sm += __shfl_xor_sync(0xffffffffu, sm, 1);
+      sm += __shfl_xor_sync(0xffffffffu, sm, 2);
+      const double tmean = sm / BN;
+      double m2 = 0.0;
+      if (rv)
+        for (int j = 0; j < QW; ++j) {
+          const double dd = (double)prow[j] - tmean;
+          m2 += dd * dd;
+        }
+      m2 += __shfl_xor_sync(0xffffffffu, m2, 1);
+      m2 += __shfl_xor_sync(0xffffffffu, m2, 2);
+      const int tn = n0 / BN, mtile = m0 / BM;
+      if (rv && qd == 0) {
+        __stcg(reinterpret_cast<double2*>(ln.stats + (int64_t)row * ln.nt + tn), make_double2(sm, m2));
+        __threadfence();
+      }
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      const int target = ln.nt * S;  // every CTA of the row block
+      if (t == 0) {
+        __threadfence();
+        atomicAdd(ln.ctr + 2 * mtile, 1);
+        int seen;
+        do {
+          asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(seen) : "l"(ln.ctr + 2 * mtile) : "memory");
+          if (seen < target) __nanosleep(64);
+        } while (seen < target);
+      }
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      if (rv) {
+        double tot = 0.0;
+        for (int tt = 0; tt < ln.nt; ++tt) tot += __ldcg(ln.stats + (int64_t)row * ln.nt + tt).x;
+        const double mean = tot / N;
+        double M2 = 0.0;
+        for (int tt = 0; tt < ln.nt; ++tt) {
+          const double2 st = __ldcg(ln.stats + (int64_t)row * ln.nt + tt);
+          const double dm = st.x / BN - mean;
+          M2 += st.y + (double)BN * dm * dm;
+        }
+        const double inv = 1.0 / sqrt(M2 / N + ln.eps);
+        const int c0 = n0 + qd * QW;
+        for (int j = 0; j < QW; j += 4) {
+          const float4 g = __ldg(reinterpret_cast<const float4*>(ln.gamma + c0 + j));
+          const float4 bb = __ldg(reinterpret_cast<const float4*>(ln.beta + c0 + j));
+          float4 o;  // kernels.py:35: fp32((x - mean) * inv) * gamma + beta, two roundings
+          o.x = fadd_rn(fmul_rn((float)(((double)prow[j] - mean) * inv), g.x), bb.x);
+          o.y = fadd_rn(fmul_rn((float)(((double)prow[j + 1] - mean) * inv), g.y), bb.y);
+          o.z = fadd_rn(fmul_rn((float)(((double)prow[j + 2] - mean) * inv), g.z), bb.z);
+          o.w = fadd_rn(fmul_rn((float)(((double)prow[j + 3] - mean) * inv), g.w), bb.w);
+          if (ln.out) *reinterpret_cast<float4*>(ln.out + (int64_t)row * ln.ldo + c0 + j) = o;
+          if (ln.out16) {
+            __nv_bfloat162 lo = __floats2bfloat162_rn(o.x, o.y), hi = __floats2bfloat162_rn(o.z, o.w);
+            uint2 pk;
+            pk.x = *reinterpret_cast<uint32_t*>(&lo);
+            pk.y = *reinterpret_cast<uint32_t*>(&hi);
+            *reinterpret_cast<uint2*>(ln.out16 + (int64_t)row * ln.ldo16 + c0 + j) = pk;
+          }
+        }
+      }
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      if (t == 0) {  // the last CTA to finish reading resets the row block's counters
+        __threadfence();
+        if (atomicAdd(ln.ctr + 2 * mtile + 1, 1) == target - 1) {
+          ln.ctr[2 * mtile] = 0;
+          ln.ctr[2 * mtile + 1] = 0;
         }
       }
     }
@@ -913,9 +1018,10 @@ static int launch(const void* a, int64_t lda, const void* b, int64_t ldb, const 
   return launch_status("fq_gemm(tcgen05)");
 }
 
-template <int BN, int STAGES>
+template <int BN, int STAGES, bool LNF = false>
 static int launch_splitk(const void* a, int64_t lda, const void* b, int64_t ldb, const Epi& ep,
-                         int64_t M, int64_t N, int64_t K, int S, cudaStream_t s) {
+                         int64_t M, int64_t N, int64_t K, int S, cudaStream_t s,
+                         const LnEpi& ln = LnEpi{}) {
   CUtensorMap ma, mb;
   int rc;
   if ((rc = make_map(&ma, a, M, K, lda, BM)) != FQ_OK) return rc;
@@ -923,9 +1029,10 @@ static int launch_splitk(const void* a, int64_t lda, const void* b, int64_t ldb,
   const int64_t tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
   const int nkb = (int)((K + BK - 1) / BK);
   const int kbs = (nkb + S - 1) / S;
-  cudaError_t e = launch_kernel(tc_gemm_splitk_kernel<BN, STAGES>, dim3((unsigned)(tiles * S)),
-                                dim3(kThreads), smem_bytes_splitk<BN, STAGES>(), s, (unsigned)S,
-                                ma, mb, ep, (int)M, (int)N, (int)K, kbs);
+  cudaError_t e = launch_kernel(tc_gemm_splitk_kernel<BN, STAGES, LNF>,
+                                dim3((unsigned)(tiles * S)), dim3(kThreads),
+                                smem_bytes_splitk<BN, STAGES>(), s, (unsigned)S, ma, mb, ep,
+                                (int)M, (int)N, (int)K, kbs, ln);
   if (e != cudaSuccess) {
     set_error("fq_gemm(tcgen05 split-K): launch failed: %s", cudaGetErrorString(e));
     return FQ_ERR_CUDA;
@@ -933,9 +1040,9 @@ static int launch_splitk(const void* a, int64_t lda, const void* b, int64_t ldb,
   return launch_status("fq_gemm(tcgen05 split-K)");
 }
 
-template <int BN, int STAGES>
+template <int BN, int STAGES, bool LNF = false>
 static int prep_splitk() {
-  return cudaFuncSetAttribute(tc_gemm_splitk_kernel<BN, STAGES>,
+  return cudaFuncSetAttribute(tc_gemm_splitk_kernel<BN, STAGES, LNF>,
                               cudaFuncAttributeMaxDynamicSharedMemorySize,
                               smem_bytes_splitk<BN, STAGES>()) == cudaSuccess
              ? FQ_OK
@@ -957,7 +1064,8 @@ int gemm_tc_prepare() {
   if (tc::prep<256, 4>() || tc::prep<224, 4>() || tc::prep<192, 4>() || tc::prep<128, 6>() ||
       tc::prep<224, 4, true>() ||
       tc::prep<64, 8>() || tc::prep<32, 8>() ||
-      tc::prep_splitk<256, 4>() || tc::prep_splitk<128, 6>() || tc::prep_splitk<64, 8>()) {
+      tc::prep_splitk<256, 4>() || tc::prep_splitk<128, 6>() || tc::prep_splitk<64, 8>() ||
+      tc::prep_splitk<128, 6, true>()) {
     set_error("fq_prepare: tcgen05 GEMM smem opt-in failed");
     return FQ_ERR_CUDA;
   }
@@ -1055,6 +1163,64 @@ extern "C" int fq_logits_hars(const void* x16, int64_t ldx, const void* emb16, i
                  (int)ldt};
   return tc::launch<224, 4, true>(x16, ldx, emb16, lde, ep, rows, vocab, d, 1, 1,
                                   as_stream(stream), he);
+}
+
+// bf16 GEMM + bias + residual + LayerNorm (the decode step's self-out/LN1,
+// cross-out/LN2, FFN2/LN3): the split-K x4 kernel with the LN epilogue when
+// the plan is split-K over 128-column tiles and every cluster of the launch can
+// be resident at once (the row-block statistics exchange waits for all CTAs of
+// the row block), else the GEMM then fq_layer_norm. ws: stats [M][N/128]
+// double2 then counters [ceil(M/128)][2] int32, zeroed once by the caller.
+extern "C" int fq_gemm_ln(const void* a, int64_t lda, const void* w, int64_t ldw,
+                          const float* bias, const float* res, int64_t ldr, const float* gamma,
+                          const float* beta, double eps, float* out, int64_t ldo, void* out16,
+                          int64_t ldo16, void* ws, int64_t ws_bytes, int64_t M, int64_t N,
+                          int64_t K, fq_stream_t stream) {
+  FQ_CHECK_ARG(a && w && gamma && beta && out && M > 0 && N > 0 && K > 0, FQ_ERR_DIMENSION,
+               "fq_gemm_ln: bad args");
+  const TcPlan p = plan_tc(M, N, K);
+  const int64_t mt = (M + 127) / 128, nt = N / 128;
+  const int64_t need = M * nt * (int64_t)sizeof(double2) + mt * 2 * (int64_t)sizeof(int);
+  bool fused = p.split == 4 && p.bn == 128 && p.cm == 1 && p.cn == 1 && N % 128 == 0 &&
+               ws && ws_bytes >= need && ((uintptr_t)ws & 15) == 0 && ldo % 4 == 0 &&
+               (!out16 || ldo16 % 4 == 0) && (!res || ldr % 4 == 0) &&
+               ((uintptr_t)gamma & 15) == 0 && ((uintptr_t)beta & 15) == 0;
+  if (fused) {  // every cluster resident at once?
+    static int max_clusters = -1;
+    if (max_clusters < 0) {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(4);
+      cfg.blockDim = dim3(tc::kThreads);
+      cfg.dynamicSmemBytes = tc::smem_bytes_splitk<128, 6>();
+      cudaLaunchAttribute at;
+      at.id = cudaLaunchAttributeClusterDimension;
+      at.val.clusterDim.x = 4;
+      at.val.clusterDim.y = 1;
+      at.val.clusterDim.z = 1;
+      cfg.attrs = &at;
+      cfg.numAttrs = 1;
+      int n = 0;
+      if (cudaOccupancyMaxActiveClusters(&n, tc::tc_gemm_splitk_kernel<128, 6, true>, &cfg) !=
+          cudaSuccess)
+        n = 0;
+      cudaGetLastError();
+      max_clusters = n;
+    }
+    fused = mt * nt <= max_clusters;
+  }
+  if (fused) {
+    tc::Epi ep{nullptr, 0, 0, 0, bias, res, ldr, 0, g_gemm_dbg};
+    tc::LnEpi ln{gamma, beta, eps, out, ldo, reinterpret_cast<__nv_bfloat16*>(out16), ldo16,
+                 reinterpret_cast<double2*>(ws),
+                 reinterpret_cast<int*>(reinterpret_cast<char*>(ws) + M * nt * sizeof(double2)),
+                 (int)nt};
+    return tc::launch_splitk<128, 6, true>(a, lda, w, ldw, ep, M, N, K, 4, as_stream(stream),
+                                           ln);
+  }
+  int rc = launch_tc_gemm(a, lda, w, ldw, out, 0, ldo, M, N, K, 0, bias, res, ldr, 0,
+                          as_stream(stream));
+  if (rc != FQ_OK) return rc;
+  return fq_layer_norm(out, ldo, gamma, beta, eps, M, N, out, ldo, out16, ldo16, stream);
 }
 
 // Benchmarks only: force (bn, cm, cn) for shapes it divides; bn = 0 restores auto.

@@ -194,8 +194,10 @@ class Session:
                                                           precision=self.precision)
             gp = packed[i0 * seq:i1 * seq]
             gm = mask[i0:i1] if mask is not None else None
+            # the fused LN's row-block exchange needs every CTA of its launch resident:
+            # one step chain at a time (not with the two-stream overlap)
             step = M.DecoderStep(self.dw, self.config, nb, K, seq, cache, gp, gm, bufs,
-                                 self.counters, self.timers)
+                                 self.counters, self.timers, fuse_ln=ngroups == 1)
             st = D.DeviceBeamState(nb, K, self.config.max_seq_len, bufs)
             st.init()
             step.tokens.fill_(bos_token)

@@ -24,6 +24,7 @@ Every intermediate is a view of the session arena (``plan_intermediates``).
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -382,6 +383,31 @@ def _ln(x, g, b, eps, out, out16, residual=None, bias=None, counters=None):
     (counters or global_counters()).count_fused("layer_norm", x.numel() * 8)
 
 
+def _lin_ln(dw: DeviceWeights, a32, a16, w, bias, residual, g, b, eps, out, out16, ws, *,
+            counters=None, timers=None):
+    """GEMM + bias + residual, then LayerNorm: one fq_gemm_ln launch in bf16 mode
+    with a statistics workspace (the LN inside the split-K epilogue), else the
+    GEMM and the LN kernel."""
+    if dw.bf16 and ws is not None:
+        M, K = a16.shape
+        N = w.shape[0]
+        _abi.call("fq_gemm_ln", a16.data_ptr(), a16.stride(0), w.data_ptr(), w.stride(0),
+                  bias.data_ptr(), residual.data_ptr(), residual.stride(0), g.data_ptr(),
+                  b.data_ptr(), eps, out.data_ptr(), out.stride(0), _abi.ptr(out16),
+                  out16.stride(0) if out16 is not None else 0, ws.data_ptr(),
+                  ws.numel() * ws.element_size(), M, N, K, _abi.stream_handle())
+        (counters or global_counters()).count_fused("layer_norm", M * N * 8)
+        return
+    tmp = out
+    _lin(dw, a32, a16, w, tmp, bias=bias, residual=residual, counters=counters, timers=timers)
+    _ln(tmp, g, b, eps, out, out16, counters=counters)
+
+
+def ln_ws_bytes(rows: int, d: int) -> int:
+    """fq_gemm_ln workspace: per-row, per-128-column-tile statistics + counters."""
+    return rows * ((d + 127) // 128) * 16 + ((rows + 127) // 128) * 8
+
+
 def _check_tokens(tokens: np.ndarray, config: ModelConfig):
     if tokens.size and (tokens.min() < 0 or tokens.max() >= config.vocab_size):
         raise InputError(f"token id out of range [0, {config.vocab_size})")
@@ -601,7 +627,7 @@ class DecoderStep:
 
     def __init__(self, dw: DeviceWeights, config: ModelConfig, batch: int, beam: int,
                  enc_seq: int, cache: KVCache, cross_packed: torch.Tensor, enc_mask, buffers,
-                 counters=None, timers=None):
+                 counters=None, timers=None, fuse_ln: bool = True):
         self.dw, self.config = dw, config
         self.batch, self.beam, self.rows, self.enc_seq = batch, beam, batch * beam, enc_seq
         self.cache, self.cross, self.mask = cache, cross_packed, enc_mask
@@ -626,6 +652,14 @@ class DecoderStep:
         self.u = b.get("dec.ffn_out", (R, d))
         self.logits = b.get("dec.logits", (R, V))
         self.bad = b.get("dec.bad", (1,), torch.int32)
+        # FQ_FUSE_LN=1 (opt-in): GEMM + LN pairs as fq_gemm_ln (the LN inside the
+        # split-K epilogue). Measured slower at C2 (152k vs 165k tok/s): the row
+        # block's statistics exchange waits for its slowest CTA and costs more
+        # round trips than the LN launch it replaces
+        self.ln_ws = None
+        if dw.bf16 and fuse_ln and os.environ.get("FQ_FUSE_LN", "0") == "1":
+            self.ln_ws = b.get("dec.ln_ws", ((ln_ws_bytes(R, d) + 3) // 4,), torch.int32)
+            self.ln_ws.zero_()
 
     def embed(self):
         """Decoder input of the current position (model.py:559)."""
@@ -659,10 +693,15 @@ class DecoderStep:
                       c.max_seq_len, scale, None if dw.bf16 else self.sctx.data_ptr(),
                       self.sctx.data_ptr() if dw.bf16 else None, d, exact, stream)
             ctr.count_fused("decoder_self_attention", R * d * 16)
-            _lin(dw, self.sctx, self.sctx, lw["w_so"], self.sres, bias=lw["b_so"], residual=x,
-                 counters=ctr, timers=tm)
-            _ln(self.sres, lw["ln1_g"], lw["ln1_b"], c.ln_eps, self.snorm, self.snorm16,
-                counters=ctr)
+            if self.ln_ws is not None:
+                _lin_ln(dw, self.sctx, self.sctx, lw["w_so"], lw["b_so"], x, lw["ln1_g"],
+                        lw["ln1_b"], c.ln_eps, self.snorm, self.snorm16, self.ln_ws,
+                        counters=ctr, timers=tm)
+            else:
+                _lin(dw, self.sctx, self.sctx, lw["w_so"], self.sres, bias=lw["b_so"],
+                     residual=x, counters=ctr, timers=tm)
+                _ln(self.sres, lw["ln1_g"], lw["ln1_b"], c.ln_eps, self.snorm, self.snorm16,
+                    counters=ctr)
             _lin(dw, self.snorm, self.snorm16, lw["w_cq"], self.cq, bias=lw["b_cq"],
                  counters=ctr, timers=tm)
             ld = self.cross.stride(0)
@@ -674,15 +713,25 @@ class DecoderStep:
                       self.cctx.data_ptr() if dw.bf16 else None, d, exact,
                       self.bad.data_ptr(), stream)
             ctr.count_fused("cross_attention", R * d * 16)
-            _lin(dw, self.cctx, self.cctx, lw["w_co"], self.cres, bias=lw["b_co"],
-                 residual=self.snorm, counters=ctr, timers=tm)
-            _ln(self.cres, lw["ln2_g"], lw["ln2_b"], c.ln_eps, self.cnorm, self.cnorm16,
-                counters=ctr)
+            if self.ln_ws is not None:
+                _lin_ln(dw, self.cctx, self.cctx, lw["w_co"], lw["b_co"], self.snorm,
+                        lw["ln2_g"], lw["ln2_b"], c.ln_eps, self.cnorm, self.cnorm16,
+                        self.ln_ws, counters=ctr, timers=tm)
+            else:
+                _lin(dw, self.cctx, self.cctx, lw["w_co"], self.cres, bias=lw["b_co"],
+                     residual=self.snorm, counters=ctr, timers=tm)
+                _ln(self.cres, lw["ln2_g"], lw["ln2_b"], c.ln_eps, self.cnorm, self.cnorm16,
+                    counters=ctr)
             _lin(dw, self.cnorm, self.cnorm16, lw["w_ff1"], self.ffn_h, bias=lw["b_ff1"],
                  act=c.activation, counters=ctr, timers=tm)
-            _lin(dw, self.ffn_h, self.ffn_h, lw["w_ff2"], self.u, bias=lw["b_ff2"],
-                 residual=self.cnorm, counters=ctr, timers=tm)
-            _ln(self.u, lw["ln3_g"], lw["ln3_b"], c.ln_eps, self.x, self.x16, counters=ctr)
+            if self.ln_ws is not None:
+                _lin_ln(dw, self.ffn_h, self.ffn_h, lw["w_ff2"], lw["b_ff2"], self.cnorm,
+                        lw["ln3_g"], lw["ln3_b"], c.ln_eps, self.x, self.x16, self.ln_ws,
+                        counters=ctr, timers=tm)
+            else:
+                _lin(dw, self.ffn_h, self.ffn_h, lw["w_ff2"], self.u, bias=lw["b_ff2"],
+                     residual=self.cnorm, counters=ctr, timers=tm)
+                _ln(self.u, lw["ln3_g"], lw["ln3_b"], c.ln_eps, self.x, self.x16, counters=ctr)
             x, x16 = self.x, self.x16
         if not logits:
             return None
@@ -787,6 +836,7 @@ def plan_intermediates(config: ModelConfig, precision: str = "fp32") -> list[Int
                        ("ffn_out", R * d * 4)):
             add(f"dec.{nm}", sz, dec0, end - 3)
         if bf:
+            add("dec.ln_ws", ln_ws_bytes(R, d), dec0, end - 3)
             add("dec.snorm16", R * d * 2, dec0, end - 3)
             add("dec.cnorm16", R * d * 2, dec0, end - 3)
         add("dec.logits", R * V * 4, end - 3, end)
