@@ -249,7 +249,7 @@ __device__ __forceinline__ float ex2_ftz(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
-constexpr int kSwU = 4;   // pilot vectors per thread
+constexpr int kSwU = 8;   // pilot vectors per thread
 constexpr int kSwP = 8;   // async ring depth (vectors in flight per thread)
 // CTAs (cluster) per row. 2 balances rows over SMs but needs 7 resident CTAs
 // per SM for one wave, which the ring + survivor smem does not allow: measured
