@@ -235,6 +235,8 @@ def probe_step_gemms(sess, src_dev, dc):
             continue
         if name == "fq_logits_hars":  # (x16, ldx, emb16, lde, rows, vocab, d, ...)
             M, N, K = int(a[4]), int(a[5]), int(a[6])
+        elif name == "fq_gemm_ln":  # (..., ws, ws_bytes, M, N, K, stream)
+            M, N, K = int(a[16]), int(a[17]), int(a[18])
         else:
             M, N, K = int(a[10]), int(a[11]), int(a[12])
         rows.append((M, N, K, e0.elapsed_time(e1) / 1e3))
@@ -360,7 +362,9 @@ def run_ours(args, rank, world):
             "kernel": "tc_gemm (tcgen05/TMEM/TMA bf16 GEMM with fused epilogue): every GEMM "
                       "launch of one decode step (QKV, self-out, cross-q, cross-out, FFN1, FFN2 "
                       "x 6 layers + the logits GEMM, whose epilogue computes HARS stage 1), "
-                      "timed with events inside the step graph",
+                      "timed with events inside the step graph; self-out, cross-out and FFN2 "
+                      "run as fq_gemm_ln (split-K GEMM writing K-slice slabs + the LN kernel "
+                      "that reduces them), timed with their LN",
             "bound": "tensor", "achieved": g_flops / g_time / 1e12, "peak": tc_peak,
             "unit": "TFLOP/s", "frac": g_flops / g_time / 1e12 / tc_peak, "traffic": traffic,
             "launches_per_step": len(gemms), "flops_per_launch_mean": g_flops / max(len(gemms), 1),

@@ -67,6 +67,17 @@ int fq_bias_residual_layer_norm(const float* x, int64_t ldx, const float* bias,
                                 float* out, int64_t ldo, void* out16, int64_t ldo16,
                                 fq_stream_t stream);
 
+/* The split-K consumer of fq_gemm_ln's slab path: LN((sum_s slabs[s] +
+ * bias) + residual), slabs [nslab][rows][ld] fp32 (slab s = the GEMM's K
+ * slice s), summed in slab order — bit-identical to the split-K GEMM's
+ * in-kernel reduction followed by fq_layer_norm. nslab in {2, 4}, d in
+ * {512, 1024, 2048}, 16-byte aligned rows. */
+int fq_splitk_bias_residual_layer_norm(const float* slabs, int nslab, int64_t ld,
+                                       const float* bias, const float* residual, int64_t ldr,
+                                       const float* gamma, const float* beta, double eps,
+                                       int64_t rows, int64_t d, float* out, int64_t ldo,
+                                       void* out16, int64_t ldo16, fq_stream_t stream);
+
 /* kernels.py:39 bias_residual_act_kernel: act(x + bias) (+ residual). In place
  * allowed (out == x). act: enum fq_act. residual may be NULL. */
 int fq_bias_residual_act(const float* x, int64_t ldx, const float* bias,
@@ -123,11 +134,16 @@ int fq_kv_gather_append(const float* src_k, const float* src_v, const float* new
 
 /* out = LN(a . w^T + bias + residual) (bf16 operands, fp32 out, optional bf16
  * copy): model.py:596-627's GEMM + fused_bias_residual_layer_norm pairs
- * (kernels.py:57-73) in one launch when the GEMM runs split-K over 128-column
- * tiles and all its clusters fit on the GPU at once (the LN statistics of a
- * row block are exchanged between its CTAs through ws); otherwise the GEMM then
- * fq_layer_norm. ws: M * (N/128) * 16 + ceil(M/128) * 8 bytes, zeroed once
- * (the counters reset themselves); one launch per stream at a time. */
+ * (kernels.py:57-73). When the GEMM runs split-K over 128-column tiles:
+ * - ws >= split * M * N * 4 bytes (slab path, the engine default): the split-K
+ *   GEMM writes one fp32 partial slab per K slice into ws with no in-kernel
+ *   reduction, then fq_splitk_bias_residual_layer_norm sums them (same order,
+ *   same bits as the reduced GEMM + LN);
+ * - else ws >= M * (N/128) * 16 + ceil(M/128) * 8 bytes, zeroed once, and all
+ *   clusters fit on the GPU at once: one launch, the LN statistics of a row
+ *   block exchanged between its CTAs through ws (the counters reset
+ *   themselves).
+ * Otherwise the GEMM then fq_layer_norm. One launch per stream at a time. */
 int fq_gemm_ln(const void* a, int64_t lda, const void* w, int64_t ldw, const float* bias,
                const float* res, int64_t ldr, const float* gamma, const float* beta, double eps,
                float* out, int64_t ldo, void* out16, int64_t ldo16, void* ws, int64_t ws_bytes,

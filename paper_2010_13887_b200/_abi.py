@@ -38,6 +38,8 @@ SIGNATURES = {
     "fq_layer_norm": ([P, I64, P, P, F64, I64, I64, P, I64, P, I64, P], I32),
     "fq_bias_residual_layer_norm": ([P, I64, P, P, I64, P, P, F64, I64, I64, P, I64, P, I64, P],
                                     I32),
+    "fq_splitk_bias_residual_layer_norm": ([P, I32, I64, P, P, I64, P, P, F64, I64, I64, P,
+                                            I64, P, I64, P], I32),
     "fq_bias_residual_act": ([P, I64, P, P, I64, I32, I64, I64, P, I64, P], I32),
     "fq_qkv_bias_reshape": ([P, I64, P, I64, I64, I64, I64, P, P, P, P], I32),
     "fq_bias_reshape_heads": ([P, I64, P, I64, I64, I64, I64, P, P], I32),
@@ -118,7 +120,7 @@ def load():
 # become event-record nodes inside a captured CUDA graph) and
 # (name, args, start, end) is appended. Off (None) on the product path.
 PROBE = None
-PROBE_NAMES = ("fq_gemm", "fq_logits_hars")
+PROBE_NAMES = ("fq_gemm", "fq_logits_hars", "fq_gemm_ln")
 
 
 def call(name: str, *args) -> int:

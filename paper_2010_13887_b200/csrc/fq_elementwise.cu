@@ -179,6 +179,84 @@ __global__ void __launch_bounds__(128) layer_norm_row128_kernel(
   }
 }
 
+// Split-K consumer: x = the S fp32 partial slabs of a split-K GEMM ([S][rows][ld],
+// slab s = K slice s), summed in split order, + bias, + residual, then the LN
+// of layer_norm_row128_kernel — the same additions in the same order as the
+// split-K kernel's DSMEM epilogue followed by fq_layer_norm.
+template <int V, int NS>
+__global__ void __launch_bounds__(128) layer_norm_slabs_row128_kernel(
+    const float* __restrict__ x, int64_t ld, int64_t slab, const float* __restrict__ bias,
+    const float* __restrict__ res, int64_t ldr, const float* __restrict__ gamma,
+    const float* __restrict__ beta, double eps, int d, float* __restrict__ out, int64_t ldo,
+    __nv_bfloat16* __restrict__ out16, int64_t ldo16) {
+  pdl_enter();
+  __shared__ double red[2][4];
+  const int64_t row = blockIdx.x;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  float4 u[V];
+  double s = 0.0;
+  float4 p[V][NS];
+#pragma unroll
+  for (int i = 0; i < V; ++i) {
+    const int c = (i * 128 + threadIdx.x) * 4;
+#pragma unroll
+    for (int k = 0; k < NS; ++k) p[i][k] = __ldcg(reinterpret_cast<const float4*>(x + k * slab + row * ld + c));
+  }
+#pragma unroll
+  for (int i = 0; i < V; ++i) {
+    const int c = (i * 128 + threadIdx.x) * 4;
+    float4 a = p[i][0];
+#pragma unroll
+    for (int k = 1; k < NS; ++k) {
+      a.x = fadd_rn(a.x, p[i][k].x);
+      a.y = fadd_rn(a.y, p[i][k].y);
+      a.z = fadd_rn(a.z, p[i][k].z);
+      a.w = fadd_rn(a.w, p[i][k].w);
+    }
+    const float4 b = *reinterpret_cast<const float4*>(bias + c);
+    const float4 r = *reinterpret_cast<const float4*>(res + row * ldr + c);
+    a.x = fadd_rn(fadd_rn(a.x, b.x), r.x);
+    a.y = fadd_rn(fadd_rn(a.y, b.y), r.y);
+    a.z = fadd_rn(fadd_rn(a.z, b.z), r.z);
+    a.w = fadd_rn(fadd_rn(a.w, b.w), r.w);
+    u[i] = a;
+    s += ((double)a.x + (double)a.y) + ((double)a.z + (double)a.w);
+  }
+  s = warp_sum(s);
+  if (lane == 0) red[0][w] = s;
+  __syncthreads();
+  const double mean = ((red[0][0] + red[0][1]) + (red[0][2] + red[0][3])) / d;
+  double v = 0.0;
+#pragma unroll
+  for (int i = 0; i < V; ++i) {
+    double t0 = u[i].x - mean, t1 = u[i].y - mean, t2 = u[i].z - mean, t3 = u[i].w - mean;
+    v += (t0 * t0 + t1 * t1) + (t2 * t2 + t3 * t3);
+  }
+  v = warp_sum(v);
+  if (lane == 0) red[1][w] = v;
+  __syncthreads();
+  const double inv = 1.0 / sqrt(((red[1][0] + red[1][1]) + (red[1][2] + red[1][3])) / d + eps);
+#pragma unroll
+  for (int i = 0; i < V; ++i) {
+    const int c = (i * 128 + threadIdx.x) * 4;
+    const float4 g = *reinterpret_cast<const float4*>(gamma + c);
+    const float4 bb = *reinterpret_cast<const float4*>(beta + c);
+    float4 o;
+    o.x = fadd_rn(fmul_rn((float)((u[i].x - mean) * inv), g.x), bb.x);  // kernels.py:35
+    o.y = fadd_rn(fmul_rn((float)((u[i].y - mean) * inv), g.y), bb.y);
+    o.z = fadd_rn(fmul_rn((float)((u[i].z - mean) * inv), g.z), bb.z);
+    o.w = fadd_rn(fmul_rn((float)((u[i].w - mean) * inv), g.w), bb.w);
+    if (out) *reinterpret_cast<float4*>(out + row * ldo + c) = o;
+    if (out16) {
+      __nv_bfloat162 lo = __floats2bfloat162_rn(o.x, o.y), hi = __floats2bfloat162_rn(o.z, o.w);
+      uint2 pk;
+      pk.x = *reinterpret_cast<uint32_t*>(&lo);
+      pk.y = *reinterpret_cast<uint32_t*>(&hi);
+      *reinterpret_cast<uint2*>(out16 + row * ldo16 + c) = pk;
+    }
+  }
+}
+
 static inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
 template <bool kBiasRes>
@@ -388,6 +466,39 @@ int fq_bias_residual_layer_norm(const float* x, int64_t ldx, const float* bias,
   launch_ln<true>(x, ldx, bias, residual, ldr, gamma, beta, eps, rows, d, out, ldo,
                   reinterpret_cast<__nv_bfloat16*>(out16), ldo16, as_stream(stream));
   return launch_status("fq_bias_residual_layer_norm");
+}
+
+int fq_splitk_bias_residual_layer_norm(const float* slabs, int nslab, int64_t ld,
+                                       const float* bias, const float* residual, int64_t ldr,
+                                       const float* gamma, const float* beta, double eps,
+                                       int64_t rows, int64_t d, float* out, int64_t ldo,
+                                       void* out16, int64_t ldo16, fq_stream_t stream) {
+  FQ_CHECK_ARG(slabs && bias && residual && gamma && beta && rows >= 0 && (out || out16) &&
+                   (nslab == 2 || nslab == 4) && (d == 512 || d == 1024 || d == 2048) &&
+                   ld >= d && ld % 4 == 0 && ldr % 4 == 0 && aligned16(slabs) &&
+                   aligned16(bias) && aligned16(residual) && aligned16(gamma) &&
+                   aligned16(beta) && (!out || (ldo % 4 == 0 && aligned16(out))) &&
+                   (!out16 || (ldo16 % 4 == 0 && (reinterpret_cast<uintptr_t>(out16) & 7) == 0)),
+               FQ_ERR_DIMENSION, "fq_splitk_bias_residual_layer_norm: bad args");
+  FQ_CHECK_ARG(eps >= 0, FQ_ERR_DIMENSION, "eps must be non-negative");
+  if (rows == 0) return FQ_OK;
+  auto* o16 = reinterpret_cast<__nv_bfloat16*>(out16);
+  const int64_t slab = rows * ld;
+  cudaStream_t s = as_stream(stream);
+#define FQ_LNS(V, NS)                                                                         \
+  launch_kernel(layer_norm_slabs_row128_kernel<V, NS>, (unsigned)rows, 128, 0, s, 1u, slabs, ld, \
+                slab, bias, residual, ldr, gamma, beta, eps, (int)d, out, ldo, o16, ldo16)
+  if (nslab == 4) {
+    if (d == 512) FQ_LNS(1, 4);
+    else if (d == 1024) FQ_LNS(2, 4);
+    else FQ_LNS(4, 4);
+  } else {
+    if (d == 512) FQ_LNS(1, 2);
+    else if (d == 1024) FQ_LNS(2, 2);
+    else FQ_LNS(4, 2);
+  }
+#undef FQ_LNS
+  return launch_status("fq_splitk_bias_residual_layer_norm");
 }
 
 int fq_bias_residual_act(const float* x, int64_t ldx, const float* bias, const float* residual,

@@ -613,11 +613,15 @@ __device__ __forceinline__ float4 ld_dsmem_f4(uint32_t local_addr, uint32_t rank
   return v;
 }
 
-template <int BN, int STAGES, bool LNF = false>
+// SLAB: no cluster and no in-kernel reduction — split s writes its fp32
+// partial tile to slab s of ep.c ([S][M][ldc], plain coalesced stores) and the
+// consumer (fq_splitk_bias_residual_layer_norm) sums the S slabs in split
+// order, so the result is bit-identical to the DSMEM reduction's.
+template <int BN, int STAGES, bool LNF = false, bool SLAB = false>
 __global__ void __launch_bounds__(kThreads, 1)
     tc_gemm_splitk_kernel(const __grid_constant__ CUtensorMap tma_a,
                           const __grid_constant__ CUtensorMap tma_b, const Epi ep, int M, int N,
-                          int K, int kb_per_split, const LnEpi ln) {
+                          int K, int kb_per_split, const LnEpi ln, int nsplit) {
   constexpr int A_BYTES = BM * BK * 2;
   constexpr int B_BYTES = BN * BK * 2;
   constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
@@ -635,7 +639,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   pdl_launch_dependents();
   if (threadIdx.x == 0) dbg_stamp(ep.dbg, 0);
-  const int S = (int)cluster_nrank(), rank = (int)cluster_rank();
+  const int S = SLAB ? nsplit : (int)cluster_nrank();
+  const int rank = SLAB ? (int)(blockIdx.x % nsplit) : (int)cluster_rank();
   const int mt = (M + BM - 1) / BM;
   const int tile = blockIdx.x / S;
   const int m0 = (tile % mt) * BM, n0 = (tile / mt) * BN;
@@ -718,6 +723,33 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int j = 0; j < 32; j += 4)
         *reinterpret_cast<float4*>(prow + cc + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
     }
+    if constexpr (SLAB) {  // my 32 rows, one row (BN * 4 contiguous bytes) per warp pass
+      __syncwarp();
+      float* slab = reinterpret_cast<float*>(ep.c) + (int64_t)rank * M * ep.ldc;
+#pragma unroll 4
+      for (int r = 0; r < 32; ++r) {
+        const int lr = q * 32 + r, row = m0 + lr;
+        if (row >= M) break;
+#pragma unroll
+        for (int c4 = lane; c4 < BN / 4; c4 += 32) {
+          const int col = n0 + c4 * 4;
+          if (col < N)
+            *reinterpret_cast<float4*>(slab + (int64_t)row * ep.ldc + col) =
+                *reinterpret_cast<const float4*>(part + lr * PLD + c4 * 4);
+        }
+      }
+    }
+  }
+  if constexpr (SLAB) {
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (threadIdx.x == 0) dbg_stamp(ep.dbg, 6);
+    if (warp == 1) {
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                   "r"(TMEM_COLS));
+    }
+    return;
   }
   __syncwarp();
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -1018,7 +1050,7 @@ static int launch(const void* a, int64_t lda, const void* b, int64_t ldb, const 
   return launch_status("fq_gemm(tcgen05)");
 }
 
-template <int BN, int STAGES, bool LNF = false>
+template <int BN, int STAGES, bool LNF = false, bool SLAB = false>
 static int launch_splitk(const void* a, int64_t lda, const void* b, int64_t ldb, const Epi& ep,
                          int64_t M, int64_t N, int64_t K, int S, cudaStream_t s,
                          const LnEpi& ln = LnEpi{}) {
@@ -1029,10 +1061,10 @@ static int launch_splitk(const void* a, int64_t lda, const void* b, int64_t ldb,
   const int64_t tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
   const int nkb = (int)((K + BK - 1) / BK);
   const int kbs = (nkb + S - 1) / S;
-  cudaError_t e = launch_kernel(tc_gemm_splitk_kernel<BN, STAGES, LNF>,
+  cudaError_t e = launch_kernel(tc_gemm_splitk_kernel<BN, STAGES, LNF, SLAB>,
                                 dim3((unsigned)(tiles * S)), dim3(kThreads),
-                                smem_bytes_splitk<BN, STAGES>(), s, (unsigned)S, ma, mb, ep,
-                                (int)M, (int)N, (int)K, kbs, ln);
+                                smem_bytes_splitk<BN, STAGES>(), s, SLAB ? 1u : (unsigned)S, ma,
+                                mb, ep, (int)M, (int)N, (int)K, kbs, ln, S);
   if (e != cudaSuccess) {
     set_error("fq_gemm(tcgen05 split-K): launch failed: %s", cudaGetErrorString(e));
     return FQ_ERR_CUDA;
@@ -1040,9 +1072,9 @@ static int launch_splitk(const void* a, int64_t lda, const void* b, int64_t ldb,
   return launch_status("fq_gemm(tcgen05 split-K)");
 }
 
-template <int BN, int STAGES, bool LNF = false>
+template <int BN, int STAGES, bool LNF = false, bool SLAB = false>
 static int prep_splitk() {
-  return cudaFuncSetAttribute(tc_gemm_splitk_kernel<BN, STAGES, LNF>,
+  return cudaFuncSetAttribute(tc_gemm_splitk_kernel<BN, STAGES, LNF, SLAB>,
                               cudaFuncAttributeMaxDynamicSharedMemorySize,
                               smem_bytes_splitk<BN, STAGES>()) == cudaSuccess
              ? FQ_OK
@@ -1065,7 +1097,7 @@ int gemm_tc_prepare() {
       tc::prep<224, 4, true>() ||
       tc::prep<64, 8>() || tc::prep<32, 8>() ||
       tc::prep_splitk<256, 4>() || tc::prep_splitk<128, 6>() || tc::prep_splitk<64, 8>() ||
-      tc::prep_splitk<128, 6, true>()) {
+      tc::prep_splitk<128, 6, true>() || tc::prep_splitk<128, 6, false, true>()) {
     set_error("fq_prepare: tcgen05 GEMM smem opt-in failed");
     return FQ_ERR_CUDA;
   }
@@ -1179,6 +1211,18 @@ extern "C" int fq_gemm_ln(const void* a, int64_t lda, const void* w, int64_t ldw
   FQ_CHECK_ARG(a && w && gamma && beta && out && M > 0 && N > 0 && K > 0, FQ_ERR_DIMENSION,
                "fq_gemm_ln: bad args");
   const TcPlan p = plan_tc(M, N, K);
+  const int64_t slab_need = (int64_t)p.split * M * N * (int64_t)sizeof(float);
+  if (p.split > 1 && p.bn == 128 && p.cm == 1 && p.cn == 1 && bias && res && ws &&
+      ws_bytes >= slab_need && ((uintptr_t)ws & 15) == 0 && N % 4 == 0 &&
+      (p.split == 2 || p.split == 4) && (N == 512 || N == 1024 || N == 2048)) {
+    tc::Epi ep{ws, N, 0, 0, nullptr, nullptr, 0, 0, g_gemm_dbg};
+    int rc = tc::launch_splitk<128, 6, false, true>(a, lda, w, ldw, ep, M, N, K, p.split,
+                                                    as_stream(stream));
+    if (rc != FQ_OK) return rc;
+    return fq_splitk_bias_residual_layer_norm(reinterpret_cast<const float*>(ws), p.split, N,
+                                              bias, res, ldr, gamma, beta, eps, M, N, out, ldo,
+                                              out16, ldo16, stream);
+  }
   const int64_t mt = (M + 127) / 128, nt = N / 128;
   const int64_t need = M * nt * (int64_t)sizeof(double2) + mt * 2 * (int64_t)sizeof(int);
   bool fused = p.split == 4 && p.bn == 128 && p.cm == 1 && p.cn == 1 && N % 128 == 0 &&

@@ -403,9 +403,12 @@ def _lin_ln(dw: DeviceWeights, a32, a16, w, bias, residual, g, b, eps, out, out1
     _ln(tmp, g, b, eps, out, out16, counters=counters)
 
 
-def ln_ws_bytes(rows: int, d: int) -> int:
-    """fq_gemm_ln workspace: per-row, per-128-column-tile statistics + counters."""
-    return rows * ((d + 127) // 128) * 16 + ((rows + 127) // 128) * 8
+def ln_ws_bytes(rows: int, d: int, slabs: bool = True) -> int:
+    """fq_gemm_ln workspace. ``slabs``: room for the split-K partial slabs (at
+    most 4 K slices of [rows, d] fp32; the default path), else the co-resident
+    variant's per-row, per-128-column-tile statistics + counters."""
+    stats = rows * ((d + 127) // 128) * 16 + ((rows + 127) // 128) * 8
+    return max(stats, 4 * rows * d * 4) if slabs else stats
 
 
 def _check_tokens(tokens: np.ndarray, config: ModelConfig):
@@ -652,14 +655,20 @@ class DecoderStep:
         self.u = b.get("dec.ffn_out", (R, d))
         self.logits = b.get("dec.logits", (R, V))
         self.bad = b.get("dec.bad", (1,), torch.int32)
-        # FQ_FUSE_LN=1 (opt-in): GEMM + LN pairs as fq_gemm_ln (the LN inside the
-        # split-K epilogue). Measured slower at C2 (152k vs 165k tok/s): the row
-        # block's statistics exchange waits for its slowest CTA and costs more
-        # round trips than the LN launch it replaces
+        # GEMM + LN pairs as fq_gemm_ln. Default (bf16): the split-K GEMM writes
+        # one partial slab per K slice and the LN kernel reduces them, so the
+        # GEMM has no in-kernel (DSMEM) reduction. FQ_FUSE_LN=coresident: the LN
+        # inside the split-K epilogue, measured slower at C2 (152k vs 165k
+        # tok/s: the row block's statistics exchange waits for its slowest CTA).
+        # FQ_FUSE_LN=0: GEMM with the reduction, then the LN kernel.
         self.ln_ws = None
-        if dw.bf16 and fuse_ln and os.environ.get("FQ_FUSE_LN", "0") == "1":
-            self.ln_ws = b.get("dec.ln_ws", ((ln_ws_bytes(R, d) + 3) // 4,), torch.int32)
-            self.ln_ws.zero_()
+        mode = os.environ.get("FQ_FUSE_LN", "slab")
+        if dw.bf16 and fuse_ln and mode != "0":
+            ws = b.get("dec.ln_ws", ((ln_ws_bytes(R, d) + 3) // 4,), torch.int32)
+            if mode == "coresident":
+                ws = ws[:(ln_ws_bytes(R, d, slabs=False) + 3) // 4]
+                ws.zero_()
+            self.ln_ws = ws
 
     def embed(self):
         """Decoder input of the current position (model.py:559)."""

@@ -163,3 +163,40 @@ def test_gemm_ln_equals_gemm_then_layer_norm(M, N, K):
     # counters back to zero
     nst = M * ((N + 127) // 128) * 4
     assert int(ws[nst:nst + ((M + 127) // 128) * 2].abs().sum()) == 0
+
+
+@pytest.mark.parametrize("M,N,K", [(512, 1024, 1024), (512, 1024, 4096), (300, 1024, 1024),
+                                   (128, 512, 2048), (512, 768, 1024)])
+def test_gemm_ln_slab_path_bit_identical(M, N, K):
+    """fq_gemm_ln with a workspace large enough for the split-K partial slabs:
+    the GEMM writes one fp32 slab per K slice, fq_splitk_bias_residual_layer_norm
+    sums them in split order — bit-identical to fq_gemm (in-kernel DSMEM
+    reduction + bias + residual) followed by fq_layer_norm. N = 768 takes the
+    unfused fallback."""
+    import torch
+    from paper_2010_13887_b200 import _abi
+    import paper_2010_13887_b200 as P
+    g = torch.Generator(device="cuda").manual_seed(7 * M + N + K)
+    a = torch.randn(M, K, device="cuda", generator=g).bfloat16()
+    w = (torch.randn(N, K, device="cuda", generator=g) / K ** 0.5).bfloat16()
+    bias = torch.randn(N, device="cuda", generator=g) * 0.1
+    res = torch.randn(M, N, device="cuda", generator=g)
+    gam = torch.randn(N, device="cuda", generator=g)
+    bet = torch.randn(N, device="cuda", generator=g) * 0.1
+    pre = torch.empty(M, N, device="cuda")
+    P.gemm(a, w, pre, transpose_b=True, bias=bias, residual=res)
+    want = torch.empty(M, N, device="cuda")
+    want16 = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    hs = _abi.stream_handle
+    _abi.call("fq_layer_norm", pre.data_ptr(), N, gam.data_ptr(), bet.data_ptr(), 1e-5, M, N,
+              want.data_ptr(), N, want16.data_ptr(), N, hs())
+    ws = torch.full((4 * M * N,), float("nan"), device="cuda")
+    for _ in range(2):
+        out = torch.full((M, N), float("nan"), device="cuda")
+        out16 = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+        _abi.call("fq_gemm_ln", a.data_ptr(), K, w.data_ptr(), K, bias.data_ptr(), res.data_ptr(),
+                  N, gam.data_ptr(), bet.data_ptr(), 1e-5, out.data_ptr(), N, out16.data_ptr(), N,
+                  ws.data_ptr(), ws.numel() * 4, M, N, K, hs())
+        torch.cuda.synchronize()
+        assert torch.equal(out, want)
+        assert torch.equal(out16, want16)

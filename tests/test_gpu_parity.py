@@ -615,19 +615,27 @@ def test_logits_hars_equals_materialised_path(P, B, d, V):
         assert int((gmax != -2139095041).sum()) == 0  # reset for the next step
 
 
-def test_fused_layer_norm_engine_path(P, monkeypatch):
-    """Session.generate with FQ_FUSE_LN=1 (GEMM + LN pairs as fq_gemm_ln) gives
-    the same hypotheses as the default path at a bf16 config whose decode GEMMs
-    run split-K (d = 1024)."""
+@pytest.mark.parametrize("mode", ["slab", "coresident"])
+def test_fused_layer_norm_engine_path(P, monkeypatch, mode):
+    """Session.generate with the GEMM + LN pairs as fq_gemm_ln gives the same
+    hypotheses as the unfused path (FQ_FUSE_LN=0) at a bf16 config whose decode
+    GEMMs run split-K (d = 1024). The slab path (the default) reduces the K
+    slices in the same order as the in-kernel reduction: bit-identical."""
     cfg = P.ModelConfig(num_encoder_layers=1, num_decoder_layers=2, d_model=1024, d_ff=4096,
                         num_heads=16, vocab_size=4096, max_batch=32, max_seq_len=12,
                         max_beam_size=4)
     w = P.make_random_weights(cfg, seed=6)
     src = np.random.default_rng(3).integers(3, cfg.vocab_size, size=(32, 8))
     dc = P.DecodeConfig(beam_size=4, max_steps=8, eos_token=2)
+    monkeypatch.setenv("FQ_FUSE_LN", "0")
     want = P.Session(cfg, w, precision="bf16").generate(src, dc)
-    monkeypatch.setenv("FQ_FUSE_LN", "1")
+    monkeypatch.setenv("FQ_FUSE_LN", mode)
     got = P.Session(cfg, w, precision="bf16").generate(src, dc)
+    if mode == "slab":
+        for x, y in zip(got, want):
+            assert [h.tokens for h in x] == [h.tokens for h in y]
+            assert [h.score for h in x] == [h.score for h in y]
+        return
     same = sum(x[0].tokens == y[0].tokens for x, y in zip(got, want))
     assert same >= len(want) - 1  # LN statistics summed in another order: near-ties may flip
     for x, y in zip(got, want):
