@@ -237,6 +237,8 @@ def probe_step_gemms(sess, src_dev, dc):
             M, N, K = int(a[4]), int(a[5]), int(a[6])
         elif name == "fq_gemm_ln":  # (..., ws, ws_bytes, M, N, K, stream)
             M, N, K = int(a[16]), int(a[17]), int(a[18])
+        elif name == "fq_gemm_splitk_slabs":  # (a, lda, w, ldw, ws, ws_bytes, M, N, K, ...)
+            M, N, K = int(a[6]), int(a[7]), int(a[8])
         else:
             M, N, K = int(a[10]), int(a[11]), int(a[12])
         rows.append((M, N, K, e0.elapsed_time(e1) / 1e3))
@@ -364,7 +366,8 @@ def run_ours(args, rank, world):
                       "x 6 layers + the logits GEMM, whose epilogue computes HARS stage 1), "
                       "timed with events inside the step graph; self-out, cross-out and FFN2 "
                       "run as fq_gemm_ln (split-K GEMM writing K-slice slabs + the LN kernel "
-                      "that reduces them), timed with their LN",
+                      "that reduces them), timed with their LN; cross-q writes slabs that the "
+                      "cross-attention kernel sums",
             "bound": "tensor", "achieved": g_flops / g_time / 1e12, "peak": tc_peak,
             "unit": "TFLOP/s", "frac": g_flops / g_time / 1e12 / tc_peak, "traffic": traffic,
             "launches_per_step": len(gemms), "flops_per_launch_mean": g_flops / max(len(gemms), 1),

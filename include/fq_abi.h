@@ -149,6 +149,16 @@ int fq_gemm_ln(const void* a, int64_t lda, const void* w, int64_t ldw, const flo
                float* out, int64_t ldo, void* out16, int64_t ldo16, void* ws, int64_t ws_bytes,
                int64_t M, int64_t N, int64_t K, fq_stream_t stream);
 
+/* The split-K bf16 GEMM's per-K-slice fp32 partials without the reduction:
+ * ws [nslab][M][N], slab s = a[:, slice s] . w[:, slice s]^T (a [M,K], w
+ * [N,K]). Sets *nslab = 0 and launches nothing when this shape's plan is not
+ * split-K or ws < split * M * N * 4 bytes. The consumer sums the slabs in slab
+ * order (fq_splitk_bias_residual_layer_norm, fq_cross_attention_slabs), which
+ * reproduces the split-K kernel's own reduction bit for bit. */
+int fq_gemm_splitk_slabs(const void* a, int64_t lda, const void* w, int64_t ldw, void* ws,
+                         int64_t ws_bytes, int64_t M, int64_t N, int64_t K, int* nslab,
+                         fq_stream_t stream);
+
 /* C[M,N] = epilogue(A[M,K] @ op(B)); op(B) = B [K,N] (ldb) or B^T with B
  * [N,K] when transpose_b. Epilogue (fused, fp32 math): t = acc (+ C if
  * accumulate) (+ bias[N]); t = act(t); t = t + residual[M,N] (ldr).
@@ -320,6 +330,16 @@ int fq_cross_attention(const float* cq, int64_t ldcq, const void* ck, const void
                        int64_t heads, int64_t head_dim, float scale, const float* mask,
                        float* out, void* out16, int64_t ldo, int exact, int* d_bad,
                        fq_stream_t stream);
+
+/* fq_cross_attention (bf16 K/V, head_dim 64, seq <= 64, beam <= 8) whose
+ * query is given as the nslab K-slice slabs of the split-K query GEMM
+ * (fq_gemm_splitk_slabs; slab s at q_slabs + s * batch*beam*ldq) plus q_bias:
+ * q = ((slab0 + slab1) + ...) + bias, the GEMM's own epilogue order. */
+int fq_cross_attention_slabs(const float* q_slabs, int nslab, int64_t ldq, const float* q_bias,
+                             const void* ck, const void* cv, int64_t ldkv, int64_t batch,
+                             int64_t beam, int64_t seq, int64_t heads, int64_t head_dim,
+                             float scale, const float* mask, float* out, void* out16, int64_t ldo,
+                             int* d_bad, fq_stream_t stream);
 
 /* ---- weight preparation (cast once at load) -------------- */
 

@@ -73,6 +73,9 @@ SIGNATURES = {
     "fq_cross_attention": ([P, I64, P, P, I32, I64, I64, I64, I64, I64, I64, F32, P, P, P, I64,
                             I32, P, P], I32),
     "fq_cast_bf16": ([P, I64, I64, I32, P, P], I32),
+    "fq_cross_attention_slabs": ([P, I32, I64, P, P, P, I64, I64, I64, I64, I64, I64, F32, P, P,
+                                  P, I64, P, P], I32),
+    "fq_gemm_splitk_slabs": ([P, I64, P, I64, P, I64, I64, I64, I64, P, P], I32),
 }
 
 _ERRORS = {-1: DimensionError, -2: ParameterError, -3: AliasingError, -4: CapacityError,
@@ -120,7 +123,7 @@ def load():
 # become event-record nodes inside a captured CUDA graph) and
 # (name, args, start, end) is appended. Off (None) on the product path.
 PROBE = None
-PROBE_NAMES = ("fq_gemm", "fq_logits_hars", "fq_gemm_ln")
+PROBE_NAMES = ("fq_gemm", "fq_logits_hars", "fq_gemm_ln", "fq_gemm_splitk_slabs")
 
 
 def call(name: str, *args) -> int:
@@ -144,7 +147,9 @@ def call(name: str, *args) -> int:
     else:
         rc = getattr(lib, name)(*args)
     if name not in _NO_PREPARE:
-        _launches[0] += 1  # every other entry point launches exactly one kernel
+        # every other entry point launches one kernel; fq_gemm_ln two (the
+        # split-K slab GEMM + the reducing LN, or the GEMM + LN fallback)
+        _launches[0] += 2 if name == "fq_gemm_ln" else 1
     if rc < 0:
         msg = lib.fq_last_error().decode("utf-8", "replace")
         raise _ERRORS.get(rc, EngineError)(f"{name}: {msg}")

@@ -1014,7 +1014,8 @@ __global__ void __launch_bounds__(32 * kCrossWarps) cross_attention_tma(
     const __grid_constant__ CUtensorMap tk, const __grid_constant__ CUtensorMap tv,
     const float* __restrict__ cq, int64_t ldcq, int beam, int seq, float scale,
     const float* __restrict__ mask, float* __restrict__ out, __nv_bfloat16* __restrict__ out16,
-    int64_t ldo, int* d_bad, int heads, int npairs) {
+    int64_t ldo, int* d_bad, int heads, int npairs, int nslab, int64_t slab,
+    const float* __restrict__ qbias) {
   constexpr int HD = 64, NT = 4, NP = 64;
   extern __shared__ __align__(1024) uint8_t smraw[];
   const int wid = threadIdx.x >> 5;
@@ -1058,6 +1059,26 @@ __global__ void __launch_bounds__(32 * kCrossWarps) cross_attention_tma(
     for (int kk = 0; kk < HD / 16; ++kk) {
       float2 x0 = ok ? *reinterpret_cast<const float2*>(qp + 16 * kk + 2 * t4) : make_float2(0.f, 0.f);
       float2 x1 = ok ? *reinterpret_cast<const float2*>(qp + 16 * kk + 2 * t4 + 8) : make_float2(0.f, 0.f);
+      if (nslab > 0 && ok) {
+        // q = the split-K query GEMM's K-slice slabs summed in slab order, then
+        // + bias: the additions of the GEMM's own reduction epilogue, same order
+        for (int sl = 1; sl < nslab; ++sl) {
+          const float2 y0 = *reinterpret_cast<const float2*>(qp + sl * slab + 16 * kk + 2 * t4);
+          const float2 y1 = *reinterpret_cast<const float2*>(qp + sl * slab + 16 * kk + 2 * t4 + 8);
+          x0.x = fadd_rn(x0.x, y0.x);
+          x0.y = fadd_rn(x0.y, y0.y);
+          x1.x = fadd_rn(x1.x, y1.x);
+          x1.y = fadd_rn(x1.y, y1.y);
+        }
+        if (qbias) {
+          const float2 b0 = *reinterpret_cast<const float2*>(qbias + h * HD + 16 * kk + 2 * t4);
+          const float2 b1 = *reinterpret_cast<const float2*>(qbias + h * HD + 16 * kk + 2 * t4 + 8);
+          x0.x = fadd_rn(x0.x, b0.x);
+          x0.y = fadd_rn(x0.y, b0.y);
+          x1.x = fadd_rn(x1.x, b1.x);
+          x1.y = fadd_rn(x1.y, b1.y);
+        }
+      }
       split2(x0.x, x0.y, qh[kk][0], ql[kk][0]);
       split2(x1.x, x1.y, qh[kk][1], ql[kk][1]);
     }
@@ -1639,6 +1660,31 @@ int fq_decoder_self_attention(const float* sqkv, int64_t ldq, void* kcache, void
   return launch_status("fq_decoder_self_attention");
 }
 
+int fq_cross_attention_slabs(const float* q_slabs, int nslab, int64_t ldq, const float* q_bias,
+                             const void* ck, const void* cv, int64_t ldkv, int64_t batch,
+                             int64_t beam, int64_t seq, int64_t heads, int64_t head_dim,
+                             float scale, const float* mask, float* out, void* out16, int64_t ldo,
+                             int* d_bad, fq_stream_t stream) {
+  FQ_CHECK_ARG(q_slabs && nslab >= 1 && nslab <= 8 && ck && cv && (out || out16) && batch > 0 &&
+                   beam > 0 && beam <= 8 && seq > 0 && seq <= 64 && heads > 0 &&
+                   head_dim == 64 && ldq % 2 == 0 && ((uintptr_t)q_slabs & 7) == 0 &&
+                   ldkv % 8 == 0 && ((uintptr_t)ck & 15) == 0 && ((uintptr_t)cv & 15) == 0 &&
+                   (!q_bias || ((uintptr_t)q_bias & 7) == 0),
+               FQ_ERR_DIMENSION, "fq_cross_attention_slabs: unsupported shape");
+  CUtensorMap tk, tv;
+  const int64_t nrows = batch * seq, ncols = heads * head_dim;
+  int rc;
+  if ((rc = make_tmap_bf16_sw128(&tk, ck, nrows, ncols, ldkv, 64, 64)) != FQ_OK) return rc;
+  if ((rc = make_tmap_bf16_sw128(&tv, cv, nrows, ncols, ldkv, 64, 64)) != FQ_OK) return rc;
+  const int npairs = (int)(batch * heads);
+  launch_kernel(cross_attention_tma, (unsigned)((npairs + kCrossWarps - 1) / kCrossWarps),
+                32 * kCrossWarps, (size_t)kCrossWarps * 2 * 64 * 128 + 1024, as_stream(stream),
+                1u, tk, tv, q_slabs, ldq, (int)beam, (int)seq, scale, mask, out,
+                reinterpret_cast<__nv_bfloat16*>(out16), ldo, d_bad, (int)heads, npairs, nslab,
+                (int64_t)(batch * beam) * ldq, q_bias);
+  return launch_status("fq_cross_attention_slabs");
+}
+
 int fq_cross_attention(const float* cq, int64_t ldcq, const void* ck, const void* cv,
                        int kv_dtype, int64_t ldkv, int64_t batch, int64_t beam, int64_t seq,
                        int64_t heads, int64_t head_dim, float scale, const float* mask,
@@ -1659,7 +1705,7 @@ int fq_cross_attention(const float* cq, int64_t ldcq, const void* ck, const void
                     32 * kCrossWarps, (size_t)kCrossWarps * 2 * 64 * 128 + 1024,
                     as_stream(stream), 1u, tk, tv, cq, ldcq, (int)beam, (int)seq, scale, mask,
                     out, reinterpret_cast<__nv_bfloat16*>(out16), ldo, d_bad, (int)heads,
-                    npairs);
+                    npairs, 0, (int64_t)0, (const float*)nullptr);
       return launch_status("fq_cross_attention");
     }
   }

@@ -259,6 +259,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __shared__ __align__(8) uint64_t empty_bar[STAGES];
   __shared__ __align__(8) uint64_t tfull_bar[2];
   __shared__ __align__(8) uint64_t tempty_bar[2];
+  __shared__ __align__(8) uint64_t edone_bar;  // the 4 epilogue warps finished with TMEM
   __shared__ uint32_t tmem_base_sh;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -286,6 +287,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&tfull_bar[s], 1);
       mbar_init(&tempty_bar[s], 4);  // one arrive per epilogue warp
     }
+    mbar_init(&edone_bar, 4);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tma_a)));
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tma_b)));
@@ -503,6 +505,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int g = cluster_id; g < ngroups; g += nclusters, ++local) {
       const int as = local & 1;
       const int m0 = ((g % mg) * cm + ry) * BM, n0 = ((g / mg) * cn + rx) * BN;
+      // the tile's bias columns are requested before the accumulator wait, so
+      // their latency hides under the mainloop (per-chunk loads after the wait
+      // cost one L2/HBM round trip per 32 columns: 7.7 -> ~1 us epilogue)
+      float bpre[BN / 32];
+#pragma unroll
+      for (int j = 0; j < BN / 32; ++j) {
+        const int bc = n0 + j * 32 + lane;
+        bpre[j] = (ep.bias && bc < N) ? __ldg(ep.bias + bc) : 0.0f;
+      }
       mbar_wait(&tfull_bar[as], (local >> 1) & 1);
       if (local == 0 && threadIdx.x == 64) dbg_stamp(ep.dbg, 4);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -542,7 +553,10 @@ __global__ void __launch_bounds__(kThreads, 1)
               for (int i = 0; i < 16; ++i) x[i] = fadd_rn(cv[i], x[i]);
             }
             if (ep.bias) {
-              const float bias = __ldg(ep.bias + col);
+              float bias = bpre[0];
+#pragma unroll
+              for (int j = 1; j < BN / 32; ++j)
+                if (cc == j * 32) bias = bpre[j];
 #pragma unroll
               for (int i = 0; i < 16; ++i) x[i] = fadd_rn(x[i], bias);
             }
@@ -576,10 +590,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (threadIdx.x == 64) dbg_stamp(ep.dbg, 5);  // epilogue done
   __syncwarp();
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  if (warp >= 2 && lane == 0) mbar_arrive(&edone_bar);
   if (csize > 1) cluster_sync_all();  // no CTA leaves while peers may still signal it
   else __syncthreads();
   if (threadIdx.x == 0) dbg_stamp(ep.dbg, 6);
   if (warp == 1) {
+    // dealloc strictly after every epilogue warp's last tcgen05.ld (measured:
+    // the block barrier alone released warps 0-1 before the epilogue ended)
+    mbar_wait(&edone_bar, 0);
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
                  "r"(TMEM_COLS));
@@ -1265,6 +1283,26 @@ extern "C" int fq_gemm_ln(const void* a, int64_t lda, const void* w, int64_t ldw
                           as_stream(stream));
   if (rc != FQ_OK) return rc;
   return fq_layer_norm(out, ldo, gamma, beta, eps, M, N, out, ldo, out16, ldo16, stream);
+}
+
+// The split-K GEMM's K-slice partials as slabs (no reduction): ws [nslab][M][N]
+// fp32, slab s = a[:, slice s] . w[:, slice s]^T. *nslab = 0 (nothing launched)
+// when the plan for this shape is not split-K or ws is too small.
+extern "C" int fq_gemm_splitk_slabs(const void* a, int64_t lda, const void* w, int64_t ldw,
+                                    void* ws, int64_t ws_bytes, int64_t M, int64_t N, int64_t K,
+                                    int* nslab, fq_stream_t stream) {
+  FQ_CHECK_ARG(a && w && nslab && M > 0 && N > 0 && K > 0 && lda % 8 == 0 && ldw % 8 == 0,
+               FQ_ERR_DIMENSION, "fq_gemm_splitk_slabs: bad args");
+  *nslab = 0;
+  const TcPlan p = plan_tc(M, N, K);
+  if (!(p.split > 1 && p.bn == 128 && p.cm == 1 && p.cn == 1 && ws && N % 4 == 0 &&
+        ((uintptr_t)ws & 15) == 0 && ws_bytes >= (int64_t)p.split * M * N * (int64_t)sizeof(float)))
+    return FQ_OK;
+  tc::Epi ep{ws, N, 0, 0, nullptr, nullptr, 0, 0, g_gemm_dbg};
+  const int rc = tc::launch_splitk<128, 6, false, true>(a, lda, w, ldw, ep, M, N, K, p.split,
+                                                        as_stream(stream));
+  if (rc == FQ_OK) *nslab = p.split;
+  return rc;
 }
 
 // Benchmarks only: force (bn, cm, cn) for shapes it divides; bn = 0 restores auto.

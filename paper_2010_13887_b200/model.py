@@ -23,6 +23,7 @@ Every intermediate is a view of the session arena (``plan_intermediates``).
 
 from __future__ import annotations
 
+import ctypes
 import math
 import os
 from dataclasses import dataclass
@@ -669,6 +670,11 @@ class DecoderStep:
                 ws = ws[:(ln_ws_bytes(R, d, slabs=False) + 3) // 4]
                 ws.zero_()
             self.ln_ws = ws
+        # the cross-attention query GEMM as K-slice slabs summed by the
+        # cross-attention kernel (no in-GEMM reduction), same bits
+        self.q_slabs = (self.ln_ws is not None and mode != "coresident" and
+                        config.head_dim == 64 and beam <= 8 and enc_seq <= 64)
+        self._nslab = ctypes.c_int(0)
 
     def embed(self):
         """Decoder input of the current position (model.py:559)."""
@@ -711,16 +717,32 @@ class DecoderStep:
                      residual=x, counters=ctr, timers=tm)
                 _ln(self.sres, lw["ln1_g"], lw["ln1_b"], c.ln_eps, self.snorm, self.snorm16,
                     counters=ctr)
-            _lin(dw, self.snorm, self.snorm16, lw["w_cq"], self.cq, bias=lw["b_cq"],
-                 counters=ctr, timers=tm)
             ld = self.cross.stride(0)
             ck = self.cross[:, 2 * i * d:]
             cv = self.cross[:, (2 * i + 1) * d:]
-            _abi.call("fq_cross_attention", self.cq.data_ptr(), self.cq.stride(0), ck.data_ptr(),
-                      cv.data_ptr(), kvdt, ld, self.batch, self.beam, self.enc_seq, h, hd, scale,
-                      _abi.ptr(self.mask), None if dw.bf16 else self.cctx.data_ptr(),
-                      self.cctx.data_ptr() if dw.bf16 else None, d, exact,
-                      self.bad.data_ptr(), stream)
+            nsl = 0
+            if self.q_slabs:
+                w = lw["w_cq"]
+                _abi.call("fq_gemm_splitk_slabs", self.snorm16.data_ptr(), self.snorm16.stride(0),
+                          w.data_ptr(), w.stride(0), self.ln_ws.data_ptr(),
+                          self.ln_ws.numel() * self.ln_ws.element_size(), R, d, d,
+                          ctypes.addressof(self._nslab), stream)
+                nsl = self._nslab.value
+            if nsl:
+                ctr.count_gemm((R * d + d * d) * 2 + 4 * R * d * 4)
+                _abi.call("fq_cross_attention_slabs", self.ln_ws.data_ptr(), nsl, d,
+                          lw["b_cq"].data_ptr(), ck.data_ptr(), cv.data_ptr(), ld, self.batch,
+                          self.beam, self.enc_seq, h, hd, scale, _abi.ptr(self.mask), None,
+                          self.cctx.data_ptr(), d, self.bad.data_ptr(), stream)
+            else:
+                _lin(dw, self.snorm, self.snorm16, lw["w_cq"], self.cq, bias=lw["b_cq"],
+                     counters=ctr, timers=tm)
+                _abi.call("fq_cross_attention", self.cq.data_ptr(), self.cq.stride(0),
+                          ck.data_ptr(), cv.data_ptr(), kvdt, ld, self.batch, self.beam,
+                          self.enc_seq, h, hd, scale, _abi.ptr(self.mask),
+                          None if dw.bf16 else self.cctx.data_ptr(),
+                          self.cctx.data_ptr() if dw.bf16 else None, d, exact,
+                          self.bad.data_ptr(), stream)
             ctr.count_fused("cross_attention", R * d * 16)
             if self.ln_ws is not None:
                 _lin_ln(dw, self.cctx, self.cctx, lw["w_co"], lw["b_co"], self.snorm,
