@@ -82,6 +82,17 @@ __device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, uint64_t* ba
       : "memory");
 }
 
+// TMA tensor store of one smem box (bulk-group completion).
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int c0,
+                                             int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+          reinterpret_cast<uint64_t>(map)),
+      "r"(c0), "r"(c1), "r"(smem_u32(src))
+      : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+
 // K-major operand, 128-byte swizzle: rows of 128 B, 8-row atoms 1024 B apart.
 __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
   uint64_t d = 0;
@@ -146,6 +157,7 @@ struct Epi {
   int64_t ldr;
   int act;
   unsigned long long* dbg;  // per-CTA [start, end] %globaltimer (profiling only)
+  int tstore;  // 1: C through TMA tensor stores (tma_c: 32-row x 128-byte boxes)
 };
 
 // HARS stage-1 statistics computed in the logits GEMM's epilogue (the [rows,
@@ -242,7 +254,7 @@ template <int BN, int STAGES, bool HS = false>
 __global__ void __launch_bounds__(kThreads, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tma_a,
                    const __grid_constant__ CUtensorMap tma_b, const Epi ep, int M, int N, int K,
-                   int cm, int cn, const HarsEpi he) {
+                   int cm, int cn, const HarsEpi he, const __grid_constant__ CUtensorMap tma_c) {
   constexpr int A_BYTES = BM * BK * 2;
   constexpr int B_BYTES = BN * BK * 2;
   constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
@@ -528,6 +540,64 @@ __global__ void __launch_bounds__(kThreads, 1)
           __syncwarp();
           if (lane == 0) mbar_arrive(&tempty_bar[as]);
         }
+        if (ep.tstore) {
+          // thread = row: epilogue math on the tcgen05.ld registers, the
+          // 32 x 32 chunk written swizzled into this warp's 4 KB box area
+          // (conflict-free 16-byte stores), then one TMA tensor store per chunk
+          // (full-line writes; fp32: one 4 KB box, bf16: two 2 KB boxes)
+          uint8_t* box = reinterpret_cast<uint8_t*>(stage_out) + (warp - 2) * 4096;
+          const int col0 = n0 + cc;
+          if (ep.bias) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const float4 b = (col0 + 4 * j + 3 < N)
+                                   ? __ldg(reinterpret_cast<const float4*>(ep.bias + col0 + 4 * j))
+                                   : make_float4(0.f, 0.f, 0.f, 0.f);
+              v[4 * j] = fadd_rn(v[4 * j], b.x);
+              v[4 * j + 1] = fadd_rn(v[4 * j + 1], b.y);
+              v[4 * j + 2] = fadd_rn(v[4 * j + 2], b.z);
+              v[4 * j + 3] = fadd_rn(v[4 * j + 3], b.w);
+            }
+          }
+          if (ep.act) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = apply_act(v[j], ep.act);
+          }
+          if (lane == 0) {  // my box area is free again (bf16: the one two chunks back)
+            if (ep.c_bf16) asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(1) : "memory");
+            else asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(0) : "memory");
+          }
+          __syncwarp();
+          if (ep.c_bf16) {
+            uint8_t* bx = box + ((cc >> 5) & 1) * 2048;  // 32 rows x 64 B, 64-byte swizzle
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              uint4 pk;
+              __nv_bfloat162 hh;
+              hh = __floats2bfloat162_rn(v[8 * j], v[8 * j + 1]);
+              pk.x = *reinterpret_cast<uint32_t*>(&hh);
+              hh = __floats2bfloat162_rn(v[8 * j + 2], v[8 * j + 3]);
+              pk.y = *reinterpret_cast<uint32_t*>(&hh);
+              hh = __floats2bfloat162_rn(v[8 * j + 4], v[8 * j + 5]);
+              pk.z = *reinterpret_cast<uint32_t*>(&hh);
+              hh = __floats2bfloat162_rn(v[8 * j + 6], v[8 * j + 7]);
+              pk.w = *reinterpret_cast<uint32_t*>(&hh);
+              *reinterpret_cast<uint4*>(bx + lane * 64 + ((j ^ ((lane >> 1) & 3)) << 4)) = pk;
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) tma_store_2d(&tma_c, bx, col0, rbase);
+          } else {  // 32 rows x 128 B, 128-byte swizzle
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              *reinterpret_cast<float4*>(box + lane * 128 + ((j ^ (lane & 7)) << 4)) =
+                  make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) tma_store_2d(&tma_c, box, col0, rbase);
+          }
+          continue;
+        }
         // transpose through smem: thread = row on the TMEM side, column on the store side
 #pragma unroll
         for (int j = 0; j < 32; ++j) st[lane * 33 + j] = v[j];
@@ -586,6 +656,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         __syncwarp();  // staging free for the next chunk
       }
     }
+  }
+  if constexpr (!HS) {  // TMA stores complete (smem read, writes performed) before exit
+    if (ep.tstore && warp >= 2 && lane == 0)
+      asm volatile("cp.async.bulk.wait_group %0;" ::"n"(0) : "memory");
   }
   if (threadIdx.x == 64) dbg_stamp(ep.dbg, 5);  // epilogue done
   __syncwarp();
@@ -1007,6 +1081,34 @@ static int make_map(CUtensorMap* map, const void* ptr, int64_t rows, int64_t col
   return FQ_OK;
 }
 
+// Output map for the TMA-store epilogue: [rows, cols] row-major (ld elements),
+// box 32 rows x 32 elements (fp32: 128 B rows, 128-byte swizzle; bf16: 64 B
+// rows, 64-byte swizzle) — the layout the epilogue writes its boxes in.
+static int make_map_c(CUtensorMap* map, void* ptr, int64_t rows, int64_t cols, int64_t ld,
+                      bool bf16) {
+  EncodeFn enc = get_encode();
+  if (!enc) return FQ_ERR_CUDA;
+  const int es = bf16 ? 2 : 4;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * es)};
+  cuuint32_t box[2] = {32u, 32u};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                   2, ptr, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   bf16 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? FQ_OK : FQ_ERR_CUDA;
+}
+
+static bool tma_store_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("FQ_TMA_STORE");
+    on = (e && e[0] == '0') ? 0 : 1;
+  }
+  return on == 1;
+}
+
 }  // namespace tc
 
 // 2D bf16 tensor map with 128-byte swizzle for other kernels (attention):
@@ -1049,18 +1151,25 @@ template <int BN, int STAGES, bool HS = false>
 static int launch(const void* a, int64_t lda, const void* b, int64_t ldb, const Epi& ep,
                   int64_t M, int64_t N, int64_t K, int cm, int cn, cudaStream_t s,
                   const HarsEpi& he = HarsEpi{}) {
-  CUtensorMap ma, mb;
+  CUtensorMap ma, mb, mc;
   int rc;
   if ((rc = make_map(&ma, a, M, K, lda, BM / cn)) != FQ_OK) return rc;
   if ((rc = make_map(&mb, b, N, K, ldb, BN / cm)) != FQ_OK) return rc;
+  Epi e2 = ep;
+  e2.tstore = 0;
+  mc = ma;
+  if (!HS && ep.c && !ep.accumulate && !ep.res && N % 32 == 0 && tma_store_enabled() &&
+      ((uintptr_t)ep.c & 15) == 0 && (ep.ldc * (ep.c_bf16 ? 2 : 4)) % 16 == 0 &&
+      make_map_c(&mc, ep.c, M, N, ep.ldc, ep.c_bf16 != 0) == FQ_OK)
+    e2.tstore = 1;
   const int csize = cm * cn;
   const int64_t groups = ((M + BM - 1) / BM / cm) * ((N + BN - 1) / BN / cn);
   const int64_t max_clusters = num_sms() / csize;
   const int64_t clusters = groups < max_clusters ? groups : max_clusters;
   cudaError_t e = launch_kernel(tc_gemm_kernel<BN, STAGES, HS>,
                                 dim3((unsigned)(clusters * csize)), dim3(kThreads),
-                                smem_bytes<BN, STAGES, HS>(), s, (unsigned)csize, ma, mb, ep,
-                                (int)M, (int)N, (int)K, cm, cn, he);
+                                smem_bytes<BN, STAGES, HS>(), s, (unsigned)csize, ma, mb, e2,
+                                (int)M, (int)N, (int)K, cm, cn, he, mc);
   if (e != cudaSuccess) {
     set_error("fq_gemm(tcgen05): launch failed: %s", cudaGetErrorString(e));
     return FQ_ERR_CUDA;

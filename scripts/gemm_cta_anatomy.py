@@ -22,11 +22,15 @@ for sh in shapes.split(","):
     bias = torch.randn(N, device="cuda")
     c = torch.empty(M, N, device="cuda", dtype=torch.float32 if os.environ.get("F32") else torch.bfloat16)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    clean = torch.ones(64 << 20, dtype=torch.float32, device="cuda")  # read after the fill:
+    # evicts the fill's dirty lines, so the GEMM does not pay their write-back
     dbg = torch.zeros(8 * 1024, dtype=torch.int64, device="cuda")
     for i in range(4):
         P.gemm(a, bs[i], c, transpose_b=True, bias=bias, activation="relu")
     for rep in range(3):
         flush.fill_(1)
+        if os.environ.get("CLEAN", "1") == "1":
+            clean.sum()
         dbg.zero_()
         torch.cuda.synchronize()
         lib.fq_gemm_debug_timestamps(dbg.data_ptr())
