@@ -713,7 +713,8 @@ template <int BN, int STAGES, bool LNF = false, bool SLAB = false>
 __global__ void __launch_bounds__(kThreads, 1)
     tc_gemm_splitk_kernel(const __grid_constant__ CUtensorMap tma_a,
                           const __grid_constant__ CUtensorMap tma_b, const Epi ep, int M, int N,
-                          int K, int kb_per_split, const LnEpi ln, int nsplit) {
+                          int K, int kb_per_split, const LnEpi ln, int nsplit,
+                          const __grid_constant__ CUtensorMap tma_c) {
   constexpr int A_BYTES = BM * BK * 2;
   constexpr int B_BYTES = BN * BK * 2;
   constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
@@ -807,15 +808,38 @@ __global__ void __launch_bounds__(kThreads, 1)
     mbar_wait(&tfull_bar, 0);
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     float* prow = part + (q * 32 + lane) * PLD;
+    if constexpr (SLAB) {
+      if (ep.tstore) {
+        // slab tile straight from TMEM through TMA tensor stores: per warp and
+        // 32-column chunk one swizzled 32 x 128 B box in the (idle) ring, rows
+        // rank * M + m0 + q * 32 of the [S * M, N] slab map
 #pragma unroll 1
-    for (int cc = 0; cc < BN; cc += 32) {
+        for (int cc = 0; cc < BN; cc += 32) {
+          float v[32];
+          tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + cc, v);
+          uint8_t* box = smem + q * (BN / 32) * 4096 + (cc / 32) * 4096;
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            *reinterpret_cast<float4*>(box + lane * 128 + ((j ^ (lane & 7)) << 4)) =
+                make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncwarp();
+          if (lane == 0 && m0 + q * 32 < M)  // M % 32 == 0: whole boxes inside the slab
+            tma_store_2d(&tma_c, box, n0 + cc, rank * M + m0 + q * 32);
+        }
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group %0;" ::"n"(0) : "memory");
+        __syncwarp();
+      }
+    }
+#pragma unroll 1
+    for (int cc = 0; cc < BN && !(SLAB && ep.tstore); cc += 32) {
       float v[32];
       tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + cc, v);
 #pragma unroll
       for (int j = 0; j < 32; j += 4)
         *reinterpret_cast<float4*>(prow + cc + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
     }
-    if constexpr (SLAB) {  // my 32 rows, one row (BN * 4 contiguous bytes) per warp pass
+    if (SLAB && !ep.tstore) {  // my 32 rows, one row (BN * 4 contiguous bytes) per warp pass
       __syncwarp();
       float* slab = reinterpret_cast<float*>(ep.c) + (int64_t)rank * M * ep.ldc;
 #pragma unroll 4
@@ -1181,17 +1205,23 @@ template <int BN, int STAGES, bool LNF = false, bool SLAB = false>
 static int launch_splitk(const void* a, int64_t lda, const void* b, int64_t ldb, const Epi& ep,
                          int64_t M, int64_t N, int64_t K, int S, cudaStream_t s,
                          const LnEpi& ln = LnEpi{}) {
-  CUtensorMap ma, mb;
+  CUtensorMap ma, mb, mc;
   int rc;
   if ((rc = make_map(&ma, a, M, K, lda, BM)) != FQ_OK) return rc;
   if ((rc = make_map(&mb, b, N, K, ldb, BN)) != FQ_OK) return rc;
+  Epi e2 = ep;
+  e2.tstore = 0;
+  mc = ma;
+  if (SLAB && M % 32 == 0 && N % 32 == 0 && tma_store_enabled() && ((uintptr_t)ep.c & 15) == 0 &&
+      (ep.ldc * 4) % 16 == 0 && make_map_c(&mc, ep.c, S * M, N, ep.ldc, false) == FQ_OK)
+    e2.tstore = 1;
   const int64_t tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
   const int nkb = (int)((K + BK - 1) / BK);
   const int kbs = (nkb + S - 1) / S;
   cudaError_t e = launch_kernel(tc_gemm_splitk_kernel<BN, STAGES, LNF, SLAB>,
                                 dim3((unsigned)(tiles * S)), dim3(kThreads),
                                 smem_bytes_splitk<BN, STAGES>(), s, SLAB ? 1u : (unsigned)S, ma,
-                                mb, ep, (int)M, (int)N, (int)K, kbs, ln, S);
+                                mb, e2, (int)M, (int)N, (int)K, kbs, ln, S, mc);
   if (e != cudaSuccess) {
     set_error("fq_gemm(tcgen05 split-K): launch failed: %s", cudaGetErrorString(e));
     return FQ_ERR_CUDA;
