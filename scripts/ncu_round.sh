@@ -26,7 +26,7 @@ timeout 600 ncu --set full --clock-control none --import-source on --kernel-name
 echo "harsstep rc=$?"
 cap selfattn "decoder_self_attention" 190
 cap crossattn "cross_attention" 190
-cap ln "layer_norm_row128" 570
+cap ln "layer_norm_slabs_row128" 540
 cap logits "tc_gemm_kernel<.int.224" 30
 cap ffn1 "tc_gemm_kernel<.int.128" 380
 cap splitk "tc_gemm_splitk" 760
@@ -38,3 +38,6 @@ done
 python scripts/launch_summary.py gpurun_out/${T}_launches.csv 30 > gpurun_out/${T}_launches_summary.txt 2>&1
 rm -f gpurun_out/${T}_launches.csv gpurun_out/${T}_*.ncu-rep
 ls -la gpurun_out | grep $T
+python scripts/gemm_traffic_json.py gpurun_out/${T}_step_gemms.csv gpurun_out/${T}_ncu_gemm_traffic.json \
+  "ncu (--clock-control none) of the tc_gemm launches of one C2 bf16 decode step (step 11 of a generate; scripts/ncu_round.sh ${T}): dram__bytes_read.sum + dram__bytes_write.sum per launch" \
+  > gpurun_out/${T}_traffic.log 2>&1
