@@ -245,3 +245,45 @@ def test_encoder_attention_tiled(T, S, hd, exact):
     want = (P @ V).permute(0, 2, 1, 3).reshape(B * S, d)
     assert _rel(out, want) <= (1e-5 if exact else 1e-4)
     assert _rel(out16.float(), want) <= 1e-2
+
+
+@pytest.mark.parametrize("M,beam,S", [(512, 4, 64), (96, 3, 37)])
+def test_cross_attention_slabs_equal_reduced_query(T, M, beam, S):
+    """The engine's cross-q path: fq_gemm_splitk_slabs (the split-K GEMM's 4
+    K-slice partials, no reduction) + fq_cross_attention_slabs (slabs summed in
+    order + bias on load) is bit-identical to fq_gemm (split-K with its own
+    reduction, + bias) followed by fq_cross_attention."""
+    import ctypes
+    A = _abi()
+    g = T.Generator(device="cuda").manual_seed(M + beam + S)
+    d, H, hd, L = 1024, 16, 64, 2
+    B = M // beam
+    R = B * beam
+    x16 = T.randn(R, d, device="cuda", generator=g).to(T.bfloat16)
+    w = (T.randn(d, d, device="cuda", generator=g) / 32).to(T.bfloat16)
+    bias = T.randn(d, device="cuda", generator=g) * 0.1
+    ld = 2 * L * d
+    packed = T.randn(B * S, ld, device="cuda", generator=g).to(T.bfloat16)
+    mask = T.zeros(B, S, device="cuda")
+    mask[0, S // 2:] = -math.inf
+    scale = float(np.float32(1 / math.sqrt(hd)))
+    ck, cv = packed[:, 2 * d:], packed[:, 3 * d:]
+    q = T.empty(R, d, device="cuda")
+    import paper_2010_13887_b200 as P
+    P.gemm(x16, w, q, transpose_b=True, bias=bias)
+    want = T.empty(R, d, device="cuda", dtype=T.bfloat16)
+    bad = T.zeros(1, dtype=T.int32, device="cuda")
+    A.call("fq_cross_attention", q.data_ptr(), d, ck.data_ptr(), cv.data_ptr(), 1, ld, B, beam, S,
+           H, hd, scale, mask.data_ptr(), None, want.data_ptr(), d, 0, bad.data_ptr(),
+           A.stream_handle())
+    ws = T.full((4 * R * d,), float("nan"), device="cuda")
+    ns = ctypes.c_int(-1)
+    A.call("fq_gemm_splitk_slabs", x16.data_ptr(), d, w.data_ptr(), d, ws.data_ptr(),
+           ws.numel() * 4, R, d, d, ctypes.addressof(ns), A.stream_handle())
+    assert ns.value == 4
+    got = T.empty(R, d, device="cuda", dtype=T.bfloat16)
+    A.call("fq_cross_attention_slabs", ws.data_ptr(), ns.value, d, bias.data_ptr(), ck.data_ptr(),
+           cv.data_ptr(), ld, B, beam, S, H, hd, scale, mask.data_ptr(), None, got.data_ptr(), d,
+           bad.data_ptr(), A.stream_handle())
+    T.cuda.synchronize()
+    assert T.equal(got, want)
