@@ -390,6 +390,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         mma_commit(&tfull_bar[as]);   // accumulator stage complete
         if (local == 0) dbg_stamp(ep.dbg, 3);  // first tile's MMAs issued
       }
+      dbg_stamp(ep.dbg, 7);  // every tile's MMAs issued
     }
   } else if constexpr (HS) {  // ---- HARS statistics epilogue (thread = row) ----
     pdl_wait();  // the group counts / running maxima come from the previous kernel
