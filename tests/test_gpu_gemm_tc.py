@@ -200,3 +200,25 @@ def test_gemm_ln_slab_path_bit_identical(M, N, K):
         torch.cuda.synchronize()
         assert torch.equal(out, want)
         assert torch.equal(out16, want16)
+
+
+@pytest.mark.parametrize("dt", ["f32", "bf16"])
+@pytest.mark.parametrize("M,N,K,pad", [(200, 256, 256, 64), (512, 96, 512, 32), (77, 160, 128, 3)])
+def test_tc_gemm_tma_store_strided_views(P, dt, M, N, K, pad):
+    """The TMA-store epilogue writes through a tensor map with the output's
+    leading dimension: a column slice of a wider buffer (ld = N + pad) gets
+    exactly its M x N block, the padding columns stay untouched; pad = 3 makes
+    the rows unaligned for TMA and takes the transposed-store path."""
+    import torch
+    dtype = torch.float32 if dt == "f32" else torch.bfloat16
+    g = torch.Generator(device="cuda").manual_seed(M + N + pad)
+    a = torch.randn(M, K, device="cuda", generator=g).to(torch.bfloat16)
+    b = torch.randn(N, K, device="cuda", generator=g).to(torch.bfloat16)
+    bias = torch.randn(N, device="cuda", generator=g)
+    big = torch.full((M, N + pad), 7.0, device="cuda", dtype=dtype)
+    view = big[:, pad:]
+    P.gemm(a, b, view, transpose_b=True, bias=bias, activation="relu")
+    torch.cuda.synchronize()
+    tol = 1e-3 if dt == "f32" else 8e-3
+    assert _rel(view.float(), _ref(a, b, bias, "relu")) <= tol
+    assert bool((big[:, :pad].float() == 7.0).all())
