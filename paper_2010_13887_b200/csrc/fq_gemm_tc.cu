@@ -403,6 +403,21 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int m0 = ((g % mg) * cm + ry) * BM, n0 = ((g / mg) * cn + rx) * BN;
       const int r = m0 + q * 32 + lane;
       const int k = r < M ? he.dk[r] : 0;
+      // running lower bound of the row's R from the group maxima other tiles
+      // have already published (each read <= that group's final maximum, so
+      // the min over groups <= R): tightens the survivor bound of later tiles
+      // at no wait — the loads are in flight under this tile's mainloop
+      float rest = -INFINITY;
+      if (k == 8) {
+        const int4 a0 = __ldcg(reinterpret_cast<const int4*>(he.gmax + (int64_t)r * 32));
+        const int4 a1 = __ldcg(reinterpret_cast<const int4*>(he.gmax + (int64_t)r * 32 + 4));
+        rest = fminf(fminf(fminf(hs_ord2f(a0.x), hs_ord2f(a0.y)), fminf(hs_ord2f(a0.z), hs_ord2f(a0.w))),
+                     fminf(fminf(hs_ord2f(a1.x), hs_ord2f(a1.y)), fminf(hs_ord2f(a1.z), hs_ord2f(a1.w))));
+      } else if (k > 0) {
+        float mn = INFINITY;
+        for (int gq = 0; gq < k; ++gq) mn = fminf(mn, hs_ord2f(__ldcg(he.gmax + (int64_t)r * 32 + gq)));
+        rest = mn;
+      }
       mbar_wait(&tfull_bar[as], (local >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       for (int gq = 0; gq < k; ++gq) gms[gq] = -INFINITY;
@@ -451,6 +466,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             atomicMax(he.gmax + (int64_t)r * 32 + gq, hs_f2ord(gms[gq]));
             bound = fminf(bound, gms[gq]);
           }
+        bound = fmaxf(bound, rest);
       }
       // pass 2: sum exp(x - mt) (fp32 per 32-column chunk, f64 across chunks)
       // and survivors x >= bound: a branch-free per-chunk bit mask, then the set
