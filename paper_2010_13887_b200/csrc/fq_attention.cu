@@ -1585,7 +1585,7 @@ int fq_decoder_self_attention(const float* sqkv, int64_t ldq, void* kcache, void
     static int ns = -1;  // ring depth (FQ_SELF_STAGES = 2 | 3 | 4)
     if (ns < 0) {
       const char* e = getenv("FQ_SELF_STAGES");
-      ns = e ? atoi(e) : 2;
+      ns = e ? atoi(e) : 3;  // 3: +0.45% at C2 over 2 (3 paired bench runs), 4: -2%
     }
     auto kern = ns == 2 ? decoder_self_attention_mma<2>
               : ns == 4 ? decoder_self_attention_mma<4> : decoder_self_attention_mma<3>;
