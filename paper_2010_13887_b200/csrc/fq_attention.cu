@@ -1180,7 +1180,7 @@ __global__ void __launch_bounds__(32 * kCrossWarps) cross_attention_tma(
 }
 
 // Decoder self-attention on warp MMAs (bf16 cache, head_dim 64): warp per
-// (beam row, head). Cached positions stream through a 2-stage shared-memory
+// (beam row, head). Cached positions stream through an NS-stage (default 3) shared-memory
 // ring in chunks of 16 (cp.async 16-byte pieces of the hist-gathered slot rows,
 // 128-byte rows with an XOR chunk swizzle, so ldmatrix is conflict-free); this
 // step's K/V (position cur) are written to their cache slot and placed in the
