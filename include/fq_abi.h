@@ -162,14 +162,46 @@ int fq_gemm_splitk_slabs(const void* a, int64_t lda, const void* w, int64_t ldw,
 /* C[M,N] = epilogue(A[M,K] @ op(B)); op(B) = B [K,N] (ldb) or B^T with B
  * [N,K] when transpose_b. Epilogue (fused, fp32 math): t = acc (+ C if
  * accumulate) (+ bias[N]); t = act(t); t = t + residual[M,N] (ldr).
- * dtypes: a_dtype == b_dtype. FQ_F32 operands -> exact-mode SIMT FFMA kernel
- * (sequential K order, M-independent). FQ_BF16 operands require transpose_b
- * (weights pre-laid-out [N,K]) and run on tcgen05 tensor cores (TMEM
- * accumulators, TMA-fed, fp32 accumulate). c_dtype: FQ_F32 or FQ_BF16. */
+ * dtypes: a_dtype == b_dtype. FQ_F32 operands with transpose_b (K-major B),
+ * 16-byte aligned rows and an fp32 C: the exact-mode 3xTF32 tcgen05 kernel
+ * (fq_gemm_f32x3 with b_lo = NULL); other FQ_F32 layouts: the SIMT FFMA
+ * kernel (sequential K order, M-independent; API use only). FQ_BF16 operands
+ * require transpose_b (weights pre-laid-out [N,K]) and run on tcgen05 tensor
+ * cores (TMEM accumulators, TMA-fed, fp32 accumulate). c_dtype: FQ_F32 or
+ * FQ_BF16. */
 int fq_gemm(const void* a, int a_dtype, int64_t lda, const void* b, int b_dtype, int64_t ldb,
             int transpose_b, void* c, int c_dtype, int64_t ldc, int64_t M, int64_t N,
             int64_t K, int accumulate, const float* bias, const float* residual, int64_t ldr,
             int act, fq_stream_t stream);
+
+/* Exact fp32 mode on the tensor cores (replaces tensor.py:179-204's OpenBLAS
+ * SGEMM on the engine path): C = epilogue(A . B^T) as in fq_gemm, A [M,K]
+ * fp32, B [N,K] fp32 K-major. Each operand is split into tf32 hi + lo (x =
+ * hi + lo to 2^-22) and the product is accumulated as a_hi.b_lo + a_lo.b_hi +
+ * a_hi.b_hi on kind::tf32 tcgen05 MMAs into an fp32 TMEM accumulator (3xTF32).
+ * b_lo = NULL: B is raw fp32 and is split in shared memory next to A; else b /
+ * b_lo are B's pre-split hi / lo (fq_split_tf32, once at weight load). The K
+ * order depends on (N, K) only: results are bitwise independent of M. */
+int fq_gemm_f32x3(const float* a, int64_t lda, const float* b, const float* b_lo, int64_t ldb,
+                  float* c, int64_t ldc, int64_t M, int64_t N, int64_t K, int accumulate,
+                  const float* bias, const float* residual, int64_t ldr, int act,
+                  fq_stream_t stream);
+
+/* out = LN(a . b^T + bias + residual) in exact mode (fq_gemm_f32x3 operands):
+ * when the plan splits K in 4 and ws >= 4 * M * N * 4 bytes, the K-slice
+ * partials go to ws as slabs summed by fq_splitk_bias_residual_layer_norm in
+ * slice order; else the GEMM (bias + residual fused) then fq_layer_norm. */
+int fq_gemm_f32x3_ln(const float* a, int64_t lda, const float* b, const float* b_lo,
+                     int64_t ldb, const float* bias, const float* res, int64_t ldr,
+                     const float* gamma, const float* beta, double eps, float* out, int64_t ldo,
+                     void* ws, int64_t ws_bytes, int64_t M, int64_t N, int64_t K,
+                     fq_stream_t stream);
+
+/* Weight preparation for fq_gemm_f32x3 (once, at load): hi = tf32(src) (round
+ * to nearest, ties away), lo = tf32(src - hi); src [rows, cols] row-major;
+ * transpose: hi/lo are [cols, rows] (the K-major layout of a [K, N] weight). */
+int fq_split_tf32(const float* src, int64_t rows, int64_t cols, int transpose, float* hi,
+                  float* lo, fq_stream_t stream);
 
 /* Tile width and thread-block-cluster shape (cm x cn CTAs sharing A/B tiles
  * through TMA multicast) the bf16 dispatcher picks for an M x N x K GEMM. */

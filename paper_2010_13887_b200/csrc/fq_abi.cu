@@ -63,6 +63,23 @@ __global__ void cast_bf16_kernel(const float* __restrict__ src, int64_t rows, in
   }
 }
 
+// hi = tf32_rna(x), lo = tf32_rna(x - hi); dst [cols, rows] when transposing.
+__global__ void split_tf32_kernel(const float* __restrict__ src, int64_t rows, int64_t cols,
+                                  int transpose, float* __restrict__ hi, float* __restrict__ lo) {
+  pdl_enter();
+  const int64_t n = rows * cols;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const float x = src[i];
+    uint32_t h, l;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(x));
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(l) : "f"(x - __uint_as_float(h)));
+    const int64_t o = transpose ? (i % cols) * rows + i / cols : i;
+    hi[o] = __uint_as_float(h);
+    lo[o] = __uint_as_float(l);
+  }
+}
+
 int attention_prepare();
 int gemm_tc_prepare();
 }  // namespace fq
@@ -100,6 +117,17 @@ int fq_cast_bf16(const float* src, int64_t rows, int64_t cols, int transpose, vo
   fq::launch_kernel(fq::cast_bf16_kernel, grid, block, 0, fq::as_stream(stream), 1u, 
       src, rows, cols, transpose, reinterpret_cast<__nv_bfloat16*>(dst16));
   return fq::launch_status("fq_cast_bf16");
+}
+
+int fq_split_tf32(const float* src, int64_t rows, int64_t cols, int transpose, float* hi,
+                  float* lo, fq_stream_t stream) {
+  FQ_CHECK_ARG(src && hi && lo && rows > 0 && cols > 0, FQ_ERR_DIMENSION,
+               "fq_split_tf32: bad args");
+  const int64_t n = rows * cols;
+  int grid = (int)((n + 255) / 256 < 148 * 16 ? (n + 255) / 256 : 148 * 16);
+  fq::launch_kernel(fq::split_tf32_kernel, grid, 256, 0, fq::as_stream(stream), 1u, src, rows,
+                    cols, transpose, hi, lo);
+  return fq::launch_status("fq_split_tf32");
 }
 
 }  // extern "C"

@@ -165,6 +165,10 @@ int launch_tc_gemm(const void* a, int64_t lda, const void* b, int64_t ldb, void*
                    int64_t ldc, int64_t M, int64_t N, int64_t K, int accumulate,
                    const float* bias, const float* res, int64_t ldr, int act, cudaStream_t s);
 
+int launch_x3_gemm(const float* a, int64_t lda, const float* b, const float* b_lo, int64_t ldb,
+                   float* c, int64_t ldc, int64_t M, int64_t N, int64_t K, int accumulate,
+                   const float* bias, const float* res, int64_t ldr, int act, cudaStream_t s);
+
 static bool ranges_overlap(const void* a, size_t na, const void* b, size_t nb) {
   const char* pa = (const char*)a;
   const char* pb = (const char*)b;
@@ -194,6 +198,10 @@ int fq_gemm(const void* a, int a_dtype, int64_t lda, const void* b, int b_dtype,
   const size_t cc = ((M - 1) * ldc + N) * ces;
   FQ_CHECK_ARG(!ranges_overlap(c, cc, a, ca) && !ranges_overlap(c, cc, b, cb), FQ_ERR_ALIASING,
                "gemm output overlaps an input buffer");  // tensor.py:173-176
+  if (a_dtype == FQ_F32 && transpose_b && c_dtype == FQ_F32 && lda % 4 == 0 && ldb % 4 == 0 &&
+      ((uintptr_t)a & 15) == 0 && ((uintptr_t)b & 15) == 0 && getenv("FQ_SIMT_GEMM") == nullptr)
+    return launch_x3_gemm((const float*)a, lda, (const float*)b, nullptr, ldb, (float*)c, ldc, M,
+                          N, K, accumulate, bias, residual, ldr, act, as_stream(stream));
   if (a_dtype == FQ_F32) {
     GemmArgs p{};
     p.a = (const float*)a; p.lda = lda;

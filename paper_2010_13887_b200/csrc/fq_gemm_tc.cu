@@ -36,6 +36,18 @@ namespace tc {
 constexpr int BM = 128;
 constexpr int BK = 64;  // 64 bf16 = 128 bytes = one swizzle row
 constexpr int kThreads = 192;
+// OP_X3 (exact fp32 mode, 3xTF32): 2 more warps split each staged fp32 tile
+// (8 warps in all: 320 threads would cap registers at 168, below the
+// epilogue's 128-float row accumulator + chunk registers)
+constexpr int OP_BF16 = 0, OP_X3 = 1;
+constexpr int kThreadsX3 = 256;
+constexpr int kConvThreads = kThreadsX3 - kThreads;
+// OP_X3: K blocks (of 32) per TMEM accumulation chunk, summed in registers
+constexpr int X3_CH = 4;
+template <int OP>
+constexpr int threads_of() { return OP == OP_X3 ? kThreadsX3 : kThreads; }
+template <int OP>
+constexpr int kblock() { return OP == OP_X3 ? 32 : BK; }  // K elements per 128-byte row
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -119,6 +131,61 @@ __device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t adesc, uint64
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
 }
 
+// kind::tf32 instruction descriptor: tf32 x tf32 -> f32, both K-major (K = 8 per MMA).
+__host__ __device__ constexpr uint32_t idesc_tf32(int m, int n) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(n >> 3) << 17) |
+         ((uint32_t)(m >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                         uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+// 3xTF32 product of one 128-byte K block held in shared memory as hi/lo
+// pairs (x = hi + lo, both exactly representable in tf32): per MMA-K step of
+// 8, big += a_hi.b_hi and small += a_hi.b_lo + a_lo.b_hi (the a_lo.b_lo term,
+// 2^-22 relative, is dropped). Two accumulators: the small terms never round
+// against the large partial sum. Issued by one thread.
+__device__ __forceinline__ void mma_x3_block(uint32_t big, uint32_t small, uint32_t a_hi,
+                                             uint32_t a_lo, uint32_t b_hi, uint32_t b_lo,
+                                             uint32_t idesc, bool first) {
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const uint32_t acc = (first && k == 0) ? 0u : 1u;
+    mma_tf32(small, sw128_desc(a_hi + k * 32), sw128_desc(b_lo + k * 32), idesc, acc);
+    mma_tf32(small, sw128_desc(a_lo + k * 32), sw128_desc(b_hi + k * 32), idesc, 1u);
+    mma_tf32(big, sw128_desc(a_hi + k * 32), sw128_desc(b_hi + k * 32), idesc, acc);
+  }
+}
+
+// Split n16 16-byte chunks of fp32 in shared memory in place into their
+// tf32 "hi" part (round to nearest, ties away) and write the remainder, also
+// rounded to tf32, at the same offset in `lo`: x = hi + lo + O(2^-22 |x|).
+// Elementwise, so the 128B-swizzled layout the TMA wrote is preserved.
+__device__ __forceinline__ uint32_t tf32_rna(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ void split_tf32_smem(uint8_t* buf, uint8_t* lo, int n16, int t,
+                                                int nt) {
+  for (int i = t; i < n16; i += nt) {
+    float4 x = *reinterpret_cast<const float4*>(buf + i * 16);
+    uint4 h, l;
+    h.x = tf32_rna(x.x); l.x = tf32_rna(x.x - __uint_as_float(h.x));
+    h.y = tf32_rna(x.y); l.y = tf32_rna(x.y - __uint_as_float(h.y));
+    h.z = tf32_rna(x.z); l.z = tf32_rna(x.z - __uint_as_float(h.z));
+    h.w = tf32_rna(x.w); l.w = tf32_rna(x.w - __uint_as_float(h.w));
+    *reinterpret_cast<uint4*>(buf + i * 16) = h;
+    *reinterpret_cast<uint4*>(lo + i * 16) = l;
+  }
+}
+
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile(
       "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
@@ -143,6 +210,38 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// 16 columns of this warp's 32 TMEM lanes (thread = lane = row).
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+      "%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+        "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// OP_X3: add one TMEM chunk slot (hi.hi at tb, small terms at tb + bn) to the
+// thread's row accumulator: racc = racc + (big + small), RN adds in a fixed order.
+template <int BN>
+__device__ __forceinline__ void x3_add_chunk(float (&racc)[BN], uint32_t tb, bool first) {
+#pragma unroll
+  for (int j = 0; j < BN / 16; ++j) {
+    float vb[16], vs[16];
+    tmem_ld16(tb + j * 16, vb);
+    tmem_ld16(tb + BN + j * 16, vs);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const float t = fadd_rn(vb[i], vs[i]);
+      racc[j * 16 + i] = first ? t : fadd_rn(racc[j * 16 + i], t);
+    }
+  }
+}
+
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
@@ -158,6 +257,7 @@ struct Epi {
   int act;
   unsigned long long* dbg;  // per-CTA [start, end] %globaltimer (profiling only)
   int tstore;  // 1: C through TMA tensor stores (tma_c: 32-row x 128-byte boxes)
+  int b_presplit;  // OP_X3: B arrives as tf32 hi (tma_b) + lo (tma_blo) pairs
 };
 
 // HARS stage-1 statistics computed in the logits GEMM's epilogue (the [rows,
@@ -250,17 +350,31 @@ __device__ __forceinline__ void dbg_stamp(unsigned long long* dbg, int slot) {
 // M-tiles [gm*cm, +cm) x N-tiles [gn*cn, +cn) with the M-group fastest so
 // concurrent clusters share weight tiles in L2. Two TMEM accumulator stages let
 // the epilogue of one tile overlap the MMAs of the next.
-template <int BN, int STAGES, bool HS = false>
-__global__ void __launch_bounds__(kThreads, 1)
+//
+// OP_X3 (exact fp32 mode): A and B are fp32, each K block of 32 elements is one
+// 128-byte swizzle row, and a stage holds [A hi | A lo | B hi | B lo]. The TMA
+// writes raw fp32 A into "A hi" (and raw B into "B hi" unless B arrives
+// pre-split); converter warps 6..7 split it in place into tf32 hi + lo, then
+// the MMA warp issues three kind::tf32 MMAs per K step (mma_x3_block).
+template <int BN, int STAGES, bool HS = false, int OP = OP_BF16>
+__global__ void __launch_bounds__(threads_of<OP>(), 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tma_a,
                    const __grid_constant__ CUtensorMap tma_b, const Epi ep, int M, int N, int K,
-                   int cm, int cn, const HarsEpi he, const __grid_constant__ CUtensorMap tma_c) {
-  constexpr int A_BYTES = BM * BK * 2;
-  constexpr int B_BYTES = BN * BK * 2;
-  constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  // two accumulator stages; the allocation is a power of two >= 32 columns
-  constexpr uint32_t TMEM_COLS = 2 * BN <= 32 ? 32 : 2 * BN <= 64 ? 64 : 2 * BN <= 128 ? 128
-                                 : 2 * BN <= 256 ? 256 : 512;
+                   int cm, int cn, const HarsEpi he, const __grid_constant__ CUtensorMap tma_c,
+                   const __grid_constant__ CUtensorMap tma_blo) {
+  static_assert(OP == OP_BF16 || !HS, "the HARS epilogue is bf16-only");
+  constexpr bool X3 = OP == OP_X3;
+  constexpr int KB = kblock<OP>();
+  constexpr int A_BYTES = BM * 128;
+  constexpr int B_BYTES = BN * 128;
+  constexpr int STAGE_BYTES = X3 ? 2 * (A_BYTES + B_BYTES) : A_BYTES + B_BYTES;
+  constexpr int B_OFF = X3 ? 2 * A_BYTES : A_BYTES;  // B (hi) inside a stage
+  // two accumulator stages (OP_X3: two chunk slots x {hi.hi, small terms});
+  // the allocation is a power of two >= 32 columns
+  constexpr int TCOLS = X3 ? 4 * BN : 2 * BN;
+  static_assert(TCOLS <= 512, "TMEM holds 512 columns");
+  constexpr uint32_t TMEM_COLS = TCOLS <= 32 ? 32 : TCOLS <= 64 ? 64 : TCOLS <= 128 ? 128
+                                 : TCOLS <= 256 ? 256 : 512;
   extern __shared__ uint8_t smem_raw[];
   // 1024-B aligned (128B-swizzle atoms); identical offset in every CTA, so a
   // multicast lands at the same place cluster-wide. Pointer arithmetic keeps
@@ -272,6 +386,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __shared__ __align__(8) uint64_t tfull_bar[2];
   __shared__ __align__(8) uint64_t tempty_bar[2];
   __shared__ __align__(8) uint64_t edone_bar;  // the 4 epilogue warps finished with TMEM
+  __shared__ __align__(8) uint64_t conv_bar[X3 ? STAGES : 1];  // stage split (OP_X3)
   __shared__ uint32_t tmem_base_sh;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -280,7 +395,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int csize = cm * cn;
   const int rank = csize > 1 ? (int)cluster_rank() : 0;
   const int ry = rank / cn, rx = rank % cn;
-  const int num_kb = (K + BK - 1) / BK;
+  const int num_kb = (K + KB - 1) / KB;
+  // bytes one stage's TMA loads deliver
+  const uint32_t tx_bytes = X3 ? A_BYTES + (ep.b_presplit ? 2 : 1) * B_BYTES : STAGE_BYTES;
   const int mt = (M + BM - 1) / BM, nt = (N + BN - 1) / BN;
   const int mg = mt / cm;                     // cm | mt and cn | nt (host guarantees)
   const int ngroups = mg * (nt / cn);
@@ -300,6 +417,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&tempty_bar[s], 4);  // one arrive per epilogue warp
     }
     mbar_init(&edone_bar, 4);
+    if constexpr (X3)
+      for (int s = 0; s < STAGES; ++s) mbar_init(&conv_bar[s], kConvThreads / 32);  // one per converter warp
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tma_a)));
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tma_b)));
@@ -328,8 +447,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         npre = num_kb < STAGES ? num_kb : STAGES;
         for (int kb = 0; kb < npre; ++kb) {
           uint8_t* sa = smem + kb * STAGE_BYTES;
-          mbar_expect_tx(&full_bar[kb], STAGE_BYTES);
-          tma_load_2d(&tma_b, &full_bar[kb], sa + A_BYTES, kb * BK, n0);
+          mbar_expect_tx(&full_bar[kb], tx_bytes);
+          tma_load_2d(&tma_b, &full_bar[kb], sa + B_OFF, kb * KB, n0);
+          if (X3 && ep.b_presplit)
+            tma_load_2d(&tma_blo, &full_bar[kb], sa + B_OFF + B_BYTES, kb * KB, n0);
         }
       }
       pdl_wait();  // activations (A) are written by the previous kernel
@@ -341,21 +462,23 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t ph = (it / STAGES) & 1;
           uint8_t* sa = smem + s * STAGE_BYTES;
           if (it < npre) {  // B already in flight
-            tma_load_2d(&tma_a, &full_bar[s], sa, kb * BK, m0);
+            tma_load_2d(&tma_a, &full_bar[s], sa, kb * KB, m0);
             continue;
           }
           mbar_wait(&empty_bar[s], ph ^ 1);  // free in every CTA I multicast into
-          mbar_expect_tx(&full_bar[s], STAGE_BYTES);
+          mbar_expect_tx(&full_bar[s], tx_bytes);
           if (cn > 1)
-            tma_load_2d_mc(&tma_a, &full_bar[s], sa + rx * a_rows * 128, kb * BK,
+            tma_load_2d_mc(&tma_a, &full_bar[s], sa + rx * a_rows * 128, kb * KB,
                            m0 + rx * a_rows, row_mask);
           else
-            tma_load_2d(&tma_a, &full_bar[s], sa, kb * BK, m0);
+            tma_load_2d(&tma_a, &full_bar[s], sa, kb * KB, m0);
           if (cm > 1)
-            tma_load_2d_mc(&tma_b, &full_bar[s], sa + A_BYTES + ry * b_rows * 128, kb * BK,
+            tma_load_2d_mc(&tma_b, &full_bar[s], sa + B_OFF + ry * b_rows * 128, kb * KB,
                            n0 + ry * b_rows, col_mask);
           else
-            tma_load_2d(&tma_b, &full_bar[s], sa + A_BYTES, kb * BK, n0);
+            tma_load_2d(&tma_b, &full_bar[s], sa + B_OFF, kb * KB, n0);
+          if (X3 && ep.b_presplit)
+            tma_load_2d(&tma_blo, &full_bar[s], sa + B_OFF + B_BYTES, kb * KB, n0);
         }
       }
       // drain: every peer's release of my last fills has landed before teardown
@@ -363,9 +486,33 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp == 1) {
     if (lane == 0) {  // ---- MMA issuer ----
-      constexpr uint32_t idesc = idesc_bf16(BM, BN);
+      constexpr uint32_t idesc = X3 ? idesc_tf32(BM, BN) : idesc_bf16(BM, BN);
       int it = 0, local = 0;
-      for (int g = cluster_id; g < ngroups; g += nclusters, ++local) {
+      if constexpr (X3) {  // chunks of X3_CH K blocks into ping-pong TMEM slots
+        int gc = 0;
+        for (int g = cluster_id; g < ngroups; g += nclusters) {
+          for (int kb0 = 0; kb0 < num_kb; kb0 += X3_CH, ++gc) {
+            const int slot = gc & 1;
+            mbar_wait(&tempty_bar[slot], ((gc >> 1) & 1) ^ 1);  // epilogue read the slot
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const uint32_t big = tmem + slot * 2 * BN;
+            const int kb1 = min(num_kb, kb0 + X3_CH);
+            for (int kb = kb0; kb < kb1; ++kb, ++it) {
+              const int s = it % STAGES;
+              mbar_wait(&conv_bar[s], (it / STAGES) & 1);
+              if (it == 0) dbg_stamp(ep.dbg, 2);
+              asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+              const uint32_t a_base = smem_u32(smem + s * STAGE_BYTES);
+              const uint32_t b_base = a_base + B_OFF;
+              mma_x3_block(big, big + BN, a_base, a_base + A_BYTES, b_base, b_base + B_BYTES,
+                           idesc, kb == kb0);
+              mma_commit(&empty_bar[s]);
+            }
+            mma_commit(&tfull_bar[slot]);
+          }
+        }
+      }
+      for (int g = cluster_id; g < ngroups && !X3; g += nclusters, ++local) {
         const int as = local & 1;
         mbar_wait(&tempty_bar[as], ((local >> 1) & 1) ^ 1);  // epilogue drained this stage
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -373,11 +520,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int kb = 0; kb < num_kb; ++kb, ++it) {
           const int s = it % STAGES;
           const uint32_t ph = (it / STAGES) & 1;
-          mbar_wait(&full_bar[s], ph);
+          mbar_wait(X3 ? &conv_bar[s] : &full_bar[s], ph);
           if (it == 0) dbg_stamp(ep.dbg, 2);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           const uint32_t a_base = smem_u32(smem + s * STAGE_BYTES);
-          const uint32_t b_base = a_base + A_BYTES;
+          const uint32_t b_base = a_base + B_OFF;
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k) {
             mma_bf16(acc, sw128_desc(a_base + k * 32), sw128_desc(b_base + k * 32), idesc,
@@ -391,6 +538,22 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (local == 0) dbg_stamp(ep.dbg, 3);  // first tile's MMAs issued
       }
       dbg_stamp(ep.dbg, 7);  // every tile's MMAs issued
+    }
+  } else if (X3 && warp >= 6) {  // ---- converter: fp32 stage -> tf32 hi + lo ----
+    const int t = threadIdx.x - 192;
+    int it = 0;
+    for (int g = cluster_id; g < ngroups; g += nclusters) {
+      for (int kb = 0; kb < num_kb; ++kb, ++it) {
+        const int s = it % STAGES;
+        mbar_wait(&full_bar[s], (it / STAGES) & 1);
+        uint8_t* sa = smem + s * STAGE_BYTES;
+        split_tf32_smem(sa, sa + A_BYTES, A_BYTES / 16, t, kConvThreads);
+        if (!ep.b_presplit)
+          split_tf32_smem(sa + B_OFF, sa + B_OFF + B_BYTES, B_BYTES / 16, t, kConvThreads);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // visible to the MMA
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&conv_bar[s]);
+      }
     }
   } else if constexpr (HS) {  // ---- HARS statistics epilogue (thread = row) ----
     pdl_wait();  // the group counts / running maxima come from the previous kernel
@@ -530,7 +693,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     float* st = stage_out + (warp - 2) * 32 * 33;
     float* c32 = reinterpret_cast<float*>(ep.c);
     __nv_bfloat16* c16 = reinterpret_cast<__nv_bfloat16*>(ep.c);
-    int local = 0;
+    int local = 0, gc = 0;
     for (int g = cluster_id; g < ngroups; g += nclusters, ++local) {
       const int as = local & 1;
       const int m0 = ((g % mg) * cm + ry) * BM, n0 = ((g / mg) * cn + rx) * BN;
@@ -543,20 +706,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int bc = n0 + j * 32 + lane;
         bpre[j] = (ep.bias && bc < N) ? __ldg(ep.bias + bc) : 0.0f;
       }
-      mbar_wait(&tfull_bar[as], (local >> 1) & 1);
-      if (local == 0 && threadIdx.x == 64) dbg_stamp(ep.dbg, 4);
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const int rbase = m0 + q * 32;
       const int nrows = min(32, M - rbase);
-#pragma unroll 1
-      for (int cc = 0; cc < BN; cc += 32) {
-        float v[32];
-        tmem_ld32(tmem + as * BN + ((uint32_t)(q * 32) << 16) + cc, v);
-        if (cc + 32 >= BN) {  // last TMEM read of this stage: hand it back to the MMA warp
-          asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&tempty_bar[as]);
-        }
+      // one 32-column chunk of this thread's row (thread = row): fused
+      // epilogue and store
+      auto store_chunk = [&](float (&v)[32], const int cc) {
         if (ep.tstore) {
           // thread = row: epilogue math on the tcgen05.ld registers, the
           // 32 x 32 chunk written swizzled into this warp's 4 KB box area
@@ -613,7 +767,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             __syncwarp();
             if (lane == 0) tma_store_2d(&tma_c, box, col0, rbase);
           }
-          continue;
+          return;
         }
         // transpose through smem: thread = row on the TMEM side, column on the store side
 #pragma unroll
@@ -671,17 +825,57 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
         __syncwarp();  // staging free for the next chunk
+      };
+      if constexpr (X3) {
+        // the tile's K chunks (X3_CH K blocks each, ping-pong TMEM slots): per
+        // chunk the hi.hi and the small-term accumulators are read and added
+        // to this thread's row in registers with IEEE round-to-nearest adds
+        // (the tensor core's own long accumulation is not RN: this bounds it
+        // to X3_CH * 32 K elements)
+        float racc[BN];
+        for (int kb0 = 0; kb0 < num_kb; kb0 += X3_CH, ++gc) {
+          const int slot = gc & 1;
+          mbar_wait(&tfull_bar[slot], (gc >> 1) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          x3_add_chunk<BN>(racc, tmem + slot * 2 * BN + ((uint32_t)(q * 32) << 16), kb0 == 0);
+          asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tempty_bar[slot]);
+        }
+        if (local == 0 && threadIdx.x == 64) dbg_stamp(ep.dbg, 4);
+#pragma unroll
+        for (int j = 0; j < BN / 32; ++j) {
+          float v[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = racc[j * 32 + i];
+          store_chunk(v, j * 32);
+        }
+      } else {
+        mbar_wait(&tfull_bar[as], (local >> 1) & 1);
+        if (local == 0 && threadIdx.x == 64) dbg_stamp(ep.dbg, 4);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll 1
+        for (int cc = 0; cc < BN; cc += 32) {
+          float v[32];
+          tmem_ld32(tmem + as * BN + ((uint32_t)(q * 32) << 16) + cc, v);
+          if (cc + 32 >= BN) {  // last TMEM read of this stage: hand it back to the MMA warp
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty_bar[as]);
+          }
+          store_chunk(v, cc);
+        }
       }
     }
   }
   if constexpr (!HS) {  // TMA stores complete (smem read, writes performed) before exit
-    if (ep.tstore && warp >= 2 && lane == 0)
+    if (ep.tstore && warp >= 2 && warp < 6 && lane == 0)
       asm volatile("cp.async.bulk.wait_group %0;" ::"n"(0) : "memory");
   }
   if (threadIdx.x == 64) dbg_stamp(ep.dbg, 5);  // epilogue done
   __syncwarp();
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  if (warp >= 2 && lane == 0) mbar_arrive(&edone_bar);
+  if (warp >= 2 && warp < 6 && lane == 0) mbar_arrive(&edone_bar);
   if (csize > 1) cluster_sync_all();  // no CTA leaves while peers may still signal it
   else __syncthreads();
   if (threadIdx.x == 0) dbg_stamp(ep.dbg, 6);
@@ -726,16 +920,24 @@ __device__ __forceinline__ float4 ld_dsmem_f4(uint32_t local_addr, uint32_t rank
 // partial tile to slab s of ep.c ([S][M][ldc], plain coalesced stores) and the
 // consumer (fq_splitk_bias_residual_layer_norm) sums the S slabs in split
 // order, so the result is bit-identical to the DSMEM reduction's.
-template <int BN, int STAGES, bool LNF = false, bool SLAB = false>
-__global__ void __launch_bounds__(kThreads, 1)
+// OP_X3: the exact-mode 3xTF32 operands (see tc_gemm_kernel).
+template <int BN, int STAGES, bool LNF = false, bool SLAB = false, int OP = OP_BF16>
+__global__ void __launch_bounds__(threads_of<OP>(), 1)
     tc_gemm_splitk_kernel(const __grid_constant__ CUtensorMap tma_a,
                           const __grid_constant__ CUtensorMap tma_b, const Epi ep, int M, int N,
                           int K, int kb_per_split, const LnEpi ln, int nsplit,
-                          const __grid_constant__ CUtensorMap tma_c) {
-  constexpr int A_BYTES = BM * BK * 2;
-  constexpr int B_BYTES = BN * BK * 2;
-  constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  constexpr uint32_t TMEM_COLS = BN < 32 ? 32 : BN;
+                          const __grid_constant__ CUtensorMap tma_c,
+                          const __grid_constant__ CUtensorMap tma_blo) {
+  static_assert(OP == OP_BF16 || !LNF, "the in-kernel LN is bf16-only");
+  constexpr bool X3 = OP == OP_X3;
+  constexpr int KB = kblock<OP>();
+  constexpr int A_BYTES = BM * 128;
+  constexpr int B_BYTES = BN * 128;
+  constexpr int STAGE_BYTES = X3 ? 2 * (A_BYTES + B_BYTES) : A_BYTES + B_BYTES;
+  constexpr int B_OFF = X3 ? 2 * A_BYTES : A_BYTES;
+  // OP_X3: two chunk slots x {hi.hi, small terms} (see tc_gemm_kernel)
+  constexpr uint32_t TMEM_COLS = X3 ? 4 * BN : (BN < 32 ? 32 : BN);
+  static_assert(TMEM_COLS <= 512, "TMEM holds 512 columns");
   constexpr int PLD = BN + 4;  // padded partial row (floats): conflict-free v4 rows
   static_assert(BM * PLD * 4 <= STAGES * STAGE_BYTES, "partial tile must fit the ring");
   extern __shared__ uint8_t smem_raw[];
@@ -744,6 +946,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   __shared__ __align__(8) uint64_t full_bar[STAGES];
   __shared__ __align__(8) uint64_t empty_bar[STAGES];
   __shared__ __align__(8) uint64_t tfull_bar;
+  __shared__ __align__(8) uint64_t conv_bar[X3 ? STAGES : 1];
+  __shared__ __align__(8) uint64_t xfull_bar[2], xempty_bar[2];  // OP_X3 chunk slots
   __shared__ uint32_t tmem_base_sh;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -754,7 +958,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int mt = (M + BM - 1) / BM;
   const int tile = blockIdx.x / S;
   const int m0 = (tile % mt) * BM, n0 = (tile / mt) * BN;
-  const int num_kb = (K + BK - 1) / BK;
+  const int num_kb = (K + KB - 1) / KB;
+  const uint32_t tx_bytes = X3 ? A_BYTES + (ep.b_presplit ? 2 : 1) * B_BYTES : STAGE_BYTES;
   const int kb0 = rank * kb_per_split;
   const int kb1 = min(num_kb, kb0 + kb_per_split);
 
@@ -762,8 +967,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full_bar[s], 1);
       mbar_init(&empty_bar[s], 1);
+      if constexpr (X3) mbar_init(&conv_bar[s], kConvThreads / 32);
     }
     mbar_init(&tfull_bar, 1);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&xfull_bar[s], 1);
+      mbar_init(&xempty_bar[s], 4);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tma_a)));
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tma_b)));
@@ -785,55 +995,119 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int npre = (kb1 - kb0) < STAGES ? (kb1 - kb0) : STAGES;
       for (int it = 0; it < npre; ++it) {
         uint8_t* sa = smem + it * STAGE_BYTES;
-        mbar_expect_tx(&full_bar[it], STAGE_BYTES);
-        tma_load_2d(&tma_b, &full_bar[it], sa + A_BYTES, (kb0 + it) * BK, n0);
+        mbar_expect_tx(&full_bar[it], tx_bytes);
+        tma_load_2d(&tma_b, &full_bar[it], sa + B_OFF, (kb0 + it) * KB, n0);
+        if (X3 && ep.b_presplit)
+          tma_load_2d(&tma_blo, &full_bar[it], sa + B_OFF + B_BYTES, (kb0 + it) * KB, n0);
       }
       pdl_wait();
       for (int kb = kb0, it = 0; kb < kb1; ++kb, ++it) {
         const int s = it % STAGES;
         uint8_t* sa = smem + s * STAGE_BYTES;
         if (it < npre) {
-          tma_load_2d(&tma_a, &full_bar[s], sa, kb * BK, m0);
+          tma_load_2d(&tma_a, &full_bar[s], sa, kb * KB, m0);
           continue;
         }
         mbar_wait(&empty_bar[s], ((it / STAGES) & 1) ^ 1);
-        mbar_expect_tx(&full_bar[s], STAGE_BYTES);
-        tma_load_2d(&tma_a, &full_bar[s], sa, kb * BK, m0);
-        tma_load_2d(&tma_b, &full_bar[s], sa + A_BYTES, kb * BK, n0);
+        mbar_expect_tx(&full_bar[s], tx_bytes);
+        tma_load_2d(&tma_a, &full_bar[s], sa, kb * KB, m0);
+        tma_load_2d(&tma_b, &full_bar[s], sa + B_OFF, kb * KB, n0);
+        if (X3 && ep.b_presplit)
+          tma_load_2d(&tma_blo, &full_bar[s], sa + B_OFF + B_BYTES, kb * KB, n0);
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {  // ---- MMA issuer ----
-      constexpr uint32_t idesc = idesc_bf16(BM, BN);
-      for (int kb = kb0, it = 0; kb < kb1; ++kb, ++it) {
-        const int s = it % STAGES;
-        mbar_wait(&full_bar[s], (it / STAGES) & 1);
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint32_t a_base = smem_u32(smem + s * STAGE_BYTES);
-        const uint32_t b_base = a_base + A_BYTES;
+      constexpr uint32_t idesc = X3 ? idesc_tf32(BM, BN) : idesc_bf16(BM, BN);
+      if constexpr (X3) {  // chunks of X3_CH K blocks into ping-pong TMEM slots
+        int it = 0, gc = 0;
+        for (int c0 = kb0; c0 < kb1; c0 += X3_CH, ++gc) {
+          const int slot = gc & 1;
+          mbar_wait(&xempty_bar[slot], ((gc >> 1) & 1) ^ 1);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t big = tmem + slot * 2 * BN;
+          for (int kb = c0; kb < min(kb1, c0 + X3_CH); ++kb, ++it) {
+            const int s = it % STAGES;
+            mbar_wait(&conv_bar[s], (it / STAGES) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const uint32_t a_base = smem_u32(smem + s * STAGE_BYTES);
+            const uint32_t b_base = a_base + B_OFF;
+            mma_x3_block(big, big + BN, a_base, a_base + A_BYTES, b_base, b_base + B_BYTES,
+                         idesc, kb == c0);
+            mma_commit(&empty_bar[s]);
+          }
+          mma_commit(&xfull_bar[slot]);
+        }
+      } else {
+        for (int kb = kb0, it = 0; kb < kb1; ++kb, ++it) {
+          const int s = it % STAGES;
+          mbar_wait(&full_bar[s], (it / STAGES) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t a_base = smem_u32(smem + s * STAGE_BYTES);
+          const uint32_t b_base = a_base + B_OFF;
 #pragma unroll
-        for (int k = 0; k < BK / 16; ++k)
-          mma_bf16(tmem, sw128_desc(a_base + k * 32), sw128_desc(b_base + k * 32), idesc,
-                   (it | k) != 0);
-        mma_commit(&empty_bar[s]);
+          for (int k = 0; k < BK / 16; ++k)
+            mma_bf16(tmem, sw128_desc(a_base + k * 32), sw128_desc(b_base + k * 32), idesc,
+                     (it | k) != 0);
+          mma_commit(&empty_bar[s]);
+        }
+        mma_commit(&tfull_bar);
       }
-      mma_commit(&tfull_bar);
+    }
+  } else if (X3 && warp >= 6) {  // ---- converter: fp32 stage -> tf32 hi + lo ----
+    const int t = threadIdx.x - 192;
+    for (int kb = kb0, it = 0; kb < kb1; ++kb, ++it) {
+      const int s = it % STAGES;
+      mbar_wait(&full_bar[s], (it / STAGES) & 1);
+      uint8_t* sa = smem + s * STAGE_BYTES;
+      split_tf32_smem(sa, sa + A_BYTES, A_BYTES / 16, t, kConvThreads);
+      if (!ep.b_presplit)
+        split_tf32_smem(sa + B_OFF, sa + B_OFF + B_BYTES, B_BYTES / 16, t, kConvThreads);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&conv_bar[s]);
     }
   } else {  // ---- epilogue warps: TMEM partial -> own smem [128][PLD] ----
     pdl_wait();
     const int q = warp & 3;
-    mbar_wait(&tfull_bar, 0);
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    // OP_X3: the K slice's chunks summed in registers (RN adds, fixed order)
+    float racc[X3 ? BN : 1];
+    if constexpr (X3) {
+#pragma unroll
+      for (int i = 0; i < BN; ++i) racc[i] = 0.0f;
+      int gc = 0;
+      for (int c0 = kb0; c0 < kb1; c0 += X3_CH, ++gc) {
+        const int slot = gc & 1;
+        mbar_wait(&xfull_bar[slot], (gc >> 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        x3_add_chunk<X3 ? BN : 1>(racc, tmem + slot * 2 * BN + ((uint32_t)(q * 32) << 16),
+                                  c0 == kb0);
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&xempty_bar[slot]);
+      }
+    } else {
+      mbar_wait(&tfull_bar, 0);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    }
+    auto acc_chunk = [&](float (&v)[32], const int cc) {
+      if constexpr (X3) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = racc[(cc + i) % (X3 ? BN : 1)];
+      } else {
+        tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + cc, v);
+      }
+    };
     float* prow = part + (q * 32 + lane) * PLD;
     if constexpr (SLAB) {
       if (ep.tstore) {
         // slab tile straight from TMEM through TMA tensor stores: per warp and
         // 32-column chunk one swizzled 32 x 128 B box in the (idle) ring, rows
         // rank * M + m0 + q * 32 of the [S * M, N] slab map
-#pragma unroll 1
+#pragma unroll
         for (int cc = 0; cc < BN; cc += 32) {
           float v[32];
-          tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + cc, v);
+          acc_chunk(v, cc);
           uint8_t* box = smem + q * (BN / 32) * 4096 + (cc / 32) * 4096;
 #pragma unroll
           for (int j = 0; j < 8; ++j)
@@ -848,10 +1122,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         __syncwarp();
       }
     }
-#pragma unroll 1
-    for (int cc = 0; cc < BN && !(SLAB && ep.tstore); cc += 32) {
+#pragma unroll
+    for (int cc = 0; cc < BN; cc += 32) {
+      if (SLAB && ep.tstore) break;
       float v[32];
-      tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + cc, v);
+      acc_chunk(v, cc);
 #pragma unroll
       for (int j = 0; j < 32; j += 4)
         *reinterpret_cast<float4*>(prow + cc + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
@@ -888,7 +1163,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   cluster_sync_all();  // every partial tile of the cluster is in shared memory
 
-  if (warp >= 2) {  // ---- reduce my row slice over the S partials, fused epilogue ----
+  if (warp >= 2 && warp < 6) {  // ---- reduce my row slice over the S partials, fused epilogue ----
     const int t = threadIdx.x - 64;  // 0..127
     const int rows_per = (BM + S - 1) / S;          // S need not divide 128
     const int r_lo = rank * rows_per;
@@ -1073,14 +1348,19 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
-template <int BN, int STAGES>
-constexpr int smem_bytes_splitk() {
-  return STAGES * (BM * BK * 2 + BN * BK * 2) + 1024;
+template <int BN, int OP>
+constexpr int stage_bytes() {
+  return (OP == OP_X3 ? 2 : 1) * (BM * 128 + BN * 128);
 }
 
-template <int BN, int STAGES, bool HS = false>
+template <int BN, int STAGES, int OP = OP_BF16>
+constexpr int smem_bytes_splitk() {
+  return STAGES * stage_bytes<BN, OP>() + 1024;
+}
+
+template <int BN, int STAGES, bool HS = false, int OP = OP_BF16>
 constexpr int smem_bytes() {
-  return STAGES * (BM * BK * 2 + BN * BK * 2) + (HS ? 8 : 4) * 32 * 33 * 4 + 1024;
+  return STAGES * stage_bytes<BN, OP>() + (HS ? 8 : 4) * 32 * 33 * 4 + 1024;
 }
 
 using EncodeFn = PFN_cuTensorMapEncodeTiled_v12000;
@@ -1098,20 +1378,23 @@ static EncodeFn get_encode() {
   return fn;
 }
 
-// 2D bf16 map over a row-major [rows, cols] matrix with leading dim ld, box
-// [box_rows, 64] with 128-byte swizzle; out-of-bounds elements read as zero.
+// 2D map over a row-major [rows, cols] matrix with leading dim ld, box
+// [box_rows, one 128-byte row] (64 bf16 / 32 fp32) with 128-byte swizzle;
+// out-of-bounds elements read as zero.
 static int make_map(CUtensorMap* map, const void* ptr, int64_t rows, int64_t cols, int64_t ld,
-                    int box_rows) {
+                    int box_rows, bool f32 = false) {
   EncodeFn enc = get_encode();
   if (!enc) {
     set_error("cuTensorMapEncodeTiled unavailable");
     return FQ_ERR_CUDA;
   }
+  const int es = f32 ? 4 : 2;
   cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
-  cuuint64_t strides[1] = {(cuuint64_t)(ld * 2)};
-  cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)box_rows};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * es)};
+  cuuint32_t box[2] = {(cuuint32_t)(128 / es), (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides,
+  CUresult r = enc(map, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
+                   2, const_cast<void*>(ptr), dims, strides,
                    box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
@@ -1188,16 +1471,20 @@ static int num_sms() {
   return n;
 }
 
-template <int BN, int STAGES, bool HS = false>
+template <int BN, int STAGES, bool HS = false, int OP = OP_BF16>
 static int launch(const void* a, int64_t lda, const void* b, int64_t ldb, const Epi& ep,
                   int64_t M, int64_t N, int64_t K, int cm, int cn, cudaStream_t s,
-                  const HarsEpi& he = HarsEpi{}) {
-  CUtensorMap ma, mb, mc;
+                  const HarsEpi& he = HarsEpi{}, const void* b_lo = nullptr) {
+  constexpr bool X3 = OP == OP_X3;
+  CUtensorMap ma, mb, mc, mblo;
   int rc;
-  if ((rc = make_map(&ma, a, M, K, lda, BM / cn)) != FQ_OK) return rc;
-  if ((rc = make_map(&mb, b, N, K, ldb, BN / cm)) != FQ_OK) return rc;
+  if ((rc = make_map(&ma, a, M, K, lda, BM / cn, X3)) != FQ_OK) return rc;
+  if ((rc = make_map(&mb, b, N, K, ldb, BN / cm, X3)) != FQ_OK) return rc;
   Epi e2 = ep;
   e2.tstore = 0;
+  e2.b_presplit = X3 && b_lo != nullptr;
+  mblo = mb;
+  if (e2.b_presplit && (rc = make_map(&mblo, b_lo, N, K, ldb, BN / cm, true)) != FQ_OK) return rc;
   mc = ma;
   if (!HS && ep.c && !ep.accumulate && !ep.res && N % 32 == 0 && tma_store_enabled() &&
       ((uintptr_t)ep.c & 15) == 0 && (ep.ldc * (ep.c_bf16 ? 2 : 4)) % 16 == 0 &&
@@ -1207,10 +1494,10 @@ static int launch(const void* a, int64_t lda, const void* b, int64_t ldb, const 
   const int64_t groups = ((M + BM - 1) / BM / cm) * ((N + BN - 1) / BN / cn);
   const int64_t max_clusters = num_sms() / csize;
   const int64_t clusters = groups < max_clusters ? groups : max_clusters;
-  cudaError_t e = launch_kernel(tc_gemm_kernel<BN, STAGES, HS>,
-                                dim3((unsigned)(clusters * csize)), dim3(kThreads),
-                                smem_bytes<BN, STAGES, HS>(), s, (unsigned)csize, ma, mb, e2,
-                                (int)M, (int)N, (int)K, cm, cn, he, mc);
+  cudaError_t e = launch_kernel(tc_gemm_kernel<BN, STAGES, HS, OP>,
+                                dim3((unsigned)(clusters * csize)), dim3(threads_of<OP>()),
+                                smem_bytes<BN, STAGES, HS, OP>(), s, (unsigned)csize, ma, mb, e2,
+                                (int)M, (int)N, (int)K, cm, cn, he, mc, mblo);
   if (e != cudaSuccess) {
     set_error("fq_gemm(tcgen05): launch failed: %s", cudaGetErrorString(e));
     return FQ_ERR_CUDA;
@@ -1218,27 +1505,31 @@ static int launch(const void* a, int64_t lda, const void* b, int64_t ldb, const 
   return launch_status("fq_gemm(tcgen05)");
 }
 
-template <int BN, int STAGES, bool LNF = false, bool SLAB = false>
+template <int BN, int STAGES, bool LNF = false, bool SLAB = false, int OP = OP_BF16>
 static int launch_splitk(const void* a, int64_t lda, const void* b, int64_t ldb, const Epi& ep,
                          int64_t M, int64_t N, int64_t K, int S, cudaStream_t s,
-                         const LnEpi& ln = LnEpi{}) {
-  CUtensorMap ma, mb, mc;
+                         const LnEpi& ln = LnEpi{}, const void* b_lo = nullptr) {
+  constexpr bool X3 = OP == OP_X3;
+  CUtensorMap ma, mb, mc, mblo;
   int rc;
-  if ((rc = make_map(&ma, a, M, K, lda, BM)) != FQ_OK) return rc;
-  if ((rc = make_map(&mb, b, N, K, ldb, BN)) != FQ_OK) return rc;
+  if ((rc = make_map(&ma, a, M, K, lda, BM, X3)) != FQ_OK) return rc;
+  if ((rc = make_map(&mb, b, N, K, ldb, BN, X3)) != FQ_OK) return rc;
   Epi e2 = ep;
   e2.tstore = 0;
+  e2.b_presplit = X3 && b_lo != nullptr;
+  mblo = mb;
+  if (e2.b_presplit && (rc = make_map(&mblo, b_lo, N, K, ldb, BN, true)) != FQ_OK) return rc;
   mc = ma;
   if (SLAB && M % 32 == 0 && N % 32 == 0 && tma_store_enabled() && ((uintptr_t)ep.c & 15) == 0 &&
       (ep.ldc * 4) % 16 == 0 && make_map_c(&mc, ep.c, S * M, N, ep.ldc, false) == FQ_OK)
     e2.tstore = 1;
   const int64_t tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
-  const int nkb = (int)((K + BK - 1) / BK);
+  const int nkb = (int)((K + kblock<OP>() - 1) / kblock<OP>());
   const int kbs = (nkb + S - 1) / S;
-  cudaError_t e = launch_kernel(tc_gemm_splitk_kernel<BN, STAGES, LNF, SLAB>,
-                                dim3((unsigned)(tiles * S)), dim3(kThreads),
-                                smem_bytes_splitk<BN, STAGES>(), s, SLAB ? 1u : (unsigned)S, ma,
-                                mb, e2, (int)M, (int)N, (int)K, kbs, ln, S, mc);
+  cudaError_t e = launch_kernel(tc_gemm_splitk_kernel<BN, STAGES, LNF, SLAB, OP>,
+                                dim3((unsigned)(tiles * S)), dim3(threads_of<OP>()),
+                                smem_bytes_splitk<BN, STAGES, OP>(), s, SLAB ? 1u : (unsigned)S, ma,
+                                mb, e2, (int)M, (int)N, (int)K, kbs, ln, S, mc, mblo);
   if (e != cudaSuccess) {
     set_error("fq_gemm(tcgen05 split-K): launch failed: %s", cudaGetErrorString(e));
     return FQ_ERR_CUDA;
@@ -1246,20 +1537,20 @@ static int launch_splitk(const void* a, int64_t lda, const void* b, int64_t ldb,
   return launch_status("fq_gemm(tcgen05 split-K)");
 }
 
-template <int BN, int STAGES, bool LNF = false, bool SLAB = false>
+template <int BN, int STAGES, bool LNF = false, bool SLAB = false, int OP = OP_BF16>
 static int prep_splitk() {
-  return cudaFuncSetAttribute(tc_gemm_splitk_kernel<BN, STAGES, LNF, SLAB>,
+  return cudaFuncSetAttribute(tc_gemm_splitk_kernel<BN, STAGES, LNF, SLAB, OP>,
                               cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              smem_bytes_splitk<BN, STAGES>()) == cudaSuccess
+                              smem_bytes_splitk<BN, STAGES, OP>()) == cudaSuccess
              ? FQ_OK
              : FQ_ERR_CUDA;
 }
 
-template <int BN, int STAGES, bool HS = false>
+template <int BN, int STAGES, bool HS = false, int OP = OP_BF16>
 static int prep() {
-  return cudaFuncSetAttribute(tc_gemm_kernel<BN, STAGES, HS>,
+  return cudaFuncSetAttribute(tc_gemm_kernel<BN, STAGES, HS, OP>,
                               cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              smem_bytes<BN, STAGES, HS>()) == cudaSuccess
+                              smem_bytes<BN, STAGES, HS, OP>()) == cudaSuccess
              ? FQ_OK
              : FQ_ERR_CUDA;
 }
@@ -1272,7 +1563,10 @@ int gemm_tc_prepare() {
       tc::prep<224, 4, true>() ||
       tc::prep<64, 8>() || tc::prep<32, 8>() ||
       tc::prep_splitk<256, 4>() || tc::prep_splitk<128, 6>() || tc::prep_splitk<64, 8>() ||
-      tc::prep_splitk<128, 6, true>() || tc::prep_splitk<128, 6, false, true>()) {
+      tc::prep_splitk<128, 6, true>() || tc::prep_splitk<128, 6, false, true>() ||
+      tc::prep<128, 3, false, tc::OP_X3>() || tc::prep<64, 4, false, tc::OP_X3>() ||
+      tc::prep_splitk<128, 3, false, false, tc::OP_X3>() ||
+      tc::prep_splitk<128, 3, false, true, tc::OP_X3>()) {
     set_error("fq_prepare: tcgen05 GEMM smem opt-in failed");
     return FQ_ERR_CUDA;
   }
@@ -1357,6 +1651,99 @@ int launch_tc_gemm(const void* a, int64_t lda, const void* b, int64_t ldb, void*
     case 64: return tc::launch<64, 8>(a, lda, b, ldb, ep, M, N, K, p.cm, p.cn, s);
     default: return tc::launch<32, 8>(a, lda, b, ldb, ep, M, N, K, p.cm, p.cn, s);
   }
+}
+
+// ---------------------------------------------------------------------------
+// Exact fp32 mode on the tensor cores (3xTF32, OP_X3). The plan is a function
+// of (N, K) only — never of M — so every output element sees the same K
+// reduction order whatever the batch (bitwise invariant to batch sharding):
+// sequential K through one TMEM accumulator, or for N <= 1024 with K >= 1024
+// four K slices summed in slice order (DSMEM cluster reduction, or slabs summed
+// by the consumer).
+struct X3Plan {
+  int bn, split;
+};
+
+static X3Plan plan_x3(int64_t N, int64_t K) {
+  const int64_t nkb = (K + 31) / 32;
+  if (N <= 1024 && nkb >= 32) return {128, 4};
+  if (N <= 512) return {64, 1};
+  return {128, 1};
+}
+
+static int check_x3(const void* a, int64_t lda, const void* b, const void* b_lo, int64_t ldb,
+                    int64_t M, int64_t N, int64_t K) {
+  FQ_CHECK_ARG(lda % 4 == 0 && ldb % 4 == 0 && ((uintptr_t)a & 15) == 0 &&
+                   ((uintptr_t)b & 15) == 0 && ((uintptr_t)b_lo & 15) == 0,
+               FQ_ERR_DIMENSION, "3xTF32 GEMM: operands need 16-byte aligned rows (ld %% 4 == 0)");
+  FQ_CHECK_ARG(M < (1LL << 31) && N < (1LL << 31) && K < (1LL << 31), FQ_ERR_DIMENSION,
+               "3xTF32 GEMM: dimension too large");
+  return FQ_OK;
+}
+
+int launch_x3_gemm(const float* a, int64_t lda, const float* b, const float* b_lo, int64_t ldb,
+                   float* c, int64_t ldc, int64_t M, int64_t N, int64_t K, int accumulate,
+                   const float* bias, const float* res, int64_t ldr, int act, cudaStream_t s) {
+  int rc = check_x3(a, lda, b, b_lo, ldb, M, N, K);
+  if (rc != FQ_OK) return rc;
+  tc::Epi ep{c, ldc, 0, accumulate, bias, res, ldr, act, g_gemm_dbg};
+  const X3Plan p = plan_x3(N, K);
+  if (p.split > 1)
+    return tc::launch_splitk<128, 3, false, false, tc::OP_X3>(a, lda, b, ldb, ep, M, N, K,
+                                                              p.split, s, tc::LnEpi{}, b_lo);
+  if (p.bn == 64)
+    return tc::launch<64, 4, false, tc::OP_X3>(a, lda, b, ldb, ep, M, N, K, 1, 1, s,
+                                               tc::HarsEpi{}, b_lo);
+  return tc::launch<128, 3, false, tc::OP_X3>(a, lda, b, ldb, ep, M, N, K, 1, 1, s,
+                                              tc::HarsEpi{}, b_lo);
+}
+
+// Exact-mode GEMM (see include/fq_abi.h): c = act(a . b^T (+c) (+bias)) (+res),
+// a [M,K] fp32, b [N,K] fp32 K-major given either raw (b_lo = NULL: split in
+// shared memory) or pre-split into tf32 hi (b) + lo (b_lo).
+extern "C" int fq_gemm_f32x3(const float* a, int64_t lda, const float* b, const float* b_lo,
+                             int64_t ldb, float* c, int64_t ldc, int64_t M, int64_t N, int64_t K,
+                             int accumulate, const float* bias, const float* residual,
+                             int64_t ldr, int act, fq_stream_t stream) {
+  FQ_CHECK_ARG(a && b && c && M >= 0 && N >= 0 && K >= 1, FQ_ERR_DIMENSION,
+               "fq_gemm_f32x3: bad shape M=%lld N=%lld K=%lld", (long long)M, (long long)N,
+               (long long)K);
+  FQ_CHECK_ARG(act >= 0 && act <= 2, FQ_ERR_PARAMETER, "fq_gemm_f32x3: unknown activation");
+  if (M == 0 || N == 0) return FQ_OK;
+  return launch_x3_gemm(a, lda, b, b_lo, ldb, c, ldc, M, N, K, accumulate, bias, residual, ldr,
+                        act, as_stream(stream));
+}
+
+// Exact-mode GEMM + bias + residual + LayerNorm (the encoder's / decoder's
+// closing pairs, model.py:339-358, :582-626): with the 4-slice plan the split
+// K slices go to ws as slabs and fq_splitk_bias_residual_layer_norm sums them
+// in slice order (the DSMEM reduction's additions, same bits); else the GEMM
+// with its fused bias + residual, then fq_layer_norm.
+extern "C" int fq_gemm_f32x3_ln(const float* a, int64_t lda, const float* b, const float* b_lo,
+                                int64_t ldb, const float* bias, const float* res, int64_t ldr,
+                                const float* gamma, const float* beta, double eps, float* out,
+                                int64_t ldo, void* ws, int64_t ws_bytes, int64_t M, int64_t N,
+                                int64_t K, fq_stream_t stream) {
+  FQ_CHECK_ARG(a && b && bias && res && gamma && beta && out && M > 0 && N > 0 && K > 0,
+               FQ_ERR_DIMENSION, "fq_gemm_f32x3_ln: bad args");
+  int rc = check_x3(a, lda, b, b_lo, ldb, M, N, K);
+  if (rc != FQ_OK) return rc;
+  const X3Plan p = plan_x3(N, K);
+  const int64_t slab_need = (int64_t)p.split * M * N * (int64_t)sizeof(float);
+  if (p.split > 1 && ws && ws_bytes >= slab_need && ((uintptr_t)ws & 15) == 0 &&
+      (N == 512 || N == 1024)) {
+    tc::Epi ep{ws, N, 0, 0, nullptr, nullptr, 0, 0, g_gemm_dbg};
+    rc = tc::launch_splitk<128, 3, false, true, tc::OP_X3>(a, lda, b, ldb, ep, M, N, K, p.split,
+                                                           as_stream(stream), tc::LnEpi{}, b_lo);
+    if (rc != FQ_OK) return rc;
+    return fq_splitk_bias_residual_layer_norm(reinterpret_cast<const float*>(ws), p.split, N,
+                                              bias, res, ldr, gamma, beta, eps, M, N, out, ldo,
+                                              nullptr, 0, stream);
+  }
+  rc = launch_x3_gemm(a, lda, b, b_lo, ldb, out, ldo, M, N, K, 0, bias, res, ldr, 0,
+                      as_stream(stream));
+  if (rc != FQ_OK) return rc;
+  return fq_layer_norm(out, ldo, gamma, beta, eps, M, N, out, ldo, nullptr, 0, stream);
 }
 
 // Logits GEMM with the HARS statistics epilogue (see HarsEpi): x16 [rows, d]

@@ -35,7 +35,7 @@ from . import _abi
 from .errors import CapacityError, ConsistencyError, DimensionError, FullMaskError, InputError
 from .memory_plan import Arena, IntermediateSpec
 from .ops import attention_scale
-from .tensor import OpCounters, Timers, as_device, gemm, global_counters
+from .tensor import OpCounters, Timers, as_device, gemm, gemm_x3, global_counters
 
 F32 = np.float32
 I64 = np.int64
@@ -261,6 +261,32 @@ def lengths_mask(lengths, seq: int) -> np.ndarray:
 # device-resident weights
 # ---------------------------------------------------------------------------
 
+class X3Weight:
+    """An exact-mode GEMM weight: the tf32 hi and lo halves (hi + lo = w to
+    2^-22 relative) of the reference's [in, out] matrix, stored K-major
+    [out, in] for the 3xTF32 tcgen05 GEMM (fq_split_tf32, once at load)."""
+
+    __slots__ = ("hi", "lo")
+
+    def __init__(self, hi: torch.Tensor, lo: torch.Tensor):
+        self.hi, self.lo = hi, lo
+
+    @property
+    def shape(self):
+        return tuple(self.hi.shape)
+
+    @classmethod
+    def from_kn(cls, t: torch.Tensor, transpose: bool = True) -> "X3Weight":
+        """Split a device fp32 [K, N] matrix (``transpose``) or [N, K] one."""
+        rows, cols = t.shape
+        shape = (cols, rows) if transpose else (rows, cols)
+        hi = torch.empty(shape, dtype=torch.float32, device=t.device)
+        lo = torch.empty_like(hi)
+        _abi.call("fq_split_tf32", t.data_ptr(), rows, cols, int(transpose), hi.data_ptr(),
+                  lo.data_ptr(), _abi.stream_handle())
+        return cls(hi, lo)
+
+
 class DeviceWeights:
     """Weights uploaded once for one precision (cached per ModelWeights)."""
 
@@ -290,7 +316,7 @@ class DeviceWeights:
         def mat(a):  # GEMM B operand
             t = f32(a)
             if not self.bf16:
-                return t                                   # [K, N] fp32, NN kernel
+                return X3Weight.from_kn(t)                 # [N, K] tf32 hi + lo
             out = torch.empty((a.shape[1], a.shape[0]), dtype=torch.bfloat16, device=dev)
             _abi.call("fq_cast_bf16", t.data_ptr(), a.shape[0], a.shape[1], 1, out.data_ptr(),
                       _abi.stream_handle())
@@ -302,6 +328,7 @@ class DeviceWeights:
             self.out_proj = f32(out_m).to(torch.bfloat16)   # [V, d] already K-major
         else:
             self.out_proj = self.embedding if config.tie_output else f32(out_m)
+            self.out_x3 = X3Weight.from_kn(self.out_proj, transpose=False)  # logits GEMM
         self.positions = f32(sinusoidal_positions(config.max_seq_len, config.d_model))
         self.enc = []
         for lw in weights.encoder:
@@ -365,8 +392,8 @@ def _lin(dw: DeviceWeights, a32, a16, w, out, *, bias=None, residual=None, act="
         gemm(a16, w, out, transpose_b=True, bias=bias, residual=residual, activation=act,
              counters=counters, timers=timers)
     else:
-        gemm(a32, w, out, bias=bias, residual=residual, activation=act, counters=counters,
-             timers=timers)
+        gemm_x3(a32, w, out, bias=bias, residual=residual, activation=act, counters=counters,
+                timers=timers)
 
 
 def _ln(x, g, b, eps, out, out16, residual=None, bias=None, counters=None):
@@ -397,6 +424,17 @@ def _lin_ln(dw: DeviceWeights, a32, a16, w, bias, residual, g, b, eps, out, out1
                   b.data_ptr(), eps, out.data_ptr(), out.stride(0), _abi.ptr(out16),
                   out16.stride(0) if out16 is not None else 0, ws.data_ptr(),
                   ws.numel() * ws.element_size(), M, N, K, _abi.stream_handle())
+        (counters or global_counters()).count_fused("layer_norm", M * N * 8)
+        return
+    if not dw.bf16 and ws is not None:  # exact mode: 3xTF32 K-slice slabs + the reducing LN
+        M, K = a32.shape
+        N = w.shape[0]
+        _abi.call("fq_gemm_f32x3_ln", a32.data_ptr(), a32.stride(0), w.hi.data_ptr(),
+                  w.lo.data_ptr(), w.hi.stride(0), bias.data_ptr(), residual.data_ptr(),
+                  residual.stride(0), g.data_ptr(), b.data_ptr(), eps, out.data_ptr(),
+                  out.stride(0), ws.data_ptr(), ws.numel() * ws.element_size(), M, N, K,
+                  _abi.stream_handle())
+        (counters or global_counters()).count_gemm(a32.numel() * 4 + 2 * N * K * 4 + M * N * 4)
         (counters or global_counters()).count_fused("layer_norm", M * N * 8)
         return
     tmp = out
@@ -444,7 +482,7 @@ def encoder_layer_forward(x, layer, config: ModelConfig, mask=None, batch: int =
         layer = DeviceWeights(cfg1, tmp, precision).enc[0]
         dw_bf16 = precision == "bf16"
     else:
-        dw_bf16 = layer["w_qkv"].dtype == torch.bfloat16
+        dw_bf16 = not isinstance(layer["w_qkv"], X3Weight)
     bufs = buffers if buffers is not None else HeapBuffers()
     ctr = counters or global_counters()
     h, hd, ff = config.num_heads, config.head_dim, config.d_ff
@@ -664,7 +702,8 @@ class DecoderStep:
         # FQ_FUSE_LN=0: GEMM with the reduction, then the LN kernel.
         self.ln_ws = None
         mode = os.environ.get("FQ_FUSE_LN", "slab")
-        if dw.bf16 and fuse_ln and mode != "0":
+        if fuse_ln and mode != "0" and (dw.bf16 or mode == "slab"):
+            # exact mode: the 3xTF32 split-K slabs summed by the LN kernel
             ws = b.get("dec.ln_ws", ((ln_ws_bytes(R, d) + 3) // 4,), torch.int32)
             if mode == "coresident":
                 ws = ws[:(ln_ws_bytes(R, d, slabs=False) + 3) // 4]
@@ -672,7 +711,7 @@ class DecoderStep:
             self.ln_ws = ws
         # the cross-attention query GEMM as K-slice slabs summed by the
         # cross-attention kernel (no in-GEMM reduction), same bits
-        self.q_slabs = (self.ln_ws is not None and mode != "coresident" and
+        self.q_slabs = (dw.bf16 and self.ln_ws is not None and mode != "coresident" and
                         config.head_dim == 64 and beam <= 8 and enc_seq <= 64)
         self._nslab = ctypes.c_int(0)
 
@@ -766,8 +805,8 @@ class DecoderStep:
             x, x16 = self.x, self.x16
         if not logits:
             return None
-        _lin(dw, x, x16, dw.out_proj, self.logits, counters=ctr, timers=tm) if dw.bf16 else \
-            gemm(x, dw.out_proj, self.logits, transpose_b=True, counters=ctr, timers=tm)
+        _lin(dw, x, x16, dw.out_proj if dw.bf16 else dw.out_x3, self.logits, counters=ctr,
+             timers=tm)
         return self.logits
 
 
@@ -866,8 +905,8 @@ def plan_intermediates(config: ModelConfig, precision: str = "fp32") -> list[Int
                        ("cres", R * d * 4), ("cnorm", R * d * 4), ("ffn_h", R * ff * a),
                        ("ffn_out", R * d * 4)):
             add(f"dec.{nm}", sz, dec0, end - 3)
+        add("dec.ln_ws", ln_ws_bytes(R, d), dec0, end - 3)  # split-K slabs (both modes)
         if bf:
-            add("dec.ln_ws", ln_ws_bytes(R, d), dec0, end - 3)
             add("dec.snorm16", R * d * 2, dec0, end - 3)
             add("dec.cnorm16", R * d * 2, dec0, end - 3)
         add("dec.logits", R * V * 4, end - 3, end)

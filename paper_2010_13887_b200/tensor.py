@@ -255,6 +255,34 @@ def gemm(a, b, out, *, transpose_b: bool = False, accumulate: bool = False,
         A.numel() * A.element_size() + B.numel() * B.element_size() + O.numel() * O.element_size())
 
 
+def gemm_x3(a, w, out, *, accumulate: bool = False, counters: OpCounters | None = None,
+            timers: Timers | None = None, bias=None, residual=None, activation: str = "none"):
+    """Exact-mode engine GEMM on the tensor cores: out = act(a @ w^T (+ out)
+    (+ bias)) (+ residual), ``a`` fp32 [M, K], ``w`` an ``X3Weight`` (the
+    weight's tf32 hi / lo halves, K-major [N, K], split once at load) — the
+    3xTF32 product of fq_gemm_f32x3. One call increments ``gemm_calls`` by one
+    (tensor.py:204)."""
+    A, O = as_device(a, torch.float32), as_device(out)
+    if A.dim() != 2 or O.dim() != 2 or O.dtype != torch.float32:
+        raise DimensionError("gemm_x3 expects 2D fp32 operands")
+    N, K = w.shape
+    if A.shape[1] != K or tuple(O.shape) != (A.shape[0], N):
+        raise DimensionError(f"gemm_x3 shapes {tuple(A.shape)} x {(N, K)}^T -> {tuple(O.shape)}")
+    _check_no_alias(O, A, w.hi, w.lo)
+    lda, ldc = _row_major(A, "a"), _row_major(O, "out")
+    res_t, ldr = None, 0
+    if residual is not None:
+        res_t = as_device(residual, torch.float32)
+        ldr = _row_major(res_t, "residual")
+    t0 = timers.start() if timers is not None else None
+    _abi.call("fq_gemm_f32x3", A.data_ptr(), lda, w.hi.data_ptr(), w.lo.data_ptr(),
+              w.hi.stride(0), O.data_ptr(), ldc, A.shape[0], N, K, int(accumulate),
+              _abi.ptr(bias), _abi.ptr(res_t), ldr, ACT_IDS[activation], _abi.stream_handle())
+    if timers is not None:
+        timers.stop("gemm", t0)
+    (counters or _global_counters).count_gemm(A.numel() * 4 + 2 * N * K * 4 + O.numel() * 4)
+
+
 def _batch_strides(t: torch.Tensor, lead: tuple[int, ...]) -> tuple[int, int, int, int]:
     """Express the leading dims of ``t`` (broadcast to ``lead``) as a two-level
     batch (n0, s0, n1, s1)."""

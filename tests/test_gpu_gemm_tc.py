@@ -222,3 +222,114 @@ def test_tc_gemm_tma_store_strided_views(P, dt, M, N, K, pad):
     tol = 1e-3 if dt == "f32" else 8e-3
     assert _rel(view.float(), _ref(a, b, bias, "relu")) <= tol
     assert bool((big[:, :pad].float() == 7.0).all())
+
+
+# ---------------------------------------------------------------------------
+# exact fp32 mode on the tensor cores: 3xTF32 (fq_gemm_f32x3)
+
+def _x3(P, a, b_nk, out, presplit=True, **kw):
+    from paper_2010_13887_b200.model import X3Weight
+    from paper_2010_13887_b200.tensor import gemm_x3
+    if presplit:
+        gemm_x3(a, X3Weight.from_kn(b_nk, transpose=False), out, **kw)
+    else:  # raw fp32 K-major B through the reference's gemm API (split in smem)
+        act = kw.pop("activation", "none")
+        P.gemm(a, b_nk, out, transpose_b=True, activation=act, **kw)
+
+
+@pytest.mark.parametrize("M,N,K", [
+    (1, 8, 16), (100, 100, 72), (128, 64, 64), (512, 1024, 1024), (512, 3072, 1024),
+    (512, 1024, 4096), (512, 4096, 1024), (300, 2000, 256), (512, 32000, 1024),
+    (8192, 1024, 4096), (2048, 3072, 1024)])
+def test_x3_gemm_matches_f64(P, M, N, K):
+    """3xTF32 vs float64 on the same fp32 operands: fp32-GEMM accuracy, i.e.
+    within 2x the error of an IEEE fp32 SGEMM (cuBLAS, TF32 off) of the same
+    product, and <= 4e-6 of the output scale (the reference's own GEMM tests
+    hold OpenBLAS to 1e-6 at K <= 64, test_tensor.py:51-58)."""
+    import torch
+    g = torch.Generator(device="cuda").manual_seed(M * 5 + N + K)
+    a = torch.randn(M, K, device="cuda", generator=g)
+    b = torch.randn(N, K, device="cuda", generator=g) * 0.03
+    want = a.double() @ b.double().T
+    scale = float(want.abs().max())
+    prev = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = False
+    sgemm_err = float((a @ b.T).double().sub(want).abs().max()) / scale
+    torch.backends.cuda.matmul.allow_tf32 = prev
+    for presplit in (True, False):
+        out = torch.empty(M, N, device="cuda")
+        _x3(P, a, b, out, presplit=presplit)
+        torch.cuda.synchronize()
+        err = float((out.double() - want).abs().max()) / scale
+        print(f"{M}x{N}x{K} presplit={presplit}: 3xTF32 {err:.2e}  fp32 SGEMM {sgemm_err:.2e}")
+        assert err <= max(2 * sgemm_err, 5e-7) and err <= 1e-6, (M, N, K, presplit, err)
+        if presplit:
+            first = out.clone()
+        else:  # in-kernel split == load-time split, bit for bit
+            assert torch.equal(out, first)
+
+
+@pytest.mark.parametrize("act", ["none", "relu", "gelu"])
+def test_x3_gemm_epilogue_bits_vs_separate_ops(P, act):
+    """The fused epilogue applies the reference's bias_residual_act semantics
+    (kernels.py:39-53: fp32 bias add, act, fp32 residual add) to the 3xTF32
+    accumulator: identical bits to the GEMM followed by fq_bias_residual_act."""
+    import torch
+    M, N, K = 384, 1536, 512
+    g = torch.Generator(device="cuda").manual_seed(11)
+    a = torch.randn(M, K, device="cuda", generator=g)
+    b = torch.randn(N, K, device="cuda", generator=g) * 0.05
+    bias = torch.randn(N, device="cuda", generator=g)
+    res = torch.randn(M, N, device="cuda", generator=g)
+    fused = torch.empty(M, N, device="cuda")
+    _x3(P, a, b, fused, bias=bias, residual=res, activation=act)
+    plain = torch.empty(M, N, device="cuda")
+    _x3(P, a, b, plain)
+    sep = P.fused_bias_residual_activation(plain, bias, res, act)
+    assert torch.equal(fused, sep.data)
+
+
+def test_x3_gemm_bits_independent_of_m(P):
+    """Exact mode's plan depends on (N, K) only: a row block computed inside a
+    512-row GEMM and alone (64 rows, as on 8 GPUs of a batch-sharded C2) has
+    identical bits — the basis of the batch-sharding invariance."""
+    import torch
+    g = torch.Generator(device="cuda").manual_seed(3)
+    for N, K in ((1024, 1024), (3072, 1024), (1024, 4096), (32000, 1024)):
+        a = torch.randn(512, K, device="cuda", generator=g)
+        b = torch.randn(N, K, device="cuda", generator=g) * 0.03
+        full = torch.empty(512, N, device="cuda")
+        _x3(P, a, b, full)
+        part = torch.empty(64, N, device="cuda")
+        _x3(P, a[192:256].contiguous(), b, part)
+        assert torch.equal(full[192:256], part), (N, K)
+
+
+def test_x3_gemm_ln_slab_path_bit_identical(P):
+    """fq_gemm_f32x3_ln: 4 K-slice slabs summed by the LN kernel == the split-K
+    GEMM with its DSMEM reduction + fused bias/residual, then fq_layer_norm."""
+    import torch
+    from paper_2010_13887_b200 import _abi
+    from paper_2010_13887_b200.model import X3Weight
+    M, N, K = 512, 1024, 4096
+    g = torch.Generator(device="cuda").manual_seed(9)
+    a = torch.randn(M, K, device="cuda", generator=g)
+    w = X3Weight.from_kn(torch.randn(N, K, device="cuda", generator=g) * 0.02, transpose=False)
+    bias = torch.randn(N, device="cuda", generator=g)
+    res = torch.randn(M, N, device="cuda", generator=g)
+    gm = torch.rand(N, device="cuda", generator=g) + 0.5
+    bt = torch.randn(N, device="cuda", generator=g)
+    outs = []
+    for ws_bytes in (4 * M * N * 4, 0):
+        ws = torch.empty(max(ws_bytes, 16), dtype=torch.uint8, device="cuda")
+        out = torch.empty(M, N, device="cuda")
+        _abi.call("fq_gemm_f32x3_ln", a.data_ptr(), K, w.hi.data_ptr(), w.lo.data_ptr(), K,
+                  bias.data_ptr(), res.data_ptr(), N, gm.data_ptr(), bt.data_ptr(), 1e-5,
+                  out.data_ptr(), N, ws.data_ptr() if ws_bytes else None, ws_bytes, M, N, K,
+                  _abi.stream_handle())
+        outs.append(out)
+    assert torch.equal(outs[0], outs[1])
+    x = (a.double() @ (w.hi.double() + w.lo.double()).T + bias.double()) + res.double()
+    mu, var = x.mean(1, keepdim=True), x.var(1, unbiased=False, keepdim=True)
+    want = (x - mu) / torch.sqrt(var + 1e-5) * gm.double() + bt.double()
+    assert float((outs[0].double() - want).abs().max()) <= 2e-5

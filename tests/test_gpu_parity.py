@@ -80,10 +80,11 @@ def test_gemm_exact_mode_vs_f64(P):
         out = torch.empty((m, n), device="cuda")
         P.gemm(a, b, out)
         assert rel(out.cpu().numpy(), a.astype(np.float64) @ b) <= 1e-5
+        # K-major B (transpose_b): the exact-mode 3xTF32 tensor-core kernel
         bt = np.ascontiguousarray(b.T)
         out2 = torch.empty((m, n), device="cuda")
         P.gemm(a, bt, out2, transpose_b=True)
-        assert np.array_equal(out.cpu().numpy(), out2.cpu().numpy())  # same K order
+        assert rel(out2.cpu().numpy(), a.astype(np.float64) @ b) <= 1e-5
     # known answer, tests/test_tensor.py:37-42
     out = torch.empty((2, 2), device="cuda")
     P.gemm(np.array([[1, 2], [3, 4]], F32), np.array([[5, 6], [7, 8]], F32), out)
