@@ -48,6 +48,10 @@ enum fq_act { FQ_ACT_NONE = 0, FQ_ACT_RELU = 1, FQ_ACT_GELU = 2 }; /* ops.py:61 
 int fq_abi_version(void);
 const char* fq_last_error(void);
 int fq_num_sms(void);
+/* Programmatic dependent launch for later launches / captures: 1 on, 0 off,
+ * -1 back to the FQ_PDL environment default (on). Not a reference interface:
+ * the benchmark's clean kernel timeline (PDL overlaps kernel durations). */
+int fq_set_pdl(int mode);
 /* Opt every kernel into the shared-memory sizes it may request, once, before
  * any stream capture (cudaFuncSetAttribute is not a stream operation). */
 int fq_prepare(void);

@@ -34,6 +34,7 @@ SIGNATURES = {
     "fq_abi_version": ([], I32),
     "fq_last_error": ([], ctypes.c_char_p),
     "fq_num_sms": ([], I32),
+    "fq_set_pdl": ([I32], I32),
     "fq_prepare": ([], I32),
     "fq_layer_norm": ([P, I64, P, P, F64, I64, I64, P, I64, P, I64, P], I32),
     "fq_bias_residual_layer_norm": ([P, I64, P, P, I64, P, P, F64, I64, I64, P, I64, P, I64, P],
@@ -88,7 +89,8 @@ _ERRORS = {-1: DimensionError, -2: ParameterError, -3: AliasingError, -4: Capaci
 _lib = None
 _lock = threading.Lock()
 _prepared = False
-_NO_PREPARE = {"fq_abi_version", "fq_last_error", "fq_num_sms", "fq_prepare", "fq_gemm_plan"}
+_NO_PREPARE = {"fq_abi_version", "fq_last_error", "fq_num_sms", "fq_prepare", "fq_gemm_plan",
+               "fq_set_pdl"}
 _launches = [0]
 
 

@@ -14,13 +14,17 @@ void set_error(const char* fmt, ...) {
   va_end(ap);
 }
 
+// -1: follow FQ_PDL (default on); 0 / 1: fq_set_pdl override (bench.py turns
+// PDL off for one profiled request so CUPTI kernel durations do not overlap)
+int g_pdl_override = -1;
+
 bool pdl_enabled() {
   static const bool on = [] {
     // default on; FQ_PDL=0 launches without programmatic serialization
     const char* e = getenv("FQ_PDL");
     return !(e && e[0] == '0');
   }();
-  return on;
+  return g_pdl_override < 0 ? on : g_pdl_override != 0;
 }
 
 int launch_status(const char* what) {
@@ -100,6 +104,11 @@ int fq_prepare(void) {
 int fq_abi_version(void) { return 1; }
 
 const char* fq_last_error(void) { return fq::g_err; }
+
+int fq_set_pdl(int mode) {
+  fq::g_pdl_override = mode < 0 ? -1 : (mode != 0);
+  return 0;
+}
 
 int fq_num_sms(void) {
   int dev = 0, n = 0;
