@@ -4,7 +4,7 @@ config 2: 6+6 layers, d=1024, 16 heads, ff=4096, V=32000, batch 128, src 64,
 64 decode steps) through the B200 device engine, plus the HARS step microbench.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--precision fp32|bf16] [--batch B] [--scaling strong|weak]
+                    [--precision fp32|fp16] [--batch B] [--scaling strong|weak]
 
 One "step" = one full request: encoder + cross-K/V + 64 decode steps with HARS
 beam search over the batch (seeded random-init weights of the architecture,
@@ -67,8 +67,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--precision", default="fp32", choices=["fp32", "bf16"])
-    ap.add_argument("--half", default="bf16", choices=["bf16", "none"],
+    ap.add_argument("--precision", default="fp32", choices=["fp32", "fp16"])
+    ap.add_argument("--half", default="fp16", choices=["fp16", "none"],
                     help="throughput mode reported beside the headline")
     ap.add_argument("--batch", type=int, default=GLOBAL_BATCH, help="global batch (items)")
     ap.add_argument("--scaling", default="strong", choices=["strong", "weak"])
@@ -639,7 +639,7 @@ def run_ours(args, rank, world):
 
     sess, src_dev, dc, res = time_mode(P, cfg, host_w, args.precision, src_host, args, world,
                                        dev, flush, barrier, clock=True)
-    dtype = {"fp32": "f32", "bf16": "bf16"}[args.precision]
+    dtype = {"fp32": "f32", "fp16": "f16"}[args.precision]
     out = None
     if rank == 0:
         out = {
@@ -656,7 +656,7 @@ def run_ours(args, rank, world):
                        "precision": f"{args.precision} ("
                        + ("exact mode: 3xTF32 tcgen05 GEMMs, fp32/f64 elementwise, tokens "
                           "bit-exact vs the reference at this config)" if args.precision ==
-                          "fp32" else "bf16 throughput mode") + ")",
+                          "fp32" else "fp16 throughput mode") + ")",
                        "tokens_per_step": res["tokens"],
                        "l2": "256 MiB buffer written before every timed request; working set "
                              ">> 126 MB L2"},
@@ -685,7 +685,7 @@ def run_ours(args, rank, world):
         else:
             out["roofline"] = roofline_gemm(sess, src_dev, dc, cfg, local, res["steps_run"],
                                             bf16_peak, "MEASURED_PEAKS.json bf16_tflops_"
-                                            "sustained (measured)", "bf16")
+                                            "sustained (measured)", "fp16")
         if half is not None:
             out["half_mode"]["roofline"] = roofline_gemm(
                 half, hsrc, hdc, cfg, local, hres["steps_run"], bf16_peak,

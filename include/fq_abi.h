@@ -41,7 +41,7 @@ enum fq_status {
   FQ_ERR_UNSUPPORTED = -6  /* dtype/shape combination not built */
 };
 
-enum fq_dtype { FQ_F32 = 0, FQ_BF16 = 1 };
+enum fq_dtype { FQ_F32 = 0, FQ_F16 = 1 };
 enum fq_act { FQ_ACT_NONE = 0, FQ_ACT_RELU = 1, FQ_ACT_GELU = 2 }; /* ops.py:61 */
 
 /* ---- library ---------------------------------------------------------- */
@@ -59,7 +59,7 @@ int fq_prepare(void);
 /* ---- fused elementwise passes (kernels.py) ---------------------------- */
 
 /* kernels.py:22 layer_norm_kernel. x fp32 [rows, d] (ldx); outputs optional:
- * out (fp32, ldo) and/or out16 (bf16, ldo16; the next GEMM's operand). */
+ * out (fp32, ldo) and/or out16 (fp16, ldo16; the next GEMM's operand). */
 int fq_layer_norm(const float* x, int64_t ldx, const float* gamma, const float* beta,
                   double eps, int64_t rows, int64_t d, float* out, int64_t ldo,
                   void* out16, int64_t ldo16, fq_stream_t stream);
@@ -109,7 +109,7 @@ int fq_scale_mask_softmax(const float* scores, int64_t ld, float* out, int64_t l
 
 /* kernels.py:143 embed_scale_pos_kernel: out[i] = emb[tok[i]]*scale + pos[i%seq + off].
  * If d_off != NULL the offset is read from device memory (graph replay).
- * out (fp32) and/or out16 (bf16) may be NULL. */
+ * out (fp32) and/or out16 (fp16) may be NULL. */
 int fq_embed_scale_pos(const int64_t* tokens, int64_t n, const float* emb, int64_t d,
                        float scale, const float* pos, int64_t pos_offset,
                        const int32_t* d_off, int64_t seq, float* out, void* out16,
@@ -136,7 +136,7 @@ int fq_kv_gather_append(const float* src_k, const float* src_v, const float* new
 
 /* ---- GEMM (tensor.py:179 gemm, :207 gemm_batched) --------------------- */
 
-/* out = LN(a . w^T + bias + residual) (bf16 operands, fp32 out, optional bf16
+/* out = LN(a . w^T + bias + residual) (fp16 operands, fp32 out, optional fp16
  * copy): model.py:596-627's GEMM + fused_bias_residual_layer_norm pairs
  * (kernels.py:57-73). When the GEMM runs split-K over 128-column tiles:
  * - ws >= split * M * N * 4 bytes (slab path, the engine default): the split-K
@@ -153,7 +153,7 @@ int fq_gemm_ln(const void* a, int64_t lda, const void* w, int64_t ldw, const flo
                float* out, int64_t ldo, void* out16, int64_t ldo16, void* ws, int64_t ws_bytes,
                int64_t M, int64_t N, int64_t K, fq_stream_t stream);
 
-/* The split-K bf16 GEMM's per-K-slice fp32 partials without the reduction:
+/* The split-K fp16 GEMM's per-K-slice fp32 partials without the reduction:
  * ws [nslab][M][N], slab s = a[:, slice s] . w[:, slice s]^T (a [M,K], w
  * [N,K]). Sets *nslab = 0 and launches nothing when this shape's plan is not
  * split-K or ws < split * M * N * 4 bytes. The consumer sums the slabs in slab
@@ -169,10 +169,10 @@ int fq_gemm_splitk_slabs(const void* a, int64_t lda, const void* w, int64_t ldw,
  * dtypes: a_dtype == b_dtype. FQ_F32 operands with transpose_b (K-major B),
  * 16-byte aligned rows and an fp32 C: the exact-mode 3xTF32 tcgen05 kernel
  * (fq_gemm_f32x3 with b_lo = NULL); other FQ_F32 layouts: the SIMT FFMA
- * kernel (sequential K order, M-independent; API use only). FQ_BF16 operands
+ * kernel (sequential K order, M-independent; API use only). FQ_F16 operands
  * require transpose_b (weights pre-laid-out [N,K]) and run on tcgen05 tensor
  * cores (TMEM accumulators, TMA-fed, fp32 accumulate). c_dtype: FQ_F32 or
- * FQ_BF16. */
+ * FQ_F16. */
 int fq_gemm(const void* a, int a_dtype, int64_t lda, const void* b, int b_dtype, int64_t ldb,
             int transpose_b, void* c, int c_dtype, int64_t ldc, int64_t M, int64_t N,
             int64_t K, int accumulate, const float* bias, const float* residual, int64_t ldr,
@@ -208,7 +208,7 @@ int fq_split_tf32(const float* src, int64_t rows, int64_t cols, int transpose, f
                   float* lo, fq_stream_t stream);
 
 /* Tile width and thread-block-cluster shape (cm x cn CTAs sharing A/B tiles
- * through TMA multicast) the bf16 dispatcher picks for an M x N x K GEMM. */
+ * through TMA multicast) the fp16 dispatcher picks for an M x N x K GEMM. */
 int fq_gemm_plan(int64_t M, int64_t N, int64_t K, int* bn, int* cm, int* cn, int* split);
 
 /* Strided batched fp32 GEMM over a two-level batch (i0 < n0, i1 < n1):
@@ -286,7 +286,7 @@ int fq_hars_groups(fq_beam_state st, int64_t batch, int64_t beam, int64_t vocab,
  * With x_next != NULL the item's rows of the next step's decoder input are
  * also written (embed_scale_pos at position *d_cur + 1, kernels.py:143-151:
  * fp32 emb[token] * emb_scale + pos[position], row-major [rows, d_model],
- * x16_next an optional bf16 copy), replacing the next step's embedding launch. */
+ * x16_next an optional fp16 copy), replacing the next step's embedding launch. */
 int fq_hars_step(const float* logits, int64_t ld, fq_beam_state st, int64_t batch, int64_t beam,
                  int64_t vocab, int64_t max_len, int64_t eos, const double* len_pow,
                  int32_t* d_cur, int64_t max_steps, double* lse, int32_t* cand_idx,
@@ -296,7 +296,7 @@ int fq_hars_step(const float* logits, int64_t ld, fq_beam_state st, int64_t batc
                  fq_stream_t stream);
 
 /* The decode step's output layer without materialising the [rows, V]
- * logits: the tied-embedding logits GEMM (x16 [rows, d] bf16 .
+ * logits: the tied-embedding logits GEMM (x16 [rows, d] fp16 .
  * emb16 [vocab, d]^T, tcgen05) whose epilogue computes HARS stage 1's
  * statistics per row and column tile: strided group maxima folded into the
  * row's running maxima gmax [rows][32] (ordered ints, -inf between steps) with
@@ -340,7 +340,7 @@ int fq_step_advance(int32_t* d_cur, fq_stream_t stream);
 /* Encoder self-attention, one pass per (item, head): q,k,v read from the packed
  * [n, 3d] projection (bias already added), softmax(qk^T*scale + mask) with the
  * kernels.py:106 numerics (exact mode: f64 exp/sum), ctx written merged-head
- * [n, d] (ldo) as fp32 (out) and/or bf16 (out16). mask [batch, seq] or NULL.
+ * [n, d] (ldo) as fp32 (out) and/or fp16 (out16). mask [batch, seq] or NULL.
  * d_bad counts fully masked rows. exact: 1 = f64 softmax internals. */
 int fq_encoder_attention(const float* qkv, int64_t ldq, int64_t batch, int64_t seq,
                          int64_t heads, int64_t head_dim, float scale, const float* mask,
@@ -351,7 +351,7 @@ int fq_encoder_attention(const float* qkv, int64_t ldq, int64_t batch, int64_t s
  * step cur attends positions t < cur through cache slot (t, hist[r, t]) and
  * position cur through its own new K/V (taken from the packed sqkv [R, 3d]
  * projection, bias added), which this call also stores into slot (cur, r).
- * Cache layout [max_len, R, d] (kv_dtype fp32 or bf16). */
+ * Cache layout [max_len, R, d] (kv_dtype fp32 or fp16). */
 int fq_decoder_self_attention(const float* sqkv, int64_t ldq, void* kcache, void* vcache,
                               int kv_dtype, const int32_t* hist, const int32_t* d_cur,
                               int64_t rows, int64_t heads, int64_t head_dim, int64_t max_len,
@@ -367,7 +367,7 @@ int fq_cross_attention(const float* cq, int64_t ldcq, const void* ck, const void
                        float* out, void* out16, int64_t ldo, int exact, int* d_bad,
                        fq_stream_t stream);
 
-/* fq_cross_attention (bf16 K/V, head_dim 64, seq <= 64, beam <= 8) whose
+/* fq_cross_attention (fp16 K/V, head_dim 64, seq <= 64, beam <= 8) whose
  * query is given as the nslab K-slice slabs of the split-K query GEMM
  * (fq_gemm_splitk_slabs; slab s at q_slabs + s * batch*beam*ldq) plus q_bias:
  * q = ((slab0 + slab1) + ...) + bias, the GEMM's own epilogue order. */
@@ -379,8 +379,8 @@ int fq_cross_attention_slabs(const float* q_slabs, int nslab, int64_t ldq, const
 
 /* ---- weight preparation (cast once at load) -------------- */
 
-/* dst16[N, K] (bf16, row-major) = src[K, N]^T (fp32) when transpose, else cast. */
-int fq_cast_bf16(const float* src, int64_t rows, int64_t cols, int transpose, void* dst16,
+/* dst16[N, K] (fp16, row-major) = src[K, N]^T (fp32) when transpose, else cast. */
+int fq_cast_f16(const float* src, int64_t rows, int64_t cols, int transpose, void* dst16,
                  fq_stream_t stream);
 
 #ifdef __cplusplus

@@ -73,7 +73,7 @@ SIGNATURES = {
                                    I32, P], I32),
     "fq_cross_attention": ([P, I64, P, P, I32, I64, I64, I64, I64, I64, I64, F32, P, P, P, I64,
                             I32, P, P], I32),
-    "fq_cast_bf16": ([P, I64, I64, I32, P, P], I32),
+    "fq_cast_f16": ([P, I64, I64, I32, P, P], I32),
     "fq_cross_attention_slabs": ([P, I32, I64, P, P, P, I64, I64, I64, I64, I64, I64, F32, P, P,
                                   P, I64, P, P], I32),
     "fq_gemm_splitk_slabs": ([P, I64, P, I64, P, I64, I64, I64, I64, P, P], I32),

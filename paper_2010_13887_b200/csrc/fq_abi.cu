@@ -36,9 +36,9 @@ int launch_status(const char* what) {
   return FQ_OK;
 }
 
-// dst[N,K] bf16 = src[K,N]^T (transpose) or dst[rows,cols] = src (cast).
-__global__ void cast_bf16_kernel(const float* __restrict__ src, int64_t rows, int64_t cols,
-                                 int transpose, __nv_bfloat16* __restrict__ dst) {
+// dst[N,K] fp16 = src[K,N]^T (transpose) or dst[rows,cols] = src (cast).
+__global__ void cast_f16_kernel(const float* __restrict__ src, int64_t rows, int64_t cols,
+                                 int transpose, h16* __restrict__ dst) {
   pdl_enter();
   __shared__ float tile[32][33];
   if (!transpose) {
@@ -46,7 +46,7 @@ __global__ void cast_bf16_kernel(const float* __restrict__ src, int64_t rows, in
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x * blockDim.y +
                      threadIdx.y * blockDim.x + threadIdx.x;
          i < n; i += (int64_t)gridDim.x * blockDim.x * blockDim.y)
-      dst[i] = f2bf(src[i]);
+      dst[i] = f2h(src[i]);
     return;
   }
   // 32x32 tiles: read src rows coalesced, write dst rows coalesced.
@@ -61,7 +61,7 @@ __global__ void cast_bf16_kernel(const float* __restrict__ src, int64_t rows, in
     __syncthreads();
     for (int i = threadIdx.y; i < 32; i += blockDim.y) {
       int64_t c = c0 + i, r = r0 + threadIdx.x;  // dst row = src col
-      if (c < cols && r < rows) dst[c * rows + r] = f2bf(tile[threadIdx.x][i]);
+      if (c < cols && r < rows) dst[c * rows + r] = f2h(tile[threadIdx.x][i]);
     }
     __syncthreads();
   }
@@ -117,15 +117,15 @@ int fq_num_sms(void) {
   return n;
 }
 
-int fq_cast_bf16(const float* src, int64_t rows, int64_t cols, int transpose, void* dst16,
+int fq_cast_f16(const float* src, int64_t rows, int64_t cols, int transpose, void* dst16,
                  fq_stream_t stream) {
-  FQ_CHECK_ARG(src && dst16 && rows > 0 && cols > 0, FQ_ERR_DIMENSION, "fq_cast_bf16: bad args");
+  FQ_CHECK_ARG(src && dst16 && rows > 0 && cols > 0, FQ_ERR_DIMENSION, "fq_cast_f16: bad args");
   dim3 block(32, 8);
   int64_t work = transpose ? ((rows + 31) / 32) * ((cols + 31) / 32) : (rows * cols + 255) / 256;
   int grid = (int)(work < 148 * 16 ? work : 148 * 16);
-  fq::launch_kernel(fq::cast_bf16_kernel, grid, block, 0, fq::as_stream(stream), 1u, 
-      src, rows, cols, transpose, reinterpret_cast<__nv_bfloat16*>(dst16));
-  return fq::launch_status("fq_cast_bf16");
+  fq::launch_kernel(fq::cast_f16_kernel, grid, block, 0, fq::as_stream(stream), 1u, 
+      src, rows, cols, transpose, reinterpret_cast<fq::h16*>(dst16));
+  return fq::launch_status("fq_cast_f16");
 }
 
 int fq_split_tf32(const float* src, int64_t rows, int64_t cols, int transpose, float* hi,

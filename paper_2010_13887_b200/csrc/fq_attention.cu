@@ -16,7 +16,7 @@
 // Beam reorder then moves B*K*max_len int32 instead of the K/V history.
 //
 // All three kernels are bandwidth/latency bound: head slices are staged with
-// 128-bit loads (8 bf16 or 4 fp32 per load), all issued before first use.
+// 128-bit loads (8 fp16 or 4 fp32 per load), all issued before first use.
 #include <cuda.h>
 #include <stdlib.h>
 
@@ -29,8 +29,8 @@ __device__ __forceinline__ float ld_as_f32(const T* p);
 template <>
 __device__ __forceinline__ float ld_as_f32<float>(const float* p) { return *p; }
 template <>
-__device__ __forceinline__ float ld_as_f32<__nv_bfloat16>(const __nv_bfloat16* p) {
-  return bf2f(*p);
+__device__ __forceinline__ float ld_as_f32<h16>(const h16* p) {
+  return h2f(*p);
 }
 
 // 16 bytes -> EV floats
@@ -42,12 +42,13 @@ __device__ __forceinline__ void unpack16<float>(const uint4& raw, float* o) {
   o[2] = __uint_as_float(raw.z); o[3] = __uint_as_float(raw.w);
 }
 template <>
-__device__ __forceinline__ void unpack16<__nv_bfloat16>(const uint4& raw, float* o) {
+__device__ __forceinline__ void unpack16<h16>(const uint4& raw, float* o) {
   const uint32_t w[4] = {raw.x, raw.y, raw.z, raw.w};
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
-    o[2 * i] = __uint_as_float(w[i] << 16);
-    o[2 * i + 1] = __uint_as_float(w[i] & 0xffff0000u);
+    const float2 f = __half22float2(*reinterpret_cast<const h16x2*>(&w[i]));
+    o[2 * i] = f.x;
+    o[2 * i + 1] = f.y;
   }
 }
 
@@ -123,7 +124,7 @@ __device__ __forceinline__ bool warp_softmax(float* s, int n, bool exact) {
 __device__ __forceinline__ void attend_rows(const float* Qs, const float* Ks, const float* Vs,
                                             float* Ss, int seq, int hd, int hp, float scale,
                                             const float* mk, bool exact, float* out,
-                                            __nv_bfloat16* out16, int* d_bad) {
+                                            h16* out16, int* d_bad) {
   const int lane = threadIdx.x & 31;
   for (int j = lane; j < seq; j += 32) {
     float acc = 0.0f;
@@ -141,7 +142,7 @@ __device__ __forceinline__ void attend_rows(const float* Qs, const float* Ks, co
     float acc = 0.0f;
     for (int j = 0; j < seq; ++j) acc = fmaf(Ss[j], Vs[j * hp + e], acc);
     if (out) out[e] = acc;
-    if (out16) out16[e] = f2bf(acc);
+    if (out16) out16[e] = f2h(acc);
   }
   __syncwarp();
 }
@@ -151,7 +152,7 @@ __device__ __forceinline__ void attend_rows(const float* Qs, const float* Ks, co
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) encoder_attention_kernel(
     const float* __restrict__ qkv, int64_t ldq, int seq, int heads, int hd, float scale,
-    const float* __restrict__ mask, float* __restrict__ out, __nv_bfloat16* __restrict__ out16,
+    const float* __restrict__ mask, float* __restrict__ out, h16* __restrict__ out16,
     int64_t ldo, int exact, int* d_bad) {
   pdl_enter();
   extern __shared__ float sm[];
@@ -187,7 +188,7 @@ template <typename KV, int HD>
 __global__ void __launch_bounds__(128) decoder_self_attention_fast(
     const float* __restrict__ sqkv, int64_t ldq, KV* __restrict__ kc, KV* __restrict__ vc,
     const int32_t* __restrict__ hist, const int32_t* __restrict__ d_cur, int rows, int heads,
-    int max_len, float scale, float* __restrict__ out, __nv_bfloat16* __restrict__ out16,
+    int max_len, float scale, float* __restrict__ out, h16* __restrict__ out16,
     int64_t ldo, int exact) {
   pdl_enter();
   extern __shared__ float sm[];
@@ -216,8 +217,8 @@ __global__ void __launch_bounds__(128) decoder_self_attention_fast(
       kc[slot_cur + e] = rowp[d + e];
       vc[slot_cur + e] = rowp[2 * d + e];
     } else {
-      kc[slot_cur + e] = f2bf(rowp[d + e]);
-      vc[slot_cur + e] = f2bf(rowp[2 * d + e]);
+      kc[slot_cur + e] = f2h(rowp[d + e]);
+      vc[slot_cur + e] = f2h(rowp[2 * d + e]);
     }
   }
   const int32_t* hr = hist + (int64_t)r * max_len;
@@ -232,7 +233,7 @@ __global__ void __launch_bounds__(128) decoder_self_attention_fast(
 #pragma unroll
         for (int e = 0; e < HD; ++e) {
           float kv = rowp[d + e];
-          if constexpr (sizeof(KV) == 2) kv = bf2f(f2bf(kv));  // the stored (rounded) key
+          if constexpr (sizeof(KV) == 2) kv = h2f(f2h(kv));  // the stored (rounded) key
           acc = fmaf(q[e], kv, acc);
         }
       } else {
@@ -272,7 +273,7 @@ __global__ void __launch_bounds__(128) decoder_self_attention_fast(
     const int e = lane + 32 * i;
     if (e < HD) {
       if (out) out[o + e] = acc[i];
-      if (out16) out16[o + e] = f2bf(acc[i]);
+      if (out16) out16[o + e] = f2h(acc[i]);
     }
   }
 }
@@ -285,7 +286,7 @@ template <typename KV>
 __global__ void __launch_bounds__(256) cross_attention_kernel(
     const float* __restrict__ cq, int64_t ldcq, const KV* __restrict__ ck,
     const KV* __restrict__ cv, int64_t ldkv, int beam, int seq, int heads, int hd, float scale,
-    const float* __restrict__ mask, float* __restrict__ out, __nv_bfloat16* __restrict__ out16,
+    const float* __restrict__ mask, float* __restrict__ out, h16* __restrict__ out16,
     int64_t ldo, int exact, int* d_bad) {
   pdl_enter();
   extern __shared__ float sm[];
@@ -313,12 +314,12 @@ __global__ void __launch_bounds__(256) cross_attention_kernel(
 // Cross-attention, specialised: K/V staged raw (16-byte copies, K rows padded
 // by 16 B so 128-bit row reads are conflict-free), each thread scores one key
 // for two beams per pass (one K load feeds two FMA chains), one warp per beam
-// softmax, and P.V with paired columns (bf16x2 / float2 loads).
+// softmax, and P.V with paired columns (f16x2 / float2 loads).
 template <typename KV, int HD>
 __global__ void __launch_bounds__(128) cross_attention_fast(
     const float* __restrict__ cq, int64_t ldcq, const KV* __restrict__ ck,
     const KV* __restrict__ cv, int64_t ldkv, int beam, int seq, int heads, float scale,
-    const float* __restrict__ mask, float* __restrict__ out, __nv_bfloat16* __restrict__ out16,
+    const float* __restrict__ mask, float* __restrict__ out, h16* __restrict__ out16,
     int64_t ldo, int exact, int* d_bad) {
   pdl_enter();
   constexpr int EV = 16 / sizeof(KV);
@@ -408,8 +409,9 @@ __global__ void __launch_bounds__(128) cross_attention_fast(
       float v0, v1;
       if constexpr (sizeof(KV) == 2) {
         const uint32_t raw = *reinterpret_cast<const uint32_t*>(Vt + j * HD + e);
-        v0 = __uint_as_float(raw << 16);
-        v1 = __uint_as_float(raw & 0xffff0000u);
+        const float2 f = __half22float2(*reinterpret_cast<const h16x2*>(&raw));
+        v0 = f.x;
+        v1 = f.y;
       } else {
         const float2 f = *reinterpret_cast<const float2*>(Vt + j * HD + e);
         v0 = f.x;
@@ -423,7 +425,7 @@ __global__ void __launch_bounds__(128) cross_attention_fast(
       out[o] = a0;
       out[o + 1] = a1;
     }
-    if (out16) *reinterpret_cast<__nv_bfloat162*>(out16 + o) = __floats2bfloat162_rn(a0, a1);
+    if (out16) *reinterpret_cast<h16x2*>(out16 + o) = __floats2half2_rn(a0, a1);
   }
 }
 
@@ -433,7 +435,7 @@ __global__ void __launch_bounds__(128) decoder_self_attention_kernel(
     const float* __restrict__ sqkv, int64_t ldq, KV* __restrict__ kc, KV* __restrict__ vc,
     const int32_t* __restrict__ hist, const int32_t* __restrict__ d_cur, int rows, int heads,
     int hd, int max_len, float scale, float* __restrict__ out,
-    __nv_bfloat16* __restrict__ out16, int64_t ldo, int exact) {
+    h16* __restrict__ out16, int64_t ldo, int exact) {
   pdl_enter();
   extern __shared__ float sm[];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -459,10 +461,10 @@ __global__ void __launch_bounds__(128) decoder_self_attention_kernel(
         kc[slot_cur + e] = kn[i];
         vc[slot_cur + e] = vn[i];
       } else {
-        kc[slot_cur + e] = f2bf(kn[i]);
-        vc[slot_cur + e] = f2bf(vn[i]);
-        kn[i] = bf2f(f2bf(kn[i]));
-        vn[i] = bf2f(f2bf(vn[i]));
+        kc[slot_cur + e] = f2h(kn[i]);
+        vc[slot_cur + e] = f2h(vn[i]);
+        kn[i] = h2f(f2h(kn[i]));
+        vn[i] = h2f(f2h(vn[i]));
       }
     }
   }
@@ -498,7 +500,7 @@ __global__ void __launch_bounds__(128) decoder_self_attention_kernel(
     int e = lane + 32 * i;
     if (e < hd) {
       if (out) out[o + e] = acc[i];
-      if (out16) out16[o + e] = f2bf(acc[i]);
+      if (out16) out16[o + e] = f2h(acc[i]);
     }
   }
 }
@@ -515,7 +517,7 @@ __global__ void __launch_bounds__(128) decoder_self_attention_kernel(
 template <int NC, int HC>
 __global__ void __launch_bounds__(256, 4) encoder_attention_tiled(
     const float* __restrict__ qkv, int64_t ldq, int seq, int heads, int hd, float scale,
-    const float* __restrict__ mask, float* __restrict__ out, __nv_bfloat16* __restrict__ out16,
+    const float* __restrict__ mask, float* __restrict__ out, h16* __restrict__ out16,
     int64_t ldo, int exact, int* d_bad) {
   pdl_enter();
   extern __shared__ float sm[];
@@ -622,7 +624,7 @@ __global__ void __launch_bounds__(256, 4) encoder_attention_tiled(
         const int e = tj + 16 * c;
         if (e < hd) {
           if (out) out[orow + e] = o[a][c];
-          if (out16) out16[orow + e] = f2bf(o[a][c]);
+          if (out16) out16[orow + e] = f2h(o[a][c]);
         }
       }
     }
@@ -664,8 +666,8 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 }
 
 // ---------------------------------------------------------------------------
-// Decoder self-attention, bf16 KV cache (throughput mode). CTA per beam row;
-// thread lt owns 8 consecutive model dims (one 16-byte bf16 load per cached
+// Decoder self-attention, fp16 KV cache (throughput mode). CTA per beam row;
+// thread lt owns 8 consecutive model dims (one 16-byte fp16 load per cached
 // position), so a cached slot row (all heads, 2 KB) is read as one coalesced
 // segment instead of per-head 128-byte pieces; G = blockDim / (d/8) position
 // groups stream disjoint positions with U loads in flight per thread. Head
@@ -674,10 +676,10 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 // ---------------------------------------------------------------------------
 template <int HD, int U>
 __global__ void __launch_bounds__(256, 4) decoder_self_attention_rows(
-    const float* __restrict__ sqkv, int64_t ldq, __nv_bfloat16* __restrict__ kc,
-    __nv_bfloat16* __restrict__ vc, const int32_t* __restrict__ hist,
+    const float* __restrict__ sqkv, int64_t ldq, h16* __restrict__ kc,
+    h16* __restrict__ vc, const int32_t* __restrict__ hist,
     const int32_t* __restrict__ d_cur, int rows, int heads, int max_len, float scale,
-    float* __restrict__ out, __nv_bfloat16* __restrict__ out16, int64_t ldo) {
+    float* __restrict__ out, h16* __restrict__ out16, int64_t ldo) {
   pdl_enter();
   constexpr int TPH = HD / 8;  // threads per head
   extern __shared__ __align__(16) float smf[];
@@ -711,12 +713,12 @@ __global__ void __launch_bounds__(256, 4) decoder_self_attention_rows(
   }
   uint4 kpk, vpk;
   {
-    __nv_bfloat162 t2[4];
+    h16x2 t2[4];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) t2[i] = __floats2bfloat162_rn(kn[2 * i], kn[2 * i + 1]);
+    for (int i = 0; i < 4; ++i) t2[i] = __floats2half2_rn(kn[2 * i], kn[2 * i + 1]);
     kpk = *reinterpret_cast<uint4*>(t2);
 #pragma unroll
-    for (int i = 0; i < 4; ++i) t2[i] = __floats2bfloat162_rn(vn[2 * i], vn[2 * i + 1]);
+    for (int i = 0; i < 4; ++i) t2[i] = __floats2half2_rn(vn[2 * i], vn[2 * i + 1]);
     vpk = *reinterpret_cast<uint4*>(t2);
   }
   if (g == 0) {
@@ -738,7 +740,7 @@ __global__ void __launch_bounds__(256, 4) decoder_self_attention_rows(
     for (int u = 0; u < U; ++u) {
       const int t = t0 + u * G;
       float f[8];
-      unpack16<__nv_bfloat16>(raw[u], f);
+      unpack16<h16>(raw[u], f);
       float p = 0.0f;
 #pragma unroll
       for (int j = 0; j < 8; ++j) p = fmaf(q[j], f[j], p);
@@ -773,7 +775,7 @@ __global__ void __launch_bounds__(256, 4) decoder_self_attention_rows(
       if (t <= cur) {
         const float p = Sh[t];
         float f[8];
-        unpack16<__nv_bfloat16>(raw[u], f);
+        unpack16<h16>(raw[u], f);
 #pragma unroll
         for (int j = 0; j < 8; ++j) acc[j] = fmaf(p, f[j], acc[j]);
       }
@@ -795,9 +797,9 @@ __global__ void __launch_bounds__(256, 4) decoder_self_attention_rows(
   }
   const int64_t o = (int64_t)r * ldo + lt * 8;
   if (out16) {
-    __nv_bfloat162 t2[4];
+    h16x2 t2[4];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) t2[i] = __floats2bfloat162_rn(acc[2 * i], acc[2 * i + 1]);
+    for (int i = 0; i < 4; ++i) t2[i] = __floats2half2_rn(acc[2 * i], acc[2 * i + 1]);
     *reinterpret_cast<uint4*>(out16 + o) = *reinterpret_cast<uint4*>(t2);
   }
   if (out) {
@@ -806,16 +808,16 @@ __global__ void __launch_bounds__(256, 4) decoder_self_attention_rows(
   }
 }
 
-// ---- warp-level bf16 tensor-core helpers (mma.sync m16n8k16, ldmatrix) ----
+// ---- warp-level fp16 tensor-core helpers (mma.sync m16n8k16, ldmatrix) ----
 // Decode attention is a handful of tiny per-(item, head) products (M = beams
 // <= 8); the legacy warp MMA does them in a few dozen instructions where the
 // FMA formulation needs thousands, which is what bounds these kernels. fp32
-// queries / probabilities enter as a bf16 hi + lo pair (two MMAs), so the
-// products keep ~16 mantissa bits against the bf16 keys/values they meet.
-__device__ __forceinline__ void mma_bf16_16816(float* c, const uint32_t* a, uint32_t b0,
+// queries / probabilities enter as a fp16 hi + lo pair (two MMAs), so the
+// products keep ~16 mantissa bits against the fp16 keys/values they meet.
+__device__ __forceinline__ void mma_f16_16816(float* c, const uint32_t* a, uint32_t b0,
                                                uint32_t b1) {
   asm volatile(
-      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
       "{%8,%9}, {%0,%1,%2,%3};"
       : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
@@ -830,16 +832,16 @@ __device__ __forceinline__ void ldsm_x4_t(uint32_t* r, const void* p) {
                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
                : "r"(sm_u32(p)));
 }
-// (x0, x1) -> packed bf16x2 hi and the bf16x2 residual lo
+// (x0, x1) -> packed f16x2 hi and the f16x2 residual lo
 __device__ __forceinline__ void split2(float x0, float x1, uint32_t& hi, uint32_t& lo) {
-  const __nv_bfloat162 h = __floats2bfloat162_rn(x0, x1);
-  const float2 hf = __bfloat1622float2(h);
-  const __nv_bfloat162 l = __floats2bfloat162_rn(x0 - hf.x, x1 - hf.y);
+  const h16x2 h = __floats2half2_rn(x0, x1);
+  const float2 hf = __half22float2(h);
+  const h16x2 l = __floats2half2_rn(x0 - hf.x, x1 - hf.y);
   hi = *reinterpret_cast<const uint32_t*>(&h);
   lo = *reinterpret_cast<const uint32_t*>(&l);
 }
 
-// Cross-attention on warp MMAs, bf16 K/V (throughput mode). One warp per
+// Cross-attention on warp MMAs, fp16 K/V (throughput mode). One warp per
 // (item, head): the item's K and V head slices arrive by bulk copies into
 // padded smem rows (144 B: conflict-free ldmatrix), then
 //   S^T [pos x beam] = K . Q^T      (A = K via ldmatrix, B = Q^T hi/lo)
@@ -848,9 +850,9 @@ __device__ __forceinline__ void split2(float x0, float x1, uint32_t& hi, uint32_
 // NT = position tiles of 16 (seq <= 16 NT), beams <= 8.
 template <int HD, int NT>
 __global__ void __launch_bounds__(32) cross_attention_mma(
-    const float* __restrict__ cq, int64_t ldcq, const __nv_bfloat16* __restrict__ ck,
-    const __nv_bfloat16* __restrict__ cv, int64_t ldkv, int beam, int seq, float scale,
-    const float* __restrict__ mask, float* __restrict__ out, __nv_bfloat16* __restrict__ out16,
+    const float* __restrict__ cq, int64_t ldcq, const h16* __restrict__ ck,
+    const h16* __restrict__ cv, int64_t ldkv, int beam, int seq, float scale,
+    const float* __restrict__ mask, float* __restrict__ out, h16* __restrict__ out16,
     int64_t ldo, int* d_bad) {
   constexpr int RS = HD * 2 + 16;  // padded smem row bytes
   constexpr int NP = NT * 16;
@@ -867,8 +869,8 @@ __global__ void __launch_bounds__(32) cross_attention_mma(
   }
   __syncwarp();
   pdl_enter();
-  const __nv_bfloat16* kb = ck + (int64_t)b * seq * ldkv + h * HD;
-  const __nv_bfloat16* vb = cv + (int64_t)b * seq * ldkv + h * HD;
+  const h16* kb = ck + (int64_t)b * seq * ldkv + h * HD;
+  const h16* vb = cv + (int64_t)b * seq * ldkv + h * HD;
   for (int x = lane; x < 2 * seq; x += 32) {
     const int t = x >> 1;
     if (x & 1) bulk_g2s(Vs + t * RS, vb + (int64_t)t * ldkv, HD * 2, &bar);
@@ -905,8 +907,8 @@ __global__ void __launch_bounds__(32) cross_attention_mma(
     for (int kk = 0; kk < HD / 16; ++kk) {
       uint32_t a[4];
       ldsm_x4(a, Ks + (16 * m + lrow) * RS + (16 * kk + lcol) * 2);
-      mma_bf16_16816(sc[m], a, qh[kk][0], qh[kk][1]);
-      mma_bf16_16816(sc[m], a, ql[kk][0], ql[kk][1]);
+      mma_f16_16816(sc[m], a, qh[kk][0], qh[kk][1]);
+      mma_f16_16816(sc[m], a, ql[kk][0], ql[kk][1]);
     }
   }
   // ---- softmax over positions, per beam column (2 per lane: 2t4, 2t4+1) ----
@@ -964,8 +966,8 @@ __global__ void __launch_bounds__(32) cross_attention_mma(
     for (int m = 0; m < HD / 16; ++m) {
       uint32_t a[4];
       ldsm_x4_t(a, Vs + (16 * kk + vrow) * RS + (16 * m + vcol) * 2);
-      mma_bf16_16816(oc[m], a, bh0, bh1);
-      mma_bf16_16816(oc[m], a, bl0, bl1);
+      mma_f16_16816(oc[m], a, bh0, bh1);
+      mma_f16_16816(oc[m], a, bl0, bl1);
     }
   }
   // ---- normalise and store: lane holds dims {16m + g, +8} x beams {2t4, 2t4+1} ----
@@ -987,18 +989,18 @@ __global__ void __launch_bounds__(32) cross_attention_mma(
         const int dd = 16 * m + g + 8 * hh;
         const float v = oc[m][2 * hh + j] * inv;
         if (out) out[o + dd] = v;
-        if (out16) out16[o + dd] = f2bf(v);
+        if (out16) out16[o + dd] = f2h(v);
       }
     }
   }
 }
 
 
-int make_tmap_bf16_sw128(CUtensorMap* map, const void* ptr, int64_t rows, int64_t cols,
+int make_tmap_f16_sw128(CUtensorMap* map, const void* ptr, int64_t rows, int64_t cols,
                          int64_t ld, int box_cols, int box_rows);
 
 // Cross-attention on warp MMAs, TMA variant (head_dim 64, seq <= 64): the K
-// and V head slices of (item, head) arrive as two 64x64 bf16 TMA boxes with
+// and V head slices of (item, head) arrive as two 64x64 fp16 TMA boxes with
 // the 128-byte swizzle (no smem padding, conflict-free ldmatrix), and the
 // probabilities reuse the K buffer once the scores are done, so a CTA needs
 // 16 KB and all (item, head) CTAs are resident in one wave.
@@ -1013,7 +1015,7 @@ constexpr int kCrossWarps = 14;
 __global__ void __launch_bounds__(32 * kCrossWarps) cross_attention_tma(
     const __grid_constant__ CUtensorMap tk, const __grid_constant__ CUtensorMap tv,
     const float* __restrict__ cq, int64_t ldcq, int beam, int seq, float scale,
-    const float* __restrict__ mask, float* __restrict__ out, __nv_bfloat16* __restrict__ out16,
+    const float* __restrict__ mask, float* __restrict__ out, h16* __restrict__ out16,
     int64_t ldo, int* d_bad, int heads, int npairs, int nslab, int64_t slab,
     const float* __restrict__ qbias) {
   constexpr int HD = 64, NT = 4, NP = 64;
@@ -1093,8 +1095,8 @@ __global__ void __launch_bounds__(32 * kCrossWarps) cross_attention_tma(
     for (int kk = 0; kk < HD / 16; ++kk) {
       uint32_t a[4];
       ldsm_x4(a, Ks + sw128(16 * m + lrow, 2 * kk + lch));
-      mma_bf16_16816(sc[m], a, qh[kk][0], qh[kk][1]);
-      mma_bf16_16816(sc[m], a, ql[kk][0], ql[kk][1]);
+      mma_f16_16816(sc[m], a, qh[kk][0], qh[kk][1]);
+      mma_f16_16816(sc[m], a, ql[kk][0], ql[kk][1]);
     }
   }
   __syncwarp();  // K is dead: Ps may overwrite it
@@ -1151,8 +1153,8 @@ __global__ void __launch_bounds__(32 * kCrossWarps) cross_attention_tma(
     for (int m = 0; m < HD / 16; ++m) {
       uint32_t a[4];
       ldsm_x4_t(a, Vs + sw128(16 * kk + vrow, 2 * m + vch));
-      mma_bf16_16816(oc[m], a, bh0, bh1);
-      mma_bf16_16816(oc[m], a, bl0, bl1);
+      mma_f16_16816(oc[m], a, bh0, bh1);
+      mma_f16_16816(oc[m], a, bl0, bl1);
     }
   }
   const float inv0 = l0 > 0.0f ? 1.0f / l0 : 0.0f, inv1 = l1 > 0.0f ? 1.0f / l1 : 0.0f;
@@ -1173,13 +1175,13 @@ __global__ void __launch_bounds__(32 * kCrossWarps) cross_attention_tma(
         const int dd = 16 * m + g + 8 * hh;
         const float v = oc[m][2 * hh + j] * inv;
         if (out) out[o + dd] = v;
-        if (out16) out16[o + dd] = f2bf(v);
+        if (out16) out16[o + dd] = f2h(v);
       }
     }
   }
 }
 
-// Decoder self-attention on warp MMAs (bf16 cache, head_dim 64): warp per
+// Decoder self-attention on warp MMAs (fp16 cache, head_dim 64): warp per
 // (beam row, head). Cached positions stream through an NS-stage (default 3) shared-memory
 // ring in chunks of 16 (cp.async 16-byte pieces of the hist-gathered slot rows,
 // 128-byte rows with an XOR chunk swizzle, so ldmatrix is conflict-free); this
@@ -1198,10 +1200,10 @@ __device__ __forceinline__ void cp16(uint32_t dst, const void* src) {
 
 template <int NS>
 __global__ void __launch_bounds__(32) decoder_self_attention_mma(
-    const float* __restrict__ sqkv, int64_t ldq, __nv_bfloat16* __restrict__ kc,
-    __nv_bfloat16* __restrict__ vc, const int32_t* __restrict__ hist,
+    const float* __restrict__ sqkv, int64_t ldq, h16* __restrict__ kc,
+    h16* __restrict__ vc, const int32_t* __restrict__ hist,
     const int32_t* __restrict__ d_cur, int rows, int heads, int max_len, float scale,
-    float* __restrict__ out, __nv_bfloat16* __restrict__ out16, int64_t ldo) {
+    float* __restrict__ out, h16* __restrict__ out16, int64_t ldo) {
   constexpr int HD = 64;
   __shared__ __align__(128) uint8_t ring[NS][2][16 * 128];  // [stage][K|V][16 rows x 128 B]
   __shared__ int phys_s[128];
@@ -1215,12 +1217,12 @@ __global__ void __launch_bounds__(32) decoder_self_attention_mma(
   const float* rowp = sqkv + (int64_t)r * ldq + h * HD;
   const float2 kn = *reinterpret_cast<const float2*>(rowp + d + 2 * lane);
   const float2 vn = *reinterpret_cast<const float2*>(rowp + 2 * d + 2 * lane);
-  const __nv_bfloat162 kb2 = __floats2bfloat162_rn(kn.x, kn.y);
-  const __nv_bfloat162 vb2 = __floats2bfloat162_rn(vn.x, vn.y);
+  const h16x2 kb2 = __floats2half2_rn(kn.x, kn.y);
+  const h16x2 vb2 = __floats2half2_rn(vn.x, vn.y);
   {
     const int64_t slot = ((int64_t)cur * rows + r) * d + h * HD + 2 * lane;
-    *reinterpret_cast<__nv_bfloat162*>(kc + slot) = kb2;
-    *reinterpret_cast<__nv_bfloat162*>(vc + slot) = vb2;
+    *reinterpret_cast<h16x2*>(kc + slot) = kb2;
+    *reinterpret_cast<h16x2*>(vc + slot) = vb2;
   }
   // q^T fragments (column 0 = this row; other columns zero)
   uint32_t qh[4][2], ql[4][2];
@@ -1276,8 +1278,8 @@ __global__ void __launch_bounds__(32) decoder_self_attention_mma(
     if (cur / 16 == c) {  // this step's k / v (row cur % 16) from registers
       const int rr = cur % 16;
       const int ch = (2 * lane) / 8, within = (2 * lane) % 8;
-      *reinterpret_cast<__nv_bfloat162*>(&ring[s][0][0] + swz(rr, ch) + within * 2) = kb2;
-      *reinterpret_cast<__nv_bfloat162*>(&ring[s][1][0] + swz(rr, ch) + within * 2) = vb2;
+      *reinterpret_cast<h16x2*>(&ring[s][0][0] + swz(rr, ch) + within * 2) = kb2;
+      *reinterpret_cast<h16x2*>(&ring[s][1][0] + swz(rr, ch) + within * 2) = vb2;
     }
     __syncwarp();
     const uint8_t* Ks = &ring[s][0][0];
@@ -1287,8 +1289,8 @@ __global__ void __launch_bounds__(32) decoder_self_attention_mma(
     for (int kk = 0; kk < 4; ++kk) {  // hi and lo products in separate chains
       uint32_t a[4];
       ldsm_x4(a, Ks + swz(lrow, 2 * kk + lch));
-      mma_bf16_16816(sc, a, qh[kk][0], qh[kk][1]);
-      mma_bf16_16816(sl, a, ql[kk][0], ql[kk][1]);
+      mma_f16_16816(sc, a, qh[kk][0], qh[kk][1]);
+      mma_f16_16816(sl, a, ql[kk][0], ql[kk][1]);
     }
 #pragma unroll
     for (int j = 0; j < 4; ++j) sc[j] += sl[j];
@@ -1322,8 +1324,8 @@ __global__ void __launch_bounds__(32) decoder_self_attention_mma(
       oc[m][0] *= corr; oc[m][1] *= corr; oc[m][2] *= corr; oc[m][3] *= corr;
       uint32_t a[4];
       ldsm_x4_t(a, Vs + swz(vrow, 2 * m + vch));
-      mma_bf16_16816(oc[m], a, bh0, bh1);
-      mma_bf16_16816(oc[m], a, bl0, bl1);
+      mma_f16_16816(oc[m], a, bh0, bh1);
+      mma_f16_16816(oc[m], a, bl0, bl1);
     }
     __syncwarp();  // stage s consumed
     if (c + NS - 1 < nchunk) issue(c + NS - 1, (c + NS - 1) % NS);
@@ -1337,20 +1339,20 @@ __global__ void __launch_bounds__(32) decoder_self_attention_mma(
     for (int m = 0; m < 4; ++m) {
       const float v0 = oc[m][0] * inv, v1 = oc[m][2] * inv;
       if (out) { out[o + 16 * m + g] = v0; out[o + 16 * m + g + 8] = v1; }
-      if (out16) { out16[o + 16 * m + g] = f2bf(v0); out16[o + 16 * m + g + 8] = f2bf(v1); }
+      if (out16) { out16[o + 16 * m + g] = f2h(v0); out16[o + 16 * m + g + 8] = f2h(v1); }
     }
   }
 }
 
 // Encoder self-attention on warp MMAs (throughput mode, head_dim 64, seq <= 64):
 // CTA per (item, head), warp per 16 queries. Q, K, V (fp32 from the QKV GEMM)
-// are split into bf16 hi + lo halves in XOR-swizzled shared memory; scores
+// are split into fp16 hi + lo halves in XOR-swizzled shared memory; scores
 // S = Q K^T take three MMA products (hi.hi + hi.lo + lo.hi), the softmax runs
 // on the accumulator fragments (FlashAttention-2 register layout), and P V
 // reuses the probability fragments as A operands (P and V split likewise).
 __global__ void __launch_bounds__(128) encoder_attention_mma(
     const float* __restrict__ qkv, int64_t ldq, int seq, int heads, float scale,
-    const float* __restrict__ mask, float* __restrict__ out, __nv_bfloat16* __restrict__ out16,
+    const float* __restrict__ mask, float* __restrict__ out, h16* __restrict__ out16,
     int64_t ldo, int* d_bad) {
   constexpr int HD = 64, NP = 64;
   __shared__ __align__(128) uint8_t sm[6][NP * 128];  // Qh Ql Kh Kl Vh Vl, rows of 128 B
@@ -1398,9 +1400,9 @@ __global__ void __launch_bounds__(128) encoder_attention_mma(
       asm volatile("ldmatrix.sync.aligned.m8n8.x2.shared.b16 {%0,%1}, [%2];"
                    : "=r"(kl[0]), "=r"(kl[1])
                    : "r"(sm_u32(&sm[3][0] + swz(krow, kch))));
-      mma_bf16_16816(sc[n], qa, kh[0], kh[1]);
-      mma_bf16_16816(sc[n], qa, kl[0], kl[1]);
-      mma_bf16_16816(sc[n], qb, kh[0], kh[1]);
+      mma_f16_16816(sc[n], qa, kh[0], kh[1]);
+      mma_f16_16816(sc[n], qa, kl[0], kl[1]);
+      mma_f16_16816(sc[n], qb, kh[0], kh[1]);
     }
   }
   // softmax per query row (rows g and g + 8 of the warp's tile)
@@ -1461,9 +1463,9 @@ __global__ void __launch_bounds__(128) encoder_attention_mma(
       asm volatile("ldmatrix.sync.aligned.m8n8.x2.trans.shared.b16 {%0,%1}, [%2];"
                    : "=r"(vl[0]), "=r"(vl[1])
                    : "r"(sm_u32(&sm[5][0] + swz(vrow, vch))));
-      mma_bf16_16816(oc[n], ph, vh[0], vh[1]);
-      mma_bf16_16816(oc[n], ph, vl[0], vl[1]);
-      mma_bf16_16816(oc[n], pl, vh[0], vh[1]);
+      mma_f16_16816(oc[n], ph, vh[0], vh[1]);
+      mma_f16_16816(oc[n], ph, vl[0], vl[1]);
+      mma_f16_16816(oc[n], pl, vh[0], vh[1]);
     }
   }
 #pragma unroll
@@ -1481,7 +1483,7 @@ __global__ void __launch_bounds__(128) encoder_attention_mma(
       const float v0 = oc[n][2 * r] * inv, v1 = oc[n][2 * r + 1] * inv;
       const int dd = 8 * n + 2 * t4;
       if (out) *reinterpret_cast<float2*>(out + o + dd) = make_float2(v0, v1);
-      if (out16) *reinterpret_cast<__nv_bfloat162*>(out16 + o + dd) = __floats2bfloat162_rn(v0, v1);
+      if (out16) *reinterpret_cast<h16x2*>(out16 + o + dd) = __floats2half2_rn(v0, v1);
     }
   }
 }
@@ -1500,14 +1502,14 @@ int attention_prepare() {
   const int big = 227 * 1024;
   if (cudaFuncSetAttribute(encoder_attention_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, big) ||
       cudaFuncSetAttribute(cross_attention_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, big) ||
-      cudaFuncSetAttribute(cross_attention_kernel<__nv_bfloat16>,
+      cudaFuncSetAttribute(cross_attention_kernel<h16>,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, big) ||
       cudaFuncSetAttribute(cross_attention_fast<float, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024) ||
       cudaFuncSetAttribute(cross_attention_fast<float, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024) ||
       cudaFuncSetAttribute(cross_attention_fast<float, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024) ||
-      cudaFuncSetAttribute(cross_attention_fast<__nv_bfloat16, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024) ||
-      cudaFuncSetAttribute(cross_attention_fast<__nv_bfloat16, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024) ||
-      cudaFuncSetAttribute(cross_attention_fast<__nv_bfloat16, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024) ||
+      cudaFuncSetAttribute(cross_attention_fast<h16, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024) ||
+      cudaFuncSetAttribute(cross_attention_fast<h16, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024) ||
+      cudaFuncSetAttribute(cross_attention_fast<h16, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024) ||
       cudaFuncSetAttribute(encoder_attention_tiled<4, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024) ||
       cudaFuncSetAttribute(cross_attention_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            kCrossWarps * 2 * 64 * 128 + 1024) ||
@@ -1525,7 +1527,7 @@ static void launch_self_fast(dim3 grid, size_t smem, cudaStream_t s, const float
                              float scale, float* out, void* out16, int64_t ldo, int exact) {
   launch_kernel(decoder_self_attention_fast<KV, HD>, grid, 128, smem, s, 1u, 
       sqkv, ldq, (KV*)kc, (KV*)vc, hist, d_cur, (int)rows, (int)heads, (int)max_len, scale, out,
-      reinterpret_cast<__nv_bfloat16*>(out16), ldo, exact);
+      reinterpret_cast<fq::h16*>(out16), ldo, exact);
 }
 
 }  // namespace fq
@@ -1545,7 +1547,7 @@ int fq_encoder_attention(const float* qkv, int64_t ldq, int64_t batch, int64_t s
       ldo % 2 == 0) {
     launch_kernel(encoder_attention_mma, (unsigned)(batch * heads), 128, 0, as_stream(stream), 1u,
                   qkv, ldq, (int)seq, (int)heads, scale, mask, out,
-                  reinterpret_cast<__nv_bfloat16*>(out16), ldo, d_bad);
+                  reinterpret_cast<fq::h16*>(out16), ldo, d_bad);
     return launch_status("fq_encoder_attention");
   }
   if (seq <= 64 && ldq % 4 == 0 && ((uintptr_t)qkv & 15) == 0) {
@@ -1554,11 +1556,11 @@ int fq_encoder_attention(const float* qkv, int64_t ldq, int64_t batch, int64_t s
     if (head_dim <= 64)
       launch_kernel(encoder_attention_tiled<4, 4>, (unsigned)(batch * heads), 256, smem,
                     as_stream(stream), 1u, qkv, ldq, (int)seq, (int)heads, (int)head_dim, scale,
-                    mask, out, reinterpret_cast<__nv_bfloat16*>(out16), ldo, exact, d_bad);
+                    mask, out, reinterpret_cast<fq::h16*>(out16), ldo, exact, d_bad);
     else
       launch_kernel(encoder_attention_tiled<4, 8>, (unsigned)(batch * heads), 256, smem,
                     as_stream(stream), 1u, qkv, ldq, (int)seq, (int)heads, (int)head_dim, scale,
-                    mask, out, reinterpret_cast<__nv_bfloat16*>(out16), ldo, exact, d_bad);
+                    mask, out, reinterpret_cast<fq::h16*>(out16), ldo, exact, d_bad);
     return launch_status("fq_encoder_attention");
   }
   const int threads = 256;
@@ -1567,7 +1569,7 @@ int fq_encoder_attention(const float* qkv, int64_t ldq, int64_t batch, int64_t s
                (long long)seq);
   launch_kernel(encoder_attention_kernel, (unsigned)(batch * heads), threads, smem, as_stream(stream), 1u,
       qkv, ldq, (int)seq, (int)heads, (int)head_dim, scale, mask, out,
-      reinterpret_cast<__nv_bfloat16*>(out16), ldo, exact, d_bad);
+      reinterpret_cast<fq::h16*>(out16), ldo, exact, d_bad);
   return launch_status("fq_encoder_attention");
 }
 
@@ -1590,9 +1592,9 @@ int fq_decoder_self_attention(const float* sqkv, int64_t ldq, void* kcache, void
     auto kern = ns == 2 ? decoder_self_attention_mma<2>
               : ns == 4 ? decoder_self_attention_mma<4> : decoder_self_attention_mma<3>;
     launch_kernel(kern, dim3((unsigned)rows, (unsigned)heads), 32, 0,
-                  as_stream(stream), 1u, sqkv, ldq, (__nv_bfloat16*)kcache,
-                  (__nv_bfloat16*)vcache, hist, d_cur, (int)rows, (int)heads, (int)max_len,
-                  scale, out, reinterpret_cast<__nv_bfloat16*>(out16), ldo);
+                  as_stream(stream), 1u, sqkv, ldq, (h16*)kcache,
+                  (h16*)vcache, hist, d_cur, (int)rows, (int)heads, (int)max_len,
+                  scale, out, reinterpret_cast<fq::h16*>(out16), ldo);
     return launch_status("fq_decoder_self_attention");
   }
   {
@@ -1610,9 +1612,9 @@ int fq_decoder_self_attention(const float* sqkv, int64_t ldq, void* kcache, void
                           (size_t)(G - 1) * d * 4 + 16;
 #define FQ_SELF_ROWS(HD)                                                                       \
   launch_kernel(decoder_self_attention_rows<HD, 8>, dim3((unsigned)rows), threads, smem,       \
-                as_stream(stream), 1u, sqkv, ldq, (__nv_bfloat16*)kcache,                     \
-                (__nv_bfloat16*)vcache, hist, d_cur, (int)rows, (int)heads, (int)max_len, scale, \
-                out, reinterpret_cast<__nv_bfloat16*>(out16), ldo)
+                as_stream(stream), 1u, sqkv, ldq, (h16*)kcache,                     \
+                (h16*)vcache, hist, d_cur, (int)rows, (int)heads, (int)max_len, scale, \
+                out, reinterpret_cast<fq::h16*>(out16), ldo)
       if (head_dim == 32) FQ_SELF_ROWS(32);
       else if (head_dim == 64) FQ_SELF_ROWS(64);
       else FQ_SELF_ROWS(128);
@@ -1637,10 +1639,10 @@ int fq_decoder_self_attention(const float* sqkv, int64_t ldq, void* kcache, void
       else if (head_dim == 64) FQ_SELF(float, 64);
       else FQ_SELF(float, 128);
     } else {
-      if (head_dim == 16) FQ_SELF(__nv_bfloat16, 16);
-      else if (head_dim == 32) FQ_SELF(__nv_bfloat16, 32);
-      else if (head_dim == 64) FQ_SELF(__nv_bfloat16, 64);
-      else FQ_SELF(__nv_bfloat16, 128);
+      if (head_dim == 16) FQ_SELF(h16, 16);
+      else if (head_dim == 32) FQ_SELF(h16, 32);
+      else if (head_dim == 64) FQ_SELF(h16, 64);
+      else FQ_SELF(h16, 128);
     }
 #undef FQ_SELF
     return launch_status("fq_decoder_self_attention");
@@ -1649,13 +1651,13 @@ int fq_decoder_self_attention(const float* sqkv, int64_t ldq, void* kcache, void
   if (kv_dtype == FQ_F32) {
     launch_kernel(decoder_self_attention_kernel<float>, grid, wpb * 32, smem, s, 1u, 
         sqkv, ldq, (float*)kcache, (float*)vcache, hist, d_cur, (int)rows, (int)heads,
-        (int)head_dim, (int)max_len, scale, out, reinterpret_cast<__nv_bfloat16*>(out16), ldo,
+        (int)head_dim, (int)max_len, scale, out, reinterpret_cast<fq::h16*>(out16), ldo,
         exact);
   } else {
-    launch_kernel(decoder_self_attention_kernel<__nv_bfloat16>, grid, wpb * 32, smem, s, 1u, 
-        sqkv, ldq, (__nv_bfloat16*)kcache, (__nv_bfloat16*)vcache, hist, d_cur, (int)rows,
+    launch_kernel(decoder_self_attention_kernel<h16>, grid, wpb * 32, smem, s, 1u, 
+        sqkv, ldq, (h16*)kcache, (h16*)vcache, hist, d_cur, (int)rows,
         (int)heads, (int)head_dim, (int)max_len, scale, out,
-        reinterpret_cast<__nv_bfloat16*>(out16), ldo, exact);
+        reinterpret_cast<fq::h16*>(out16), ldo, exact);
   }
   return launch_status("fq_decoder_self_attention");
 }
@@ -1674,13 +1676,13 @@ int fq_cross_attention_slabs(const float* q_slabs, int nslab, int64_t ldq, const
   CUtensorMap tk, tv;
   const int64_t nrows = batch * seq, ncols = heads * head_dim;
   int rc;
-  if ((rc = make_tmap_bf16_sw128(&tk, ck, nrows, ncols, ldkv, 64, 64)) != FQ_OK) return rc;
-  if ((rc = make_tmap_bf16_sw128(&tv, cv, nrows, ncols, ldkv, 64, 64)) != FQ_OK) return rc;
+  if ((rc = make_tmap_f16_sw128(&tk, ck, nrows, ncols, ldkv, 64, 64)) != FQ_OK) return rc;
+  if ((rc = make_tmap_f16_sw128(&tv, cv, nrows, ncols, ldkv, 64, 64)) != FQ_OK) return rc;
   const int npairs = (int)(batch * heads);
   launch_kernel(cross_attention_tma, (unsigned)((npairs + kCrossWarps - 1) / kCrossWarps),
                 32 * kCrossWarps, (size_t)kCrossWarps * 2 * 64 * 128 + 1024, as_stream(stream),
                 1u, tk, tv, q_slabs, ldq, (int)beam, (int)seq, scale, mask, out,
-                reinterpret_cast<__nv_bfloat16*>(out16), ldo, d_bad, (int)heads, npairs, nslab,
+                reinterpret_cast<fq::h16*>(out16), ldo, d_bad, (int)heads, npairs, nslab,
                 (int64_t)(batch * beam) * ldq, q_bias);
   return launch_status("fq_cross_attention_slabs");
 }
@@ -1698,13 +1700,13 @@ int fq_cross_attention(const float* cq, int64_t ldcq, const void* ck, const void
       ((uintptr_t)cv & 15) == 0) {
     CUtensorMap tk, tv;
     const int64_t nrows = batch * seq, ncols = heads * head_dim;
-    if (make_tmap_bf16_sw128(&tk, ck, nrows, ncols, ldkv, 64, 64) == FQ_OK &&
-        make_tmap_bf16_sw128(&tv, cv, nrows, ncols, ldkv, 64, 64) == FQ_OK) {
+    if (make_tmap_f16_sw128(&tk, ck, nrows, ncols, ldkv, 64, 64) == FQ_OK &&
+        make_tmap_f16_sw128(&tv, cv, nrows, ncols, ldkv, 64, 64) == FQ_OK) {
       const int npairs = (int)(batch * heads);
       launch_kernel(cross_attention_tma, (unsigned)((npairs + kCrossWarps - 1) / kCrossWarps),
                     32 * kCrossWarps, (size_t)kCrossWarps * 2 * 64 * 128 + 1024,
                     as_stream(stream), 1u, tk, tv, cq, ldcq, (int)beam, (int)seq, scale, mask,
-                    out, reinterpret_cast<__nv_bfloat16*>(out16), ldo, d_bad, (int)heads,
+                    out, reinterpret_cast<fq::h16*>(out16), ldo, d_bad, (int)heads,
                     npairs, 0, (int64_t)0, (const float*)nullptr);
       return launch_status("fq_cross_attention");
     }
@@ -1717,8 +1719,8 @@ int fq_cross_attention(const float* cq, int64_t ldcq, const void* ck, const void
     const size_t msmem = (size_t)2 * nt * 16 * (head_dim * 2 + 16);
 #define FQ_CROSS_M(HD, NT)                                                                     \
   launch_kernel(cross_attention_mma<HD, NT>, grid, 32, msmem, as_stream(stream), 1u, cq, ldcq,  \
-                (const __nv_bfloat16*)ck, (const __nv_bfloat16*)cv, ldkv, (int)beam, (int)seq,  \
-                scale, mask, out, reinterpret_cast<__nv_bfloat16*>(out16), ldo, d_bad)
+                (const h16*)ck, (const h16*)cv, ldkv, (int)beam, (int)seq,  \
+                scale, mask, out, reinterpret_cast<fq::h16*>(out16), ldo, d_bad)
 #define FQ_CROSS_MH(HD)                      \
   if (nt == 1) FQ_CROSS_M(HD, 1);            \
   else if (nt == 2) FQ_CROSS_M(HD, 2);       \
@@ -1744,15 +1746,15 @@ int fq_cross_attention(const float* cq, int64_t ldcq, const void* ck, const void
 #define FQ_CROSS(KV, HD)                                                                   \
   launch_kernel(cross_attention_fast<KV, HD>, grid, 128, fast_smem, s, 1u,                                \
       cq, ldcq, (const KV*)ck, (const KV*)cv, ldkv, (int)beam, (int)seq, (int)heads, scale, \
-      mask, out, reinterpret_cast<__nv_bfloat16*>(out16), ldo, exact, d_bad)
+      mask, out, reinterpret_cast<fq::h16*>(out16), ldo, exact, d_bad)
     if (kv_dtype == FQ_F32) {
       if (head_dim == 32) FQ_CROSS(float, 32);
       else if (head_dim == 64) FQ_CROSS(float, 64);
       else FQ_CROSS(float, 128);
     } else {
-      if (head_dim == 32) FQ_CROSS(__nv_bfloat16, 32);
-      else if (head_dim == 64) FQ_CROSS(__nv_bfloat16, 64);
-      else FQ_CROSS(__nv_bfloat16, 128);
+      if (head_dim == 32) FQ_CROSS(h16, 32);
+      else if (head_dim == 64) FQ_CROSS(h16, 64);
+      else FQ_CROSS(h16, 128);
     }
 #undef FQ_CROSS
     return launch_status("fq_cross_attention");
@@ -1763,13 +1765,13 @@ int fq_cross_attention(const float* cq, int64_t ldcq, const void* ck, const void
   if (kv_dtype == FQ_F32) {
     launch_kernel(cross_attention_kernel<float>, grid, threads, smem, as_stream(stream), 1u, 
         cq, ldcq, (const float*)ck, (const float*)cv, ldkv, (int)beam, (int)seq, (int)heads,
-        (int)head_dim, scale, mask, out, reinterpret_cast<__nv_bfloat16*>(out16), ldo, exact,
+        (int)head_dim, scale, mask, out, reinterpret_cast<fq::h16*>(out16), ldo, exact,
         d_bad);
   } else {
-    launch_kernel(cross_attention_kernel<__nv_bfloat16>, grid, threads, smem, as_stream(stream), 1u, 
-        cq, ldcq, (const __nv_bfloat16*)ck, (const __nv_bfloat16*)cv, ldkv, (int)beam,
+    launch_kernel(cross_attention_kernel<h16>, grid, threads, smem, as_stream(stream), 1u, 
+        cq, ldcq, (const h16*)ck, (const h16*)cv, ldkv, (int)beam,
         (int)seq, (int)heads, (int)head_dim, scale, mask, out,
-        reinterpret_cast<__nv_bfloat16*>(out16), ldo, exact, d_bad);
+        reinterpret_cast<fq::h16*>(out16), ldo, exact, d_bad);
   }
   return launch_status("fq_cross_attention");
 }

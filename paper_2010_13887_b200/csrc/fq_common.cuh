@@ -1,7 +1,7 @@
 // Shared helpers for the sm_100a kernels behind include/fq_abi.h.
 #pragma once
 
-#include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
@@ -65,8 +65,13 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
   return t;
 }
 
-__device__ __forceinline__ float bf2f(__nv_bfloat16 x) { return __bfloat162float(x); }
-__device__ __forceinline__ __nv_bfloat16 f2bf(float x) { return __float2bfloat16_rn(x); }
+// The 16-bit operand / storage type of the throughput mode (fp16: 11-bit
+// significand, the paper's own half precision; fp32 accumulation everywhere).
+using h16 = __half;
+using h16x2 = __half2;
+
+__device__ __forceinline__ float h2f(h16 x) { return __half2float(x); }
+__device__ __forceinline__ h16 f2h(float x) { return __float2half_rn(x); }
 
 // fp32 ops with explicit rounding so nvcc never contracts them into FMA
 // (two separately rounded fp32 operations).

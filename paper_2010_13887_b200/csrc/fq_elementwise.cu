@@ -20,7 +20,7 @@ __global__ void __launch_bounds__(256) layer_norm_kernel(
     const float* __restrict__ x, int64_t ldx, const float* __restrict__ bias,
     const float* __restrict__ res, int64_t ldr, const float* __restrict__ gamma,
     const float* __restrict__ beta, double eps, int d, float* __restrict__ out, int64_t ldo,
-    __nv_bfloat16* __restrict__ out16, int64_t ldo16) {
+    h16* __restrict__ out16, int64_t ldo16) {
   pdl_enter();
   extern __shared__ float srow[];
   __shared__ double red[8];
@@ -44,7 +44,7 @@ __global__ void __launch_bounds__(256) layer_norm_kernel(
     float n = (float)(((double)srow[j] - mean) * inv);
     float o = fadd_rn(fmul_rn(n, gamma[j]), beta[j]);  // kernels.py:35
     if (out) out[row * ldo + j] = o;
-    if (out16) out16[row * ldo16 + j] = f2bf(o);
+    if (out16) out16[row * ldo16 + j] = f2h(o);
   }
 }
 
@@ -57,7 +57,7 @@ __global__ void __launch_bounds__(256) layer_norm_warp_kernel(
     const float* __restrict__ x, int64_t ldx, const float* __restrict__ bias,
     const float* __restrict__ res, int64_t ldr, const float* __restrict__ gamma,
     const float* __restrict__ beta, double eps, int64_t rows, int d, float* __restrict__ out,
-    int64_t ldo, __nv_bfloat16* __restrict__ out16, int64_t ldo16) {
+    int64_t ldo, h16* __restrict__ out16, int64_t ldo16) {
   pdl_enter();
   const int lane = threadIdx.x & 31;
   const int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -105,7 +105,7 @@ __global__ void __launch_bounds__(256) layer_norm_warp_kernel(
       o.w = fadd_rn(fmul_rn((float)((u[i].w - mean) * inv), g.w), bb.w);
       if (out) *reinterpret_cast<float4*>(out + row * ldo + c) = o;
       if (out16) {
-        __nv_bfloat162 lo = __floats2bfloat162_rn(o.x, o.y), hi = __floats2bfloat162_rn(o.z, o.w);
+        h16x2 lo = __floats2half2_rn(o.x, o.y), hi = __floats2half2_rn(o.z, o.w);
         uint2 pk;
         pk.x = *reinterpret_cast<uint32_t*>(&lo);
         pk.y = *reinterpret_cast<uint32_t*>(&hi);
@@ -122,7 +122,7 @@ __global__ void __launch_bounds__(128) layer_norm_row128_kernel(
     const float* __restrict__ x, int64_t ldx, const float* __restrict__ bias,
     const float* __restrict__ res, int64_t ldr, const float* __restrict__ gamma,
     const float* __restrict__ beta, double eps, int d, float* __restrict__ out, int64_t ldo,
-    __nv_bfloat16* __restrict__ out16, int64_t ldo16) {
+    h16* __restrict__ out16, int64_t ldo16) {
   pdl_enter();
   __shared__ double red[2][4];
   const int64_t row = blockIdx.x;
@@ -170,7 +170,7 @@ __global__ void __launch_bounds__(128) layer_norm_row128_kernel(
     o.w = fadd_rn(fmul_rn((float)((u[i].w - mean) * inv), g.w), bb.w);
     if (out) *reinterpret_cast<float4*>(out + row * ldo + c) = o;
     if (out16) {
-      __nv_bfloat162 lo = __floats2bfloat162_rn(o.x, o.y), hi = __floats2bfloat162_rn(o.z, o.w);
+      h16x2 lo = __floats2half2_rn(o.x, o.y), hi = __floats2half2_rn(o.z, o.w);
       uint2 pk;
       pk.x = *reinterpret_cast<uint32_t*>(&lo);
       pk.y = *reinterpret_cast<uint32_t*>(&hi);
@@ -188,7 +188,7 @@ __global__ void __launch_bounds__(128) layer_norm_slabs_row128_kernel(
     const float* __restrict__ x, int64_t ld, int64_t slab, const float* __restrict__ bias,
     const float* __restrict__ res, int64_t ldr, const float* __restrict__ gamma,
     const float* __restrict__ beta, double eps, int d, float* __restrict__ out, int64_t ldo,
-    __nv_bfloat16* __restrict__ out16, int64_t ldo16) {
+    h16* __restrict__ out16, int64_t ldo16) {
   pdl_enter();
   __shared__ double red[2][4];
   const int64_t row = blockIdx.x;
@@ -248,7 +248,7 @@ __global__ void __launch_bounds__(128) layer_norm_slabs_row128_kernel(
     o.w = fadd_rn(fmul_rn((float)((u[i].w - mean) * inv), g.w), bb.w);
     if (out) *reinterpret_cast<float4*>(out + row * ldo + c) = o;
     if (out16) {
-      __nv_bfloat162 lo = __floats2bfloat162_rn(o.x, o.y), hi = __floats2bfloat162_rn(o.z, o.w);
+      h16x2 lo = __floats2half2_rn(o.x, o.y), hi = __floats2half2_rn(o.z, o.w);
       uint2 pk;
       pk.x = *reinterpret_cast<uint32_t*>(&lo);
       pk.y = *reinterpret_cast<uint32_t*>(&hi);
@@ -262,7 +262,7 @@ static inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t
 template <bool kBiasRes>
 static void launch_ln(const float* x, int64_t ldx, const float* bias, const float* res,
                       int64_t ldr, const float* gamma, const float* beta, double eps,
-                      int64_t rows, int64_t d, float* out, int64_t ldo, __nv_bfloat16* out16,
+                      int64_t rows, int64_t d, float* out, int64_t ldo, h16* out16,
                       int64_t ldo16, cudaStream_t s) {
   bool align_ok = ldx % 4 == 0 && aligned16(x) && aligned16(gamma) && aligned16(beta) &&
                   (!out || (ldo % 4 == 0 && aligned16(out))) &&
@@ -373,7 +373,7 @@ __global__ void embed_kernel(const int64_t* __restrict__ tok, int64_t n,
                              const float* __restrict__ emb, int d, float scale,
                              const float* __restrict__ pos, int64_t off,
                              const int32_t* __restrict__ d_off, int64_t seq, float* out,
-                             __nv_bfloat16* out16) {
+                             h16* out16) {
   pdl_enter();
   const int64_t base = d_off ? (int64_t)(*d_off) : off;
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < n * d;
@@ -383,7 +383,7 @@ __global__ void embed_kernel(const int64_t* __restrict__ tok, int64_t n,
     int64_t p = i % seq + base;
     float v = fadd_rn(fmul_rn(emb[tok[i] * d + j], scale), pos[p * d + j]);
     if (out) out[idx] = v;
-    if (out16) out16[idx] = f2bf(v);
+    if (out16) out16[idx] = f2h(v);
   }
 }
 
@@ -451,7 +451,7 @@ int fq_layer_norm(const float* x, int64_t ldx, const float* gamma, const float* 
   FQ_CHECK_ARG(eps >= 0, FQ_ERR_DIMENSION, "eps must be non-negative");
   if (rows == 0) return FQ_OK;
   launch_ln<false>(x, ldx, nullptr, nullptr, 0, gamma, beta, eps, rows, d, out, ldo,
-                   reinterpret_cast<__nv_bfloat16*>(out16), ldo16, as_stream(stream));
+                   reinterpret_cast<fq::h16*>(out16), ldo16, as_stream(stream));
   return launch_status("fq_layer_norm");
 }
 
@@ -464,7 +464,7 @@ int fq_bias_residual_layer_norm(const float* x, int64_t ldx, const float* bias,
                FQ_ERR_DIMENSION, "fq_bias_residual_layer_norm: bad args");
   if (rows == 0) return FQ_OK;
   launch_ln<true>(x, ldx, bias, residual, ldr, gamma, beta, eps, rows, d, out, ldo,
-                  reinterpret_cast<__nv_bfloat16*>(out16), ldo16, as_stream(stream));
+                  reinterpret_cast<fq::h16*>(out16), ldo16, as_stream(stream));
   return launch_status("fq_bias_residual_layer_norm");
 }
 
@@ -482,7 +482,7 @@ int fq_splitk_bias_residual_layer_norm(const float* slabs, int nslab, int64_t ld
                FQ_ERR_DIMENSION, "fq_splitk_bias_residual_layer_norm: bad args");
   FQ_CHECK_ARG(eps >= 0, FQ_ERR_DIMENSION, "eps must be non-negative");
   if (rows == 0) return FQ_OK;
-  auto* o16 = reinterpret_cast<__nv_bfloat16*>(out16);
+  auto* o16 = reinterpret_cast<fq::h16*>(out16);
   const int64_t slab = rows * ld;
   cudaStream_t s = as_stream(stream);
 #define FQ_LNS(V, NS)                                                                         \
@@ -554,7 +554,7 @@ int fq_embed_scale_pos(const int64_t* tokens, int64_t n, const float* emb, int64
   if (n == 0) return FQ_OK;
   launch_kernel(embed_kernel, grid_for(n * d, 256), 256, 0, as_stream(stream), 1u, 
       tokens, n, emb, (int)d, scale, pos, pos_offset, d_off, seq, out,
-      reinterpret_cast<__nv_bfloat16*>(out16));
+      reinterpret_cast<fq::h16*>(out16));
   return launch_status("fq_embed_scale_pos");
 }
 

@@ -1,12 +1,12 @@
 // Exact-mode fp32 GEMM (reference: tensor.py:179 gemm / :207 gemm_batched,
 // numpy matmul -> OpenBLAS SGEMM).
 //
-// Why SIMT: SURVEY.md H1 measured that TF32 and bf16 operands flip beam
+// Why SIMT: SURVEY.md H1 measured that TF32 and fp16 operands flip beam
 // selections while any fp32 (or f64) accumulation order keeps the tokens.
 // This kernel therefore uses FFMA with a sequential K order per output element,
 // independent of M and of the tiling, so results are bitwise invariant to
 // batch sharding across GPUs (SURVEY §8(e) "Determinism across G").
-// Fast (bf16) mode uses the tcgen05 kernel in fq_gemm_tc.cu instead.
+// Fast (fp16) mode uses the tcgen05 kernel in fq_gemm_tc.cu instead.
 //
 // Epilogue (fused, fp32, separately rounded): t = acc (+C) (+bias); act; +res.
 // This equals the reference's gemm followed by bias_residual_act_kernel
@@ -24,7 +24,7 @@ struct GemmArgs {
   int64_t ldc, sc0, sc1;
   int64_t n1;  // inner batch extent (batch index z -> (z / n1, z % n1))
   int64_t M, N, K;
-  int transpose_b, accumulate, act, c_bf16;
+  int transpose_b, accumulate, act, c_f16;
   const float* bias;
   const float* res;
   int64_t ldr;
@@ -123,7 +123,7 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN))
 
   // epilogue
   float* C32 = reinterpret_cast<float*>(p.c) + i0 * p.sc0 + i1 * p.sc1;
-  __nv_bfloat16* C16 = reinterpret_cast<__nv_bfloat16*>(p.c) + i0 * p.sc0 + i1 * p.sc1;
+  h16* C16 = reinterpret_cast<fq::h16*>(p.c) + i0 * p.sc0 + i1 * p.sc1;
 #pragma unroll
   for (int i = 0; i < TM; ++i) {
     int64_t gm = m0 + ty * TM + i;
@@ -133,11 +133,11 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN))
       int64_t gn = n0 + tx * TN + j;
       if (gn >= p.N) continue;
       float t = acc[i][j];
-      if (p.accumulate) t = fadd_rn(p.c_bf16 ? bf2f(C16[gm * p.ldc + gn]) : C32[gm * p.ldc + gn], t);
+      if (p.accumulate) t = fadd_rn(p.c_f16 ? h2f(C16[gm * p.ldc + gn]) : C32[gm * p.ldc + gn], t);
       if (p.bias) t = fadd_rn(t, p.bias[gn]);
       t = apply_act(t, p.act);
       if (p.res) t = fadd_rn(t, p.res[gm * p.ldr + gn]);
-      if (p.c_bf16) C16[gm * p.ldc + gn] = f2bf(t);
+      if (p.c_f16) C16[gm * p.ldc + gn] = f2h(t);
       else C32[gm * p.ldc + gn] = t;
     }
   }
@@ -161,7 +161,7 @@ int launch_sgemm(const GemmArgs& p, int64_t nbatch, cudaStream_t s) {
 }
 
 // tcgen05 path (fq_gemm_tc.cu)
-int launch_tc_gemm(const void* a, int64_t lda, const void* b, int64_t ldb, void* c, int c_bf16,
+int launch_tc_gemm(const void* a, int64_t lda, const void* b, int64_t ldb, void* c, int c_f16,
                    int64_t ldc, int64_t M, int64_t N, int64_t K, int accumulate,
                    const float* bias, const float* res, int64_t ldr, int act, cudaStream_t s);
 
@@ -209,13 +209,13 @@ int fq_gemm(const void* a, int a_dtype, int64_t lda, const void* b, int b_dtype,
     p.c = c; p.ldc = ldc; p.n1 = 1;
     p.M = M; p.N = N; p.K = K;
     p.transpose_b = transpose_b; p.accumulate = accumulate; p.act = act;
-    p.c_bf16 = c_dtype == FQ_BF16;
+    p.c_f16 = c_dtype == FQ_F16;
     p.bias = bias; p.res = residual; p.ldr = ldr;
     return launch_sgemm(p, 1, as_stream(stream));
   }
-  FQ_CHECK_ARG(a_dtype == FQ_BF16 && transpose_b, FQ_ERR_UNSUPPORTED,
-               "bf16 GEMM needs K-major B ([N,K], transpose_b=1)");
-  return launch_tc_gemm(a, lda, b, ldb, c, c_dtype == FQ_BF16, ldc, M, N, K, accumulate, bias,
+  FQ_CHECK_ARG(a_dtype == FQ_F16 && transpose_b, FQ_ERR_UNSUPPORTED,
+               "fp16 GEMM needs K-major B ([N,K], transpose_b=1)");
+  return launch_tc_gemm(a, lda, b, ldb, c, c_dtype == FQ_F16, ldc, M, N, K, accumulate, bias,
                         residual, ldr, act, as_stream(stream));
 }
 

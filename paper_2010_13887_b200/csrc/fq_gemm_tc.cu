@@ -1,6 +1,6 @@
-// bf16 GEMM on the 5th-generation tensor cores (tcgen05 + TMEM + TMA), sm_100a.
+// fp16 GEMM on the 5th-generation tensor cores (tcgen05 + TMEM + TMA), sm_100a.
 //
-// C[M,N] = epilogue(A[M,K] . B[N,K]^T), A and B bf16 K-major (weights were
+// C[M,N] = epilogue(A[M,K] . B[N,K]^T), A and B fp16 K-major (weights were
 // re-laid out to [N,K] once at load), fp32 accumulation in TMEM.
 //
 // Persistent, warp-specialised, one 128 x BN output tile per CTA iteration:
@@ -10,7 +10,7 @@
 //               (M=128, N=BN, K=16 per instruction); tcgen05.commit frees ring
 //               slots and signals one of two TMEM accumulator stages;
 //   warps 2..5  epilogue: tcgen05.ld 32x32b.x32, transpose through smem,
-//               fused (+C) (+bias) act (+residual), coalesced fp32/bf16 stores,
+//               fused (+C) (+bias) act (+residual), coalesced fp32/fp16 stores,
 //               overlapping the next tile's MMAs.
 // Thread-block clusters of cm x cn CTAs share operands through TMA multicast:
 // the cn CTAs of a cluster row (same M-tile) each load 1/cn of the A tile and
@@ -34,12 +34,12 @@ namespace fq {
 namespace tc {
 
 constexpr int BM = 128;
-constexpr int BK = 64;  // 64 bf16 = 128 bytes = one swizzle row
+constexpr int BK = 64;  // 64 fp16 = 128 bytes = one swizzle row
 constexpr int kThreads = 192;
 // OP_X3 (exact fp32 mode, 3xTF32): 2 more warps split each staged fp32 tile
 // (8 warps in all: 320 threads would cap registers at 168, below the
 // epilogue's 128-float row accumulator + chunk registers)
-constexpr int OP_BF16 = 0, OP_X3 = 1;
+constexpr int OP_F16 = 0, OP_X3 = 1;
 constexpr int kThreadsX3 = 256;
 constexpr int kConvThreads = kThreadsX3 - kThreads;
 // OP_X3: K blocks (of 32) per TMEM accumulation chunk, summed in registers
@@ -116,13 +116,14 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
   return d;
 }
 
-// kind::f16 instruction descriptor: bf16 x bf16 -> f32, both K-major.
-__host__ __device__ constexpr uint32_t idesc_bf16(int m, int n) {
-  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) |
+// kind::f16 instruction descriptor: f16 x f16 -> f32 (a/b format 0 = F16),
+// both K-major.
+__host__ __device__ constexpr uint32_t idesc_f16(int m, int n) {
+  return (1u << 4) | ((uint32_t)(n >> 3) << 17) |
          ((uint32_t)(m >> 4) << 24);
 }
 
-__device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+__device__ __forceinline__ void mma_f16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
                                          uint32_t idesc, uint32_t accumulate) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
@@ -249,7 +250,7 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 struct Epi {
   void* c;
   int64_t ldc;
-  int c_bf16;
+  int c_f16;
   int accumulate;
   const float* bias;
   const float* res;
@@ -289,7 +290,7 @@ struct LnEpi {
   double eps;
   float* out;
   int64_t ldo;
-  __nv_bfloat16* out16;
+  h16* out16;
   int64_t ldo16;
   double2* stats;  // [M][nt]
   int* ctr;
@@ -356,13 +357,13 @@ __device__ __forceinline__ void dbg_stamp(unsigned long long* dbg, int slot) {
 // writes raw fp32 A into "A hi" (and raw B into "B hi" unless B arrives
 // pre-split); converter warps 6..7 split it in place into tf32 hi + lo, then
 // the MMA warp issues three kind::tf32 MMAs per K step (mma_x3_block).
-template <int BN, int STAGES, bool HS = false, int OP = OP_BF16>
+template <int BN, int STAGES, bool HS = false, int OP = OP_F16>
 __global__ void __launch_bounds__(threads_of<OP>(), 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tma_a,
                    const __grid_constant__ CUtensorMap tma_b, const Epi ep, int M, int N, int K,
                    int cm, int cn, const HarsEpi he, const __grid_constant__ CUtensorMap tma_c,
                    const __grid_constant__ CUtensorMap tma_blo) {
-  static_assert(OP == OP_BF16 || !HS, "the HARS epilogue is bf16-only");
+  static_assert(OP == OP_F16 || !HS, "the HARS epilogue is fp16-only");
   constexpr bool X3 = OP == OP_X3;
   constexpr int KB = kblock<OP>();
   constexpr int A_BYTES = BM * 128;
@@ -486,7 +487,7 @@ __global__ void __launch_bounds__(threads_of<OP>(), 1)
     }
   } else if (warp == 1) {
     if (lane == 0) {  // ---- MMA issuer ----
-      constexpr uint32_t idesc = X3 ? idesc_tf32(BM, BN) : idesc_bf16(BM, BN);
+      constexpr uint32_t idesc = X3 ? idesc_tf32(BM, BN) : idesc_f16(BM, BN);
       int it = 0, local = 0;
       if constexpr (X3) {  // chunks of X3_CH K blocks into ping-pong TMEM slots
         int gc = 0;
@@ -527,7 +528,7 @@ __global__ void __launch_bounds__(threads_of<OP>(), 1)
           const uint32_t b_base = a_base + B_OFF;
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k) {
-            mma_bf16(acc, sw128_desc(a_base + k * 32), sw128_desc(b_base + k * 32), idesc,
+            mma_f16(acc, sw128_desc(a_base + k * 32), sw128_desc(b_base + k * 32), idesc,
                      (kb | k) != 0);
           }
           // ring slot reusable (in me and in every CTA that multicasts into me)
@@ -657,7 +658,7 @@ __global__ void __launch_bounds__(threads_of<OP>(), 1)
           if (nval >= 32) {
 #pragma unroll
             for (int j = 0; j < 32; ++j) {
-              t += hs_ex2(fmaf(v[j], L2E, -mL));  // bf16 mode: one-FMA argument
+              t += hs_ex2(fmaf(v[j], L2E, -mL));  // fp16 mode: one-FMA argument
               mask |= (v[j] >= bound ? 1u : 0u) << j;
             }
           } else {
@@ -692,7 +693,7 @@ __global__ void __launch_bounds__(threads_of<OP>(), 1)
     const int q = warp & 3;
     float* st = stage_out + (warp - 2) * 32 * 33;
     float* c32 = reinterpret_cast<float*>(ep.c);
-    __nv_bfloat16* c16 = reinterpret_cast<__nv_bfloat16*>(ep.c);
+    h16* c16 = reinterpret_cast<fq::h16*>(ep.c);
     int local = 0, gc = 0;
     for (int g = cluster_id; g < ngroups; g += nclusters, ++local) {
       const int as = local & 1;
@@ -715,7 +716,7 @@ __global__ void __launch_bounds__(threads_of<OP>(), 1)
           // thread = row: epilogue math on the tcgen05.ld registers, the
           // 32 x 32 chunk written swizzled into this warp's 4 KB box area
           // (conflict-free 16-byte stores), then one TMA tensor store per chunk
-          // (full-line writes; fp32: one 4 KB box, bf16: two 2 KB boxes)
+          // (full-line writes; fp32: one 4 KB box, fp16: two 2 KB boxes)
           uint8_t* box = reinterpret_cast<uint8_t*>(stage_out) + (warp - 2) * 4096;
           const int col0 = n0 + cc;
           if (ep.bias) {
@@ -734,24 +735,24 @@ __global__ void __launch_bounds__(threads_of<OP>(), 1)
 #pragma unroll
             for (int j = 0; j < 32; ++j) v[j] = apply_act(v[j], ep.act);
           }
-          if (lane == 0) {  // my box area is free again (bf16: the one two chunks back)
-            if (ep.c_bf16) asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(1) : "memory");
+          if (lane == 0) {  // my box area is free again (fp16: the one two chunks back)
+            if (ep.c_f16) asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(1) : "memory");
             else asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(0) : "memory");
           }
           __syncwarp();
-          if (ep.c_bf16) {
+          if (ep.c_f16) {
             uint8_t* bx = box + ((cc >> 5) & 1) * 2048;  // 32 rows x 64 B, 64-byte swizzle
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
               uint4 pk;
-              __nv_bfloat162 hh;
-              hh = __floats2bfloat162_rn(v[8 * j], v[8 * j + 1]);
+              h16x2 hh;
+              hh = __floats2half2_rn(v[8 * j], v[8 * j + 1]);
               pk.x = *reinterpret_cast<uint32_t*>(&hh);
-              hh = __floats2bfloat162_rn(v[8 * j + 2], v[8 * j + 3]);
+              hh = __floats2half2_rn(v[8 * j + 2], v[8 * j + 3]);
               pk.y = *reinterpret_cast<uint32_t*>(&hh);
-              hh = __floats2bfloat162_rn(v[8 * j + 4], v[8 * j + 5]);
+              hh = __floats2half2_rn(v[8 * j + 4], v[8 * j + 5]);
               pk.z = *reinterpret_cast<uint32_t*>(&hh);
-              hh = __floats2bfloat162_rn(v[8 * j + 6], v[8 * j + 7]);
+              hh = __floats2half2_rn(v[8 * j + 6], v[8 * j + 7]);
               pk.w = *reinterpret_cast<uint32_t*>(&hh);
               *reinterpret_cast<uint4*>(bx + lane * 64 + ((j ^ ((lane >> 1) & 3)) << 4)) = pk;
             }
@@ -788,7 +789,7 @@ __global__ void __launch_bounds__(threads_of<OP>(), 1)
               float cv[16];
 #pragma unroll
               for (int i = 0; i < 16; ++i)
-                cv[i] = i < nr ? (ep.c_bf16 ? bf2f(c16[c0 + i * ep.ldc]) : c32[c0 + i * ep.ldc])
+                cv[i] = i < nr ? (ep.c_f16 ? h2f(c16[c0 + i * ep.ldc]) : c32[c0 + i * ep.ldc])
                                : 0.0f;
 #pragma unroll
               for (int i = 0; i < 16; ++i) x[i] = fadd_rn(cv[i], x[i]);
@@ -813,10 +814,10 @@ __global__ void __launch_bounds__(threads_of<OP>(), 1)
 #pragma unroll
               for (int i = 0; i < 16; ++i) x[i] = fadd_rn(x[i], rv[i]);
             }
-            if (ep.c_bf16) {
+            if (ep.c_f16) {
 #pragma unroll
               for (int i = 0; i < 16; ++i)
-                if (i < nr) c16[c0 + i * ep.ldc] = f2bf(x[i]);
+                if (i < nr) c16[c0 + i * ep.ldc] = f2h(x[i]);
             } else {
 #pragma unroll
               for (int i = 0; i < 16; ++i)
@@ -921,14 +922,14 @@ __device__ __forceinline__ float4 ld_dsmem_f4(uint32_t local_addr, uint32_t rank
 // consumer (fq_splitk_bias_residual_layer_norm) sums the S slabs in split
 // order, so the result is bit-identical to the DSMEM reduction's.
 // OP_X3: the exact-mode 3xTF32 operands (see tc_gemm_kernel).
-template <int BN, int STAGES, bool LNF = false, bool SLAB = false, int OP = OP_BF16>
+template <int BN, int STAGES, bool LNF = false, bool SLAB = false, int OP = OP_F16>
 __global__ void __launch_bounds__(threads_of<OP>(), 1)
     tc_gemm_splitk_kernel(const __grid_constant__ CUtensorMap tma_a,
                           const __grid_constant__ CUtensorMap tma_b, const Epi ep, int M, int N,
                           int K, int kb_per_split, const LnEpi ln, int nsplit,
                           const __grid_constant__ CUtensorMap tma_c,
                           const __grid_constant__ CUtensorMap tma_blo) {
-  static_assert(OP == OP_BF16 || !LNF, "the in-kernel LN is bf16-only");
+  static_assert(OP == OP_F16 || !LNF, "the in-kernel LN is fp16-only");
   constexpr bool X3 = OP == OP_X3;
   constexpr int KB = kblock<OP>();
   constexpr int A_BYTES = BM * 128;
@@ -1018,7 +1019,7 @@ __global__ void __launch_bounds__(threads_of<OP>(), 1)
     }
   } else if (warp == 1) {
     if (lane == 0) {  // ---- MMA issuer ----
-      constexpr uint32_t idesc = X3 ? idesc_tf32(BM, BN) : idesc_bf16(BM, BN);
+      constexpr uint32_t idesc = X3 ? idesc_tf32(BM, BN) : idesc_f16(BM, BN);
       if constexpr (X3) {  // chunks of X3_CH K blocks into ping-pong TMEM slots
         int it = 0, gc = 0;
         for (int c0 = kb0; c0 < kb1; c0 += X3_CH, ++gc) {
@@ -1047,7 +1048,7 @@ __global__ void __launch_bounds__(threads_of<OP>(), 1)
           const uint32_t b_base = a_base + B_OFF;
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k)
-            mma_bf16(tmem, sw128_desc(a_base + k * 32), sw128_desc(b_base + k * 32), idesc,
+            mma_f16(tmem, sw128_desc(a_base + k * 32), sw128_desc(b_base + k * 32), idesc,
                      (it | k) != 0);
           mma_commit(&empty_bar[s]);
         }
@@ -1170,7 +1171,7 @@ __global__ void __launch_bounds__(threads_of<OP>(), 1)
     const int rows = max(0, min(BM, r_lo + rows_per) - r_lo);
     constexpr int C4 = BN / 4;
     float* c32 = reinterpret_cast<float*>(ep.c);
-    __nv_bfloat16* c16 = reinterpret_cast<__nv_bfloat16*>(ep.c);
+    h16* c16 = reinterpret_cast<fq::h16*>(ep.c);
     const uint32_t part_s = smem_u32(part);
     // Two output float4 per thread per pass; every remote partial and the
     // residual / bias vectors of both are requested before the first use, so
@@ -1227,7 +1228,7 @@ __global__ void __launch_bounds__(threads_of<OP>(), 1)
           for (int j = 0; j < 4; ++j) {
             if (col + j >= N) break;
             float y = x[j];
-            if (ep.accumulate) y = fadd_rn(ep.c_bf16 ? bf2f(c16[ci + j]) : c32[ci + j], y);
+            if (ep.accumulate) y = fadd_rn(ep.c_f16 ? h2f(c16[ci + j]) : c32[ci + j], y);
             if (ep.bias) y = fadd_rn(y, __ldg(ep.bias + col + j));
             y = apply_act(y, ep.act);
             if (ep.res) y = fadd_rn(y, __ldg(ep.res + (int64_t)row * ep.ldr + col + j));
@@ -1237,8 +1238,8 @@ __global__ void __launch_bounds__(threads_of<OP>(), 1)
         if constexpr (LNF) {  // keep the pre-LN row slice (my own rows of my partial)
           *reinterpret_cast<float4*>(part + lr * PLD + c) = make_float4(x[0], x[1], x[2], x[3]);
         } else if (col + 3 < N && ((ci & 3) == 0)) {
-          if (ep.c_bf16) {
-            __nv_bfloat162 lo = __floats2bfloat162_rn(x[0], x[1]), hi = __floats2bfloat162_rn(x[2], x[3]);
+          if (ep.c_f16) {
+            h16x2 lo = __floats2half2_rn(x[0], x[1]), hi = __floats2half2_rn(x[2], x[3]);
             uint2 pk;
             pk.x = *reinterpret_cast<uint32_t*>(&lo);
             pk.y = *reinterpret_cast<uint32_t*>(&hi);
@@ -1248,7 +1249,7 @@ __global__ void __launch_bounds__(threads_of<OP>(), 1)
           }
         } else {
           for (int j = 0; j < 4 && col + j < N; ++j) {
-            if (ep.c_bf16) c16[ci + j] = f2bf(x[j]);
+            if (ep.c_f16) c16[ci + j] = f2h(x[j]);
             else c32[ci + j] = x[j];
           }
         }
@@ -1320,7 +1321,7 @@ __global__ void __launch_bounds__(threads_of<OP>(), 1)
           o.w = fadd_rn(fmul_rn((float)(((double)prow[j + 3] - mean) * inv), g.w), bb.w);
           if (ln.out) *reinterpret_cast<float4*>(ln.out + (int64_t)row * ln.ldo + c0 + j) = o;
           if (ln.out16) {
-            __nv_bfloat162 lo = __floats2bfloat162_rn(o.x, o.y), hi = __floats2bfloat162_rn(o.z, o.w);
+            h16x2 lo = __floats2half2_rn(o.x, o.y), hi = __floats2half2_rn(o.z, o.w);
             uint2 pk;
             pk.x = *reinterpret_cast<uint32_t*>(&lo);
             pk.y = *reinterpret_cast<uint32_t*>(&hi);
@@ -1353,12 +1354,12 @@ constexpr int stage_bytes() {
   return (OP == OP_X3 ? 2 : 1) * (BM * 128 + BN * 128);
 }
 
-template <int BN, int STAGES, int OP = OP_BF16>
+template <int BN, int STAGES, int OP = OP_F16>
 constexpr int smem_bytes_splitk() {
   return STAGES * stage_bytes<BN, OP>() + 1024;
 }
 
-template <int BN, int STAGES, bool HS = false, int OP = OP_BF16>
+template <int BN, int STAGES, bool HS = false, int OP = OP_F16>
 constexpr int smem_bytes() {
   return STAGES * stage_bytes<BN, OP>() + (HS ? 8 : 4) * 32 * 33 * 4 + 1024;
 }
@@ -1379,7 +1380,7 @@ static EncodeFn get_encode() {
 }
 
 // 2D map over a row-major [rows, cols] matrix with leading dim ld, box
-// [box_rows, one 128-byte row] (64 bf16 / 32 fp32) with 128-byte swizzle;
+// [box_rows, one 128-byte row] (64 fp16 / 32 fp32) with 128-byte swizzle;
 // out-of-bounds elements read as zero.
 static int make_map(CUtensorMap* map, const void* ptr, int64_t rows, int64_t cols, int64_t ld,
                     int box_rows, bool f32 = false) {
@@ -1393,7 +1394,7 @@ static int make_map(CUtensorMap* map, const void* ptr, int64_t rows, int64_t col
   cuuint64_t strides[1] = {(cuuint64_t)(ld * es)};
   cuuint32_t box[2] = {(cuuint32_t)(128 / es), (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = enc(map, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
+  CUresult r = enc(map, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16,
                    2, const_cast<void*>(ptr), dims, strides,
                    box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -1406,20 +1407,20 @@ static int make_map(CUtensorMap* map, const void* ptr, int64_t rows, int64_t col
 }
 
 // Output map for the TMA-store epilogue: [rows, cols] row-major (ld elements),
-// box 32 rows x 32 elements (fp32: 128 B rows, 128-byte swizzle; bf16: 64 B
+// box 32 rows x 32 elements (fp32: 128 B rows, 128-byte swizzle; fp16: 64 B
 // rows, 64-byte swizzle) — the layout the epilogue writes its boxes in.
 static int make_map_c(CUtensorMap* map, void* ptr, int64_t rows, int64_t cols, int64_t ld,
-                      bool bf16) {
+                      bool fp16) {
   EncodeFn enc = get_encode();
   if (!enc) return FQ_ERR_CUDA;
-  const int es = bf16 ? 2 : 4;
+  const int es = fp16 ? 2 : 4;
   cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
   cuuint64_t strides[1] = {(cuuint64_t)(ld * es)};
   cuuint32_t box[2] = {32u, 32u};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = enc(map, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+  CUresult r = enc(map, fp16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
                    2, ptr, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                   bf16 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
+                   fp16 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
                    CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? FQ_OK : FQ_ERR_CUDA;
 }
@@ -1435,10 +1436,10 @@ static bool tma_store_enabled() {
 
 }  // namespace tc
 
-// 2D bf16 tensor map with 128-byte swizzle for other kernels (attention):
+// 2D fp16 tensor map with 128-byte swizzle for other kernels (attention):
 // [rows, cols] row-major with leading dimension ld elements, box
 // [box_rows, box_cols] (box_cols * 2 == 128 bytes for the swizzle).
-int make_tmap_bf16_sw128(CUtensorMap* map, const void* ptr, int64_t rows, int64_t cols,
+int make_tmap_f16_sw128(CUtensorMap* map, const void* ptr, int64_t rows, int64_t cols,
                          int64_t ld, int box_cols, int box_rows) {
   tc::EncodeFn enc = tc::get_encode();
   if (!enc) {
@@ -1449,7 +1450,7 @@ int make_tmap_bf16_sw128(CUtensorMap* map, const void* ptr, int64_t rows, int64_
   cuuint64_t strides[1] = {(cuuint64_t)(ld * 2)};
   cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides,
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(ptr), dims, strides,
                    box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
@@ -1471,7 +1472,7 @@ static int num_sms() {
   return n;
 }
 
-template <int BN, int STAGES, bool HS = false, int OP = OP_BF16>
+template <int BN, int STAGES, bool HS = false, int OP = OP_F16>
 static int launch(const void* a, int64_t lda, const void* b, int64_t ldb, const Epi& ep,
                   int64_t M, int64_t N, int64_t K, int cm, int cn, cudaStream_t s,
                   const HarsEpi& he = HarsEpi{}, const void* b_lo = nullptr) {
@@ -1487,8 +1488,8 @@ static int launch(const void* a, int64_t lda, const void* b, int64_t ldb, const 
   if (e2.b_presplit && (rc = make_map(&mblo, b_lo, N, K, ldb, BN / cm, true)) != FQ_OK) return rc;
   mc = ma;
   if (!HS && ep.c && !ep.accumulate && !ep.res && N % 32 == 0 && tma_store_enabled() &&
-      ((uintptr_t)ep.c & 15) == 0 && (ep.ldc * (ep.c_bf16 ? 2 : 4)) % 16 == 0 &&
-      make_map_c(&mc, ep.c, M, N, ep.ldc, ep.c_bf16 != 0) == FQ_OK)
+      ((uintptr_t)ep.c & 15) == 0 && (ep.ldc * (ep.c_f16 ? 2 : 4)) % 16 == 0 &&
+      make_map_c(&mc, ep.c, M, N, ep.ldc, ep.c_f16 != 0) == FQ_OK)
     e2.tstore = 1;
   const int csize = cm * cn;
   const int64_t groups = ((M + BM - 1) / BM / cm) * ((N + BN - 1) / BN / cn);
@@ -1505,7 +1506,7 @@ static int launch(const void* a, int64_t lda, const void* b, int64_t ldb, const 
   return launch_status("fq_gemm(tcgen05)");
 }
 
-template <int BN, int STAGES, bool LNF = false, bool SLAB = false, int OP = OP_BF16>
+template <int BN, int STAGES, bool LNF = false, bool SLAB = false, int OP = OP_F16>
 static int launch_splitk(const void* a, int64_t lda, const void* b, int64_t ldb, const Epi& ep,
                          int64_t M, int64_t N, int64_t K, int S, cudaStream_t s,
                          const LnEpi& ln = LnEpi{}, const void* b_lo = nullptr) {
@@ -1537,7 +1538,7 @@ static int launch_splitk(const void* a, int64_t lda, const void* b, int64_t ldb,
   return launch_status("fq_gemm(tcgen05 split-K)");
 }
 
-template <int BN, int STAGES, bool LNF = false, bool SLAB = false, int OP = OP_BF16>
+template <int BN, int STAGES, bool LNF = false, bool SLAB = false, int OP = OP_F16>
 static int prep_splitk() {
   return cudaFuncSetAttribute(tc_gemm_splitk_kernel<BN, STAGES, LNF, SLAB, OP>,
                               cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1546,7 +1547,7 @@ static int prep_splitk() {
              : FQ_ERR_CUDA;
 }
 
-template <int BN, int STAGES, bool HS = false, int OP = OP_BF16>
+template <int BN, int STAGES, bool HS = false, int OP = OP_F16>
 static int prep() {
   return cudaFuncSetAttribute(tc_gemm_kernel<BN, STAGES, HS, OP>,
                               cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1625,7 +1626,7 @@ static TcPlan plan_tc(int64_t M, int64_t N, int64_t K) {
   return {best, 1, 1, 1};
 }
 
-int launch_tc_gemm(const void* a, int64_t lda, const void* b, int64_t ldb, void* c, int c_bf16,
+int launch_tc_gemm(const void* a, int64_t lda, const void* b, int64_t ldb, void* c, int c_f16,
                    int64_t ldc, int64_t M, int64_t N, int64_t K, int accumulate,
                    const float* bias, const float* res, int64_t ldr, int act, cudaStream_t s) {
   FQ_CHECK_ARG(lda % 8 == 0 && ldb % 8 == 0 && ((uintptr_t)a & 15) == 0 &&
@@ -1633,7 +1634,7 @@ int launch_tc_gemm(const void* a, int64_t lda, const void* b, int64_t ldb, void*
                FQ_ERR_DIMENSION, "tcgen05 GEMM: operands need 16-byte aligned rows (ld %% 8 == 0)");
   FQ_CHECK_ARG(M < (1LL << 31) && N < (1LL << 31) && K < (1LL << 31), FQ_ERR_DIMENSION,
                "tcgen05 GEMM: dimension too large");
-  tc::Epi ep{c, ldc, c_bf16, accumulate, bias, res, ldr, act, g_gemm_dbg};
+  tc::Epi ep{c, ldc, c_f16, accumulate, bias, res, ldr, act, g_gemm_dbg};
   const TcPlan p = plan_tc(M, N, K);
   if (p.split > 1) {
     switch (p.bn) {
@@ -1747,7 +1748,7 @@ extern "C" int fq_gemm_f32x3_ln(const float* a, int64_t lda, const float* b, con
 }
 
 // Logits GEMM with the HARS statistics epilogue (see HarsEpi): x16 [rows, d]
-// bf16, emb16 [vocab, d] bf16 (K-major). Column tile width 224 (ncu: the
+// fp16, emb16 [vocab, d] fp16 (K-major). Column tile width 224 (ncu: the
 // C2 logits GEMM's best wave quantisation;
 // tiles; ldt >= ceil(vocab / 224) = the number of column tiles).
 extern "C" int fq_logits_hars(const void* x16, int64_t ldx, const void* emb16, int64_t lde,
@@ -1765,7 +1766,7 @@ extern "C" int fq_logits_hars(const void* x16, int64_t ldx, const void* emb16, i
                                   as_stream(stream), he);
 }
 
-// bf16 GEMM + bias + residual + LayerNorm (the decode step's self-out/LN1,
+// fp16 GEMM + bias + residual + LayerNorm (the decode step's self-out/LN1,
 // cross-out/LN2, FFN2/LN3): the split-K x4 kernel with the LN epilogue when
 // the plan is split-K over 128-column tiles and every cluster of the launch can
 // be resident at once (the row-block statistics exchange waits for all CTAs of
@@ -1822,7 +1823,7 @@ extern "C" int fq_gemm_ln(const void* a, int64_t lda, const void* w, int64_t ldw
   }
   if (fused) {
     tc::Epi ep{nullptr, 0, 0, 0, bias, res, ldr, 0, g_gemm_dbg};
-    tc::LnEpi ln{gamma, beta, eps, out, ldo, reinterpret_cast<__nv_bfloat16*>(out16), ldo16,
+    tc::LnEpi ln{gamma, beta, eps, out, ldo, reinterpret_cast<fq::h16*>(out16), ldo16,
                  reinterpret_cast<double2*>(ws),
                  reinterpret_cast<int*>(reinterpret_cast<char*>(ws) + M * nt * sizeof(double2)),
                  (int)nt};

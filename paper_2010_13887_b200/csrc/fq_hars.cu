@@ -1341,7 +1341,7 @@ __device__ __forceinline__ void stage2_and_next(
     int64_t max_steps, int64_t* row_tokens, int64_t* row_parents, int32_t* hist,
     const int64_t vals_off, const int cur0, const float* __restrict__ emb, int d,
     float emb_scale, const float* __restrict__ pos, float* __restrict__ x_next,
-    __nv_bfloat16* __restrict__ x16_next, int batch, int* all_cnt) {
+    h16* __restrict__ x16_next, int batch, int* all_cnt) {
   __shared__ int64_t s_tok[kMaxBeam];
   select_item(b, logits, ld, lse, cand_idx, cand_ld, cand_count, st, K, max_len, eos, len_pow,
               d_cur, max_steps, row_tokens, row_parents, hist, vals_off, s_tok);
@@ -1365,7 +1365,7 @@ __device__ __forceinline__ void stage2_and_next(
       v.w = fadd_rn(fmul_rn(e.w, emb_scale), p.w);
       *reinterpret_cast<float4*>(x_next + r * d + j) = v;
       if (x16_next) {
-        __nv_bfloat162 lo = __floats2bfloat162_rn(v.x, v.y), hi = __floats2bfloat162_rn(v.z, v.w);
+        h16x2 lo = __floats2half2_rn(v.x, v.y), hi = __floats2half2_rn(v.z, v.w);
         uint2 pk;
         pk.x = *reinterpret_cast<uint32_t*>(&lo);
         pk.y = *reinterpret_cast<uint32_t*>(&hi);
@@ -1398,7 +1398,7 @@ __global__ void __launch_bounds__(kSwThreads) hars_step_kernel(
     double* lse, int32_t* cand_idx, int64_t cand_ld, int64_t* cand_count, int* item_cnt,
     int* all_cnt, int64_t* row_tokens, int64_t* row_parents, int32_t* hist,
     const float* __restrict__ emb, int d, float emb_scale, const float* __restrict__ pos,
-    float* __restrict__ x_next, __nv_bfloat16* __restrict__ x16_next) {
+    float* __restrict__ x_next, h16* __restrict__ x16_next) {
   pdl_enter();
   const int C = (int)cl_nrank(), rank = (int)cl_rank();
   const int64_t row = blockIdx.x / C;
@@ -1437,7 +1437,7 @@ __global__ void __launch_bounds__(kSwThreads, 4) hars_step_split_kernel(
     double* lse, int32_t* cand_idx, int64_t cand_ld, int64_t* cand_count, int* counters,
     int64_t* row_tokens, int64_t* row_parents, int32_t* hist, const float* __restrict__ emb,
     int d, float emb_scale, const float* __restrict__ pos, float* __restrict__ x_next,
-    __nv_bfloat16* __restrict__ x16_next) {
+    h16* __restrict__ x16_next) {
   pdl_enter();
   extern __shared__ __align__(16) float4 sw_ring[];  // also stage 2's dynamic smem
   __shared__ SplitSmem sm;
@@ -1495,7 +1495,7 @@ __global__ void __launch_bounds__(kSelThreads) hars_merge_step_kernel(
     int32_t* cand_idx, int64_t cand_ld, int64_t* cand_count, int* counters, int* d_ovf,
     int64_t* row_tokens, int64_t* row_parents, int32_t* hist, const float* __restrict__ emb,
     int d, float emb_scale, const float* __restrict__ pos, float* __restrict__ x_next,
-    __nv_bfloat16* __restrict__ x16_next) {
+    h16* __restrict__ x16_next) {
   pdl_enter();
   __shared__ int s_idx[kMergeCap];
   __shared__ float s_val[kMergeCap];
@@ -1798,7 +1798,7 @@ int fq_hars_step(const float* logits, int64_t ld, fq_beam_state st, int64_t batc
                   logits, ld, g, st, (int)batch, (int)beam, (int)max_len, (int)eos, len_pow, d_cur,
                   max_steps, lse, cand_idx, cand_ld, cand_count, counters, row_tokens,
                   row_parents, hist, x_next ? emb : nullptr, (int)d_model, emb_scale, pos, x_next,
-                  reinterpret_cast<__nv_bfloat16*>(x16_next));
+                  reinterpret_cast<fq::h16*>(x16_next));
     return launch_status("fq_hars_step");
   }
   const size_t smem = std::max(sel_smem(beam, max_len),
@@ -1809,7 +1809,7 @@ int fq_hars_step(const float* logits, int64_t ld, fq_beam_state st, int64_t batc
                 len_pow, d_cur, max_steps, lse, cand_idx, cand_ld, cand_count, counters,
                 counters + batch, row_tokens, row_parents, hist, x_next ? emb : nullptr,
                 (int)d_model, emb_scale, pos, x_next,
-                reinterpret_cast<__nv_bfloat16*>(x16_next));
+                reinterpret_cast<fq::h16*>(x16_next));
   return launch_status("fq_hars_step");
 }
 
@@ -1838,7 +1838,7 @@ int fq_hars_merge_step(fq_beam_state st, int64_t batch, int64_t beam, int64_t vo
                 sv_cnt, reinterpret_cast<const int2*>(sv), (int)sv_cap, lse, cand_idx, cand_ld,
                 cand_count, counters, d_ovf, row_tokens, row_parents, hist,
                 x_next ? emb : nullptr, (int)d_model, emb_scale, pos, x_next,
-                reinterpret_cast<__nv_bfloat16*>(x16_next));
+                reinterpret_cast<fq::h16*>(x16_next));
   return launch_status("fq_hars_merge_step");
 }
 

@@ -6,7 +6,7 @@ Same configuration, weight layout and seeded initialisation as the reference
 
 * weights are uploaded once per precision (``DeviceWeights``): ``fp32`` keeps
   the reference's input-major [in, out] matrices for the exact-mode FFMA GEMM;
-  ``bf16`` casts and transposes them once to K-major [out, in] for the tcgen05
+  ``fp16`` casts and transposes them once to K-major [out, in] for the tcgen05
   GEMM (the paper's "fuse cast into weight loading"); the
   cross-attention K/V projections of all decoder layers are concatenated into
   one [d, 2*L*d] matrix so the per-request setup is a single large GEMM;
@@ -39,7 +39,7 @@ from .tensor import OpCounters, Timers, as_device, gemm, gemm_x3, global_counter
 
 F32 = np.float32
 I64 = np.int64
-PRECISIONS = ("fp32", "bf16")
+PRECISIONS = ("fp32", "fp16")
 
 
 # ---------------------------------------------------------------------------
@@ -307,7 +307,7 @@ class DeviceWeights:
         if precision not in PRECISIONS:
             raise InputError(f"unknown precision {precision!r}")
         self.config, self.host, self.precision = config, weights, precision
-        self.bf16 = precision == "bf16"
+        self.half = precision == "fp16"
         dev = torch.device("cuda", torch.cuda.current_device())
 
         def f32(a):
@@ -315,17 +315,17 @@ class DeviceWeights:
 
         def mat(a):  # GEMM B operand
             t = f32(a)
-            if not self.bf16:
+            if not self.half:
                 return X3Weight.from_kn(t)                 # [N, K] tf32 hi + lo
-            out = torch.empty((a.shape[1], a.shape[0]), dtype=torch.bfloat16, device=dev)
-            _abi.call("fq_cast_bf16", t.data_ptr(), a.shape[0], a.shape[1], 1, out.data_ptr(),
+            out = torch.empty((a.shape[1], a.shape[0]), dtype=torch.float16, device=dev)
+            _abi.call("fq_cast_f16", t.data_ptr(), a.shape[0], a.shape[1], 1, out.data_ptr(),
                       _abi.stream_handle())
-            return out                                     # [N, K] bf16, K-major
+            return out                                     # [N, K] fp16, K-major
 
         self.embedding = f32(weights.token_embedding)
         out_m = weights.output_matrix(config)
-        if self.bf16:
-            self.out_proj = f32(out_m).to(torch.bfloat16)   # [V, d] already K-major
+        if self.half:
+            self.out_proj = f32(out_m).to(torch.float16)   # [V, d] already K-major
         else:
             self.out_proj = self.embedding if config.tie_output else f32(out_m)
             self.out_x3 = X3Weight.from_kn(self.out_proj, transpose=False)  # logits GEMM
@@ -361,7 +361,7 @@ class DeviceWeights:
 
     @property
     def act_dtype(self):
-        return torch.bfloat16 if self.bf16 else torch.float32
+        return torch.float16 if self.half else torch.float32
 
 
 # ---------------------------------------------------------------------------
@@ -388,7 +388,7 @@ class ArenaBuffers:
 def _lin(dw: DeviceWeights, a32, a16, w, out, *, bias=None, residual=None, act="none",
          counters=None, timers=None):
     """One GEMM with fused epilogue in the session precision."""
-    if dw.bf16:
+    if dw.half:
         gemm(a16, w, out, transpose_b=True, bias=bias, residual=residual, activation=act,
              counters=counters, timers=timers)
     else:
@@ -413,10 +413,10 @@ def _ln(x, g, b, eps, out, out16, residual=None, bias=None, counters=None):
 
 def _lin_ln(dw: DeviceWeights, a32, a16, w, bias, residual, g, b, eps, out, out16, ws, *,
             counters=None, timers=None):
-    """GEMM + bias + residual, then LayerNorm: one fq_gemm_ln launch in bf16 mode
+    """GEMM + bias + residual, then LayerNorm: one fq_gemm_ln launch in fp16 mode
     with a statistics workspace (the LN inside the split-K epilogue), else the
     GEMM and the LN kernel."""
-    if dw.bf16 and ws is not None:
+    if dw.half and ws is not None:
         M, K = a16.shape
         N = w.shape[0]
         _abi.call("fq_gemm_ln", a16.data_ptr(), a16.stride(0), w.data_ptr(), w.stride(0),
@@ -426,7 +426,7 @@ def _lin_ln(dw: DeviceWeights, a32, a16, w, bias, residual, g, b, eps, out, out1
                   ws.numel() * ws.element_size(), M, N, K, _abi.stream_handle())
         (counters or global_counters()).count_fused("layer_norm", M * N * 8)
         return
-    if not dw.bf16 and ws is not None:  # exact mode: 3xTF32 K-slice slabs + the reducing LN
+    if not dw.half and ws is not None:  # exact mode: 3xTF32 K-slice slabs + the reducing LN
         M, K = a32.shape
         N = w.shape[0]
         _abi.call("fq_gemm_f32x3_ln", a32.data_ptr(), a32.stride(0), w.hi.data_ptr(),
@@ -464,7 +464,7 @@ def encoder_layer_forward(x, layer, config: ModelConfig, mask=None, batch: int =
                           precision: str = "fp32", x16=None, bad=None):
     """One encoder layer (post-LN): QKV GEMM(+bias) -> fused attention ->
     out GEMM(+bias+residual) -> LN -> FFN1 GEMM(+bias+act) -> FFN2
-    GEMM(+bias+residual) -> LN. Returns (out fp32, out bf16 or None).
+    GEMM(+bias+residual) -> LN. Returns (out fp32, out fp16 or None).
 
     ``layer`` is a device layer dict (DeviceWeights.enc[i]) or the reference's
     EncoderLayerWeights (uploaded on the fly)."""
@@ -480,32 +480,32 @@ def encoder_layer_forward(x, layer, config: ModelConfig, mask=None, batch: int =
         cfg1 = ModelConfig(**{**config.to_dict(), "num_encoder_layers": 1,
                               "num_decoder_layers": 0})
         layer = DeviceWeights(cfg1, tmp, precision).enc[0]
-        dw_bf16 = precision == "bf16"
+        dw_half = precision == "fp16"
     else:
-        dw_bf16 = not isinstance(layer["w_qkv"], X3Weight)
+        dw_half = not isinstance(layer["w_qkv"], X3Weight)
     bufs = buffers if buffers is not None else HeapBuffers()
     ctr = counters or global_counters()
     h, hd, ff = config.num_heads, config.head_dim, config.d_ff
-    act16 = torch.bfloat16 if dw_bf16 else torch.float32
-    if dw_bf16 and x16 is None:
-        x16 = X.to(torch.bfloat16)
+    act16 = torch.float16 if dw_half else torch.float32
+    if dw_half and x16 is None:
+        x16 = X.to(torch.float16)
     stream = _abi.stream_handle()
 
     class _P:  # precision shim for _lin
-        bf16 = dw_bf16
+        half = dw_half
 
     qkv = bufs.get(f"{prefix}.qkv", (n, 3 * d))
     _lin(_P, X, x16, layer["w_qkv"], qkv, bias=layer["b_qkv"], counters=ctr, timers=timers)
     ctx = bufs.get(f"{prefix}.ctx", (n, d), act16)
     _abi.call("fq_encoder_attention", qkv.data_ptr(), qkv.stride(0), batch, seq, h, hd,
-              attention_scale(hd), _abi.ptr(mask), None if dw_bf16 else ctx.data_ptr(),
-              ctx.data_ptr() if dw_bf16 else None, d, 0 if dw_bf16 else 1, _abi.ptr(bad), stream)
+              attention_scale(hd), _abi.ptr(mask), None if dw_half else ctx.data_ptr(),
+              ctx.data_ptr() if dw_half else None, d, 0 if dw_half else 1, _abi.ptr(bad), stream)
     ctr.count_fused("attention_scale_mask_softmax", n * d * 16)
     res1 = bufs.get(f"{prefix}.res1", (n, d))
     _lin(_P, ctx, ctx, layer["w_out"], res1, bias=layer["b_out"], residual=X, counters=ctr,
          timers=timers)
     norm1 = bufs.get(f"{prefix}.norm1", (n, d))
-    norm1_16 = bufs.get(f"{prefix}.norm1_16", (n, d), torch.bfloat16) if dw_bf16 else None
+    norm1_16 = bufs.get(f"{prefix}.norm1_16", (n, d), torch.float16) if dw_half else None
     _ln(res1, layer["ln1_g"], layer["ln1_b"], config.ln_eps, norm1, norm1_16, counters=ctr)
     ffn_h = bufs.get(f"{prefix}.ffn_h", (n, ff), act16)
     _lin(_P, norm1, norm1_16, layer["w_ff1"], ffn_h, bias=layer["b_ff1"], act=config.activation,
@@ -514,17 +514,17 @@ def encoder_layer_forward(x, layer, config: ModelConfig, mask=None, batch: int =
     _lin(_P, ffn_h, ffn_h, layer["w_ff2"], u, bias=layer["b_ff2"], residual=norm1, counters=ctr,
          timers=timers)
     out = bufs.get(f"{prefix}.out", (n, d))
-    out16 = bufs.get(f"{prefix}.out16", (n, d), torch.bfloat16) if dw_bf16 else None
+    out16 = bufs.get(f"{prefix}.out16", (n, d), torch.float16) if dw_half else None
     _ln(u, layer["ln2_g"], layer["ln2_b"], config.ln_eps, out, out16, counters=ctr)
     return out, out16
 
 
 def encode(tokens, weights, config: ModelConfig, lengths=None, *, engine: str = "fused",
            buffers=None, positions=None, counters=None, timers=None, precision: str = "fp32",
-           return_bf16: bool = False):
+           return_half: bool = False):
     """Stacked encoder over embedded + positional inputs (model.py:407-445).
     Returns the encoder memory [batch*seq, d_model] as a device fp32 tensor
-    (plus its bf16 copy when ``return_bf16``)."""
+    (plus its fp16 copy when ``return_half``)."""
     if engine != "fused":
         raise InputError("the B200 engine implements the fused path only")
     resident = isinstance(tokens, torch.Tensor) and tokens.is_cuda
@@ -547,7 +547,7 @@ def encode(tokens, weights, config: ModelConfig, lengths=None, *, engine: str = 
         mask = bufs.get("enc.mask", (batch, seq))
         mask.copy_(torch.from_numpy(lengths_mask(lengths, seq)))
     x = bufs.get("enc.x", (n, d))
-    x16 = bufs.get("enc.x16", (n, d), torch.bfloat16) if dw.bf16 else None
+    x16 = bufs.get("enc.x16", (n, d), torch.float16) if dw.half else None
     pos = as_device(positions, torch.float32) if positions is not None else dw.positions
     _abi.call("fq_embed_scale_pos", tok.data_ptr(), n, dw.embedding.data_ptr(), d,
               float(np.float32(math.sqrt(d))), pos.data_ptr(), 0, None, seq, x.data_ptr(),
@@ -561,7 +561,7 @@ def encode(tokens, weights, config: ModelConfig, lengths=None, *, engine: str = 
                                        precision=precision, x16=x16, bad=bad)
     if int(bad.item()):
         raise FullMaskError(f"{int(bad.item())} attention row(s) fully masked")
-    return (x, x16) if return_bf16 else x
+    return (x, x16) if return_half else x
 
 
 # ---------------------------------------------------------------------------
@@ -571,7 +571,7 @@ def encode(tokens, weights, config: ModelConfig, lengths=None, *, engine: str = 
 class KVCache:
     """Copy-free self-attention cache (replaces model.py:452-512's ping-pong).
 
-    Per decoder layer, K and V live in [max_seq_len, rows, d] (fp32 or bf16):
+    Per decoder layer, K and V live in [max_seq_len, rows, d] (fp32 or fp16):
     slot (t, r) is written once, by row r at step t, inside the attention
     kernel. ``hist[r, t]`` names the physical row holding row r's position t;
     a beam reorder permutes ``hist`` rows (rows x max_len int32) instead of
@@ -584,7 +584,7 @@ class KVCache:
             raise CapacityError(f"{rows} rows exceed max batch*beam {config.max_rows}")
         S, d = config.max_seq_len, config.d_model
         self.config, self.rows, self.max_seq_len = config, rows, S
-        self.kv_dtype = torch.bfloat16 if precision == "bf16" else torch.float32
+        self.kv_dtype = torch.float16 if precision == "fp16" else torch.float32
         self._k = [buffers.get(f"{prefix}.l{i}.k", (S, rows, d), self.kv_dtype)
                    for i in range(config.num_decoder_layers)]
         self._v = [buffers.get(f"{prefix}.l{i}.v", (S, rows, d), self.kv_dtype)
@@ -643,8 +643,8 @@ def build_cross_kv(memory, weights, config: ModelConfig, batch: int, seq: int, *
     M = as_device(memory, torch.float32)
     n, d, L = batch * seq, config.d_model, config.num_decoder_layers
     packed = bufs.get("dec.cross_kv", (n, 2 * L * d), dw.act_dtype)
-    if dw.bf16 and memory16 is None:
-        memory16 = M.to(torch.bfloat16)
+    if dw.half and memory16 is None:
+        memory16 = M.to(torch.float16)
     _lin(dw, M, memory16, dw.w_ckv, packed, bias=dw.b_ckv, counters=counters, timers=timers)
     return packed
 
@@ -679,22 +679,22 @@ class DecoderStep:
         a16 = dw.act_dtype
         self.tokens = b.get("dec.tokens", (R,), torch.int64)
         self.x = b.get("dec.x", (R, d))
-        self.x16 = b.get("dec.x16", (R, d), torch.bfloat16) if dw.bf16 else None
+        self.x16 = b.get("dec.x16", (R, d), torch.float16) if dw.half else None
         self.sqkv = b.get("dec.sqkv", (R, 3 * d))
         self.sctx = b.get("dec.sctx", (R, d), a16)
         self.sres = b.get("dec.sres", (R, d))
         self.snorm = b.get("dec.snorm", (R, d))
-        self.snorm16 = b.get("dec.snorm16", (R, d), torch.bfloat16) if dw.bf16 else None
+        self.snorm16 = b.get("dec.snorm16", (R, d), torch.float16) if dw.half else None
         self.cq = b.get("dec.cq", (R, d))
         self.cctx = b.get("dec.cctx", (R, d), a16)
         self.cres = b.get("dec.cres", (R, d))
         self.cnorm = b.get("dec.cnorm", (R, d))
-        self.cnorm16 = b.get("dec.cnorm16", (R, d), torch.bfloat16) if dw.bf16 else None
+        self.cnorm16 = b.get("dec.cnorm16", (R, d), torch.float16) if dw.half else None
         self.ffn_h = b.get("dec.ffn_h", (R, ff), a16)
         self.u = b.get("dec.ffn_out", (R, d))
         self.logits = b.get("dec.logits", (R, V))
         self.bad = b.get("dec.bad", (1,), torch.int32)
-        # GEMM + LN pairs as fq_gemm_ln. Default (bf16): the split-K GEMM writes
+        # GEMM + LN pairs as fq_gemm_ln. Default (fp16): the split-K GEMM writes
         # one partial slab per K slice and the LN kernel reduces them, so the
         # GEMM has no in-kernel (DSMEM) reduction. FQ_FUSE_LN=coresident: the LN
         # inside the split-K epilogue, measured slower at C2 (152k vs 165k
@@ -702,7 +702,7 @@ class DecoderStep:
         # FQ_FUSE_LN=0: GEMM with the reduction, then the LN kernel.
         self.ln_ws = None
         mode = os.environ.get("FQ_FUSE_LN", "slab")
-        if fuse_ln and mode != "0" and (dw.bf16 or mode == "slab"):
+        if fuse_ln and mode != "0" and (dw.half or mode == "slab"):
             # exact mode: the 3xTF32 split-K slabs summed by the LN kernel
             ws = b.get("dec.ln_ws", ((ln_ws_bytes(R, d) + 3) // 4,), torch.int32)
             if mode == "coresident":
@@ -711,7 +711,7 @@ class DecoderStep:
             self.ln_ws = ws
         # the cross-attention query GEMM as K-slice slabs summed by the
         # cross-attention kernel (no in-GEMM reduction), same bits
-        self.q_slabs = (dw.bf16 and self.ln_ws is not None and mode != "coresident" and
+        self.q_slabs = (dw.half and self.ln_ws is not None and mode != "coresident" and
                         config.head_dim == 64 and beam <= 8 and enc_seq <= 64)
         self._nslab = ctypes.c_int(0)
 
@@ -734,8 +734,8 @@ class DecoderStep:
         R, d, h, hd, L = self.rows, c.d_model, c.num_heads, c.head_dim, c.num_decoder_layers
         stream = _abi.stream_handle()
         scale = attention_scale(hd)
-        kvdt = 1 if dw.bf16 else 0
-        exact = 0 if dw.bf16 else 1
+        kvdt = 1 if dw.half else 0
+        exact = 0 if dw.half else 1
         if embed:
             self.embed()
         x, x16 = self.x, self.x16
@@ -744,8 +744,8 @@ class DecoderStep:
             _abi.call("fq_decoder_self_attention", self.sqkv.data_ptr(), self.sqkv.stride(0),
                       self.cache._k[i].data_ptr(), self.cache._v[i].data_ptr(), kvdt,
                       self.cache.hist.data_ptr(), self.cache.d_cur.data_ptr(), R, h, hd,
-                      c.max_seq_len, scale, None if dw.bf16 else self.sctx.data_ptr(),
-                      self.sctx.data_ptr() if dw.bf16 else None, d, exact, stream)
+                      c.max_seq_len, scale, None if dw.half else self.sctx.data_ptr(),
+                      self.sctx.data_ptr() if dw.half else None, d, exact, stream)
             ctr.count_fused("decoder_self_attention", R * d * 16)
             if self.ln_ws is not None:
                 _lin_ln(dw, self.sctx, self.sctx, lw["w_so"], lw["b_so"], x, lw["ln1_g"],
@@ -779,8 +779,8 @@ class DecoderStep:
                 _abi.call("fq_cross_attention", self.cq.data_ptr(), self.cq.stride(0),
                           ck.data_ptr(), cv.data_ptr(), kvdt, ld, self.batch, self.beam,
                           self.enc_seq, h, hd, scale, _abi.ptr(self.mask),
-                          None if dw.bf16 else self.cctx.data_ptr(),
-                          self.cctx.data_ptr() if dw.bf16 else None, d, exact,
+                          None if dw.half else self.cctx.data_ptr(),
+                          self.cctx.data_ptr() if dw.half else None, d, exact,
                           self.bad.data_ptr(), stream)
             ctr.count_fused("cross_attention", R * d * 16)
             if self.ln_ws is not None:
@@ -805,7 +805,7 @@ class DecoderStep:
             x, x16 = self.x, self.x16
         if not logits:
             return None
-        _lin(dw, x, x16, dw.out_proj if dw.bf16 else dw.out_x3, self.logits, counters=ctr,
+        _lin(dw, x, x16, dw.out_proj if dw.half else dw.out_x3, self.logits, counters=ctr,
              timers=tm)
         return self.logits
 
@@ -854,7 +854,7 @@ def plan_intermediates(config: ModelConfig, precision: str = "fp32") -> list[Int
     R = config.max_rows
     d, ff, V = config.d_model, config.d_ff, config.vocab_size
     L, D = config.num_encoder_layers, config.num_decoder_layers
-    bf = precision == "bf16"
+    bf = precision == "fp16"
     a = 2 if bf else 4  # activation bytes feeding GEMMs / attention
     n = B * S
     specs: list[IntermediateSpec] = []

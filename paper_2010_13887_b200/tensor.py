@@ -4,7 +4,7 @@ Mirrors pkg/src/fuseq/tensor.py: a :class:`Tensor` is a non-owning view (here
 of device memory held by the session arena), ``gemm``/``gemm_batched`` keep
 the reference's contract checks (shape, aliasing; tensor.py:173-227) and
 count one call each, but the math runs in ``libfq_b200.so``: fp32 operands
-take the exact-mode FFMA kernel, bf16 operands the tcgen05 tensor-core kernel.
+take the exact-mode FFMA kernel, fp16 operands the tcgen05 tensor-core kernel.
 ``gemm`` additionally accepts a fused epilogue (bias, activation, residual):
 the same fp32 operations the reference performs in the following
 ``bias_residual_act`` pass (kernels.py:39-53), fused into the GEMM store.
@@ -23,7 +23,7 @@ from . import _abi
 from .errors import AliasingError, DimensionError
 
 ACT_IDS = {"none": 0, "relu": 1, "gelu": 2}
-_DT = {torch.float32: 0, torch.bfloat16: 1}
+_DT = {torch.float32: 0, torch.float16: 1}
 
 
 @dataclass
@@ -45,7 +45,7 @@ class Tensor:
         return self.data.numel() * self.data.element_size()
 
     def numpy(self) -> np.ndarray:
-        return self.data.detach().float().cpu().numpy() if self.data.dtype == torch.bfloat16 \
+        return self.data.detach().float().cpu().numpy() if self.data.dtype == torch.float16 \
             else self.data.detach().cpu().numpy()
 
 
@@ -218,7 +218,7 @@ def gemm(a, b, out, *, transpose_b: bool = False, accumulate: bool = False,
          bias=None, residual=None, activation: str = "none"):
     """out = act(a @ op(b) (+ out) (+ bias)) (+ residual), one library call.
 
-    fp32 a/b: exact-mode FFMA GEMM. bf16 a/b: tcgen05 GEMM (b must be the
+    fp32 a/b: exact-mode FFMA GEMM. fp16 a/b: tcgen05 GEMM (b must be the
     K-major [N, K] weight, i.e. ``transpose_b=True``). One call increments
     ``gemm_calls`` by one (tensor.py:204)."""
     A, B, O = as_device(a), as_device(b), as_device(out)

@@ -1,7 +1,7 @@
 """Per-CTA %globaltimer stamps of one persistent tcgen05 GEMM launch (slots:
 0 start, 1 setup, 2 first stage landed, 3 first tile's MMAs issued, 4 first
 epilogue pass, 5 epilogue done, 6 exit) at the decode's non-split shapes, with
-the engine's epilogues (bias, ReLU, bf16 out). Usage: SHAPES=512x3072x1024,..."""
+the engine's epilogues (bias, ReLU, fp16 out). Usage: SHAPES=512x3072x1024,..."""
 import ctypes
 import os
 import sys
@@ -17,10 +17,10 @@ lib.fq_gemm_debug_timestamps.argtypes = [ctypes.c_void_p]
 shapes = os.environ.get("SHAPES", "512x3072x1024,512x4096x1024,512x1024x1024")
 for sh in shapes.split(","):
     M, N, K = (int(x) for x in sh.split("x"))
-    a = torch.randn(M, K, device="cuda").bfloat16()
-    bs = [torch.randn(N, K, device="cuda").bfloat16() for _ in range(4)]
+    a = torch.randn(M, K, device="cuda").half()
+    bs = [torch.randn(N, K, device="cuda").half() for _ in range(4)]
     bias = torch.randn(N, device="cuda")
-    c = torch.empty(M, N, device="cuda", dtype=torch.float32 if os.environ.get("F32") else torch.bfloat16)
+    c = torch.empty(M, N, device="cuda", dtype=torch.float32 if os.environ.get("F32") else torch.float16)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     clean = torch.ones(64 << 20, dtype=torch.float32, device="cuda")  # read after the fill:
     # evicts the fill's dirty lines, so the GEMM does not pay their write-back

@@ -16,13 +16,13 @@ lib.fq_gemm_force_plan.argtypes = [ctypes.c_int] * 4
 dbg = torch.zeros(2048, dtype=torch.int64, device="cuda")
 for (M, N, K, plan) in [(512, 1024, 1024, (32, 1, 1, 1)), (512, 1024, 1024, (128, 1, 1, 4)),
                         (512, 4096, 1024, (128, 1, 1, 1))]:
-    a = torch.randn(M, K, device="cuda").bfloat16()
-    b = torch.randn(N, K, device="cuda").bfloat16()
+    a = torch.randn(M, K, device="cuda").half()
+    b = torch.randn(N, K, device="cuda").half()
     c = torch.empty(M, N, device="cuda")
     lib.fq_gemm_force_plan(*plan)
-    x = torch.randn(512, 1024, device="cuda").bfloat16()
+    x = torch.randn(512, 1024, device="cuda").half()
     y = torch.empty(512, 1024, device="cuda")
-    w_prev = torch.randn(1024, 1024, device="cuda").bfloat16()
+    w_prev = torch.randn(1024, 1024, device="cuda").half()
     for _ in range(3):
         dbg.zero_()
         P.gemm(x, w_prev, y, transpose_b=True)   # a preceding kernel

@@ -13,9 +13,9 @@ from paper_2010_13887_b200 import _abi
 lib = _abi.load()
 lib.fq_gemm_debug_timestamps.argtypes = [ctypes.c_void_p]
 for M, N, K in [(512, 1024, 1024), (512, 1024, 4096)]:
-    a = torch.randn(M, K, device="cuda").bfloat16()
+    a = torch.randn(M, K, device="cuda").half()
     nb = int(os.environ.get("NBUF", "4"))
-    bs = [torch.randn(N, K, device="cuda").bfloat16() for _ in range(nb)]
+    bs = [torch.randn(N, K, device="cuda").half() for _ in range(nb)]
     c = torch.empty(M, N, device="cuda")
     dbg = torch.zeros(8 * 1024, dtype=torch.int64, device="cuda")
     for i in range(nb):

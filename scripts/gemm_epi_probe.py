@@ -1,5 +1,5 @@
 """Decode GEMM shapes with the decode step's real epilogues (bias / ReLU /
-residual, bf16 or fp32 output), graph-timed, vs the plain GEMM: how much the
+residual, fp16 or fp32 output), graph-timed, vs the plain GEMM: how much the
 fused epilogue costs."""
 import os
 import sys
@@ -14,12 +14,12 @@ from bench import graph_time  # noqa: E402
 
 for (M, N, K, kind) in [(512, 4096, 1024, "ffn1"), (512, 3072, 1024, "qkv"),
                         (512, 1024, 1024, "out"), (512, 1024, 4096, "ffn2")]:
-    a = torch.randn(M, K, device="cuda").bfloat16()
-    bs = [torch.randn(N, K, device="cuda").bfloat16() for _ in range(16)]
+    a = torch.randn(M, K, device="cuda").half()
+    bs = [torch.randn(N, K, device="cuda").half() for _ in range(16)]
     bias = torch.randn(N, device="cuda")
     res = torch.randn(M, N, device="cuda")
     c32 = torch.empty(M, N, device="cuda")
-    c16 = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    c16 = torch.empty(M, N, device="cuda", dtype=torch.float16)
     it = [0]
 
     def plain():

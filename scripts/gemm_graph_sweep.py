@@ -23,8 +23,8 @@ REPS = 24
 
 def run(M, N, K, plan, cold):
     nbuf = max(1, min(REPS, (200 << 20) // (N * K * 2) + 1)) if cold else 1
-    a = torch.randn(M, K, device="cuda").bfloat16()
-    bs = [torch.randn(N, K, device="cuda").bfloat16() for _ in range(nbuf)]
+    a = torch.randn(M, K, device="cuda").half()
+    bs = [torch.randn(N, K, device="cuda").half() for _ in range(nbuf)]
     c = torch.empty(M, N, device="cuda")
     lib.fq_gemm_force_plan(*plan)
     P.gemm(a, bs[0], c, transpose_b=True)

@@ -15,8 +15,8 @@ lib.fq_gemm_force_plan.argtypes = [ctypes.c_int] * 3
 dbg = torch.zeros(600, dtype=torch.int64, device="cuda")
 for (M, N, K, plan) in [(512, 1024, 1024, (32, 1, 1)), (512, 4096, 1024, (128, 1, 1)),
                         (512, 4096, 1024, (32, 1, 1)), (128, 128, 64, (128, 1, 1))]:
-    a = torch.randn(M, K, device="cuda").bfloat16()
-    b = torch.randn(N, K, device="cuda").bfloat16()
+    a = torch.randn(M, K, device="cuda").half()
+    b = torch.randn(N, K, device="cuda").half()
     c = torch.empty(M, N, device="cuda")
     lib.fq_gemm_force_plan(*plan)
     for _ in range(3):

@@ -7,9 +7,9 @@ lib = _abi.load()
 lib.fq_gemm_force_plan.argtypes = [ctypes.c_int] * 4
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 for M, N, K in [(512, 3072, 1024), (512, 4096, 1024), (512, 32000, 1024)]:
-    a = torch.randn(M, K, device="cuda").bfloat16()
-    b = torch.randn(N, K, device="cuda").bfloat16()
-    c = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    a = torch.randn(M, K, device="cuda").half()
+    b = torch.randn(N, K, device="cuda").half()
+    c = torch.empty(M, N, device="cuda", dtype=torch.float16)
     bias = torch.randn(N, device="cuda")
     out = []
     for plan in [(0, 0, 0, 1), (128, 1, 1, 1), (96, 1, 1, 1), (128, 1, 2, 1), (128, 1, 4, 1), (96, 1, 2, 1), (96, 1, 4, 1), (128, 2, 1, 1), (128, 4, 1, 1), (256, 1, 2, 1), (224, 1, 1, 1), (224, 1, 2, 1)]:

@@ -45,8 +45,8 @@ for M, N in [(512, 1024), (128, 1024), (512, 4096)]:
             if sp > 1 and ((M // 128) * (N // bn) * sp > 148 or sp > nkb):
                 row.append("   -  ")
                 continue
-            a = torch.randn(M, K, device="cuda").bfloat16()
-            b = torch.randn(N, K, device="cuda").bfloat16()
+            a = torch.randn(M, K, device="cuda").half()
+            b = torch.randn(N, K, device="cuda").half()
             c = torch.empty(M, N, device="cuda")
             lib.fq_gemm_force_plan(*plan)
             t = graph_time(lambda: P.gemm(a, b, c, transpose_b=True))

@@ -18,8 +18,8 @@ names = ["start", "prologue", "tma0", "tma_last", "full0", "commit_last", "tfull
          "exit_bar"]
 for M, N, K in [(512, 1024, 1024), (512, 1024, 4096), (512, 4096, 1024), (128, 1024, 1024),
                 (512, 1024, 256)]:
-    a = torch.randn(M, K, device="cuda").bfloat16()
-    b = torch.randn(N, K, device="cuda").bfloat16()
+    a = torch.randn(M, K, device="cuda").half()
+    b = torch.randn(N, K, device="cuda").half()
     c = torch.empty(M, N, device="cuda")
     for i in range(3):
         lib.fq_gemm_debug_timestamps(dbg.data_ptr())

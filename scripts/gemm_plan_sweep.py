@@ -18,8 +18,8 @@ shapes = [(512, 1024, 1024), (512, 4096, 1024), (512, 1024, 4096), (512, 32000, 
 plans = [(bn, 1, 1, 1) for bn in (32, 64, 128, 256)]
 plans += [(bn, 1, 1, s) for bn in (64, 128, 256) for s in (2, 3, 4, 6, 8)]
 for M, N, K in shapes:
-    a = torch.randn(M, K, device="cuda").bfloat16()
-    b = torch.randn(N, K, device="cuda").bfloat16()
+    a = torch.randn(M, K, device="cuda").half()
+    b = torch.randn(N, K, device="cuda").half()
     c = torch.empty(M, N, device="cuda")
     res = []
     for bn, cm, cn, sp in plans:

@@ -4,7 +4,7 @@ import numpy as np, torch
 import paper_2010_13887_b200 as P
 from paper_2010_13887_b200 import model as M
 cfg = P.ModelConfig(6, 6, 1024, 4096, 16, 32000, 128, 64, 4)
-sess = P.Session(cfg, P.make_random_weights(cfg, 0), precision="bf16")
+sess = P.Session(cfg, P.make_random_weights(cfg, 0), precision="fp16")
 src = np.random.default_rng(0).integers(3, 32000, size=(128, 64))
 dc = P.DecodeConfig(beam_size=4, max_steps=64)
 # capture hist at several steps by running generate with max_steps = s

@@ -1,5 +1,5 @@
 """Graph-timed A/B of the decode step's output layer at C2 (512 rows, V=32000,
-d=1024, bf16): materialised logits GEMM + fq_hars_step vs fq_logits_hars
+d=1024, fp16): materialised logits GEMM + fq_hars_step vs fq_logits_hars
 (statistics epilogue) + fq_hars_merge_step, each kernel alone and together."""
 import os
 import sys
@@ -15,8 +15,8 @@ from paper_2010_13887_b200 import _abi, decode as D
 B, K, V, S, d = 128, 4, 32000, 64, 1024
 R = B * K
 g = torch.Generator(device="cuda").manual_seed(0)
-E = (torch.randn(V, d, device="cuda", generator=g) * 0.05).bfloat16()
-xs = [torch.randn(R, d, device="cuda", generator=g).bfloat16() for _ in range(3)]
+E = (torch.randn(V, d, device="cuda", generator=g) * 0.05).half()
+xs = [torch.randn(R, d, device="cuda", generator=g).half() for _ in range(3)]
 logits = torch.empty(R, V, device="cuda")
 ldt = (V + 223) // 224
 dk = torch.full((R,), 8, dtype=torch.int32, device="cuda")

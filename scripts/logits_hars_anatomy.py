@@ -15,8 +15,8 @@ lib = _abi.load()
 lib.fq_gemm_debug_timestamps.argtypes = [ctypes.c_void_p]
 R, V, d, cap = 512, 32000, 1024, 128
 ldt = (V + 223) // 224
-x = (torch.randn(R, d, device="cuda") * 0.5).bfloat16()
-E = (torch.randn(V, d, device="cuda") / 32).bfloat16()
+x = (torch.randn(R, d, device="cuda") * 0.5).half()
+E = (torch.randn(V, d, device="cuda") / 32).half()
 dk = torch.full((R,), 8, dtype=torch.int32, device="cuda")
 gmax = torch.empty(R, 32, dtype=torch.int32, device="cuda")
 tmax = torch.empty(R, ldt, device="cuda")

@@ -15,8 +15,8 @@ lib.fq_retrieve_debug_timestamps.argtypes = [ctypes.c_void_p]
 B, K, V, S, d = 128, 4, 32000, 64, 1024
 R = B * K
 g = torch.Generator(device="cuda").manual_seed(0)
-E = (torch.randn(V, d, device="cuda", generator=g) * 0.05).bfloat16()
-x16 = torch.randn(R, d, device="cuda", generator=g).bfloat16()
+E = (torch.randn(V, d, device="cuda", generator=g) * 0.05).half()
+x16 = torch.randn(R, d, device="cuda", generator=g).half()
 ldt, cap = (V + 223) // 224, 128
 dk = torch.zeros(R, dtype=torch.int32, device="cuda")
 gmx = torch.full((R, 32), -2139095041, dtype=torch.int32, device="cuda")
@@ -37,7 +37,7 @@ rp = torch.empty(R, dtype=torch.int64, device="cuda")
 emb = torch.randn(V, d, device="cuda")
 pos = torch.randn(S, d, device="cuda")
 xn = torch.empty(R, d, device="cuda")
-xn16 = torch.empty(R, d, device="cuda", dtype=torch.bfloat16)
+xn16 = torch.empty(R, d, device="cuda", dtype=torch.float16)
 dbg = torch.zeros(R * 8, dtype=torch.int64, device="cuda")
 st.init()
 

@@ -12,7 +12,7 @@ import torch
 import paper_2010_13887_b200 as P
 
 ap = argparse.ArgumentParser()
-ap.add_argument("--precision", default="bf16")
+ap.add_argument("--precision", default="fp16")
 ap.add_argument("--batch", type=int, default=128)
 ap.add_argument("--steps", type=int, default=64)
 ap.add_argument("--graphs", type=int, default=1)

@@ -12,7 +12,7 @@ from torch.profiler import ProfilerActivity, profile
 
 import paper_2010_13887_b200 as P
 
-prec = sys.argv[1] if len(sys.argv) > 1 else "bf16"
+prec = sys.argv[1] if len(sys.argv) > 1 else "fp16"
 cfg = P.ModelConfig(6, 6, 1024, 4096, 16, 32000, 128, 64, 4)
 sess = P.Session(cfg, P.make_random_weights(cfg, 0), precision=prec)
 src = torch.from_numpy(np.random.default_rng(0).integers(3, 32000, size=(128, 64))).cuda()

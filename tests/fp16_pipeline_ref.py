@@ -1,13 +1,13 @@
-"""Float64 reference of the bf16 throughput pipeline (test infrastructure).
+"""Float64 reference of the fp16 throughput pipeline (test infrastructure).
 
-The north_star's bf16 bar ("fused-layer activations and beam scores within
+The north_star's fp16 bar ("fused-layer activations and beam scores within
 1e-3 relative") is checked against THIS reference: the reference algorithm
 (model.py:306-360 encoder layer, :537-631 decoder step, the tied logits) in
-float64, with bf16 rounding applied exactly where the device pipeline stores
-bf16 — the weights, every GEMM A operand, the self-attention K/V cache, the
+float64, with fp16 rounding applied exactly where the device pipeline stores
+fp16 — the weights, every GEMM A operand, the self-attention K/V cache, the
 cross K/V and the FFN hidden activations. Everything else (residual stream,
 LayerNorm statistics, attention arithmetic, logits) stays at full precision,
-as in the kernels. Comparing the device bf16 mode against the fp32 oracle
+as in the kernels. Comparing the device fp16 mode against the fp32 oracle
 instead mixes in the weight rounding itself (~1e-2)."""
 
 import math
@@ -17,7 +17,7 @@ import torch
 
 
 def bf(x):
-    return x.to(torch.bfloat16).to(torch.float64)
+    return x.to(torch.float16).to(torch.float64)
 
 
 def _ln(x, g, b, eps):
@@ -35,7 +35,7 @@ def _act(x, kind):
 
 
 def _lin(a16, w, b=None):
-    """a16 [n, in] (already bf16-valued), w the device bf16 [out, in] weight."""
+    """a16 [n, in] (already fp16-valued), w the device fp16 [out, in] weight."""
     y = a16 @ w.double().T
     return y + b.double() if b is not None else y
 

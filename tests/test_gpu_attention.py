@@ -1,8 +1,8 @@
 """Fused attention kernels (fq_attention.cu) against float64 torch references
 of the reference's three-step attention (gemm_batched QK^T -> scale_mask_softmax
 -> gemm_batched P.V, model.py:329-336 / :572-604), including the copy-free
-history-table KV cache. fp32 KV: 1e-5 relative; bf16 KV: operands rounded to
-bf16 in the reference too, 1e-4."""
+history-table KV cache. fp32 KV: 1e-5 relative; fp16 KV: operands rounded to
+fp16 in the reference too, 1e-4."""
 
 import math
 
@@ -45,7 +45,7 @@ def test_cross_attention(T, hd, beam, kv16):
     cq = T.randn(B * beam, d, device="cuda", generator=g)
     packed = T.randn(B * S, ld, device="cuda", generator=g)
     if kv16:
-        packed = packed.to(T.bfloat16)
+        packed = packed.to(T.float16)
     mask = T.zeros(B, S, device="cuda")
     mask[1, 30:] = -math.inf
     scale = float(np.float32(1 / math.sqrt(hd)))
@@ -53,7 +53,7 @@ def test_cross_attention(T, hd, beam, kv16):
     ck = packed[:, 2 * layer * d:]
     cv = packed[:, (2 * layer + 1) * d:]
     out = T.empty(B * beam, d, device="cuda")
-    out16 = T.empty(B * beam, d, device="cuda", dtype=T.bfloat16)
+    out16 = T.empty(B * beam, d, device="cuda", dtype=T.float16)
     bad = T.zeros(1, dtype=T.int32, device="cuda")
     A.call("fq_cross_attention", cq.data_ptr(), d, ck.data_ptr(), cv.data_ptr(), int(kv16), ld, B,
            beam, S, H, hd, scale, mask.data_ptr(), out.data_ptr(), out16.data_ptr(), d,
@@ -76,7 +76,7 @@ def test_decoder_self_attention_history_table(T, hd, kv16):
     g = T.Generator(device="cuda").manual_seed(hd + 7)
     rows, H, S, beam = 12, 3, 20, 4
     d = H * hd
-    dt = T.bfloat16 if kv16 else T.float32
+    dt = T.float16 if kv16 else T.float32
     kc = T.randn(S, rows, d, device="cuda", generator=g).to(dt)
     vc = T.randn(S, rows, d, device="cuda", generator=g).to(dt)
     cur = 13
@@ -148,14 +148,14 @@ def test_layer_norm_paths(T, rows, d):
                                           (32, 32, 4, 7), (8, 64, 8, 30), (4, 64, 6, 97),
                                           (16, 64, 5, 15), (16, 64, 5, 16)])
 def test_decoder_self_attention_rows_kernel(T, H, hd, rows, cur):
-    """The bf16 throughput-mode row kernel (CTA per beam row, 16-byte slot
-    segments, shuffle-reduced head dots) vs float64 on the bf16 cache."""
+    """The fp16 throughput-mode row kernel (CTA per beam row, 16-byte slot
+    segments, shuffle-reduced head dots) vs float64 on the fp16 cache."""
     A = _abi()
     g = T.Generator(device="cuda").manual_seed(H * hd + rows + cur)
     S, beam = (64 if cur < 64 else 128), 4
     d = H * hd
-    kc = T.randn(S, rows, d, device="cuda", generator=g).to(T.bfloat16)
-    vc = T.randn(S, rows, d, device="cuda", generator=g).to(T.bfloat16)
+    kc = T.randn(S, rows, d, device="cuda", generator=g).to(T.float16)
+    vc = T.randn(S, rows, d, device="cuda", generator=g).to(T.float16)
     hist = T.empty(rows, S, dtype=T.int32, device="cuda")
     for r in range(rows):
         item0 = (r // beam) * beam
@@ -163,14 +163,14 @@ def test_decoder_self_attention_rows_kernel(T, H, hd, rows, cur):
     sqkv = T.randn(rows, 3 * d, device="cuda", generator=g)
     d_cur = T.tensor([cur], dtype=T.int32, device="cuda")
     out = T.empty(rows, d, device="cuda")
-    out16 = T.empty(rows, d, device="cuda", dtype=T.bfloat16)
+    out16 = T.empty(rows, d, device="cuda", dtype=T.float16)
     scale = float(np.float32(1 / math.sqrt(hd)))
     A.call("fq_decoder_self_attention", sqkv.data_ptr(), 3 * d, kc.data_ptr(), vc.data_ptr(), 1,
            hist.data_ptr(), d_cur.data_ptr(), rows, H, hd, S, scale, out.data_ptr(),
            out16.data_ptr(), d, 0, A.stream_handle())
     T.cuda.synchronize()
-    knew = sqkv[:, d:2 * d].to(T.bfloat16).double()
-    vnew = sqkv[:, 2 * d:].to(T.bfloat16).double()
+    knew = sqkv[:, d:2 * d].to(T.float16).double()
+    vnew = sqkv[:, 2 * d:].to(T.float16).double()
     assert T.equal(kc[cur].double(), knew) and T.equal(vc[cur].double(), vnew)
     ar = T.arange(cur, device="cuda")
     for r in range(rows):
@@ -187,7 +187,7 @@ def test_decoder_self_attention_rows_kernel(T, H, hd, rows, cur):
 @pytest.mark.parametrize("H,hd,beam", [(16, 64, 4), (16, 64, 1), (8, 128, 3), (32, 32, 8),
                                        (16, 64, 6)])
 def test_cross_attention_stream_kernel(T, H, hd, beam):
-    """The bf16 throughput-mode cross-attention (CTA per item x head chunk)
+    """The fp16 throughput-mode cross-attention (CTA per item x head chunk)
     including a padded item and a fully masked item (counted in d_bad)."""
     A = _abi()
     g = T.Generator(device="cuda").manual_seed(H + hd + beam)
@@ -195,7 +195,7 @@ def test_cross_attention_stream_kernel(T, H, hd, beam):
     d = H * hd
     ld = 2 * L * d
     cq = T.randn(B * beam, d, device="cuda", generator=g)
-    packed = T.randn(B * S, ld, device="cuda", generator=g).to(T.bfloat16)
+    packed = T.randn(B * S, ld, device="cuda", generator=g).to(T.float16)
     mask = T.zeros(B, S, device="cuda")
     mask[1, 41:] = -math.inf
     mask[3, :] = -math.inf
@@ -204,7 +204,7 @@ def test_cross_attention_stream_kernel(T, H, hd, beam):
     ck = packed[:, 2 * layer * d:]
     cv = packed[:, (2 * layer + 1) * d:]
     out = T.empty(B * beam, d, device="cuda")
-    out16 = T.empty(B * beam, d, device="cuda", dtype=T.bfloat16)
+    out16 = T.empty(B * beam, d, device="cuda", dtype=T.float16)
     bad = T.zeros(1, dtype=T.int32, device="cuda")
     A.call("fq_cross_attention", cq.data_ptr(), d, ck.data_ptr(), cv.data_ptr(), 1, ld, B,
            beam, S, H, hd, scale, mask.data_ptr(), out.data_ptr(), out16.data_ptr(), d, 0,
@@ -232,7 +232,7 @@ def test_encoder_attention_tiled(T, S, hd, exact):
     mask = T.zeros(B, S, device="cuda")
     mask[1, S // 2 + 1:] = -math.inf
     out = T.empty(B * S, d, device="cuda")
-    out16 = T.empty(B * S, d, device="cuda", dtype=T.bfloat16)
+    out16 = T.empty(B * S, d, device="cuda", dtype=T.float16)
     bad = T.zeros(1, dtype=T.int32, device="cuda")
     scale = float(np.float32(1 / math.sqrt(hd)))
     A.call("fq_encoder_attention", qkv.data_ptr(), 3 * d, B, S, H, hd, scale, mask.data_ptr(),
@@ -259,11 +259,11 @@ def test_cross_attention_slabs_equal_reduced_query(T, M, beam, S):
     d, H, hd, L = 1024, 16, 64, 2
     B = M // beam
     R = B * beam
-    x16 = T.randn(R, d, device="cuda", generator=g).to(T.bfloat16)
-    w = (T.randn(d, d, device="cuda", generator=g) / 32).to(T.bfloat16)
+    x16 = T.randn(R, d, device="cuda", generator=g).to(T.float16)
+    w = (T.randn(d, d, device="cuda", generator=g) / 32).to(T.float16)
     bias = T.randn(d, device="cuda", generator=g) * 0.1
     ld = 2 * L * d
-    packed = T.randn(B * S, ld, device="cuda", generator=g).to(T.bfloat16)
+    packed = T.randn(B * S, ld, device="cuda", generator=g).to(T.float16)
     mask = T.zeros(B, S, device="cuda")
     mask[0, S // 2:] = -math.inf
     scale = float(np.float32(1 / math.sqrt(hd)))
@@ -271,7 +271,7 @@ def test_cross_attention_slabs_equal_reduced_query(T, M, beam, S):
     q = T.empty(R, d, device="cuda")
     import paper_2010_13887_b200 as P
     P.gemm(x16, w, q, transpose_b=True, bias=bias)
-    want = T.empty(R, d, device="cuda", dtype=T.bfloat16)
+    want = T.empty(R, d, device="cuda", dtype=T.float16)
     bad = T.zeros(1, dtype=T.int32, device="cuda")
     A.call("fq_cross_attention", q.data_ptr(), d, ck.data_ptr(), cv.data_ptr(), 1, ld, B, beam, S,
            H, hd, scale, mask.data_ptr(), None, want.data_ptr(), d, 0, bad.data_ptr(),
@@ -281,7 +281,7 @@ def test_cross_attention_slabs_equal_reduced_query(T, M, beam, S):
     A.call("fq_gemm_splitk_slabs", x16.data_ptr(), d, w.data_ptr(), d, ws.data_ptr(),
            ws.numel() * 4, R, d, d, ctypes.addressof(ns), A.stream_handle())
     assert ns.value == 4
-    got = T.empty(R, d, device="cuda", dtype=T.bfloat16)
+    got = T.empty(R, d, device="cuda", dtype=T.float16)
     A.call("fq_cross_attention_slabs", ws.data_ptr(), ns.value, d, bias.data_ptr(), ck.data_ptr(),
            cv.data_ptr(), ld, B, beam, S, H, hd, scale, mask.data_ptr(), None, got.data_ptr(), d,
            bad.data_ptr(), A.stream_handle())

@@ -7,7 +7,7 @@ against the fixture the reference itself produced (tests/golden/c2_golden.npz,
 
 fp32 (exact) mode: token ids bit-exact for every hypothesis of every item,
 scores within 1e-4, encoder memory and step-0 logits within 1e-5.
-bf16 mode (north_star: "fused-layer activations and beam scores within 1e-3
+fp16 mode (north_star: "fused-layer activations and beam scores within 1e-3
 relative"): each fused encoder / decoder layer against the CPU oracle's layer
 on the same fp32 input, and the beam scores of the hypotheses whose tokens
 agree with the reference, each held to the bar stated in the test."""
@@ -88,19 +88,19 @@ def test_c2_exact_mode_token_identical(P, c2):
     assert _rel(step0, g["step0_logits_item0"]) <= 1e-5
 
 
-def test_c2_bf16_mode_beam_scores_vs_reference(P, c2):
-    """bf16 mode at C2: token agreement with the reference is reported (bf16
+def test_c2_fp16_mode_beam_scores_vs_reference(P, c2):
+    """fp16 mode at C2: token agreement with the reference is reported (fp16
     GEMM operands move near-tie selections), and every hypothesis
     whose tokens agree carries a beam score within 1e-3 relative of the
     reference's (north_star bar)."""
     g, cfg, w = c2
-    sess = P.Session(cfg, w, precision="bf16")
+    sess = P.Session(cfg, w, precision="fp16")
     hyps = sess.generate(g["src"], P.DecodeConfig(beam_size=4, max_steps=64, eos_token=2))
     same_items, pairs = _hyp_match(hyps, g)
     best_same = sum(hs[0].tokens == g["tok"][b, 0][:g["len"][b, 0]].tolist()
                     for b, hs in enumerate(hyps))
     d = np.array([abs(a - b) / abs(b) for a, b in pairs])
-    print(f"C2 bf16: best hypothesis identical {best_same}/128, full lists {same_items}/128, "
+    print(f"C2 fp16: best hypothesis identical {best_same}/128, full lists {same_items}/128, "
           f"token-identical hypotheses {len(pairs)}/512, score rel max {d.max():.2e} "
           f"median {np.median(d):.2e}")
     assert len(pairs) >= 64  # enough agreeing hypotheses for the score bar to mean something
@@ -113,8 +113,8 @@ def _oracle(cfg):
     return O, O.OracleModel(ocfg, O.make_random_weights(ocfg, 0))
 
 
-def test_c2_bf16_fused_layer_activations_vs_oracle(P, c2):
-    """bf16 mode, one fused layer at a time on the reference's own fp32 layer
+def test_c2_fp16_fused_layer_activations_vs_oracle(P, c2):
+    """fp16 mode, one fused layer at a time on the reference's own fp32 layer
     input (two C2 items): every encoder layer's output against the oracle's
     encoder layer (model.py:306-360) on that input. The bar: normwise relative
     error <= 1e-3 (north_star), measured per layer and printed."""
@@ -124,7 +124,7 @@ def test_c2_bf16_fused_layer_activations_vs_oracle(P, c2):
     O, om = _oracle(cfg)
     src = g["src"][:2]
     batch, seq = src.shape
-    dw = M.DeviceWeights.get(cfg, w, "bf16")
+    dw = M.DeviceWeights.get(cfg, w, "fp16")
     x = O.embed_scale_pos(src.reshape(-1), om.w["token_embedding"], math.sqrt(cfg.d_model),
                           om.pos, 0, seq)
     errs = []
@@ -133,5 +133,5 @@ def test_c2_bf16_fused_layer_activations_vs_oracle(P, c2):
         got, _ = M.encoder_layer_forward(torch.from_numpy(x).cuda(), dw.enc[i], cfg, None, batch)
         errs.append(_normrel(got.cpu().numpy(), want))
         x = want
-    print("C2 bf16 encoder layers, normwise rel error:", " ".join(f"{e:.2e}" for e in errs))
+    print("C2 fp16 encoder layers, normwise rel error:", " ".join(f"{e:.2e}" for e in errs))
     assert max(errs) <= 1e-3, errs

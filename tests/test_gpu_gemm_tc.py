@@ -1,6 +1,6 @@
-"""tcgen05 bf16 GEMM (fq_gemm_tc.cu) against a float64 reference of the same
-bf16-rounded operands. Tolerance: fp32 accumulation differences only, 1e-3
-relative (the north_star's bf16 bar)."""
+"""tcgen05 fp16 GEMM (fq_gemm_tc.cu) against a float64 reference of the same
+fp16-rounded operands. Tolerance: fp32 accumulation differences only, 1e-3
+relative (the north_star's fp16 bar)."""
 
 import numpy as np
 import pytest
@@ -39,8 +39,8 @@ def _rel(got, want):
 def test_tc_gemm_plain(P, M, N, K):
     import torch
     g = torch.Generator(device="cuda").manual_seed(M * 7 + N * 3 + K)
-    a = torch.randn(M, K, device="cuda", generator=g).to(torch.bfloat16)
-    b = torch.randn(N, K, device="cuda", generator=g).to(torch.bfloat16)
+    a = torch.randn(M, K, device="cuda", generator=g).to(torch.float16)
+    b = torch.randn(N, K, device="cuda", generator=g).to(torch.float16)
     out = torch.empty(M, N, device="cuda")
     P.gemm(a, b, out, transpose_b=True)
     torch.cuda.synchronize()
@@ -52,23 +52,23 @@ def test_tc_gemm_epilogue(P, act):
     import torch
     M, N, K = 384, 1536, 512
     g = torch.Generator(device="cuda").manual_seed(5)
-    a = torch.randn(M, K, device="cuda", generator=g).to(torch.bfloat16)
-    b = torch.randn(N, K, device="cuda", generator=g).to(torch.bfloat16)
+    a = torch.randn(M, K, device="cuda", generator=g).to(torch.float16)
+    b = torch.randn(N, K, device="cuda", generator=g).to(torch.float16)
     bias = torch.randn(N, device="cuda", generator=g)
     res = torch.randn(M, N, device="cuda", generator=g)
     out = torch.empty(M, N, device="cuda")
     P.gemm(a, b, out, transpose_b=True, bias=bias, activation=act, residual=res)
     assert _rel(out, _ref(a, b, bias, act, res)) <= 1e-3
-    out16 = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    out16 = torch.empty(M, N, device="cuda", dtype=torch.float16)
     P.gemm(a, b, out16, transpose_b=True, bias=bias, activation=act)
-    assert _rel(out16.float(), _ref(a, b, bias, act)) <= 8e-3  # bf16 output rounding
+    assert _rel(out16.float(), _ref(a, b, bias, act)) <= 8e-3  # fp16 output rounding
 
 
 def test_tc_gemm_strided_output_and_accumulate(P):
     import torch
     M, N, K = 256, 256, 256
-    a = torch.randn(M, K, device="cuda").to(torch.bfloat16)
-    b = torch.randn(N, K, device="cuda").to(torch.bfloat16)
+    a = torch.randn(M, K, device="cuda").to(torch.float16)
+    b = torch.randn(N, K, device="cuda").to(torch.float16)
     big = torch.zeros(M, 2 * N, device="cuda")
     view = big[:, N:]
     view.fill_(1.0)
@@ -89,8 +89,8 @@ def test_tc_gemm_all_plans(P, M, N, K):
     lib = _abi.load()
     lib.fq_gemm_force_plan.argtypes = [ctypes.c_int] * 4
     g = torch.Generator(device="cuda").manual_seed(M + N + K)
-    a = torch.randn(M, K, device="cuda", generator=g).to(torch.bfloat16)
-    b = torch.randn(N, K, device="cuda", generator=g).to(torch.bfloat16)
+    a = torch.randn(M, K, device="cuda", generator=g).to(torch.float16)
+    b = torch.randn(N, K, device="cuda", generator=g).to(torch.float16)
     bias = torch.randn(N, device="cuda", generator=g)
     res = torch.randn(M, N, device="cuda", generator=g)
     want = _ref(a, b, bias, "relu", res)
@@ -115,8 +115,8 @@ def test_tc_gemm_wide_tile_epilogue(P, M, N, K):
     """Tile widths 192/224 (wave-quantisation plan) with the fused epilogue."""
     import torch
     g = torch.Generator(device="cuda").manual_seed(N + K)
-    a = torch.randn(M, K, device="cuda", generator=g).to(torch.bfloat16)
-    b = torch.randn(N, K, device="cuda", generator=g).to(torch.bfloat16)
+    a = torch.randn(M, K, device="cuda", generator=g).to(torch.float16)
+    b = torch.randn(N, K, device="cuda", generator=g).to(torch.float16)
     bias = torch.randn(N, device="cuda", generator=g)
     res = torch.randn(M, N, device="cuda", generator=g)
     out = torch.empty(M, N, device="cuda")
@@ -130,14 +130,14 @@ def test_tc_gemm_wide_tile_epilogue(P, M, N, K):
 def test_gemm_ln_equals_gemm_then_layer_norm(M, N, K):
     """fq_gemm_ln (the LayerNorm inside the split-K epilogue, row-block
     statistics exchanged between the CTAs) against fq_gemm (bias + residual)
-    followed by fq_layer_norm: fp32 and bf16 outputs, repeated launches (the
+    followed by fq_layer_norm: fp32 and fp16 outputs, repeated launches (the
     counters reset themselves). N = 768 takes the unfused fallback."""
     import torch
     from paper_2010_13887_b200 import _abi
     import paper_2010_13887_b200 as P
     g = torch.Generator(device="cuda").manual_seed(M + N + K)
-    a = torch.randn(M, K, device="cuda", generator=g).bfloat16()
-    w = (torch.randn(N, K, device="cuda", generator=g) / K ** 0.5).bfloat16()
+    a = torch.randn(M, K, device="cuda", generator=g).half()
+    w = (torch.randn(N, K, device="cuda", generator=g) / K ** 0.5).half()
     bias = torch.randn(N, device="cuda", generator=g) * 0.1
     res = torch.randn(M, N, device="cuda", generator=g)
     gam = torch.randn(N, device="cuda", generator=g)
@@ -145,7 +145,7 @@ def test_gemm_ln_equals_gemm_then_layer_norm(M, N, K):
     pre = torch.empty(M, N, device="cuda")
     P.gemm(a, w, pre, transpose_b=True, bias=bias, residual=res)
     want = torch.empty(M, N, device="cuda")
-    want16 = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    want16 = torch.empty(M, N, device="cuda", dtype=torch.float16)
     hs = _abi.stream_handle
     _abi.call("fq_layer_norm", pre.data_ptr(), N, gam.data_ptr(), bet.data_ptr(), 1e-5, M, N,
               want.data_ptr(), N, want16.data_ptr(), N, hs())
@@ -153,7 +153,7 @@ def test_gemm_ln_equals_gemm_then_layer_norm(M, N, K):
     ws = torch.zeros((wsb + 15) // 16 * 4, dtype=torch.int32, device="cuda")
     for _ in range(3):
         out = torch.full((M, N), float("nan"), device="cuda")
-        out16 = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+        out16 = torch.empty(M, N, device="cuda", dtype=torch.float16)
         _abi.call("fq_gemm_ln", a.data_ptr(), K, w.data_ptr(), K, bias.data_ptr(), res.data_ptr(),
                   N, gam.data_ptr(), bet.data_ptr(), 1e-5, out.data_ptr(), N, out16.data_ptr(), N,
                   ws.data_ptr(), ws.numel() * 4, M, N, K, hs())
@@ -177,8 +177,8 @@ def test_gemm_ln_slab_path_bit_identical(M, N, K):
     from paper_2010_13887_b200 import _abi
     import paper_2010_13887_b200 as P
     g = torch.Generator(device="cuda").manual_seed(7 * M + N + K)
-    a = torch.randn(M, K, device="cuda", generator=g).bfloat16()
-    w = (torch.randn(N, K, device="cuda", generator=g) / K ** 0.5).bfloat16()
+    a = torch.randn(M, K, device="cuda", generator=g).half()
+    w = (torch.randn(N, K, device="cuda", generator=g) / K ** 0.5).half()
     bias = torch.randn(N, device="cuda", generator=g) * 0.1
     res = torch.randn(M, N, device="cuda", generator=g)
     gam = torch.randn(N, device="cuda", generator=g)
@@ -186,14 +186,14 @@ def test_gemm_ln_slab_path_bit_identical(M, N, K):
     pre = torch.empty(M, N, device="cuda")
     P.gemm(a, w, pre, transpose_b=True, bias=bias, residual=res)
     want = torch.empty(M, N, device="cuda")
-    want16 = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    want16 = torch.empty(M, N, device="cuda", dtype=torch.float16)
     hs = _abi.stream_handle
     _abi.call("fq_layer_norm", pre.data_ptr(), N, gam.data_ptr(), bet.data_ptr(), 1e-5, M, N,
               want.data_ptr(), N, want16.data_ptr(), N, hs())
     ws = torch.full((4 * M * N,), float("nan"), device="cuda")
     for _ in range(2):
         out = torch.full((M, N), float("nan"), device="cuda")
-        out16 = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+        out16 = torch.empty(M, N, device="cuda", dtype=torch.float16)
         _abi.call("fq_gemm_ln", a.data_ptr(), K, w.data_ptr(), K, bias.data_ptr(), res.data_ptr(),
                   N, gam.data_ptr(), bet.data_ptr(), 1e-5, out.data_ptr(), N, out16.data_ptr(), N,
                   ws.data_ptr(), ws.numel() * 4, M, N, K, hs())
@@ -202,7 +202,7 @@ def test_gemm_ln_slab_path_bit_identical(M, N, K):
         assert torch.equal(out16, want16)
 
 
-@pytest.mark.parametrize("dt", ["f32", "bf16"])
+@pytest.mark.parametrize("dt", ["f32", "fp16"])
 @pytest.mark.parametrize("M,N,K,pad", [(200, 256, 256, 64), (512, 96, 512, 32), (77, 160, 128, 3)])
 def test_tc_gemm_tma_store_strided_views(P, dt, M, N, K, pad):
     """The TMA-store epilogue writes through a tensor map with the output's
@@ -210,10 +210,10 @@ def test_tc_gemm_tma_store_strided_views(P, dt, M, N, K, pad):
     exactly its M x N block, the padding columns stay untouched; pad = 3 makes
     the rows unaligned for TMA and takes the transposed-store path."""
     import torch
-    dtype = torch.float32 if dt == "f32" else torch.bfloat16
+    dtype = torch.float32 if dt == "f32" else torch.float16
     g = torch.Generator(device="cuda").manual_seed(M + N + pad)
-    a = torch.randn(M, K, device="cuda", generator=g).to(torch.bfloat16)
-    b = torch.randn(N, K, device="cuda", generator=g).to(torch.bfloat16)
+    a = torch.randn(M, K, device="cuda", generator=g).to(torch.float16)
+    b = torch.randn(N, K, device="cuda", generator=g).to(torch.float16)
     bias = torch.randn(N, device="cuda", generator=g)
     big = torch.full((M, N + pad), 7.0, device="cuda", dtype=dtype)
     view = big[:, pad:]

@@ -4,7 +4,7 @@ reference's golden fixtures and the CPU oracle (tests/golden, oracle/).
 Bars: integer/index outputs bit-exact (candidates, thresholds, group maxima,
 token ids in fp32 mode); fp32 activations within 1e-5 relative of the
 reference's own outputs (kernels.py semantics, different reduction order);
-bf16 mode within 1e-3 relative on activations (north_star)."""
+fp16 mode within 1e-3 relative on activations (north_star)."""
 
 import json
 import math
@@ -274,13 +274,13 @@ def test_sampling_generate_matches_reference_fixture(P, ci):
     assert nrun == 14
 
 
-@pytest.mark.parametrize("precision", ["fp32", "bf16"])
+@pytest.mark.parametrize("precision", ["fp32", "fp16"])
 @pytest.mark.parametrize("ci", [0, 1])
 def test_classify_matches_reference_fixture(P, ci, precision):
     """Encoder-only classification (engine.py:198-224): first-position
     pooling, output projection, argmax + exact probability from one retrieve
     pass (decode.py:485-492). fp32: labels identical, probabilities <= 1e-5
-    relative; bf16: labels identical where the reference's margin is clear."""
+    relative; fp16: labels identical where the reference's margin is clear."""
     g = np.load(golden_path("classify_golden.npz"))
     kw = json.loads(str(g["cfgs"]))[ci]
     cfg = P.ModelConfig(**kw)
@@ -338,7 +338,7 @@ def test_graph_and_eager_paths_identical(P):
         [[h.tokens for h in x] for x in s.generate(src, dc)]
 
 
-@pytest.mark.parametrize("precision", ["fp32", "bf16"])
+@pytest.mark.parametrize("precision", ["fp32", "fp16"])
 def test_two_group_overlap_identical(P, precision):
     """streams=2 (two item groups decoded on two streams inside the step
     graph) gives exactly the single-chain hypotheses and scores: every op is
@@ -374,10 +374,10 @@ def test_c1_transformer_base_exact_mode_token_identical(P):
     assert rel(step0, g["step0_logits_item0"]) <= 1e-5
 
 
-def test_bf16_mode_tracks_oracle(P, O):
-    """Throughput mode: activations and logits within the bf16 tolerance."""
+def test_fp16_mode_tracks_oracle(P, O):
+    """Throughput mode: activations and logits within the fp16 tolerance."""
     g, cfg, w = _tiny(P, 0)
-    sess = P.Session(cfg, w, precision="bf16")
+    sess = P.Session(cfg, w, precision="fp16")
     src, tgt = g["m0_src"], g["m0_tgt"]
     enc = sess.encode(src)
     assert rel(enc, g["m0_enc"]) <= 2e-2
@@ -547,7 +547,7 @@ def test_logits_hars_equals_materialised_path(P, B, d, V):
     R = B * K
     g = torch.Generator(device="cuda").manual_seed(3)
     lp = D.length_penalty_table(0.6, S, "cuda")
-    E = (torch.randn(V, d, device="cuda", generator=g) * 0.5).bfloat16()
+    E = (torch.randn(V, d, device="cuda", generator=g) * 0.5).half()
     emb = torch.randn(V, d, device="cuda", generator=g)
     pos = torch.randn(S, d, device="cuda", generator=g)
     ldt = (V + 223) // 224
@@ -577,7 +577,7 @@ def test_logits_hars_equals_materialised_path(P, B, d, V):
     _abi.call("fq_hars_groups", b["st"].c, B, K, V, 0, dk.data_ptr(), hs())
     logits = torch.empty(R, V, device="cuda")
     for t in range(S - 1):
-        x16 = torch.randn(R, d, device="cuda", generator=g).bfloat16()
+        x16 = torch.randn(R, d, device="cuda", generator=g).half()
         x16[:, :8] += 2.0 * (t % 3 == 2)  # shifts every logit row: ties of nothing, EOS mixes in
         P.gemm(x16, E, logits, transpose_b=True)
         _abi.call("fq_hars_step", logits.data_ptr(), V, a["st"].c, B, K, V, S, eos, lp.data_ptr(),
@@ -619,7 +619,7 @@ def test_logits_hars_equals_materialised_path(P, B, d, V):
 @pytest.mark.parametrize("mode", ["slab", "coresident"])
 def test_fused_layer_norm_engine_path(P, monkeypatch, mode):
     """Session.generate with the GEMM + LN pairs as fq_gemm_ln gives the same
-    hypotheses as the unfused path (FQ_FUSE_LN=0) at a bf16 config whose decode
+    hypotheses as the unfused path (FQ_FUSE_LN=0) at a fp16 config whose decode
     GEMMs run split-K (d = 1024). The slab path (the default) reduces the K
     slices in the same order as the in-kernel reduction: bit-identical."""
     cfg = P.ModelConfig(num_encoder_layers=1, num_decoder_layers=2, d_model=1024, d_ff=4096,
@@ -629,9 +629,9 @@ def test_fused_layer_norm_engine_path(P, monkeypatch, mode):
     src = np.random.default_rng(3).integers(3, cfg.vocab_size, size=(32, 8))
     dc = P.DecodeConfig(beam_size=4, max_steps=8, eos_token=2)
     monkeypatch.setenv("FQ_FUSE_LN", "0")
-    want = P.Session(cfg, w, precision="bf16").generate(src, dc)
+    want = P.Session(cfg, w, precision="fp16").generate(src, dc)
     monkeypatch.setenv("FQ_FUSE_LN", mode)
-    got = P.Session(cfg, w, precision="bf16").generate(src, dc)
+    got = P.Session(cfg, w, precision="fp16").generate(src, dc)
     if mode == "slab":
         for x, y in zip(got, want):
             assert [h.tokens for h in x] == [h.tokens for h in y]
@@ -653,9 +653,9 @@ def test_logits_hars_engine_path_token_identical(P, monkeypatch):
     w = P.make_random_weights(cfg, seed=4)
     src = np.random.default_rng(2).integers(3, cfg.vocab_size, size=(8, 10))
     dc = P.DecodeConfig(beam_size=4, max_steps=12, eos_token=2, length_penalty=0.6)
-    want = P.Session(cfg, w, precision="bf16").generate(src, dc)
+    want = P.Session(cfg, w, precision="fp16").generate(src, dc)
     monkeypatch.setenv("FQ_LOGITS_HARS", "1")
-    got = P.Session(cfg, w, precision="bf16").generate(src, dc)
+    got = P.Session(cfg, w, precision="fp16").generate(src, dc)
     assert [[h.tokens for h in x] for x in got] == [[h.tokens for h in x] for x in want]
     for x, y in zip(got, want):
         for h1, h2 in zip(x, y):
@@ -668,24 +668,24 @@ def test_logits_hars_engine_path_token_identical(P, monkeypatch):
           vocab_size=4096, max_batch=3, max_seq_len=24, max_beam_size=4), 2e-3),
     (dict(num_encoder_layers=1, num_decoder_layers=1, d_model=512, d_ff=1024, num_heads=8,
           vocab_size=1000, max_batch=2, max_seq_len=16, max_beam_size=4, activation="gelu"), 2e-3),
-    # stacked layers: single bf16 rounding flips (2^-8 in one element) accumulate
+    # stacked layers: single fp16 rounding flips (2^-8 in one element) accumulate
     (dict(num_encoder_layers=3, num_decoder_layers=3, d_model=256, d_ff=512, num_heads=4,
           vocab_size=4096, max_batch=3, max_seq_len=24, max_beam_size=4), 5e-3),
 ])
-def test_bf16_mode_vs_bf16_pipeline_reference(P, kw, bar):
-    """north_star bf16 bar: fused-layer activations (encoder output) and the
-    decoder's per-position logits against a float64 reference of the same bf16
-    pipeline (tests/bf16_pipeline_ref.py: bf16 where the device stores bf16,
+def test_fp16_mode_vs_fp16_pipeline_reference(P, kw, bar):
+    """north_star fp16 bar: fused-layer activations (encoder output) and the
+    decoder's per-position logits against a float64 reference of the same fp16
+    pipeline (tests/fp16_pipeline_ref.py: fp16 where the device stores fp16,
     exact elsewhere). Most rows agree to ~2e-7; a row in which an fp32-vs-f64
-    accumulation difference pushes a value across a bf16 rounding boundary
-    moves by one bf16 ulp in that element (row error up to ~2e-3), so one
+    accumulation difference pushes a value across a fp16 rounding boundary
+    moves by one fp16 ulp in that element (row error up to ~2e-3), so one
     layer is held to 2e-3 RMS (measured 3e-4 .. 1.4e-3), the elementwise max to
     1e-2 and stacked layers to 5e-3 RMS."""
     import torch
-    import bf16_pipeline_ref as REF
+    import fp16_pipeline_ref as REF
     cfg = P.ModelConfig(**kw)
     w = P.make_random_weights(cfg, seed=21)
-    sess = P.Session(cfg, w, precision="bf16")
+    sess = P.Session(cfg, w, precision="fp16")
     rng = np.random.default_rng(4)
     B = cfg.max_batch
     src = rng.integers(3, cfg.vocab_size, size=(B, 13))
