@@ -201,6 +201,47 @@ int fq_gemm_f32x3_ln(const float* a, int64_t lda, const float* b, const float* b
                      void* ws, int64_t ws_bytes, int64_t M, int64_t N, int64_t K,
                      fq_stream_t stream);
 
+/* Exact fp32 mode, 3xFP16 (replaces tensor.py:179-204's OpenBLAS SGEMM on the
+ * engine path): C = epilogue(A . B^T) as in fq_gemm with A [M,K] and B [N,K]
+ * given as fp16 pairs x = hi + lo * 2^-11 (fq_split_f16; the producing
+ * kernels write them directly). tcgen05 kind::f16 MMAs accumulate
+ * a_hi.b_hi and a_hi.b_lo + a_lo.b_hi into two fp32 TMEM accumulators, summed
+ * with RN adds every 128 K elements; the K order depends on (N, K) only
+ * (bitwise independent of M). 22-bit operand precision, like 3xTF32, at the
+ * kind::f16 rate and half the operand bytes. Operands |x| < 65504. */
+int fq_gemm_x3h(const void* a, const void* a_lo, int64_t lda, const void* b, const void* b_lo,
+                int64_t ldb, float* c, int64_t ldc, int64_t M, int64_t N, int64_t K,
+                int accumulate, const float* bias, const float* residual, int64_t ldr, int act,
+                fq_stream_t stream);
+
+/* out = LN(a . b^T + bias + residual) with fq_gemm_x3h operands (the closing
+ * GEMM + LN pairs, model.py:339-358 / :582-626); out16 / out16_lo (optional)
+ * receive the output's fp16 pair for the next exact-mode GEMM. The 4-slice
+ * plan writes K-slice slabs to ws, summed in slice order by the LN kernel. */
+int fq_gemm_x3h_ln(const void* a, const void* a_lo, int64_t lda, const void* b,
+                   const void* b_lo, int64_t ldb, const float* bias, const float* res,
+                   int64_t ldr, const float* gamma, const float* beta, double eps, float* out,
+                   int64_t ldo, void* out16, void* out16_lo, int64_t ldo16, void* ws,
+                   int64_t ws_bytes, int64_t M, int64_t N, int64_t K, fq_stream_t stream);
+
+/* fp16 pairs (hi, lo) of a row-major fp32 [rows, cols] matrix (leading dim
+ * lds): x = hi + lo * 2^-11. transpose: hi/lo are [cols, rows] (the K-major
+ * layout of a [K, N] weight; ldo >= rows), else [rows, cols] (ldo >= cols). */
+int fq_split_f16(const float* src, int64_t lds, int64_t rows, int64_t cols, int transpose,
+                 void* hi, void* lo, int64_t ldo, fq_stream_t stream);
+
+/* fq_layer_norm / fq_splitk_bias_residual_layer_norm whose fp16 output is the
+ * exact mode's pair: out16 = hi, out16_lo = lo (fq_split_f16 semantics). */
+int fq_layer_norm_xh(const float* x, int64_t ldx, const float* gamma, const float* beta,
+                     double eps, int64_t rows, int64_t d, float* out, int64_t ldo, void* out16,
+                     void* out16_lo, int64_t ldo16, fq_stream_t stream);
+int fq_splitk_bias_residual_layer_norm_xh(const float* slabs, int nslab, int64_t ld,
+                                          const float* bias, const float* residual, int64_t ldr,
+                                          const float* gamma, const float* beta, double eps,
+                                          int64_t rows, int64_t d, float* out, int64_t ldo,
+                                          void* out16, void* out16_lo, int64_t ldo16,
+                                          fq_stream_t stream);
+
 /* Weight preparation for fq_gemm_f32x3 (once, at load): hi = tf32(src) (round
  * to nearest, ties away), lo = tf32(src - hi); src [rows, cols] row-major;
  * transpose: hi/lo are [cols, rows] (the K-major layout of a [K, N] weight). */

@@ -81,6 +81,13 @@ SIGNATURES = {
     "fq_gemm_f32x3_ln": ([P, I64, P, P, I64, P, P, I64, P, P, F64, P, I64, P, I64, I64, I64, I64,
                           P], I32),
     "fq_split_tf32": ([P, I64, I64, I32, P, P, P], I32),
+    "fq_gemm_x3h": ([P, P, I64, P, P, I64, P, I64, I64, I64, I64, I32, P, P, I64, I32, P], I32),
+    "fq_gemm_x3h_ln": ([P, P, I64, P, P, I64, P, P, I64, P, P, F64, P, I64, P, P, I64, P, I64, I64,
+                        I64, I64, P], I32),
+    "fq_split_f16": ([P, I64, I64, I64, I32, P, P, I64, P], I32),
+    "fq_layer_norm_xh": ([P, I64, P, P, F64, I64, I64, P, I64, P, P, I64, P], I32),
+    "fq_splitk_bias_residual_layer_norm_xh": ([P, I32, I64, P, P, I64, P, P, F64, I64, I64, P, I64,
+                                               P, P, I64, P], I32),
 }
 
 _ERRORS = {-1: DimensionError, -2: ParameterError, -3: AliasingError, -4: CapacityError,
@@ -130,7 +137,7 @@ def load():
 # (name, args, start, end) is appended. Off (None) on the product path.
 PROBE = None
 PROBE_NAMES = ("fq_gemm", "fq_logits_hars", "fq_gemm_ln", "fq_gemm_splitk_slabs", "fq_gemm_f32x3",
-               "fq_gemm_f32x3_ln")
+               "fq_gemm_f32x3_ln", "fq_gemm_x3h", "fq_gemm_x3h_ln")
 
 
 def call(name: str, *args) -> int:
@@ -156,7 +163,7 @@ def call(name: str, *args) -> int:
     if name not in _NO_PREPARE:
         # every other entry point launches one kernel; fq_gemm_ln two (the
         # split-K slab GEMM + the reducing LN, or the GEMM + LN fallback)
-        _launches[0] += 2 if name in ("fq_gemm_ln", "fq_gemm_f32x3_ln") else 1
+        _launches[0] += 2 if name in ("fq_gemm_ln", "fq_gemm_f32x3_ln", "fq_gemm_x3h_ln") else 1
     if rc < 0:
         msg = lib.fq_last_error().decode("utf-8", "replace")
         raise _ERRORS.get(rc, EngineError)(f"{name}: {msg}")

@@ -84,6 +84,25 @@ __global__ void split_tf32_kernel(const float* __restrict__ src, int64_t rows, i
   }
 }
 
+// Exact-mode fp16 pairs (split_xh) of a row-major fp32 [rows, cols] matrix
+// (leading dim lds); transpose: hi/lo are [cols, rows] (ldo = rows), the
+// K-major layout of a [K, N] weight, else [rows, cols] with leading dim ldo.
+__global__ void split_xh_kernel(const float* __restrict__ src, int64_t lds, int64_t rows,
+                                int64_t cols, int transpose, h16* __restrict__ hi,
+                                h16* __restrict__ lo, int64_t ldo) {
+  pdl_enter();
+  const int64_t n = rows * cols;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / cols, c = i % cols;
+    h16 h, l;
+    split_xh(src[r * lds + c], h, l);
+    const int64_t o = transpose ? c * ldo + r : r * ldo + c;
+    hi[o] = h;
+    lo[o] = l;
+  }
+}
+
 int attention_prepare();
 int gemm_tc_prepare();
 }  // namespace fq
@@ -137,6 +156,19 @@ int fq_split_tf32(const float* src, int64_t rows, int64_t cols, int transpose, f
   fq::launch_kernel(fq::split_tf32_kernel, grid, 256, 0, fq::as_stream(stream), 1u, src, rows,
                     cols, transpose, hi, lo);
   return fq::launch_status("fq_split_tf32");
+}
+
+int fq_split_f16(const float* src, int64_t lds, int64_t rows, int64_t cols, int transpose,
+                 void* hi, void* lo, int64_t ldo, fq_stream_t stream) {
+  FQ_CHECK_ARG(src && hi && lo && rows > 0 && cols > 0 && lds >= cols &&
+                   ldo >= (transpose ? rows : cols),
+               FQ_ERR_DIMENSION, "fq_split_f16: bad args");
+  const int64_t n = rows * cols;
+  int grid = (int)((n + 255) / 256 < 148 * 16 ? (n + 255) / 256 : 148 * 16);
+  fq::launch_kernel(fq::split_xh_kernel, grid, 256, 0, fq::as_stream(stream), 1u, src, lds, rows,
+                    cols, transpose, reinterpret_cast<fq::h16*>(hi),
+                    reinterpret_cast<fq::h16*>(lo), ldo);
+  return fq::launch_status("fq_split_f16");
 }
 
 }  // extern "C"

@@ -73,6 +73,23 @@ using h16x2 = __half2;
 __device__ __forceinline__ float h2f(h16 x) { return __half2float(x); }
 __device__ __forceinline__ h16 f2h(float x) { return __float2half_rn(x); }
 
+// Exact-mode operand pair (OP_X3H GEMMs, 3xFP16): x = hi + lo * 2^-11 with
+// hi = fp16(x) and lo = fp16((x - hi) * 2^11), both round-to-nearest. x - hi is
+// exact in fp32 and the 2^11 scale keeps lo out of fp16's subnormal range, so
+// the pair holds 22 significant bits (|x| < 65504).
+constexpr float kXhScale = 2048.0f;
+__device__ __forceinline__ void split_xh(float x, h16& hi, h16& lo) {
+  hi = __float2half_rn(x);
+  lo = __float2half_rn((x - __half2float(hi)) * kXhScale);
+}
+__device__ __forceinline__ void split_xh2(float x0, float x1, uint32_t& hi, uint32_t& lo) {
+  const h16x2 h = __floats2half2_rn(x0, x1);
+  const float2 hf = __half22float2(h);
+  const h16x2 l = __floats2half2_rn((x0 - hf.x) * kXhScale, (x1 - hf.y) * kXhScale);
+  hi = *reinterpret_cast<const uint32_t*>(&h);
+  lo = *reinterpret_cast<const uint32_t*>(&l);
+}
+
 // fp32 ops with explicit rounding so nvcc never contracts them into FMA
 // (two separately rounded fp32 operations).
 __device__ __forceinline__ float fmul_rn(float a, float b) { return __fmul_rn(a, b); }

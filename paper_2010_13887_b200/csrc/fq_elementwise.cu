@@ -11,6 +11,16 @@
 
 namespace fq {
 
+// fp16 copy of 4 outputs (the next GEMM's operand): hi only (throughput mode)
+// or the exact mode's hi + lo pair (split_xh) when lo != NULL.
+__device__ __forceinline__ void store_half4(h16* hi, h16* lo, int64_t off, float4 o) {
+  uint2 ph, pl;
+  split_xh2(o.x, o.y, ph.x, pl.x);
+  split_xh2(o.z, o.w, ph.y, pl.y);
+  *reinterpret_cast<uint2*>(hi + off) = ph;
+  if (lo) *reinterpret_cast<uint2*>(lo + off) = pl;
+}
+
 // ---------------------------------------------------------------------------
 // layer norm / bias+residual+layer norm: one CTA per row, the row staged in
 // shared memory so the three sweeps of kernels.py:22-35 read HBM once.
@@ -20,7 +30,7 @@ __global__ void __launch_bounds__(256) layer_norm_kernel(
     const float* __restrict__ x, int64_t ldx, const float* __restrict__ bias,
     const float* __restrict__ res, int64_t ldr, const float* __restrict__ gamma,
     const float* __restrict__ beta, double eps, int d, float* __restrict__ out, int64_t ldo,
-    h16* __restrict__ out16, int64_t ldo16) {
+    h16* __restrict__ out16, h16* __restrict__ out16lo, int64_t ldo16) {
   pdl_enter();
   extern __shared__ float srow[];
   __shared__ double red[8];
@@ -44,7 +54,10 @@ __global__ void __launch_bounds__(256) layer_norm_kernel(
     float n = (float)(((double)srow[j] - mean) * inv);
     float o = fadd_rn(fmul_rn(n, gamma[j]), beta[j]);  // kernels.py:35
     if (out) out[row * ldo + j] = o;
-    if (out16) out16[row * ldo16 + j] = f2h(o);
+    if (out16) {
+      if (out16lo) split_xh(o, out16[row * ldo16 + j], out16lo[row * ldo16 + j]);
+      else out16[row * ldo16 + j] = f2h(o);
+    }
   }
 }
 
@@ -57,7 +70,7 @@ __global__ void __launch_bounds__(256) layer_norm_warp_kernel(
     const float* __restrict__ x, int64_t ldx, const float* __restrict__ bias,
     const float* __restrict__ res, int64_t ldr, const float* __restrict__ gamma,
     const float* __restrict__ beta, double eps, int64_t rows, int d, float* __restrict__ out,
-    int64_t ldo, h16* __restrict__ out16, int64_t ldo16) {
+    int64_t ldo, h16* __restrict__ out16, h16* __restrict__ out16lo, int64_t ldo16) {
   pdl_enter();
   const int lane = threadIdx.x & 31;
   const int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -105,11 +118,7 @@ __global__ void __launch_bounds__(256) layer_norm_warp_kernel(
       o.w = fadd_rn(fmul_rn((float)((u[i].w - mean) * inv), g.w), bb.w);
       if (out) *reinterpret_cast<float4*>(out + row * ldo + c) = o;
       if (out16) {
-        h16x2 lo = __floats2half2_rn(o.x, o.y), hi = __floats2half2_rn(o.z, o.w);
-        uint2 pk;
-        pk.x = *reinterpret_cast<uint32_t*>(&lo);
-        pk.y = *reinterpret_cast<uint32_t*>(&hi);
-        *reinterpret_cast<uint2*>(out16 + row * ldo16 + c) = pk;
+        store_half4(out16, out16lo, row * ldo16 + c, o);
       }
     }
   }
@@ -122,7 +131,7 @@ __global__ void __launch_bounds__(128) layer_norm_row128_kernel(
     const float* __restrict__ x, int64_t ldx, const float* __restrict__ bias,
     const float* __restrict__ res, int64_t ldr, const float* __restrict__ gamma,
     const float* __restrict__ beta, double eps, int d, float* __restrict__ out, int64_t ldo,
-    h16* __restrict__ out16, int64_t ldo16) {
+    h16* __restrict__ out16, h16* __restrict__ out16lo, int64_t ldo16) {
   pdl_enter();
   __shared__ double red[2][4];
   const int64_t row = blockIdx.x;
@@ -170,11 +179,7 @@ __global__ void __launch_bounds__(128) layer_norm_row128_kernel(
     o.w = fadd_rn(fmul_rn((float)((u[i].w - mean) * inv), g.w), bb.w);
     if (out) *reinterpret_cast<float4*>(out + row * ldo + c) = o;
     if (out16) {
-      h16x2 lo = __floats2half2_rn(o.x, o.y), hi = __floats2half2_rn(o.z, o.w);
-      uint2 pk;
-      pk.x = *reinterpret_cast<uint32_t*>(&lo);
-      pk.y = *reinterpret_cast<uint32_t*>(&hi);
-      *reinterpret_cast<uint2*>(out16 + row * ldo16 + c) = pk;
+      store_half4(out16, out16lo, row * ldo16 + c, o);
     }
   }
 }
@@ -188,7 +193,7 @@ __global__ void __launch_bounds__(128) layer_norm_slabs_row128_kernel(
     const float* __restrict__ x, int64_t ld, int64_t slab, const float* __restrict__ bias,
     const float* __restrict__ res, int64_t ldr, const float* __restrict__ gamma,
     const float* __restrict__ beta, double eps, int d, float* __restrict__ out, int64_t ldo,
-    h16* __restrict__ out16, int64_t ldo16) {
+    h16* __restrict__ out16, h16* __restrict__ out16lo, int64_t ldo16) {
   pdl_enter();
   __shared__ double red[2][4];
   const int64_t row = blockIdx.x;
@@ -248,11 +253,7 @@ __global__ void __launch_bounds__(128) layer_norm_slabs_row128_kernel(
     o.w = fadd_rn(fmul_rn((float)((u[i].w - mean) * inv), g.w), bb.w);
     if (out) *reinterpret_cast<float4*>(out + row * ldo + c) = o;
     if (out16) {
-      h16x2 lo = __floats2half2_rn(o.x, o.y), hi = __floats2half2_rn(o.z, o.w);
-      uint2 pk;
-      pk.x = *reinterpret_cast<uint32_t*>(&lo);
-      pk.y = *reinterpret_cast<uint32_t*>(&hi);
-      *reinterpret_cast<uint2*>(out16 + row * ldo16 + c) = pk;
+      store_half4(out16, out16lo, row * ldo16 + c, o);
     }
   }
 }
@@ -263,10 +264,11 @@ template <bool kBiasRes>
 static void launch_ln(const float* x, int64_t ldx, const float* bias, const float* res,
                       int64_t ldr, const float* gamma, const float* beta, double eps,
                       int64_t rows, int64_t d, float* out, int64_t ldo, h16* out16,
-                      int64_t ldo16, cudaStream_t s) {
+                      int64_t ldo16, cudaStream_t s, h16* out16lo = nullptr) {
   bool align_ok = ldx % 4 == 0 && aligned16(x) && aligned16(gamma) && aligned16(beta) &&
                   (!out || (ldo % 4 == 0 && aligned16(out))) &&
-                  (!out16 || (ldo16 % 4 == 0 && (reinterpret_cast<uintptr_t>(out16) & 7) == 0));
+                  (!out16 || (ldo16 % 4 == 0 && (reinterpret_cast<uintptr_t>(out16) & 7) == 0)) &&
+                  (!out16lo || (reinterpret_cast<uintptr_t>(out16lo) & 7) == 0);
   if (kBiasRes) align_ok = align_ok && ldr % 4 == 0 && aligned16(res) && aligned16(bias);
   const bool warp_ok = align_ok && d % 128 == 0 && d <= 128 * kMaxV;
   const bool row128 = align_ok && (d == 512 || d == 1024 || d == 2048) &&
@@ -275,7 +277,7 @@ static void launch_ln(const float* x, int64_t ldx, const float* bias, const floa
     // few rows (decoder): 128 threads per row keep enough loads in flight
 #define FQ_LN128(V)                                                                       \
   launch_kernel(layer_norm_row128_kernel<kBiasRes, V>, (unsigned)rows, 128, 0, s, 1u,                    \
-      x, ldx, bias, res, ldr, gamma, beta, eps, (int)d, out, ldo, out16, ldo16)
+      x, ldx, bias, res, ldr, gamma, beta, eps, (int)d, out, ldo, out16, out16lo, ldo16)
     if (d == 512) FQ_LN128(1);
     else if (d == 1024) FQ_LN128(2);
     else FQ_LN128(4);
@@ -283,11 +285,11 @@ static void launch_ln(const float* x, int64_t ldx, const float* bias, const floa
   } else if (warp_ok) {
     const int64_t threads = rows * 32;
     launch_kernel(layer_norm_warp_kernel<kBiasRes>, (unsigned)((threads + 255) / 256), 256, 0, s, 1u, 
-        x, ldx, bias, res, ldr, gamma, beta, eps, rows, (int)d, out, ldo, out16, ldo16);
+        x, ldx, bias, res, ldr, gamma, beta, eps, rows, (int)d, out, ldo, out16, out16lo, ldo16);
   } else {
     int threads = d >= 1024 ? 256 : 128;
     launch_kernel(layer_norm_kernel<kBiasRes>, (unsigned)rows, threads, d * sizeof(float), s, 1u, 
-        x, ldx, bias, res, ldr, gamma, beta, eps, (int)d, out, ldo, out16, ldo16);
+        x, ldx, bias, res, ldr, gamma, beta, eps, (int)d, out, ldo, out16, out16lo, ldo16);
   }
 }
 
@@ -468,26 +470,27 @@ int fq_bias_residual_layer_norm(const float* x, int64_t ldx, const float* bias,
   return launch_status("fq_bias_residual_layer_norm");
 }
 
-int fq_splitk_bias_residual_layer_norm(const float* slabs, int nslab, int64_t ld,
-                                       const float* bias, const float* residual, int64_t ldr,
-                                       const float* gamma, const float* beta, double eps,
-                                       int64_t rows, int64_t d, float* out, int64_t ldo,
-                                       void* out16, int64_t ldo16, fq_stream_t stream) {
+static int splitk_ln(const float* slabs, int nslab, int64_t ld, const float* bias,
+                     const float* residual, int64_t ldr, const float* gamma, const float* beta,
+                     double eps, int64_t rows, int64_t d, float* out, int64_t ldo, void* out16,
+                     void* out16lo, int64_t ldo16, fq_stream_t stream) {
   FQ_CHECK_ARG(slabs && bias && residual && gamma && beta && rows >= 0 && (out || out16) &&
                    (nslab == 2 || nslab == 4) && (d == 512 || d == 1024 || d == 2048) &&
                    ld >= d && ld % 4 == 0 && ldr % 4 == 0 && aligned16(slabs) &&
                    aligned16(bias) && aligned16(residual) && aligned16(gamma) &&
                    aligned16(beta) && (!out || (ldo % 4 == 0 && aligned16(out))) &&
-                   (!out16 || (ldo16 % 4 == 0 && (reinterpret_cast<uintptr_t>(out16) & 7) == 0)),
+                   (!out16 || (ldo16 % 4 == 0 && (reinterpret_cast<uintptr_t>(out16) & 7) == 0)) &&
+                   (!out16lo || (out16 && (reinterpret_cast<uintptr_t>(out16lo) & 7) == 0)),
                FQ_ERR_DIMENSION, "fq_splitk_bias_residual_layer_norm: bad args");
   FQ_CHECK_ARG(eps >= 0, FQ_ERR_DIMENSION, "eps must be non-negative");
   if (rows == 0) return FQ_OK;
   auto* o16 = reinterpret_cast<fq::h16*>(out16);
+  auto* o16lo = reinterpret_cast<fq::h16*>(out16lo);
   const int64_t slab = rows * ld;
   cudaStream_t s = as_stream(stream);
 #define FQ_LNS(V, NS)                                                                         \
   launch_kernel(layer_norm_slabs_row128_kernel<V, NS>, (unsigned)rows, 128, 0, s, 1u, slabs, ld, \
-                slab, bias, residual, ldr, gamma, beta, eps, (int)d, out, ldo, o16, ldo16)
+                slab, bias, residual, ldr, gamma, beta, eps, (int)d, out, ldo, o16, o16lo, ldo16)
   if (nslab == 4) {
     if (d == 512) FQ_LNS(1, 4);
     else if (d == 1024) FQ_LNS(2, 4);
@@ -499,6 +502,38 @@ int fq_splitk_bias_residual_layer_norm(const float* slabs, int nslab, int64_t ld
   }
 #undef FQ_LNS
   return launch_status("fq_splitk_bias_residual_layer_norm");
+}
+
+int fq_splitk_bias_residual_layer_norm(const float* slabs, int nslab, int64_t ld,
+                                       const float* bias, const float* residual, int64_t ldr,
+                                       const float* gamma, const float* beta, double eps,
+                                       int64_t rows, int64_t d, float* out, int64_t ldo,
+                                       void* out16, int64_t ldo16, fq_stream_t stream) {
+  return splitk_ln(slabs, nslab, ld, bias, residual, ldr, gamma, beta, eps, rows, d, out, ldo,
+                   out16, nullptr, ldo16, stream);
+}
+
+int fq_splitk_bias_residual_layer_norm_xh(const float* slabs, int nslab, int64_t ld,
+                                          const float* bias, const float* residual, int64_t ldr,
+                                          const float* gamma, const float* beta, double eps,
+                                          int64_t rows, int64_t d, float* out, int64_t ldo,
+                                          void* out16, void* out16_lo, int64_t ldo16,
+                                          fq_stream_t stream) {
+  return splitk_ln(slabs, nslab, ld, bias, residual, ldr, gamma, beta, eps, rows, d, out, ldo,
+                   out16, out16_lo, ldo16, stream);
+}
+
+int fq_layer_norm_xh(const float* x, int64_t ldx, const float* gamma, const float* beta,
+                     double eps, int64_t rows, int64_t d, float* out, int64_t ldo, void* out16,
+                     void* out16_lo, int64_t ldo16, fq_stream_t stream) {
+  FQ_CHECK_ARG(x && gamma && beta && rows >= 0 && d > 0 && d <= 12288 && (out || out16) &&
+                   (!out16_lo || out16),
+               FQ_ERR_DIMENSION, "fq_layer_norm_xh: bad args");
+  if (rows == 0) return FQ_OK;
+  launch_ln<false>(x, ldx, nullptr, nullptr, 0, gamma, beta, eps, rows, d, out, ldo,
+                   reinterpret_cast<fq::h16*>(out16), ldo16, as_stream(stream),
+                   reinterpret_cast<fq::h16*>(out16_lo));
+  return launch_status("fq_layer_norm_xh");
 }
 
 int fq_bias_residual_act(const float* x, int64_t ldx, const float* bias, const float* residual,

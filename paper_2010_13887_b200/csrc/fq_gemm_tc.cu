@@ -39,15 +39,27 @@ constexpr int kThreads = 192;
 // OP_X3 (exact fp32 mode, 3xTF32): 2 more warps split each staged fp32 tile
 // (8 warps in all: 320 threads would cap registers at 168, below the
 // epilogue's 128-float row accumulator + chunk registers)
-constexpr int OP_F16 = 0, OP_X3 = 1;
+// OP_X3H (exact fp32 mode, 3xFP16): operands arrive pre-split as fp16 pairs
+// x = hi + lo * 2^-11 (hi = fp16(x), lo = fp16((x - hi) * 2^11): 22
+// significant bits, the tf32 pair's precision at twice the kind::f16 MMA rate
+// and half its bytes) written by the producing kernels; no converter warps.
+constexpr int OP_F16 = 0, OP_X3 = 1, OP_X3H = 2;
 constexpr int kThreadsX3 = 256;
 constexpr int kConvThreads = kThreadsX3 - kThreads;
-// OP_X3: K blocks (of 32) per TMEM accumulation chunk, summed in registers
+// OP_X3 / OP_X3H: K blocks (of 32 / 64 elements) per TMEM accumulation chunk,
+// summed in registers: 128 K elements per chunk either way
 constexpr int X3_CH = 4;
 template <int OP>
-constexpr int threads_of() { return OP == OP_X3 ? kThreadsX3 : kThreads; }
+__host__ __device__ constexpr int threads_of() { return OP == OP_X3 ? kThreadsX3 : kThreads; }
 template <int OP>
-constexpr int kblock() { return OP == OP_X3 ? 32 : BK; }  // K elements per 128-byte row
+__host__ __device__ constexpr int kblock() { return OP == OP_X3 ? 32 : BK; }  // K elements per 128-byte row
+template <int OP>
+__host__ __device__ constexpr int xchunk() { return OP == OP_X3 ? X3_CH : X3_CH / 2; }
+template <int OP>
+__host__ __device__ constexpr bool split3() { return OP == OP_X3 || OP == OP_X3H; }
+// scale of the small-term accumulator (OP_X3H: lo carries 2^11)
+template <int OP>
+__host__ __device__ constexpr float small_scale() { return OP == OP_X3H ? 1.0f / 2048.0f : 1.0f; }
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -187,6 +199,20 @@ __device__ __forceinline__ void split_tf32_smem(uint8_t* buf, uint8_t* lo, int n
   }
 }
 
+// OP_X3H: the same three products on fp16 pairs, K = 16 per kind::f16 MMA:
+// big += a_hi.b_hi, small += a_hi.b_lo + a_lo.b_hi (lo scaled by 2^11).
+__device__ __forceinline__ void mma_xh_block(uint32_t big, uint32_t small, uint32_t a_hi,
+                                             uint32_t a_lo, uint32_t b_hi, uint32_t b_lo,
+                                             uint32_t idesc, bool first) {
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const uint32_t acc = (first && k == 0) ? 0u : 1u;
+    mma_f16(small, sw128_desc(a_hi + k * 32), sw128_desc(b_lo + k * 32), idesc, acc);
+    mma_f16(small, sw128_desc(a_lo + k * 32), sw128_desc(b_hi + k * 32), idesc, 1u);
+    mma_f16(big, sw128_desc(a_hi + k * 32), sw128_desc(b_hi + k * 32), idesc, acc);
+  }
+}
+
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile(
       "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
@@ -226,9 +252,10 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
-// OP_X3: add one TMEM chunk slot (hi.hi at tb, small terms at tb + bn) to the
-// thread's row accumulator: racc = racc + (big + small), RN adds in a fixed order.
-template <int BN>
+// OP_X3 / OP_X3H: add one TMEM chunk slot (hi.hi at tb, small terms at tb +
+// bn) to the thread's row accumulator: racc = racc + (big + small * SC), RN
+// adds in a fixed order (SC a power of two: exact).
+template <int BN, int OP>
 __device__ __forceinline__ void x3_add_chunk(float (&racc)[BN], uint32_t tb, bool first) {
 #pragma unroll
   for (int j = 0; j < BN / 16; ++j) {
@@ -237,7 +264,7 @@ __device__ __forceinline__ void x3_add_chunk(float (&racc)[BN], uint32_t tb, boo
     tmem_ld16(tb + BN + j * 16, vs);
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
-      const float t = fadd_rn(vb[i], vs[i]);
+      const float t = fadd_rn(vb[i], OP == OP_X3H ? vs[i] * small_scale<OP>() : vs[i]);
       racc[j * 16 + i] = first ? t : fadd_rn(racc[j * 16 + i], t);
     }
   }
@@ -362,17 +389,20 @@ __global__ void __launch_bounds__(threads_of<OP>(), 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tma_a,
                    const __grid_constant__ CUtensorMap tma_b, const Epi ep, int M, int N, int K,
                    int cm, int cn, const HarsEpi he, const __grid_constant__ CUtensorMap tma_c,
-                   const __grid_constant__ CUtensorMap tma_blo) {
+                   const __grid_constant__ CUtensorMap tma_blo,
+                   const __grid_constant__ CUtensorMap tma_alo) {
   static_assert(OP == OP_F16 || !HS, "the HARS epilogue is fp16-only");
   constexpr bool X3 = OP == OP_X3;
+  constexpr bool XH = OP == OP_X3H;
+  constexpr bool XS = split3<OP>();
   constexpr int KB = kblock<OP>();
   constexpr int A_BYTES = BM * 128;
   constexpr int B_BYTES = BN * 128;
-  constexpr int STAGE_BYTES = X3 ? 2 * (A_BYTES + B_BYTES) : A_BYTES + B_BYTES;
-  constexpr int B_OFF = X3 ? 2 * A_BYTES : A_BYTES;  // B (hi) inside a stage
+  constexpr int STAGE_BYTES = XS ? 2 * (A_BYTES + B_BYTES) : A_BYTES + B_BYTES;
+  constexpr int B_OFF = XS ? 2 * A_BYTES : A_BYTES;  // B (hi) inside a stage
   // two accumulator stages (OP_X3: two chunk slots x {hi.hi, small terms});
   // the allocation is a power of two >= 32 columns
-  constexpr int TCOLS = X3 ? 4 * BN : 2 * BN;
+  constexpr int TCOLS = XS ? 4 * BN : 2 * BN;
   static_assert(TCOLS <= 512, "TMEM holds 512 columns");
   constexpr uint32_t TMEM_COLS = TCOLS <= 32 ? 32 : TCOLS <= 64 ? 64 : TCOLS <= 128 ? 128
                                  : TCOLS <= 256 ? 256 : 512;
@@ -450,7 +480,7 @@ __global__ void __launch_bounds__(threads_of<OP>(), 1)
           uint8_t* sa = smem + kb * STAGE_BYTES;
           mbar_expect_tx(&full_bar[kb], tx_bytes);
           tma_load_2d(&tma_b, &full_bar[kb], sa + B_OFF, kb * KB, n0);
-          if (X3 && ep.b_presplit)
+          if ((X3 && ep.b_presplit) || XH)
             tma_load_2d(&tma_blo, &full_bar[kb], sa + B_OFF + B_BYTES, kb * KB, n0);
         }
       }
@@ -464,6 +494,7 @@ __global__ void __launch_bounds__(threads_of<OP>(), 1)
           uint8_t* sa = smem + s * STAGE_BYTES;
           if (it < npre) {  // B already in flight
             tma_load_2d(&tma_a, &full_bar[s], sa, kb * KB, m0);
+            if (XH) tma_load_2d(&tma_alo, &full_bar[s], sa + A_BYTES, kb * KB, m0);
             continue;
           }
           mbar_wait(&empty_bar[s], ph ^ 1);  // free in every CTA I multicast into
@@ -473,12 +504,13 @@ __global__ void __launch_bounds__(threads_of<OP>(), 1)
                            m0 + rx * a_rows, row_mask);
           else
             tma_load_2d(&tma_a, &full_bar[s], sa, kb * KB, m0);
+          if (XH) tma_load_2d(&tma_alo, &full_bar[s], sa + A_BYTES, kb * KB, m0);
           if (cm > 1)
             tma_load_2d_mc(&tma_b, &full_bar[s], sa + B_OFF + ry * b_rows * 128, kb * KB,
                            n0 + ry * b_rows, col_mask);
           else
             tma_load_2d(&tma_b, &full_bar[s], sa + B_OFF, kb * KB, n0);
-          if (X3 && ep.b_presplit)
+          if ((X3 && ep.b_presplit) || XH)
             tma_load_2d(&tma_blo, &full_bar[s], sa + B_OFF + B_BYTES, kb * KB, n0);
         }
       }
@@ -489,31 +521,37 @@ __global__ void __launch_bounds__(threads_of<OP>(), 1)
     if (lane == 0) {  // ---- MMA issuer ----
       constexpr uint32_t idesc = X3 ? idesc_tf32(BM, BN) : idesc_f16(BM, BN);
       int it = 0, local = 0;
-      if constexpr (X3) {  // chunks of X3_CH K blocks into ping-pong TMEM slots
+      if constexpr (XS) {  // chunks of xchunk K blocks into ping-pong TMEM slots
+        constexpr int CH = xchunk<OP>();
         int gc = 0;
         for (int g = cluster_id; g < ngroups; g += nclusters) {
-          for (int kb0 = 0; kb0 < num_kb; kb0 += X3_CH, ++gc) {
+          for (int kb0 = 0; kb0 < num_kb; kb0 += CH, ++gc) {
             const int slot = gc & 1;
             mbar_wait(&tempty_bar[slot], ((gc >> 1) & 1) ^ 1);  // epilogue read the slot
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             const uint32_t big = tmem + slot * 2 * BN;
-            const int kb1 = min(num_kb, kb0 + X3_CH);
+            const int kb1 = min(num_kb, kb0 + CH);
             for (int kb = kb0; kb < kb1; ++kb, ++it) {
               const int s = it % STAGES;
-              mbar_wait(&conv_bar[s], (it / STAGES) & 1);
+              if constexpr (X3) mbar_wait(&conv_bar[s], (it / STAGES) & 1);
+              else mbar_wait(&full_bar[s], (it / STAGES) & 1);
               if (it == 0) dbg_stamp(ep.dbg, 2);
               asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
               const uint32_t a_base = smem_u32(smem + s * STAGE_BYTES);
               const uint32_t b_base = a_base + B_OFF;
-              mma_x3_block(big, big + BN, a_base, a_base + A_BYTES, b_base, b_base + B_BYTES,
-                           idesc, kb == kb0);
+              if constexpr (X3)
+                mma_x3_block(big, big + BN, a_base, a_base + A_BYTES, b_base, b_base + B_BYTES,
+                             idesc, kb == kb0);
+              else
+                mma_xh_block(big, big + BN, a_base, a_base + A_BYTES, b_base, b_base + B_BYTES,
+                             idesc, kb == kb0);
               mma_commit(&empty_bar[s]);
             }
             mma_commit(&tfull_bar[slot]);
           }
         }
       }
-      for (int g = cluster_id; g < ngroups && !X3; g += nclusters, ++local) {
+      for (int g = cluster_id; g < ngroups && !XS; g += nclusters, ++local) {
         const int as = local & 1;
         mbar_wait(&tempty_bar[as], ((local >> 1) & 1) ^ 1);  // epilogue drained this stage
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -827,18 +865,18 @@ __global__ void __launch_bounds__(threads_of<OP>(), 1)
         }
         __syncwarp();  // staging free for the next chunk
       };
-      if constexpr (X3) {
+      if constexpr (XS) {
         // the tile's K chunks (X3_CH K blocks each, ping-pong TMEM slots): per
         // chunk the hi.hi and the small-term accumulators are read and added
         // to this thread's row in registers with IEEE round-to-nearest adds
         // (the tensor core's own long accumulation is not RN: this bounds it
         // to X3_CH * 32 K elements)
         float racc[BN];
-        for (int kb0 = 0; kb0 < num_kb; kb0 += X3_CH, ++gc) {
+        for (int kb0 = 0; kb0 < num_kb; kb0 += xchunk<OP>(), ++gc) {
           const int slot = gc & 1;
           mbar_wait(&tfull_bar[slot], (gc >> 1) & 1);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          x3_add_chunk<BN>(racc, tmem + slot * 2 * BN + ((uint32_t)(q * 32) << 16), kb0 == 0);
+          x3_add_chunk<BN, OP>(racc, tmem + slot * 2 * BN + ((uint32_t)(q * 32) << 16), kb0 == 0);
           asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
           __syncwarp();
           if (lane == 0) mbar_arrive(&tempty_bar[slot]);
@@ -928,16 +966,19 @@ __global__ void __launch_bounds__(threads_of<OP>(), 1)
                           const __grid_constant__ CUtensorMap tma_b, const Epi ep, int M, int N,
                           int K, int kb_per_split, const LnEpi ln, int nsplit,
                           const __grid_constant__ CUtensorMap tma_c,
-                          const __grid_constant__ CUtensorMap tma_blo) {
+                          const __grid_constant__ CUtensorMap tma_blo,
+                          const __grid_constant__ CUtensorMap tma_alo) {
   static_assert(OP == OP_F16 || !LNF, "the in-kernel LN is fp16-only");
   constexpr bool X3 = OP == OP_X3;
+  constexpr bool XH = OP == OP_X3H;
+  constexpr bool XS = split3<OP>();
   constexpr int KB = kblock<OP>();
   constexpr int A_BYTES = BM * 128;
   constexpr int B_BYTES = BN * 128;
-  constexpr int STAGE_BYTES = X3 ? 2 * (A_BYTES + B_BYTES) : A_BYTES + B_BYTES;
-  constexpr int B_OFF = X3 ? 2 * A_BYTES : A_BYTES;
+  constexpr int STAGE_BYTES = XS ? 2 * (A_BYTES + B_BYTES) : A_BYTES + B_BYTES;
+  constexpr int B_OFF = XS ? 2 * A_BYTES : A_BYTES;
   // OP_X3: two chunk slots x {hi.hi, small terms} (see tc_gemm_kernel)
-  constexpr uint32_t TMEM_COLS = X3 ? 4 * BN : (BN < 32 ? 32 : BN);
+  constexpr uint32_t TMEM_COLS = XS ? 4 * BN : (BN < 32 ? 32 : BN);
   static_assert(TMEM_COLS <= 512, "TMEM holds 512 columns");
   constexpr int PLD = BN + 4;  // padded partial row (floats): conflict-free v4 rows
   static_assert(BM * PLD * 4 <= STAGES * STAGE_BYTES, "partial tile must fit the ring");
@@ -998,7 +1039,7 @@ __global__ void __launch_bounds__(threads_of<OP>(), 1)
         uint8_t* sa = smem + it * STAGE_BYTES;
         mbar_expect_tx(&full_bar[it], tx_bytes);
         tma_load_2d(&tma_b, &full_bar[it], sa + B_OFF, (kb0 + it) * KB, n0);
-        if (X3 && ep.b_presplit)
+        if ((X3 && ep.b_presplit) || XH)
           tma_load_2d(&tma_blo, &full_bar[it], sa + B_OFF + B_BYTES, (kb0 + it) * KB, n0);
       }
       pdl_wait();
@@ -1007,34 +1048,42 @@ __global__ void __launch_bounds__(threads_of<OP>(), 1)
         uint8_t* sa = smem + s * STAGE_BYTES;
         if (it < npre) {
           tma_load_2d(&tma_a, &full_bar[s], sa, kb * KB, m0);
+          if (XH) tma_load_2d(&tma_alo, &full_bar[s], sa + A_BYTES, kb * KB, m0);
           continue;
         }
         mbar_wait(&empty_bar[s], ((it / STAGES) & 1) ^ 1);
         mbar_expect_tx(&full_bar[s], tx_bytes);
         tma_load_2d(&tma_a, &full_bar[s], sa, kb * KB, m0);
+        if (XH) tma_load_2d(&tma_alo, &full_bar[s], sa + A_BYTES, kb * KB, m0);
         tma_load_2d(&tma_b, &full_bar[s], sa + B_OFF, kb * KB, n0);
-        if (X3 && ep.b_presplit)
+        if ((X3 && ep.b_presplit) || XH)
           tma_load_2d(&tma_blo, &full_bar[s], sa + B_OFF + B_BYTES, kb * KB, n0);
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {  // ---- MMA issuer ----
       constexpr uint32_t idesc = X3 ? idesc_tf32(BM, BN) : idesc_f16(BM, BN);
-      if constexpr (X3) {  // chunks of X3_CH K blocks into ping-pong TMEM slots
+      if constexpr (XS) {  // chunks of xchunk K blocks into ping-pong TMEM slots
+        constexpr int CH = xchunk<OP>();
         int it = 0, gc = 0;
-        for (int c0 = kb0; c0 < kb1; c0 += X3_CH, ++gc) {
+        for (int c0 = kb0; c0 < kb1; c0 += CH, ++gc) {
           const int slot = gc & 1;
           mbar_wait(&xempty_bar[slot], ((gc >> 1) & 1) ^ 1);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           const uint32_t big = tmem + slot * 2 * BN;
-          for (int kb = c0; kb < min(kb1, c0 + X3_CH); ++kb, ++it) {
+          for (int kb = c0; kb < min(kb1, c0 + CH); ++kb, ++it) {
             const int s = it % STAGES;
-            mbar_wait(&conv_bar[s], (it / STAGES) & 1);
+            if constexpr (X3) mbar_wait(&conv_bar[s], (it / STAGES) & 1);
+            else mbar_wait(&full_bar[s], (it / STAGES) & 1);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             const uint32_t a_base = smem_u32(smem + s * STAGE_BYTES);
             const uint32_t b_base = a_base + B_OFF;
-            mma_x3_block(big, big + BN, a_base, a_base + A_BYTES, b_base, b_base + B_BYTES,
-                         idesc, kb == c0);
+            if constexpr (X3)
+              mma_x3_block(big, big + BN, a_base, a_base + A_BYTES, b_base, b_base + B_BYTES,
+                           idesc, kb == c0);
+            else
+              mma_xh_block(big, big + BN, a_base, a_base + A_BYTES, b_base, b_base + B_BYTES,
+                           idesc, kb == c0);
             mma_commit(&empty_bar[s]);
           }
           mma_commit(&xfull_bar[slot]);
@@ -1072,16 +1121,16 @@ __global__ void __launch_bounds__(threads_of<OP>(), 1)
     pdl_wait();
     const int q = warp & 3;
     // OP_X3: the K slice's chunks summed in registers (RN adds, fixed order)
-    float racc[X3 ? BN : 1];
-    if constexpr (X3) {
+    float racc[XS ? BN : 1];
+    if constexpr (XS) {
 #pragma unroll
       for (int i = 0; i < BN; ++i) racc[i] = 0.0f;
       int gc = 0;
-      for (int c0 = kb0; c0 < kb1; c0 += X3_CH, ++gc) {
+      for (int c0 = kb0; c0 < kb1; c0 += xchunk<OP>(), ++gc) {
         const int slot = gc & 1;
         mbar_wait(&xfull_bar[slot], (gc >> 1) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        x3_add_chunk<X3 ? BN : 1>(racc, tmem + slot * 2 * BN + ((uint32_t)(q * 32) << 16),
+        x3_add_chunk<XS ? BN : 1, OP>(racc, tmem + slot * 2 * BN + ((uint32_t)(q * 32) << 16),
                                   c0 == kb0);
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
         __syncwarp();
@@ -1092,9 +1141,9 @@ __global__ void __launch_bounds__(threads_of<OP>(), 1)
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     }
     auto acc_chunk = [&](float (&v)[32], const int cc) {
-      if constexpr (X3) {
+      if constexpr (XS) {
 #pragma unroll
-        for (int i = 0; i < 32; ++i) v[i] = racc[(cc + i) % (X3 ? BN : 1)];
+        for (int i = 0; i < 32; ++i) v[i] = racc[(cc + i) % (XS ? BN : 1)];
       } else {
         tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + cc, v);
       }
@@ -1351,7 +1400,7 @@ __global__ void __launch_bounds__(threads_of<OP>(), 1)
 
 template <int BN, int OP>
 constexpr int stage_bytes() {
-  return (OP == OP_X3 ? 2 : 1) * (BM * 128 + BN * 128);
+  return (split3<OP>() ? 2 : 1) * (BM * 128 + BN * 128);
 }
 
 template <int BN, int STAGES, int OP = OP_F16>
@@ -1475,17 +1524,20 @@ static int num_sms() {
 template <int BN, int STAGES, bool HS = false, int OP = OP_F16>
 static int launch(const void* a, int64_t lda, const void* b, int64_t ldb, const Epi& ep,
                   int64_t M, int64_t N, int64_t K, int cm, int cn, cudaStream_t s,
-                  const HarsEpi& he = HarsEpi{}, const void* b_lo = nullptr) {
-  constexpr bool X3 = OP == OP_X3;
-  CUtensorMap ma, mb, mc, mblo;
+                  const HarsEpi& he = HarsEpi{}, const void* b_lo = nullptr,
+                  const void* a_lo = nullptr) {
+  constexpr bool X3 = OP == OP_X3, XH = OP == OP_X3H;
+  CUtensorMap ma, mb, mc, mblo, malo;
   int rc;
   if ((rc = make_map(&ma, a, M, K, lda, BM / cn, X3)) != FQ_OK) return rc;
   if ((rc = make_map(&mb, b, N, K, ldb, BN / cm, X3)) != FQ_OK) return rc;
   Epi e2 = ep;
   e2.tstore = 0;
-  e2.b_presplit = X3 && b_lo != nullptr;
+  e2.b_presplit = (X3 || XH) && b_lo != nullptr;
   mblo = mb;
-  if (e2.b_presplit && (rc = make_map(&mblo, b_lo, N, K, ldb, BN / cm, true)) != FQ_OK) return rc;
+  malo = ma;
+  if (e2.b_presplit && (rc = make_map(&mblo, b_lo, N, K, ldb, BN / cm, X3)) != FQ_OK) return rc;
+  if (XH && (rc = make_map(&malo, a_lo, M, K, lda, BM / cn, false)) != FQ_OK) return rc;
   mc = ma;
   if (!HS && ep.c && !ep.accumulate && !ep.res && N % 32 == 0 && tma_store_enabled() &&
       ((uintptr_t)ep.c & 15) == 0 && (ep.ldc * (ep.c_f16 ? 2 : 4)) % 16 == 0 &&
@@ -1498,7 +1550,7 @@ static int launch(const void* a, int64_t lda, const void* b, int64_t ldb, const 
   cudaError_t e = launch_kernel(tc_gemm_kernel<BN, STAGES, HS, OP>,
                                 dim3((unsigned)(clusters * csize)), dim3(threads_of<OP>()),
                                 smem_bytes<BN, STAGES, HS, OP>(), s, (unsigned)csize, ma, mb, e2,
-                                (int)M, (int)N, (int)K, cm, cn, he, mc, mblo);
+                                (int)M, (int)N, (int)K, cm, cn, he, mc, mblo, malo);
   if (e != cudaSuccess) {
     set_error("fq_gemm(tcgen05): launch failed: %s", cudaGetErrorString(e));
     return FQ_ERR_CUDA;
@@ -1509,17 +1561,20 @@ static int launch(const void* a, int64_t lda, const void* b, int64_t ldb, const 
 template <int BN, int STAGES, bool LNF = false, bool SLAB = false, int OP = OP_F16>
 static int launch_splitk(const void* a, int64_t lda, const void* b, int64_t ldb, const Epi& ep,
                          int64_t M, int64_t N, int64_t K, int S, cudaStream_t s,
-                         const LnEpi& ln = LnEpi{}, const void* b_lo = nullptr) {
-  constexpr bool X3 = OP == OP_X3;
-  CUtensorMap ma, mb, mc, mblo;
+                         const LnEpi& ln = LnEpi{}, const void* b_lo = nullptr,
+                         const void* a_lo = nullptr) {
+  constexpr bool X3 = OP == OP_X3, XH = OP == OP_X3H;
+  CUtensorMap ma, mb, mc, mblo, malo;
   int rc;
   if ((rc = make_map(&ma, a, M, K, lda, BM, X3)) != FQ_OK) return rc;
   if ((rc = make_map(&mb, b, N, K, ldb, BN, X3)) != FQ_OK) return rc;
   Epi e2 = ep;
   e2.tstore = 0;
-  e2.b_presplit = X3 && b_lo != nullptr;
+  e2.b_presplit = (X3 || XH) && b_lo != nullptr;
   mblo = mb;
-  if (e2.b_presplit && (rc = make_map(&mblo, b_lo, N, K, ldb, BN, true)) != FQ_OK) return rc;
+  malo = ma;
+  if (e2.b_presplit && (rc = make_map(&mblo, b_lo, N, K, ldb, BN, X3)) != FQ_OK) return rc;
+  if (XH && (rc = make_map(&malo, a_lo, M, K, lda, BM, false)) != FQ_OK) return rc;
   mc = ma;
   if (SLAB && M % 32 == 0 && N % 32 == 0 && tma_store_enabled() && ((uintptr_t)ep.c & 15) == 0 &&
       (ep.ldc * 4) % 16 == 0 && make_map_c(&mc, ep.c, S * M, N, ep.ldc, false) == FQ_OK)
@@ -1530,7 +1585,7 @@ static int launch_splitk(const void* a, int64_t lda, const void* b, int64_t ldb,
   cudaError_t e = launch_kernel(tc_gemm_splitk_kernel<BN, STAGES, LNF, SLAB, OP>,
                                 dim3((unsigned)(tiles * S)), dim3(threads_of<OP>()),
                                 smem_bytes_splitk<BN, STAGES, OP>(), s, SLAB ? 1u : (unsigned)S, ma,
-                                mb, e2, (int)M, (int)N, (int)K, kbs, ln, S, mc, mblo);
+                                mb, e2, (int)M, (int)N, (int)K, kbs, ln, S, mc, mblo, malo);
   if (e != cudaSuccess) {
     set_error("fq_gemm(tcgen05 split-K): launch failed: %s", cudaGetErrorString(e));
     return FQ_ERR_CUDA;
@@ -1567,7 +1622,10 @@ int gemm_tc_prepare() {
       tc::prep_splitk<128, 6, true>() || tc::prep_splitk<128, 6, false, true>() ||
       tc::prep<128, 3, false, tc::OP_X3>() || tc::prep<64, 4, false, tc::OP_X3>() ||
       tc::prep_splitk<128, 3, false, false, tc::OP_X3>() ||
-      tc::prep_splitk<128, 3, false, true, tc::OP_X3>()) {
+      tc::prep_splitk<128, 3, false, true, tc::OP_X3>() ||
+      tc::prep<128, 3, false, tc::OP_X3H>() || tc::prep<64, 4, false, tc::OP_X3H>() ||
+      tc::prep_splitk<128, 3, false, false, tc::OP_X3H>() ||
+      tc::prep_splitk<128, 3, false, true, tc::OP_X3H>()) {
     set_error("fq_prepare: tcgen05 GEMM smem opt-in failed");
     return FQ_ERR_CUDA;
   }
@@ -1745,6 +1803,82 @@ extern "C" int fq_gemm_f32x3_ln(const float* a, int64_t lda, const float* b, con
                       as_stream(stream));
   if (rc != FQ_OK) return rc;
   return fq_layer_norm(out, ldo, gamma, beta, eps, M, N, out, ldo, nullptr, 0, stream);
+}
+
+// ---------------------------------------------------------------------------
+// Exact fp32 mode, 3xFP16 (OP_X3H): operands as fp16 pairs (split_xh), same
+// M-independent plan as 3xTF32 (K slices of 1024 for N <= 1024 and K >= 2048
+// ... in units of 64-element K blocks), 128-element accumulation chunks.
+static int check_xh(const void* a, const void* a_lo, int64_t lda, const void* b,
+                    const void* b_lo, int64_t ldb, int64_t M, int64_t N, int64_t K) {
+  FQ_CHECK_ARG(a && a_lo && b && b_lo, FQ_ERR_DIMENSION, "3xFP16 GEMM: null operand");
+  FQ_CHECK_ARG(lda % 8 == 0 && ldb % 8 == 0 &&
+                   (((uintptr_t)a | (uintptr_t)a_lo | (uintptr_t)b | (uintptr_t)b_lo) & 15) == 0,
+               FQ_ERR_DIMENSION, "3xFP16 GEMM: operands need 16-byte aligned rows (ld %% 8 == 0)");
+  FQ_CHECK_ARG(M < (1LL << 31) && N < (1LL << 31) && K < (1LL << 31), FQ_ERR_DIMENSION,
+               "3xFP16 GEMM: dimension too large");
+  return FQ_OK;
+}
+
+int launch_xh_gemm(const void* a, const void* a_lo, int64_t lda, const void* b,
+                   const void* b_lo, int64_t ldb, float* c, int64_t ldc, int64_t M, int64_t N,
+                   int64_t K, int accumulate, const float* bias, const float* res, int64_t ldr,
+                   int act, cudaStream_t s) {
+  int rc = check_xh(a, a_lo, lda, b, b_lo, ldb, M, N, K);
+  if (rc != FQ_OK) return rc;
+  tc::Epi ep{c, ldc, 0, accumulate, bias, res, ldr, act, g_gemm_dbg};
+  const X3Plan p = plan_x3(N, K);
+  if (p.split > 1)
+    return tc::launch_splitk<128, 3, false, false, tc::OP_X3H>(a, lda, b, ldb, ep, M, N, K,
+                                                               p.split, s, tc::LnEpi{}, b_lo, a_lo);
+  if (p.bn == 64)
+    return tc::launch<64, 4, false, tc::OP_X3H>(a, lda, b, ldb, ep, M, N, K, 1, 1, s,
+                                                tc::HarsEpi{}, b_lo, a_lo);
+  return tc::launch<128, 3, false, tc::OP_X3H>(a, lda, b, ldb, ep, M, N, K, 1, 1, s,
+                                               tc::HarsEpi{}, b_lo, a_lo);
+}
+
+extern "C" int fq_gemm_x3h(const void* a, const void* a_lo, int64_t lda, const void* b,
+                           const void* b_lo, int64_t ldb, float* c, int64_t ldc, int64_t M,
+                           int64_t N, int64_t K, int accumulate, const float* bias,
+                           const float* residual, int64_t ldr, int act, fq_stream_t stream) {
+  FQ_CHECK_ARG(c && M >= 0 && N >= 0 && K >= 1, FQ_ERR_DIMENSION,
+               "fq_gemm_x3h: bad shape M=%lld N=%lld K=%lld", (long long)M, (long long)N,
+               (long long)K);
+  FQ_CHECK_ARG(act >= 0 && act <= 2, FQ_ERR_PARAMETER, "fq_gemm_x3h: unknown activation");
+  if (M == 0 || N == 0) return FQ_OK;
+  return launch_xh_gemm(a, a_lo, lda, b, b_lo, ldb, c, ldc, M, N, K, accumulate, bias, residual,
+                        ldr, act, as_stream(stream));
+}
+
+extern "C" int fq_gemm_x3h_ln(const void* a, const void* a_lo, int64_t lda, const void* b,
+                              const void* b_lo, int64_t ldb, const float* bias, const float* res,
+                              int64_t ldr, const float* gamma, const float* beta, double eps,
+                              float* out, int64_t ldo, void* out16, void* out16_lo,
+                              int64_t ldo16, void* ws, int64_t ws_bytes, int64_t M, int64_t N,
+                              int64_t K, fq_stream_t stream) {
+  FQ_CHECK_ARG(bias && res && gamma && beta && out && M > 0 && N > 0 && K > 0,
+               FQ_ERR_DIMENSION, "fq_gemm_x3h_ln: bad args");
+  int rc = check_xh(a, a_lo, lda, b, b_lo, ldb, M, N, K);
+  if (rc != FQ_OK) return rc;
+  const X3Plan p = plan_x3(N, K);
+  const int64_t slab_need = (int64_t)p.split * M * N * (int64_t)sizeof(float);
+  if (p.split > 1 && ws && ws_bytes >= slab_need && ((uintptr_t)ws & 15) == 0 &&
+      (N == 512 || N == 1024)) {
+    tc::Epi ep{ws, N, 0, 0, nullptr, nullptr, 0, 0, g_gemm_dbg};
+    rc = tc::launch_splitk<128, 3, false, true, tc::OP_X3H>(a, lda, b, ldb, ep, M, N, K, p.split,
+                                                            as_stream(stream), tc::LnEpi{}, b_lo,
+                                                            a_lo);
+    if (rc != FQ_OK) return rc;
+    return fq_splitk_bias_residual_layer_norm_xh(reinterpret_cast<const float*>(ws), p.split, N,
+                                                 bias, res, ldr, gamma, beta, eps, M, N, out,
+                                                 ldo, out16, out16_lo, ldo16, stream);
+  }
+  rc = launch_xh_gemm(a, a_lo, lda, b, b_lo, ldb, out, ldo, M, N, K, 0, bias, res, ldr, 0,
+                      as_stream(stream));
+  if (rc != FQ_OK) return rc;
+  return fq_layer_norm_xh(out, ldo, gamma, beta, eps, M, N, out, ldo, out16, out16_lo, ldo16,
+                          stream);
 }
 
 // Logits GEMM with the HARS statistics epilogue (see HarsEpi): x16 [rows, d]

@@ -271,7 +271,7 @@ class Session:
                           self.dw.embedding.data_ptr(), self.config.d_model,
                           float(np.float32(math.sqrt(self.config.d_model))),
                           self.dw.positions.data_ptr(), step.x.data_ptr(),
-                          _abi.ptr(step.x16), stream)
+                          _abi.ptr(step.x16) if self.dw.half else None, stream)
                 self.counters.count_fused("retrieve", nr * V * 4)
                 return
             _abi.call("fq_hars_groups", st.c, nb, K, V, exhaustive, hk.data_ptr(), stream)

@@ -35,7 +35,8 @@ from . import _abi
 from .errors import CapacityError, ConsistencyError, DimensionError, FullMaskError, InputError
 from .memory_plan import Arena, IntermediateSpec
 from .ops import attention_scale
-from .tensor import OpCounters, Timers, as_device, gemm, gemm_x3, global_counters
+from .tensor import (OpCounters, Timers, as_device, gemm, gemm_x3, gemm_xh, global_counters,
+                     split_pair)
 
 F32 = np.float32
 I64 = np.int64
@@ -287,6 +288,48 @@ class X3Weight:
         return cls(hi, lo)
 
 
+class XHWeight:
+    """An exact-mode GEMM weight for the 3xFP16 tcgen05 GEMM (fq_gemm_x3h): the
+    fp16 pair hi + lo * 2^-11 (22 significant bits) of the reference's [in,
+    out] matrix, stored K-major [out, in] (fq_split_f16, once at load)."""
+
+    __slots__ = ("hi", "lo")
+
+    def __init__(self, hi: torch.Tensor, lo: torch.Tensor):
+        self.hi, self.lo = hi, lo
+
+    @property
+    def shape(self):
+        return tuple(self.hi.shape)
+
+    @classmethod
+    def from_kn(cls, t: torch.Tensor, transpose: bool = True) -> "XHWeight":
+        """Split a device fp32 [K, N] matrix (``transpose``) or [N, K] one."""
+        rows, cols = t.shape
+        shape = (cols, rows) if transpose else (rows, cols)
+        hi = torch.empty(shape, dtype=torch.float16, device=t.device)
+        lo = torch.empty_like(hi)
+        _abi.call("fq_split_f16", t.data_ptr(), t.stride(0), rows, cols, int(transpose),
+                  hi.data_ptr(), lo.data_ptr(), shape[1], _abi.stream_handle())
+        return cls(hi, lo)
+
+
+def half_operand(bufs, name: str, shape, half: bool):
+    """The fp16 GEMM operand buffer of an fp32 activation: its fp16 copy in
+    the fp16 mode, its exact-mode (hi, lo) pair in fp32 mode."""
+    if half:
+        return bufs.get(name, shape, torch.float16)
+    t = bufs.get(name, (2,) + tuple(shape), torch.float16)
+    return (t[0], t[1])
+
+
+def fill_pair(a32, pair):
+    """Exact mode: write the fp16 pair of ``a32`` (for producers that do not
+    emit it themselves)."""
+    if isinstance(pair, tuple):
+        split_pair(a32, pair)
+
+
 class DeviceWeights:
     """Weights uploaded once for one precision (cached per ModelWeights)."""
 
@@ -316,7 +359,7 @@ class DeviceWeights:
         def mat(a):  # GEMM B operand
             t = f32(a)
             if not self.half:
-                return X3Weight.from_kn(t)                 # [N, K] tf32 hi + lo
+                return XHWeight.from_kn(t)                 # [N, K] fp16 hi + lo pair
             out = torch.empty((a.shape[1], a.shape[0]), dtype=torch.float16, device=dev)
             _abi.call("fq_cast_f16", t.data_ptr(), a.shape[0], a.shape[1], 1, out.data_ptr(),
                       _abi.stream_handle())
@@ -328,7 +371,7 @@ class DeviceWeights:
             self.out_proj = f32(out_m).to(torch.float16)   # [V, d] already K-major
         else:
             self.out_proj = self.embedding if config.tie_output else f32(out_m)
-            self.out_x3 = X3Weight.from_kn(self.out_proj, transpose=False)  # logits GEMM
+            self.out_xh = XHWeight.from_kn(self.out_proj, transpose=False)  # logits GEMM
         self.positions = f32(sinusoidal_positions(config.max_seq_len, config.d_model))
         self.enc = []
         for lw in weights.encoder:
@@ -391,6 +434,9 @@ def _lin(dw: DeviceWeights, a32, a16, w, out, *, bias=None, residual=None, act="
     if dw.half:
         gemm(a16, w, out, transpose_b=True, bias=bias, residual=residual, activation=act,
              counters=counters, timers=timers)
+    elif isinstance(w, XHWeight):  # exact mode: a16 is the activation's fp16 pair
+        gemm_xh(a16, w, out, bias=bias, residual=residual, activation=act, counters=counters,
+                timers=timers)
     else:
         gemm_x3(a32, w, out, bias=bias, residual=residual, activation=act, counters=counters,
                 timers=timers)
@@ -399,7 +445,14 @@ def _lin(dw: DeviceWeights, a32, a16, w, out, *, bias=None, residual=None, act="
 def _ln(x, g, b, eps, out, out16, residual=None, bias=None, counters=None):
     stream = _abi.stream_handle()
     rows, d = x.shape
-    if residual is None:
+    if isinstance(out16, tuple):  # exact mode: the output's fp16 pair for the next GEMM
+        if residual is not None:
+            raise InputError("bias+residual LN with an fp16 pair output is not fused")
+        hi, lo = out16
+        _abi.call("fq_layer_norm_xh", x.data_ptr(), x.stride(0), g.data_ptr(), b.data_ptr(), eps,
+                  rows, d, _abi.ptr(out), out.stride(0) if out is not None else 0, hi.data_ptr(),
+                  lo.data_ptr(), hi.stride(0), stream)
+    elif residual is None:
         _abi.call("fq_layer_norm", x.data_ptr(), x.stride(0), g.data_ptr(), b.data_ptr(), eps, rows,
                   d, _abi.ptr(out), out.stride(0) if out is not None else 0, _abi.ptr(out16),
                   out16.stride(0) if out16 is not None else 0, stream)
@@ -424,6 +477,21 @@ def _lin_ln(dw: DeviceWeights, a32, a16, w, bias, residual, g, b, eps, out, out1
                   b.data_ptr(), eps, out.data_ptr(), out.stride(0), _abi.ptr(out16),
                   out16.stride(0) if out16 is not None else 0, ws.data_ptr(),
                   ws.numel() * ws.element_size(), M, N, K, _abi.stream_handle())
+        (counters or global_counters()).count_fused("layer_norm", M * N * 8)
+        return
+    if not dw.half and ws is not None and isinstance(w, XHWeight):
+        # exact mode: 3xFP16 K-slice slabs + the LN kernel reducing them
+        hi, lo = a16
+        M, K = hi.shape
+        N = w.shape[0]
+        ohi, olo = out16 if out16 is not None else (None, None)
+        _abi.call("fq_gemm_x3h_ln", hi.data_ptr(), lo.data_ptr(), hi.stride(0), w.hi.data_ptr(),
+                  w.lo.data_ptr(), w.hi.stride(0), bias.data_ptr(), residual.data_ptr(),
+                  residual.stride(0), g.data_ptr(), b.data_ptr(), eps, out.data_ptr(),
+                  out.stride(0), _abi.ptr(ohi), _abi.ptr(olo),
+                  ohi.stride(0) if ohi is not None else 0, ws.data_ptr(),
+                  ws.numel() * ws.element_size(), M, N, K, _abi.stream_handle())
+        (counters or global_counters()).count_gemm(hi.numel() * 4 + N * K * 4 + M * N * 4)
         (counters or global_counters()).count_fused("layer_norm", M * N * 8)
         return
     if not dw.half and ws is not None:  # exact mode: 3xTF32 K-slice slabs + the reducing LN
@@ -482,13 +550,15 @@ def encoder_layer_forward(x, layer, config: ModelConfig, mask=None, batch: int =
         layer = DeviceWeights(cfg1, tmp, precision).enc[0]
         dw_half = precision == "fp16"
     else:
-        dw_half = not isinstance(layer["w_qkv"], X3Weight)
+        dw_half = not isinstance(layer["w_qkv"], (X3Weight, XHWeight))
     bufs = buffers if buffers is not None else HeapBuffers()
     ctr = counters or global_counters()
     h, hd, ff = config.num_heads, config.head_dim, config.d_ff
     act16 = torch.float16 if dw_half else torch.float32
     if dw_half and x16 is None:
         x16 = X.to(torch.float16)
+    if not dw_half and x16 is None:  # exact mode: the input's fp16 pair
+        x16 = split_pair(X)
     stream = _abi.stream_handle()
 
     class _P:  # precision shim for _lin
@@ -501,20 +571,28 @@ def encoder_layer_forward(x, layer, config: ModelConfig, mask=None, batch: int =
               attention_scale(hd), _abi.ptr(mask), None if dw_half else ctx.data_ptr(),
               ctx.data_ptr() if dw_half else None, d, 0 if dw_half else 1, _abi.ptr(bad), stream)
     ctr.count_fused("attention_scale_mask_softmax", n * d * 16)
+    ctx16 = ctx
+    if not dw_half:
+        ctx16 = half_operand(bufs, f"{prefix}.ctx16", (n, d), False)
+        fill_pair(ctx, ctx16)
     res1 = bufs.get(f"{prefix}.res1", (n, d))
-    _lin(_P, ctx, ctx, layer["w_out"], res1, bias=layer["b_out"], residual=X, counters=ctr,
+    _lin(_P, ctx, ctx16, layer["w_out"], res1, bias=layer["b_out"], residual=X, counters=ctr,
          timers=timers)
     norm1 = bufs.get(f"{prefix}.norm1", (n, d))
-    norm1_16 = bufs.get(f"{prefix}.norm1_16", (n, d), torch.float16) if dw_half else None
+    norm1_16 = half_operand(bufs, f"{prefix}.norm1_16", (n, d), dw_half)
     _ln(res1, layer["ln1_g"], layer["ln1_b"], config.ln_eps, norm1, norm1_16, counters=ctr)
     ffn_h = bufs.get(f"{prefix}.ffn_h", (n, ff), act16)
     _lin(_P, norm1, norm1_16, layer["w_ff1"], ffn_h, bias=layer["b_ff1"], act=config.activation,
          counters=ctr, timers=timers)
+    ffn_h16 = ffn_h
+    if not dw_half:
+        ffn_h16 = half_operand(bufs, f"{prefix}.ffn_h16", (n, ff), False)
+        fill_pair(ffn_h, ffn_h16)
     u = bufs.get(f"{prefix}.ffn_out", (n, d))
-    _lin(_P, ffn_h, ffn_h, layer["w_ff2"], u, bias=layer["b_ff2"], residual=norm1, counters=ctr,
+    _lin(_P, ffn_h, ffn_h16, layer["w_ff2"], u, bias=layer["b_ff2"], residual=norm1, counters=ctr,
          timers=timers)
     out = bufs.get(f"{prefix}.out", (n, d))
-    out16 = bufs.get(f"{prefix}.out16", (n, d), torch.float16) if dw_half else None
+    out16 = half_operand(bufs, f"{prefix}.out16", (n, d), dw_half)
     _ln(u, layer["ln2_g"], layer["ln2_b"], config.ln_eps, out, out16, counters=ctr)
     return out, out16
 
@@ -547,11 +625,12 @@ def encode(tokens, weights, config: ModelConfig, lengths=None, *, engine: str = 
         mask = bufs.get("enc.mask", (batch, seq))
         mask.copy_(torch.from_numpy(lengths_mask(lengths, seq)))
     x = bufs.get("enc.x", (n, d))
-    x16 = bufs.get("enc.x16", (n, d), torch.float16) if dw.half else None
+    x16 = half_operand(bufs, "enc.x16", (n, d), dw.half)
     pos = as_device(positions, torch.float32) if positions is not None else dw.positions
     _abi.call("fq_embed_scale_pos", tok.data_ptr(), n, dw.embedding.data_ptr(), d,
               float(np.float32(math.sqrt(d))), pos.data_ptr(), 0, None, seq, x.data_ptr(),
-              _abi.ptr(x16), _abi.stream_handle())
+              _abi.ptr(x16) if dw.half else None, _abi.stream_handle())
+    fill_pair(x, x16)
     ctr.count_fused("embed_scale_pos", n * d * 8)
     bad = bufs.get("enc.bad", (1,), torch.int32)
     bad.zero_()
@@ -645,6 +724,8 @@ def build_cross_kv(memory, weights, config: ModelConfig, batch: int, seq: int, *
     packed = bufs.get("dec.cross_kv", (n, 2 * L * d), dw.act_dtype)
     if dw.half and memory16 is None:
         memory16 = M.to(torch.float16)
+    if not dw.half and memory16 is None:
+        memory16 = split_pair(M)
     _lin(dw, M, memory16, dw.w_ckv, packed, bias=dw.b_ckv, counters=counters, timers=timers)
     return packed
 
@@ -679,18 +760,23 @@ class DecoderStep:
         a16 = dw.act_dtype
         self.tokens = b.get("dec.tokens", (R,), torch.int64)
         self.x = b.get("dec.x", (R, d))
-        self.x16 = b.get("dec.x16", (R, d), torch.float16) if dw.half else None
+        hf = dw.half
+        # fp16 GEMM operands: fp16 copies (fp16 mode) or exact-mode (hi, lo) pairs
+        self.x16 = half_operand(b, "dec.x16", (R, d), hf)
         self.sqkv = b.get("dec.sqkv", (R, 3 * d))
         self.sctx = b.get("dec.sctx", (R, d), a16)
         self.sres = b.get("dec.sres", (R, d))
         self.snorm = b.get("dec.snorm", (R, d))
-        self.snorm16 = b.get("dec.snorm16", (R, d), torch.float16) if dw.half else None
+        self.snorm16 = half_operand(b, "dec.snorm16", (R, d), hf)
         self.cq = b.get("dec.cq", (R, d))
         self.cctx = b.get("dec.cctx", (R, d), a16)
         self.cres = b.get("dec.cres", (R, d))
         self.cnorm = b.get("dec.cnorm", (R, d))
-        self.cnorm16 = b.get("dec.cnorm16", (R, d), torch.float16) if dw.half else None
+        self.cnorm16 = half_operand(b, "dec.cnorm16", (R, d), hf)
         self.ffn_h = b.get("dec.ffn_h", (R, ff), a16)
+        self.sctx16 = self.sctx if hf else half_operand(b, "dec.sctx16", (R, d), False)
+        self.cctx16 = self.cctx if hf else half_operand(b, "dec.cctx16", (R, d), False)
+        self.ffn_h16 = self.ffn_h if hf else half_operand(b, "dec.ffn_h16", (R, ff), False)
         self.u = b.get("dec.ffn_out", (R, d))
         self.logits = b.get("dec.logits", (R, V))
         self.bad = b.get("dec.bad", (1,), torch.int32)
@@ -721,8 +807,8 @@ class DecoderStep:
         R, d = self.rows, c.d_model
         _abi.call("fq_embed_scale_pos", self.tokens.data_ptr(), R, dw.embedding.data_ptr(), d,
                   float(np.float32(math.sqrt(d))), dw.positions.data_ptr(), 0,
-                  self.cache.d_cur.data_ptr(), 1, self.x.data_ptr(), _abi.ptr(self.x16),
-                  _abi.stream_handle())
+                  self.cache.d_cur.data_ptr(), 1, self.x.data_ptr(),
+                  _abi.ptr(self.x16) if dw.half else None, _abi.stream_handle())
         self.counters.count_fused("embed_scale_pos", R * d * 8)
 
     def run(self, embed: bool = True, logits: bool = True):
@@ -739,6 +825,7 @@ class DecoderStep:
         if embed:
             self.embed()
         x, x16 = self.x, self.x16
+        fill_pair(x, x16)  # exact mode: the step input's fp16 pair
         for i, lw in enumerate(dw.dec):
             _lin(dw, x, x16, lw["w_qkv"], self.sqkv, bias=lw["b_qkv"], counters=ctr, timers=tm)
             _abi.call("fq_decoder_self_attention", self.sqkv.data_ptr(), self.sqkv.stride(0),
@@ -747,12 +834,13 @@ class DecoderStep:
                       c.max_seq_len, scale, None if dw.half else self.sctx.data_ptr(),
                       self.sctx.data_ptr() if dw.half else None, d, exact, stream)
             ctr.count_fused("decoder_self_attention", R * d * 16)
+            fill_pair(self.sctx, self.sctx16)
             if self.ln_ws is not None:
-                _lin_ln(dw, self.sctx, self.sctx, lw["w_so"], lw["b_so"], x, lw["ln1_g"],
+                _lin_ln(dw, self.sctx, self.sctx16, lw["w_so"], lw["b_so"], x, lw["ln1_g"],
                         lw["ln1_b"], c.ln_eps, self.snorm, self.snorm16, self.ln_ws,
                         counters=ctr, timers=tm)
             else:
-                _lin(dw, self.sctx, self.sctx, lw["w_so"], self.sres, bias=lw["b_so"],
+                _lin(dw, self.sctx, self.sctx16, lw["w_so"], self.sres, bias=lw["b_so"],
                      residual=x, counters=ctr, timers=tm)
                 _ln(self.sres, lw["ln1_g"], lw["ln1_b"], c.ln_eps, self.snorm, self.snorm16,
                     counters=ctr)
@@ -783,29 +871,31 @@ class DecoderStep:
                           self.cctx.data_ptr() if dw.half else None, d, exact,
                           self.bad.data_ptr(), stream)
             ctr.count_fused("cross_attention", R * d * 16)
+            fill_pair(self.cctx, self.cctx16)
             if self.ln_ws is not None:
-                _lin_ln(dw, self.cctx, self.cctx, lw["w_co"], lw["b_co"], self.snorm,
+                _lin_ln(dw, self.cctx, self.cctx16, lw["w_co"], lw["b_co"], self.snorm,
                         lw["ln2_g"], lw["ln2_b"], c.ln_eps, self.cnorm, self.cnorm16,
                         self.ln_ws, counters=ctr, timers=tm)
             else:
-                _lin(dw, self.cctx, self.cctx, lw["w_co"], self.cres, bias=lw["b_co"],
+                _lin(dw, self.cctx, self.cctx16, lw["w_co"], self.cres, bias=lw["b_co"],
                      residual=self.snorm, counters=ctr, timers=tm)
                 _ln(self.cres, lw["ln2_g"], lw["ln2_b"], c.ln_eps, self.cnorm, self.cnorm16,
                     counters=ctr)
             _lin(dw, self.cnorm, self.cnorm16, lw["w_ff1"], self.ffn_h, bias=lw["b_ff1"],
                  act=c.activation, counters=ctr, timers=tm)
+            fill_pair(self.ffn_h, self.ffn_h16)
             if self.ln_ws is not None:
-                _lin_ln(dw, self.ffn_h, self.ffn_h, lw["w_ff2"], lw["b_ff2"], self.cnorm,
+                _lin_ln(dw, self.ffn_h, self.ffn_h16, lw["w_ff2"], lw["b_ff2"], self.cnorm,
                         lw["ln3_g"], lw["ln3_b"], c.ln_eps, self.x, self.x16, self.ln_ws,
                         counters=ctr, timers=tm)
             else:
-                _lin(dw, self.ffn_h, self.ffn_h, lw["w_ff2"], self.u, bias=lw["b_ff2"],
+                _lin(dw, self.ffn_h, self.ffn_h16, lw["w_ff2"], self.u, bias=lw["b_ff2"],
                      residual=self.cnorm, counters=ctr, timers=tm)
                 _ln(self.u, lw["ln3_g"], lw["ln3_b"], c.ln_eps, self.x, self.x16, counters=ctr)
             x, x16 = self.x, self.x16
         if not logits:
             return None
-        _lin(dw, x, x16, dw.out_proj if dw.half else dw.out_x3, self.logits, counters=ctr,
+        _lin(dw, x, x16, dw.out_proj if dw.half else dw.out_xh, self.logits, counters=ctr,
              timers=tm)
         return self.logits
 
@@ -856,6 +946,7 @@ def plan_intermediates(config: ModelConfig, precision: str = "fp32") -> list[Int
     L, D = config.num_encoder_layers, config.num_decoder_layers
     bf = precision == "fp16"
     a = 2 if bf else 4  # activation bytes feeding GEMMs / attention
+    h = 2 if bf else 4  # fp16 GEMM operand bytes: fp16 copy, or the exact mode's (hi, lo) pair
     n = B * S
     specs: list[IntermediateSpec] = []
 
@@ -870,22 +961,23 @@ def plan_intermediates(config: ModelConfig, precision: str = "fp32") -> list[Int
     add("enc.mask", n * 4, 0, end)
     add("enc.bad", 4, 0, setup)
     add("enc.x", n * d * 4, 0, enc0 + 2)
-    if bf:
-        add("enc.x16", n * d * 2, 0, enc0)
+    add("enc.x16", n * d * h, 0, enc0)
     for i in range(L):
         b0 = enc0 + 8 * i
         add(f"enc.l{i}.qkv", n * 3 * d * 4, b0, b0 + 1)
         add(f"enc.l{i}.ctx", n * d * a, b0 + 1, b0 + 2)
+        if not bf:
+            add(f"enc.l{i}.ctx16", n * d * h, b0 + 1, b0 + 2)
         add(f"enc.l{i}.res1", n * d * 4, b0 + 2, b0 + 3)
         add(f"enc.l{i}.norm1", n * d * 4, b0 + 3, b0 + 5)
-        if bf:
-            add(f"enc.l{i}.norm1_16", n * d * 2, b0 + 3, b0 + 4)
+        add(f"enc.l{i}.norm1_16", n * d * h, b0 + 3, b0 + 4)
         add(f"enc.l{i}.ffn_h", n * ff * a, b0 + 4, b0 + 5)
+        if not bf:
+            add(f"enc.l{i}.ffn_h16", n * ff * h, b0 + 4, b0 + 5)
         add(f"enc.l{i}.ffn_out", n * d * 4, b0 + 5, b0 + 6)
         last = setup if i == L - 1 else b0 + 8 + 2
         add(f"enc.l{i}.out", n * d * 4, b0 + 6, last)
-        if bf:
-            add(f"enc.l{i}.out16", n * d * 2, b0 + 6, setup if i == L - 1 else b0 + 8)
+        add(f"enc.l{i}.out16", n * d * h, b0 + 6, setup if i == L - 1 else b0 + 8)
     if D:
         add("dec.cross_kv", n * 2 * D * d * a, setup, end)
         kv = 2 if bf else 4
@@ -898,17 +990,18 @@ def plan_intermediates(config: ModelConfig, precision: str = "fp32") -> list[Int
         add("dec.parents", R * 8, setup, end)
         add("dec.bad", 4, setup, end)
         add("dec.x", R * d * 4, dec0, end)
-        if bf:
-            add("dec.x16", R * d * 2, dec0, end)
+        add("dec.x16", R * d * h, dec0, end)
         for nm, sz in (("sqkv", R * 3 * d * 4), ("sctx", R * d * a), ("sres", R * d * 4),
                        ("snorm", R * d * 4), ("cq", R * d * 4), ("cctx", R * d * a),
                        ("cres", R * d * 4), ("cnorm", R * d * 4), ("ffn_h", R * ff * a),
                        ("ffn_out", R * d * 4)):
             add(f"dec.{nm}", sz, dec0, end - 3)
         add("dec.ln_ws", ln_ws_bytes(R, d), dec0, end - 3)  # split-K slabs (both modes)
-        if bf:
-            add("dec.snorm16", R * d * 2, dec0, end - 3)
-            add("dec.cnorm16", R * d * 2, dec0, end - 3)
+        add("dec.snorm16", R * d * h, dec0, end - 3)
+        add("dec.cnorm16", R * d * h, dec0, end - 3)
+        if not bf:
+            for nm, sz in (("sctx16", R * d * h), ("cctx16", R * d * h), ("ffn_h16", R * ff * h)):
+                add(f"dec.{nm}", sz, dec0, end - 3)
         add("dec.logits", R * V * 4, end - 3, end)
         # HARS stage 1 / 2 and the device beam state (whole request)
         add("hars.k", R * 4, setup, end)  # persists across steps (fq_hars_merge_step)

@@ -283,6 +283,51 @@ def gemm_x3(a, w, out, *, accumulate: bool = False, counters: OpCounters | None 
     (counters or _global_counters).count_gemm(A.numel() * 4 + 2 * N * K * 4 + O.numel() * 4)
 
 
+def split_pair(a, pair=None):
+    """The exact mode's fp16 operand pair of an fp32 [M, K] matrix (x = hi +
+    lo * 2^-11, fq_split_f16): into ``pair`` = (hi, lo) when given."""
+    A = as_device(a, torch.float32)
+    if pair is None:
+        pair = tuple(torch.empty(A.shape, dtype=torch.float16, device=A.device) for _ in range(2))
+    hi, lo = pair
+    if tuple(hi.shape) != tuple(A.shape) or hi.stride(0) != lo.stride(0):
+        raise DimensionError(f"pair shape {tuple(hi.shape)} != {tuple(A.shape)}")
+    _abi.call("fq_split_f16", A.data_ptr(), _row_major(A, "a"), A.shape[0], A.shape[1], 0,
+              hi.data_ptr(), lo.data_ptr(), hi.stride(0), _abi.stream_handle())
+    return pair
+
+
+def gemm_xh(a_pair, w, out, *, accumulate: bool = False, counters: OpCounters | None = None,
+            timers: Timers | None = None, bias=None, residual=None, activation: str = "none"):
+    """Exact-mode engine GEMM, 3xFP16 (fq_gemm_x3h): out = act(a @ w^T (+ out)
+    (+ bias)) (+ residual) with ``a_pair`` the fp16 (hi, lo) pair of the fp32
+    activation [M, K] (written by its producer, or ``split_pair``) and ``w`` an
+    ``XHWeight`` (the weight's pair, K-major [N, K], split once at load). One
+    call increments ``gemm_calls`` by one (tensor.py:204)."""
+    hi, lo = a_pair
+    O = as_device(out)
+    if hi.dim() != 2 or O.dim() != 2 or O.dtype != torch.float32 or hi.dtype != torch.float16:
+        raise DimensionError("gemm_xh expects an fp16 [M, K] pair and an fp32 output")
+    N, K = w.shape
+    if hi.shape[1] != K or tuple(O.shape) != (hi.shape[0], N) or lo.shape != hi.shape:
+        raise DimensionError(f"gemm_xh shapes {tuple(hi.shape)} x {(N, K)}^T -> {tuple(O.shape)}")
+    if hi.stride(0) != lo.stride(0):
+        raise DimensionError("gemm_xh: hi and lo need the same leading dimension")
+    _check_no_alias(O, hi, lo, w.hi, w.lo)
+    lda, ldc = _row_major(hi, "a"), _row_major(O, "out")
+    res_t, ldr = None, 0
+    if residual is not None:
+        res_t = as_device(residual, torch.float32)
+        ldr = _row_major(res_t, "residual")
+    t0 = timers.start() if timers is not None else None
+    _abi.call("fq_gemm_x3h", hi.data_ptr(), lo.data_ptr(), lda, w.hi.data_ptr(), w.lo.data_ptr(),
+              w.hi.stride(0), O.data_ptr(), ldc, hi.shape[0], N, K, int(accumulate),
+              _abi.ptr(bias), _abi.ptr(res_t), ldr, ACT_IDS[activation], _abi.stream_handle())
+    if timers is not None:
+        timers.stop("gemm", t0)
+    (counters or _global_counters).count_gemm(hi.numel() * 4 + N * K * 4 + O.numel() * 4)
+
+
 def _batch_strides(t: torch.Tensor, lead: tuple[int, ...]) -> tuple[int, int, int, int]:
     """Express the leading dims of ``t`` (broadcast to ``lead``) as a two-level
     batch (n0, s0, n1, s1)."""

@@ -333,3 +333,125 @@ def test_x3_gemm_ln_slab_path_bit_identical(P):
     mu, var = x.mean(1, keepdim=True), x.var(1, unbiased=False, keepdim=True)
     want = (x - mu) / torch.sqrt(var + 1e-5) * gm.double() + bt.double()
     assert float((outs[0].double() - want).abs().max()) <= 2e-5
+
+
+# ---------------------------------------------------------------------------
+# exact fp32 mode, 3xFP16 (fq_gemm_x3h): the engine's exact-mode GEMM
+
+def _xh(a, b_nk, out, **kw):
+    from paper_2010_13887_b200.model import XHWeight
+    from paper_2010_13887_b200.tensor import gemm_xh, split_pair
+    gemm_xh(split_pair(a), XHWeight.from_kn(b_nk, transpose=False), out, **kw)
+
+
+def test_split_pair_exact_representation(P):
+    """x = hi + lo * 2^-11 to 2^-22 relative (22 significant bits), hi the
+    round-to-nearest fp16 of x (== the fp16 mode's operand)."""
+    import torch
+    from paper_2010_13887_b200.tensor import split_pair
+    g = torch.Generator(device="cuda").manual_seed(1)
+    x = torch.randn(300, 1000, device="cuda", generator=g) * torch.exp(
+        torch.randn(300, 1000, device="cuda", generator=g) * 3).clamp(max=2e4)
+    hi, lo = split_pair(x)
+    torch.cuda.synchronize()
+    assert torch.equal(hi, x.half())
+    rec = hi.double() + lo.double() / 2048
+    err = ((rec - x.double()).abs() / x.double().abs().clamp(min=6e-5)).max()
+    assert float(err) <= 2.0 ** -21
+
+
+@pytest.mark.parametrize("M,N,K", [
+    (1, 8, 16), (100, 100, 72), (128, 64, 64), (512, 1024, 1024), (512, 3072, 1024),
+    (512, 1024, 4096), (512, 4096, 1024), (300, 2000, 256), (512, 32000, 1024),
+    (8192, 1024, 4096), (2048, 3072, 1024)])
+def test_xh_gemm_matches_f64(P, M, N, K):
+    """3xFP16 vs float64 on the same fp32 operands: fp32-GEMM accuracy (within
+    2x an IEEE fp32 SGEMM's error of the same product and <= 1e-6 of the
+    output scale), like the 3xTF32 kernel it replaces on the engine path."""
+    import torch
+    g = torch.Generator(device="cuda").manual_seed(M * 5 + N + K)
+    a = torch.randn(M, K, device="cuda", generator=g)
+    b = torch.randn(N, K, device="cuda", generator=g) * 0.03
+    want = a.double() @ b.double().T
+    scale = float(want.abs().max())
+    prev = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = False
+    sgemm_err = float((a @ b.T).double().sub(want).abs().max()) / scale
+    torch.backends.cuda.matmul.allow_tf32 = prev
+    out = torch.empty(M, N, device="cuda")
+    _xh(a, b, out)
+    torch.cuda.synchronize()
+    err = float((out.double() - want).abs().max()) / scale
+    print(f"{M}x{N}x{K}: 3xFP16 {err:.2e}  fp32 SGEMM {sgemm_err:.2e}")
+    assert err <= max(2 * sgemm_err, 5e-7) and err <= 1e-6, (M, N, K, err)
+
+
+@pytest.mark.parametrize("act", ["none", "relu", "gelu"])
+def test_xh_gemm_epilogue_bits_vs_separate_ops(P, act):
+    """Fused bias / act / residual epilogue == the GEMM then fq_bias_residual_act."""
+    import torch
+    M, N, K = 384, 1536, 512
+    g = torch.Generator(device="cuda").manual_seed(11)
+    a = torch.randn(M, K, device="cuda", generator=g)
+    b = torch.randn(N, K, device="cuda", generator=g) * 0.05
+    bias = torch.randn(N, device="cuda", generator=g)
+    res = torch.randn(M, N, device="cuda", generator=g)
+    fused = torch.empty(M, N, device="cuda")
+    _xh(a, b, fused, bias=bias, residual=res, activation=act)
+    plain = torch.empty(M, N, device="cuda")
+    _xh(a, b, plain)
+    sep = P.fused_bias_residual_activation(plain, bias, res, act)
+    assert torch.equal(fused, sep.data)
+
+
+def test_xh_gemm_bits_independent_of_m(P):
+    """The 3xFP16 plan depends on (N, K) only: a row block computed inside a
+    512-row GEMM and alone has identical bits (batch-sharding invariance)."""
+    import torch
+    g = torch.Generator(device="cuda").manual_seed(3)
+    for N, K in ((1024, 1024), (3072, 1024), (1024, 4096), (32000, 1024)):
+        a = torch.randn(512, K, device="cuda", generator=g)
+        b = torch.randn(N, K, device="cuda", generator=g) * 0.03
+        full = torch.empty(512, N, device="cuda")
+        _xh(a, b, full)
+        part = torch.empty(64, N, device="cuda")
+        _xh(a[192:256].contiguous(), b, part)
+        assert torch.equal(full[192:256], part), (N, K)
+
+
+def test_xh_gemm_ln_slab_path_bit_identical(P):
+    """fq_gemm_x3h_ln: 4 K-slice slabs summed by the LN kernel == the split-K
+    GEMM with its DSMEM reduction + fused bias/residual, then the LN; the fp16
+    pair output == fq_split_f16 of the fp32 output."""
+    import torch
+    from paper_2010_13887_b200 import _abi
+    from paper_2010_13887_b200.model import XHWeight
+    from paper_2010_13887_b200.tensor import split_pair
+    M, N, K = 512, 1024, 4096
+    g = torch.Generator(device="cuda").manual_seed(9)
+    a = torch.randn(M, K, device="cuda", generator=g)
+    ap = split_pair(a)
+    w = XHWeight.from_kn(torch.randn(N, K, device="cuda", generator=g) * 0.02, transpose=False)
+    bias = torch.randn(N, device="cuda", generator=g)
+    res = torch.randn(M, N, device="cuda", generator=g)
+    gm = torch.rand(N, device="cuda", generator=g) + 0.5
+    bt = torch.randn(N, device="cuda", generator=g)
+    outs, pairs = [], []
+    for ws_bytes in (4 * M * N * 4, 0):
+        ws = torch.empty(max(ws_bytes, 16), dtype=torch.uint8, device="cuda")
+        out = torch.empty(M, N, device="cuda")
+        pr = torch.empty(2, M, N, dtype=torch.float16, device="cuda")
+        _abi.call("fq_gemm_x3h_ln", ap[0].data_ptr(), ap[1].data_ptr(), K, w.hi.data_ptr(),
+                  w.lo.data_ptr(), K, bias.data_ptr(), res.data_ptr(), N, gm.data_ptr(),
+                  bt.data_ptr(), 1e-5, out.data_ptr(), N, pr[0].data_ptr(), pr[1].data_ptr(), N,
+                  ws.data_ptr() if ws_bytes else None, ws_bytes, M, N, K, _abi.stream_handle())
+        outs.append(out)
+        pairs.append(pr)
+    assert torch.equal(outs[0], outs[1])
+    ref_pair = split_pair(outs[0])
+    assert torch.equal(pairs[0][0], ref_pair[0]) and torch.equal(pairs[0][1], ref_pair[1])
+    assert torch.equal(pairs[1][0], ref_pair[0]) and torch.equal(pairs[1][1], ref_pair[1])
+    x = (a.double() @ (w.hi.double() + w.lo.double() / 2048).T + bias.double()) + res.double()
+    mu, var = x.mean(1, keepdim=True), x.var(1, unbiased=False, keepdim=True)
+    want = (x - mu) / torch.sqrt(var + 1e-5) * gm.double() + bt.double()
+    assert float((outs[0].double() - want).abs().max()) <= 2e-5
