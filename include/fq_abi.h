@@ -420,6 +420,25 @@ int fq_cross_attention_slabs(const float* q_slabs, int nslab, int64_t ldq, const
 
 /* ---- weight preparation (cast once at load) -------------- */
 
+/* Exact fp32 mode attention on warp MMAs (3xFP16: every fp32 operand as its
+ * fp16 pair, three MMAs per product; the reference's exact f64 softmax in
+ * between), replacing model.py:565-578 (decoder self-attention over the
+ * KVCache) and :594-604 (cross-attention). Self-attention cache: fp16 pair
+ * planes, hi at kcache / vcache and lo at + plane elements, each [max_len,
+ * rows, d]; this step's K/V are split and written to slot (cur, r). Cross K/V:
+ * pair planes of the [batch*seq, ldkv] cross-K/V buffer. ctx goes to out
+ * (fp32) and/or its pair (out_hi, out_lo) for the next exact-mode GEMM. */
+int fq_decoder_self_attention_xh(const float* sqkv, int64_t ldq, void* kcache, void* vcache,
+                                 int64_t plane, const int32_t* hist, const int32_t* d_cur,
+                                 int64_t rows, int64_t heads, int64_t head_dim, int64_t max_len,
+                                 float scale, float* out, void* out_hi, void* out_lo,
+                                 int64_t ldo, fq_stream_t stream);
+int fq_cross_attention_xh(const float* cq, int64_t ldcq, const void* ck, const void* cv,
+                          int64_t plane, int64_t ldkv, int64_t batch, int64_t beam, int64_t seq,
+                          int64_t heads, int64_t head_dim, float scale, const float* mask,
+                          float* out, void* out_hi, void* out_lo, int64_t ldo, int* d_bad,
+                          fq_stream_t stream);
+
 /* dst16[N, K] (fp16, row-major) = src[K, N]^T (fp32) when transpose, else cast. */
 int fq_cast_f16(const float* src, int64_t rows, int64_t cols, int transpose, void* dst16,
                  fq_stream_t stream);

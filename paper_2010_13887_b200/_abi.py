@@ -84,6 +84,10 @@ SIGNATURES = {
     "fq_gemm_x3h": ([P, P, I64, P, P, I64, P, I64, I64, I64, I64, I32, P, P, I64, I32, P], I32),
     "fq_gemm_x3h_ln": ([P, P, I64, P, P, I64, P, P, I64, P, P, F64, P, I64, P, P, I64, P, I64, I64,
                         I64, I64, P], I32),
+    "fq_decoder_self_attention_xh": ([P, I64, P, P, I64, P, P, I64, I64, I64, I64, F32, P, P, P,
+                                      I64, P], I32),
+    "fq_cross_attention_xh": ([P, I64, P, P, I64, I64, I64, I64, I64, I64, I64, F32, P, P, P, P,
+                               I64, P, P], I32),
     "fq_split_f16": ([P, I64, I64, I64, I32, P, P, I64, P], I32),
     "fq_layer_norm_xh": ([P, I64, P, P, F64, I64, I64, P, I64, P, P, I64, P], I32),
     "fq_splitk_bias_residual_layer_norm_xh": ([P, I32, I64, P, P, I64, P, P, F64, I64, I64, P, I64,

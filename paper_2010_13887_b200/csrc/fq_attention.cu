@@ -1498,7 +1498,10 @@ static bool mma_self_disabled() {
   return v == 1;
 }
 
+int attention_xh_prepare();
+
 int attention_prepare() {
+  if (attention_xh_prepare() != FQ_OK) return FQ_ERR_CUDA;
   const int big = 227 * 1024;
   if (cudaFuncSetAttribute(encoder_attention_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, big) ||
       cudaFuncSetAttribute(cross_attention_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, big) ||
@@ -1517,6 +1520,393 @@ int attention_prepare() {
     set_error("fq_prepare: cannot opt in to large shared memory (attention)");
     return FQ_ERR_CUDA;
   }
+  return FQ_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Exact fp32 mode on warp MMAs (3xFP16). Every fp32 operand enters as its fp16
+// pair x = hi + lo * 2^-11 (split_xh: 22 significant bits); a product takes
+// three m16n8k16 MMAs, big += a_hi.b_hi and small += a_hi.b_lo + a_lo.b_hi,
+// and the result is big + small * 2^-11 — fp32-GEMM accuracy for the
+// reference's QK^T and P.V GEMMs (model.py:570-578, :594-604). The softmax
+// between them is the reference's exact one (kernels.py:106-139, Appendix A
+// E8): fp32 scores t = fp32(s * scale) (+ mask), exp(t - max) and the sum in
+// f64, p = fp32(exp * (1 / sum)) — over all positions before P.V, so scores
+// go to shared memory first (no online rescaling).
+// Self-attention K/V cache: fp16 planes [2][max_len][rows][d] (hi, then lo at
+// + plane elements); slot (t, r) written once, at step t, by row r.
+// ---------------------------------------------------------------------------
+constexpr float kXhInv = 1.0f / 2048.0f;
+
+template <int HD, int NS>
+__global__ void __launch_bounds__(32) decoder_self_attention_xh(
+    const float* __restrict__ sqkv, int64_t ldq, h16* __restrict__ kc, h16* __restrict__ vc,
+    int64_t plane, const int32_t* __restrict__ hist, const int32_t* __restrict__ d_cur,
+    int rows, int heads, int max_len, float scale, float* __restrict__ out,
+    h16* __restrict__ out_hi, h16* __restrict__ out_lo, int64_t ldo) {
+  constexpr int RS = HD * 2 + 16;  // padded smem row bytes: conflict-free ldmatrix
+  constexpr int CPR = HD * 2 / 16;  // 16-byte pieces per row
+  constexpr int KT = HD / 16;
+  constexpr int KE = (HD + 63) / 64;  // float2 of this step's k / v per lane
+  __shared__ __align__(128) uint8_t ring[NS][2][16 * RS];  // [stage][hi | lo][16 rows]
+  extern __shared__ __align__(16) float dyn[];
+  float* sb = dyn;                                          // scores / p, [max_len + 16]
+  int* phys_s = reinterpret_cast<int*>(dyn + max_len + 16);  // [max_len]
+  pdl_enter();
+  const int r = blockIdx.x, h = blockIdx.y, lane = threadIdx.x;
+  const int g = lane >> 2, t4 = lane & 3;
+  const int d = heads * HD;
+  const int cur = *d_cur;
+  for (int t = lane; t < cur; t += 32) phys_s[t] = hist[(int64_t)r * max_len + t];
+  const float* rowp = sqkv + (int64_t)r * ldq + h * HD;
+  // this step's k, v as pairs -> cache slot (cur, r); kept for the ring
+  uint32_t knh[KE], knl[KE], vnh[KE], vnl[KE];
+  {
+    const int64_t slot = ((int64_t)cur * rows + r) * d + h * HD;
+#pragma unroll
+    for (int i = 0; i < KE; ++i) {
+      const int e = 2 * lane + 64 * i;
+      if (e < HD) {
+        const float2 kn = *reinterpret_cast<const float2*>(rowp + d + e);
+        const float2 vn = *reinterpret_cast<const float2*>(rowp + 2 * d + e);
+        split_xh2(kn.x, kn.y, knh[i], knl[i]);
+        split_xh2(vn.x, vn.y, vnh[i], vnl[i]);
+        *reinterpret_cast<uint32_t*>(kc + slot + e) = knh[i];
+        *reinterpret_cast<uint32_t*>(kc + plane + slot + e) = knl[i];
+        *reinterpret_cast<uint32_t*>(vc + slot + e) = vnh[i];
+        *reinterpret_cast<uint32_t*>(vc + plane + slot + e) = vnl[i];
+      }
+    }
+  }
+  // q^T fragments (column 0 = this row's query)
+  uint32_t qh[KT][2], ql[KT][2];
+#pragma unroll
+  for (int kk = 0; kk < KT; ++kk) {
+    float2 x0 = make_float2(0.f, 0.f), x1 = x0;
+    if (g == 0) {
+      x0 = *reinterpret_cast<const float2*>(rowp + 16 * kk + 2 * t4);
+      x1 = *reinterpret_cast<const float2*>(rowp + 16 * kk + 2 * t4 + 8);
+    }
+    split_xh2(x0.x, x0.y, qh[kk][0], ql[kk][0]);
+    split_xh2(x1.x, x1.y, qh[kk][1], ql[kk][1]);
+  }
+  __syncwarp();
+  const int npos = cur + 1, nchunk = (npos + 15) / 16;
+  // chunk c of plane pair `src` (K or V) into stage s; position cur comes from registers
+  auto issue = [&](const h16* src, int c, int s) {
+    for (int x = lane; x < 16 * CPR; x += 32) {
+      const int rr = x / CPR, ch = x % CPR;
+      const int t = 16 * c + rr;
+      uint8_t* dh = &ring[s][0][0] + rr * RS + ch * 16;
+      uint8_t* dl = &ring[s][1][0] + rr * RS + ch * 16;
+      if (t < cur) {
+        const int64_t off = ((int64_t)t * rows + phys_s[t]) * d + h * HD + ch * 8;
+        cp16(sm_u32(dh), src + off);
+        cp16(sm_u32(dl), src + plane + off);
+      } else if (t > cur) {  // beyond the sequence: zeros (p = 0, never NaN)
+        *reinterpret_cast<uint4*>(dh) = make_uint4(0, 0, 0, 0);
+        *reinterpret_cast<uint4*>(dl) = make_uint4(0, 0, 0, 0);
+      }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  auto put_cur = [&](int s, const uint32_t* hi, const uint32_t* lo) {
+    const int rr = cur % 16;
+#pragma unroll
+    for (int i = 0; i < KE; ++i) {
+      const int e = 2 * lane + 64 * i;
+      if (e < HD) {
+        *reinterpret_cast<uint32_t*>(&ring[s][0][0] + rr * RS + e * 2) = hi[i];
+        *reinterpret_cast<uint32_t*>(&ring[s][1][0] + rr * RS + e * 2) = lo[i];
+      }
+    }
+  };
+  const int lrow = (lane & 7) + ((lane >> 3) & 1) * 8, lcol = (lane >> 4) * 8;
+  // ---- pass 1: scores S^T[16 pos x 8] = K . q^T per chunk ----
+#pragma unroll
+  for (int c = 0; c < NS - 1; ++c) {
+    if (c < nchunk) issue(kc, c, c);
+    else asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+  for (int c = 0; c < nchunk; ++c) {
+    const int s = c % NS;
+    asm volatile("cp.async.wait_group %0;" ::"n"(NS - 2) : "memory");
+    if (cur / 16 == c) put_cur(s, knh, knl);
+    __syncwarp();
+    const uint8_t* Kh = &ring[s][0][0];
+    const uint8_t* Kl = &ring[s][1][0];
+    float big[4] = {0.f, 0.f, 0.f, 0.f}, sml[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int kk = 0; kk < KT; ++kk) {
+      uint32_t ah[4], al[4];
+      ldsm_x4(ah, Kh + lrow * RS + (16 * kk + lcol) * 2);
+      ldsm_x4(al, Kl + lrow * RS + (16 * kk + lcol) * 2);
+      mma_f16_16816(big, ah, qh[kk][0], qh[kk][1]);
+      mma_f16_16816(sml, ah, ql[kk][0], ql[kk][1]);
+      mma_f16_16816(sml, al, qh[kk][0], qh[kk][1]);
+    }
+    if (t4 == 0) {  // column 0: positions 16c + g (reg 0) and + 8 (reg 2)
+      const int p0 = 16 * c + g, p1 = p0 + 8;
+      if (p0 <= cur) sb[p0] = fmul_rn(fadd_rn(big[0], sml[0] * kXhInv), scale);
+      if (p1 <= cur) sb[p1] = fmul_rn(fadd_rn(big[2], sml[2] * kXhInv), scale);
+    }
+    __syncwarp();  // stage s consumed
+    if (c + NS - 1 < nchunk) issue(kc, c + NS - 1, (c + NS - 1) % NS);
+    else asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+  __syncwarp();
+  // ---- exact softmax over positions 0..cur (no mask: causality is implicit) ----
+  warp_softmax(sb, npos, true);
+  for (int t = npos + lane; t < 16 * nchunk; t += 32) sb[t] = 0.0f;
+  __syncwarp();
+  // ---- pass 2: O^T[HD x 8] += V^T . p^T per chunk ----
+#pragma unroll
+  for (int c = 0; c < NS - 1; ++c) {
+    if (c < nchunk) issue(vc, c, c);
+    else asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+  float ob[KT][4], os[KT][4];
+#pragma unroll
+  for (int m = 0; m < KT; ++m)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) ob[m][j] = os[m][j] = 0.0f;
+  const int mi = lane >> 3;
+  const int vrow = (lane & 7) + ((mi >> 1) & 1) * 8, vcol = (mi & 1) * 8;
+  for (int c = 0; c < nchunk; ++c) {
+    const int s = c % NS;
+    asm volatile("cp.async.wait_group %0;" ::"n"(NS - 2) : "memory");
+    if (cur / 16 == c) put_cur(s, vnh, vnl);
+    __syncwarp();
+    const uint8_t* Vh = &ring[s][0][0];
+    const uint8_t* Vl = &ring[s][1][0];
+    uint32_t bh0, bl0, bh1, bl1;
+    {
+      const float* pp = sb + 16 * c + 2 * t4;
+      split_xh2(g == 0 ? pp[0] : 0.f, g == 0 ? pp[1] : 0.f, bh0, bl0);
+      split_xh2(g == 0 ? pp[8] : 0.f, g == 0 ? pp[9] : 0.f, bh1, bl1);
+    }
+#pragma unroll
+    for (int m = 0; m < KT; ++m) {
+      uint32_t ah[4], al[4];
+      ldsm_x4_t(ah, Vh + vrow * RS + (16 * m + vcol) * 2);
+      ldsm_x4_t(al, Vl + vrow * RS + (16 * m + vcol) * 2);
+      mma_f16_16816(ob[m], ah, bh0, bh1);
+      mma_f16_16816(os[m], ah, bl0, bl1);
+      mma_f16_16816(os[m], al, bh0, bh1);
+    }
+    __syncwarp();
+    if (c + NS - 1 < nchunk) issue(vc, c + NS - 1, (c + NS - 1) % NS);
+    else asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+  // column 0 of O^T: lanes t4 == 0 hold dims 16m + g (reg 0) and 16m + g + 8 (reg 2)
+  if (t4 == 0) {
+    const int64_t o = (int64_t)r * ldo + h * HD;
+#pragma unroll
+    for (int m = 0; m < KT; ++m) {
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh) {
+        const int dd = 16 * m + g + 8 * hh;
+        const float v = fadd_rn(ob[m][2 * hh], os[m][2 * hh] * kXhInv);
+        if (out) out[o + dd] = v;
+        if (out_hi) split_xh(v, out_hi[o + dd], out_lo[o + dd]);
+      }
+    }
+  }
+}
+
+// Exact-mode cross-attention (3xFP16 warp MMAs), warp per (item, head), beams
+// as the MMA's 8 query columns: the item's K / V head slices (fp16 pair planes
+// of the cross-K/V buffer, [2][items * seq][ldkv]) arrive by bulk copies into
+// padded rows; scores S^T[pos x beam] = K . Q^T, the exact masked softmax per
+// beam column (model.py:594-604 + kernels.py:106-139), O^T = V^T . P^T.
+template <int HD, int NT>
+__global__ void __launch_bounds__(32) cross_attention_xh(
+    const float* __restrict__ cq, int64_t ldcq, const h16* __restrict__ ck,
+    const h16* __restrict__ cv, int64_t plane, int64_t ldkv, int beam, int seq, float scale,
+    const float* __restrict__ mask, float* __restrict__ out, h16* __restrict__ out_hi,
+    h16* __restrict__ out_lo, int64_t ldo, int* d_bad) {
+  constexpr int RS = HD * 2 + 16;
+  constexpr int NP = NT * 16;
+  constexpr int KT = HD / 16;
+  extern __shared__ __align__(128) uint8_t smb[];
+  __shared__ __align__(8) uint64_t bar;
+  __shared__ float Ps[8][NP + 4];
+  uint8_t* Kh = smb;
+  uint8_t* Kl = Kh + NP * RS;
+  uint8_t* Vh = Kl + NP * RS;
+  uint8_t* Vl = Vh + NP * RS;
+  const int b = blockIdx.x, h = blockIdx.y, lane = threadIdx.x;
+  const int g = lane >> 2, t4 = lane & 3;
+  if (lane == 0) {
+    bar_init(&bar, 1);
+    bar_expect(&bar, (uint32_t)(4 * seq * HD * 2));
+  }
+  __syncwarp();
+  pdl_enter();
+  const int64_t base = (int64_t)b * seq * ldkv + h * HD;
+  for (int x = lane; x < 4 * seq; x += 32) {
+    const int t = x >> 2, w = x & 3;
+    const h16* src = (w & 2 ? cv : ck) + (w & 1 ? plane : 0) + base + (int64_t)t * ldkv;
+    uint8_t* dst = (w == 0 ? Kh : w == 1 ? Kl : w == 2 ? Vh : Vl) + t * RS;
+    bulk_g2s(dst, src, HD * 2, &bar);
+  }
+  for (int x = lane; x < (NP - seq) * (HD / 8); x += 32) {  // zero the padded positions
+    const int t = seq + x / (HD / 8), c = (x % (HD / 8)) * 16;
+    *reinterpret_cast<uint4*>(Kh + t * RS + c) = make_uint4(0, 0, 0, 0);
+    *reinterpret_cast<uint4*>(Kl + t * RS + c) = make_uint4(0, 0, 0, 0);
+    *reinterpret_cast<uint4*>(Vh + t * RS + c) = make_uint4(0, 0, 0, 0);
+    *reinterpret_cast<uint4*>(Vl + t * RS + c) = make_uint4(0, 0, 0, 0);
+  }
+  // Q^T fragments: lane (g, t4) holds beam g, dims 16k + {2t4, 2t4+1, 2t4+8, 2t4+9}
+  uint32_t qh[KT][2], ql[KT][2];
+  {
+    const bool ok = g < beam;
+    const float* qp = cq + ((int64_t)b * beam + (ok ? g : 0)) * ldcq + h * HD;
+#pragma unroll
+    for (int kk = 0; kk < KT; ++kk) {
+      const float2 x0 = ok ? *reinterpret_cast<const float2*>(qp + 16 * kk + 2 * t4) : make_float2(0.f, 0.f);
+      const float2 x1 = ok ? *reinterpret_cast<const float2*>(qp + 16 * kk + 2 * t4 + 8) : make_float2(0.f, 0.f);
+      split_xh2(x0.x, x0.y, qh[kk][0], ql[kk][0]);
+      split_xh2(x1.x, x1.y, qh[kk][1], ql[kk][1]);
+    }
+  }
+  __syncwarp();
+  bar_wait(&bar, 0);
+  // ---- scores ----
+  float sc[NT][4];
+  const int lrow = (lane & 7) + ((lane >> 3) & 1) * 8, lcol = (lane >> 4) * 8;
+#pragma unroll
+  for (int m = 0; m < NT; ++m) {
+    float big[4] = {0.f, 0.f, 0.f, 0.f}, sml[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int kk = 0; kk < KT; ++kk) {
+      uint32_t ah[4], al[4];
+      ldsm_x4(ah, Kh + (16 * m + lrow) * RS + (16 * kk + lcol) * 2);
+      ldsm_x4(al, Kl + (16 * m + lrow) * RS + (16 * kk + lcol) * 2);
+      mma_f16_16816(big, ah, qh[kk][0], qh[kk][1]);
+      mma_f16_16816(sml, ah, ql[kk][0], ql[kk][1]);
+      mma_f16_16816(sml, al, qh[kk][0], qh[kk][1]);
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) sc[m][j] = fadd_rn(big[j], sml[j] * kXhInv);
+  }
+  // ---- exact softmax per beam column (lane: columns 2t4, 2t4+1) ----
+  const float* mk = mask ? mask + (int64_t)b * seq : nullptr;
+  float mx0 = -INFINITY, mx1 = -INFINITY;
+#pragma unroll
+  for (int m = 0; m < NT; ++m) {
+#pragma unroll
+    for (int hh = 0; hh < 2; ++hh) {
+      const int p = 16 * m + g + 8 * hh;
+      float t0 = -INFINITY, t1 = -INFINITY;
+      if (p < seq) {
+        t0 = fmul_rn(sc[m][2 * hh], scale);
+        t1 = fmul_rn(sc[m][2 * hh + 1], scale);
+        if (mk) {
+          t0 = fadd_rn(t0, mk[p]);
+          t1 = fadd_rn(t1, mk[p]);
+        }
+      }
+      sc[m][2 * hh] = t0;
+      sc[m][2 * hh + 1] = t1;
+      mx0 = fmaxf(mx0, t0);
+      mx1 = fmaxf(mx1, t1);
+    }
+  }
+#pragma unroll
+  for (int o = 4; o < 32; o <<= 1) {
+    mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, o));
+    mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, o));
+  }
+  double l0 = 0.0, l1 = 0.0;
+#pragma unroll
+  for (int m = 0; m < NT; ++m) {
+#pragma unroll
+    for (int hh = 0; hh < 2; ++hh) {
+      const float t0 = sc[m][2 * hh], t1 = sc[m][2 * hh + 1];
+      if (t0 != -INFINITY) l0 += exp((double)t0 - (double)mx0);
+      if (t1 != -INFINITY) l1 += exp((double)t1 - (double)mx1);
+    }
+  }
+#pragma unroll
+  for (int o = 4; o < 32; o <<= 1) {
+    l0 += __shfl_xor_sync(0xffffffffu, l0, o);
+    l1 += __shfl_xor_sync(0xffffffffu, l1, o);
+  }
+  const double inv0 = l0 > 0.0 ? 1.0 / l0 : 0.0, inv1 = l1 > 0.0 ? 1.0 / l1 : 0.0;
+#pragma unroll
+  for (int m = 0; m < NT; ++m) {
+#pragma unroll
+    for (int hh = 0; hh < 2; ++hh) {
+      const int p = 16 * m + g + 8 * hh;
+      const float t0 = sc[m][2 * hh], t1 = sc[m][2 * hh + 1];
+      Ps[2 * t4][p] = t0 == -INFINITY ? 0.0f : (float)(exp((double)t0 - (double)mx0) * inv0);
+      Ps[2 * t4 + 1][p] = t1 == -INFINITY ? 0.0f : (float)(exp((double)t1 - (double)mx1) * inv1);
+    }
+  }
+  if (d_bad && g == 0) {
+    if (2 * t4 < beam && !(l0 > 0.0)) atomicAdd(d_bad, 1);
+    if (2 * t4 + 1 < beam && !(l1 > 0.0)) atomicAdd(d_bad, 1);
+  }
+  __syncwarp();
+  // ---- O^T = V^T . P^T ----
+  float ob[KT][4], os[KT][4];
+#pragma unroll
+  for (int m = 0; m < KT; ++m)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) ob[m][j] = os[m][j] = 0.0f;
+  const int mi = lane >> 3;
+  const int vrow = (lane & 7) + ((mi >> 1) & 1) * 8, vcol = (mi & 1) * 8;
+#pragma unroll
+  for (int kk = 0; kk < NT; ++kk) {
+    uint32_t bh0, bl0, bh1, bl1;
+    split_xh2(Ps[g][16 * kk + 2 * t4], Ps[g][16 * kk + 2 * t4 + 1], bh0, bl0);
+    split_xh2(Ps[g][16 * kk + 2 * t4 + 8], Ps[g][16 * kk + 2 * t4 + 9], bh1, bl1);
+#pragma unroll
+    for (int m = 0; m < KT; ++m) {
+      uint32_t ah[4], al[4];
+      ldsm_x4_t(ah, Vh + (16 * kk + vrow) * RS + (16 * m + vcol) * 2);
+      ldsm_x4_t(al, Vl + (16 * kk + vrow) * RS + (16 * m + vcol) * 2);
+      mma_f16_16816(ob[m], ah, bh0, bh1);
+      mma_f16_16816(os[m], ah, bl0, bl1);
+      mma_f16_16816(os[m], al, bh0, bh1);
+    }
+  }
+  // ---- store: lane holds dims {16m + g, +8} x beams {2t4, 2t4+1} ----
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    const int bi = 2 * t4 + j;
+    if (bi >= beam) continue;
+    const int64_t o = ((int64_t)b * beam + bi) * ldo + h * HD;
+#pragma unroll
+    for (int m = 0; m < KT; ++m) {
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh) {
+        const int dd = 16 * m + g + 8 * hh;
+        const float v = fadd_rn(ob[m][2 * hh + j], os[m][2 * hh + j] * kXhInv);
+        if (out) out[o + dd] = v;
+        if (out_hi) split_xh(v, out_hi[o + dd], out_lo[o + dd]);
+      }
+    }
+  }
+}
+
+int attention_xh_prepare() {
+  const int sz = 200 * 1024;
+#define FQ_XH_OPT(HD)                                                                           \
+  cudaFuncSetAttribute(cross_attention_xh<HD, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sz) || \
+      cudaFuncSetAttribute(cross_attention_xh<HD, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sz) || \
+      cudaFuncSetAttribute(cross_attention_xh<HD, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, sz) || \
+      cudaFuncSetAttribute(cross_attention_xh<HD, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, sz) || \
+      cudaFuncSetAttribute(cross_attention_xh<HD, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, sz) || \
+      cudaFuncSetAttribute(decoder_self_attention_xh<HD, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, sz)
+  if (FQ_XH_OPT(16) || FQ_XH_OPT(32) || FQ_XH_OPT(64) || FQ_XH_OPT(128)) {
+    set_error("fq_prepare: cannot opt in to large shared memory (exact attention)");
+    return FQ_ERR_CUDA;
+  }
+#undef FQ_XH_OPT
   return FQ_OK;
 }
 
@@ -1660,6 +2050,66 @@ int fq_decoder_self_attention(const float* sqkv, int64_t ldq, void* kcache, void
         reinterpret_cast<fq::h16*>(out16), ldo, exact);
   }
   return launch_status("fq_decoder_self_attention");
+}
+
+int fq_decoder_self_attention_xh(const float* sqkv, int64_t ldq, void* kcache, void* vcache,
+                                 int64_t plane, const int32_t* hist, const int32_t* d_cur,
+                                 int64_t rows, int64_t heads, int64_t head_dim, int64_t max_len,
+                                 float scale, float* out, void* out_hi, void* out_lo,
+                                 int64_t ldo, fq_stream_t stream) {
+  FQ_CHECK_ARG(sqkv && kcache && vcache && hist && d_cur && (out || out_hi) &&
+                   (!out_hi == !out_lo) && rows > 0 && heads > 0 && max_len > 0 &&
+                   (head_dim == 16 || head_dim == 32 || head_dim == 64 || head_dim == 128) &&
+                   ldq % 2 == 0 && ((uintptr_t)sqkv & 7) == 0 && plane % 8 == 0 &&
+                   ((uintptr_t)kcache & 15) == 0 && ((uintptr_t)vcache & 15) == 0,
+               FQ_ERR_DIMENSION, "fq_decoder_self_attention_xh: bad args");
+  const size_t smem = (size_t)(max_len + 16) * 4 + (size_t)max_len * 4;
+  FQ_CHECK_ARG(smem <= 200 * 1024, FQ_ERR_CAPACITY, "decoder self-attention: max_len too long");
+  const dim3 grid((unsigned)rows, (unsigned)heads);
+#define FQ_SELF_XH(HD)                                                                        \
+  launch_kernel(decoder_self_attention_xh<HD, 3>, grid, 32, smem, as_stream(stream), 1u, sqkv, \
+                ldq, (h16*)kcache, (h16*)vcache, plane, hist, d_cur, (int)rows, (int)heads,    \
+                (int)max_len, scale, out, (h16*)out_hi, (h16*)out_lo, ldo)
+  if (head_dim == 16) FQ_SELF_XH(16);
+  else if (head_dim == 32) FQ_SELF_XH(32);
+  else if (head_dim == 64) FQ_SELF_XH(64);
+  else FQ_SELF_XH(128);
+#undef FQ_SELF_XH
+  return launch_status("fq_decoder_self_attention_xh");
+}
+
+int fq_cross_attention_xh(const float* cq, int64_t ldcq, const void* ck, const void* cv,
+                          int64_t plane, int64_t ldkv, int64_t batch, int64_t beam, int64_t seq,
+                          int64_t heads, int64_t head_dim, float scale, const float* mask,
+                          float* out, void* out_hi, void* out_lo, int64_t ldo, int* d_bad,
+                          fq_stream_t stream) {
+  FQ_CHECK_ARG(cq && ck && cv && (out || out_hi) && (!out_hi == !out_lo) && batch > 0 &&
+                   beam > 0 && beam <= 8 && seq > 0 && seq <= 128 && heads > 0 &&
+                   (head_dim == 16 || head_dim == 32 || head_dim == 64 || head_dim == 128) &&
+                   ldcq % 2 == 0 && ((uintptr_t)cq & 7) == 0 && ldkv % 8 == 0 && plane % 8 == 0 &&
+                   ((uintptr_t)ck & 15) == 0 && ((uintptr_t)cv & 15) == 0,
+               FQ_ERR_DIMENSION, "fq_cross_attention_xh: unsupported shape");
+  const dim3 grid((unsigned)batch, (unsigned)heads);
+  const int nt = (int)((seq + 15) / 16);
+  const size_t smem = (size_t)4 * nt * 16 * (head_dim * 2 + 16);
+  FQ_CHECK_ARG(smem <= 200 * 1024, FQ_ERR_CAPACITY, "cross attention: seq too long");
+#define FQ_CROSS_XH(HD, NT)                                                                   \
+  launch_kernel(cross_attention_xh<HD, NT>, grid, 32, smem, as_stream(stream), 1u, cq, ldcq,   \
+                (const h16*)ck, (const h16*)cv, plane, ldkv, (int)beam, (int)seq, scale, mask, \
+                out, (h16*)out_hi, (h16*)out_lo, ldo, d_bad)
+#define FQ_CROSS_XHH(HD)                                                                      \
+  if (nt == 1) FQ_CROSS_XH(HD, 1);                                                            \
+  else if (nt == 2) FQ_CROSS_XH(HD, 2);                                                       \
+  else if (nt == 3) FQ_CROSS_XH(HD, 3);                                                       \
+  else if (nt == 4) FQ_CROSS_XH(HD, 4);                                                       \
+  else FQ_CROSS_XH(HD, 8);
+  if (head_dim == 16) { FQ_CROSS_XHH(16) }
+  else if (head_dim == 32) { FQ_CROSS_XHH(32) }
+  else if (head_dim == 64) { FQ_CROSS_XHH(64) }
+  else { FQ_CROSS_XHH(128) }
+#undef FQ_CROSS_XHH
+#undef FQ_CROSS_XH
+  return launch_status("fq_cross_attention_xh");
 }
 
 int fq_cross_attention_slabs(const float* q_slabs, int nslab, int64_t ldq, const float* q_bias,

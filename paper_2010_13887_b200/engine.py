@@ -192,7 +192,8 @@ class Session:
             bufs = self._buffers if g == 0 else self._group_buffers()
             cache = cache0 if ngroups == 1 else M.KVCache(self.config, nr, bufs,
                                                           precision=self.precision)
-            gp = packed[i0 * seq:i1 * seq]
+            # (exact mode: packed is the [2, n, 2*L*d] fp16 pair planes)
+            gp = packed[:, i0 * seq:i1 * seq] if packed.dim() == 3 else packed[i0 * seq:i1 * seq]
             gm = mask[i0:i1] if mask is not None else None
             # the fused LN's row-block exchange needs every CTA of its launch resident:
             # one step chain at a time (not with the two-stream overlap)

@@ -663,11 +663,16 @@ class KVCache:
             raise CapacityError(f"{rows} rows exceed max batch*beam {config.max_rows}")
         S, d = config.max_seq_len, config.d_model
         self.config, self.rows, self.max_seq_len = config, rows, S
-        self.kv_dtype = torch.float16 if precision == "fp16" else torch.float32
-        self._k = [buffers.get(f"{prefix}.l{i}.k", (S, rows, d), self.kv_dtype)
+        # fp16 mode: fp16 [S, rows, d]; exact mode: the fp16 pair planes
+        # [2, S, rows, d] (hi, lo) the 3xFP16 attention reads
+        self.kv_dtype = torch.float16
+        self.pairs = precision != "fp16"
+        shape = (2, S, rows, d) if self.pairs else (S, rows, d)
+        self._k = [buffers.get(f"{prefix}.l{i}.k", shape, torch.float16)
                    for i in range(config.num_decoder_layers)]
-        self._v = [buffers.get(f"{prefix}.l{i}.v", (S, rows, d), self.kv_dtype)
+        self._v = [buffers.get(f"{prefix}.l{i}.v", shape, torch.float16)
                    for i in range(config.num_decoder_layers)]
+        self.plane = S * rows * d
         self.hist = buffers.get(f"{prefix}.hist", (rows, S), torch.int32)
         self.d_cur = buffers.get(f"{prefix}.cur", (1,), torch.int32)
         self.reset()
@@ -697,7 +702,10 @@ class KVCache:
         c, rows, h, hd = self.current_len, self.rows, self.config.num_heads, self.config.head_dim
         t = torch.arange(c, device=self.hist.device)
         phys = self.hist[:, :c].long()                       # [rows, c]
-        g = store[layer][t[None, :], phys]                   # [rows, c, d]
+        st = store[layer]
+        if self.pairs:  # x = hi + lo * 2^-11
+            st = st[0].double() + st[1].double() / 2048.0
+        g = st[t[None, :], phys]                             # [rows, c, d]
         return g.view(rows, c, h, hd).permute(0, 2, 1, 3).float()
 
     def k(self, layer: int) -> torch.Tensor:
@@ -727,6 +735,10 @@ def build_cross_kv(memory, weights, config: ModelConfig, batch: int, seq: int, *
     if not dw.half and memory16 is None:
         memory16 = split_pair(M)
     _lin(dw, M, memory16, dw.w_ckv, packed, bias=dw.b_ckv, counters=counters, timers=timers)
+    if not dw.half:  # exact mode: the fp16 pair planes [2, n, 2*L*d] the attention reads
+        pair = bufs.get("dec.cross_kv16", (2, n, 2 * L * d), torch.float16)
+        split_pair(packed, (pair[0], pair[1]))
+        return pair
     return packed
 
 
@@ -801,6 +813,41 @@ class DecoderStep:
                         config.head_dim == 64 and beam <= 8 and enc_seq <= 64)
         self._nslab = ctypes.c_int(0)
 
+    def _exact_layer(self, i, lw, x, x16, scale, stream):
+        """One decoder layer after its QKV GEMM in exact mode: attention on the
+        fp16 pair cache / cross K/V (fq_*_attention_xh, ctx emitted as pairs),
+        the 3xFP16 GEMMs, and the split-K slab LNs emitting the next pairs."""
+        c, dw, ctr, tm = self.config, self.dw, self.counters, self.timers
+        R, d, h, hd = self.rows, c.d_model, c.num_heads, c.head_dim
+        k, v = self.cache._k[i], self.cache._v[i]
+        sh, sl = self.sctx16
+        _abi.call("fq_decoder_self_attention_xh", self.sqkv.data_ptr(), self.sqkv.stride(0),
+                  k.data_ptr(), v.data_ptr(), self.cache.plane, self.cache.hist.data_ptr(),
+                  self.cache.d_cur.data_ptr(), R, h, hd, c.max_seq_len, scale, None,
+                  sh.data_ptr(), sl.data_ptr(), sh.stride(0), stream)
+        ctr.count_fused("decoder_self_attention", R * d * 16)
+        _lin_ln(dw, self.sctx, self.sctx16, lw["w_so"], lw["b_so"], x, lw["ln1_g"], lw["ln1_b"],
+                c.ln_eps, self.snorm, self.snorm16, self.ln_ws, counters=ctr, timers=tm)
+        _lin(dw, self.snorm, self.snorm16, lw["w_cq"], self.cq, bias=lw["b_cq"], counters=ctr,
+             timers=tm)
+        cr = self.cross  # [2, n, 2*L*d] pair planes
+        ld = cr.stride(1)
+        ch, cl = self.cctx16
+        _abi.call("fq_cross_attention_xh", self.cq.data_ptr(), self.cq.stride(0),
+                  cr[0, :, 2 * i * d:].data_ptr(), cr[0, :, (2 * i + 1) * d:].data_ptr(),
+                  cr.stride(0), ld, self.batch, self.beam, self.enc_seq, h, hd, scale,
+                  _abi.ptr(self.mask), None, ch.data_ptr(), cl.data_ptr(), ch.stride(0),
+                  self.bad.data_ptr(), stream)
+        ctr.count_fused("cross_attention", R * d * 16)
+        _lin_ln(dw, self.cctx, self.cctx16, lw["w_co"], lw["b_co"], self.snorm, lw["ln2_g"],
+                lw["ln2_b"], c.ln_eps, self.cnorm, self.cnorm16, self.ln_ws, counters=ctr,
+                timers=tm)
+        _lin(dw, self.cnorm, self.cnorm16, lw["w_ff1"], self.ffn_h, bias=lw["b_ff1"],
+             act=c.activation, counters=ctr, timers=tm)
+        fill_pair(self.ffn_h, self.ffn_h16)
+        _lin_ln(dw, self.ffn_h, self.ffn_h16, lw["w_ff2"], lw["b_ff2"], self.cnorm, lw["ln3_g"],
+                lw["ln3_b"], c.ln_eps, self.x, self.x16, self.ln_ws, counters=ctr, timers=tm)
+
     def embed(self):
         """Decoder input of the current position (model.py:559)."""
         c, dw = self.config, self.dw
@@ -828,6 +875,10 @@ class DecoderStep:
         fill_pair(x, x16)  # exact mode: the step input's fp16 pair
         for i, lw in enumerate(dw.dec):
             _lin(dw, x, x16, lw["w_qkv"], self.sqkv, bias=lw["b_qkv"], counters=ctr, timers=tm)
+            if not dw.half:  # exact mode: 3xFP16 warp-MMA attention on the pair cache
+                self._exact_layer(i, lw, x, x16, scale, stream)
+                x, x16 = self.x, self.x16
+                continue
             _abi.call("fq_decoder_self_attention", self.sqkv.data_ptr(), self.sqkv.stride(0),
                       self.cache._k[i].data_ptr(), self.cache._v[i].data_ptr(), kvdt,
                       self.cache.hist.data_ptr(), self.cache.d_cur.data_ptr(), R, h, hd,
@@ -914,7 +965,7 @@ def decode_step(last_tokens, cache: KVCache, cross_kv, enc_mask, weights, config
     dw = DeviceWeights.get(config, weights, precision)
     bufs = buffers if buffers is not None else HeapBuffers()
     if enc_seq is None:
-        enc_seq = cross_kv.shape[0] // batch
+        enc_seq = cross_kv.shape[-2] // batch
     cache.begin_step(parents)
     step = DecoderStep(dw, config, batch, beam, enc_seq, cache, cross_kv, enc_mask, bufs,
                        counters, timers)
@@ -979,7 +1030,11 @@ def plan_intermediates(config: ModelConfig, precision: str = "fp32") -> list[Int
         add(f"enc.l{i}.out", n * d * 4, b0 + 6, last)
         add(f"enc.l{i}.out16", n * d * h, b0 + 6, setup if i == L - 1 else b0 + 8)
     if D:
-        add("dec.cross_kv", n * 2 * D * d * a, setup, end)
+        if bf:
+            add("dec.cross_kv", n * 2 * D * d * 2, setup, end)
+        else:  # exact mode: fp32 GEMM output, then its fp16 pair planes for the attention
+            add("dec.cross_kv", n * 2 * D * d * 4, setup, setup)
+            add("dec.cross_kv16", n * 2 * D * d * 4, setup, end)
         kv = 2 if bf else 4
         for i in range(D):
             add(f"dec.cache.l{i}.k", S * R * d * kv, setup, end)
