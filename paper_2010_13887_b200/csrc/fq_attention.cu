@@ -1717,10 +1717,14 @@ __global__ void __launch_bounds__(32) decoder_self_attention_xh(
 }
 
 // Exact-mode cross-attention (3xFP16 warp MMAs), warp per (item, head), beams
-// as the MMA's 8 query columns: the item's K / V head slices (fp16 pair planes
-// of the cross-K/V buffer, [2][items * seq][ldkv]) arrive by bulk copies into
-// padded rows; scores S^T[pos x beam] = K . Q^T, the exact masked softmax per
-// beam column (model.py:594-604 + kernels.py:106-139), O^T = V^T . P^T.
+// as the MMA's 8 query columns. The item's K then V head slices (fp16 pair
+// planes of the cross-K/V buffer, [2][items * seq][ldkv]) stream through a
+// shared-memory ring in 16-position chunks (cp.async, padded rows) — 12 KB per
+// warp, so a whole C2 layer's (item, head) warps are resident in one wave:
+//   pass 1  S^T[pos x beam] = K . Q^T, scores kept in registers;
+//   softmax the reference's exact masked one per beam column (model.py:594-604,
+//           kernels.py:106-139: fp32 t = s * scale + mask, f64 exp and sum);
+//   pass 2  O^T = V^T . P^T.
 template <int HD, int NT>
 __global__ void __launch_bounds__(32) cross_attention_xh(
     const float* __restrict__ cq, int64_t ldcq, const h16* __restrict__ ck,
@@ -1728,37 +1732,42 @@ __global__ void __launch_bounds__(32) cross_attention_xh(
     const float* __restrict__ mask, float* __restrict__ out, h16* __restrict__ out_hi,
     h16* __restrict__ out_lo, int64_t ldo, int* d_bad) {
   constexpr int RS = HD * 2 + 16;
+  constexpr int CPR = HD * 2 / 16;
   constexpr int NP = NT * 16;
   constexpr int KT = HD / 16;
-  extern __shared__ __align__(128) uint8_t smb[];
-  __shared__ __align__(8) uint64_t bar;
+  constexpr int NS = 3;
+  __shared__ __align__(128) uint8_t ring[NS][2][16 * RS];
   __shared__ float Ps[8][NP + 4];
-  uint8_t* Kh = smb;
-  uint8_t* Kl = Kh + NP * RS;
-  uint8_t* Vh = Kl + NP * RS;
-  uint8_t* Vl = Vh + NP * RS;
   const int b = blockIdx.x, h = blockIdx.y, lane = threadIdx.x;
   const int g = lane >> 2, t4 = lane & 3;
-  if (lane == 0) {
-    bar_init(&bar, 1);
-    bar_expect(&bar, (uint32_t)(4 * seq * HD * 2));
-  }
-  __syncwarp();
   pdl_enter();
   const int64_t base = (int64_t)b * seq * ldkv + h * HD;
-  for (int x = lane; x < 4 * seq; x += 32) {
-    const int t = x >> 2, w = x & 3;
-    const h16* src = (w & 2 ? cv : ck) + (w & 1 ? plane : 0) + base + (int64_t)t * ldkv;
-    uint8_t* dst = (w == 0 ? Kh : w == 1 ? Kl : w == 2 ? Vh : Vl) + t * RS;
-    bulk_g2s(dst, src, HD * 2, &bar);
-  }
-  for (int x = lane; x < (NP - seq) * (HD / 8); x += 32) {  // zero the padded positions
-    const int t = seq + x / (HD / 8), c = (x % (HD / 8)) * 16;
-    *reinterpret_cast<uint4*>(Kh + t * RS + c) = make_uint4(0, 0, 0, 0);
-    *reinterpret_cast<uint4*>(Kl + t * RS + c) = make_uint4(0, 0, 0, 0);
-    *reinterpret_cast<uint4*>(Vh + t * RS + c) = make_uint4(0, 0, 0, 0);
-    *reinterpret_cast<uint4*>(Vl + t * RS + c) = make_uint4(0, 0, 0, 0);
-  }
+  auto issue = [&](const h16* src, int c, int st) {
+    for (int x = lane; x < 16 * CPR; x += 32) {
+      const int rr = x / CPR, pc = x % CPR;
+      const int t = 16 * c + rr;
+      uint8_t* dh = &ring[st][0][0] + rr * RS + pc * 16;
+      uint8_t* dl = &ring[st][1][0] + rr * RS + pc * 16;
+      if (t < seq) {
+        const h16* p = src + base + (int64_t)t * ldkv + pc * 8;
+        cp16(sm_u32(dh), p);
+        cp16(sm_u32(dl), p + plane);
+      } else {  // padded positions: zeros (p = 0, never NaN)
+        *reinterpret_cast<uint4*>(dh) = make_uint4(0, 0, 0, 0);
+        *reinterpret_cast<uint4*>(dl) = make_uint4(0, 0, 0, 0);
+      }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  const int nchunk = (seq + 15) / 16;
+  // global chunk sequence: K chunks 0..nchunk-1, then V chunks; gi -> stage gi % NS
+  auto issue_g = [&](int gi) {
+    if (gi < nchunk) issue(ck, gi, gi % NS);
+    else if (gi < 2 * nchunk) issue(cv, gi - nchunk, gi % NS);
+    else asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+#pragma unroll
+  for (int c = 0; c < NS - 1; ++c) issue_g(c);
   // Q^T fragments: lane (g, t4) holds beam g, dims 16k + {2t4, 2t4+1, 2t4+8, 2t4+9}
   uint32_t qh[KT][2], ql[KT][2];
   {
@@ -1772,25 +1781,33 @@ __global__ void __launch_bounds__(32) cross_attention_xh(
       split_xh2(x1.x, x1.y, qh[kk][1], ql[kk][1]);
     }
   }
-  __syncwarp();
-  bar_wait(&bar, 0);
-  // ---- scores ----
+  // ---- pass 1: scores ----
   float sc[NT][4];
   const int lrow = (lane & 7) + ((lane >> 3) & 1) * 8, lcol = (lane >> 4) * 8;
 #pragma unroll
   for (int m = 0; m < NT; ++m) {
-    float big[4] = {0.f, 0.f, 0.f, 0.f}, sml[4] = {0.f, 0.f, 0.f, 0.f};
+    sc[m][0] = sc[m][1] = sc[m][2] = sc[m][3] = 0.0f;
+    if (m < nchunk) {
+      const int st = m % NS;
+      asm volatile("cp.async.wait_group %0;" ::"n"(NS - 2) : "memory");
+      __syncwarp();
+      const uint8_t* Kh = &ring[st][0][0];
+      const uint8_t* Kl = &ring[st][1][0];
+      float big[4] = {0.f, 0.f, 0.f, 0.f}, sml[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-    for (int kk = 0; kk < KT; ++kk) {
-      uint32_t ah[4], al[4];
-      ldsm_x4(ah, Kh + (16 * m + lrow) * RS + (16 * kk + lcol) * 2);
-      ldsm_x4(al, Kl + (16 * m + lrow) * RS + (16 * kk + lcol) * 2);
-      mma_f16_16816(big, ah, qh[kk][0], qh[kk][1]);
-      mma_f16_16816(sml, ah, ql[kk][0], ql[kk][1]);
-      mma_f16_16816(sml, al, qh[kk][0], qh[kk][1]);
+      for (int kk = 0; kk < KT; ++kk) {
+        uint32_t ah[4], al[4];
+        ldsm_x4(ah, Kh + lrow * RS + (16 * kk + lcol) * 2);
+        ldsm_x4(al, Kl + lrow * RS + (16 * kk + lcol) * 2);
+        mma_f16_16816(big, ah, qh[kk][0], qh[kk][1]);
+        mma_f16_16816(sml, ah, ql[kk][0], ql[kk][1]);
+        mma_f16_16816(sml, al, qh[kk][0], qh[kk][1]);
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) sc[m][j] = fadd_rn(big[j], sml[j] * kXhInv);
+      __syncwarp();
+      issue_g(m + NS - 1);  // K chunks, then the first V chunks
     }
-#pragma unroll
-    for (int j = 0; j < 4; ++j) sc[m][j] = fadd_rn(big[j], sml[j] * kXhInv);
   }
   // ---- exact softmax per beam column (lane: columns 2t4, 2t4+1) ----
   const float* mk = mask ? mask + (int64_t)b * seq : nullptr;
@@ -1805,8 +1822,9 @@ __global__ void __launch_bounds__(32) cross_attention_xh(
         t0 = fmul_rn(sc[m][2 * hh], scale);
         t1 = fmul_rn(sc[m][2 * hh + 1], scale);
         if (mk) {
-          t0 = fadd_rn(t0, mk[p]);
-          t1 = fadd_rn(t1, mk[p]);
+          const float mv = mk[p];
+          t0 = fadd_rn(t0, mv);
+          t1 = fadd_rn(t1, mv);
         }
       }
       sc[m][2 * hh] = t0;
@@ -1820,14 +1838,17 @@ __global__ void __launch_bounds__(32) cross_attention_xh(
     mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, o));
     mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, o));
   }
+  double e[NT][4];
   double l0 = 0.0, l1 = 0.0;
 #pragma unroll
   for (int m = 0; m < NT; ++m) {
 #pragma unroll
     for (int hh = 0; hh < 2; ++hh) {
       const float t0 = sc[m][2 * hh], t1 = sc[m][2 * hh + 1];
-      if (t0 != -INFINITY) l0 += exp((double)t0 - (double)mx0);
-      if (t1 != -INFINITY) l1 += exp((double)t1 - (double)mx1);
+      e[m][2 * hh] = t0 == -INFINITY ? 0.0 : exp((double)t0 - (double)mx0);
+      e[m][2 * hh + 1] = t1 == -INFINITY ? 0.0 : exp((double)t1 - (double)mx1);
+      l0 += e[m][2 * hh];
+      l1 += e[m][2 * hh + 1];
     }
   }
 #pragma unroll
@@ -1841,9 +1862,8 @@ __global__ void __launch_bounds__(32) cross_attention_xh(
 #pragma unroll
     for (int hh = 0; hh < 2; ++hh) {
       const int p = 16 * m + g + 8 * hh;
-      const float t0 = sc[m][2 * hh], t1 = sc[m][2 * hh + 1];
-      Ps[2 * t4][p] = t0 == -INFINITY ? 0.0f : (float)(exp((double)t0 - (double)mx0) * inv0);
-      Ps[2 * t4 + 1][p] = t1 == -INFINITY ? 0.0f : (float)(exp((double)t1 - (double)mx1) * inv1);
+      Ps[2 * t4][p] = (float)(e[m][2 * hh] * inv0);
+      Ps[2 * t4 + 1][p] = (float)(e[m][2 * hh + 1] * inv1);
     }
   }
   if (d_bad && g == 0) {
@@ -1851,7 +1871,7 @@ __global__ void __launch_bounds__(32) cross_attention_xh(
     if (2 * t4 + 1 < beam && !(l1 > 0.0)) atomicAdd(d_bad, 1);
   }
   __syncwarp();
-  // ---- O^T = V^T . P^T ----
+  // ---- pass 2: O^T = V^T . P^T over the V chunks (ring continues) ----
   float ob[KT][4], os[KT][4];
 #pragma unroll
   for (int m = 0; m < KT; ++m)
@@ -1861,19 +1881,29 @@ __global__ void __launch_bounds__(32) cross_attention_xh(
   const int vrow = (lane & 7) + ((mi >> 1) & 1) * 8, vcol = (mi & 1) * 8;
 #pragma unroll
   for (int kk = 0; kk < NT; ++kk) {
-    uint32_t bh0, bl0, bh1, bl1;
-    split_xh2(Ps[g][16 * kk + 2 * t4], Ps[g][16 * kk + 2 * t4 + 1], bh0, bl0);
-    split_xh2(Ps[g][16 * kk + 2 * t4 + 8], Ps[g][16 * kk + 2 * t4 + 9], bh1, bl1);
+    if (kk < nchunk) {
+      const int st = (nchunk + kk) % NS;
+      asm volatile("cp.async.wait_group %0;" ::"n"(NS - 2) : "memory");
+      __syncwarp();
+      const uint8_t* Vh = &ring[st][0][0];
+      const uint8_t* Vl = &ring[st][1][0];
+      uint32_t bh0, bl0, bh1, bl1;
+      split_xh2(Ps[g][16 * kk + 2 * t4], Ps[g][16 * kk + 2 * t4 + 1], bh0, bl0);
+      split_xh2(Ps[g][16 * kk + 2 * t4 + 8], Ps[g][16 * kk + 2 * t4 + 9], bh1, bl1);
 #pragma unroll
-    for (int m = 0; m < KT; ++m) {
-      uint32_t ah[4], al[4];
-      ldsm_x4_t(ah, Vh + (16 * kk + vrow) * RS + (16 * m + vcol) * 2);
-      ldsm_x4_t(al, Vl + (16 * kk + vrow) * RS + (16 * m + vcol) * 2);
-      mma_f16_16816(ob[m], ah, bh0, bh1);
-      mma_f16_16816(os[m], ah, bl0, bl1);
-      mma_f16_16816(os[m], al, bh0, bh1);
+      for (int m = 0; m < KT; ++m) {
+        uint32_t ah[4], al[4];
+        ldsm_x4_t(ah, Vh + vrow * RS + (16 * m + vcol) * 2);
+        ldsm_x4_t(al, Vl + vrow * RS + (16 * m + vcol) * 2);
+        mma_f16_16816(ob[m], ah, bh0, bh1);
+        mma_f16_16816(os[m], ah, bl0, bl1);
+        mma_f16_16816(os[m], al, bh0, bh1);
+      }
+      __syncwarp();
+      issue_g(nchunk + kk + NS - 1);
     }
   }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
   // ---- store: lane holds dims {16m + g, +8} x beams {2t4, 2t4+1} ----
 #pragma unroll
   for (int j = 0; j < 2; ++j) {
@@ -1894,14 +1924,9 @@ __global__ void __launch_bounds__(32) cross_attention_xh(
 }
 
 int attention_xh_prepare() {
-  const int sz = 200 * 1024;
+  const int sz = 160 * 1024;  // scores + history of long max_len (static ring <= 26 KB)
 #define FQ_XH_OPT(HD)                                                                           \
-  cudaFuncSetAttribute(cross_attention_xh<HD, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sz) || \
-      cudaFuncSetAttribute(cross_attention_xh<HD, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sz) || \
-      cudaFuncSetAttribute(cross_attention_xh<HD, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, sz) || \
-      cudaFuncSetAttribute(cross_attention_xh<HD, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, sz) || \
-      cudaFuncSetAttribute(cross_attention_xh<HD, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, sz) || \
-      cudaFuncSetAttribute(decoder_self_attention_xh<HD, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, sz)
+  cudaFuncSetAttribute(decoder_self_attention_xh<HD, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, sz)
   if (FQ_XH_OPT(16) || FQ_XH_OPT(32) || FQ_XH_OPT(64) || FQ_XH_OPT(128)) {
     set_error("fq_prepare: cannot opt in to large shared memory (exact attention)");
     return FQ_ERR_CUDA;
@@ -2091,8 +2116,7 @@ int fq_cross_attention_xh(const float* cq, int64_t ldcq, const void* ck, const v
                FQ_ERR_DIMENSION, "fq_cross_attention_xh: unsupported shape");
   const dim3 grid((unsigned)batch, (unsigned)heads);
   const int nt = (int)((seq + 15) / 16);
-  const size_t smem = (size_t)4 * nt * 16 * (head_dim * 2 + 16);
-  FQ_CHECK_ARG(smem <= 200 * 1024, FQ_ERR_CAPACITY, "cross attention: seq too long");
+  const size_t smem = 0;
 #define FQ_CROSS_XH(HD, NT)                                                                   \
   launch_kernel(cross_attention_xh<HD, NT>, grid, 32, smem, as_stream(stream), 1u, cq, ldcq,   \
                 (const h16*)ck, (const h16*)cv, plane, ldkv, (int)beam, (int)seq, scale, mask, \
