@@ -237,6 +237,20 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// 32 columns without the wait (the caller batches several loads per wait::ld).
+__device__ __forceinline__ void tmem_ld32_nowait(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+      "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+        "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]),
+        "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]),
+        "=r"(r[31])
+      : "r"(taddr));
+}
+
 // 16 columns of this warp's 32 TMEM lanes (thread = lane = row).
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
   uint32_t r[16];
@@ -257,15 +271,32 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
 // adds in a fixed order (SC a power of two: exact).
 template <int BN, int OP>
 __device__ __forceinline__ void x3_add_chunk(float (&racc)[BN], uint32_t tb, bool first) {
+  if constexpr (BN % 32 == 0) {  // 32 columns of each accumulator per tcgen05.wait::ld
 #pragma unroll
-  for (int j = 0; j < BN / 16; ++j) {
-    float vb[16], vs[16];
-    tmem_ld16(tb + j * 16, vb);
-    tmem_ld16(tb + BN + j * 16, vs);
+    for (int j = 0; j < BN / 32; ++j) {
+      uint32_t rb[32], rs[32];
+      tmem_ld32_nowait(tb + j * 32, rb);
+      tmem_ld32_nowait(tb + BN + j * 32, rs);
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      const float t = fadd_rn(vb[i], OP == OP_X3H ? vs[i] * small_scale<OP>() : vs[i]);
-      racc[j * 16 + i] = first ? t : fadd_rn(racc[j * 16 + i], t);
+      for (int i = 0; i < 32; ++i) {
+        const float vs = __uint_as_float(rs[i]);
+        const float t = fadd_rn(__uint_as_float(rb[i]),
+                                OP == OP_X3H ? vs * small_scale<OP>() : vs);
+        racc[j * 32 + i] = first ? t : fadd_rn(racc[j * 32 + i], t);
+      }
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < BN / 16; ++j) {
+      float vb[16], vs[16];
+      tmem_ld16(tb + j * 16, vb);
+      tmem_ld16(tb + BN + j * 16, vs);
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const float t = fadd_rn(vb[i], OP == OP_X3H ? vs[i] * small_scale<OP>() : vs[i]);
+        racc[j * 16 + i] = first ? t : fadd_rn(racc[j * 16 + i], t);
+      }
     }
   }
 }
@@ -286,6 +317,7 @@ struct Epi {
   unsigned long long* dbg;  // per-CTA [start, end] %globaltimer (profiling only)
   int tstore;  // 1: C through TMA tensor stores (tma_c: 32-row x 128-byte boxes)
   int b_presplit;  // OP_X3: B arrives as tf32 hi (tma_b) + lo (tma_blo) pairs
+  int chunk_kb;    // OP_X3H: K blocks per TMEM accumulation chunk (0: xchunk)
 };
 
 // HARS stage-1 statistics computed in the logits GEMM's epilogue (the [rows,
@@ -522,7 +554,7 @@ __global__ void __launch_bounds__(threads_of<OP>(), 1)
       constexpr uint32_t idesc = X3 ? idesc_tf32(BM, BN) : idesc_f16(BM, BN);
       int it = 0, local = 0;
       if constexpr (XS) {  // chunks of xchunk K blocks into ping-pong TMEM slots
-        constexpr int CH = xchunk<OP>();
+        const int CH = (XH && ep.chunk_kb > 0) ? ep.chunk_kb : xchunk<OP>();
         int gc = 0;
         for (int g = cluster_id; g < ngroups; g += nclusters) {
           for (int kb0 = 0; kb0 < num_kb; kb0 += CH, ++gc) {
@@ -872,7 +904,8 @@ __global__ void __launch_bounds__(threads_of<OP>(), 1)
         // (the tensor core's own long accumulation is not RN: this bounds it
         // to X3_CH * 32 K elements)
         float racc[BN];
-        for (int kb0 = 0; kb0 < num_kb; kb0 += xchunk<OP>(), ++gc) {
+        const int CH = (XH && ep.chunk_kb > 0) ? ep.chunk_kb : xchunk<OP>();
+        for (int kb0 = 0; kb0 < num_kb; kb0 += CH, ++gc) {
           const int slot = gc & 1;
           mbar_wait(&tfull_bar[slot], (gc >> 1) & 1);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -1064,7 +1097,7 @@ __global__ void __launch_bounds__(threads_of<OP>(), 1)
     if (lane == 0) {  // ---- MMA issuer ----
       constexpr uint32_t idesc = X3 ? idesc_tf32(BM, BN) : idesc_f16(BM, BN);
       if constexpr (XS) {  // chunks of xchunk K blocks into ping-pong TMEM slots
-        constexpr int CH = xchunk<OP>();
+        const int CH = (XH && ep.chunk_kb > 0) ? ep.chunk_kb : xchunk<OP>();
         int it = 0, gc = 0;
         for (int c0 = kb0; c0 < kb1; c0 += CH, ++gc) {
           const int slot = gc & 1;
@@ -1126,7 +1159,8 @@ __global__ void __launch_bounds__(threads_of<OP>(), 1)
 #pragma unroll
       for (int i = 0; i < BN; ++i) racc[i] = 0.0f;
       int gc = 0;
-      for (int c0 = kb0; c0 < kb1; c0 += xchunk<OP>(), ++gc) {
+      const int CH = (XH && ep.chunk_kb > 0) ? ep.chunk_kb : xchunk<OP>();
+      for (int c0 = kb0; c0 < kb1; c0 += CH, ++gc) {
         const int slot = gc & 1;
         mbar_wait(&xfull_bar[slot], (gc >> 1) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -1820,14 +1854,35 @@ static int check_xh(const void* a, const void* a_lo, int64_t lda, const void* b,
   return FQ_OK;
 }
 
+// The exact mode's numerics are fixed by (N, K) alone: K runs in chunks of
+// 256 elements (4 K blocks) — or, for N <= 1024 and K >= 1024, in 4 slices of
+// K/4 — each accumulated in TMEM and added to the fp32 result with RN adds in
+// K order. The kernel is then a free, M-dependent choice with identical bits:
+// the 4-slice shapes run split-K over 4 CTAs (DSMEM reduction, or slabs summed
+// by the consumer) for M <= 1024 (the decode step) and the persistent kernel
+// with slice-long chunks for larger M (the encoder).
+struct XhPlan {
+  int bn, split, chunk_kb;
+};
+
+static XhPlan plan_xh(int64_t M, int64_t N, int64_t K) {
+  const int nkb = (int)((K + 63) / 64);
+  if (N <= 1024 && nkb >= 16) {
+    const int slice = (nkb + 3) / 4;
+    return M <= 1024 ? XhPlan{128, 4, slice} : XhPlan{128, 1, slice};
+  }
+  return XhPlan{N <= 512 ? 64 : 128, 1, 4};
+}
+
 int launch_xh_gemm(const void* a, const void* a_lo, int64_t lda, const void* b,
                    const void* b_lo, int64_t ldb, float* c, int64_t ldc, int64_t M, int64_t N,
                    int64_t K, int accumulate, const float* bias, const float* res, int64_t ldr,
                    int act, cudaStream_t s) {
   int rc = check_xh(a, a_lo, lda, b, b_lo, ldb, M, N, K);
   if (rc != FQ_OK) return rc;
+  const XhPlan p = plan_xh(M, N, K);
   tc::Epi ep{c, ldc, 0, accumulate, bias, res, ldr, act, g_gemm_dbg};
-  const X3Plan p = plan_x3(N, K);
+  ep.chunk_kb = p.chunk_kb;
   if (p.split > 1)
     return tc::launch_splitk<128, 3, false, false, tc::OP_X3H>(a, lda, b, ldb, ep, M, N, K,
                                                                p.split, s, tc::LnEpi{}, b_lo, a_lo);
@@ -1861,11 +1916,12 @@ extern "C" int fq_gemm_x3h_ln(const void* a, const void* a_lo, int64_t lda, cons
                FQ_ERR_DIMENSION, "fq_gemm_x3h_ln: bad args");
   int rc = check_xh(a, a_lo, lda, b, b_lo, ldb, M, N, K);
   if (rc != FQ_OK) return rc;
-  const X3Plan p = plan_x3(N, K);
+  const XhPlan p = plan_xh(M, N, K);
   const int64_t slab_need = (int64_t)p.split * M * N * (int64_t)sizeof(float);
   if (p.split > 1 && ws && ws_bytes >= slab_need && ((uintptr_t)ws & 15) == 0 &&
       (N == 512 || N == 1024)) {
     tc::Epi ep{ws, N, 0, 0, nullptr, nullptr, 0, 0, g_gemm_dbg};
+    ep.chunk_kb = p.chunk_kb;
     rc = tc::launch_splitk<128, 3, false, true, tc::OP_X3H>(a, lda, b, ldb, ep, M, N, K, p.split,
                                                             as_stream(stream), tc::LnEpi{}, b_lo,
                                                             a_lo);
