@@ -214,6 +214,13 @@ int fq_gemm_x3h(const void* a, const void* a_lo, int64_t lda, const void* b, con
                 int accumulate, const float* bias, const float* residual, int64_t ldr, int act,
                 fq_stream_t stream);
 
+/* fq_gemm_x3h whose output act(a . b^T + bias) is written only as the next
+ * exact-mode GEMM's fp16 pair: c = hi, c_lo = lo, both [M, ldc] fp16 (the
+ * FFN1 and cross-K/V projections, whose only consumers read the pair). */
+int fq_gemm_x3h_pair(const void* a, const void* a_lo, int64_t lda, const void* b,
+                     const void* b_lo, int64_t ldb, void* c, void* c_lo, int64_t ldc, int64_t M,
+                     int64_t N, int64_t K, const float* bias, int act, fq_stream_t stream);
+
 /* out = LN(a . b^T + bias + residual) with fq_gemm_x3h operands (the closing
  * GEMM + LN pairs, model.py:339-358 / :582-626); out16 / out16_lo (optional)
  * receive the output's fp16 pair for the next exact-mode GEMM. The 4-slice

@@ -318,6 +318,7 @@ struct Epi {
   int tstore;  // 1: C through TMA tensor stores (tma_c: 32-row x 128-byte boxes)
   int b_presplit;  // OP_X3: B arrives as tf32 hi (tma_b) + lo (tma_blo) pairs
   int chunk_kb;    // OP_X3H: K blocks per TMEM accumulation chunk (0: xchunk)
+  void* c_lo;      // non-null (with c_f16): C is the exact mode's fp16 pair, hi at c, lo here
 };
 
 // HARS stage-1 statistics computed in the logits GEMM's epilogue (the [rows,
@@ -422,7 +423,8 @@ __global__ void __launch_bounds__(threads_of<OP>(), 1)
                    const __grid_constant__ CUtensorMap tma_b, const Epi ep, int M, int N, int K,
                    int cm, int cn, const HarsEpi he, const __grid_constant__ CUtensorMap tma_c,
                    const __grid_constant__ CUtensorMap tma_blo,
-                   const __grid_constant__ CUtensorMap tma_alo) {
+                   const __grid_constant__ CUtensorMap tma_alo,
+                   const __grid_constant__ CUtensorMap tma_clo) {
   static_assert(OP == OP_F16 || !HS, "the HARS epilogue is fp16-only");
   constexpr bool X3 = OP == OP_X3;
   constexpr bool XH = OP == OP_X3H;
@@ -806,11 +808,29 @@ __global__ void __launch_bounds__(threads_of<OP>(), 1)
             for (int j = 0; j < 32; ++j) v[j] = apply_act(v[j], ep.act);
           }
           if (lane == 0) {  // my box area is free again (fp16: the one two chunks back)
-            if (ep.c_f16) asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(1) : "memory");
+            if (ep.c_f16 && !ep.c_lo) asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(1) : "memory");
             else asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(0) : "memory");
           }
           __syncwarp();
-          if (ep.c_f16) {
+          if (ep.c_lo) {  // exact-mode pair: hi box + lo box (32 rows x 64 B each)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              uint4 ph, pl;
+              split_xh2(v[8 * j], v[8 * j + 1], ph.x, pl.x);
+              split_xh2(v[8 * j + 2], v[8 * j + 3], ph.y, pl.y);
+              split_xh2(v[8 * j + 4], v[8 * j + 5], ph.z, pl.z);
+              split_xh2(v[8 * j + 6], v[8 * j + 7], ph.w, pl.w);
+              const int off = lane * 64 + ((j ^ ((lane >> 1) & 3)) << 4);
+              *reinterpret_cast<uint4*>(box + off) = ph;
+              *reinterpret_cast<uint4*>(box + 2048 + off) = pl;
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) {
+              tma_store_2d(&tma_c, box, col0, rbase);
+              tma_store_2d(&tma_clo, box + 2048, col0, rbase);
+            }
+          } else if (ep.c_f16) {
             uint8_t* bx = box + ((cc >> 5) & 1) * 2048;  // 32 rows x 64 B, 64-byte swizzle
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
@@ -884,7 +904,12 @@ __global__ void __launch_bounds__(threads_of<OP>(), 1)
 #pragma unroll
               for (int i = 0; i < 16; ++i) x[i] = fadd_rn(x[i], rv[i]);
             }
-            if (ep.c_f16) {
+            if (ep.c_lo) {
+              h16* c16lo = reinterpret_cast<fq::h16*>(ep.c_lo);
+#pragma unroll
+              for (int i = 0; i < 16; ++i)
+                if (i < nr) split_xh(x[i], c16[c0 + i * ep.ldc], c16lo[c0 + i * ep.ldc]);
+            } else if (ep.c_f16) {
 #pragma unroll
               for (int i = 0; i < 16; ++i)
                 if (i < nr) c16[c0 + i * ep.ldc] = f2h(x[i]);
@@ -1320,6 +1345,9 @@ __global__ void __launch_bounds__(threads_of<OP>(), 1)
         }
         if constexpr (LNF) {  // keep the pre-LN row slice (my own rows of my partial)
           *reinterpret_cast<float4*>(part + lr * PLD + c) = make_float4(x[0], x[1], x[2], x[3]);
+        } else if (ep.c_lo) {  // exact-mode pair output
+          h16* c16lo = reinterpret_cast<fq::h16*>(ep.c_lo);
+          for (int j = 0; j < 4 && col + j < N; ++j) split_xh(x[j], c16[ci + j], c16lo[ci + j]);
         } else if (col + 3 < N && ((ci & 3) == 0)) {
           if (ep.c_f16) {
             h16x2 lo = __floats2half2_rn(x[0], x[1]), hi = __floats2half2_rn(x[2], x[3]);
@@ -1573,9 +1601,12 @@ static int launch(const void* a, int64_t lda, const void* b, int64_t ldb, const 
   if (e2.b_presplit && (rc = make_map(&mblo, b_lo, N, K, ldb, BN / cm, X3)) != FQ_OK) return rc;
   if (XH && (rc = make_map(&malo, a_lo, M, K, lda, BM / cn, false)) != FQ_OK) return rc;
   mc = ma;
+  CUtensorMap mclo = ma;
   if (!HS && ep.c && !ep.accumulate && !ep.res && N % 32 == 0 && tma_store_enabled() &&
       ((uintptr_t)ep.c & 15) == 0 && (ep.ldc * (ep.c_f16 ? 2 : 4)) % 16 == 0 &&
-      make_map_c(&mc, ep.c, M, N, ep.ldc, ep.c_f16 != 0) == FQ_OK)
+      (!ep.c_lo || ((uintptr_t)ep.c_lo & 15) == 0) &&
+      make_map_c(&mc, ep.c, M, N, ep.ldc, ep.c_f16 != 0) == FQ_OK &&
+      (!ep.c_lo || make_map_c(&mclo, ep.c_lo, M, N, ep.ldc, true) == FQ_OK))
     e2.tstore = 1;
   const int csize = cm * cn;
   const int64_t groups = ((M + BM - 1) / BM / cm) * ((N + BN - 1) / BN / cn);
@@ -1584,7 +1615,7 @@ static int launch(const void* a, int64_t lda, const void* b, int64_t ldb, const 
   cudaError_t e = launch_kernel(tc_gemm_kernel<BN, STAGES, HS, OP>,
                                 dim3((unsigned)(clusters * csize)), dim3(threads_of<OP>()),
                                 smem_bytes<BN, STAGES, HS, OP>(), s, (unsigned)csize, ma, mb, e2,
-                                (int)M, (int)N, (int)K, cm, cn, he, mc, mblo, malo);
+                                (int)M, (int)N, (int)K, cm, cn, he, mc, mblo, malo, mclo);
   if (e != cudaSuccess) {
     set_error("fq_gemm(tcgen05): launch failed: %s", cudaGetErrorString(e));
     return FQ_ERR_CUDA;
@@ -1904,6 +1935,33 @@ extern "C" int fq_gemm_x3h(const void* a, const void* a_lo, int64_t lda, const v
   if (M == 0 || N == 0) return FQ_OK;
   return launch_xh_gemm(a, a_lo, lda, b, b_lo, ldb, c, ldc, M, N, K, accumulate, bias, residual,
                         ldr, act, as_stream(stream));
+}
+
+// The exact-mode GEMM whose output is written only as the next GEMM's fp16
+// pair (c = hi, c_lo = lo, both [M, ldc]): the FFN1 / cross-K/V producers.
+extern "C" int fq_gemm_x3h_pair(const void* a, const void* a_lo, int64_t lda, const void* b,
+                                const void* b_lo, int64_t ldb, void* c, void* c_lo, int64_t ldc,
+                                int64_t M, int64_t N, int64_t K, const float* bias, int act,
+                                fq_stream_t stream) {
+  FQ_CHECK_ARG(c && c_lo && M >= 0 && N >= 0 && K >= 1, FQ_ERR_DIMENSION,
+               "fq_gemm_x3h_pair: bad args");
+  FQ_CHECK_ARG(act >= 0 && act <= 2, FQ_ERR_PARAMETER, "fq_gemm_x3h_pair: unknown activation");
+  if (M == 0 || N == 0) return FQ_OK;
+  int rc = check_xh(a, a_lo, lda, b, b_lo, ldb, M, N, K);
+  if (rc != FQ_OK) return rc;
+  const XhPlan p = plan_xh(M, N, K);
+  tc::Epi ep{c, ldc, 1, 0, bias, nullptr, 0, act, g_gemm_dbg};
+  ep.chunk_kb = p.chunk_kb;
+  ep.c_lo = c_lo;
+  cudaStream_t s = as_stream(stream);
+  if (p.split > 1)
+    return tc::launch_splitk<128, 3, false, false, tc::OP_X3H>(a, lda, b, ldb, ep, M, N, K,
+                                                               p.split, s, tc::LnEpi{}, b_lo, a_lo);
+  if (p.bn == 64)
+    return tc::launch<64, 4, false, tc::OP_X3H>(a, lda, b, ldb, ep, M, N, K, 1, 1, s,
+                                                tc::HarsEpi{}, b_lo, a_lo);
+  return tc::launch<128, 3, false, tc::OP_X3H>(a, lda, b, ldb, ep, M, N, K, 1, 1, s,
+                                               tc::HarsEpi{}, b_lo, a_lo);
 }
 
 extern "C" int fq_gemm_x3h_ln(const void* a, const void* a_lo, int64_t lda, const void* b,

@@ -35,8 +35,8 @@ from . import _abi
 from .errors import CapacityError, ConsistencyError, DimensionError, FullMaskError, InputError
 from .memory_plan import Arena, IntermediateSpec
 from .ops import attention_scale
-from .tensor import (OpCounters, Timers, as_device, gemm, gemm_x3, gemm_xh, global_counters,
-                     split_pair)
+from .tensor import (ACT_IDS, OpCounters, Timers, as_device, gemm, gemm_x3, gemm_xh,
+                     global_counters, split_pair)
 
 F32 = np.float32
 I64 = np.int64
@@ -442,6 +442,19 @@ def _lin(dw: DeviceWeights, a32, a16, w, out, *, bias=None, residual=None, act="
                 timers=timers)
 
 
+def _lin_pair(a16, w, pair, *, bias=None, act="none", counters=None):
+    """Exact mode: a 3xFP16 GEMM whose output act(a . w^T + bias) is written
+    only as the next GEMM's fp16 pair (fq_gemm_x3h_pair)."""
+    hi, lo = a16
+    ohi, olo = pair
+    M, K = hi.shape
+    N = w.shape[0]
+    _abi.call("fq_gemm_x3h_pair", hi.data_ptr(), lo.data_ptr(), hi.stride(0), w.hi.data_ptr(),
+              w.lo.data_ptr(), w.hi.stride(0), ohi.data_ptr(), olo.data_ptr(), ohi.stride(0), M,
+              N, K, _abi.ptr(bias), ACT_IDS[act], _abi.stream_handle())
+    (counters or global_counters()).count_gemm(hi.numel() * 4 + N * K * 4 + M * N * 4)
+
+
 def _ln(x, g, b, eps, out, out16, residual=None, bias=None, counters=None):
     stream = _abi.stream_handle()
     rows, d = x.shape
@@ -581,13 +594,16 @@ def encoder_layer_forward(x, layer, config: ModelConfig, mask=None, batch: int =
     norm1 = bufs.get(f"{prefix}.norm1", (n, d))
     norm1_16 = half_operand(bufs, f"{prefix}.norm1_16", (n, d), dw_half)
     _ln(res1, layer["ln1_g"], layer["ln1_b"], config.ln_eps, norm1, norm1_16, counters=ctr)
-    ffn_h = bufs.get(f"{prefix}.ffn_h", (n, ff), act16)
-    _lin(_P, norm1, norm1_16, layer["w_ff1"], ffn_h, bias=layer["b_ff1"], act=config.activation,
-         counters=ctr, timers=timers)
-    ffn_h16 = ffn_h
-    if not dw_half:
+    if dw_half:
+        ffn_h = bufs.get(f"{prefix}.ffn_h", (n, ff), act16)
+        _lin(_P, norm1, norm1_16, layer["w_ff1"], ffn_h, bias=layer["b_ff1"],
+             act=config.activation, counters=ctr, timers=timers)
+        ffn_h16 = ffn_h
+    else:  # exact mode: FFN1 writes the pair FFN2 reads, nothing else
+        ffn_h = None
         ffn_h16 = half_operand(bufs, f"{prefix}.ffn_h16", (n, ff), False)
-        fill_pair(ffn_h, ffn_h16)
+        _lin_pair(norm1_16, layer["w_ff1"], ffn_h16, bias=layer["b_ff1"], act=config.activation,
+                  counters=ctr)
     u = bufs.get(f"{prefix}.ffn_out", (n, d))
     _lin(_P, ffn_h, ffn_h16, layer["w_ff2"], u, bias=layer["b_ff2"], residual=norm1, counters=ctr,
          timers=timers)
@@ -729,16 +745,16 @@ def build_cross_kv(memory, weights, config: ModelConfig, batch: int, seq: int, *
     bufs = buffers if buffers is not None else HeapBuffers()
     M = as_device(memory, torch.float32)
     n, d, L = batch * seq, config.d_model, config.num_decoder_layers
-    packed = bufs.get("dec.cross_kv", (n, 2 * L * d), dw.act_dtype)
-    if dw.half and memory16 is None:
-        memory16 = M.to(torch.float16)
-    if not dw.half and memory16 is None:
-        memory16 = split_pair(M)
-    _lin(dw, M, memory16, dw.w_ckv, packed, bias=dw.b_ckv, counters=counters, timers=timers)
     if not dw.half:  # exact mode: the fp16 pair planes [2, n, 2*L*d] the attention reads
+        if memory16 is None:
+            memory16 = split_pair(M)
         pair = bufs.get("dec.cross_kv16", (2, n, 2 * L * d), torch.float16)
-        split_pair(packed, (pair[0], pair[1]))
+        _lin_pair(memory16, dw.w_ckv, (pair[0], pair[1]), bias=dw.b_ckv, counters=counters)
         return pair
+    packed = bufs.get("dec.cross_kv", (n, 2 * L * d), dw.act_dtype)
+    if memory16 is None:
+        memory16 = M.to(torch.float16)
+    _lin(dw, M, memory16, dw.w_ckv, packed, bias=dw.b_ckv, counters=counters, timers=timers)
     return packed
 
 
@@ -842,9 +858,8 @@ class DecoderStep:
         _lin_ln(dw, self.cctx, self.cctx16, lw["w_co"], lw["b_co"], self.snorm, lw["ln2_g"],
                 lw["ln2_b"], c.ln_eps, self.cnorm, self.cnorm16, self.ln_ws, counters=ctr,
                 timers=tm)
-        _lin(dw, self.cnorm, self.cnorm16, lw["w_ff1"], self.ffn_h, bias=lw["b_ff1"],
-             act=c.activation, counters=ctr, timers=tm)
-        fill_pair(self.ffn_h, self.ffn_h16)
+        _lin_pair(self.cnorm16, lw["w_ff1"], self.ffn_h16, bias=lw["b_ff1"], act=c.activation,
+                  counters=ctr)
         _lin_ln(dw, self.ffn_h, self.ffn_h16, lw["w_ff2"], lw["b_ff2"], self.cnorm, lw["ln3_g"],
                 lw["ln3_b"], c.ln_eps, self.x, self.x16, self.ln_ws, counters=ctr, timers=tm)
 
@@ -1022,8 +1037,9 @@ def plan_intermediates(config: ModelConfig, precision: str = "fp32") -> list[Int
         add(f"enc.l{i}.res1", n * d * 4, b0 + 2, b0 + 3)
         add(f"enc.l{i}.norm1", n * d * 4, b0 + 3, b0 + 5)
         add(f"enc.l{i}.norm1_16", n * d * h, b0 + 3, b0 + 4)
-        add(f"enc.l{i}.ffn_h", n * ff * a, b0 + 4, b0 + 5)
-        if not bf:
+        if bf:
+            add(f"enc.l{i}.ffn_h", n * ff * a, b0 + 4, b0 + 5)
+        else:
             add(f"enc.l{i}.ffn_h16", n * ff * h, b0 + 4, b0 + 5)
         add(f"enc.l{i}.ffn_out", n * d * 4, b0 + 5, b0 + 6)
         last = setup if i == L - 1 else b0 + 8 + 2
@@ -1032,8 +1048,7 @@ def plan_intermediates(config: ModelConfig, precision: str = "fp32") -> list[Int
     if D:
         if bf:
             add("dec.cross_kv", n * 2 * D * d * 2, setup, end)
-        else:  # exact mode: fp32 GEMM output, then its fp16 pair planes for the attention
-            add("dec.cross_kv", n * 2 * D * d * 4, setup, setup)
+        else:  # exact mode: the GEMM writes the fp16 pair planes the attention reads
             add("dec.cross_kv16", n * 2 * D * d * 4, setup, end)
         kv = 2 if bf else 4
         for i in range(D):
