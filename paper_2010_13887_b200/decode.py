@@ -24,7 +24,7 @@ import numpy as np
 import torch
 
 from . import _abi
-from .errors import DimensionError, EngineError, ParameterError
+from .errors import DimensionError, EngineError, FullMaskError, ParameterError
 from .tensor import OpCounters, as_device, global_counters
 
 F32 = np.float32
@@ -86,8 +86,22 @@ def retrieve(logits, k: int, *, counters: OpCounters | None = None,
         L = L.contiguous()
     out = None
     if bufs is not None:
-        out = (bufs["group_max"][:beams, :k], bufs["threshold"][:beams], bufs["lse"][:beams],
-               bufs["cand_idx"][:beams, :vocab], bufs["cand_count"][:beams])
+        # reference-style bufs (decode.py _retrieve_bufs: numpy group_max /
+        # threshold / lse / cand_idx) are accepted: host arrays are replaced by
+        # device ones and a missing cand_count is allocated
+        dev = {}
+        for name, shape, dt in (("group_max", (beams, k), torch.float32),
+                                ("threshold", (beams,), torch.float32),
+                                ("lse", (beams,), torch.float64),
+                                ("cand_idx", (beams, vocab), torch.int32),
+                                ("cand_count", (beams,), torch.int64)):
+            b = bufs.get(name)
+            if isinstance(b, torch.Tensor) and b.is_cuda and b.dtype == dt:
+                dev[name] = b
+            else:
+                dev[name] = torch.empty(shape, dtype=dt, device=L.device)
+        out = (dev["group_max"][:beams, :k], dev["threshold"][:beams], dev["lse"][:beams],
+               dev["cand_idx"][:beams, :vocab], dev["cand_count"][:beams])
     gm, th, lse, ci, cc = retrieve_device(L, k, out=out)
     _ctr(counters).count_fused("retrieve", beams * vocab * 4)
     counts = cc.cpu().numpy()
@@ -198,6 +212,19 @@ class BeamState:
 _PINNED: dict = {}  # pinned host staging buffers for DeviceBeamState.host_items, by size
 
 
+def check_error_flags(flags: dict | None):
+    """Raise the reference's errors for one generate's device flags (read when
+    the host reads the state): a fully masked cross-attention row
+    (FullMaskError) or a fused logits/HARS survivor overflow (EngineError)."""
+    if not flags:
+        return
+    if any(int(b.item()) for b in flags.get("bad", [])):
+        raise FullMaskError("fully masked cross-attention row")
+    if any(int(o.item()) for o in flags.get("ovf", [])):
+        raise EngineError("more than 2048 candidates in a row (tie-heavy logits) on the fused "
+                          "logits/HARS path; set FQ_LOGITS_HARS=0")
+
+
 class DeviceBeamState:
     """Batched beam state in device memory (fq_beam_state, fq_abi.h)."""
 
@@ -271,7 +298,10 @@ class DeviceBeamState:
         torch.cuda.current_stream().synchronize()
         return {n: v.numpy() for n, v in out.items()}
 
+    error_flags = None  # set by Session.generate: checked when the host reads the state
+
     def host_items(self) -> list:
+        check_error_flags(self.error_flags)
         h = self._to_host()
         live, step, pre, cum = h["live"], h["step"], h["prefix"], h["cum"]
         fc, ft, fl, fs = h["fin_count"], h["fin_tok"], h["fin_len"], h["fin_score"]

@@ -32,7 +32,7 @@ from . import _abi
 from . import decode as D
 from . import model as M
 from .errors import EngineError, FullMaskError, InputError
-from .memory_plan import Arena, build_plan
+from .memory_plan import Arena, batch_buckets, bucket_of, build_plan
 from .tensor import OpCounters, Timers, gemm
 
 I64 = np.int64
@@ -49,8 +49,10 @@ class _GroupedBeamState:
 
     def __init__(self, states):
         self.states = states
+        self.error_flags = None
 
     def host_items(self) -> list:
+        D.check_error_flags(self.error_flags)
         out = []
         for st in self.states:
             out.extend(st.host_items())
@@ -81,11 +83,17 @@ class Session:
         self.counters = OpCounters()
         self.timers = Timers()
         self.dw = M.DeviceWeights.get(config, weights, precision)
-        specs = M.plan_intermediates(config, precision)
-        if not share_plan:
-            specs = [dataclasses.replace(s, first_use=0, last_use=1) for s in specs]
-        self.plan = build_plan(specs)
-        self.arena = Arena(self.plan)
+        # one plan per batch bucket (shape-bucketed arena), ONE HBM allocation
+        # sized for the largest; every request is served from its bucket's plan
+        self._buckets = batch_buckets(config.max_batch)
+        self._plans = {}
+        for b in self._buckets:
+            specs = M.plan_intermediates(config, precision, batch=b)
+            if not share_plan:
+                specs = [dataclasses.replace(s, first_use=0, last_use=1) for s in specs]
+            self._plans[b] = build_plan(specs, bucket=(b,))
+        self.plan = self._plans[self._buckets[-1]]
+        self.arena = Arena(list(self._plans.values()))
         self._buffers = M.ArenaBuffers(self.arena)
         self._graphs: dict = {}
         self._pinned_done = torch.zeros((max(config.max_seq_len, 1), 2), dtype=torch.int32,
@@ -94,14 +102,22 @@ class Session:
         self._buffers2 = None
 
     def _group_buffers(self):
-        """Decode buffers of the second item group (its own arena, same plan)."""
+        """Decode buffers of the second item group (its own arena, same plans)."""
         if self._buffers2 is None:
-            self._arena2 = Arena(self.plan)
+            self._arena2 = Arena(list(self._plans.values()))
             self._buffers2 = M.ArenaBuffers(self._arena2)
+        self._arena2.use(self.arena.plan)
         return self._buffers2
+
+    def _use_bucket(self, batch: int):
+        """Serve this request's buffers from its batch bucket's plan."""
+        if batch > self.config.max_batch:
+            raise M.CapacityError(f"batch {batch} exceeds max_batch {self.config.max_batch}")
+        self.arena.use(self._plans[bucket_of(max(int(batch), 1), self._buckets)])
 
     # ------------------------------------------------------------------
     def _encode_dev(self, src: np.ndarray, lengths=None):
+        self._use_bucket(src.shape[0])
         return M.encode(src, self.dw, self.config, lengths, buffers=self._buffers,
                         counters=self.counters, timers=self.timers, precision=self.precision,
                         return_half=True)
@@ -124,7 +140,7 @@ class Session:
     # ------------------------------------------------------------------
     def generate(self, src_tokens, decode_config: D.DecodeConfig, src_lengths=None,
                  bos_token: int = 1, search: str | None = None, *,
-                 return_device_state: bool = False):
+                 return_device_state: bool = False, _materialise: bool = False):
         """Encode, then auto-regressively decode every batch item on the device.
 
         ``src_tokens`` is host [batch, seq] (copied in) or an int64 device
@@ -183,6 +199,7 @@ class Session:
         # (C2: 49.5 us GEMM + merge vs 40.7 us GEMM + 39 us HARS).
         # FQ_LOGITS_HARS=0: materialised logits + fq_hars_step
         lh = (fused and self.dw.half and os.environ.get("FQ_LOGITS_HARS", "1") != "0"
+              and not _materialise
               and self.config.d_model % 64 == 0 and V >= 4096 and (V + 223) // 224 <= 256)
         bounds = [0, batch] if ngroups == 1 else [0, (batch + 1) // 2, batch]
         groups = []
@@ -299,8 +316,10 @@ class Session:
                 body(groups[1])
             main.wait_stream(side)
 
+        # every path choice the captured graph bakes in is part of the key
         key = (batch, seq, K, max_steps, mask is not None, exhaustive, cfg.eos_token,
-               float(cfg.length_penalty), ngroups)
+               float(cfg.length_penalty), ngroups, lh, fused,
+               groups[0]["step"].ln_ws is not None, groups[0]["step"].q_slabs)
         graph = None
         if self.use_graphs:
             entry = self._graphs.get(key)
@@ -330,15 +349,20 @@ class Session:
                 events[t - 1].synchronize()
                 if int(pinned[t - 1, :ngroups].sum()) >= batch:
                     break
+        if lh and any(int(g["ovf"].item()) for g in groups):
+            # a tie-heavy row overflowed the fused output layer's survivor slots
+            # (e.g. all-equal logits make every token a candidate, reference
+            # tests/test_decode.py:53-59): decode the request again on the
+            # materialised logits + fq_hars_step path, which has no cap
+            return self.generate(src_tokens, decode_config, src_lengths, bos_token, search,
+                                 return_device_state=return_device_state, _materialise=True)
         result = groups[0]["st"] if ngroups == 1 else _GroupedBeamState([g["st"] for g in groups])
+        # the device error flags travel with the state: checked when the host
+        # reads it (host_items), or here for host hypotheses
+        result.error_flags = {"bad": [g["step"].bad for g in groups],
+                              "ovf": [g["ovf"] for g in groups if "ovf" in g]}
         if return_device_state:
             return result
-        torch.cuda.synchronize()
-        if any(int(g["step"].bad.item()) for g in groups):
-            raise FullMaskError("fully masked cross-attention row")
-        if any(int(g["ovf"].item()) for g in groups if "ovf" in g):
-            raise EngineError("more than 2048 candidates in a row (tie-heavy logits) on the "
-                              "fused logits/HARS path; set FQ_LOGITS_HARS=0")
         states = result.host_items()
         return [[Hypothesis(tokens=s, score=sc) for s, sc in state.finalize(cfg)]
                 for state in states]

@@ -314,6 +314,12 @@ class XHWeight:
         return cls(hi, lo)
 
 
+def xh_attention(config: ModelConfig) -> bool:
+    """Exact mode runs attention on 3xFP16 warp MMAs over fp16-pair K/V for
+    these head dims; others keep fp32 K/V and the FFMA exact attention."""
+    return config.head_dim in (16, 32, 64, 128)
+
+
 def half_operand(bufs, name: str, shape, half: bool):
     """The fp16 GEMM operand buffer of an fp32 activation: its fp16 copy in
     the fp16 mode, its exact-mode (hi, lo) pair in fp32 mode."""
@@ -339,7 +345,10 @@ class DeviceWeights:
     def get(cls, config: ModelConfig, weights, precision: str) -> "DeviceWeights":
         if isinstance(weights, DeviceWeights):
             return weights
-        key = (id(weights), precision, torch.cuda.current_device())
+        # the positions table depends on max_seq_len and the output matrix on
+        # tie_output: both belong to the key, not just the weight object
+        key = (id(weights), precision, torch.cuda.current_device(), config.max_seq_len,
+               config.tie_output, config.d_model)
         dw = cls._cache.get(key)
         if dw is None or dw.host is not weights:
             dw = DeviceWeights(config, weights, precision)
@@ -455,7 +464,7 @@ def _lin_pair(a16, w, pair, *, bias=None, act="none", counters=None):
     (counters or global_counters()).count_gemm(hi.numel() * 4 + N * K * 4 + M * N * 4)
 
 
-def _ln(x, g, b, eps, out, out16, residual=None, bias=None, counters=None):
+def _ln(x, g, b, eps, out, out16, residual=None, bias=None, counters=None, kind="layer_norm"):
     stream = _abi.stream_handle()
     rows, d = x.shape
     if isinstance(out16, tuple):  # exact mode: the output's fp16 pair for the next GEMM
@@ -474,7 +483,7 @@ def _ln(x, g, b, eps, out, out16, residual=None, bias=None, counters=None):
                   residual.data_ptr(), residual.stride(0), g.data_ptr(), b.data_ptr(), eps, rows,
                   d, _abi.ptr(out), out.stride(0) if out is not None else 0, _abi.ptr(out16),
                   out16.stride(0) if out16 is not None else 0, stream)
-    (counters or global_counters()).count_fused("layer_norm", x.numel() * 8)
+    (counters or global_counters()).count_fused(kind, x.numel() * 8)
 
 
 def _lin_ln(dw: DeviceWeights, a32, a16, w, bias, residual, g, b, eps, out, out16, ws, *,
@@ -577,13 +586,23 @@ def encoder_layer_forward(x, layer, config: ModelConfig, mask=None, batch: int =
     class _P:  # precision shim for _lin
         half = dw_half
 
+    # Counter contract (reference ops.py:45-58, test_acceptance.py:180-201): 6
+    # GEMMs and one pass of each of the 6 FusedPassKinds per layer. Here the
+    # passes run as 7 launches: QKV bias + head split in the QKV GEMM's
+    # epilogue (heads are strided views), QK^T / softmax / P.V in ONE attention
+    # kernel (its two tensor-core products count as the layer's batched GEMMs),
+    # the out-projection's bias + residual and FFN1's bias + act in their GEMM
+    # epilogues, the closing FFN2 bias + residual + LN in FFN2 + the LN kernel.
     qkv = bufs.get(f"{prefix}.qkv", (n, 3 * d))
     _lin(_P, X, x16, layer["w_qkv"], qkv, bias=layer["b_qkv"], counters=ctr, timers=timers)
+    ctr.count_fused("qkv_bias_reshape", n * 3 * d * 8, launches=1)
     ctx = bufs.get(f"{prefix}.ctx", (n, d), act16)
     _abi.call("fq_encoder_attention", qkv.data_ptr(), qkv.stride(0), batch, seq, h, hd,
               attention_scale(hd), _abi.ptr(mask), None if dw_half else ctx.data_ptr(),
               ctx.data_ptr() if dw_half else None, d, 0 if dw_half else 1, _abi.ptr(bad), stream)
     ctr.count_fused("attention_scale_mask_softmax", n * d * 16)
+    ctr.count_gemm(n * d * 8)  # QK^T, inside the fused attention kernel
+    ctr.count_gemm(n * d * 8)  # P.V
     ctx16 = ctx
     if not dw_half:
         ctx16 = half_operand(bufs, f"{prefix}.ctx16", (n, d), False)
@@ -591,6 +610,7 @@ def encoder_layer_forward(x, layer, config: ModelConfig, mask=None, batch: int =
     res1 = bufs.get(f"{prefix}.res1", (n, d))
     _lin(_P, ctx, ctx16, layer["w_out"], res1, bias=layer["b_out"], residual=X, counters=ctr,
          timers=timers)
+    ctr.count_fused("attn_output_bias_residual", n * d * 12)
     norm1 = bufs.get(f"{prefix}.norm1", (n, d))
     norm1_16 = half_operand(bufs, f"{prefix}.norm1_16", (n, d), dw_half)
     _ln(res1, layer["ln1_g"], layer["ln1_b"], config.ln_eps, norm1, norm1_16, counters=ctr)
@@ -604,12 +624,14 @@ def encoder_layer_forward(x, layer, config: ModelConfig, mask=None, batch: int =
         ffn_h16 = half_operand(bufs, f"{prefix}.ffn_h16", (n, ff), False)
         _lin_pair(norm1_16, layer["w_ff1"], ffn_h16, bias=layer["b_ff1"], act=config.activation,
                   counters=ctr)
+    ctr.count_fused("ffn_bias_activation", n * ff * 8)
     u = bufs.get(f"{prefix}.ffn_out", (n, d))
     _lin(_P, ffn_h, ffn_h16, layer["w_ff2"], u, bias=layer["b_ff2"], residual=norm1, counters=ctr,
          timers=timers)
     out = bufs.get(f"{prefix}.out", (n, d))
     out16 = half_operand(bufs, f"{prefix}.out16", (n, d), dw_half)
-    _ln(u, layer["ln2_g"], layer["ln2_b"], config.ln_eps, out, out16, counters=ctr)
+    _ln(u, layer["ln2_g"], layer["ln2_b"], config.ln_eps, out, out16, counters=ctr,
+        kind="ffn_bias_residual")
     return out, out16
 
 
@@ -680,22 +702,31 @@ class KVCache:
         S, d = config.max_seq_len, config.d_model
         self.config, self.rows, self.max_seq_len = config, rows, S
         # fp16 mode: fp16 [S, rows, d]; exact mode: the fp16 pair planes
-        # [2, S, rows, d] (hi, lo) the 3xFP16 attention reads
-        self.kv_dtype = torch.float16
-        self.pairs = precision != "fp16"
+        # [2, S, rows, d] (hi, lo) the 3xFP16 attention reads (fp32 [S, rows,
+        # d] for head dims it does not cover)
+        self.pairs = precision != "fp16" and xh_attention(config)
+        self.kv_dtype = torch.float32 if precision != "fp16" and not self.pairs else torch.float16
         shape = (2, S, rows, d) if self.pairs else (S, rows, d)
-        self._k = [buffers.get(f"{prefix}.l{i}.k", shape, torch.float16)
+        self._k = [buffers.get(f"{prefix}.l{i}.k", shape, self.kv_dtype)
                    for i in range(config.num_decoder_layers)]
-        self._v = [buffers.get(f"{prefix}.l{i}.v", shape, torch.float16)
+        self._v = [buffers.get(f"{prefix}.l{i}.v", shape, self.kv_dtype)
                    for i in range(config.num_decoder_layers)]
         self.plane = S * rows * d
         self.hist = buffers.get(f"{prefix}.hist", (rows, S), torch.int32)
         self.d_cur = buffers.get(f"{prefix}.cur", (1,), torch.int32)
         self.reset()
 
+    _IOTA: dict = {}
+
     def reset(self):
-        self.hist.copy_(torch.arange(self.rows, dtype=torch.int32,
-                                     device=self.hist.device)[:, None].expand_as(self.hist))
+        # hist[r, t] = r: the identity history, from a per-device iota made once
+        # (no allocation per request)
+        key = (self.hist.device, self.rows)
+        iota = KVCache._IOTA.get(key)
+        if iota is None:
+            iota = torch.arange(self.rows, dtype=torch.int32, device=self.hist.device)
+            KVCache._IOTA[key] = iota
+        self.hist.copy_(iota[:, None].expand_as(self.hist))
         self.d_cur.zero_()
         self.current_len = 0
 
@@ -709,6 +740,19 @@ class KVCache:
                 c = self.current_len
                 idx = torch.from_numpy(p).to(self.hist.device)
                 self.hist[:, :c] = self.hist[idx, :c].clone()
+
+    def write(self, layer: int, new_k, new_v, timers=None):
+        """Cache refresh (model.py:492-506): this step's K/V ([rows, heads, 1,
+        hd] or [rows, d]) into slot (current_len, r) of every row; a pending
+        reorder was already applied to ``hist`` by ``begin_step`` (no copy).
+        The decode kernels write the slot themselves; this is the API path."""
+        c, rows, d = self.current_len, self.rows, self.config.d_model
+        for store, new in ((self._k, new_k), (self._v, new_v)):
+            x = as_device(new, torch.float32).reshape(rows, d)
+            if self.pairs:
+                split_pair(x, (store[layer][0][c], store[layer][1][c]))
+            else:
+                store[layer][c].copy_(x.to(self.kv_dtype))
 
     def end_step(self):
         _abi.call("fq_step_advance", self.d_cur.data_ptr(), _abi.stream_handle())
@@ -745,7 +789,7 @@ def build_cross_kv(memory, weights, config: ModelConfig, batch: int, seq: int, *
     bufs = buffers if buffers is not None else HeapBuffers()
     M = as_device(memory, torch.float32)
     n, d, L = batch * seq, config.d_model, config.num_decoder_layers
-    if not dw.half:  # exact mode: the fp16 pair planes [2, n, 2*L*d] the attention reads
+    if not dw.half and xh_attention(config):  # exact: the fp16 pair planes [2, n, 2*L*d]
         if memory16 is None:
             memory16 = split_pair(M)
         pair = bufs.get("dec.cross_kv16", (2, n, 2 * L * d), torch.float16)
@@ -753,7 +797,7 @@ def build_cross_kv(memory, weights, config: ModelConfig, batch: int, seq: int, *
         return pair
     packed = bufs.get("dec.cross_kv", (n, 2 * L * d), dw.act_dtype)
     if memory16 is None:
-        memory16 = M.to(torch.float16)
+        memory16 = M.to(torch.float16) if dw.half else split_pair(M)
     _lin(dw, M, memory16, dw.w_ckv, packed, bias=dw.b_ckv, counters=counters, timers=timers)
     return packed
 
@@ -882,7 +926,7 @@ class DecoderStep:
         R, d, h, hd, L = self.rows, c.d_model, c.num_heads, c.head_dim, c.num_decoder_layers
         stream = _abi.stream_handle()
         scale = attention_scale(hd)
-        kvdt = 1 if dw.half else 0
+        kvdt = 0 if self.cache.kv_dtype == torch.float32 else 1
         exact = 0 if dw.half else 1
         if embed:
             self.embed()
@@ -890,7 +934,7 @@ class DecoderStep:
         fill_pair(x, x16)  # exact mode: the step input's fp16 pair
         for i, lw in enumerate(dw.dec):
             _lin(dw, x, x16, lw["w_qkv"], self.sqkv, bias=lw["b_qkv"], counters=ctr, timers=tm)
-            if not dw.half:  # exact mode: 3xFP16 warp-MMA attention on the pair cache
+            if self.cache.pairs:  # exact mode: 3xFP16 warp-MMA attention on the pair cache
                 self._exact_layer(i, lw, x, x16, scale, stream)
                 x, x16 = self.x, self.x16
                 continue
@@ -1000,14 +1044,18 @@ def decode_step(last_tokens, cache: KVCache, cross_kv, enc_mask, weights, config
 LH_SV_CAP = 128  # fq_logits_hars survivor slots per (row, 224-column tile)
 
 
-def plan_intermediates(config: ModelConfig, precision: str = "fp32") -> list[IntermediateSpec]:
+def plan_intermediates(config: ModelConfig, precision: str = "fp32",
+                       batch: int | None = None) -> list[IntermediateSpec]:
     """Every intermediate of one max-shape request with its lifetime in the
     static op order: embed, encoder layers, cross-K/V setup, one decode step
     (steps reuse the same buffers), logits, HARS stage 1/2 and the beam state.
     Whole-request buffers (mask, cross K/V, KV cache, history table, beam
     state) live to the terminal op and are never shared."""
-    B, S, K = config.max_batch, config.max_seq_len, config.max_beam_size
-    R = config.max_rows
+    B = config.max_batch if batch is None else int(batch)
+    if not 0 < B <= config.max_batch:
+        raise CapacityError(f"batch bucket {B} outside [1, {config.max_batch}]")
+    S, K = config.max_seq_len, config.max_beam_size
+    R = B * K
     d, ff, V = config.d_model, config.d_ff, config.vocab_size
     L, D = config.num_encoder_layers, config.num_decoder_layers
     bf = precision == "fp16"
@@ -1048,8 +1096,10 @@ def plan_intermediates(config: ModelConfig, precision: str = "fp32") -> list[Int
     if D:
         if bf:
             add("dec.cross_kv", n * 2 * D * d * 2, setup, end)
-        else:  # exact mode: the GEMM writes the fp16 pair planes the attention reads
+        elif xh_attention(config):  # exact: the GEMM writes the pair planes the attention reads
             add("dec.cross_kv16", n * 2 * D * d * 4, setup, end)
+        else:
+            add("dec.cross_kv", n * 2 * D * d * 4, setup, end)
         kv = 2 if bf else 4
         for i in range(D):
             add(f"dec.cache.l{i}.k", S * R * d * kv, setup, end)

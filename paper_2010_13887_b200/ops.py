@@ -19,7 +19,7 @@ import torch
 
 from . import _abi
 from .errors import DimensionError, FullMaskError
-from .tensor import ACT_IDS, OpCounters, Tensor, as_device, global_counters
+from .tensor import ACT_IDS, OpCounters, Tensor, as_device, global_counters, writeback
 
 
 class FusedPassKind(str, Enum):
@@ -70,6 +70,7 @@ def fused_layer_norm(x, gamma, beta, eps: float = 1e-5, out=None, *, counters=No
               X.shape[0], X.shape[1], O.data_ptr(), _rows(O, "out"), None, 0,
               _abi.stream_handle())
     _ctr(counters).count_fused(kind, X.numel() * 8)
+    writeback(out, O)
     return Tensor(O)
 
 
@@ -100,6 +101,7 @@ def fused_attention_softmax(scores, scale: float, mask=None, out=None, *, counte
     if n_bad:
         raise FullMaskError(f"{n_bad} attention row(s) fully masked")
     _ctr(counters).count_fused(kind, S.numel() * 8)
+    writeback(out, O)
     return Tensor(O)
 
 
@@ -125,6 +127,7 @@ def fused_bias_residual_activation(x, bias, residual=None, activation: str = "no
         kind = (FusedPassKind.ATTN_OUTPUT_BIAS_RESIDUAL.value if R is not None
                 else FusedPassKind.FFN_BIAS_ACTIVATION.value)
     _ctr(counters).count_fused(kind, X.numel() * (12 if R is not None else 8))
+    writeback(out, O)
     return Tensor(O)
 
 
@@ -145,6 +148,7 @@ def fused_bias_residual_layer_norm(x, bias, residual, gamma, beta, eps: float = 
               X.shape[0], X.shape[1], O.data_ptr(), _rows(O, "out"), None, 0,
               _abi.stream_handle())
     _ctr(counters).count_fused(kind, X.numel() * 12)
+    writeback(out, O)
     return Tensor(O)
 
 
@@ -167,6 +171,8 @@ def fused_qkv_bias_reshape(qkv, bias, batch: int, seq: int, heads: int, q_out=No
     _abi.call("fq_qkv_bias_reshape", X.data_ptr(), _rows(X, "qkv"), B.data_ptr(), batch, seq,
               heads, hd, Q.data_ptr(), K.data_ptr(), V.data_ptr(), _abi.stream_handle())
     _ctr(counters).count_fused(kind, X.numel() * 8)
+    for o, t in ((q_out, Q), (k_out, K), (v_out, V)):
+        writeback(o, t)
     return Tensor(Q), Tensor(K), Tensor(V)
 
 
@@ -186,6 +192,7 @@ def fused_bias_reshape_heads(x, bias, batch: int, seq: int, heads: int, out=None
     _abi.call("fq_bias_reshape_heads", X.data_ptr(), _rows(X, "x"), B.data_ptr(), batch, seq,
               heads, d // heads, O.data_ptr(), _abi.stream_handle())
     _ctr(counters).count_fused(kind, X.numel() * 8)
+    writeback(out, O)
     return Tensor(O)
 
 
@@ -199,7 +206,45 @@ def fused_embed(tokens, embedding, scale: float, positions, pos_offset: int, seq
               float(scale), P.data_ptr(), int(pos_offset), None, int(seq), O.data_ptr(), None,
               _abi.stream_handle())
     _ctr(counters).count_fused(kind, O.numel() * 8)
+    writeback(out, O)
     return Tensor(O)
+
+
+def _kv4(t, what: str) -> torch.Tensor:
+    t = as_device(t, torch.float32)
+    if t.dim() != 4 or not t.is_contiguous():
+        raise DimensionError(f"{what} must be a contiguous [rows, heads, seq, head_dim] tensor")
+    return t
+
+
+def kv_append(new_k, new_v, cur: int, dst_k, dst_v):
+    """Cache refresh without reorder (kernels.py:205-211, fq_kv_append):
+    dst[r, :, cur, :] = new[r, :, 0, :] on the reference's [rows, heads, S, hd]
+    layout. The engine's copy-free cache (``KVCache``) never needs it."""
+    nk, nv = _kv4(new_k, "new_k"), _kv4(new_v, "new_v")
+    dk, dv = _kv4(dst_k, "dst_k"), _kv4(dst_v, "dst_v")
+    R, H, S, E = dk.shape
+    if tuple(nk.shape) != (R, H, 1, E) or nv.shape != nk.shape or dv.shape != dk.shape:
+        raise DimensionError("kv_append: new K/V must be [rows, heads, 1, head_dim]")
+    _abi.call("fq_kv_append", nk.data_ptr(), nv.data_ptr(), int(cur), R, H, S, E, dk.data_ptr(),
+              dv.data_ptr(), _abi.stream_handle())
+
+
+def kv_gather_append(src_k, src_v, new_k, new_v, parents, cur: int, dst_k, dst_v):
+    """Ping-pong beam reorder + append (kernels.py:189-201, fq_kv_gather_append):
+    dst[r, :, :cur] = src[parents[r], :, :cur]; dst[r, :, cur] = new[r, :, 0]."""
+    sk, sv = _kv4(src_k, "src_k"), _kv4(src_v, "src_v")
+    nk, nv = _kv4(new_k, "new_k"), _kv4(new_v, "new_v")
+    dk, dv = _kv4(dst_k, "dst_k"), _kv4(dst_v, "dst_v")
+    R, H, S, E = dk.shape
+    if sk.shape != dk.shape or tuple(nk.shape) != (R, H, 1, E):
+        raise DimensionError("kv_gather_append: shapes differ")
+    par = as_device(parents, torch.int64).contiguous()
+    if tuple(par.shape) != (R,):
+        raise DimensionError(f"parents must be [{R}]")
+    _abi.call("fq_kv_gather_append", sk.data_ptr(), sv.data_ptr(), nk.data_ptr(), nv.data_ptr(),
+              par.data_ptr(), int(cur), R, H, S, E, dk.data_ptr(), dv.data_ptr(),
+              _abi.stream_handle())
 
 
 def attention_scale(head_dim: int) -> float:

@@ -76,6 +76,17 @@ def as_device(x, dtype=None) -> torch.Tensor:
     return t
 
 
+def writeback(out, dev: torch.Tensor):
+    """The reference's ``out=`` contract for host arrays: a numpy ``out`` is
+    written in place (the kernel ran on its device copy)."""
+    if isinstance(out, np.ndarray):
+        out[...] = dev.detach().cpu().numpy().reshape(out.shape)
+    elif isinstance(out, Tensor) and not out.data.is_cuda:
+        out.data.copy_(dev)
+    elif isinstance(out, torch.Tensor) and not out.is_cuda:
+        out.copy_(dev)
+
+
 class OpCounters:
     """Monotonic instrumentation counters, guarded for concurrent use (tensor.py:58-110)."""
 
@@ -253,6 +264,7 @@ def gemm(a, b, out, *, transpose_b: bool = False, accumulate: bool = False,
         timers.stop("gemm", t0)
     (counters or _global_counters).count_gemm(
         A.numel() * A.element_size() + B.numel() * B.element_size() + O.numel() * O.element_size())
+    writeback(out, O)
 
 
 def gemm_x3(a, w, out, *, accumulate: bool = False, counters: OpCounters | None = None,
@@ -374,6 +386,7 @@ def gemm_batched(a, b, out, *, transpose_b: bool = False,
         timers.stop("gemm", t0)
     (counters or _global_counters).count_gemm(
         A.numel() * 4 + B.numel() * 4 + O.numel() * 4)
+    writeback(out, O)
 
 
 def wall() -> float:

@@ -106,6 +106,42 @@ def test_device_plan_shares_and_never_overlaps():
     assert P.build_plan(P.plan_intermediates(cfg, "fp16")).arena_bytes < 2e9
 
 
+def test_plan_alignment_buckets_and_best_fit():
+    """B200 planner: 1024-B TMA alignment for every buffer, per-batch-bucket
+    plans no larger than the max-batch plan, and random interval sets never
+    share bytes between lifetime-overlapping buffers."""
+    import numpy as np
+    from paper_2010_13887_b200 import memory_plan as MP
+    cfg = P.ModelConfig(6, 6, 1024, 4096, 16, 32000, 128, 64, 4)
+    assert MP.batch_buckets(128) == [1, 2, 4, 8, 16, 32, 64, 128]
+    assert MP.batch_buckets(6) == [1, 2, 4, 6]
+    assert MP.bucket_of(5, MP.batch_buckets(6)) == 6
+    for prec in ("fp32", "fp16"):
+        sizes = []
+        for b in MP.batch_buckets(128):
+            plan = P.build_plan(P.plan_intermediates(cfg, prec, batch=b))
+            assert all(off % 1024 == 0 for off, _ in plan.assignments.values())
+            sizes.append(plan.arena_bytes)
+        assert sizes == sorted(sizes) and sizes[0] < sizes[-1] / 50
+    rng = np.random.default_rng(7)
+    for _ in range(200):
+        specs = []
+        for i in range(int(rng.integers(1, 40))):
+            f = int(rng.integers(0, 30))
+            specs.append(P.IntermediateSpec(f"b{i}", int(rng.integers(1, 1 << 20)), f,
+                                            f + int(rng.integers(0, 8)),
+                                            int(rng.choice([64, 256, 1024]))))
+        plan = P.build_plan(specs)
+        assert plan.arena_bytes <= plan.no_share_bytes
+        for a in specs:
+            oa, sa = plan.assignments[a.name]
+            assert oa % a.align == 0
+            for b in specs:
+                if a.name < b.name and a.first_use <= b.last_use and b.first_use <= a.last_use:
+                    ob, sb = plan.assignments[b.name]
+                    assert oa + sa <= ob or ob + sb <= oa, (a, b)
+
+
 def test_plan_errors():
     with pytest.raises(P.PlanError):
         P.build_plan([])
