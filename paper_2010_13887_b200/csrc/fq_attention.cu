@@ -1622,12 +1622,16 @@ __global__ void __launch_bounds__(32) decoder_self_attention_xh(
     }
   };
   const int lrow = (lane & 7) + ((lane >> 3) & 1) * 8, lcol = (lane >> 4) * 8;
-  // ---- pass 1: scores S^T[16 pos x 8] = K . q^T per chunk ----
-#pragma unroll
-  for (int c = 0; c < NS - 1; ++c) {
-    if (c < nchunk) issue(kc, c, c);
+  // one cp.async pipeline over the global chunk sequence K0..K(n-1), V0..V(n-1):
+  // the V chunks stream in while the last scores and the softmax are computed
+  auto issue_g = [&](int gi) {
+    if (gi < nchunk) issue(kc, gi, gi % NS);
+    else if (gi < 2 * nchunk) issue(vc, gi - nchunk, gi % NS);
     else asm volatile("cp.async.commit_group;" ::: "memory");
-  }
+  };
+#pragma unroll
+  for (int c = 0; c < NS - 1; ++c) issue_g(c);
+  // ---- pass 1: scores S^T[16 pos x 8] = K . q^T per chunk ----
   for (int c = 0; c < nchunk; ++c) {
     const int s = c % NS;
     asm volatile("cp.async.wait_group %0;" ::"n"(NS - 2) : "memory");
@@ -1651,21 +1655,13 @@ __global__ void __launch_bounds__(32) decoder_self_attention_xh(
       if (p1 <= cur) sb[p1] = fmul_rn(fadd_rn(big[2], sml[2] * kXhInv), scale);
     }
     __syncwarp();  // stage s consumed
-    if (c + NS - 1 < nchunk) issue(kc, c + NS - 1, (c + NS - 1) % NS);
-    else asm volatile("cp.async.commit_group;" ::: "memory");
+    issue_g(c + NS - 1);
   }
-  asm volatile("cp.async.wait_group 0;" ::: "memory");
-  __syncwarp();
   // ---- exact softmax over positions 0..cur (no mask: causality is implicit) ----
   warp_softmax(sb, npos, true);
   for (int t = npos + lane; t < 16 * nchunk; t += 32) sb[t] = 0.0f;
   __syncwarp();
   // ---- pass 2: O^T[HD x 8] += V^T . p^T per chunk ----
-#pragma unroll
-  for (int c = 0; c < NS - 1; ++c) {
-    if (c < nchunk) issue(vc, c, c);
-    else asm volatile("cp.async.commit_group;" ::: "memory");
-  }
   float ob[KT][4], os[KT][4];
 #pragma unroll
   for (int m = 0; m < KT; ++m)
@@ -1674,7 +1670,7 @@ __global__ void __launch_bounds__(32) decoder_self_attention_xh(
   const int mi = lane >> 3;
   const int vrow = (lane & 7) + ((mi >> 1) & 1) * 8, vcol = (mi & 1) * 8;
   for (int c = 0; c < nchunk; ++c) {
-    const int s = c % NS;
+    const int s = (nchunk + c) % NS;
     asm volatile("cp.async.wait_group %0;" ::"n"(NS - 2) : "memory");
     if (cur / 16 == c) put_cur(s, vnh, vnl);
     __syncwarp();
@@ -1696,8 +1692,7 @@ __global__ void __launch_bounds__(32) decoder_self_attention_xh(
       mma_f16_16816(os[m], al, bh0, bh1);
     }
     __syncwarp();
-    if (c + NS - 1 < nchunk) issue(vc, c + NS - 1, (c + NS - 1) % NS);
-    else asm volatile("cp.async.commit_group;" ::: "memory");
+    issue_g(nchunk + c + NS - 1);
   }
   asm volatile("cp.async.wait_group 0;" ::: "memory");
   // column 0 of O^T: lanes t4 == 0 hold dims 16m + g (reg 0) and 16m + g + 8 (reg 2)
