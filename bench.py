@@ -306,34 +306,6 @@ def cupti_profile(sess, src_dev, dc) -> dict:
                              "us_avg": round(v[1] / v[0], 2)} for k, v in top]}
 
 
-def measure_tf32_peak(dev) -> float:
-    """Dense TF32 tensor throughput (TFLOP/s) of cuBLAS on this GPU: fp32
-    8192^3 matmul with TF32 allowed, best of 10 (the exact mode's 3xTF32
-    GEMMs issue three TF32 MMAs per product: their peak is this / 3)."""
-    import torch
-    prev = torch.backends.cuda.matmul.allow_tf32
-    torch.backends.cuda.matmul.allow_tf32 = True
-    try:
-        n = 8192
-        a = torch.randn(n, n, device=dev)
-        b = torch.randn(n, n, device=dev)
-        c = torch.empty(n, n, device=dev)
-        for _ in range(3):
-            torch.matmul(a, b, out=c)
-        best = float("inf")
-        for _ in range(10):
-            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            s.record()
-            torch.matmul(a, b, out=c)
-            e.record()
-            e.synchronize()
-            best = min(best, s.elapsed_time(e) / 1e3)
-        del a, b, c
-        return 2.0 * n ** 3 / best / 1e12
-    finally:
-        torch.backends.cuda.matmul.allow_tf32 = prev
-
-
 def graph_time(fn, reps=12, rounds=3):
     """Per-call device time (s) of `fn` replayed as a CUDA graph of `reps`
     back-to-back calls (how the kernels run inside the decode-step graph);
@@ -424,6 +396,15 @@ def time_mode(P, cfg, host_w, precision, src_host, args, world, dev, flush, barr
     return sess, src_dev, dc, res
 
 
+def gemm_traffic(precision: str):
+    """Mean DRAM bytes (read + write) per tc_gemm launch of one decode step,
+    from the committed ncu capture of this precision (profiles/r2/), or None."""
+    path = os.path.join(ROOT, "profiles", "r2", f"ncu_gemm_traffic_{precision}.json")
+    if os.path.exists(path):
+        return json.load(open(path)).get("bytes_per_launch_mean")
+    return None
+
+
 def roofline_gemm(sess, src_dev, dc, cfg, batch, steps_run, peak, peak_source, dtype_note):
     prof = cupti_profile(sess, src_dev, dc)
     fl = gemm_flops(cfg, batch, SRC_LEN, BEAM, steps_run)
@@ -433,7 +414,9 @@ def roofline_gemm(sess, src_dev, dc, cfg, batch, steps_run, peak, peak_source, d
         "kernel": f"tc_gemm family ({dtype_note}): every GEMM launch of one request "
                   "(encoder, cross-K/V, 6 per decoder layer per step, logits)",
         "bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-        "frac": achieved / peak, "traffic": None,
+        "frac": achieved / peak, "traffic": gemm_traffic(sess.precision),
+        "traffic_source": "profiles/r2/ncu_gemm_traffic_<precision>.json (ncu, one decode "
+                          "step's GEMM launches, mean dram bytes read + written per launch)",
         "launches": g["n"], "us_per_launch_mean": g["us"] / max(g["n"], 1),
         "flops_per_launch_mean": fl["total"] / max(g["n"], 1),
         "algorithmic_flops": fl, "share_of_request_time": g["us"] / prof["wall_us"],
