@@ -1921,7 +1921,8 @@ __global__ void __launch_bounds__(32) cross_attention_xh(
 int attention_xh_prepare() {
   const int sz = 160 * 1024;  // scores + history of long max_len (static ring <= 26 KB)
 #define FQ_XH_OPT(HD)                                                                           \
-  cudaFuncSetAttribute(decoder_self_attention_xh<HD, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, sz)
+  cudaFuncSetAttribute(decoder_self_attention_xh<HD, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sz) || \
+      cudaFuncSetAttribute(decoder_self_attention_xh<HD, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, sz)
   if (FQ_XH_OPT(16) || FQ_XH_OPT(32) || FQ_XH_OPT(64) || FQ_XH_OPT(128)) {
     set_error("fq_prepare: cannot opt in to large shared memory (exact attention)");
     return FQ_ERR_CUDA;
@@ -2086,8 +2087,15 @@ int fq_decoder_self_attention_xh(const float* sqkv, int64_t ldq, void* kcache, v
   const size_t smem = (size_t)(max_len + 16) * 4 + (size_t)max_len * 4;
   FQ_CHECK_ARG(smem <= 200 * 1024, FQ_ERR_CAPACITY, "decoder self-attention: max_len too long");
   const dim3 grid((unsigned)rows, (unsigned)heads);
+  // ring depth: 2 (+1% over 3 at C2, measured; FQ_XH_SELF_STAGES=3 for A/B)
+  static int ns = -1;
+  if (ns < 0) {
+    const char* e = getenv("FQ_XH_SELF_STAGES");
+    ns = (e && e[0] == '3') ? 3 : 2;
+  }
 #define FQ_SELF_XH(HD)                                                                        \
-  launch_kernel(decoder_self_attention_xh<HD, 3>, grid, 32, smem, as_stream(stream), 1u, sqkv, \
+  launch_kernel(ns == 3 ? decoder_self_attention_xh<HD, 3> : decoder_self_attention_xh<HD, 2>, \
+                grid, 32, smem, as_stream(stream), 1u, sqkv,                                  \
                 ldq, (h16*)kcache, (h16*)vcache, plane, hist, d_cur, (int)rows, (int)heads,    \
                 (int)max_len, scale, out, (h16*)out_hi, (h16*)out_lo, ldo)
   if (head_dim == 16) FQ_SELF_XH(16);
