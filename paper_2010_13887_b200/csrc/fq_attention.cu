@@ -1551,13 +1551,16 @@ __global__ void __launch_bounds__(32) decoder_self_attention_xh(
   __shared__ __align__(128) uint8_t ring[NS][2][16 * RS];  // [stage][hi | lo][16 rows]
   extern __shared__ __align__(16) float dyn[];
   float* sb = dyn;                                          // scores / p, [max_len + 16]
-  int* phys_s = reinterpret_cast<int*>(dyn + max_len + 16);  // [max_len]
+  // element offset of (position t, head h) in a cache plane, made once per warp
+  // (32-bit: a plane is < 2^31 elements, checked on the host)
+  int* off_s = reinterpret_cast<int*>(dyn + max_len + 16);  // [max_len]
   pdl_enter();
   const int r = blockIdx.x, h = blockIdx.y, lane = threadIdx.x;
   const int g = lane >> 2, t4 = lane & 3;
   const int d = heads * HD;
   const int cur = *d_cur;
-  for (int t = lane; t < cur; t += 32) phys_s[t] = hist[(int64_t)r * max_len + t];
+  for (int t = lane; t < cur; t += 32)
+    off_s[t] = (t * rows + hist[(int64_t)r * max_len + t]) * d + h * HD;
   const float* rowp = sqkv + (int64_t)r * ldq + h * HD;
   // this step's k, v as pairs -> cache slot (cur, r); kept for the ring
   uint32_t knh[KE], knl[KE], vnh[KE], vnl[KE];
@@ -1600,9 +1603,9 @@ __global__ void __launch_bounds__(32) decoder_self_attention_xh(
       uint8_t* dh = &ring[s][0][0] + rr * RS + ch * 16;
       uint8_t* dl = &ring[s][1][0] + rr * RS + ch * 16;
       if (t < cur) {
-        const int64_t off = ((int64_t)t * rows + phys_s[t]) * d + h * HD + ch * 8;
-        cp16(sm_u32(dh), src + off);
-        cp16(sm_u32(dl), src + plane + off);
+        const h16* p = src + off_s[t] + ch * 8;
+        cp16(sm_u32(dh), p);
+        cp16(sm_u32(dl), p + plane);
       } else if (t > cur) {  // beyond the sequence: zeros (p = 0, never NaN)
         *reinterpret_cast<uint4*>(dh) = make_uint4(0, 0, 0, 0);
         *reinterpret_cast<uint4*>(dl) = make_uint4(0, 0, 0, 0);
@@ -2084,6 +2087,7 @@ int fq_decoder_self_attention_xh(const float* sqkv, int64_t ldq, void* kcache, v
                    ldq % 2 == 0 && ((uintptr_t)sqkv & 7) == 0 && plane % 8 == 0 &&
                    ((uintptr_t)kcache & 15) == 0 && ((uintptr_t)vcache & 15) == 0,
                FQ_ERR_DIMENSION, "fq_decoder_self_attention_xh: bad args");
+  FQ_CHECK_ARG(plane < (1LL << 31), FQ_ERR_CAPACITY, "fq_decoder_self_attention_xh: cache too large");
   const size_t smem = (size_t)(max_len + 16) * 4 + (size_t)max_len * 4;
   FQ_CHECK_ARG(smem <= 200 * 1024, FQ_ERR_CAPACITY, "decoder self-attention: max_len too long");
   const dim3 grid((unsigned)rows, (unsigned)heads);
