@@ -1460,6 +1460,272 @@ __global__ void __launch_bounds__(threads_of<OP>(), 1)
   }
 }
 
+// ---------------------------------------------------------------------------
+// Exact-mode (3xFP16) GEMM on CTA pairs (tcgen05 cta_group::2). A 2-CTA
+// cluster computes a 256 x BN tile: CTA r holds the A rows [128 r, +128) and
+// the B rows [r BN/2, +BN/2) of every K block (hi + lo pairs), so each SM
+// ingests 2 x (16 KB + BN/2 x 128 B) per 64-K block instead of 2 x (16 KB +
+// BN x 128 B) — the decode GEMMs (M = 512) are bound by that per-SM TMA
+// ingest. The leader CTA's single thread issues cta_group::2 MMAs (M = 256)
+// that read both CTAs' shared memory and accumulate each CTA's 128 rows in its
+// own TMEM; commits multicast to both CTAs' barriers; both CTAs' TMA loads
+// complete on the leader's full barrier. The epilogue is per CTA (its 128
+// rows), with the same TMEM chunking as the 1-CTA kernel: identical numerics.
+// Epilogue: bias, activation, then an fp32 C or the exact mode's fp16 pair
+// (c_lo) through TMA stores (no residual / accumulate on this path).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void mma_f16_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                             uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t"
+      ".reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void mma_xh_block_pair(uint32_t big, uint32_t small, uint32_t a_hi,
+                                                  uint32_t a_lo, uint32_t b_hi, uint32_t b_lo,
+                                                  uint32_t idesc, bool first) {
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const uint32_t acc = (first && k == 0) ? 0u : 1u;
+    mma_f16_pair(small, sw128_desc(a_hi + k * 32), sw128_desc(b_lo + k * 32), idesc, acc);
+    mma_f16_pair(small, sw128_desc(a_lo + k * 32), sw128_desc(b_hi + k * 32), idesc, 1u);
+    mma_f16_pair(big, sw128_desc(a_hi + k * 32), sw128_desc(b_hi + k * 32), idesc, acc);
+  }
+}
+
+__device__ __forceinline__ void commit_pair_mc(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(smem_u32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+
+__device__ __forceinline__ uint32_t mapa_u32(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+
+// TMA load into this CTA's shared memory whose completion is counted on the
+// pair leader's mbarrier (bar: its shared::cluster address)
+__device__ __forceinline__ void tma_load_2d_pair(const CUtensorMap* map, uint32_t bar, void* dst,
+                                                 int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar)
+      : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
+               : "memory");
+}
+
+template <int BN, int STAGES>
+__global__ void __launch_bounds__(kThreads, 1)
+    xh_pair_gemm_kernel(const __grid_constant__ CUtensorMap tma_a,
+                        const __grid_constant__ CUtensorMap tma_alo,
+                        const __grid_constant__ CUtensorMap tma_b,
+                        const __grid_constant__ CUtensorMap tma_blo,
+                        const __grid_constant__ CUtensorMap tma_c,
+                        const __grid_constant__ CUtensorMap tma_clo, const Epi ep, int M, int N,
+                        int K) {
+  constexpr int KB = 64;
+  constexpr int BH = BN / 2;  // B rows per CTA
+  constexpr int A_BYTES = BM * 128;
+  constexpr int B_BYTES = BH * 128;
+  constexpr int STAGE_BYTES = 2 * (A_BYTES + B_BYTES);
+  constexpr int B_OFF = 2 * A_BYTES;
+  constexpr uint32_t TMEM_COLS = 4 * BN;  // 2 chunk slots x {hi.hi, small terms}
+  static_assert(TMEM_COLS <= 512, "TMEM holds 512 columns");
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* boxes = smem + STAGES * STAGE_BYTES;  // 4 epilogue warps x 4 KB
+  __shared__ __align__(8) uint64_t full_bar[STAGES];
+  __shared__ __align__(8) uint64_t empty_bar[STAGES];
+  __shared__ __align__(8) uint64_t tfull_bar[2];
+  __shared__ __align__(8) uint64_t tempty_bar[2];
+  __shared__ __align__(8) uint64_t edone_bar;
+  __shared__ uint32_t tmem_base_sh;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  pdl_launch_dependents();
+  const uint32_t rank = cluster_rank();  // 0: the pair leader (issues the MMAs)
+  const int num_kb = (K + KB - 1) / KB;
+  const int mt = (M + 2 * BM - 1) / (2 * BM), nt = N / BN;
+  const int ngroups = mt * nt;
+  const int pid = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  const int CH = ep.chunk_kb > 0 ? ep.chunk_kb : 4;
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full_bar[s], 1);   // the leader's expect_tx arrive (+ both CTAs' bytes)
+      mbar_init(&empty_bar[s], 1);  // the leader's multicast commit
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull_bar[s], 1);
+      mbar_init(&tempty_bar[s], 8);  // both CTAs' 4 epilogue warps (leader's barrier)
+    }
+    mbar_init(&edone_bar, 4);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tma_a)));
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tma_b)));
+  }
+  if (warp == 1) {  // both CTAs' warp 1 (same warp id): the pair's TMEM
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(&tmem_base_sh)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  cluster_sync_all();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = tmem_base_sh;
+  const uint32_t full0 = mapa_u32(smem_u32(&full_bar[0]), 0);      // leader's, cluster space
+  const uint32_t tempty0 = mapa_u32(smem_u32(&tempty_bar[0]), 0);
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---- TMA producer (both CTAs) ----
+      pdl_wait();  // the activations are written by the previous kernel
+      int it = 0;
+      for (int g = pid; g < ngroups; g += npairs) {
+        const int m0 = (g % mt) * 2 * BM + (int)rank * BM, n0 = (g / mt) * BN + (int)rank * BH;
+        for (int kb = 0; kb < num_kb; ++kb, ++it) {
+          const int s = it % STAGES;
+          const uint32_t ph = (it / STAGES) & 1;
+          uint8_t* sa = smem + s * STAGE_BYTES;
+          mbar_wait(&empty_bar[s], ph ^ 1);
+          if (rank == 0) mbar_expect_tx(&full_bar[s], 2 * STAGE_BYTES);
+          const uint32_t fb = full0 + 8u * (uint32_t)s;
+          tma_load_2d_pair(&tma_a, fb, sa, kb * KB, m0);
+          tma_load_2d_pair(&tma_alo, fb, sa + A_BYTES, kb * KB, m0);
+          tma_load_2d_pair(&tma_b, fb, sa + B_OFF, kb * KB, n0);
+          tma_load_2d_pair(&tma_blo, fb, sa + B_OFF + B_BYTES, kb * KB, n0);
+        }
+      }
+      for (int j = 0; j < STAGES; ++j, ++it)
+        mbar_wait(&empty_bar[it % STAGES], ((it / STAGES) & 1) ^ 1);
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && rank == 0) {  // ---- MMA issuer (the leader) ----
+      constexpr uint32_t idesc = idesc_f16(2 * BM, BN);
+      int it = 0, gc = 0;
+      for (int g = pid; g < ngroups; g += npairs) {
+        for (int kb0 = 0; kb0 < num_kb; kb0 += CH, ++gc) {
+          const int slot = gc & 1;
+          mbar_wait(&tempty_bar[slot], ((gc >> 1) & 1) ^ 1);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t big = tmem + slot * 2 * BN;
+          const int kb1 = min(num_kb, kb0 + CH);
+          for (int kb = kb0; kb < kb1; ++kb, ++it) {
+            const int s = it % STAGES;
+            mbar_wait(&full_bar[s], (it / STAGES) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const uint32_t a_base = smem_u32(smem + s * STAGE_BYTES);
+            const uint32_t b_base = a_base + B_OFF;
+            mma_xh_block_pair(big, big + BN, a_base, a_base + A_BYTES, b_base, b_base + B_BYTES,
+                              idesc, kb == kb0);
+            commit_pair_mc(&empty_bar[s]);
+          }
+          commit_pair_mc(&tfull_bar[slot]);
+        }
+      }
+    }
+  } else {  // ---- epilogue: warps 2..5, this CTA's 128 rows ----
+    pdl_wait();
+    const int q = warp & 3;
+    uint8_t* box = boxes + (warp - 2) * 4096;
+    int gc = 0;
+    for (int g = pid; g < ngroups; g += npairs) {
+      const int m0 = (g % mt) * 2 * BM + (int)rank * BM, n0 = (g / mt) * BN;
+      const int rbase = m0 + q * 32;
+      float racc[BN];
+      for (int kb0 = 0; kb0 < num_kb; kb0 += CH, ++gc) {
+        const int slot = gc & 1;
+        mbar_wait(&tfull_bar[slot], (gc >> 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        x3_add_chunk<BN, OP_X3H>(racc, tmem + slot * 2 * BN + ((uint32_t)(q * 32) << 16),
+                                 kb0 == 0);
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive_remote(tempty0 + 8u * (uint32_t)slot);
+      }
+      if (rbase >= M) continue;  // this warp's rows are beyond the matrix
+#pragma unroll
+      for (int j = 0; j < BN / 32; ++j) {
+        float v[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = racc[j * 32 + i];
+        const int col0 = n0 + j * 32;
+        if (ep.bias) {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const float4 b = __ldg(reinterpret_cast<const float4*>(ep.bias + col0 + 4 * i));
+            v[4 * i] = fadd_rn(v[4 * i], b.x);
+            v[4 * i + 1] = fadd_rn(v[4 * i + 1], b.y);
+            v[4 * i + 2] = fadd_rn(v[4 * i + 2], b.z);
+            v[4 * i + 3] = fadd_rn(v[4 * i + 3], b.w);
+          }
+        }
+        if (ep.act) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = apply_act(v[i], ep.act);
+        }
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(0) : "memory");
+        __syncwarp();
+        if (ep.c_lo) {  // the exact mode's fp16 pair: hi box + lo box (32 rows x 64 B each)
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            uint4 ph, pl;
+            split_xh2(v[8 * i], v[8 * i + 1], ph.x, pl.x);
+            split_xh2(v[8 * i + 2], v[8 * i + 3], ph.y, pl.y);
+            split_xh2(v[8 * i + 4], v[8 * i + 5], ph.z, pl.z);
+            split_xh2(v[8 * i + 6], v[8 * i + 7], ph.w, pl.w);
+            const int off = lane * 64 + ((i ^ ((lane >> 1) & 3)) << 4);
+            *reinterpret_cast<uint4*>(box + off) = ph;
+            *reinterpret_cast<uint4*>(box + 2048 + off) = pl;
+          }
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d(&tma_c, box, col0, rbase);
+            tma_store_2d(&tma_clo, box + 2048, col0, rbase);
+          }
+        } else {  // fp32: 32 rows x 128 B, 128-byte swizzle
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            *reinterpret_cast<float4*>(box + lane * 128 + ((i ^ (lane & 7)) << 4)) =
+                make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) tma_store_2d(&tma_c, box, col0, rbase);
+        }
+      }
+    }
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group %0;" ::"n"(0) : "memory");
+  }
+  __syncwarp();
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  if (warp >= 2 && lane == 0) mbar_arrive(&edone_bar);
+  cluster_sync_all();  // no CTA leaves while its peer may still signal or read it
+  if (warp == 1) {
+    mbar_wait(&edone_bar, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "r"(TMEM_COLS));
+  }
+}
+
+template <int BN, int STAGES>
+constexpr int smem_bytes_pair() {
+  return STAGES * 2 * (BM * 128 + (BN / 2) * 128) + 4 * 4096 + 1024;
+}
+
 template <int BN, int OP>
 constexpr int stage_bytes() {
   return (split3<OP>() ? 2 : 1) * (BM * 128 + BN * 128);
@@ -1667,6 +1933,49 @@ static int prep_splitk() {
              : FQ_ERR_CUDA;
 }
 
+// Exact-mode pair GEMM launch: a, a_lo [M, K] and b, b_lo [N, K] fp16 pairs;
+// C fp32 [M, ldc] (c_lo == NULL) or the fp16 pair (c, c_lo). N % BN == 0.
+template <int BN, int STAGES>
+static int launch_pair(const void* a, const void* a_lo, int64_t lda, const void* b,
+                       const void* b_lo, int64_t ldb, const Epi& ep, int64_t M, int64_t N,
+                       int64_t K, cudaStream_t s) {
+  CUtensorMap ma, malo, mb, mblo, mc, mclo;
+  int rc;
+  if ((rc = make_map(&ma, a, M, K, lda, BM, false)) != FQ_OK) return rc;
+  if ((rc = make_map(&malo, a_lo, M, K, lda, BM, false)) != FQ_OK) return rc;
+  if ((rc = make_map(&mb, b, N, K, ldb, BN / 2, false)) != FQ_OK) return rc;
+  if ((rc = make_map(&mblo, b_lo, N, K, ldb, BN / 2, false)) != FQ_OK) return rc;
+  if (make_map_c(&mc, ep.c, M, N, ep.ldc, ep.c_lo != nullptr) != FQ_OK) {
+    set_error("fq_gemm_x3h (pair): output tensor map");
+    return FQ_ERR_CUDA;
+  }
+  mclo = mc;
+  if (ep.c_lo && make_map_c(&mclo, ep.c_lo, M, N, ep.ldc, true) != FQ_OK) {
+    set_error("fq_gemm_x3h (pair): output tensor map");
+    return FQ_ERR_CUDA;
+  }
+  const int64_t groups = ((M + 2 * BM - 1) / (2 * BM)) * (N / BN);
+  const int64_t max_pairs = num_sms() / 2;
+  const int64_t pairs = groups < max_pairs ? groups : max_pairs;
+  cudaError_t e = launch_kernel(xh_pair_gemm_kernel<BN, STAGES>, dim3((unsigned)(2 * pairs)),
+                                dim3(kThreads), smem_bytes_pair<BN, STAGES>(), s, 2u, ma, malo,
+                                mb, mblo, mc, mclo, ep, (int)M, (int)N, (int)K);
+  if (e != cudaSuccess) {
+    set_error("fq_gemm_x3h (pair): launch failed: %s", cudaGetErrorString(e));
+    return FQ_ERR_CUDA;
+  }
+  return launch_status("fq_gemm_x3h (pair)");
+}
+
+template <int BN, int STAGES>
+static int prep_pair() {
+  return cudaFuncSetAttribute(xh_pair_gemm_kernel<BN, STAGES>,
+                              cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              smem_bytes_pair<BN, STAGES>()) == cudaSuccess
+             ? FQ_OK
+             : FQ_ERR_CUDA;
+}
+
 template <int BN, int STAGES, bool HS = false, int OP = OP_F16>
 static int prep() {
   return cudaFuncSetAttribute(tc_gemm_kernel<BN, STAGES, HS, OP>,
@@ -1690,7 +1999,7 @@ int gemm_tc_prepare() {
       tc::prep_splitk<128, 3, false, true, tc::OP_X3>() ||
       tc::prep<128, 3, false, tc::OP_X3H>() || tc::prep<64, 4, false, tc::OP_X3H>() ||
       tc::prep_splitk<128, 3, false, false, tc::OP_X3H>() ||
-      tc::prep_splitk<128, 3, false, true, tc::OP_X3H>()) {
+      tc::prep_splitk<128, 3, false, true, tc::OP_X3H>() || tc::prep_pair<128, 4>()) {
     set_error("fq_prepare: tcgen05 GEMM smem opt-in failed");
     return FQ_ERR_CUDA;
   }
@@ -1898,11 +2207,32 @@ struct XhPlan {
 
 static XhPlan plan_xh(int64_t M, int64_t N, int64_t K) {
   const int nkb = (int)((K + 63) / 64);
+  static int dbg_chunk = -1;  // experiments only: FQ_XH_CHUNK=<K blocks> (changes numerics)
+  if (dbg_chunk < 0) {
+    const char* e = getenv("FQ_XH_CHUNK");
+    dbg_chunk = e ? atoi(e) : 0;
+  }
+  if (dbg_chunk > 0) return XhPlan{128, 1, dbg_chunk};
   if (N <= 1024 && nkb >= 16) {
     const int slice = (nkb + 3) / 4;
     return M <= 1024 ? XhPlan{128, 4, slice} : XhPlan{128, 1, slice};
   }
   return XhPlan{N <= 512 ? 64 : 128, 1, 4};
+}
+
+// The CTA-pair kernel takes the unsplit shapes whose epilogue is bias / act
+// into a TMA-stored C (the QKV, FFN1, logits, cross-K/V and encoder
+// projections). It is chosen by (N, epilogue) only, never by M, so the bits
+// stay M-independent. FQ_XH_PAIR=0 disables it (A/B).
+static bool pair_ok(int64_t N, int accumulate, const float* res, const void* c, int64_t ldc,
+                    bool half_out) {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("FQ_XH_PAIR");
+    on = (e && e[0] == '0') ? 0 : 1;
+  }
+  return on && N % 128 == 0 && !accumulate && !res && ((uintptr_t)c & 15) == 0 &&
+         (ldc * (half_out ? 2 : 4)) % 16 == 0;
 }
 
 int launch_xh_gemm(const void* a, const void* a_lo, int64_t lda, const void* b,
@@ -1914,6 +2244,8 @@ int launch_xh_gemm(const void* a, const void* a_lo, int64_t lda, const void* b,
   const XhPlan p = plan_xh(M, N, K);
   tc::Epi ep{c, ldc, 0, accumulate, bias, res, ldr, act, g_gemm_dbg};
   ep.chunk_kb = p.chunk_kb;
+  if (p.split == 1 && pair_ok(N, accumulate, res, c, ldc, false))
+    return tc::launch_pair<128, 4>(a, a_lo, lda, b, b_lo, ldb, ep, M, N, K, s);
   if (p.split > 1)
     return tc::launch_splitk<128, 3, false, false, tc::OP_X3H>(a, lda, b, ldb, ep, M, N, K,
                                                                p.split, s, tc::LnEpi{}, b_lo, a_lo);
@@ -1954,6 +2286,8 @@ extern "C" int fq_gemm_x3h_pair(const void* a, const void* a_lo, int64_t lda, co
   ep.chunk_kb = p.chunk_kb;
   ep.c_lo = c_lo;
   cudaStream_t s = as_stream(stream);
+  if (p.split == 1 && pair_ok(N, 0, nullptr, c, ldc, true) && ((uintptr_t)c_lo & 15) == 0)
+    return tc::launch_pair<128, 4>(a, a_lo, lda, b, b_lo, ldb, ep, M, N, K, s);
   if (p.split > 1)
     return tc::launch_splitk<128, 3, false, false, tc::OP_X3H>(a, lda, b, ldb, ep, M, N, K,
                                                                p.split, s, tc::LnEpi{}, b_lo, a_lo);
