@@ -1591,6 +1591,20 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp == 0) {
     if (lane == 0) {  // ---- TMA producer (both CTAs) ----
+      // the weights (B) do not depend on the previous kernel: the first
+      // tile's first stages of B stream in before the grid-dependency wait
+      int npre = 0;
+      if (pid < ngroups) {
+        const int n0 = (pid / mt) * BN + (int)rank * BH;
+        npre = num_kb < STAGES ? num_kb : STAGES;
+        for (int kb = 0; kb < npre; ++kb) {
+          uint8_t* sa = smem + kb * STAGE_BYTES;
+          if (rank == 0) mbar_expect_tx(&full_bar[kb], 2 * STAGE_BYTES);
+          const uint32_t fb = full0 + 8u * (uint32_t)kb;
+          tma_load_2d_pair(&tma_b, fb, sa + B_OFF, kb * KB, n0);
+          tma_load_2d_pair(&tma_blo, fb, sa + B_OFF + B_BYTES, kb * KB, n0);
+        }
+      }
       pdl_wait();  // the activations are written by the previous kernel
       int it = 0;
       for (int g = pid; g < ngroups; g += npairs) {
@@ -1599,6 +1613,12 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int s = it % STAGES;
           const uint32_t ph = (it / STAGES) & 1;
           uint8_t* sa = smem + s * STAGE_BYTES;
+          if (it < npre) {  // B already in flight
+            const uint32_t fb = full0 + 8u * (uint32_t)s;
+            tma_load_2d_pair(&tma_a, fb, sa, kb * KB, m0);
+            tma_load_2d_pair(&tma_alo, fb, sa + A_BYTES, kb * KB, m0);
+            continue;
+          }
           mbar_wait(&empty_bar[s], ph ^ 1);
           if (rank == 0) mbar_expect_tx(&full_bar[s], 2 * STAGE_BYTES);
           const uint32_t fb = full0 + 8u * (uint32_t)s;
