@@ -215,7 +215,9 @@ class Session:
             # the fused LN's row-block exchange needs every CTA of its launch resident:
             # one step chain at a time (not with the two-stream overlap)
             step = M.DecoderStep(self.dw, self.config, nb, K, seq, cache, gp, gm, bufs,
-                                 self.counters, self.timers, fuse_ln=ngroups == 1)
+                                 self.counters, self.timers,
+                                 fuse_ln=ngroups == 1 or os.environ.get("FQ_FUSE_LN", "slab") ==
+                                 "slab")
             st = D.DeviceBeamState(nb, K, self.config.max_seq_len, bufs)
             st.init()
             step.tokens.fill_(bos_token)
