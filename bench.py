@@ -251,7 +251,7 @@ def gemm_flops(cfg, batch, seq, beam, steps) -> dict:
             "total": enc + cross + dec + logits}
 
 
-FAMILIES = (("gemm", ("tc_gemm", "sgemm")), ("layer_norm", ("layer_norm",)),
+FAMILIES = (("gemm", ("_gemm", "sgemm")), ("layer_norm", ("layer_norm",)),
             ("self_attention", ("self_attention",)), ("cross_attention", ("cross_attention",)),
             ("encoder_attention", ("encoder_attention",)),
             ("hars", ("hars", "retrieve")), ("embed", ("embed",)))

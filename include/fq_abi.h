@@ -427,6 +427,16 @@ int fq_cross_attention_slabs(const float* q_slabs, int nslab, int64_t ldq, const
 
 /* ---- weight preparation (cast once at load) -------------- */
 
+/* Exact mode's output layer (SURVEY §8(f)1 for fp32): the 3xFP16 logits GEMM
+ * whose epilogue emits the HARS stage-1 statistics per (row, 128-column tile)
+ * for fq_hars_merge_step (ldt = ntiles = vocab / 128) — group maxima, tile max,
+ * f64 sum of exp, survivors x >= a bound <= R; the [rows, V] logits are never
+ * written. x / emb: fp16 pairs (fq_gemm_x3h operands); vocab % 128 == 0. */
+int fq_logits_hars_x3h(const void* x, const void* x_lo, int64_t ldx, const void* emb,
+                       const void* emb_lo, int64_t lde, int64_t rows, int64_t vocab, int64_t d,
+                       const int32_t* dk, int32_t* gmax, float* tmax, double* tsum, int64_t ldt,
+                       int32_t* sv_cnt, void* sv, int64_t sv_cap, fq_stream_t stream);
+
 /* Exact fp32 mode attention on warp MMAs (3xFP16: every fp32 operand as its
  * fp16 pair, three MMAs per product; the reference's exact f64 softmax in
  * between), replacing model.py:565-578 (decoder self-attention over the

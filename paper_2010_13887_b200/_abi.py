@@ -82,6 +82,8 @@ SIGNATURES = {
                           P], I32),
     "fq_split_tf32": ([P, I64, I64, I32, P, P, P], I32),
     "fq_gemm_x3h": ([P, P, I64, P, P, I64, P, I64, I64, I64, I64, I32, P, P, I64, I32, P], I32),
+    "fq_logits_hars_x3h": ([P, P, I64, P, P, I64, I64, I64, I64, P, P, P, P, I64, P, P, I64, P],
+                           I32),
     "fq_gemm_x3h_pair": ([P, P, I64, P, P, I64, P, P, I64, I64, I64, I64, P, I32, P], I32),
     "fq_gemm_x3h_ln": ([P, P, I64, P, P, I64, P, P, I64, P, P, F64, P, I64, P, P, I64, P, I64, I64,
                         I64, I64, P], I32),
@@ -142,7 +144,7 @@ def load():
 # (name, args, start, end) is appended. Off (None) on the product path.
 PROBE = None
 PROBE_NAMES = ("fq_gemm", "fq_logits_hars", "fq_gemm_ln", "fq_gemm_splitk_slabs", "fq_gemm_f32x3",
-               "fq_gemm_f32x3_ln", "fq_gemm_x3h", "fq_gemm_x3h_ln", "fq_gemm_x3h_pair")
+               "fq_gemm_f32x3_ln", "fq_gemm_x3h", "fq_gemm_x3h_ln", "fq_gemm_x3h_pair", "fq_logits_hars_x3h")
 
 
 def call(name: str, *args) -> int:

@@ -1474,6 +1474,77 @@ __global__ void __launch_bounds__(threads_of<OP>(), 1)
 // Epilogue: bias, activation, then an fp32 C or the exact mode's fp16 pair
 // (c_lo) through TMA stores (no residual / accumulate on this path).
 // ---------------------------------------------------------------------------
+// Exact-mode HARS stage-1 statistics of one row's BN-column tile, from the
+// thread's fp32 accumulator (thread = row r). gms: 32 floats of per-thread
+// scratch (group counts other than 8).
+template <int BN>
+__device__ __forceinline__ void hars_tile_stats(const float (&v)[BN], const HarsEpi& he, int r,
+                                                int M, int n0, float* gms) {
+  const int k = r < M ? he.dk[r] : 0;
+  if (k <= 0) return;
+  // running lower bound of the row's R from the maxima other tiles published
+  float rest = -INFINITY;
+  if (k == 8) {
+    const int4 a0 = __ldcg(reinterpret_cast<const int4*>(he.gmax + (int64_t)r * 32));
+    const int4 a1 = __ldcg(reinterpret_cast<const int4*>(he.gmax + (int64_t)r * 32 + 4));
+    rest = fminf(fminf(fminf(hs_ord2f(a0.x), hs_ord2f(a0.y)), fminf(hs_ord2f(a0.z), hs_ord2f(a0.w))),
+                 fminf(fminf(hs_ord2f(a1.x), hs_ord2f(a1.y)), fminf(hs_ord2f(a1.z), hs_ord2f(a1.w))));
+  } else {
+    float mn = INFINITY;
+    for (int g = 0; g < k; ++g) mn = fminf(mn, hs_ord2f(__ldcg(he.gmax + (int64_t)r * 32 + g)));
+    rest = mn;
+  }
+  // pass 1: group maxima (column c in group c % k; n0 % 8 == 0 so for k = 8
+  // column j of the tile is in group j & 7) and the tile maximum
+  float g8[8] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY,
+                 -INFINITY, -INFINITY, -INFINITY, -INFINITY};
+  float mt = -INFINITY, bound = INFINITY;
+  if (k == 8) {
+#pragma unroll
+    for (int j = 0; j < BN; ++j) g8[j & 7] = fmaxf(g8[j & 7], v[j]);
+#pragma unroll
+    for (int g = 0; g < 8; ++g) {
+      mt = fmaxf(mt, g8[g]);
+      bound = fminf(bound, g8[g]);
+      atomicMax(he.gmax + (int64_t)r * 32 + g, hs_f2ord(g8[g]));
+    }
+  } else {
+    for (int g = 0; g < k; ++g) gms[g] = -INFINITY;
+    int gi = n0 % k;
+#pragma unroll
+    for (int j = 0; j < BN; ++j) {
+      gms[gi] = fmaxf(gms[gi], v[j]);
+      if (++gi == k) gi = 0;
+    }
+    for (int g = 0; g < k; ++g) {
+      mt = fmaxf(mt, gms[g]);
+      bound = fminf(bound, gms[g]);
+      atomicMax(he.gmax + (int64_t)r * 32 + g, hs_f2ord(gms[g]));
+    }
+  }
+  bound = fmaxf(bound, rest);  // still <= the row's R: the candidate set is unchanged
+  // pass 2: sum exp(x - mt) (each term 2^(x log2e - mt log2e) with log2e as hi +
+  // lo fp32 parts, summed in f64) and the survivors x >= bound
+  constexpr float L2E = 1.4426950408889634f;
+  constexpr float L2E_LO = 1.925963033500011e-08f;
+  const float mL = mt * L2E;
+  double s = 0.0;
+  const int tn = n0 / BN;
+  int2* svr = he.sv + ((int64_t)r * he.ldt + tn) * he.sv_cap;
+  int ns = 0;
+#pragma unroll
+  for (int j = 0; j < BN; ++j) {
+    s += (double)hs_ex2(fmaf(v[j], L2E_LO, fmaf(v[j], L2E, -mL)));
+    if (v[j] >= bound) {
+      if (ns < he.sv_cap) svr[ns] = make_int2(n0 + j, __float_as_int(v[j]));
+      ++ns;
+    }
+  }
+  he.sv_cnt[(int64_t)r * he.ldt + tn] = ns;
+  he.tmax[(int64_t)r * he.ldt + tn] = mt;
+  he.tsum[(int64_t)r * he.ldt + tn] = s;
+}
+
 __device__ __forceinline__ void mma_f16_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
                                              uint32_t idesc, uint32_t accumulate) {
   asm volatile(
@@ -1526,7 +1597,12 @@ __device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
                : "memory");
 }
 
-template <int BN, int STAGES>
+// HS: the exact mode's logits GEMM with the HARS stage-1 statistics epilogue
+// (see HarsEpi): per row and 128-column tile the strided group maxima
+// (published to the row's maxima with atomics), the tile maximum, the f64 sum
+// of exp(x - tile max) and the survivors x >= a bound <= R, computed on the
+// thread's fp32 row accumulator — the [rows, V] logits are never written.
+template <int BN, int STAGES, bool HS = false>
 __global__ void __launch_bounds__(kThreads, 1)
     xh_pair_gemm_kernel(const __grid_constant__ CUtensorMap tma_a,
                         const __grid_constant__ CUtensorMap tma_alo,
@@ -1534,7 +1610,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         const __grid_constant__ CUtensorMap tma_blo,
                         const __grid_constant__ CUtensorMap tma_c,
                         const __grid_constant__ CUtensorMap tma_clo, const Epi ep, int M, int N,
-                        int K) {
+                        int K, const HarsEpi he) {
   constexpr int KB = 64;
   constexpr int BH = BN / 2;  // B rows per CTA
   constexpr int A_BYTES = BM * 128;
@@ -1676,6 +1752,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) mbar_arrive_remote(tempty0 + 8u * (uint32_t)slot);
       }
       if (rbase >= M) continue;  // this warp's rows are beyond the matrix
+      if constexpr (HS) {
+        hars_tile_stats<BN>(racc, he, rbase + lane, M, n0,
+                            reinterpret_cast<float*>(boxes) + ((warp - 2) * 32 + lane) * 32);
+        continue;
+      }
 #pragma unroll
       for (int j = 0; j < BN / 32; ++j) {
         float v[32];
@@ -1955,31 +2036,32 @@ static int prep_splitk() {
 
 // Exact-mode pair GEMM launch: a, a_lo [M, K] and b, b_lo [N, K] fp16 pairs;
 // C fp32 [M, ldc] (c_lo == NULL) or the fp16 pair (c, c_lo). N % BN == 0.
-template <int BN, int STAGES>
+template <int BN, int STAGES, bool HS = false>
 static int launch_pair(const void* a, const void* a_lo, int64_t lda, const void* b,
                        const void* b_lo, int64_t ldb, const Epi& ep, int64_t M, int64_t N,
-                       int64_t K, cudaStream_t s) {
+                       int64_t K, cudaStream_t s, const HarsEpi& he = HarsEpi{}) {
   CUtensorMap ma, malo, mb, mblo, mc, mclo;
   int rc;
   if ((rc = make_map(&ma, a, M, K, lda, BM, false)) != FQ_OK) return rc;
   if ((rc = make_map(&malo, a_lo, M, K, lda, BM, false)) != FQ_OK) return rc;
   if ((rc = make_map(&mb, b, N, K, ldb, BN / 2, false)) != FQ_OK) return rc;
   if ((rc = make_map(&mblo, b_lo, N, K, ldb, BN / 2, false)) != FQ_OK) return rc;
-  if (make_map_c(&mc, ep.c, M, N, ep.ldc, ep.c_lo != nullptr) != FQ_OK) {
+  mc = ma;
+  if (!HS && make_map_c(&mc, ep.c, M, N, ep.ldc, ep.c_lo != nullptr) != FQ_OK) {
     set_error("fq_gemm_x3h (pair): output tensor map");
     return FQ_ERR_CUDA;
   }
   mclo = mc;
-  if (ep.c_lo && make_map_c(&mclo, ep.c_lo, M, N, ep.ldc, true) != FQ_OK) {
+  if (!HS && ep.c_lo && make_map_c(&mclo, ep.c_lo, M, N, ep.ldc, true) != FQ_OK) {
     set_error("fq_gemm_x3h (pair): output tensor map");
     return FQ_ERR_CUDA;
   }
   const int64_t groups = ((M + 2 * BM - 1) / (2 * BM)) * (N / BN);
   const int64_t max_pairs = num_sms() / 2;
   const int64_t pairs = groups < max_pairs ? groups : max_pairs;
-  cudaError_t e = launch_kernel(xh_pair_gemm_kernel<BN, STAGES>, dim3((unsigned)(2 * pairs)),
+  cudaError_t e = launch_kernel(xh_pair_gemm_kernel<BN, STAGES, HS>, dim3((unsigned)(2 * pairs)),
                                 dim3(kThreads), smem_bytes_pair<BN, STAGES>(), s, 2u, ma, malo,
-                                mb, mblo, mc, mclo, ep, (int)M, (int)N, (int)K);
+                                mb, mblo, mc, mclo, ep, (int)M, (int)N, (int)K, he);
   if (e != cudaSuccess) {
     set_error("fq_gemm_x3h (pair): launch failed: %s", cudaGetErrorString(e));
     return FQ_ERR_CUDA;
@@ -1987,9 +2069,9 @@ static int launch_pair(const void* a, const void* a_lo, int64_t lda, const void*
   return launch_status("fq_gemm_x3h (pair)");
 }
 
-template <int BN, int STAGES>
+template <int BN, int STAGES, bool HS = false>
 static int prep_pair() {
-  return cudaFuncSetAttribute(xh_pair_gemm_kernel<BN, STAGES>,
+  return cudaFuncSetAttribute(xh_pair_gemm_kernel<BN, STAGES, HS>,
                               cudaFuncAttributeMaxDynamicSharedMemorySize,
                               smem_bytes_pair<BN, STAGES>()) == cudaSuccess
              ? FQ_OK
@@ -2019,7 +2101,8 @@ int gemm_tc_prepare() {
       tc::prep_splitk<128, 3, false, true, tc::OP_X3>() ||
       tc::prep<128, 3, false, tc::OP_X3H>() || tc::prep<64, 4, false, tc::OP_X3H>() ||
       tc::prep_splitk<128, 3, false, false, tc::OP_X3H>() ||
-      tc::prep_splitk<128, 3, false, true, tc::OP_X3H>() || tc::prep_pair<128, 4>()) {
+      tc::prep_splitk<128, 3, false, true, tc::OP_X3H>() || tc::prep_pair<128, 4>() ||
+      tc::prep_pair<128, 4, true>()) {
     set_error("fq_prepare: tcgen05 GEMM smem opt-in failed");
     return FQ_ERR_CUDA;
   }
@@ -2366,6 +2449,31 @@ extern "C" int fq_logits_hars(const void* x16, int64_t ldx, const void* emb16, i
                  (int)ldt};
   return tc::launch<224, 4, true>(x16, ldx, emb16, lde, ep, rows, vocab, d, 1, 1,
                                   as_stream(stream), he);
+}
+
+// Exact mode's output layer: the 3xFP16 logits GEMM (CTA pairs, 128-column
+// tiles) whose epilogue emits the HARS stage-1 statistics of every (row, tile)
+// (hars_tile_stats) for fq_hars_merge_step; x (hi, lo) [rows, d] and the
+// output matrix (hi, lo) [vocab, d] are fp16 pairs; vocab % 128 == 0,
+// ldt >= vocab / 128.
+extern "C" int fq_logits_hars_x3h(const void* x, const void* x_lo, int64_t ldx, const void* emb,
+                                  const void* emb_lo, int64_t lde, int64_t rows, int64_t vocab,
+                                  int64_t d, const int32_t* dk, int32_t* gmax, float* tmax,
+                                  double* tsum, int64_t ldt, int32_t* sv_cnt, void* sv,
+                                  int64_t sv_cap, fq_stream_t stream) {
+  FQ_CHECK_ARG(dk && gmax && tmax && tsum && sv_cnt && sv && rows > 0 && vocab > 0 && d > 0 &&
+                   vocab % 128 == 0 && ldt >= vocab / 128 && sv_cap >= 1,
+               FQ_ERR_DIMENSION, "fq_logits_hars_x3h: bad args");
+  int rc = check_xh(x, x_lo, ldx, emb, emb_lo, lde, rows, vocab, d);
+  if (rc != FQ_OK) return rc;
+  const XhPlan p = plan_xh(rows, vocab, d);
+  FQ_CHECK_ARG(p.split == 1, FQ_ERR_UNSUPPORTED, "fq_logits_hars_x3h: split-K plan");
+  tc::Epi ep{nullptr, 0, 0, 0, nullptr, nullptr, 0, 0, g_gemm_dbg};
+  ep.chunk_kb = p.chunk_kb;
+  tc::HarsEpi he{dk, gmax, tmax, tsum, sv_cnt, reinterpret_cast<int2*>(sv), (int)sv_cap,
+                 (int)ldt};
+  return tc::launch_pair<128, 4, true>(x, x_lo, ldx, emb, emb_lo, lde, ep, rows, vocab, d,
+                                       as_stream(stream), he);
 }
 
 // fp16 GEMM + bias + residual + LayerNorm (the decode step's self-out/LN1,

@@ -198,9 +198,14 @@ class Session:
         # epilogue + fq_hars_merge_step, the [rows, V] logits never written
         # (C2: 49.5 us GEMM + merge vs 40.7 us GEMM + 39 us HARS).
         # FQ_LOGITS_HARS=0: materialised logits + fq_hars_step
-        lh = (fused and self.dw.half and os.environ.get("FQ_LOGITS_HARS", "1") != "0"
-              and not _materialise
-              and self.config.d_model % 64 == 0 and V >= 4096 and (V + 223) // 224 <= 256)
+        # exact mode (opt-in, FQ_LOGITS_HARS_X3H=1): the 3xFP16 logits GEMM
+        # (128-column tiles) with the same statistics epilogue
+        # (fq_logits_hars_x3h); measured slower at C2 than the materialised
+        # logits + fq_hars_step (191 vs 130 us: the per-thread statistics on the
+        # 128-float row accumulator spill), so off by default
+        lh = (fused and os.environ.get("FQ_LOGITS_HARS", "1") != "0" and not _materialise
+              and (self.dw.half or os.environ.get("FQ_LOGITS_HARS_X3H") == "1")
+              and M.logits_hars_tiles(self.config, self.precision) > 0)
         bounds = [0, batch] if ngroups == 1 else [0, (batch + 1) // 2, batch]
         groups = []
         for g in range(ngroups):
@@ -238,7 +243,7 @@ class Session:
                 grp["hcnt"] = bufs.get("hars.counters", (nb + 1 + nr,), torch.int32)
                 grp["hcnt"].zero_()
             if fused and lh:  # fused logits + HARS stage 1 (the logits never materialised)
-                ldt = (V + 223) // 224
+                ldt = M.logits_hars_tiles(self.config, self.precision)
                 grp["ldt"] = ldt
                 grp["gmax"] = bufs.get("hars.gmax", (nr, 32), torch.int32)
                 grp["gmax"].fill_(_ORD_NEG_INF)
@@ -263,11 +268,20 @@ class Session:
                 # statistics, then the per-row merge + stage 2 + next embedding
                 step.run(embed=False, logits=False)
                 d = self.config.d_model
-                _abi.call("fq_logits_hars", step.x16.data_ptr(), d, self.dw.out_proj.data_ptr(),
-                          self.dw.out_proj.stride(0), nr, V, d, hk.data_ptr(),
-                          gr["gmax"].data_ptr(), gr["tmax"].data_ptr(), gr["tsum"].data_ptr(),
-                          gr["ldt"], gr["svcnt"].data_ptr(), gr["sv"].data_ptr(), M.LH_SV_CAP,
-                          stream)
+                if self.dw.half:
+                    _abi.call("fq_logits_hars", step.x16.data_ptr(), d,
+                              self.dw.out_proj.data_ptr(), self.dw.out_proj.stride(0), nr, V, d,
+                              hk.data_ptr(), gr["gmax"].data_ptr(), gr["tmax"].data_ptr(),
+                              gr["tsum"].data_ptr(), gr["ldt"], gr["svcnt"].data_ptr(),
+                              gr["sv"].data_ptr(), M.LH_SV_CAP, stream)
+                else:  # exact mode: the step's fp16 pair x16 (written by the last LN)
+                    xh, xl = step.x16
+                    E = self.dw.out_xh
+                    _abi.call("fq_logits_hars_x3h", xh.data_ptr(), xl.data_ptr(), xh.stride(0),
+                              E.hi.data_ptr(), E.lo.data_ptr(), E.hi.stride(0), nr, V, d,
+                              hk.data_ptr(), gr["gmax"].data_ptr(), gr["tmax"].data_ptr(),
+                              gr["tsum"].data_ptr(), gr["ldt"], gr["svcnt"].data_ptr(),
+                              gr["sv"].data_ptr(), M.LH_SV_CAP, stream)
                 _abi.call("fq_hars_merge_step", st.c, nb, K, V, self.config.max_seq_len,
                           cfg.eos_token, _abi.ptr(lp), cache.d_cur.data_ptr(), max_steps,
                           hk.data_ptr(), gr["gmax"].data_ptr(), gr["tmax"].data_ptr(),
@@ -278,7 +292,8 @@ class Session:
                           step.tokens.data_ptr(), parents.data_ptr(), cache.hist.data_ptr(),
                           self.dw.embedding.data_ptr(), d,
                           float(np.float32(math.sqrt(d))), self.dw.positions.data_ptr(),
-                          step.x.data_ptr(), _abi.ptr(step.x16), stream)
+                          step.x.data_ptr(), _abi.ptr(step.x16) if self.dw.half else None,
+                          stream)
                 self.counters.count_fused("logits_hars", nr * gr["ldt"] * 12)
                 return
             logits = step.run(embed=not fused)

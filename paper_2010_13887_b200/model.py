@@ -1041,7 +1041,19 @@ def decode_step(last_tokens, cache: KVCache, cross_kv, enc_mask, weights, config
 # static intermediate enumeration for the arena  (model.py:772-860)
 # ---------------------------------------------------------------------------
 
-LH_SV_CAP = 128  # fq_logits_hars survivor slots per (row, 224-column tile)
+LH_SV_CAP = 128  # fq_logits_hars survivor slots per (row, column tile)
+
+
+def logits_hars_tiles(config: ModelConfig, precision: str) -> int:
+    """Column tiles per row of the fused logits + HARS stage-1 output layer
+    (fq_logits_hars: 224-wide fp16 tiles; fq_logits_hars_x3h: 128-wide exact
+    tiles), or 0 when the shape keeps the materialised logits."""
+    V, d = config.vocab_size, config.d_model
+    if precision == "fp16":
+        ok = d % 64 == 0 and V >= 4096 and (V + 223) // 224 <= 256
+        return (V + 223) // 224 if ok else 0
+    ok = V % 128 == 0 and V >= 4096 and V // 128 <= 256 and d % 64 == 0
+    return V // 128 if ok else 0
 
 
 def plan_intermediates(config: ModelConfig, precision: str = "fp32",
@@ -1130,8 +1142,8 @@ def plan_intermediates(config: ModelConfig, precision: str = "fp32",
         add("hars.lse", R * 8, end - 2, end)
         add("hars.cand_idx", R * V * 4, end - 2, end)
         add("hars.cand_count", R * 8, end - 2, end)
-        if bf:  # fq_logits_hars statistics (the fused logits + HARS stage-1 output layer)
-            ldt = (V + 223) // 224
+        ldt = logits_hars_tiles(config, precision)
+        if ldt:  # fq_logits_hars(_x3h) statistics (the fused logits + HARS stage-1 layer)
             add("hars.gmax", R * 32 * 4, setup, end)
             add("hars.tmax", R * ldt * 4, end - 3, end)
             add("hars.tsum", R * ldt * 8, end - 3, end)

@@ -829,3 +829,26 @@ def test_lsqw_load_forced_logits_match_torch_golden(P, name):
     assert float(np.abs(got - g["logits"]).max()) <= 1e-4
     got16 = P.Session(cfg, w, precision="fp16").forced_logits(g["src"], g["tgt"])
     assert float(np.abs(got16 - g["logits"]).max()) <= 2e-2
+
+
+def test_exact_logits_hars_engine_path_token_identical(P, monkeypatch):
+    """Exact mode's fused output layer (fq_logits_hars_x3h: the 3xFP16 logits
+    GEMM emits HARS stage-1 statistics, no [rows, V] logits) gives the same
+    hypotheses as the materialised logits + fq_hars_step, scores within 1e-7
+    relative (the logsumexp is merged from tile sums instead of one row sweep;
+    measured 1.2e-8)."""
+    cfg = P.ModelConfig(num_encoder_layers=1, num_decoder_layers=2, d_model=128, d_ff=256,
+                        num_heads=2, vocab_size=8192, max_batch=8, max_seq_len=16,
+                        max_beam_size=4)
+    w = P.make_random_weights(cfg, seed=4)
+    src = np.random.default_rng(2).integers(3, cfg.vocab_size, size=(8, 10))
+    dc = P.DecodeConfig(beam_size=4, max_steps=12, eos_token=2, length_penalty=0.6)
+    monkeypatch.setenv("FQ_LOGITS_HARS", "0")
+    want = P.Session(cfg, w, precision="fp32").generate(src, dc)
+    monkeypatch.setenv("FQ_LOGITS_HARS", "1")
+    monkeypatch.setenv("FQ_LOGITS_HARS_X3H", "1")  # opt-in in exact mode
+    got = P.Session(cfg, w, precision="fp32").generate(src, dc)
+    assert [[h.tokens for h in x] for x in got] == [[h.tokens for h in x] for x in want]
+    for x, y in zip(got, want):
+        for h1, h2 in zip(x, y):
+            assert abs(h1.score - h2.score) <= 1e-7 * max(1.0, abs(h2.score))
