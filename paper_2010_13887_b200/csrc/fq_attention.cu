@@ -1538,6 +1538,42 @@ int attention_prepare() {
 // ---------------------------------------------------------------------------
 constexpr float kXhInv = 1.0f / 2048.0f;
 
+// exp(t - m) for the exact-mode softmax (t <= m): the difference exact in f64
+// (as the reference's (double)t - (double)m), split into fp32 hi + lo, and
+// 2^(d log2e) on the SFU with log2e as hi + lo parts: ~2 ulp of fp32, vs the
+// reference's f64 exp — the probabilities, rounded to fp32, agree to an ulp.
+// Sums stay in f64. (A f64 exp per score made these kernels DFMA-bound.)
+__device__ __forceinline__ float xh_exp_diff(float t, float m) {
+  const double dd = (double)t - (double)m;
+  const float dh = (float)dd, dl = (float)(dd - (double)dh);
+  constexpr float L2E = 1.4426950408889634f, L2E_LO = 1.925963033500011e-08f;
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(fmaf(dh, L2E, fmaf(dh, L2E_LO, dl * L2E))));
+  return y;
+}
+
+// Exact-mode softmax over n scores in smem (one warp): max, e = xh_exp_diff,
+// f64 sum, p = fp32(e / sum). False when every score is -inf.
+__device__ __forceinline__ bool warp_softmax_xh(float* s, int n) {
+  const int lane = threadIdx.x & 31;
+  float m = -INFINITY;
+  for (int j = lane; j < n; j += 32) m = fmaxf(m, s[j]);
+  m = warp_max(m);
+  if (m == -INFINITY) return false;
+  double acc = 0.0;
+  for (int j = lane; j < n; j += 32) {
+    const float t = s[j];
+    const float e = t == -INFINITY ? 0.0f : xh_exp_diff(t, m);
+    s[j] = e;
+    acc += (double)e;
+  }
+  const double inv = 1.0 / warp_sum(acc);
+  __syncwarp();
+  for (int j = lane; j < n; j += 32) s[j] = (float)((double)s[j] * inv);
+  __syncwarp();
+  return true;
+}
+
 template <int HD, int NS>
 __global__ void __launch_bounds__(32) decoder_self_attention_xh(
     const float* __restrict__ sqkv, int64_t ldq, h16* __restrict__ kc, h16* __restrict__ vc,
@@ -1661,7 +1697,7 @@ __global__ void __launch_bounds__(32) decoder_self_attention_xh(
     issue_g(c + NS - 1);
   }
   // ---- exact softmax over positions 0..cur (no mask: causality is implicit) ----
-  warp_softmax(sb, npos, true);
+  warp_softmax_xh(sb, npos);
   for (int t = npos + lane; t < 16 * nchunk; t += 32) sb[t] = 0.0f;
   __syncwarp();
   // ---- pass 2: O^T[HD x 8] += V^T . p^T per chunk ----
@@ -1723,7 +1759,7 @@ __global__ void __launch_bounds__(32) decoder_self_attention_xh(
 //   softmax the reference's exact masked one per beam column (model.py:594-604,
 //           kernels.py:106-139: fp32 t = s * scale + mask, f64 exp and sum);
 //   pass 2  O^T = V^T . P^T.
-template <int HD, int NT>
+template <int HD, int NT, int NS>
 __global__ void __launch_bounds__(32) cross_attention_xh(
     const float* __restrict__ cq, int64_t ldcq, const h16* __restrict__ ck,
     const h16* __restrict__ cv, int64_t plane, int64_t ldkv, int beam, int seq, float scale,
@@ -1733,7 +1769,6 @@ __global__ void __launch_bounds__(32) cross_attention_xh(
   constexpr int CPR = HD * 2 / 16;
   constexpr int NP = NT * 16;
   constexpr int KT = HD / 16;
-  constexpr int NS = 3;
   __shared__ __align__(128) uint8_t ring[NS][2][16 * RS];
   __shared__ float Ps[8][NP + 4];
   const int b = blockIdx.x, h = blockIdx.y, lane = threadIdx.x;
@@ -1836,17 +1871,17 @@ __global__ void __launch_bounds__(32) cross_attention_xh(
     mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, o));
     mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, o));
   }
-  double e[NT][4];
+  float e[NT][4];
   double l0 = 0.0, l1 = 0.0;
 #pragma unroll
   for (int m = 0; m < NT; ++m) {
 #pragma unroll
     for (int hh = 0; hh < 2; ++hh) {
       const float t0 = sc[m][2 * hh], t1 = sc[m][2 * hh + 1];
-      e[m][2 * hh] = t0 == -INFINITY ? 0.0 : exp((double)t0 - (double)mx0);
-      e[m][2 * hh + 1] = t1 == -INFINITY ? 0.0 : exp((double)t1 - (double)mx1);
-      l0 += e[m][2 * hh];
-      l1 += e[m][2 * hh + 1];
+      e[m][2 * hh] = t0 == -INFINITY ? 0.0f : xh_exp_diff(t0, mx0);
+      e[m][2 * hh + 1] = t1 == -INFINITY ? 0.0f : xh_exp_diff(t1, mx1);
+      l0 += (double)e[m][2 * hh];
+      l1 += (double)e[m][2 * hh + 1];
     }
   }
 #pragma unroll
@@ -1860,8 +1895,8 @@ __global__ void __launch_bounds__(32) cross_attention_xh(
 #pragma unroll
     for (int hh = 0; hh < 2; ++hh) {
       const int p = 16 * m + g + 8 * hh;
-      Ps[2 * t4][p] = (float)(e[m][2 * hh] * inv0);
-      Ps[2 * t4 + 1][p] = (float)(e[m][2 * hh + 1] * inv1);
+      Ps[2 * t4][p] = (float)((double)e[m][2 * hh] * inv0);
+      Ps[2 * t4 + 1][p] = (float)((double)e[m][2 * hh + 1] * inv1);
     }
   }
   if (d_bad && g == 0) {
@@ -2124,8 +2159,18 @@ int fq_cross_attention_xh(const float* cq, int64_t ldcq, const void* ck, const v
   const dim3 grid((unsigned)batch, (unsigned)heads);
   const int nt = (int)((seq + 15) / 16);
   const size_t smem = 0;
+  static int ns = -1;  // ring depth (FQ_XH_CROSS_STAGES = 2 | 3 | 4 | 6, A/B)
+  if (ns < 0) {
+    const char* e = getenv("FQ_XH_CROSS_STAGES");
+    ns = e ? atoi(e) : 3;
+    if (ns != 2 && ns != 4 && ns != 6) ns = 3;
+  }
 #define FQ_CROSS_XH(HD, NT)                                                                   \
-  launch_kernel(cross_attention_xh<HD, NT>, grid, 32, smem, as_stream(stream), 1u, cq, ldcq,   \
+  launch_kernel(ns == 2 ? cross_attention_xh<HD, NT, 2>                                       \
+                : ns == 4 ? cross_attention_xh<HD, NT, 4>                                     \
+                : ns == 6 ? cross_attention_xh<HD, NT, (HD <= 64 ? 6 : 3)>                    \
+                          : cross_attention_xh<HD, NT, 3>,                                    \
+                grid, 32, smem, as_stream(stream), 1u, cq, ldcq,                              \
                 (const h16*)ck, (const h16*)cv, plane, ldkv, (int)beam, (int)seq, scale, mask, \
                 out, (h16*)out_hi, (h16*)out_lo, ldo, d_bad)
 #define FQ_CROSS_XHH(HD)                                                                      \
