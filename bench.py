@@ -578,6 +578,57 @@ def output_layer_micro(P, _abi, sess16, cfg, batch, dev, ctx):
             "hbm_bytes_avoided_per_step": 2 * R * V * 4}
 
 
+def extra_workloads(P, dev, args) -> dict:
+    """BASELINE configs 4 and 5 on the same engine, exact mode
+    and fp16, end to end through the public API (host tokens in, host results
+    out; wall clock after warm-up, synchronized):
+    * BERT-base-like encoder + classification head (12 layers, d = 768, GELU,
+      V = 30522, seq 128, batch 64): Session.classify sequences/s (the
+      reference measured 6.7 seq/s on 8 CPU cores, SURVEY §6);
+    * top-k sampling generate (k = 8) on the C2 model, batch 64, 64 steps:
+      decoded tokens/s (host-driven draw in the reference's PCG64 order; a
+      decoder-only GPT-2 is not expressible in the reference)."""
+    import numpy as np
+    import torch
+    res = {}
+    bert = P.ModelConfig(num_encoder_layers=12, num_decoder_layers=0, d_model=768, d_ff=3072,
+                         num_heads=12, vocab_size=30522, max_batch=64, max_seq_len=128,
+                         max_beam_size=1, activation="gelu")
+    wb = P.make_random_weights(bert, seed=0)
+    toks = np.random.default_rng(0).integers(3, bert.vocab_size, size=(64, 128))
+    for prec in ("fp32", "fp16"):
+        sess = P.Session(bert, wb, precision=prec)
+        for _ in range(2):
+            sess.classify(toks)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        n = 5
+        for _ in range(n):
+            sess.classify(toks)
+        torch.cuda.synchronize()
+        dt = (time.perf_counter() - t0) / n
+        res[f"classify_bert_base_{prec}"] = {"value": 64 / dt, "unit": "sequences/s",
+                                             "ms_per_batch": dt * 1e3, "batch": 64, "seq": 128}
+        del sess
+    cfg = P.ModelConfig(**dict(C2, max_batch=64))
+    w = P.make_random_weights(cfg, seed=0)
+    src = synthetic_tokens(64, SRC_LEN, cfg.vocab_size, 0)
+    dc = P.DecodeConfig(method="top_k", sample_k=8, max_steps=MAX_STEPS, eos_token=2, seed=0)
+    for prec in ("fp32", "fp16"):
+        sess = P.Session(cfg, w, precision=prec)
+        sess.generate(src, dc)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        hyps = sess.generate(src, dc)
+        dt = time.perf_counter() - t0
+        ntok = sum(len(h[0].tokens) for h in hyps if h)
+        res[f"sampling_top_k_{prec}"] = {"value": ntok / dt, "unit": "tokens/s",
+                                         "ms_per_request": dt * 1e3, "batch": 64,
+                                         "max_steps": MAX_STEPS}
+        del sess
+    return res
+
+
 def cpu_baseline_sample():
     """The reference's own CPU path on the box's host cores, bounded sample
     (one 16-item C2 request, ~10 s)."""
@@ -676,6 +727,8 @@ def run_ours(args, rank, world):
         sess16 = half if half is not None else (sess if args.precision != "fp32" else None)
         if sess16 is not None:
             out["output_layer"] = output_layer_micro(P, _abi, sess16, cfg, local, dev, ctx)
+    if rank == 0 and not args.no_micro:
+        out["extras"] = extra_workloads(P, dev, args)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline_sample()
     if rank == 0:
