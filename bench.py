@@ -473,7 +473,7 @@ def hars_micro(P, D, _abi, cfg, batch, dev, hbm_peak):
                   cfg.max_seq_len, 2, None, dcur.data_ptr(), 1 << 40, lse.data_ptr(),
                   ci.data_ptr(), ci.stride(0), cc.data_ptr(), hcnt.data_ptr(),
                   rt.data_ptr(), rp.data_ptr(), hist.data_ptr(), None, 0, 0.0, None, None,
-                  None, _abi.stream_handle())
+                  None, None, _abi.stream_handle())
 
     hst.init()
     t_s1 = graph_time(stage1)
@@ -551,7 +551,7 @@ def output_layer_micro(P, _abi, sess16, cfg, batch, dev, ctx):
                   tsm.data_ptr(), ldt, ldt, svc.data_ptr(), svb.data_ptr(), cap,
                   lse.data_ptr(), ci.data_ptr(), ci.stride(0), cc.data_ptr(), mcnt.data_ptr(),
                   ovf.data_ptr(), rt.data_ptr(), rp.data_ptr(), hist.data_ptr(), None, 0, 0.0,
-                  None, None, None, _abi.stream_handle())
+                  None, None, None, None, _abi.stream_handle())
 
     def out_mat():
         resets()
@@ -562,7 +562,7 @@ def output_layer_micro(P, _abi, sess16, cfg, batch, dev, ctx):
                   cfg.max_seq_len, 2, None, dcur.data_ptr(), 1 << 40, lse.data_ptr(),
                   ci.data_ptr(), ci.stride(0), cc.data_ptr(), hcnt.data_ptr(),
                   rt.data_ptr(), rp.data_ptr(), hist.data_ptr(), None, 0, 0.0, None, None,
-                  None, _abi.stream_handle())
+                  None, None, _abi.stream_handle())
     hst.init()
     _abi.call("fq_hars_groups", hst.c, batch, BEAM, V, 0, dk.data_ptr(), _abi.stream_handle())
     t_of = graph_time(out_fused) - t_reset

@@ -334,14 +334,15 @@ int fq_hars_groups(fq_beam_state st, int64_t batch, int64_t beam, int64_t vocab,
  * With x_next != NULL the item's rows of the next step's decoder input are
  * also written (embed_scale_pos at position *d_cur + 1, kernels.py:143-151:
  * fp32 emb[token] * emb_scale + pos[position], row-major [rows, d_model],
- * x16_next an optional fp16 copy), replacing the next step's embedding launch. */
+ * x16_next an optional fp16 copy; with x16_next_lo the exact mode's fp16 pair hi / lo),
+ * replacing the next step's embedding launch. */
 int fq_hars_step(const float* logits, int64_t ld, fq_beam_state st, int64_t batch, int64_t beam,
                  int64_t vocab, int64_t max_len, int64_t eos, const double* len_pow,
                  int32_t* d_cur, int64_t max_steps, double* lse, int32_t* cand_idx,
                  int64_t cand_ld, int64_t* cand_count, int32_t* counters, int64_t* row_tokens,
                  int64_t* row_parents, int32_t* hist, const float* emb, int64_t d_model,
                  float emb_scale, const float* pos, float* x_next, void* x16_next,
-                 fq_stream_t stream);
+                 void* x16_next_lo, fq_stream_t stream);
 
 /* The decode step's output layer without materialising the [rows, V]
  * logits: the tied-embedding logits GEMM (x16 [rows, d] fp16 .
@@ -374,7 +375,8 @@ int fq_hars_merge_step(fq_beam_state st, int64_t batch, int64_t beam, int64_t vo
                        int64_t cand_ld, int64_t* cand_count, int32_t* counters, int32_t* d_ovf,
                        int64_t* row_tokens, int64_t* row_parents, int32_t* hist,
                        const float* emb, int64_t d_model, float emb_scale, const float* pos,
-                       float* x_next, void* x16_next, fq_stream_t stream);
+                       float* x_next, void* x16_next, void* x16_next_lo,
+                       fq_stream_t stream);
 
 /* Reset beam state to BeamState() (decode.py:145-151) for every item. */
 int fq_beam_state_init(fq_beam_state st, int64_t batch, int64_t beam, int64_t max_len,

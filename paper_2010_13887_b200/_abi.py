@@ -61,11 +61,11 @@ SIGNATURES = {
                         P, P, P, P, I64, P], I32),
     "fq_hars_groups": ([BeamStateC, I64, I64, I64, I32, P, P], I32),
     "fq_hars_step": ([P, I64, BeamStateC, I64, I64, I64, I64, I64, P, P, I64, P, P, I64, P, P, P,
-                      P, P, P, I64, F32, P, P, P, P], I32),
+                      P, P, P, I64, F32, P, P, P, P, P], I32),
     "fq_logits_hars": ([P, I64, P, I64, I64, I64, I64, P, P, P, P, I64, P, P, I64, P], I32),
     "fq_hars_merge_step": ([BeamStateC, I64, I64, I64, I64, I64, P, P, I64, P, P, P, P, I64, I64,
-                            P, P, I64, P, P, I64, P, P, P, P, P, P, P, I64, F32, P, P, P, P],
-                           I32),
+                            P, P, I64, P, P, I64, P, P, P, P, P, P, P, I64, F32, P, P, P, P,
+                            P], I32),
     "fq_beam_state_init": ([BeamStateC, I64, I64, I64, P], I32),
     "fq_step_advance": ([P, P], I32),
     "fq_encoder_attention": ([P, I64, I64, I64, I64, I64, F32, P, P, P, I64, I32, P, P], I32),

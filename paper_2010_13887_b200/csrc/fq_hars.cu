@@ -1341,7 +1341,7 @@ __device__ __forceinline__ void stage2_and_next(
     int64_t max_steps, int64_t* row_tokens, int64_t* row_parents, int32_t* hist,
     const int64_t vals_off, const int cur0, const float* __restrict__ emb, int d,
     float emb_scale, const float* __restrict__ pos, float* __restrict__ x_next,
-    h16* __restrict__ x16_next, int batch, int* all_cnt) {
+    h16* __restrict__ x16_next, int batch, int* all_cnt, h16* __restrict__ x16_next_lo = nullptr) {
   __shared__ int64_t s_tok[kMaxBeam];
   select_item(b, logits, ld, lse, cand_idx, cand_ld, cand_count, st, K, max_len, eos, len_pow,
               d_cur, max_steps, row_tokens, row_parents, hist, vals_off, s_tok);
@@ -1364,12 +1364,12 @@ __device__ __forceinline__ void stage2_and_next(
       v.z = fadd_rn(fmul_rn(e.z, emb_scale), p.z);
       v.w = fadd_rn(fmul_rn(e.w, emb_scale), p.w);
       *reinterpret_cast<float4*>(x_next + r * d + j) = v;
-      if (x16_next) {
-        h16x2 lo = __floats2half2_rn(v.x, v.y), hi = __floats2half2_rn(v.z, v.w);
-        uint2 pk;
-        pk.x = *reinterpret_cast<uint32_t*>(&lo);
-        pk.y = *reinterpret_cast<uint32_t*>(&hi);
-        *reinterpret_cast<uint2*>(x16_next + r * d + j) = pk;
+      if (x16_next) {  // fp16 copy, or with x16_next_lo the exact mode's pair
+        uint2 ph, pl;
+        split_xh2(v.x, v.y, ph.x, pl.x);
+        split_xh2(v.z, v.w, ph.y, pl.y);
+        *reinterpret_cast<uint2*>(x16_next + r * d + j) = ph;
+        if (x16_next_lo) *reinterpret_cast<uint2*>(x16_next_lo + r * d + j) = pl;
       }
     }
   }
@@ -1398,7 +1398,7 @@ __global__ void __launch_bounds__(kSwThreads) hars_step_kernel(
     double* lse, int32_t* cand_idx, int64_t cand_ld, int64_t* cand_count, int* item_cnt,
     int* all_cnt, int64_t* row_tokens, int64_t* row_parents, int32_t* hist,
     const float* __restrict__ emb, int d, float emb_scale, const float* __restrict__ pos,
-    float* __restrict__ x_next, h16* __restrict__ x16_next) {
+    float* __restrict__ x_next, h16* __restrict__ x16_next, h16* __restrict__ x16_next_lo) {
   pdl_enter();
   const int C = (int)cl_nrank(), rank = (int)cl_rank();
   const int64_t row = blockIdx.x / C;
@@ -1424,7 +1424,7 @@ __global__ void __launch_bounds__(kSwThreads) hars_step_kernel(
   __threadfence();
   stage2_and_next(b, logits, ld, lse, cand_idx, cand_ld, cand_count, st, K, max_len, eos,
                   len_pow, d_cur, max_steps, row_tokens, row_parents, hist, vals_off, cur0, emb,
-                  d, emb_scale, pos, x_next, x16_next, batch, all_cnt);
+                  d, emb_scale, pos, x_next, x16_next, batch, all_cnt, x16_next_lo);
 }
 
 // The fused HARS step on the balanced split (few rows: rows < 2 x SMs): as
@@ -1437,7 +1437,7 @@ __global__ void __launch_bounds__(kSwThreads, 4) hars_step_split_kernel(
     double* lse, int32_t* cand_idx, int64_t cand_ld, int64_t* cand_count, int* counters,
     int64_t* row_tokens, int64_t* row_parents, int32_t* hist, const float* __restrict__ emb,
     int d, float emb_scale, const float* __restrict__ pos, float* __restrict__ x_next,
-    h16* __restrict__ x16_next) {
+    h16* __restrict__ x16_next, h16* __restrict__ x16_next_lo) {
   pdl_enter();
   extern __shared__ __align__(16) float4 sw_ring[];  // also stage 2's dynamic smem
   __shared__ SplitSmem sm;
@@ -1471,7 +1471,7 @@ __global__ void __launch_bounds__(kSwThreads, 4) hars_step_split_kernel(
           __threadfence();
           stage2_and_next(b, logits, ld, lse, cand_idx, cand_ld, cand_count, st, K, max_len, eos,
                           len_pow, d_cur, max_steps, row_tokens, row_parents, hist, vals_off,
-                          cur0, emb, d, emb_scale, pos, x_next, x16_next, batch, all_cnt);
+                          cur0, emb, d, emb_scale, pos, x_next, x16_next, batch, all_cnt, x16_next_lo);
         }
       });
 }
@@ -1495,7 +1495,7 @@ __global__ void __launch_bounds__(kSelThreads) hars_merge_step_kernel(
     int32_t* cand_idx, int64_t cand_ld, int64_t* cand_count, int* counters, int* d_ovf,
     int64_t* row_tokens, int64_t* row_parents, int32_t* hist, const float* __restrict__ emb,
     int d, float emb_scale, const float* __restrict__ pos, float* __restrict__ x_next,
-    h16* __restrict__ x16_next) {
+    h16* __restrict__ x16_next, h16* __restrict__ x16_next_lo) {
   pdl_enter();
   __shared__ int s_idx[kMergeCap];
   __shared__ float s_val[kMergeCap];
@@ -1588,7 +1588,7 @@ __global__ void __launch_bounds__(kSelThreads) hars_merge_step_kernel(
   sw_stamp(row, 2);
   stage2_and_next(b, nullptr, 0, lse, cand_idx, cand_ld, cand_count, st, K, max_len, eos, len_pow,
                   d_cur, max_steps, row_tokens, row_parents, hist, vals_off, cur0, emb, d,
-                  emb_scale, pos, x_next, x16_next, batch, counters + batch);
+                  emb_scale, pos, x_next, x16_next, batch, counters + batch, x16_next_lo);
   __syncthreads();
   sw_stamp(row, 4);
   if (tid < K) {  // group counts of the item's rows for the next step (decode.py:230)
@@ -1774,7 +1774,7 @@ int fq_hars_step(const float* logits, int64_t ld, fq_beam_state st, int64_t batc
                  int32_t* d_cur, int64_t max_steps, double* lse, int32_t* cand_idx,
                  int64_t cand_ld, int64_t* cand_count, int32_t* counters, int64_t* row_tokens,
                  int64_t* row_parents, int32_t* hist, const float* emb, int64_t d_model,
-                 float emb_scale, const float* pos, float* x_next, void* x16_next,
+                 float emb_scale, const float* pos, float* x_next, void* x16_next, void* x16_next_lo,
                  fq_stream_t stream) {
   FQ_CHECK_ARG(logits && lse && cand_idx && cand_count && counters && d_cur && row_tokens &&
                    row_parents && batch > 0 && beam >= 1 && beam <= kMaxBeam && max_len >= 1,
@@ -1798,7 +1798,7 @@ int fq_hars_step(const float* logits, int64_t ld, fq_beam_state st, int64_t batc
                   logits, ld, g, st, (int)batch, (int)beam, (int)max_len, (int)eos, len_pow, d_cur,
                   max_steps, lse, cand_idx, cand_ld, cand_count, counters, row_tokens,
                   row_parents, hist, x_next ? emb : nullptr, (int)d_model, emb_scale, pos, x_next,
-                  reinterpret_cast<fq::h16*>(x16_next));
+                  reinterpret_cast<fq::h16*>(x16_next), reinterpret_cast<fq::h16*>(x16_next_lo));
     return launch_status("fq_hars_step");
   }
   const size_t smem = std::max(sel_smem(beam, max_len),
@@ -1809,7 +1809,7 @@ int fq_hars_step(const float* logits, int64_t ld, fq_beam_state st, int64_t batc
                 len_pow, d_cur, max_steps, lse, cand_idx, cand_ld, cand_count, counters,
                 counters + batch, row_tokens, row_parents, hist, x_next ? emb : nullptr,
                 (int)d_model, emb_scale, pos, x_next,
-                reinterpret_cast<fq::h16*>(x16_next));
+                reinterpret_cast<fq::h16*>(x16_next), reinterpret_cast<fq::h16*>(x16_next_lo));
   return launch_status("fq_hars_step");
 }
 
@@ -1821,7 +1821,7 @@ int fq_hars_merge_step(fq_beam_state st, int64_t batch, int64_t beam, int64_t vo
                        int64_t cand_ld, int64_t* cand_count, int32_t* counters, int32_t* d_ovf,
                        int64_t* row_tokens, int64_t* row_parents, int32_t* hist,
                        const float* emb, int64_t d_model, float emb_scale, const float* pos,
-                       float* x_next, void* x16_next, fq_stream_t stream) {
+                       float* x_next, void* x16_next, void* x16_next_lo, fq_stream_t stream) {
   FQ_CHECK_ARG(d_cur && dk && gmax && tmax && tsum && sv_cnt && sv && lse && cand_idx &&
                    cand_count && counters && d_ovf && row_tokens && row_parents && batch > 0 &&
                    beam >= 1 && beam <= kMaxBeam && 2 * beam <= 32 && ntiles <= ldt &&
@@ -1838,7 +1838,7 @@ int fq_hars_merge_step(fq_beam_state st, int64_t batch, int64_t beam, int64_t vo
                 sv_cnt, reinterpret_cast<const int2*>(sv), (int)sv_cap, lse, cand_idx, cand_ld,
                 cand_count, counters, d_ovf, row_tokens, row_parents, hist,
                 x_next ? emb : nullptr, (int)d_model, emb_scale, pos, x_next,
-                reinterpret_cast<fq::h16*>(x16_next));
+                reinterpret_cast<fq::h16*>(x16_next), reinterpret_cast<fq::h16*>(x16_next_lo));
   return launch_status("fq_hars_merge_step");
 }
 

@@ -109,6 +109,14 @@ class Session:
         self._arena2.use(self.arena.plan)
         return self._buffers2
 
+    @staticmethod
+    def _next16(step) -> tuple:
+        """The fused HARS launch's half outputs for the next step's input:
+        fp16 mode its fp16 copy, exact mode its fp16 pair (hi, lo)."""
+        if isinstance(step.x16, tuple):
+            return step.x16[0].data_ptr(), step.x16[1].data_ptr()
+        return _abi.ptr(step.x16), None
+
     def _use_bucket(self, batch: int):
         """Serve this request's buffers from its batch bucket's plan."""
         if batch > self.config.max_batch:
@@ -292,8 +300,7 @@ class Session:
                           step.tokens.data_ptr(), parents.data_ptr(), cache.hist.data_ptr(),
                           self.dw.embedding.data_ptr(), d,
                           float(np.float32(math.sqrt(d))), self.dw.positions.data_ptr(),
-                          step.x.data_ptr(), _abi.ptr(step.x16) if self.dw.half else None,
-                          stream)
+                          step.x.data_ptr(), *self._next16(step), stream)
                 self.counters.count_fused("logits_hars", nr * gr["ldt"] * 12)
                 return
             logits = step.run(embed=not fused)
@@ -306,7 +313,7 @@ class Session:
                           self.dw.embedding.data_ptr(), self.config.d_model,
                           float(np.float32(math.sqrt(self.config.d_model))),
                           self.dw.positions.data_ptr(), step.x.data_ptr(),
-                          _abi.ptr(step.x16) if self.dw.half else None, stream)
+                          *self._next16(step), stream)
                 self.counters.count_fused("retrieve", nr * V * 4)
                 return
             _abi.call("fq_hars_groups", st.c, nb, K, V, exhaustive, hk.data_ptr(), stream)

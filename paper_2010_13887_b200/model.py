@@ -916,11 +916,13 @@ class DecoderStep:
                   self.cache.d_cur.data_ptr(), 1, self.x.data_ptr(),
                   _abi.ptr(self.x16) if dw.half else None, _abi.stream_handle())
         self.counters.count_fused("embed_scale_pos", R * d * 8)
+        fill_pair(self.x, self.x16)  # exact mode: the step input's fp16 pair
 
     def run(self, embed: bool = True, logits: bool = True):
         """Embed -> L decoder layers -> logits. Position comes from cache.d_cur.
-        ``embed=False``: the input rows were already written (by the previous
-        step's fused HARS launch, fq_hars_step). ``logits=False``: stop after the
+        ``embed=False``: the input rows (and in exact mode their fp16 pair) were
+        already written by the previous step's fused HARS launch (fq_hars_step /
+        fq_hars_merge_step) or by :meth:`embed`. ``logits=False``: stop after the
         layers (the output layer runs as fq_logits_hars on ``x16``)."""
         c, dw, ctr, tm = self.config, self.dw, self.counters, self.timers
         R, d, h, hd, L = self.rows, c.d_model, c.num_heads, c.head_dim, c.num_decoder_layers
@@ -931,7 +933,6 @@ class DecoderStep:
         if embed:
             self.embed()
         x, x16 = self.x, self.x16
-        fill_pair(x, x16)  # exact mode: the step input's fp16 pair
         for i, lw in enumerate(dw.dec):
             _lin(dw, x, x16, lw["w_qkv"], self.sqkv, bias=lw["b_qkv"], counters=ctr, timers=tm)
             if self.cache.pairs:  # exact mode: 3xFP16 warp-MMA attention on the pair cache

@@ -31,5 +31,5 @@ for i in range(6):
     _abi.call("fq_hars_step", lg.data_ptr(), V, st.c, B, K, V, S, 2, None, dcur.data_ptr(),
               1 << 40, lse.data_ptr(), ci.data_ptr(), V, cc.data_ptr(), cnt.data_ptr(),
               rt.data_ptr(), rp.data_ptr(), hist.data_ptr(), None, 0, 0.0, None, None, None,
-              _abi.stream_handle())
+              None, _abi.stream_handle())
 torch.cuda.synchronize()

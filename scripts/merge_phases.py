@@ -59,7 +59,7 @@ def one(stamp):
               svc.data_ptr(), svb.data_ptr(), cap, lse.data_ptr(), ci.data_ptr(), V,
               cc.data_ptr(), cnt.data_ptr(), ovf.data_ptr(), rt.data_ptr(), rp.data_ptr(),
               hist.data_ptr(), emb.data_ptr(), d, 32.0, pos.data_ptr(), xn.data_ptr(),
-              xn16.data_ptr(), _abi.stream_handle())
+              xn16.data_ptr(), None, _abi.stream_handle())
     torch.cuda.synchronize()
     if stamp:
         lib.fq_retrieve_debug_timestamps(None)

@@ -68,7 +68,7 @@ def fused(lg):
     _abi.call("fq_hars_step", lg.data_ptr(), lg.stride(0), st.c, B, K, V, S, 2, None,
               dcur.data_ptr(), 1 << 40, lse.data_ptr(), ci.data_ptr(), ci.stride(0),
               cc.data_ptr(), hcnt.data_ptr(), rt.data_ptr(), rp.data_ptr(), hist.data_ptr(),
-              None, 0, 0.0, None, None, None, _abi.stream_handle())
+              None, 0, 0.0, None, None, None, None, _abi.stream_handle())
 
 
 for i in range(4):

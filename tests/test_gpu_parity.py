@@ -523,7 +523,7 @@ def test_fused_hars_step_equals_separate_launches(P, split, monkeypatch):
                   b["cur"].data_ptr(), S, b["lse"].data_ptr(), b["ci"].data_ptr(), V,
                   b["cc"].data_ptr(), b["cnt"].data_ptr(), b["tok"].data_ptr(),
                   b["par"].data_ptr(), b["hist"].data_ptr(), emb.data_ptr(), d,
-                  float(np.float32(8.0)), pos.data_ptr(), b["x"].data_ptr(), None, hs())
+                  float(np.float32(8.0)), pos.data_ptr(), b["x"].data_ptr(), None, None, hs())
         torch.cuda.synchronize()
         for key in ("tok", "par", "hist", "cur", "cc"):
             assert torch.equal(a[key], b[key]), (t, key)
@@ -584,7 +584,7 @@ def test_logits_hars_equals_materialised_path(P, B, d, V):
                   a["cur"].data_ptr(), S, a["lse"].data_ptr(), a["ci"].data_ptr(), V,
                   a["cc"].data_ptr(), a["cnt"].data_ptr(), a["tok"].data_ptr(),
                   a["par"].data_ptr(), a["hist"].data_ptr(), emb.data_ptr(), d,
-                  float(np.float32(8.0)), pos.data_ptr(), a["x"].data_ptr(), None, hs())
+                  float(np.float32(8.0)), pos.data_ptr(), a["x"].data_ptr(), None, None, hs())
         _abi.call("fq_logits_hars", x16.data_ptr(), d, E.data_ptr(), d, R, V, d, dk.data_ptr(),
                   gmax.data_ptr(), tmax.data_ptr(), tsum.data_ptr(), ldt, svc.data_ptr(),
                   sv.data_ptr(), cap, hs())
@@ -594,7 +594,7 @@ def test_logits_hars_equals_materialised_path(P, B, d, V):
                   svc.data_ptr(), sv.data_ptr(), cap, b["lse"].data_ptr(), b["ci"].data_ptr(), V,
                   b["cc"].data_ptr(), b["cnt"].data_ptr(), ovf.data_ptr(), b["tok"].data_ptr(),
                   b["par"].data_ptr(), b["hist"].data_ptr(), emb.data_ptr(), d,
-                  float(np.float32(8.0)), pos.data_ptr(), b["x"].data_ptr(), None, hs())
+                  float(np.float32(8.0)), pos.data_ptr(), b["x"].data_ptr(), None, None, hs())
         torch.cuda.synchronize()
         assert int(ovf.item()) == 0
         assert torch.equal(a["cc"], b["cc"]), t
