@@ -326,7 +326,8 @@ int fq_hars_groups(fq_beam_state st, int64_t batch, int64_t beam, int64_t vocab,
  * min(K + live, V) (decode.py:230), stage 1 (single-sweep retrieve), and for
  * each item, run by the last of its rows to finish, stage 2 (fq_hars_select
  * semantics); the last item advances *d_cur. counters: int32
- * [batch + 1 + batch*beam] (item, all-items and row arrival counters),
+ * [batch + 1 + batch*beam] (item, all-items and per-row counters: the split
+ * layout's row arrivals, the row layout's top-list marks; zero between launches),
  * zero-initialised once (they reset themselves). For long rows (V >= 64k) or
  * <= 8 rows stage 1 runs on the balanced split (every CTA of one wave streams
  * an equal share of the [rows, V] block; the CTA completing a row merges it). Needs 2*beam <= 32 and

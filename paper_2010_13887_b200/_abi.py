@@ -15,7 +15,8 @@ import threading
 from .errors import (AliasingError, CapacityError, DimensionError, EngineError, ExtensionError,
                      ParameterError)
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libfq_b200.so")
+LIB_PATH = os.environ.get("FQ_LIB") or os.path.join(  # FQ_LIB: A/B builds (scripts/)
+    os.path.dirname(os.path.abspath(__file__)), "_lib", "libfq_b200.so")
 
 P = ctypes.c_void_p
 I64 = ctypes.c_int64

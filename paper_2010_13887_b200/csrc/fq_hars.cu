@@ -237,25 +237,45 @@ __global__ void __launch_bounds__(kRetrieveThreads, 4) retrieve_kernel(
 // ---------------------------------------------------------------------------
 constexpr int kSwThreads = 256;
 __device__ unsigned long long* g_sw_dbg = nullptr;  // phase stamps (profiling only)
+// Phase stamps cost a global load of g_sw_dbg on thread 0's critical path:
+// compiled in only for the phase scripts (-DFQ_HARS_STAMPS, build_variant.sh).
 __device__ __forceinline__ void sw_stamp(int64_t row, int slot) {
+#ifdef FQ_HARS_STAMPS
   if (g_sw_dbg && threadIdx.x == 0) {
     unsigned long long t_;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
     g_sw_dbg[row * 8 + slot] = t_;
   }
+#endif
 }
 __device__ __forceinline__ float ex2_ftz(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
-constexpr int kSwU = 8;   // pilot vectors per thread
+constexpr int kSwU = 8;   // pilot vectors per thread (fewer: more survivors, measured slower)
 constexpr int kSwP = 8;   // async ring depth (vectors in flight per thread)
-// CTAs (cluster) per row. 2 balances rows over SMs but needs 7 resident CTAs
-// per SM for one wave, which the ring + survivor smem does not allow: measured
-// slower (two waves), so one CTA per row.
-constexpr int kSwSplit = 1;
+// CTAs (cluster) per row and threads per CTA (A/B builds: -DFQ_ROW_SPLIT,
+// -DFQ_ROW_NT). 2 x 128-thread CTAs per row (7 resident per SM, one wave)
+// balance bytes per SM but measured slower (stage 1 27.5 vs 24.1 us at C2):
+// the per-CTA finishing spread, not the 4-vs-3 rows per SM, sets the tail.
+#ifndef FQ_ROW_NT
+#define FQ_ROW_NT 256
+#endif
+#ifndef FQ_ROW_SPLIT
+#define FQ_ROW_SPLIT 1
+#endif
+constexpr int kSwSplit = FQ_ROW_SPLIT;
+constexpr int kRowThreads = FQ_ROW_NT;  // threads of the CTA-per-row(-part) kernels
+constexpr int kRowMinBlocks = kRowThreads >= 256 ? 4 : 7;  // one resident wave
 constexpr int kSurvCap = 2048;
+// The fused step's per-row "top list": the row's best kTopC survivors >= R by
+// (-logit, token), the only ones stage 2 can pick (it keeps K + live <= 2K <=
+// kTopC of the item's candidates, and within a row the score order is the
+// logit order). Layout at the end of the row's candidate slots: [0] count (-1:
+// none, use the full list), [1, 1 + kTopC) indices, then kTopC logits.
+constexpr int kTopC = 32;
+constexpr int kTopSlots = 1 + 2 * kTopC;
 
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
@@ -298,18 +318,21 @@ __device__ __forceinline__ T* peer_ptr(T* p, int rank) {
 // the logsumexp partial and the survivor counts are exchanged through
 // distributed shared memory. Half rows balance the 512 decode rows over 148
 // SMs (a row per CTA leaves a 4-vs-3 rows-per-SM tail).
+template <int NT>
 __device__ __forceinline__ void sweep_row(
     const float* __restrict__ logits, int64_t ld, int V, const int64_t row, const int k,
     float* __restrict__ group_max, int64_t gm_ld, float* __restrict__ threshold,
     double* __restrict__ lse, int32_t* __restrict__ cand_idx, int64_t cand_ld,
     int64_t* __restrict__ cand_count, float4* __restrict__ ring, const int C, const int rank,
-    const int64_t vals_off = 0) {
-  __shared__ float part_max[kSwThreads * 4];
-  __shared__ int32_t sv_idx[kSurvCap];
-  __shared__ float sv_val[kSurvCap];
+    const int64_t vals_off = 0, int32_t* __restrict__ top_out = nullptr,
+    int32_t* __restrict__ top_mark = nullptr) {
+  constexpr int SC = NT * 4;  // survivor list (more: ordered rescan)
+  __shared__ float part_max[NT * 4];
+  __shared__ int32_t sv_idx[SC];
+  __shared__ float sv_val[SC];
   __shared__ float gmax_s[32];
   __shared__ float s_R, s_M;
-  __shared__ double red[kSwThreads / 32];
+  __shared__ double red[NT / 32];
   __shared__ double s_S;
   __shared__ int warp_tot[32];
   __shared__ int s_cnt, s_total, s_n, s_ovf;
@@ -320,7 +343,7 @@ __device__ __forceinline__ void sweep_row(
   const float* x = logits + row * ld;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int kk = k / (k & -k) * ((k & -k) > 4 ? (k & -k) / 4 : 1);  // k / gcd(k, 4)
-  const int T = kSwThreads - kSwThreads % kk;
+  const int T = NT - NT % kk;
   const int nvec = V >> 2;
   const float4* x4 = reinterpret_cast<const float4*>(x);
   const bool act = tid < T;
@@ -334,7 +357,7 @@ __device__ __forceinline__ void sweep_row(
   // async prologue: this thread's first kSwP vectors in flight at once
 #pragma unroll
   for (int i = 0; i < kSwP; ++i) {
-    if (i < nit) cp_async16(ring + i * kSwThreads + tid, xb + i * T);
+    if (i < nit) cp_async16(ring + i * NT + tid, xb + i * T);
     cp_async_commit();
   }
   if (tid == 0) { s_cnt = 0; s_ovf = 0; }
@@ -344,7 +367,7 @@ __device__ __forceinline__ void sweep_row(
 #pragma unroll
   for (int u = 0; u < kSwU; ++u) {
     if (u < nit) {
-      const float4 e = ring[u * kSwThreads + tid];
+      const float4 e = ring[u * NT + tid];
       gm[0] = fmaxf(gm[0], e.x); gm[1] = fmaxf(gm[1], e.y);
       gm[2] = fmaxf(gm[2], e.z); gm[3] = fmaxf(gm[3], e.w);
     }
@@ -354,7 +377,7 @@ __device__ __forceinline__ void sweep_row(
     part_max[4 * tid + 2] = gm[2]; part_max[4 * tid + 3] = gm[3];
   }
   __syncthreads();
-  for (int g = w; g < k; g += kSwThreads / 32) {
+  for (int g = w; g < k; g += NT / 32) {
     float mm = NEG;
     for (int e = g + lane * k; e < 4 * T; e += 32 * k) mm = fmaxf(mm, part_max[e]);
     mm = warp_max(mm);
@@ -380,47 +403,53 @@ __device__ __forceinline__ void sweep_row(
   float m = s_M;
   float mL = m * L2E;
   double s = 0.0;
-  auto visit4 = [&](const float4& e, int v) {
-    const float m4 = fmaxf(fmaxf(e.x, e.y), fmaxf(e.z, e.w));
-    if (m4 > m + 64.f || m == NEG) {  // (practically never for logits)
-      if (m4 != NEG) {
-        s = m == NEG ? 0.0 : s * exp2((double)mL - (double)m4 * L2E_D);
-        m = m4;
-        mL = m * L2E;
-      }
-    }
-    // exp(x - m_eff) = 2^(x log2e - mL), m_eff = mL / log2e, log2e as hi + lo
-    // fp32 parts (argument exact to ~1 ulp); terms below 2^-126 flush to 0
-    if (m != NEG) {
-      const float t4 = (ex2_ftz(fmaf(e.x, L2E_LO, fmaf(e.x, L2E, -mL))) +
-                        ex2_ftz(fmaf(e.y, L2E_LO, fmaf(e.y, L2E, -mL)))) +
-                       (ex2_ftz(fmaf(e.z, L2E_LO, fmaf(e.z, L2E, -mL))) +
-                        ex2_ftz(fmaf(e.w, L2E_LO, fmaf(e.w, L2E, -mL))));
-      s += (double)t4;
-    }
-    if (m4 >= Rp) {
-      const float e4[4] = {e.x, e.y, e.z, e.w};
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        if (e4[c] >= Rp) {
-          const int p = atomicAdd(&s_cnt, 1);
-          if (p < kSurvCap) { sv_idx[p] = 4 * v + c; sv_val[p] = e4[c]; }
-        }
-      }
-    }
+  // exp(x - m_eff) = 2^(x log2e - mL), m_eff = mL / log2e, log2e as hi + lo
+  // fp32 parts (argument exact to ~1 ulp); terms below 2^-126 flush to 0
+  auto terms4 = [&](const float4& e) {
+    return (ex2_ftz(fmaf(e.x, L2E_LO, fmaf(e.x, L2E, -mL))) +
+            ex2_ftz(fmaf(e.y, L2E_LO, fmaf(e.y, L2E, -mL)))) +
+           (ex2_ftz(fmaf(e.z, L2E_LO, fmaf(e.z, L2E, -mL))) +
+            ex2_ftz(fmaf(e.w, L2E_LO, fmaf(e.w, L2E, -mL))));
   };
-  // ---- sweep: consume slot i, refill it with vector i + kSwP ----
+  // One rare branch per vector: an element reaching R' (survivor) or m + 64
+  // (rescale), or m still -inf, takes the exact per-element path; every other
+  // vector only adds its 4-term fp32 sum (same sums, same order either way).
+  float thr = m == NEG ? NEG : fminf(Rp, m + 64.f);
+  const float4* src = xb + kSwP * T;
   for (int i = 0; i < nit; ++i) {
     cp_async_wait<kSwP - 1>();
-    float4* slot = ring + (i % kSwP) * kSwThreads + tid;
+    float4* slot = ring + (i % kSwP) * NT + tid;
     const float4 e = *slot;
-    if (i + kSwP < nit) cp_async16(slot, xb + (i + kSwP) * T);
+    if (i + kSwP < nit) cp_async16(slot, src);
+    src += T;
     cp_async_commit();
-    if (i >= kSwU) {
-      gm[0] = fmaxf(gm[0], e.x); gm[1] = fmaxf(gm[1], e.y);
-      gm[2] = fmaxf(gm[2], e.z); gm[3] = fmaxf(gm[3], e.w);
+    gm[0] = fmaxf(gm[0], e.x); gm[1] = fmaxf(gm[1], e.y);
+    gm[2] = fmaxf(gm[2], e.z); gm[3] = fmaxf(gm[3], e.w);
+    const float m4 = fmaxf(fmaxf(e.x, e.y), fmaxf(e.z, e.w));
+    if (m4 >= thr) {
+      if (m4 > m + 64.f || m == NEG) {  // (practically never for logits)
+        if (m4 != NEG) {
+          s = m == NEG ? 0.0 : s * exp2((double)mL - (double)m4 * L2E_D);
+          m = m4;
+          mL = m * L2E;
+        }
+      }
+      if (m != NEG) s += (double)terms4(e);
+      if (m4 >= Rp) {
+        const int v = tid + (i_lo + i) * T;
+        const float e4[4] = {e.x, e.y, e.z, e.w};
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          if (e4[c] >= Rp) {
+            const int p = atomicAdd(&s_cnt, 1);
+            if (p < SC) { sv_idx[p] = 4 * v + c; sv_val[p] = e4[c]; }
+          }
+        }
+      }
+      thr = m == NEG ? NEG : fminf(Rp, m + 64.f);
+    } else {
+      s += (double)terms4(e);
     }
-    visit4(e, tid + (i_lo + i) * T);
   }
   cp_async_wait<0>();
   sw_stamp(row, 2);
@@ -441,12 +470,12 @@ __device__ __forceinline__ void sweep_row(
       if (m != NEG) s += (double)ex2_ftz(fmaf(xv, L2E_LO, fmaf(xv, L2E, -mL)));
       if (xv >= Rp) {
         const int p = atomicAdd(&s_cnt, 1);
-        if (p < kSurvCap) { sv_idx[p] = j; sv_val[p] = xv; }
+        if (p < SC) { sv_idx[p] = j; sv_val[p] = xv; }
       }
     }
   }
   __syncthreads();
-  for (int g = w; g < k; g += kSwThreads / 32) {
+  for (int g = w; g < k; g += NT / 32) {
     float mm = NEG;
     for (int e = g + lane * k; e < 4 * T; e += 32 * k) mm = fmaxf(mm, part_max[e]);
     mm = warp_max(mm);
@@ -478,13 +507,13 @@ __device__ __forceinline__ void sweep_row(
   // survivors >= R of this CTA, compacted, then ranked by token below
   if (tid == 0) { s_n = 0; s_S = Sl; }
   __syncthreads();
-  if (nsv <= kSurvCap) {
-    for (int i = tid; i < nsv; i += kSwThreads) {
+  if (nsv <= SC) {
+    for (int i = tid; i < nsv; i += NT) {
       const float v = sv_val[i];
       const int j = sv_idx[i];
       if (v >= R) {
         const int p = atomicAdd(&s_n, 1);
-        if (p < kSwThreads * 2) {  // (index, value) pairs
+        if (p < NT * 2) {  // (index, value) pairs
           part_max[2 * p] = __int_as_float(j);
           part_max[2 * p + 1] = v;
         }
@@ -492,7 +521,7 @@ __device__ __forceinline__ void sweep_row(
     }
   }
   __syncthreads();
-  if (tid == 0) s_ovf = (nsv > kSurvCap || s_n > kSwThreads * 2) ? 1 : 0;
+  if (tid == 0) s_ovf = (nsv > SC || s_n > NT * 2) ? 1 : 0;
   if (C > 1) cl_sync_all();  // counts, overflow flags and partial sums visible
   else __syncthreads();
   int ovf = 0, base = 0, total = 0;
@@ -506,19 +535,30 @@ __device__ __forceinline__ void sweep_row(
   }
   if (!ovf) {
     const int n = s_n;
-    for (int i = tid; i < n; i += kSwThreads) {
+    for (int i = tid; i < n; i += NT) {
       const int j = __float_as_int(part_max[2 * i]);
-      int rk = 0;
-      for (int q2 = 0; q2 < n; ++q2) rk += __float_as_int(part_max[2 * q2]) < j ? 1 : 0;
+      const float v = part_max[2 * i + 1];
+      int rk = 0, rl = 0;  // rank by token; rank by (-logit, token)
+      for (int q2 = 0; q2 < n; ++q2) {
+        const int jq = __float_as_int(part_max[2 * q2]);
+        const float vq = part_max[2 * q2 + 1];
+        rk += jq < j ? 1 : 0;
+        rl += (vq > v || (vq == v && jq < j)) ? 1 : 0;
+      }
       if (base + rk < cand_ld) out_idx[base + rk] = j;
       if (vals_off && base + rk < vals_off)  // candidate logit beside its index (stage 2)
-        out_idx[vals_off + base + rk] = __float_as_int(part_max[2 * i + 1]);
+        out_idx[vals_off + base + rk] = __float_as_int(v);
+      if (top_out && rl < kTopC) {  // the row's best kTopC (stage 2 ranks only these)
+        top_out[1 + rl] = j;
+        top_out[1 + kTopC + rl] = __float_as_int(v);
+      }
     }
     if (tid == 0 && rank == 0) cand_count[row] = total;
+    if (top_out && tid == 0) *top_mark = C == 1 ? min(n, kTopC) : -1;
   } else if (rank == 0) {
     // ordered block-scan compaction over the whole row (tie-heavy rows)
     int64_t cb = 0;
-    const int chunk = kSwThreads * 4;
+    const int chunk = NT * 4;
     for (int c0 = 0; c0 < V; c0 += chunk) {
       int flags = 0;
 #pragma unroll
@@ -542,6 +582,7 @@ __device__ __forceinline__ void sweep_row(
       __syncthreads();
     }
     if (tid == 0) cand_count[row] = cb;
+    if (top_out && tid == 0) *top_mark = -1;  // no top list: stage 2 reads the full list
   }
   if (tid == 0 && rank == 0) {
     if (threshold) threshold[row] = R;
@@ -551,7 +592,7 @@ __device__ __forceinline__ void sweep_row(
   if (C > 1) cl_sync_all();  // peers done reading my shared memory
 }
 
-__global__ void __launch_bounds__(kSwThreads, 4) retrieve_sweep_kernel(
+__global__ void __launch_bounds__(kRowThreads, kRowMinBlocks) retrieve_sweep_kernel(
     const float* __restrict__ logits, int64_t ld, int V, int k_fixed,
     const int32_t* __restrict__ d_k, float* __restrict__ group_max, int64_t gm_ld,
     float* __restrict__ threshold, double* __restrict__ lse, int32_t* __restrict__ cand_idx,
@@ -561,8 +602,15 @@ __global__ void __launch_bounds__(kSwThreads, 4) retrieve_sweep_kernel(
   const int C = (int)cl_nrank(), rank = (int)cl_rank();
   const int64_t row = blockIdx.x / C;
   if (rank == 0) sw_stamp(row, 0);
-  sweep_row(logits, ld, V, row, d_k ? d_k[row] : k_fixed, group_max, gm_ld, threshold, lse,
-            cand_idx, cand_ld, cand_count, sw_ring, C, rank);
+#ifdef FQ_HARS_STAMPS
+  if (g_sw_dbg && threadIdx.x == 0 && rank == 0) {  // SM of the row (phase scripts)
+    uint32_t smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    g_sw_dbg[(1536 + row) * 8] = smid;
+  }
+#endif
+  sweep_row<kRowThreads>(logits, ld, V, row, d_k ? d_k[row] : k_fixed, group_max, gm_ld,
+                         threshold, lse, cand_idx, cand_ld, cand_count, sw_ring, C, rank);
 }
 
 // ---------------------------------------------------------------------------
@@ -1068,6 +1116,48 @@ __device__ bool seq_less(const int32_t* a, int la, const int32_t* b, int lb) {
   return la < lb;
 }
 
+// Stage-2 inputs of one item that do not depend on stage 1 (beam-state
+// scalars, cumulative scores, old prefixes and history rows), prefetched by
+// every CTA of the fused step at its start so the CTA that ends up running the
+// item's stage 2 only has one dependent round trip left (counts, lse and a
+// window of each row's candidates). The prefix / history rows only when
+// 2 * K * max_len <= kPreCap.
+constexpr int kPreCap = 512;
+struct Stage2Pre {
+  int in[5];  // done, live, step, cur, fin_count
+  int rows_ok;
+  int64_t top_off;  // the rows' top lists at cand_idx[row * cand_ld + top_off] (0: none)
+  int32_t* top_mark;  // per-row top-list counts (-1: none), reset to 0 by stage 2
+  double fsc_last;
+  double cum[kMaxBeam];
+  int32_t ph[kPreCap];  // [K][max_len] prefixes, then [K][max_len] history rows
+};
+__device__ __forceinline__ void stage2_prefetch(Stage2Pre& p, int b, const fq_beam_state& st,
+                                                int K, int max_len, const int32_t* hist,
+                                                int cur, int64_t top_off, int32_t* top_mark) {
+  const int tid = threadIdx.x;
+  const bool rows_ok = 2 * K * max_len <= kPreCap;
+  if (tid == 0) {
+    p.top_off = top_off;
+    p.top_mark = top_mark;
+    p.in[0] = st.done[b];
+    p.in[1] = st.live[b];
+    p.in[2] = st.step[b];
+    p.in[3] = cur;
+    p.in[4] = st.fin_count[b];
+    p.fsc_last = st.fin_score[b * K + K - 1];
+    p.rows_ok = rows_ok ? 1 : 0;
+  }
+  if (tid < K) p.cum[tid] = st.cum[b * K + tid];
+  if (rows_ok) {
+    const int64_t row0 = (int64_t)b * K;
+    for (int i = tid; i < K * max_len; i += blockDim.x) {
+      p.ph[i] = st.prefix[row0 * max_len + i];
+      p.ph[K * max_len + i] = hist ? hist[row0 * max_len + i] : 0;
+    }
+  }
+}
+
 // Stage-2 body for item b (one CTA). Candidate lists, counts and lse are read
 // with ld.global.cg: in the fused step they were written by other CTAs of the
 // same grid (made visible by their fence + the arrival counter).
@@ -1076,7 +1166,7 @@ __device__ __forceinline__ void select_item(
     const int32_t* cand_idx, int64_t cand_ld, const int64_t* cand_count, fq_beam_state st, int K,
     int max_len, int eos, const double* __restrict__ len_pow, const int32_t* __restrict__ d_cur,
     int64_t max_steps, int64_t* row_tokens, int64_t* row_parents, int32_t* hist,
-    const int64_t vals_off = 0, int64_t* tok_sh = nullptr) {
+    const int64_t vals_off = 0, int64_t* tok_sh = nullptr, const Stage2Pre* pre = nullptr) {
   // dynamic smem: old prefixes [K][max_len], old hist [K][max_len], then the
   // candidate array (16-byte aligned)
   extern __shared__ int32_t sh[];
@@ -1091,15 +1181,44 @@ __device__ __forceinline__ void select_item(
 
   const int tid = threadIdx.x;
   const int64_t row0 = (int64_t)b * K;
-  int32_t* old_pref = sh;
-  int32_t* old_hist = sh + K * max_len;
+  const bool pre_rows = pre && pre->rows_ok;
+  int32_t* old_pref = pre_rows ? const_cast<int32_t*>(pre->ph) : sh;
+  int32_t* old_hist = old_pref + K * max_len;
+  // the rows' top lists [K][kTopSlots] (sweep_row), behind the candidates
+  int32_t* win = reinterpret_cast<int32_t*>(cands + kSelCap);
+  const bool use_win = pre && pre->top_off > 0;
+  __shared__ int s_top;  // every live row has a top list: rank only those
 
   // every input of the item in one round trip: state scalars, per-row counts
-  // and lse, old prefixes and whole history rows (no dependency on cur)
+  // and lse, old prefixes and whole history rows (no dependency on cur); with
+  // `pre` the stage-1-independent ones are already in shared memory and the
+  // round trip fetches the counts, lse and each row's first kCandWin
+  // candidates (index + logit)
   __shared__ int s_in[5];
   __shared__ int64_t cnt_s[kMaxBeam];
   __shared__ double lse_s[kMaxBeam], cum_s[kMaxBeam];
   __shared__ double s_fsc_last;
+  if (pre) {
+    if (tid < 5) s_in[tid] = pre->in[tid];
+    if (tid == 0) s_fsc_last = pre->fsc_last;
+    if (tid < K) {
+      cnt_s[tid] = __ldcg(cand_count + row0 + tid);
+      lse_s[tid] = __ldcg(lse + row0 + tid);
+      cum_s[tid] = pre->cum[tid];
+    }
+    if (use_win) {
+      for (int e = tid; e < K * kTopSlots; e += blockDim.x)
+        win[e] = e % kTopSlots ? __ldcg(cand_idx + (row0 + e / kTopSlots) * cand_ld +
+                                        pre->top_off + e % kTopSlots)
+                               : __ldcg(pre->top_mark + row0 + e / kTopSlots);
+    }
+    if (!pre_rows) {
+      for (int i = tid; i < K * max_len; i += blockDim.x) {
+        old_pref[i] = st.prefix[(int64_t)b * K * max_len + i];
+        if (hist) old_hist[i] = hist[row0 * max_len + i];
+      }
+    }
+  } else {
   if (tid == 0) {
     s_in[0] = st.done[b];
     s_in[1] = st.live[b];
@@ -1117,7 +1236,9 @@ __device__ __forceinline__ void select_item(
     old_pref[i] = st.prefix[(int64_t)b * K * max_len + i];
     if (hist) old_hist[i] = hist[row0 * max_len + i];
   }
+  }
   __syncthreads();
+  if (use_win && tid < K) pre->top_mark[row0 + tid] = 0;  // self-resetting (split counters)
   if (s_in[0]) {  // engine.py:148-155: dead rows get parent row0, token 0
     if (tid < K) {
       row_parents[row0 + tid] = row0;
@@ -1132,8 +1253,13 @@ __device__ __forceinline__ void select_item(
   const bool last_step = (int64_t)cur == max_steps - 1;
   if (hist && tid < K && cur < max_len) old_hist[tid * max_len + cur] = (int32_t)(row0 + tid);
   if (tid == 0) {
+    int top = use_win ? 1 : 0;
+    for (int i = 0; i < live; ++i) top &= win[i * kTopSlots] >= 0 ? 1 : 0;
+    s_top = top;
     offs[0] = 0;
-    for (int i = 0; i < live; ++i) offs[i + 1] = offs[i] + cnt_s[i];
+    // a row contributes at most K + live picks: its best K + live suffice
+    for (int i = 0; i < live; ++i)
+      offs[i + 1] = offs[i] + (top ? min(win[i * kTopSlots], K + live) : cnt_s[i]);
   }
   __syncthreads();
   const int64_t n_total = offs[live];
@@ -1145,6 +1271,13 @@ __device__ __forceinline__ void select_item(
     while (offs[i + 1] <= j) ++i;
     const int64_t r = row0 + i;
     const int64_t jj = j - offs[i];
+    if (s_top) {  // the row's top list, fetched with the counts
+      Cand c;
+      c.tok = win[i * kTopSlots + 1 + jj];
+      c.s = cum_s[i] + ((double)__int_as_float(win[i * kTopSlots + 1 + kTopC + jj]) - lse_s[i]);
+      c.beam = i;
+      return c;
+    }
     const int32_t tok = __ldcg(cand_idx + r * cand_ld + jj);
     // candidate logit stored beside the index by the fused stage 1 (one round trip)
     const double lg = (vals_off && cnt_s[i] <= vals_off)
@@ -1341,12 +1474,13 @@ __device__ __forceinline__ void stage2_and_next(
     int64_t max_steps, int64_t* row_tokens, int64_t* row_parents, int32_t* hist,
     const int64_t vals_off, const int cur0, const float* __restrict__ emb, int d,
     float emb_scale, const float* __restrict__ pos, float* __restrict__ x_next,
-    h16* __restrict__ x16_next, int batch, int* all_cnt, h16* __restrict__ x16_next_lo = nullptr) {
+    h16* __restrict__ x16_next, int batch, int* all_cnt, h16* __restrict__ x16_next_lo = nullptr,
+    const Stage2Pre* pre = nullptr) {
   __shared__ int64_t s_tok[kMaxBeam];
   select_item(b, logits, ld, lse, cand_idx, cand_ld, cand_count, st, K, max_len, eos, len_pow,
-              d_cur, max_steps, row_tokens, row_parents, hist, vals_off, s_tok);
+              d_cur, max_steps, row_tokens, row_parents, hist, vals_off, s_tok, pre);
   __syncthreads();
-  sw_stamp(blockIdx.x, 3);
+  sw_stamp(1024 + blockIdx.x, 0);  // stage-2 stamps of the fused step: rows 1024 +
   // next step's embedding of the item's rows (embed_scale_pos, kernels.py:143-151:
   // fp32 emb * sqrt(d), then + PE[cur + 1], two roundings), so the decode step
   // needs no separate embedding launch
@@ -1374,6 +1508,7 @@ __device__ __forceinline__ void stage2_and_next(
     }
   }
   __syncthreads();
+  sw_stamp(1024 + blockIdx.x, 1);
   if (threadIdx.x == 0) {
     __threadfence();
     if (atomicAdd(all_cnt, 1) == batch - 1) {  // every item read d_cur: advance it
@@ -1392,7 +1527,7 @@ __device__ __forceinline__ void stage2_and_next(
 // fq_hars_groups + fq_retrieve + fq_hars_select + fq_step_advance, and lets
 // the selection of early items overlap the retrieve of the others.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kSwThreads) hars_step_kernel(
+__global__ void __launch_bounds__(kRowThreads, kRowMinBlocks) hars_step_kernel(
     const float* __restrict__ logits, int64_t ld, int V, fq_beam_state st, int batch, int K,
     int max_len, int eos, const double* __restrict__ len_pow, int32_t* d_cur, int64_t max_steps,
     double* lse, int32_t* cand_idx, int64_t cand_ld, int64_t* cand_count, int* item_cnt,
@@ -1403,14 +1538,28 @@ __global__ void __launch_bounds__(kSwThreads) hars_step_kernel(
   const int C = (int)cl_nrank(), rank = (int)cl_rank();
   const int64_t row = blockIdx.x / C;
   const int b = (int)(row / K), i = (int)(row % K);
+  if (rank == 0) sw_stamp(row, 0);
+#ifdef FQ_HARS_STAMPS
+  if (g_sw_dbg && threadIdx.x == 0 && rank == 0) {  // SM of the row (phase scripts)
+    uint32_t smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    g_sw_dbg[(1536 + row) * 8] = smid;
+  }
+#endif
   // the position is only advanced after every item has passed its read below
   const int cur0 = *d_cur;
   const int live = st.live[b];
   const int k = (!st.done[b] && i < live) ? min(K + live, V) : 0;  // hars_groups
-  extern __shared__ __align__(16) float4 sw_ring[];  // aliases stage 2's dynamic smem
   const int64_t vals_off = cand_ld / 2 >= kSwThreads * 2 ? cand_ld / 2 : 0;
-  sweep_row(logits, ld, V, row, k, nullptr, 0, nullptr, lse, cand_idx, cand_ld, cand_count,
-            sw_ring, C, rank, vals_off);
+  const int64_t top_off =
+      (C == 1 && vals_off && vals_off + 2 * kRowThreads <= cand_ld - kTopSlots) ? cand_ld - kTopSlots : 0;
+  __shared__ Stage2Pre pre;  // in case this CTA runs the item's stage 2
+  stage2_prefetch(pre, b, st, K, max_len, hist, cur0, top_off, item_cnt + batch + 1);
+  extern __shared__ __align__(16) float4 sw_ring[];  // aliases stage 2's dynamic smem
+  sweep_row<kRowThreads>(logits, ld, V, row, k, nullptr, 0, nullptr, lse, cand_idx, cand_ld,
+                         cand_count, sw_ring, C, rank, vals_off,
+                         top_off ? cand_idx + row * cand_ld + top_off : nullptr,
+                         item_cnt + batch + 1 + row);
   __shared__ int s_last;
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -1424,7 +1573,7 @@ __global__ void __launch_bounds__(kSwThreads) hars_step_kernel(
   __threadfence();
   stage2_and_next(b, logits, ld, lse, cand_idx, cand_ld, cand_count, st, K, max_len, eos,
                   len_pow, d_cur, max_steps, row_tokens, row_parents, hist, vals_off, cur0, emb,
-                  d, emb_scale, pos, x_next, x16_next, batch, all_cnt, x16_next_lo);
+                  d, emb_scale, pos, x_next, x16_next, batch, all_cnt, x16_next_lo, &pre);
 }
 
 // The fused HARS step on the balanced split (few rows: rows < 2 x SMs): as
@@ -1636,7 +1785,8 @@ using namespace fq;
 extern "C" {
 
 static size_t sel_smem(int64_t beam, int64_t max_len) {
-  return (size_t)((2 * beam * max_len + 3) & ~3) * sizeof(int32_t) + kSelCap * sizeof(Cand);
+  return (size_t)((2 * beam * max_len + 3) & ~3) * sizeof(int32_t) + kSelCap * sizeof(Cand) +
+         (size_t)beam * kTopSlots * sizeof(int32_t);
 }
 
 // FQ_RETRIEVE_TWO_PASS=1 selects the two-pass kernel for every k (A/B runs).
@@ -1734,8 +1884,8 @@ int fq_retrieve(const float* logits, int64_t ld, int64_t rows, int64_t vocab, in
   }
   if (k >= 1 && k <= 32 && (ld % 4) == 0 && ((uintptr_t)logits & 15) == 0 &&
       !retrieve_two_pass_forced()) {
-    launch_kernel(retrieve_sweep_kernel, (unsigned)(rows * kSwSplit), kSwThreads,
-                  (size_t)kSwP * kSwThreads * sizeof(float4), as_stream(stream),
+    launch_kernel(retrieve_sweep_kernel, (unsigned)(rows * kSwSplit), kRowThreads,
+                  (size_t)kSwP * kRowThreads * sizeof(float4), as_stream(stream),
                   (unsigned)kSwSplit,
                   logits, ld, (int)vocab, (int)k, d_k, group_max, gm_ld, threshold, lse,
                   cand_idx, cand_ld, cand_count);
@@ -1802,9 +1952,9 @@ int fq_hars_step(const float* logits, int64_t ld, fq_beam_state st, int64_t batc
     return launch_status("fq_hars_step");
   }
   const size_t smem = std::max(sel_smem(beam, max_len),
-                               (size_t)kSwP * kSwThreads * sizeof(float4));
+                               (size_t)kSwP * kRowThreads * sizeof(float4));
   FQ_CHECK_ARG(smem <= 96 * 1024, FQ_ERR_CAPACITY, "fq_hars_step: max_len too large");
-  launch_kernel(hars_step_kernel, (unsigned)(batch * beam * kSwSplit), kSwThreads, smem,
+  launch_kernel(hars_step_kernel, (unsigned)(batch * beam * kSwSplit), kRowThreads, smem,
                 as_stream(stream), (unsigned)kSwSplit, logits, ld, (int)vocab, st, (int)batch, (int)beam, (int)max_len, (int)eos,
                 len_pow, d_cur, max_steps, lse, cand_idx, cand_ld, cand_count, counters,
                 counters + batch, row_tokens, row_parents, hist, x_next ? emb : nullptr,

@@ -354,6 +354,17 @@ int main() {
     snprintf(nm, 64, "bulk+work NB=12 G=444 R=%.1f", R);
     rep(nm, time_graph([&](cudaStream_t s, int i) { bulk_work<12><<<sms * 3, 288, 12 * 256 * 16, s>>>((const float4*)buf[i % 3], n / 4, R, sink); }, reps));
   }
+  // row-per-CTA geometry of the HARS step (512 rows of 125 KB over 148 SMs)
+  {
+    cudaFuncSetAttribute(cpa_stream<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    rep("rows: ldg U=4 G=512", time_graph([&](cudaStream_t s, int i) { ldg_stream<4><<<512, 256, 0, s>>>((const float4*)buf[i % 3], n / 4, sink); }, reps));
+    rep("rows: cp.async P=8 G=512", time_graph([&](cudaStream_t s, int i) { cpa_stream<8><<<512, 256, 8 * 256 * 16, s>>>((const float4*)buf[i % 3], n / 4, sink); }, reps));
+    cudaFuncSetAttribute(cpa_mode<8, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    rep("rows: mode4 G=512", time_graph([&](cudaStream_t s, int i) { cpa_mode<8, 4><<<512, 256, 8 * 256 * 16, s>>>((const float4*)buf[i % 3], n / 4, sink); }, reps));
+    rep("rows: mode4 G=592", time_graph([&](cudaStream_t s, int i) { cpa_mode<8, 4><<<592, 256, 8 * 256 * 16, s>>>((const float4*)buf[i % 3], n / 4, sink); }, reps));
+    rep("rows: mode4 G=1024 (half rows)", time_graph([&](cudaStream_t s, int i) { cpa_mode<8, 4><<<1024, 256, 8 * 256 * 16, s>>>((const float4*)buf[i % 3], n / 4, sink); }, reps));
+    rep("rows: ldg U=4 G=1024", time_graph([&](cudaStream_t s, int i) { ldg_stream<4><<<1024, 256, 0, s>>>((const float4*)buf[i % 3], n / 4, sink); }, reps));
+  }
   // reference: empty-ish launch
   rep("ldg U=8 G=592 tiny (n=592*256*4)", time_graph([&](cudaStream_t s, int i) { ldg_stream<8><<<592, 256, 0, s>>>((const float4*)buf[i % 3], 592 * 256, sink); }, reps));
   return 0;

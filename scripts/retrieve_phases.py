@@ -9,7 +9,7 @@ import torch
 
 from paper_2010_13887_b200 import _abi, decode as D
 
-lib = _abi.load()
+lib = _abi.load()  # stamps need a -DFQ_HARS_STAMPS build: FQ_LIB=build/variants/stamps.so
 lib.fq_retrieve_debug_timestamps.argtypes = [ctypes.c_void_p]
 R, V = 512, 32000
 lgs = [torch.randn(R, V, device="cuda") for _ in range(3)]

@@ -11,7 +11,7 @@ import torch
 
 from paper_2010_13887_b200 import _abi, decode as D
 
-lib = _abi.load()
+lib = _abi.load()  # stamps need a -DFQ_HARS_STAMPS build: FQ_LIB=build/variants/stamps.so
 lib.fq_retrieve_debug_timestamps.argtypes = [ctypes.c_void_p]
 B, K, V, S = (int(x) for x in os.environ.get("SHAPE", "128,4,32000,64").split(","))
 R = B * K
