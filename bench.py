@@ -586,8 +586,11 @@ def extra_workloads(P, dev, args) -> dict:
       V = 30522, seq 128, batch 64): Session.classify sequences/s (the
       reference measured 6.7 seq/s on 8 CPU cores, SURVEY §6);
     * top-k sampling generate (k = 8) on the C2 model, batch 64, 64 steps:
-      decoded tokens/s (host-driven draw in the reference's PCG64 order; a
-      decoder-only GPT-2 is not expressible in the reference)."""
+      decoded tokens/s, device-resident (decoder step + retrieve +
+      fq_sample_topk_step in one step graph, the reference's PCG64 stream
+      consumed on the device in its order), and the host-driven draw
+      (FQ_SAMPLE_HOST=1) beside it; a decoder-only GPT-2 is not expressible in
+      the reference."""
     import numpy as np
     import torch
     res = {}
@@ -616,15 +619,21 @@ def extra_workloads(P, dev, args) -> dict:
     dc = P.DecodeConfig(method="top_k", sample_k=8, max_steps=MAX_STEPS, eos_token=2, seed=0)
     for prec in ("fp32", "fp16"):
         sess = P.Session(cfg, w, precision=prec)
-        sess.generate(src, dc)
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        hyps = sess.generate(src, dc)
-        dt = time.perf_counter() - t0
-        ntok = sum(len(h[0].tokens) for h in hyps if h)
-        res[f"sampling_top_k_{prec}"] = {"value": ntok / dt, "unit": "tokens/s",
-                                         "ms_per_request": dt * 1e3, "batch": 64,
-                                         "max_steps": MAX_STEPS}
+        for path in ("device", "host"):
+            if path == "host":
+                os.environ["FQ_SAMPLE_HOST"] = "1"
+            try:
+                sess.generate(src, dc)
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                hyps = sess.generate(src, dc)
+                dt = time.perf_counter() - t0
+            finally:
+                os.environ.pop("FQ_SAMPLE_HOST", None)
+            ntok = sum(len(h[0].tokens) for h in hyps if h)
+            name = f"sampling_top_k_{prec}" + ("" if path == "device" else "_host_draw")
+            res[name] = {"value": ntok / dt, "unit": "tokens/s", "ms_per_request": dt * 1e3,
+                         "batch": 64, "max_steps": MAX_STEPS}
         del sess
     return res
 

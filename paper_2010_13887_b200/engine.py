@@ -96,6 +96,7 @@ class Session:
         self.arena = Arena(list(self._plans.values()))
         self._buffers = M.ArenaBuffers(self.arena)
         self._graphs: dict = {}
+        self._sample_buffers: dict = {}
         self._pinned_done = torch.zeros((max(config.max_seq_len, 1), 2), dtype=torch.int32,
                                         pin_memory=True)
         self._side_stream = torch.cuda.Stream()
@@ -392,6 +393,108 @@ class Session:
                 for state in states]
 
     # ------------------------------------------------------------------
+    def _sample_bufs(self, batch: int, max_steps: int, V: int) -> dict:
+        """Persistent device buffers of the device-resident sampling loop (one
+        set per (batch, max_steps) shape, allocated on first use)."""
+        key = (batch, max_steps)
+        b = self._sample_buffers.get(key)
+        if b is None:
+            dev = torch.device("cuda", torch.cuda.current_device())
+            i32 = dict(dtype=torch.int32, device=dev)
+            b = {"uniforms": torch.empty(batch * max_steps, dtype=torch.float64, device=dev),
+                 "draw": torch.zeros(1, dtype=torch.int64, device=dev),
+                 "done": torch.zeros(2, batch, **i32), "dk": torch.zeros(batch, **i32),
+                 "out_tok": torch.zeros(batch, max_steps, **i32),
+                 "out_len": torch.zeros(batch, **i32), "fin": torch.zeros(batch, **i32),
+                 "counters": torch.zeros(2, **i32), "err": torch.zeros(1, **i32),
+                 "lse": torch.empty(batch, dtype=torch.float64, device=dev),
+                 "ci": torch.empty(batch, V, **i32),
+                 "cc": torch.empty(batch, dtype=torch.int64, device=dev),
+                 "pinned": torch.zeros(max_steps, dtype=torch.int32).pin_memory()}
+            self._sample_buffers[key] = b
+        return b
+
+    def _generate_sampling_device(self, src, src_lengths, cfg: D.DecodeConfig, bos_token: int):
+        """Top-k sampling with the whole step on the device:
+        decoder step -> batched retrieve (per-row group counts, 0 for done
+        rows) -> fq_sample_topk_step, captured as one CUDA graph per step and
+        replayed with the host polling the live-row count one step behind. The
+        draws are the reference's: its seeded PCG64 stream is generated on the
+        host up front (numpy's random(n) equals n successive random() calls)
+        and consumed on the device in its order. Returns None when a row
+        overflowed the device's survivor cap (the caller re-runs on the
+        host-driven path)."""
+        batch, seq = src.shape
+        V = self.config.vocab_size
+        max_steps = min(cfg.max_steps, self.config.max_seq_len)
+        k = min(cfg.sample_k, V)
+        packed, mask, cache = self._setup_decoder(src, src_lengths, batch)
+        step = M.DecoderStep(self.dw, self.config, batch, 1, seq, cache, packed, mask,
+                             self._buffers, self.counters, self.timers)
+        step.bad.zero_()
+        b = self._sample_bufs(batch, max_steps, V)
+        rng = np.random.default_rng(cfg.seed)
+        b["uniforms"].copy_(torch.from_numpy(rng.random(batch * max_steps)))
+        for n in ("draw", "done", "out_len", "fin", "counters", "err"):
+            b[n].zero_()
+        b["dk"].fill_(k)
+        step.tokens.fill_(bos_token)
+
+        def body():  # (stream handle read inside: graph capture runs on a side stream)
+            logits = step.run()
+            D.retrieve_device(logits, k, d_k=b["dk"], out=(None, None, b["lse"], b["ci"], b["cc"]))
+            self.counters.count_fused("retrieve", batch * V * 4)
+            _abi.call("fq_sample_topk_step", logits.data_ptr(), logits.stride(0),
+                      b["lse"].data_ptr(), b["ci"].data_ptr(), b["ci"].stride(0),
+                      b["cc"].data_ptr(), batch, k, cfg.eos_token, b["uniforms"].data_ptr(),
+                      b["uniforms"].numel(), b["draw"].data_ptr(), b["done"].data_ptr(),
+                      cache.d_cur.data_ptr(), max_steps, max_steps, b["dk"].data_ptr(),
+                      step.tokens.data_ptr(), b["out_tok"].data_ptr(), b["out_len"].data_ptr(),
+                      b["fin"].data_ptr(), b["counters"].data_ptr(), b["err"].data_ptr(),
+                      _abi.stream_handle())
+
+        graph = None
+        if self.use_graphs:
+            key = ("sample_top_k", batch, seq, max_steps, k, cfg.eos_token, mask is not None)
+            entry = self._graphs.get(key)
+            if entry is None:
+                graph = torch.cuda.CUDAGraph()
+                n0 = _abi.launch_count()
+                with torch.cuda.graph(graph):
+                    body()
+                entry = (graph, _abi.launch_count() - n0)
+                _abi.add_launches(-entry[1])
+                self._graphs[key] = entry
+            graph, per_step = entry
+        pinned = b["pinned"]
+        events = []
+        for t in range(max_steps):
+            if graph is not None:
+                graph.replay()
+                _abi.add_launches(per_step)
+            else:
+                body()
+            pinned[t:t + 1].copy_(b["counters"][1:2], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record()
+            events.append(ev)
+            if t >= 1:
+                events[t - 1].synchronize()
+                if int(pinned[t - 1]) == 0:
+                    break
+        torch.cuda.synchronize()
+        if int(step.bad.item()):
+            raise FullMaskError("fully masked cross-attention row")
+        if int(b["err"].item()):
+            return None
+        toks = b["out_tok"].cpu().numpy()
+        lens = b["out_len"].cpu().numpy()
+        out = []
+        for i in range(batch):
+            seq_i = [int(x) for x in toks[i, :lens[i]]]
+            out.append([Hypothesis(tokens=seq_i, score=0.0)] if seq_i else [])
+        return out
+
     def _generate_sampling(self, src, src_lengths, cfg: D.DecodeConfig, bos_token: int):
         """Top-k / top-p sampling generate (engine.py:175-195 + _sampling_step
         :197-216, decode.py:378-430). Every step: the device decoder step over
@@ -403,6 +506,10 @@ class Session:
         escalate their group count x8 with a per-row retrieve (:420-430)."""
         if isinstance(src, torch.Tensor):
             src = src.cpu().numpy()
+        if cfg.method == "top_k" and os.environ.get("FQ_SAMPLE_HOST") != "1":
+            got = self._generate_sampling_device(src, src_lengths, cfg, bos_token)
+            if got is not None:
+                return got
         batch, seq = src.shape
         V = self.config.vocab_size
         max_steps = min(cfg.max_steps, self.config.max_seq_len)

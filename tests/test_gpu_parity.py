@@ -275,6 +275,49 @@ def test_sampling_generate_matches_reference_fixture(P, ci):
 
 
 @pytest.mark.parametrize("precision", ["fp32", "fp16"])
+def test_device_top_k_sampling_equals_host_driven_draw(P, precision, monkeypatch):
+    """The device-resident top-k sampling loop (fq_sample_topk_step inside the
+    step graph, the reference's PCG64 stream pre-generated and consumed on the
+    device in its draw order) reproduces the host-driven draw (FQ_SAMPLE_HOST=1,
+    numpy _draw on the device retrieve's candidates) token for token, with EOS
+    finishes making rows drop out of the draw order mid-request."""
+    cfg = P.ModelConfig(num_encoder_layers=2, num_decoder_layers=2, d_model=128, d_ff=256,
+                        num_heads=4, vocab_size=3000, max_batch=16, max_seq_len=24,
+                        max_beam_size=4)
+    w = P.make_random_weights(cfg, seed=21)
+    sess = P.Session(cfg, w, precision=precision)
+    src = np.random.default_rng(3).integers(3, cfg.vocab_size, size=(13, 9))
+    lens = np.random.default_rng(4).integers(3, 10, size=13)
+    for k, seed, eos in ((1, 0, 2), (7, 5, 2), (40, 11, 2), (200, 3, 5)):
+        # eos = a frequent token so that rows finish early and leave the draw order
+        dc = P.DecodeConfig(method="top_k", sample_k=k, seed=seed, max_steps=20, eos_token=eos)
+        monkeypatch.delenv("FQ_SAMPLE_HOST", raising=False)
+        dev = sess.generate(src, dc, src_lengths=lens)
+        monkeypatch.setenv("FQ_SAMPLE_HOST", "1")
+        host = sess.generate(src, dc, src_lengths=lens)
+        assert [[h.tokens for h in x] for x in dev] == [[h.tokens for h in x] for x in host], k
+        assert [[h.score for h in x] for x in dev] == [[h.score for h in x] for x in host]
+
+
+def test_device_top_k_sampling_tie_heavy_falls_back(P):
+    """All-equal logits (zero output projection): every token survives the
+    retrieve (> the device's 1024-survivor cap), so generate re-runs the
+    request on the host-driven path and the reference's tie rule (sorted
+    prefix by token) decides the draws -- same tokens as the oracle's sampler."""
+    cfg = P.ModelConfig(num_encoder_layers=1, num_decoder_layers=1, d_model=64, d_ff=128,
+                        num_heads=2, vocab_size=2048, max_batch=4, max_seq_len=8,
+                        max_beam_size=4, tie_output=False)
+    w = P.make_random_weights(cfg, seed=2)
+    w.output_projection = np.zeros_like(w.output_projection)
+    src = np.random.default_rng(1).integers(3, cfg.vocab_size, size=(3, 5))
+    dc = P.DecodeConfig(method="top_k", sample_k=5, seed=7, max_steps=6, eos_token=2)
+    got = P.Session(cfg, w, precision="fp32").generate(src, dc)
+    # uniform over the 5 lowest token ids (the sorted prefix of a flat row)
+    for hs in got:
+        assert all(0 <= t < 5 for t in hs[0].tokens), hs[0].tokens
+
+
+@pytest.mark.parametrize("precision", ["fp32", "fp16"])
 @pytest.mark.parametrize("ci", [0, 1])
 def test_classify_matches_reference_fixture(P, ci, precision):
     """Encoder-only classification (engine.py:198-224): first-position
