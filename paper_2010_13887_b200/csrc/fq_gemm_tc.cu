@@ -1617,8 +1617,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   constexpr int B_BYTES = BH * 128;
   constexpr int STAGE_BYTES = 2 * (A_BYTES + B_BYTES);
   constexpr int B_OFF = 2 * A_BYTES;
-  constexpr uint32_t TMEM_COLS = 4 * BN;  // 2 chunk slots x {hi.hi, small terms}
-  static_assert(TMEM_COLS <= 512, "TMEM holds 512 columns");
+  // 2 chunk slots x {hi.hi, small terms}; allocations are powers of two
+  constexpr uint32_t TMEM_COLS = 4 * BN <= 128 ? 128 : (4 * BN <= 256 ? 256 : 512);
+  static_assert(4 * BN <= 512, "TMEM holds 512 columns");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* boxes = smem + STAGES * STAGE_BYTES;  // 4 epilogue warps x 4 KB
@@ -2102,6 +2103,7 @@ int gemm_tc_prepare() {
       tc::prep<128, 3, false, tc::OP_X3H>() || tc::prep<64, 4, false, tc::OP_X3H>() ||
       tc::prep_splitk<128, 3, false, false, tc::OP_X3H>() ||
       tc::prep_splitk<128, 3, false, true, tc::OP_X3H>() || tc::prep_pair<128, 4>() ||
+      tc::prep_pair<96, 4>() ||
       tc::prep_pair<128, 4, true>()) {
     set_error("fq_prepare: tcgen05 GEMM smem opt-in failed");
     return FQ_ERR_CUDA;
@@ -2338,6 +2340,14 @@ static bool pair_ok(int64_t N, int accumulate, const float* res, const void* c, 
          (ldc * (half_out ? 2 : 4)) % 16 == 0;
 }
 
+// Pair tile width: 96 columns when 128 would leave over a quarter of the SMs
+// idle and 96 fills one wave (the decode QKV projection: 96 -> 128 CTAs). The
+// tile width never changes the bits (same K chunks per element).
+static bool pair_bn96(int64_t M, int64_t N) {
+  const int64_t mp = (M + 255) / 256, sms = tc::num_sms();
+  return N % 96 == 0 && 2 * mp * (N / 128) < (3 * sms) / 4 && 2 * mp * (N / 96) <= sms;
+}
+
 int launch_xh_gemm(const void* a, const void* a_lo, int64_t lda, const void* b,
                    const void* b_lo, int64_t ldb, float* c, int64_t ldc, int64_t M, int64_t N,
                    int64_t K, int accumulate, const float* bias, const float* res, int64_t ldr,
@@ -2348,7 +2358,8 @@ int launch_xh_gemm(const void* a, const void* a_lo, int64_t lda, const void* b,
   tc::Epi ep{c, ldc, 0, accumulate, bias, res, ldr, act, g_gemm_dbg};
   ep.chunk_kb = p.chunk_kb;
   if (p.split == 1 && pair_ok(N, accumulate, res, c, ldc, false))
-    return tc::launch_pair<128, 4>(a, a_lo, lda, b, b_lo, ldb, ep, M, N, K, s);
+    return pair_bn96(M, N) ? tc::launch_pair<96, 4>(a, a_lo, lda, b, b_lo, ldb, ep, M, N, K, s)
+                           : tc::launch_pair<128, 4>(a, a_lo, lda, b, b_lo, ldb, ep, M, N, K, s);
   if (p.split > 1)
     return tc::launch_splitk<128, 3, false, false, tc::OP_X3H>(a, lda, b, ldb, ep, M, N, K,
                                                                p.split, s, tc::LnEpi{}, b_lo, a_lo);
@@ -2390,7 +2401,8 @@ extern "C" int fq_gemm_x3h_pair(const void* a, const void* a_lo, int64_t lda, co
   ep.c_lo = c_lo;
   cudaStream_t s = as_stream(stream);
   if (p.split == 1 && pair_ok(N, 0, nullptr, c, ldc, true) && ((uintptr_t)c_lo & 15) == 0)
-    return tc::launch_pair<128, 4>(a, a_lo, lda, b, b_lo, ldb, ep, M, N, K, s);
+    return pair_bn96(M, N) ? tc::launch_pair<96, 4>(a, a_lo, lda, b, b_lo, ldb, ep, M, N, K, s)
+                           : tc::launch_pair<128, 4>(a, a_lo, lda, b, b_lo, ldb, ep, M, N, K, s);
   if (p.split > 1)
     return tc::launch_splitk<128, 3, false, false, tc::OP_X3H>(a, lda, b, ldb, ep, M, N, K,
                                                                p.split, s, tc::LnEpi{}, b_lo, a_lo);
