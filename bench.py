@@ -398,8 +398,8 @@ def time_mode(P, cfg, host_w, precision, src_host, args, world, dev, flush, barr
 
 def gemm_traffic(precision: str):
     """Mean DRAM bytes (read + write) per tc_gemm launch of one decode step,
-    from the committed ncu capture of this precision (profiles/r2/), or None."""
-    path = os.path.join(ROOT, "profiles", "r2", f"ncu_gemm_traffic_{precision}.json")
+    from the committed ncu capture of this precision (profiles/r2b/), or None."""
+    path = os.path.join(ROOT, "profiles", "r2b", f"ncu_gemm_traffic_{precision}.json")
     if os.path.exists(path):
         return json.load(open(path)).get("bytes_per_launch_mean")
     return None
@@ -415,7 +415,7 @@ def roofline_gemm(sess, src_dev, dc, cfg, batch, steps_run, peak, peak_source, d
                   "(encoder, cross-K/V, 6 per decoder layer per step, logits)",
         "bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
         "frac": achieved / peak, "traffic": gemm_traffic(sess.precision),
-        "traffic_source": "profiles/r2/ncu_gemm_traffic_<precision>.json (ncu, one decode "
+        "traffic_source": "profiles/r2b/ncu_gemm_traffic_<precision>.json (ncu, one decode "
                           "step's GEMM launches, mean dram bytes read + written per launch)",
         "launches": g["n"], "us_per_launch_mean": g["us"] / max(g["n"], 1),
         "flops_per_launch_mean": fl["total"] / max(g["n"], 1),

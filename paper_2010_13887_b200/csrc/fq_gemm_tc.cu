@@ -1592,9 +1592,13 @@ __device__ __forceinline__ void tma_load_2d_pair(const CUtensorMap* map, uint32_
       : "memory");
 }
 
+// Arrive on the pair leader's TMEM-slot barrier. Only the TMEM reads must be
+// complete (tcgen05.wait::ld + tcgen05.fence::before_thread_sync order them);
+// no smem / global data is handed over, so the default CTA-scope release
+// suffices -- .release.cluster compiled to MEMBAR.ALL.GPU per chunk (ncu
+// membar stalls, 14% of the pair GEMM's samples).
 __device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
-               : "memory");
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
 
 // HS: the exact mode's logits GEMM with the HARS stage-1 statistics epilogue
