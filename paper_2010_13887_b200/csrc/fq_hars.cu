@@ -344,8 +344,13 @@ __device__ __forceinline__ void sweep_row(
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int kk = k / (k & -k) * ((k & -k) > 4 ? (k & -k) / 4 : 1);  // k / gcd(k, 4)
   const int T = NT - NT % kk;
-  const int nvec = V >> 2;
-  const float4* x4 = reinterpret_cast<const float4*>(x);
+  // rows need not be 16-byte aligned (e.g. V = 50257): the first hd < 4
+  // elements are a scalar head, vector v then holds columns hd + 4v + c, so
+  // lane c of thread t stays in group (hd + 4t + c) % k (part_max[4t + c])
+  const int hd = min(V, (int)((4 - ((reinterpret_cast<uintptr_t>(x) >> 2) & 3)) & 3));
+  const int hk = hd % k;
+  const int nvec = (V - hd) >> 2;
+  const float4* x4 = reinterpret_cast<const float4*>(x + hd);
   const bool act = tid < T;
   constexpr float NEG = -INFINITY;
   const int itmax = (nvec + T - 1) / T;      // iterations of thread 0
@@ -379,7 +384,7 @@ __device__ __forceinline__ void sweep_row(
   __syncthreads();
   for (int g = w; g < k; g += NT / 32) {
     float mm = NEG;
-    for (int e = g + lane * k; e < 4 * T; e += 32 * k) mm = fmaxf(mm, part_max[e]);
+    for (int e = (g - hk + k) % k + lane * k; e < 4 * T; e += 32 * k) mm = fmaxf(mm, part_max[e]);
     mm = warp_max(mm);
     if (lane == 0) gmax_s[g] = mm;
   }
@@ -442,7 +447,7 @@ __device__ __forceinline__ void sweep_row(
         for (int c = 0; c < 4; ++c) {
           if (e4[c] >= Rp) {
             const int p = atomicAdd(&s_cnt, 1);
-            if (p < SC) { sv_idx[p] = 4 * v + c; sv_val[p] = e4[c]; }
+            if (p < SC) { sv_idx[p] = hd + 4 * v + c; sv_val[p] = e4[c]; }
           }
         }
       }
@@ -457,8 +462,9 @@ __device__ __forceinline__ void sweep_row(
     part_max[4 * tid] = gm[0]; part_max[4 * tid + 1] = gm[1];
     part_max[4 * tid + 2] = gm[2]; part_max[4 * tid + 3] = gm[3];
   }
-  if (tid == 0 && rank == C - 1) {  // V % 4 tail (the last rank)
-    for (int j = nvec << 2; j < V; ++j) {
+  if (tid == 0 && rank == C - 1) {  // scalar head and tail (the last rank)
+    for (int jj = 0; jj < hd + (V - hd - (nvec << 2)); ++jj) {
+      const int j = jj < hd ? jj : hd + (nvec << 2) + (jj - hd);
       const float xv = x[j];
       if (xv > m + 64.f || m == NEG) {
         if (xv != NEG) {
@@ -477,13 +483,16 @@ __device__ __forceinline__ void sweep_row(
   __syncthreads();
   for (int g = w; g < k; g += NT / 32) {
     float mm = NEG;
-    for (int e = g + lane * k; e < 4 * T; e += 32 * k) mm = fmaxf(mm, part_max[e]);
+    for (int e = (g - hk + k) % k + lane * k; e < 4 * T; e += 32 * k) mm = fmaxf(mm, part_max[e]);
     mm = warp_max(mm);
     if (lane == 0) gmax_s[g] = mm;
   }
   __syncthreads();
   if (tid == 0 && rank == C - 1)
-    for (int j = nvec << 2; j < V; ++j) gmax_s[j % k] = fmaxf(gmax_s[j % k], x[j]);
+    for (int jj = 0; jj < hd + (V - hd - (nvec << 2)); ++jj) {
+      const int j = jj < hd ? jj : hd + (nvec << 2) + (jj - hd);
+      gmax_s[j % k] = fmaxf(gmax_s[j % k], x[j]);
+    }
   if (C > 1) cl_sync_all();  // both halves' group maxima complete
   if (w == 0) {
     float gv = NEG;
@@ -1882,8 +1891,7 @@ int fq_retrieve(const float* logits, int64_t ld, int64_t rows, int64_t vocab, in
                   cand_count);
     return launch_status("fq_retrieve");
   }
-  if (k >= 1 && k <= 32 && (ld % 4) == 0 && ((uintptr_t)logits & 15) == 0 &&
-      !retrieve_two_pass_forced()) {
+  if (k >= 1 && k <= 32 && ((uintptr_t)logits & 3) == 0 && !retrieve_two_pass_forced()) {
     launch_kernel(retrieve_sweep_kernel, (unsigned)(rows * kSwSplit), kRowThreads,
                   (size_t)kSwP * kRowThreads * sizeof(float4), as_stream(stream),
                   (unsigned)kSwSplit,
