@@ -587,7 +587,7 @@ def extra_workloads(P, dev, args) -> dict:
       reference measured 6.7 seq/s on 8 CPU cores, SURVEY §6);
     * top-k sampling generate (k = 8) on the C2 model, batch 64, 64 steps:
       decoded tokens/s, device-resident (decoder step + retrieve +
-      fq_sample_topk_step in one step graph, the reference's PCG64 stream
+      fq_sample_step in one step graph, the reference's PCG64 stream
       consumed on the device in its order), and the host-driven draw
       (FQ_SAMPLE_HOST=1) beside it; a decoder-only GPT-2 is not expressible in
       the reference."""

@@ -386,26 +386,30 @@ int fq_beam_state_init(fq_beam_state st, int64_t batch, int64_t beam, int64_t ma
 /* *d_cur += 1 (KVCache.end_step, model.py:508-512). */
 int fq_step_advance(int32_t* d_cur, fq_stream_t stream);
 
-/* Device-resident top-k sampling step (Session._sampling_step, engine.py:175-195;
- * sample_top_k + _draw, decode.py:378-400) for every row of one decode step,
- * after fq_retrieve with per-row group counts dk (k live, 0 done): survivors
- * sorted by (-logit, token), the first k kept, probs exp(f64 logit - lse),
- * r = u * probs.sum() (numpy pairwise order), first token with r <= cumsum.
- * uniforms: the reference's PCG64 stream in its draw order (one per live row
- * per step, rows in batch order), consumed through *draw. done int32 [2][batch]
- * (step parity t = *d_cur: read [t & 1], write [(t + 1) & 1]); writes
- * out_tok[b][t] (int32 [batch][max_len]), out_len, fin (EOS), the next
- * step's dk_next / tokens (0 for done rows); the last CTA advances *draw and
- * *d_cur and stores the live-row count in counters[1] (counters int32 [2],
- * zero once). err != 0: a row had > 1024 survivors (tie-heavy) or the
- * uniform stream ran out -- re-run on the host-driven path. */
-int fq_sample_topk_step(const float* logits, int64_t ld, const double* lse,
-                        const int32_t* cand_idx, int64_t cand_ld, const int64_t* cand_count,
-                        int64_t batch, int64_t k, int64_t eos, const double* uniforms,
-                        int64_t n_uniforms, int64_t* draw, int32_t* done, int32_t* d_cur,
-                        int64_t max_steps, int64_t max_len, int32_t* dk_next, int64_t* tokens,
-                        int32_t* out_tok, int32_t* out_len, int32_t* fin, int32_t* counters,
-                        int32_t* err, fq_stream_t stream);
+/* Device-resident sampling step (Session._sampling_step, engine.py:175-195;
+ * sample_top_k / sample_top_p + _draw, decode.py:378-430) for every row of one
+ * decode step, after fq_retrieve with per-row group counts dk (live rows: k
+ * for top-k, `groups` for top-p; 0 done): survivors sorted by (-logit, token),
+ * probs exp(f64 logit - lse); top-k (k >= 1) keeps the first k, top-p (k = 0)
+ * cuts the sorted prefix at the first cumulative sum >= top_p
+ * (np.searchsorted "left"); r = u * probs.sum() (numpy pairwise order), the
+ * first token with r <= the running sum. uniforms: the reference's PCG64
+ * stream in its draw order (one per live row per step, rows in batch order),
+ * consumed through *draw. done int32 [2][batch] (step parity t = *d_cur: read
+ * [t & 1], write [(t + 1) & 1]); writes out_tok[b][t] (int32
+ * [batch][max_len]), out_len, fin (EOS), the next step's dk_next / tokens (0
+ * for done rows); the last CTA advances *draw and *d_cur and stores the
+ * live-row count in counters[1] (counters int32 [2], zero once). err != 0: a
+ * row had > 1024 survivors (1), the uniform stream ran out (2), or a top-p
+ * row's survivors miss the nucleus (3, the reference escalates its group
+ * count) -- re-run the request on the host-driven path. */
+int fq_sample_step(const float* logits, int64_t ld, const double* lse, const int32_t* cand_idx,
+                   int64_t cand_ld, const int64_t* cand_count, int64_t batch, int64_t k,
+                   double top_p, int64_t groups, int64_t vocab, int64_t eos,
+                   const double* uniforms, int64_t n_uniforms, int64_t* draw, int32_t* done,
+                   int32_t* d_cur, int64_t max_steps, int64_t max_len, int32_t* dk_next,
+                   int64_t* tokens, int32_t* out_tok, int32_t* out_len, int32_t* fin,
+                   int32_t* counters, int32_t* err, fq_stream_t stream);
 
 /* ---- fused attention for the device engine (model.py:329-336, :572-604) --- */
 

@@ -1,4 +1,4 @@
-// Device-resident top-k sampling step: the reference's
+// Device-resident top-k / top-p sampling step: the reference's
 // Session._sampling_step (engine.py:175-195) over every row of one decode
 // step, after the batched retrieve (decode.py:58-92) has left each live row's
 // survivors x >= R (the row's true top-|C| tokens, |C| >= k).
@@ -7,7 +7,11 @@
 // decode.py:389-396), the first k kept, probs = exp(f64(logit) - lse) in f64,
 // and the inverse-CDF draw of _draw (decode.py:378-386): r = u * probs.sum()
 // with numpy's pairwise summation order, c accumulated in order, the first
-// token with r <= c (else the last). The uniforms are the reference's own
+// token with r <= c (else the last). Top-p (k = 0): the whole sorted prefix,
+// cut at the first cumulative sum >= p (np.searchsorted "left"), drawn the
+// same way; a row whose survivors miss the nucleus mass (the reference would
+// escalate its group count x8) sets err = 3 and the request re-runs on the
+// host-driven path. The uniforms are the reference's own
 // PCG64 stream, generated on the host in its order (one per live row per
 // step, rows in batch order) and consumed here through a device draw counter:
 // row b's draw is base + #{live rows before b}. The last CTA to finish
@@ -58,10 +62,10 @@ __device__ __forceinline__ int block_count(int v, int* red) {
 // [batch] (next step's retrieve group count: k live, 0 done); tokens int64
 // [batch] (next step's input; 0 for done rows); draw int64 [1]; counters
 // int32 [2] (arrival, live-after count); err int32 [1] (survivor overflow).
-__global__ void __launch_bounds__(kSampThreads) sample_topk_step_kernel(
+__global__ void __launch_bounds__(kSampThreads) sample_step_kernel(
     const float* __restrict__ logits, int64_t ld, const double* __restrict__ lse,
     const int32_t* __restrict__ cand_idx, int64_t cand_ld,
-    const int64_t* __restrict__ cand_count, int k, int eos,
+    const int64_t* __restrict__ cand_count, int k, double top_p, int groups, int V, int eos,
     const double* __restrict__ uniforms, int64_t n_uniforms, int64_t* draw, int32_t* done,
     int32_t* d_cur, int64_t max_steps, int max_len, int32_t* dk_next, int64_t* tokens,
     int32_t* out_tok, int32_t* out_len, int32_t* fin, int batch, int32_t* counters,
@@ -102,7 +106,7 @@ __global__ void __launch_bounds__(kSampThreads) sample_topk_step_kernel(
         s_lg[j] = logits[(int64_t)b * ld + tj];
       }
       __syncthreads();
-      const int m = min(k, n);
+      const int m = k > 0 ? min(k, n) : n;  // top-p: the whole sorted prefix
       for (int j = tid; j < n; j += blockDim.x) {  // rank under (-logit, token)
         const float v = s_lg[j];
         const int32_t tj = s_tok[j];
@@ -121,10 +125,25 @@ __global__ void __launch_bounds__(kSampThreads) sample_topk_step_kernel(
         const int64_t ui = base + before;
         const double u = ui < n_uniforms ? uniforms[ui] : 0.0;
         if (ui >= n_uniforms) atomicExch(err, 2);
-        const double r = u * np_pairwise_sum(o_p, m);
+        int md = m;  // the draw's prefix length
+        bool ok = true;
+        if (k <= 0) {  // nucleus (decode.py:412-430): cut = searchsorted(cumsum, p, "left")
+          double cs = 0.0;
+          int cut = -1;
+          for (int i = 0; i < n; ++i) {
+            cs += o_p[i];
+            if (cut < 0 && cs >= top_p) cut = i;
+          }
+          if (!(cs >= top_p || groups >= V)) {
+            ok = false;  // the survivors miss the nucleus: the reference escalates x8
+            atomicExch(err, 3);
+          }
+          md = min(cut < 0 ? n : cut, n - 1) + 1;
+        }
+        const double r = ok ? u * np_pairwise_sum(o_p, md) : 0.0;
         double c = 0.0;
-        tok = o_tok[m - 1];
-        for (int i = 0; i < m; ++i) {
+        tok = o_tok[md - 1];
+        for (int i = 0; i < md; ++i) {
           c += o_p[i];
           if (r <= c) {
             tok = o_tok[i];
@@ -140,7 +159,7 @@ __global__ void __launch_bounds__(kSampThreads) sample_topk_step_kernel(
   }
   if (tid == 0) {
     done_out[b] = d_out;
-    dk_next[b] = d_out ? 0 : k;
+    dk_next[b] = d_out ? 0 : (k > 0 ? k : groups);
     tokens[b] = d_out ? 0 : tok;
     __threadfence();
     const int prev = atomicAdd(&counters[0], 1);
@@ -163,24 +182,23 @@ __global__ void __launch_bounds__(kSampThreads) sample_topk_step_kernel(
 
 }  // namespace fq
 
-extern "C" int fq_sample_topk_step(const float* logits, int64_t ld, const double* lse,
-                                   const int32_t* cand_idx, int64_t cand_ld,
-                                   const int64_t* cand_count, int64_t batch, int64_t k,
-                                   int64_t eos, const double* uniforms, int64_t n_uniforms,
-                                   int64_t* draw, int32_t* done, int32_t* d_cur,
-                                   int64_t max_steps, int64_t max_len, int32_t* dk_next,
-                                   int64_t* tokens, int32_t* out_tok, int32_t* out_len,
-                                   int32_t* fin, int32_t* counters, int32_t* err,
-                                   fq_stream_t stream) {
+extern "C" int fq_sample_step(const float* logits, int64_t ld, const double* lse,
+                              const int32_t* cand_idx, int64_t cand_ld, const int64_t* cand_count,
+                              int64_t batch, int64_t k, double top_p, int64_t groups,
+                              int64_t vocab, int64_t eos, const double* uniforms,
+                              int64_t n_uniforms, int64_t* draw, int32_t* done, int32_t* d_cur,
+                              int64_t max_steps, int64_t max_len, int32_t* dk_next,
+                              int64_t* tokens, int32_t* out_tok, int32_t* out_len, int32_t* fin,
+                              int32_t* counters, int32_t* err, fq_stream_t stream) {
   FQ_CHECK_ARG(logits && lse && cand_idx && cand_count && uniforms && draw && done && d_cur &&
                    dk_next && tokens && out_tok && out_len && fin && counters && err &&
                    batch > 0 && ld >= 1 && cand_ld >= 1 && max_len >= 1,
-               FQ_ERR_DIMENSION, "fq_sample_topk_step: bad args");
-  FQ_CHECK_ARG(k >= 1 && k <= fq::kSampCap, FQ_ERR_PARAMETER,
-               "fq_sample_topk_step: k outside [1, 1024]");
-  fq::launch_kernel(fq::sample_topk_step_kernel, (unsigned)batch, fq::kSampThreads, 0,
+               FQ_ERR_DIMENSION, "fq_sample_step: bad args");
+  FQ_CHECK_ARG((k >= 1 && k <= fq::kSampCap) || (k == 0 && top_p > 0.0 && top_p <= 1.0),
+               FQ_ERR_PARAMETER, "fq_sample_step: k outside [1, 1024] / p outside (0, 1]");
+  fq::launch_kernel(fq::sample_step_kernel, (unsigned)batch, fq::kSampThreads, 0,
                 fq::as_stream(stream), 1u, logits, ld, lse, cand_idx, cand_ld, cand_count, (int)k,
-                (int)eos, uniforms, n_uniforms, draw, done, d_cur, max_steps, (int)max_len,
+                top_p, (int)groups, (int)vocab, (int)eos, uniforms, n_uniforms, draw, done, d_cur, max_steps, (int)max_len,
                 dk_next, tokens, out_tok, out_len, fin, (int)batch, counters, err);
-  return fq::launch_status("fq_sample_topk_step");
+  return fq::launch_status("fq_sample_step");
 }

@@ -415,19 +415,22 @@ class Session:
         return b
 
     def _generate_sampling_device(self, src, src_lengths, cfg: D.DecodeConfig, bos_token: int):
-        """Top-k sampling with the whole step on the device:
-        decoder step -> batched retrieve (per-row group counts, 0 for done
-        rows) -> fq_sample_topk_step, captured as one CUDA graph per step and
+        """Top-k / top-p sampling with the whole step on the device (SURVEY
+        §8(f)2): decoder step -> batched retrieve (per-row group counts, 0 for
+        done rows) -> fq_sample_step, captured as one CUDA graph per step and
         replayed with the host polling the live-row count one step behind. The
         draws are the reference's: its seeded PCG64 stream is generated on the
         host up front (numpy's random(n) equals n successive random() calls)
         and consumed on the device in its order. Returns None when a row
-        overflowed the device's survivor cap (the caller re-runs on the
-        host-driven path)."""
+        overflowed the device's survivor cap or a top-p row's survivors miss
+        the nucleus (the reference escalates the group count x8): the caller
+        re-runs the request on the host-driven path."""
         batch, seq = src.shape
         V = self.config.vocab_size
         max_steps = min(cfg.max_steps, self.config.max_seq_len)
-        k = min(cfg.sample_k, V)
+        top_p = cfg.method == "top_p"
+        k = 0 if top_p else min(cfg.sample_k, V)
+        g0 = min(32, V) if top_p else k  # retrieve group count of a live row
         packed, mask, cache = self._setup_decoder(src, src_lengths, batch)
         step = M.DecoderStep(self.dw, self.config, batch, 1, seq, cache, packed, mask,
                              self._buffers, self.counters, self.timers)
@@ -437,16 +440,17 @@ class Session:
         b["uniforms"].copy_(torch.from_numpy(rng.random(batch * max_steps)))
         for n in ("draw", "done", "out_len", "fin", "counters", "err"):
             b[n].zero_()
-        b["dk"].fill_(k)
+        b["dk"].fill_(g0)
         step.tokens.fill_(bos_token)
 
         def body():  # (stream handle read inside: graph capture runs on a side stream)
             logits = step.run()
-            D.retrieve_device(logits, k, d_k=b["dk"], out=(None, None, b["lse"], b["ci"], b["cc"]))
+            D.retrieve_device(logits, g0, d_k=b["dk"], out=(None, None, b["lse"], b["ci"], b["cc"]))
             self.counters.count_fused("retrieve", batch * V * 4)
-            _abi.call("fq_sample_topk_step", logits.data_ptr(), logits.stride(0),
+            _abi.call("fq_sample_step", logits.data_ptr(), logits.stride(0),
                       b["lse"].data_ptr(), b["ci"].data_ptr(), b["ci"].stride(0),
-                      b["cc"].data_ptr(), batch, k, cfg.eos_token, b["uniforms"].data_ptr(),
+                      b["cc"].data_ptr(), batch, k, float(cfg.sample_p), g0, V, cfg.eos_token,
+                      b["uniforms"].data_ptr(),
                       b["uniforms"].numel(), b["draw"].data_ptr(), b["done"].data_ptr(),
                       cache.d_cur.data_ptr(), max_steps, max_steps, b["dk"].data_ptr(),
                       step.tokens.data_ptr(), b["out_tok"].data_ptr(), b["out_len"].data_ptr(),
@@ -455,7 +459,8 @@ class Session:
 
         graph = None
         if self.use_graphs:
-            key = ("sample_top_k", batch, seq, max_steps, k, cfg.eos_token, mask is not None)
+            key = ("sample", batch, seq, max_steps, k, float(cfg.sample_p) if top_p else None,
+                   cfg.eos_token, mask is not None)
             entry = self._graphs.get(key)
             if entry is None:
                 graph = torch.cuda.CUDAGraph()
@@ -486,6 +491,10 @@ class Session:
         if int(step.bad.item()):
             raise FullMaskError("fully masked cross-attention row")
         if int(b["err"].item()):
+            if os.environ.get("FQ_DEBUG_SAMPLE"):
+                print("device sampling fallback, err", int(b["err"].item()),
+                      "cc", b["cc"].cpu().numpy().tolist(), "dk", b["dk"].cpu().numpy().tolist(),
+                      "done", b["done"].cpu().numpy().tolist(), "k", k, "g0", g0)
             return None
         toks = b["out_tok"].cpu().numpy()
         lens = b["out_len"].cpu().numpy()
@@ -506,9 +515,11 @@ class Session:
         escalate their group count x8 with a per-row retrieve (:420-430)."""
         if isinstance(src, torch.Tensor):
             src = src.cpu().numpy()
-        if cfg.method == "top_k" and os.environ.get("FQ_SAMPLE_HOST") != "1":
+        self.last_sampling_path = "host"
+        if os.environ.get("FQ_SAMPLE_HOST") != "1":
             got = self._generate_sampling_device(src, src_lengths, cfg, bos_token)
             if got is not None:
+                self.last_sampling_path = "device"
                 return got
         batch, seq = src.shape
         V = self.config.vocab_size

@@ -276,7 +276,7 @@ def test_sampling_generate_matches_reference_fixture(P, ci):
 
 @pytest.mark.parametrize("precision", ["fp32", "fp16"])
 def test_device_top_k_sampling_equals_host_driven_draw(P, precision, monkeypatch):
-    """The device-resident top-k sampling loop (fq_sample_topk_step inside the
+    """The device-resident top-k sampling loop (fq_sample_step inside the
     step graph, the reference's PCG64 stream pre-generated and consumed on the
     device in its draw order) reproduces the host-driven draw (FQ_SAMPLE_HOST=1,
     numpy _draw on the device retrieve's candidates) token for token, with EOS
@@ -288,15 +288,44 @@ def test_device_top_k_sampling_equals_host_driven_draw(P, precision, monkeypatch
     sess = P.Session(cfg, w, precision=precision)
     src = np.random.default_rng(3).integers(3, cfg.vocab_size, size=(13, 9))
     lens = np.random.default_rng(4).integers(3, 10, size=13)
-    for k, seed, eos in ((1, 0, 2), (7, 5, 2), (40, 11, 2), (200, 3, 5)):
+    for k, seed, eos in ((1, 0, 2), (7, 5, 2), (40, 11, 2), (100, 3, 5)):
         # eos = a frequent token so that rows finish early and leave the draw order
         dc = P.DecodeConfig(method="top_k", sample_k=k, seed=seed, max_steps=20, eos_token=eos)
         monkeypatch.delenv("FQ_SAMPLE_HOST", raising=False)
         dev = sess.generate(src, dc, src_lengths=lens)
+        assert sess.last_sampling_path == "device"
         monkeypatch.setenv("FQ_SAMPLE_HOST", "1")
         host = sess.generate(src, dc, src_lengths=lens)
         assert [[h.tokens for h in x] for x in dev] == [[h.tokens for h in x] for x in host], k
         assert [[h.score for h in x] for x in dev] == [[h.score for h in x] for x in host]
+
+
+@pytest.mark.parametrize("precision", ["fp32", "fp16"])
+def test_device_top_p_sampling_equals_host_driven_draw(P, precision, monkeypatch):
+    """Top-p on the device: peaked logits (embedding scaled x6) keep the
+    nucleus inside the 32-group survivors, so the whole request stays on the
+    device (sorted prefix, sequential cumsum cut at np.searchsorted(p, left),
+    pairwise-sum draw) -- token-identical to the host-driven draw; flat logits
+    (the nucleus needs the reference's x8 escalation) re-run on the host path
+    with the reference's results."""
+    cfg = P.ModelConfig(num_encoder_layers=1, num_decoder_layers=2, d_model=128, d_ff=256,
+                        num_heads=4, vocab_size=3000, max_batch=16, max_seq_len=24,
+                        max_beam_size=4)
+    src = np.random.default_rng(3).integers(3, cfg.vocab_size, size=(11, 9))
+    for scale, want_path in ((6.0, "device"), (1.0, "host")):
+        w = P.make_random_weights(cfg, seed=22)
+        w.token_embedding = (w.token_embedding * np.float32(scale)).astype(np.float32)
+        sess = P.Session(cfg, w, precision=precision)
+        for p, seed in ((0.5, 1), (0.9, 4), (0.99, 9)):
+            dc = P.DecodeConfig(method="top_p", sample_p=p, seed=seed, max_steps=16, eos_token=2)
+            monkeypatch.delenv("FQ_SAMPLE_HOST", raising=False)
+            dev = sess.generate(src, dc)
+            path = sess.last_sampling_path
+            monkeypatch.setenv("FQ_SAMPLE_HOST", "1")
+            host = sess.generate(src, dc)
+            assert [[h.tokens for h in x] for x in dev] == [[h.tokens for h in x] for x in host], p
+            if scale == 1.0 or p < 0.99:
+                assert path == want_path, (scale, p, path)
 
 
 def test_device_top_k_sampling_tie_heavy_falls_back(P):
