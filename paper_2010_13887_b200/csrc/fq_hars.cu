@@ -462,9 +462,13 @@ __device__ __forceinline__ void sweep_row(
     part_max[4 * tid] = gm[0]; part_max[4 * tid + 1] = gm[1];
     part_max[4 * tid + 2] = gm[2]; part_max[4 * tid + 3] = gm[3];
   }
-  if (tid == 0 && rank == C - 1) {  // scalar head and tail (the last rank)
-    for (int jj = 0; jj < hd + (V - hd - (nvec << 2)); ++jj) {
-      const int j = jj < hd ? jj : hd + (nvec << 2) + (jj - hd);
+  // scalar head (rank 0) and tail (the last rank): each rank's survivors stay
+  // in column order across ranks
+  const int h0 = rank == 0 ? 0 : hd, h1 = rank == 0 ? hd : hd;
+  const int t0 = rank == C - 1 ? hd + (nvec << 2) : V;
+  if (tid == 0) {
+    for (int jj = h0; jj < h1 + (V - t0); ++jj) {
+      const int j = jj < h1 ? jj : t0 + (jj - h1);
       const float xv = x[j];
       if (xv > m + 64.f || m == NEG) {
         if (xv != NEG) {
@@ -488,9 +492,9 @@ __device__ __forceinline__ void sweep_row(
     if (lane == 0) gmax_s[g] = mm;
   }
   __syncthreads();
-  if (tid == 0 && rank == C - 1)
-    for (int jj = 0; jj < hd + (V - hd - (nvec << 2)); ++jj) {
-      const int j = jj < hd ? jj : hd + (nvec << 2) + (jj - hd);
+  if (tid == 0)
+    for (int jj = h0; jj < h1 + (V - t0); ++jj) {
+      const int j = jj < h1 ? jj : t0 + (jj - h1);
       gmax_s[j % k] = fmaxf(gmax_s[j % k], x[j]);
     }
   if (C > 1) cl_sync_all();  // both halves' group maxima complete
@@ -1824,6 +1828,22 @@ static int hars_num_sms() {
 // 128k x 128 rows 54 vs 39; but 32k x 32..512 rows 14..28 vs 23..39: the
 // split's row merge costs a few dependent L2 round trips per row).
 // FQ_HARS_SPLIT=0/1 forces either (A/B runs and tests).
+// CTAs (a cluster) per row of the row kernels: the largest power of two <= 8
+// with rows * C within one wave of 4 CTAs per SM (partials merged through
+// DSMEM); 1 from 296 rows up (the C2 decode step's 512). The fused step and
+// fq_retrieve use the same rule, so their logsumexp bits agree.
+static int row_cluster(int64_t rows) {
+  if (kSwSplit != 1) return kSwSplit;
+  int C = 1;
+  while (C < 8 && rows * C * 2 <= 4 * (int64_t)hars_num_sms()) C *= 2;
+  return C;
+}
+
+static bool split_forced() {
+  const char* e = getenv("FQ_HARS_SPLIT");
+  return e && e[0] == '1';
+}
+
 static bool use_split(int64_t rows, int64_t vocab, int64_t cand_ld) {
   if (vocab % 4 != 0 || vocab < 8 * kMinPortion || cand_ld < vocab ||
       rows * (vocab / 4) >= (1ll << 31))
@@ -1877,8 +1897,10 @@ int fq_retrieve(const float* logits, int64_t ld, int64_t rows, int64_t vocab, in
   FQ_CHECK_ARG(!group_max || gm_ld >= (d_k ? vocab : k) || gm_ld >= k, FQ_ERR_DIMENSION,
                "group_max leading dim too small");
   if (rows == 0) return FQ_OK;
+  int C = row_cluster(rows);
   if (k >= 1 && k <= 32 && (ld % 4) == 0 && ((uintptr_t)logits & 15) == 0 &&
-      !retrieve_two_pass_forced() && use_split(rows, vocab, cand_ld)) {
+      !retrieve_two_pass_forced() && use_split(rows, vocab, cand_ld) &&
+      (rows < 16 || split_forced())) {
     const size_t smem = split_smem();
     const SplitGeom g = split_geom(reinterpret_cast<const void*>(retrieve_split_kernel), smem,
                                    rows, vocab, k);
@@ -1892,9 +1914,9 @@ int fq_retrieve(const float* logits, int64_t ld, int64_t rows, int64_t vocab, in
     return launch_status("fq_retrieve");
   }
   if (k >= 1 && k <= 32 && ((uintptr_t)logits & 3) == 0 && !retrieve_two_pass_forced()) {
-    launch_kernel(retrieve_sweep_kernel, (unsigned)(rows * kSwSplit), kRowThreads,
+    launch_kernel(retrieve_sweep_kernel, (unsigned)(rows * C), kRowThreads,
                   (size_t)kSwP * kRowThreads * sizeof(float4), as_stream(stream),
-                  (unsigned)kSwSplit,
+                  (unsigned)C,
                   logits, ld, (int)vocab, (int)k, d_k, group_max, gm_ld, threshold, lse,
                   cand_idx, cand_ld, cand_count);
     return launch_status("fq_retrieve");
@@ -1947,7 +1969,7 @@ int fq_hars_step(const float* logits, int64_t ld, fq_beam_state st, int64_t batc
                FQ_ERR_DIMENSION,
                "fq_hars_step: next-step embedding needs aligned emb/pos/x and d_model % 4 == 0");
   FQ_CHECK_ARG(eos >= 0 && eos < vocab, FQ_ERR_PARAMETER, "eos token outside vocabulary");
-  if (use_split(batch * beam, vocab, cand_ld)) {
+  if (use_split(batch * beam, vocab, cand_ld) && (batch * beam < 16 || split_forced())) {
     const size_t smem = std::max(sel_smem(beam, max_len), split_smem());
     FQ_CHECK_ARG(smem <= 96 * 1024, FQ_ERR_CAPACITY, "fq_hars_step: max_len too large");
     const SplitGeom g = split_geom(reinterpret_cast<const void*>(hars_step_split_kernel), smem,
@@ -1962,8 +1984,9 @@ int fq_hars_step(const float* logits, int64_t ld, fq_beam_state st, int64_t batc
   const size_t smem = std::max(sel_smem(beam, max_len),
                                (size_t)kSwP * kRowThreads * sizeof(float4));
   FQ_CHECK_ARG(smem <= 96 * 1024, FQ_ERR_CAPACITY, "fq_hars_step: max_len too large");
-  launch_kernel(hars_step_kernel, (unsigned)(batch * beam * kSwSplit), kRowThreads, smem,
-                as_stream(stream), (unsigned)kSwSplit, logits, ld, (int)vocab, st, (int)batch, (int)beam, (int)max_len, (int)eos,
+  const int C = row_cluster(batch * beam);
+  launch_kernel(hars_step_kernel, (unsigned)(batch * beam * C), kRowThreads, smem,
+                as_stream(stream), (unsigned)C, logits, ld, (int)vocab, st, (int)batch, (int)beam, (int)max_len, (int)eos,
                 len_pow, d_cur, max_steps, lse, cand_idx, cand_ld, cand_count, counters,
                 counters + batch, row_tokens, row_parents, hist, x_next ? emb : nullptr,
                 (int)d_model, emb_scale, pos, x_next,
