@@ -1580,7 +1580,13 @@ __global__ void __launch_bounds__(32) decoder_self_attention_xh(
     int64_t plane, const int32_t* __restrict__ hist, const int32_t* __restrict__ d_cur,
     int rows, int heads, int max_len, float scale, float* __restrict__ out,
     h16* __restrict__ out_hi, h16* __restrict__ out_lo, int64_t ldo) {
-  constexpr int RS = HD * 2 + 16;  // padded smem row bytes: conflict-free ldmatrix
+  // HD = 64: 128-byte rows, 16-byte chunks XOR-swizzled by row (no padding);
+  // other head dims: a 16-byte row pad (conflict-free ldmatrix either way)
+  constexpr bool SWZ = HD == 64;
+  constexpr int RS = SWZ ? 128 : HD * 2 + 16;
+  auto soff = [](int r, int byte) {
+    return r * RS + (SWZ ? ((((byte >> 4) ^ (r & 7)) << 4) | (byte & 15)) : byte);
+  };
   constexpr int CPR = HD * 2 / 16;  // 16-byte pieces per row
   constexpr int KT = HD / 16;
   constexpr int KE = (HD + 63) / 64;  // float2 of this step's k / v per lane
@@ -1636,8 +1642,8 @@ __global__ void __launch_bounds__(32) decoder_self_attention_xh(
     for (int x = lane; x < 16 * CPR; x += 32) {
       const int rr = x / CPR, ch = x % CPR;
       const int t = 16 * c + rr;
-      uint8_t* dh = &ring[s][0][0] + rr * RS + ch * 16;
-      uint8_t* dl = &ring[s][1][0] + rr * RS + ch * 16;
+      uint8_t* dh = &ring[s][0][0] + soff(rr, ch * 16);
+      uint8_t* dl = &ring[s][1][0] + soff(rr, ch * 16);
       if (t < cur) {
         const h16* p = src + off_s[t] + ch * 8;
         cp16(sm_u32(dh), p);
@@ -1655,8 +1661,8 @@ __global__ void __launch_bounds__(32) decoder_self_attention_xh(
     for (int i = 0; i < KE; ++i) {
       const int e = 2 * lane + 64 * i;
       if (e < HD) {
-        *reinterpret_cast<uint32_t*>(&ring[s][0][0] + rr * RS + e * 2) = hi[i];
-        *reinterpret_cast<uint32_t*>(&ring[s][1][0] + rr * RS + e * 2) = lo[i];
+        *reinterpret_cast<uint32_t*>(&ring[s][0][0] + soff(rr, e * 2)) = hi[i];
+        *reinterpret_cast<uint32_t*>(&ring[s][1][0] + soff(rr, e * 2)) = lo[i];
       }
     }
   };
@@ -1682,8 +1688,8 @@ __global__ void __launch_bounds__(32) decoder_self_attention_xh(
 #pragma unroll
     for (int kk = 0; kk < KT; ++kk) {
       uint32_t ah[4], al[4];
-      ldsm_x4(ah, Kh + lrow * RS + (16 * kk + lcol) * 2);
-      ldsm_x4(al, Kl + lrow * RS + (16 * kk + lcol) * 2);
+      ldsm_x4(ah, Kh + soff(lrow, (16 * kk + lcol) * 2));
+      ldsm_x4(al, Kl + soff(lrow, (16 * kk + lcol) * 2));
       mma_f16_16816(big, ah, qh[kk][0], qh[kk][1]);
       mma_f16_16816(sml, ah, ql[kk][0], ql[kk][1]);
       mma_f16_16816(sml, al, qh[kk][0], qh[kk][1]);
@@ -1724,8 +1730,8 @@ __global__ void __launch_bounds__(32) decoder_self_attention_xh(
 #pragma unroll
     for (int m = 0; m < KT; ++m) {
       uint32_t ah[4], al[4];
-      ldsm_x4_t(ah, Vh + vrow * RS + (16 * m + vcol) * 2);
-      ldsm_x4_t(al, Vl + vrow * RS + (16 * m + vcol) * 2);
+      ldsm_x4_t(ah, Vh + soff(vrow, (16 * m + vcol) * 2));
+      ldsm_x4_t(al, Vl + soff(vrow, (16 * m + vcol) * 2));
       mma_f16_16816(ob[m], ah, bh0, bh1);
       mma_f16_16816(os[m], ah, bl0, bl1);
       mma_f16_16816(os[m], al, bh0, bh1);
@@ -1765,7 +1771,12 @@ __global__ void __launch_bounds__(32) cross_attention_xh(
     const h16* __restrict__ cv, int64_t plane, int64_t ldkv, int beam, int seq, float scale,
     const float* __restrict__ mask, float* __restrict__ out, h16* __restrict__ out_hi,
     h16* __restrict__ out_lo, int64_t ldo, int* d_bad) {
-  constexpr int RS = HD * 2 + 16;
+  // HD = 64: 128-byte rows with the 16-byte chunks XOR-swizzled by row (no
+  // padding: 12 instead of 13.5 KB of ring per warp at NS = 3); other head
+  // dims keep a 16-byte row pad against ldmatrix bank conflicts
+  constexpr bool SWZ = HD == 64;
+  constexpr int RS = SWZ ? 128 : HD * 2 + 16;
+  auto soff = [](int r, int ch) { return r * RS + (SWZ ? ((ch ^ (r & 7)) << 4) : (ch << 4)); };
   constexpr int CPR = HD * 2 / 16;
   constexpr int NP = NT * 16;
   constexpr int KT = HD / 16;
@@ -1779,8 +1790,8 @@ __global__ void __launch_bounds__(32) cross_attention_xh(
     for (int x = lane; x < 16 * CPR; x += 32) {
       const int rr = x / CPR, pc = x % CPR;
       const int t = 16 * c + rr;
-      uint8_t* dh = &ring[st][0][0] + rr * RS + pc * 16;
-      uint8_t* dl = &ring[st][1][0] + rr * RS + pc * 16;
+      uint8_t* dh = &ring[st][0][0] + soff(rr, pc);
+      uint8_t* dl = &ring[st][1][0] + soff(rr, pc);
       if (t < seq) {
         const h16* p = src + base + (int64_t)t * ldkv + pc * 8;
         cp16(sm_u32(dh), p);
@@ -1830,8 +1841,8 @@ __global__ void __launch_bounds__(32) cross_attention_xh(
 #pragma unroll
       for (int kk = 0; kk < KT; ++kk) {
         uint32_t ah[4], al[4];
-        ldsm_x4(ah, Kh + lrow * RS + (16 * kk + lcol) * 2);
-        ldsm_x4(al, Kl + lrow * RS + (16 * kk + lcol) * 2);
+        ldsm_x4(ah, Kh + soff(lrow, 2 * kk + (lcol >> 3)));
+        ldsm_x4(al, Kl + soff(lrow, 2 * kk + (lcol >> 3)));
         mma_f16_16816(big, ah, qh[kk][0], qh[kk][1]);
         mma_f16_16816(sml, ah, ql[kk][0], ql[kk][1]);
         mma_f16_16816(sml, al, qh[kk][0], qh[kk][1]);
@@ -1926,8 +1937,8 @@ __global__ void __launch_bounds__(32) cross_attention_xh(
 #pragma unroll
       for (int m = 0; m < KT; ++m) {
         uint32_t ah[4], al[4];
-        ldsm_x4_t(ah, Vh + vrow * RS + (16 * m + vcol) * 2);
-        ldsm_x4_t(al, Vl + vrow * RS + (16 * m + vcol) * 2);
+        ldsm_x4_t(ah, Vh + soff(vrow, 2 * m + (vcol >> 3)));
+        ldsm_x4_t(al, Vl + soff(vrow, 2 * m + (vcol >> 3)));
         mma_f16_16816(ob[m], ah, bh0, bh1);
         mma_f16_16816(os[m], ah, bl0, bl1);
         mma_f16_16816(os[m], al, bh0, bh1);
