@@ -194,18 +194,30 @@ __global__ void __launch_bounds__(128) layer_norm_slabs_row128_kernel(
     const float* __restrict__ res, int64_t ldr, const float* __restrict__ gamma,
     const float* __restrict__ beta, double eps, int d, float* __restrict__ out, int64_t ldo,
     h16* __restrict__ out16, h16* __restrict__ out16lo, int64_t ldo16) {
-  pdl_enter();
+  pdl_launch_dependents();
   __shared__ double red[2][4];
   const int64_t row = blockIdx.x;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  // the (constant) bias / gamma / beta before the grid-dependency wait: their
+  // fetch overlaps the producing GEMM's tail instead of adding a round trip
+  float4 bv[V], gv[V], ev[V];
+#pragma unroll
+  for (int i = 0; i < V; ++i) {
+    const int c = (i * 128 + threadIdx.x) * 4;
+    bv[i] = *reinterpret_cast<const float4*>(bias + c);
+    gv[i] = *reinterpret_cast<const float4*>(gamma + c);
+    ev[i] = *reinterpret_cast<const float4*>(beta + c);
+  }
+  pdl_wait();
   float4 u[V];
   double s = 0.0;
-  float4 p[V][NS];
+  float4 p[V][NS], rv[V];
 #pragma unroll
   for (int i = 0; i < V; ++i) {
     const int c = (i * 128 + threadIdx.x) * 4;
 #pragma unroll
     for (int k = 0; k < NS; ++k) p[i][k] = __ldcg(reinterpret_cast<const float4*>(x + k * slab + row * ld + c));
+    rv[i] = *reinterpret_cast<const float4*>(res + row * ldr + c);
   }
 #pragma unroll
   for (int i = 0; i < V; ++i) {
@@ -218,8 +230,8 @@ __global__ void __launch_bounds__(128) layer_norm_slabs_row128_kernel(
       a.z = fadd_rn(a.z, p[i][k].z);
       a.w = fadd_rn(a.w, p[i][k].w);
     }
-    const float4 b = *reinterpret_cast<const float4*>(bias + c);
-    const float4 r = *reinterpret_cast<const float4*>(res + row * ldr + c);
+    const float4 b = bv[i];
+    const float4 r = rv[i];
     a.x = fadd_rn(fadd_rn(a.x, b.x), r.x);
     a.y = fadd_rn(fadd_rn(a.y, b.y), r.y);
     a.z = fadd_rn(fadd_rn(a.z, b.z), r.z);
@@ -244,8 +256,8 @@ __global__ void __launch_bounds__(128) layer_norm_slabs_row128_kernel(
 #pragma unroll
   for (int i = 0; i < V; ++i) {
     const int c = (i * 128 + threadIdx.x) * 4;
-    const float4 g = *reinterpret_cast<const float4*>(gamma + c);
-    const float4 bb = *reinterpret_cast<const float4*>(beta + c);
+    const float4 g = gv[i];
+    const float4 bb = ev[i];
     float4 o;
     o.x = fadd_rn(fmul_rn((float)((u[i].x - mean) * inv), g.x), bb.x);  // kernels.py:35
     o.y = fadd_rn(fmul_rn((float)((u[i].y - mean) * inv), g.y), bb.y);
