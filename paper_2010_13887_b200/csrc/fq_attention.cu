@@ -1784,7 +1784,10 @@ __global__ void __launch_bounds__(32) cross_attention_xh(
   __shared__ float Ps[8][NP + 4];
   const int b = blockIdx.x, h = blockIdx.y, lane = threadIdx.x;
   const int g = lane >> 2, t4 = lane & 3;
-  pdl_enter();
+  // the cross K/V planes are written once per request, before the decode
+  // step graph: the first chunks stream in before the grid-dependency wait
+  // (only the query comes from the preceding GEMM)
+  pdl_launch_dependents();
   const int64_t base = (int64_t)b * seq * ldkv + h * HD;
   auto issue = [&](const h16* src, int c, int st) {
     for (int x = lane; x < 16 * CPR; x += 32) {
@@ -1812,6 +1815,7 @@ __global__ void __launch_bounds__(32) cross_attention_xh(
   };
 #pragma unroll
   for (int c = 0; c < NS - 1; ++c) issue_g(c);
+  pdl_wait();
   // Q^T fragments: lane (g, t4) holds beam g, dims 16k + {2t4, 2t4+1, 2t4+8, 2t4+9}
   uint32_t qh[KT][2], ql[KT][2];
   {
