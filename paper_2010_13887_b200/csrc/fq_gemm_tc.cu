@@ -398,12 +398,19 @@ __device__ __forceinline__ void mma_commit_mc(uint64_t* bar, uint16_t mask) {
       : "memory");
 }
 
+// Per-CTA phase stamps for scripts/xh_cta_anatomy.py: compiled in only with
+// -DFQ_GEMM_STAMPS (scripts/build_variant.sh), off the product path.
 __device__ __forceinline__ void dbg_stamp(unsigned long long* dbg, int slot) {
+#ifdef FQ_GEMM_STAMPS
   if (dbg) {
     unsigned long long t_;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
     dbg[8 * blockIdx.x + slot] = t_;
   }
+#else
+  (void)dbg;
+  (void)slot;
+#endif
 }
 
 // Persistent over tile groups: a cluster (cm x cn CTAs, rank r -> (ry = r / cn,

@@ -14,7 +14,7 @@ from paper_2010_13887_b200 import _abi
 from paper_2010_13887_b200.model import XHWeight
 from paper_2010_13887_b200.tensor import split_pair
 
-lib = _abi.load()
+lib = _abi.load()  # stamps need a -DFQ_GEMM_STAMPS build: FQ_LIB=build/variants/<name>.so
 lib.fq_gemm_debug_timestamps.argtypes = [ctypes.c_void_p]
 shapes = os.environ.get("SHAPES", "512x3072x1024,512x4096x1024,512x32000x1024")
 for sh in shapes.split(","):
