@@ -11,7 +11,7 @@ import torch
 import paper_2010_13887_b200 as P
 
 cfg = P.ModelConfig(6, 6, 1024, 4096, 16, 32000, 128, 64, 4)
-sess = P.Session(cfg, P.make_random_weights(cfg, 0), precision="fp16")
+sess = P.Session(cfg, P.make_random_weights(cfg, 0), precision=os.environ.get("PREC", "fp32"))
 src = np.random.default_rng(0).integers(3, 32000, size=(128, 64))
 src_dev = torch.from_numpy(src).cuda()
 src_pin = torch.from_numpy(src).pin_memory()
