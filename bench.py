@@ -732,11 +732,13 @@ def run_ours(args, rank, world):
             out["half_mode"]["roofline"] = roofline_gemm(
                 half, hsrc, hdc, cfg, local, hres["steps_run"], f16_peak,
                 "MEASURED_PEAKS.json bf16_tflops_sustained (measured)", args.half)
+    # the single-GPU micro-benchmarks (HARS step + stage-1 sweep, output layer,
+    # BASELINE configs 4/5) belong to the N = 1 line only
+    if rank == 0 and world == 1 and not args.no_micro:
         out["hars"], ctx = hars_micro(P, D, _abi, cfg, local, dev, hbm_peak)
         sess16 = half if half is not None else (sess if args.precision != "fp32" else None)
         if sess16 is not None:
             out["output_layer"] = output_layer_micro(P, _abi, sess16, cfg, local, dev, ctx)
-    if rank == 0 and not args.no_micro:
         out["extras"] = extra_workloads(P, dev, args)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline_sample()
@@ -753,9 +755,17 @@ def main():
         return
     import torch
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # FQ_BENCH_ONE_GPU=1: every rank on cuda:0 with gloo (plumbing checks of the
+    # multi-rank path on a 1-GPU box; NCCL needs one GPU per rank)
+    one_gpu = os.environ.get("FQ_BENCH_ONE_GPU") == "1"
+    if one_gpu:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if one_gpu:
+            torch.distributed.init_process_group("gloo")
+        else:
+            torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local))
     try:
         run_ours(args, rank, world)
     finally:

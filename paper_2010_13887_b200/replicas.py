@@ -26,6 +26,8 @@ def _dist():
 def reduce_step_stats(seconds: float, tokens: float, device=None) -> tuple[float, float]:
     """(max seconds over ranks, total tokens over ranks); identity when single-process."""
     dev = device if device is not None else torch.device("cpu")
+    if _dist() and torch.distributed.get_backend() == "gloo":
+        dev = torch.device("cpu")
     t = torch.tensor([seconds], dtype=torch.float64, device=dev)
     n = torch.tensor([tokens], dtype=torch.float64, device=dev)
     if _dist():
