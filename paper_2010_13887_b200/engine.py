@@ -490,11 +490,8 @@ class Session:
         torch.cuda.synchronize()
         if int(step.bad.item()):
             raise FullMaskError("fully masked cross-attention row")
-        if int(b["err"].item()):
-            if os.environ.get("FQ_DEBUG_SAMPLE"):
-                print("device sampling fallback, err", int(b["err"].item()),
-                      "cc", b["cc"].cpu().numpy().tolist(), "dk", b["dk"].cpu().numpy().tolist(),
-                      "done", b["done"].cpu().numpy().tolist(), "k", k, "g0", g0)
+        self.last_sampling_err = int(b["err"].item())  # 1 cap, 2 uniforms, 3 nucleus
+        if self.last_sampling_err:
             return None
         toks = b["out_tok"].cpu().numpy()
         lens = b["out_len"].cpu().numpy()
