@@ -326,10 +326,13 @@ __device__ __forceinline__ void sweep_row(
     int64_t* __restrict__ cand_count, float4* __restrict__ ring, const int C, const int rank,
     const int64_t vals_off = 0, int32_t* __restrict__ top_out = nullptr,
     int32_t* __restrict__ top_mark = nullptr) {
-  constexpr int SC = NT * 4;  // survivor list (more: ordered rescan)
+  // survivors >= R' in per-thread slots ([slot][thread]: no atomics in the
+  // sweep), a thread's survivors beyond SL in a shared spill list (atomics,
+  // rare); a spill overflow (tie-heavy rows) -> the ordered rescan
+  constexpr int SL = 4, SP = NT * 2;
   __shared__ float part_max[NT * 4];
-  __shared__ int32_t sv_idx[SC];
-  __shared__ float sv_val[SC];
+  __shared__ int2 tsv[SL][NT];
+  __shared__ int2 spill[SP];
   __shared__ float gmax_s[32];
   __shared__ float s_R, s_M;
   __shared__ double red[NT / 32];
@@ -366,6 +369,16 @@ __device__ __forceinline__ void sweep_row(
     cp_async_commit();
   }
   if (tid == 0) { s_cnt = 0; s_ovf = 0; }
+  int nt_sv = 0;  // this thread's survivors (may exceed SL: overflow)
+  auto keep = [&](int j, float v) {
+    if (nt_sv < SL) {
+      tsv[nt_sv][tid] = make_int2(j, __float_as_int(v));
+      ++nt_sv;
+    } else {
+      const int p = atomicAdd(&s_cnt, 1);
+      if (p < SP) spill[p] = make_int2(j, __float_as_int(v));
+    }
+  };
   // ---- pilot (first kSwU vectors): partial group maxima -> R' <= R, M' ----
   float gm[4] = {NEG, NEG, NEG, NEG};
   cp_async_wait<kSwP - kSwU>();
@@ -416,10 +429,9 @@ __device__ __forceinline__ void sweep_row(
            (ex2_ftz(fmaf(e.z, L2E_LO, fmaf(e.z, L2E, -mL))) +
             ex2_ftz(fmaf(e.w, L2E_LO, fmaf(e.w, L2E, -mL))));
   };
-  // One rare branch per vector: an element reaching R' (survivor) or m + 64
-  // (rescale), or m still -inf, takes the exact per-element path; every other
-  // vector only adds its 4-term fp32 sum (same sums, same order either way).
-  float thr = m == NEG ? NEG : fminf(Rp, m + 64.f);
+  // rescale threshold (m + 64; -inf while m is -inf): the running maximum
+  // moves only for wildly larger elements (the terms stay exact to ~1e-7)
+  float thr = m == NEG ? NEG : m + 64.f;
   const float4* src = xb + kSwP * T;
   for (int i = 0; i < nit; ++i) {
     cp_async_wait<kSwP - 1>();
@@ -431,30 +443,21 @@ __device__ __forceinline__ void sweep_row(
     gm[0] = fmaxf(gm[0], e.x); gm[1] = fmaxf(gm[1], e.y);
     gm[2] = fmaxf(gm[2], e.z); gm[3] = fmaxf(gm[3], e.w);
     const float m4 = fmaxf(fmaxf(e.x, e.y), fmaxf(e.z, e.w));
-    if (m4 >= thr) {
-      if (m4 > m + 64.f || m == NEG) {  // (practically never for logits)
-        if (m4 != NEG) {
-          s = m == NEG ? 0.0 : s * exp2((double)mL - (double)m4 * L2E_D);
-          m = m4;
-          mL = m * L2E;
-        }
+    if (m4 > thr) {  // new maximum beyond m + 64, or m still -inf (practically never)
+      if (m4 != NEG) {
+        s = m == NEG ? 0.0 : s * exp2((double)mL - (double)m4 * L2E_D);
+        m = m4;
+        mL = m * L2E;
       }
-      if (m != NEG) s += (double)terms4(e);
-      if (m4 >= Rp) {
-        const int v = tid + (i_lo + i) * T;
-        const float e4[4] = {e.x, e.y, e.z, e.w};
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          if (e4[c] >= Rp) {
-            const int p = atomicAdd(&s_cnt, 1);
-            if (p < SC) { sv_idx[p] = hd + 4 * v + c; sv_val[p] = e4[c]; }
-          }
-        }
-      }
-      thr = m == NEG ? NEG : fminf(Rp, m + 64.f);
-    } else {
-      s += (double)terms4(e);
+      thr = m == NEG ? NEG : m + 64.f;
     }
+    if (m != NEG) s += (double)terms4(e);
+    // survivors: predicated slot stores, one per element >= R'
+    const int j0 = hd + 4 * (tid + (i_lo + i) * T);
+    if (e.x >= Rp) keep(j0, e.x);
+    if (e.y >= Rp) keep(j0 + 1, e.y);
+    if (e.z >= Rp) keep(j0 + 2, e.z);
+    if (e.w >= Rp) keep(j0 + 3, e.w);
   }
   cp_async_wait<0>();
   sw_stamp(row, 2);
@@ -478,10 +481,7 @@ __device__ __forceinline__ void sweep_row(
         }
       }
       if (m != NEG) s += (double)ex2_ftz(fmaf(xv, L2E_LO, fmaf(xv, L2E, -mL)));
-      if (xv >= Rp) {
-        const int p = atomicAdd(&s_cnt, 1);
-        if (p < SC) { sv_idx[p] = j; sv_val[p] = xv; }
-      }
+      if (xv >= Rp) keep(j, xv);
     }
   }
   __syncthreads();
@@ -515,26 +515,25 @@ __device__ __forceinline__ void sweep_row(
   const double st = m == NEG ? 0.0 : s * exp2((double)mL - (double)M * L2E_D);
   const double Sl = block_sum(st, red);  // contains __syncthreads
   sw_stamp(row, 3);
-  const int nsv = s_cnt;
   int32_t* out_idx = cand_idx + row * cand_ld;
   // survivors >= R of this CTA, compacted, then ranked by token below
   if (tid == 0) { s_n = 0; s_S = Sl; }
   __syncthreads();
-  if (nsv <= SC) {
-    for (int i = tid; i < nsv; i += NT) {
-      const float v = sv_val[i];
-      const int j = sv_idx[i];
-      if (v >= R) {
-        const int p = atomicAdd(&s_n, 1);
-        if (p < NT * 2) {  // (index, value) pairs
-          part_max[2 * p] = __int_as_float(j);
-          part_max[2 * p + 1] = v;
-        }
+  const int nsp = s_cnt;  // spilled survivors
+  auto filt = [&](int2 sv) {
+    const float v = __int_as_float(sv.y);
+    if (v >= R) {
+      const int p = atomicAdd(&s_n, 1);
+      if (p < NT * 2) {  // (index, value) pairs
+        part_max[2 * p] = __int_as_float(sv.x);
+        part_max[2 * p + 1] = v;
       }
     }
-  }
+  };
+  for (int i = 0; i < nt_sv; ++i) filt(tsv[i][tid]);
+  for (int i = tid; i < min(nsp, SP); i += NT) filt(spill[i]);
   __syncthreads();
-  if (tid == 0) s_ovf = (nsv > SC || s_n > NT * 2) ? 1 : 0;
+  if (tid == 0) s_ovf = (nsp > SP || s_n > NT * 2) ? 1 : 0;
   if (C > 1) cl_sync_all();  // counts, overflow flags and partial sums visible
   else __syncthreads();
   int ovf = 0, base = 0, total = 0;

@@ -8,9 +8,11 @@ cd "$(dirname "$0")/.."
 python -m paper_2010_13887_b200.build > /dev/null
 mkdir -p build/variants
 B=$(basename $F .cu)
+SRC=paper_2010_13887_b200/csrc/$F
+[ -f "$F" ] && SRC=$F  # a path: e.g. an older revision of a csrc file (same basename)
 nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -lineinfo -Xcompiler -fPIC \
   --expt-relaxed-constexpr -I include -I paper_2010_13887_b200/csrc "$@" \
-  -c paper_2010_13887_b200/csrc/$F -o build/variants/$N.$B.o
+  -c $SRC -o build/variants/$N.$B.o
 OBJS=$(ls build/obj/*.o | grep -v "/$B.o")
 nvcc -gencode arch=compute_100a,code=sm_100a -shared -o build/variants/$N.so $OBJS \
   build/variants/$N.$B.o -lcudart -ldl
