@@ -253,7 +253,7 @@ __device__ __forceinline__ float ex2_ftz(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
-constexpr int kSwU = 8;   // pilot vectors per thread (fewer: more survivors, measured slower)
+constexpr int kSwU = 8;  // pilot vectors per thread (2 / 4 / 6 measured slower or equal)
 constexpr int kSwP = 8;   // async ring depth (vectors in flight per thread)
 // CTAs (cluster) per row and threads per CTA (A/B builds: -DFQ_ROW_SPLIT,
 // -DFQ_ROW_NT). 2 x 128-thread CTAs per row (7 resident per SM, one wave)
