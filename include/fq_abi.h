@@ -478,6 +478,13 @@ int fq_decoder_self_attention_xh(const float* sqkv, int64_t ldq, void* kcache, v
                                  int64_t rows, int64_t heads, int64_t head_dim, int64_t max_len,
                                  float scale, float* out, void* out_hi, void* out_lo,
                                  int64_t ldo, fq_stream_t stream);
+/* Exact-mode encoder self-attention on 3xFP16 warp MMAs (head_dim 64, seq <=
+ * 64; model.py:329-336, kernels.py:106-139 softmax): ctx written as the
+ * out-projection GEMM's fp16 pair (out_hi, out_lo) and optionally fp32 `out`. */
+int fq_encoder_attention_xh(const float* qkv, int64_t ldq, int64_t batch, int64_t seq,
+                            int64_t heads, int64_t head_dim, float scale, const float* mask,
+                            float* out, void* out_hi, void* out_lo, int64_t ldo, int* d_bad,
+                            fq_stream_t stream);
 int fq_cross_attention_xh(const float* cq, int64_t ldcq, const void* ck, const void* cv,
                           int64_t plane, int64_t ldkv, int64_t batch, int64_t beam, int64_t seq,
                           int64_t heads, int64_t head_dim, float scale, const float* mask,

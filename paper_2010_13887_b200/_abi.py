@@ -69,6 +69,7 @@ SIGNATURES = {
                             P], I32),
     "fq_beam_state_init": ([BeamStateC, I64, I64, I64, P], I32),
     "fq_step_advance": ([P, P], I32),
+    "fq_encoder_attention_xh": ([P, I64, I64, I64, I64, I64, F32, P, P, P, P, I64, P, P], I32),
     "fq_sample_step": ([P, I64, P, P, I64, P, I64, I64, F64, I64, I64, I64, P, I64, P, P, P,
                         I64, I64, P, P, P, P, P, P, P, P], I32),
     "fq_encoder_attention": ([P, I64, I64, I64, I64, I64, F32, P, P, P, I64, I32, P, P], I32),

@@ -1971,6 +1971,165 @@ __global__ void __launch_bounds__(32) cross_attention_xh(
   }
 }
 
+// Exact-mode encoder self-attention (model.py:329-336, kernels.py:106-139) for
+// head_dim 64, seq <= 64: CTA per (item, head), 4 warps x 16 queries. Q, K, V
+// as fp16 pairs (split_xh2) in XOR-swizzled shared memory; S = Q K^T and
+// O = P V as 3xFP16 m16n8k16 products (big = hi.hi, small = hi.lo + lo.hi,
+// combined with RN adds); between them the reference's softmax as in the
+// decoder kernels (fp32 score x scale (+ mask) with two roundings, exp of the
+// f64-exact difference on the SFU, f64 sums, p = fp32(e / sum)); the context is
+// written as the out-projection GEMM's fp16 pair (and fp32 when asked).
+__global__ void __launch_bounds__(128) encoder_attention_xh(
+    const float* __restrict__ qkv, int64_t ldq, int seq, int heads, float scale,
+    const float* __restrict__ mask, float* __restrict__ out, h16* __restrict__ out_hi,
+    h16* __restrict__ out_lo, int64_t ldo, int* d_bad) {
+  constexpr int HD = 64, NP = 64;
+  __shared__ __align__(128) uint8_t sm[6][NP * 128];  // Qh Ql Kh Kl Vh Vl, rows of 128 B
+  pdl_enter();
+  const int b = blockIdx.x / heads, h = blockIdx.x % heads;
+  const int d = heads * HD;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int g = lane >> 2, t4 = lane & 3;
+  for (int x = tid; x < 3 * NP * (HD / 4); x += 128) {
+    const int tsr = x / (NP * (HD / 4)), rem = x % (NP * (HD / 4));
+    const int row = rem / (HD / 4), c4 = rem % (HD / 4);
+    float4 f = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (row < seq)
+      f = *reinterpret_cast<const float4*>(qkv + ((int64_t)b * seq + row) * ldq + tsr * d +
+                                           h * HD + 4 * c4);
+    uint32_t h0, l0, h1, l1;
+    split_xh2(f.x, f.y, h0, l0);
+    split_xh2(f.z, f.w, h1, l1);
+    const uint32_t off = (uint32_t)(row * 128 + (((c4 >> 1) ^ (row & 7)) << 4) + (c4 & 1) * 8);
+    *reinterpret_cast<uint2*>(&sm[2 * tsr][0] + off) = make_uint2(h0, h1);
+    *reinterpret_cast<uint2*>(&sm[2 * tsr + 1][0] + off) = make_uint2(l0, l1);
+  }
+  __syncthreads();
+  const int q0 = 16 * w;
+  if (q0 >= seq) return;
+  const int lrow = (lane & 7) + ((lane >> 3) & 1) * 8, lch = lane >> 4;
+  float sb[8][4], ss[8][4];
+#pragma unroll
+  for (int n = 0; n < 8; ++n)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) sb[n][j] = ss[n][j] = 0.0f;
+#pragma unroll
+  for (int kk = 0; kk < 4; ++kk) {
+    uint32_t qa[4], qb[4];
+    ldsm_x4(qa, &sm[0][0] + swz(q0 + lrow, 2 * kk + lch));
+    ldsm_x4(qb, &sm[1][0] + swz(q0 + lrow, 2 * kk + lch));
+#pragma unroll
+    for (int n = 0; n < 8; ++n) {
+      uint32_t kh[2], kl[2];
+      const int krow = 8 * n + (lane & 7), kch = 2 * kk + ((lane >> 3) & 1);
+      asm volatile("ldmatrix.sync.aligned.m8n8.x2.shared.b16 {%0,%1}, [%2];"
+                   : "=r"(kh[0]), "=r"(kh[1])
+                   : "r"(sm_u32(&sm[2][0] + swz(krow, kch))));
+      asm volatile("ldmatrix.sync.aligned.m8n8.x2.shared.b16 {%0,%1}, [%2];"
+                   : "=r"(kl[0]), "=r"(kl[1])
+                   : "r"(sm_u32(&sm[3][0] + swz(krow, kch))));
+      mma_f16_16816(sb[n], qa, kh[0], kh[1]);
+      mma_f16_16816(ss[n], qa, kl[0], kl[1]);
+      mma_f16_16816(ss[n], qb, kh[0], kh[1]);
+    }
+  }
+  // softmax per query row (rows g and g + 8 of the warp's tile; lane t4 holds
+  // keys 8n + 2t4, +1)
+  const float* mk = mask ? mask + (int64_t)b * seq : nullptr;
+  float sc[8][4];
+  float mx[2] = {-INFINITY, -INFINITY};
+#pragma unroll
+  for (int n = 0; n < 8; ++n) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int key = 8 * n + 2 * t4 + (j & 1);
+      float t = -INFINITY;
+      if (key < seq) {
+        t = fmul_rn(fadd_rn(sb[n][j], ss[n][j] * kXhInv), scale);
+        if (mk) t = fadd_rn(t, mk[key]);
+      }
+      sc[n][j] = t;
+      mx[j >> 1] = fmaxf(mx[j >> 1], t);
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffffu, mx[r], 1));
+    mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffffu, mx[r], 2));
+  }
+  double l[2] = {0.0, 0.0};
+#pragma unroll
+  for (int n = 0; n < 8; ++n) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int r = j >> 1;
+      const float e = sc[n][j] == -INFINITY ? 0.0f : xh_exp_diff(sc[n][j], mx[r]);
+      sc[n][j] = e;
+      l[r] += (double)e;
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    l[r] += __shfl_xor_sync(0xffffffffu, l[r], 1);
+    l[r] += __shfl_xor_sync(0xffffffffu, l[r], 2);
+  }
+  const double inv[2] = {l[0] > 0.0 ? 1.0 / l[0] : 0.0, l[1] > 0.0 ? 1.0 / l[1] : 0.0};
+#pragma unroll
+  for (int n = 0; n < 8; ++n)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) sc[n][j] = (float)((double)sc[n][j] * inv[j >> 1]);
+  float ob[8][4], os[8][4];
+#pragma unroll
+  for (int n = 0; n < 8; ++n)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) ob[n][j] = os[n][j] = 0.0f;
+#pragma unroll
+  for (int kk = 0; kk < 4; ++kk) {
+    uint32_t ph[4], pl[4];
+    split_xh2(sc[2 * kk][0], sc[2 * kk][1], ph[0], pl[0]);
+    split_xh2(sc[2 * kk][2], sc[2 * kk][3], ph[1], pl[1]);
+    split_xh2(sc[2 * kk + 1][0], sc[2 * kk + 1][1], ph[2], pl[2]);
+    split_xh2(sc[2 * kk + 1][2], sc[2 * kk + 1][3], ph[3], pl[3]);
+#pragma unroll
+    for (int n = 0; n < 8; ++n) {
+      uint32_t vh[2], vl[2];
+      const int vrow = 16 * kk + (lane & 7) + ((lane >> 3) & 1) * 8, vch = n;
+      asm volatile("ldmatrix.sync.aligned.m8n8.x2.trans.shared.b16 {%0,%1}, [%2];"
+                   : "=r"(vh[0]), "=r"(vh[1])
+                   : "r"(sm_u32(&sm[4][0] + swz(vrow, vch))));
+      asm volatile("ldmatrix.sync.aligned.m8n8.x2.trans.shared.b16 {%0,%1}, [%2];"
+                   : "=r"(vl[0]), "=r"(vl[1])
+                   : "r"(sm_u32(&sm[5][0] + swz(vrow, vch))));
+      mma_f16_16816(ob[n], ph, vh[0], vh[1]);
+      mma_f16_16816(os[n], ph, vl[0], vl[1]);
+      mma_f16_16816(os[n], pl, vh[0], vh[1]);
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    const int q = q0 + g + 8 * r;
+    if (q >= seq) continue;
+    if (!(l[r] > 0.0)) {
+      if (t4 == 0 && d_bad) atomicAdd(d_bad, 1);
+      continue;
+    }
+    const int64_t o = ((int64_t)b * seq + q) * ldo + h * HD;
+#pragma unroll
+    for (int n = 0; n < 8; ++n) {
+      const float v0 = fadd_rn(ob[n][2 * r], os[n][2 * r] * kXhInv);
+      const float v1 = fadd_rn(ob[n][2 * r + 1], os[n][2 * r + 1] * kXhInv);
+      const int dd = 8 * n + 2 * t4;
+      if (out) *reinterpret_cast<float2*>(out + o + dd) = make_float2(v0, v1);
+      if (out_hi) {
+        uint32_t ph, pl;
+        split_xh2(v0, v1, ph, pl);
+        *reinterpret_cast<uint32_t*>(out_hi + o + dd) = ph;
+        *reinterpret_cast<uint32_t*>(out_lo + o + dd) = pl;
+      }
+    }
+  }
+}
+
 int attention_xh_prepare() {
   const int sz = 160 * 1024;  // scores + history of long max_len (static ring <= 26 KB)
 #define FQ_XH_OPT(HD)                                                                           \
@@ -2035,6 +2194,19 @@ int fq_encoder_attention(const float* qkv, int64_t ldq, int64_t batch, int64_t s
       qkv, ldq, (int)seq, (int)heads, (int)head_dim, scale, mask, out,
       reinterpret_cast<fq::h16*>(out16), ldo, exact, d_bad);
   return launch_status("fq_encoder_attention");
+}
+
+int fq_encoder_attention_xh(const float* qkv, int64_t ldq, int64_t batch, int64_t seq,
+                            int64_t heads, int64_t head_dim, float scale, const float* mask,
+                            float* out, void* out_hi, void* out_lo, int64_t ldo, int* d_bad,
+                            fq_stream_t stream) {
+  FQ_CHECK_ARG(qkv && out_hi && out_lo && batch > 0 && seq > 0 && seq <= 64 && heads > 0 &&
+                   head_dim == 64 && ldq % 4 == 0 && ((uintptr_t)qkv & 15) == 0 && ldo % 2 == 0,
+               FQ_ERR_DIMENSION, "fq_encoder_attention_xh: needs head_dim 64, seq <= 64");
+  launch_kernel(encoder_attention_xh, (unsigned)(batch * heads), 128, 0, as_stream(stream), 1u,
+                qkv, ldq, (int)seq, (int)heads, scale, mask, out, (h16*)out_hi, (h16*)out_lo,
+                ldo, d_bad);
+  return launch_status("fq_encoder_attention_xh");
 }
 
 int fq_decoder_self_attention(const float* sqkv, int64_t ldq, void* kcache, void* vcache,

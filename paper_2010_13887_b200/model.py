@@ -597,16 +597,26 @@ def encoder_layer_forward(x, layer, config: ModelConfig, mask=None, batch: int =
     _lin(_P, X, x16, layer["w_qkv"], qkv, bias=layer["b_qkv"], counters=ctr, timers=timers)
     ctr.count_fused("qkv_bias_reshape", n * 3 * d * 8, launches=1)
     ctx = bufs.get(f"{prefix}.ctx", (n, d), act16)
-    _abi.call("fq_encoder_attention", qkv.data_ptr(), qkv.stride(0), batch, seq, h, hd,
-              attention_scale(hd), _abi.ptr(mask), None if dw_half else ctx.data_ptr(),
-              ctx.data_ptr() if dw_half else None, d, 0 if dw_half else 1, _abi.ptr(bad), stream)
+    ctx16 = ctx
+    if not dw_half and hd == 64 and seq <= 64:
+        # exact mode on 3xFP16 warp MMAs, the ctx written as the GEMM's pair
+        ctx16 = half_operand(bufs, f"{prefix}.ctx16", (n, d), False)
+        _abi.call("fq_encoder_attention_xh", qkv.data_ptr(), qkv.stride(0), batch, seq, h, hd,
+                  attention_scale(hd), _abi.ptr(mask),
+                  ctx.data_ptr() if isinstance(layer["w_out"], X3Weight) else None,
+                  ctx16[0].data_ptr(),
+                  ctx16[1].data_ptr(), d, _abi.ptr(bad), stream)
+    else:
+        _abi.call("fq_encoder_attention", qkv.data_ptr(), qkv.stride(0), batch, seq, h, hd,
+                  attention_scale(hd), _abi.ptr(mask), None if dw_half else ctx.data_ptr(),
+                  ctx.data_ptr() if dw_half else None, d, 0 if dw_half else 1, _abi.ptr(bad),
+                  stream)
+        if not dw_half:
+            ctx16 = half_operand(bufs, f"{prefix}.ctx16", (n, d), False)
+            fill_pair(ctx, ctx16)
     ctr.count_fused("attention_scale_mask_softmax", n * d * 16)
     ctr.count_gemm(n * d * 8)  # QK^T, inside the fused attention kernel
     ctr.count_gemm(n * d * 8)  # P.V
-    ctx16 = ctx
-    if not dw_half:
-        ctx16 = half_operand(bufs, f"{prefix}.ctx16", (n, d), False)
-        fill_pair(ctx, ctx16)
     res1 = bufs.get(f"{prefix}.res1", (n, d))
     _lin(_P, ctx, ctx16, layer["w_out"], res1, bias=layer["b_out"], residual=X, counters=ctr,
          timers=timers)

@@ -287,3 +287,41 @@ def test_cross_attention_slabs_equal_reduced_query(T, M, beam, S):
            bad.data_ptr(), A.stream_handle())
     T.cuda.synchronize()
     assert T.equal(got, want)
+
+
+@pytest.mark.parametrize("S", [1, 17, 64])
+def test_encoder_attention_xh(T, S):
+    """Exact-mode encoder attention on 3xFP16 warp MMAs (head_dim 64, seq <= 64):
+    the fp32 context and its fp16 pair vs float64 (masked keys, a fully masked
+    row counted), the pair reconstructing the fp32 output."""
+    A = _abi()
+    g = T.Generator(device="cuda").manual_seed(S + 5)
+    B, H, hd = 3, 4, 64
+    d = H * hd
+    qkv = T.randn(B * S, 3 * d, device="cuda", generator=g)
+    mask = T.zeros(B, S, device="cuda")
+    if S > 1:
+        mask[1, S // 2 + 1:] = -math.inf
+    out = T.empty(B * S, d, device="cuda")
+    hi = T.empty(B * S, d, device="cuda", dtype=T.float16)
+    lo = T.empty_like(hi)
+    bad = T.zeros(1, dtype=T.int32, device="cuda")
+    scale = float(np.float32(1 / math.sqrt(hd)))
+    A.call("fq_encoder_attention_xh", qkv.data_ptr(), 3 * d, B, S, H, hd, scale,
+           mask.data_ptr(), out.data_ptr(), hi.data_ptr(), lo.data_ptr(), d, bad.data_ptr(),
+           A.stream_handle())
+    T.cuda.synchronize()
+    assert int(bad.item()) == 0
+    x = qkv.double().view(B, S, 3, H, hd)
+    Q, K, V = (x[:, :, i].permute(0, 2, 1, 3) for i in range(3))
+    P = _softmax_ref(T, (Q @ K.transpose(-1, -2)) * scale, mask.double()[:, None, None, :])
+    want = (P @ V).permute(0, 2, 1, 3).reshape(B * S, d)
+    assert _rel(out, want) <= 1e-5
+    back = hi.double() + lo.double() / 2048.0
+    assert float((back - out.double()).abs().max()) <= 1e-6 * float(out.abs().max()) + 1e-9
+    mask[2, :] = -math.inf  # a fully masked row: counted, not written
+    A.call("fq_encoder_attention_xh", qkv.data_ptr(), 3 * d, B, S, H, hd, scale,
+           mask.data_ptr(), out.data_ptr(), hi.data_ptr(), lo.data_ptr(), d, bad.data_ptr(),
+           A.stream_handle())
+    T.cuda.synchronize()
+    assert int(bad.item()) == S * H
