@@ -1140,6 +1140,12 @@ struct Stage2Pre {
   int rows_ok;
   int64_t top_off;  // the rows' top lists at cand_idx[row * cand_ld + top_off] (0: none)
   int32_t* top_mark;  // per-row top-list counts (-1: none), reset to 0 by stage 2
+  // item-cluster variant: the rows' counts, lse and top lists already gathered
+  // (tops = the peers' shared-memory top lists through DSMEM)
+  int rows_ready;
+  int64_t cnt[kMaxBeam];
+  double lse[kMaxBeam];
+  const int32_t* tops[kMaxBeam];
   double fsc_last;
   double cum[kMaxBeam];
   int32_t ph[kPreCap];  // [K][max_len] prefixes, then [K][max_len] history rows
@@ -1152,6 +1158,7 @@ __device__ __forceinline__ void stage2_prefetch(Stage2Pre& p, int b, const fq_be
   if (tid == 0) {
     p.top_off = top_off;
     p.top_mark = top_mark;
+    p.rows_ready = 0;
     p.in[0] = st.done[b];
     p.in[1] = st.live[b];
     p.in[2] = st.step[b];
@@ -1198,7 +1205,7 @@ __device__ __forceinline__ void select_item(
   int32_t* old_hist = old_pref + K * max_len;
   // the rows' top lists [K][kTopSlots] (sweep_row), behind the candidates
   int32_t* win = reinterpret_cast<int32_t*>(cands + kSelCap);
-  const bool use_win = pre && pre->top_off > 0;
+  const bool use_win = pre && (pre->top_off > 0 || pre->rows_ready);
   __shared__ int s_top;  // every live row has a top list: rank only those
 
   // every input of the item in one round trip: state scalars, per-row counts
@@ -1214,11 +1221,14 @@ __device__ __forceinline__ void select_item(
     if (tid < 5) s_in[tid] = pre->in[tid];
     if (tid == 0) s_fsc_last = pre->fsc_last;
     if (tid < K) {
-      cnt_s[tid] = __ldcg(cand_count + row0 + tid);
-      lse_s[tid] = __ldcg(lse + row0 + tid);
+      cnt_s[tid] = pre->rows_ready ? pre->cnt[tid] : __ldcg(cand_count + row0 + tid);
+      lse_s[tid] = pre->rows_ready ? pre->lse[tid] : __ldcg(lse + row0 + tid);
       cum_s[tid] = pre->cum[tid];
     }
-    if (use_win) {
+    if (pre->rows_ready) {  // the rows' top lists from the item cluster's shared memory
+      for (int e = tid; e < K * kTopSlots; e += blockDim.x)
+        win[e] = pre->tops[e / kTopSlots][e % kTopSlots];
+    } else if (use_win) {
       for (int e = tid; e < K * kTopSlots; e += blockDim.x)
         win[e] = e % kTopSlots ? __ldcg(cand_idx + (row0 + e / kTopSlots) * cand_ld +
                                         pre->top_off + e % kTopSlots)
@@ -1250,7 +1260,7 @@ __device__ __forceinline__ void select_item(
   }
   }
   __syncthreads();
-  if (use_win && tid < K) pre->top_mark[row0 + tid] = 0;  // self-resetting (split counters)
+  if (use_win && !pre->rows_ready && tid < K) pre->top_mark[row0 + tid] = 0;  // self-resetting
   if (s_in[0]) {  // engine.py:148-155: dead rows get parent row0, token 0
     if (tid < K) {
       row_parents[row0 + tid] = row0;
@@ -1588,6 +1598,89 @@ __global__ void __launch_bounds__(kRowThreads, kRowMinBlocks) hars_step_kernel(
                   d, emb_scale, pos, x_next, x16_next, batch, all_cnt, x16_next_lo, &pre);
 }
 
+// The fused HARS step with one thread-block cluster per item (cluster = the
+// item's K rows, one CTA each): each CTA sweeps its row (stage 1) and keeps its
+// count, lse and best-32 top list in shared memory; after a cluster barrier
+// the leader (rank 0) reads them through DSMEM (no global arrival counter,
+// fence or candidate round trip), runs stage 2 and publishes the new tokens;
+// after a second barrier every CTA writes its own row of the next step's
+// input, and a third keeps the leader's shared memory alive until read.
+__global__ void __launch_bounds__(kRowThreads, kRowMinBlocks) hars_step_item_kernel(
+    const float* __restrict__ logits, int64_t ld, int V, fq_beam_state st, int batch, int K,
+    int max_len, int eos, const double* __restrict__ len_pow, int32_t* d_cur, int64_t max_steps,
+    double* lse, int32_t* cand_idx, int64_t cand_ld, int64_t* cand_count, int* all_cnt,
+    int64_t* row_tokens, int64_t* row_parents, int32_t* hist, const float* __restrict__ emb,
+    int d, float emb_scale, const float* __restrict__ pos, float* __restrict__ x_next,
+    h16* __restrict__ x16_next, h16* __restrict__ x16_next_lo) {
+  pdl_enter();
+  const int rank = (int)cl_rank();
+  const int64_t row = blockIdx.x;
+  const int b = (int)(row / K), i = (int)(row % K);
+  const int cur0 = *d_cur;
+  const int live = st.live[b];
+  const int k = (!st.done[b] && i < live) ? min(K + live, V) : 0;  // hars_groups
+  extern __shared__ __align__(16) float4 sw_ring[];  // aliases stage 2's dynamic smem
+  const int64_t vals_off = cand_ld / 2 >= kSwThreads * 2 ? cand_ld / 2 : 0;
+  __shared__ Stage2Pre pre;
+  __shared__ int32_t s_top[kTopSlots];
+  __shared__ double s_lse;
+  __shared__ int64_t s_cnt_row, s_tok[kMaxBeam];
+  if (rank == 0) stage2_prefetch(pre, b, st, K, max_len, hist, cur0, 0, nullptr);
+  sweep_row<kRowThreads>(logits, ld, V, row, k, nullptr, 0, nullptr, lse, cand_idx, cand_ld,
+                         cand_count, sw_ring, 1, 0, vals_off, s_top, &s_top[0]);
+  __syncthreads();
+  if (threadIdx.x == 0) {  // this thread wrote them (sweep_row's tid 0)
+    s_lse = k > 0 ? lse[row] : 0.0;
+    s_cnt_row = k > 0 ? cand_count[row] : 0;
+  }
+  cl_sync_all();  // every row of the item swept
+  if (rank == 0) {
+    if (threadIdx.x < K) {
+      pre.cnt[threadIdx.x] = *peer_ptr(&s_cnt_row, threadIdx.x);
+      pre.lse[threadIdx.x] = *peer_ptr(&s_lse, threadIdx.x);
+      pre.tops[threadIdx.x] = peer_ptr(&s_top[0], threadIdx.x);
+    }
+    if (threadIdx.x == 0) pre.rows_ready = 1;
+    __syncthreads();
+    select_item(b, logits, ld, lse, cand_idx, cand_ld, cand_count, st, K, max_len, eos, len_pow,
+                d_cur, max_steps, row_tokens, row_parents, hist, vals_off, s_tok, &pre);
+    __syncthreads();
+  }
+  cl_sync_all();  // the leader's new tokens are published
+  // this row of the next step's decoder input (embed_scale_pos, kernels.py:143-151)
+  const int nxt = cur0 + 1;
+  if (x_next && nxt < max_len) {
+    const int64_t tok = *peer_ptr(&s_tok[i], 0);
+    const int d4 = d >> 2;
+    for (int idx = threadIdx.x; idx < d4; idx += blockDim.x) {
+      const int j = 4 * idx;
+      const float4 e = *reinterpret_cast<const float4*>(emb + tok * d + j);
+      const float4 p = *reinterpret_cast<const float4*>(pos + (int64_t)nxt * d + j);
+      float4 v;
+      v.x = fadd_rn(fmul_rn(e.x, emb_scale), p.x);
+      v.y = fadd_rn(fmul_rn(e.y, emb_scale), p.y);
+      v.z = fadd_rn(fmul_rn(e.z, emb_scale), p.z);
+      v.w = fadd_rn(fmul_rn(e.w, emb_scale), p.w);
+      *reinterpret_cast<float4*>(x_next + row * d + j) = v;
+      if (x16_next) {
+        uint2 ph, pl;
+        split_xh2(v.x, v.y, ph.x, pl.x);
+        split_xh2(v.z, v.w, ph.y, pl.y);
+        *reinterpret_cast<uint2*>(x16_next + row * d + j) = ph;
+        if (x16_next_lo) *reinterpret_cast<uint2*>(x16_next_lo + row * d + j) = pl;
+      }
+    }
+  }
+  cl_sync_all();  // peers done reading the leader's tokens
+  if (rank == 0 && threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(all_cnt, 1) == batch - 1) {  // every item read d_cur: advance it
+      *all_cnt = 0;
+      *d_cur += 1;
+    }
+  }
+}
+
 // The fused HARS step on the balanced split (few rows: rows < 2 x SMs): as
 // hars_step_kernel, but stage 1 runs on split_walk; the CTA that completes a
 // row arrives at its item, the one completing the item runs stage 2 + the
@@ -1838,6 +1931,17 @@ static int row_cluster(int64_t rows) {
   return C;
 }
 
+// FQ_HARS_ITEMCL=0 returns the fused step to the global arrival-counter
+// hand-over (A/B runs).
+static bool item_cluster_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("FQ_HARS_ITEMCL");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
 static bool split_forced() {
   const char* e = getenv("FQ_HARS_SPLIT");
   return e && e[0] == '1';
@@ -1984,6 +2088,15 @@ int fq_hars_step(const float* logits, int64_t ld, fq_beam_state st, int64_t batc
                                (size_t)kSwP * kRowThreads * sizeof(float4));
   FQ_CHECK_ARG(smem <= 96 * 1024, FQ_ERR_CAPACITY, "fq_hars_step: max_len too large");
   const int C = row_cluster(batch * beam);
+  if (C == 1 && beam <= 8 && item_cluster_enabled()) {
+    launch_kernel(hars_step_item_kernel, (unsigned)(batch * beam), kRowThreads, smem,
+                  as_stream(stream), (unsigned)beam, logits, ld, (int)vocab, st, (int)batch,
+                  (int)beam, (int)max_len, (int)eos, len_pow, d_cur, max_steps, lse, cand_idx,
+                  cand_ld, cand_count, counters + batch, row_tokens, row_parents, hist,
+                  x_next ? emb : nullptr, (int)d_model, emb_scale, pos, x_next,
+                  reinterpret_cast<fq::h16*>(x16_next), reinterpret_cast<fq::h16*>(x16_next_lo));
+    return launch_status("fq_hars_step");
+  }
   launch_kernel(hars_step_kernel, (unsigned)(batch * beam * C), kRowThreads, smem,
                 as_stream(stream), (unsigned)C, logits, ld, (int)vocab, st, (int)batch, (int)beam, (int)max_len, (int)eos,
                 len_pow, d_cur, max_steps, lse, cand_idx, cand_ld, cand_count, counters,
@@ -2045,6 +2158,8 @@ int fq_hars_prepare(void) {
   if (cudaFuncSetAttribute(hars_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            160 * 1024) != cudaSuccess ||
       cudaFuncSetAttribute(hars_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           96 * 1024) != cudaSuccess ||
+      cudaFuncSetAttribute(hars_step_item_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            96 * 1024) != cudaSuccess ||
       cudaFuncSetAttribute(retrieve_sweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            64 * 1024) != cudaSuccess ||
