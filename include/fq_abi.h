@@ -225,6 +225,12 @@ int fq_gemm_x3h_pair(const void* a, const void* a_lo, int64_t lda, const void* b
  * GEMM + LN pairs, model.py:339-358 / :582-626); out16 / out16_lo (optional)
  * receive the output's fp16 pair for the next exact-mode GEMM. The 4-slice
  * plan writes K-slice slabs to ws, summed in slice order by the LN kernel. */
+/* Exact-mode GEMM as split-K partial slabs only ([S][M][N] fp32 in ws, slab s
+ * = K slice s) for the K/4-slice shapes (N <= 1024, K >= 1024); *nslab (host
+ * int) receives S. FQ_ERR_UNSUPPORTED for other shapes. */
+int fq_gemm_x3h_slabs(const void* a, const void* a_lo, int64_t lda, const void* b,
+                      const void* b_lo, int64_t ldb, void* ws, int64_t ws_bytes, int64_t M,
+                      int64_t N, int64_t K, int32_t* nslab, fq_stream_t stream);
 int fq_gemm_x3h_ln(const void* a, const void* a_lo, int64_t lda, const void* b,
                    const void* b_lo, int64_t ldb, const float* bias, const float* res,
                    int64_t ldr, const float* gamma, const float* beta, double eps, float* out,
@@ -485,6 +491,15 @@ int fq_encoder_attention_xh(const float* qkv, int64_t ldq, int64_t batch, int64_
                             int64_t heads, int64_t head_dim, float scale, const float* mask,
                             float* out, void* out_hi, void* out_lo, int64_t ldo, int* d_bad,
                             fq_stream_t stream);
+/* fq_cross_attention_xh with the query as the nslab split-K slabs of its GEMM
+ * (fq_gemm_x3h_slabs: q_slabs + s * slab_stride, row stride ldq) summed in
+ * slab order, + q_bias -- the DSMEM epilogue's additions, so the same bits. */
+int fq_cross_attention_xh_slabs(const float* q_slabs, int64_t nslab, int64_t ldq,
+                                int64_t slab_stride, const float* q_bias, const void* ck,
+                                const void* cv, int64_t plane, int64_t ldkv, int64_t batch,
+                                int64_t beam, int64_t seq, int64_t heads, int64_t head_dim,
+                                float scale, const float* mask, float* out, void* out_hi,
+                                void* out_lo, int64_t ldo, int* d_bad, fq_stream_t stream);
 int fq_cross_attention_xh(const float* cq, int64_t ldcq, const void* ck, const void* cv,
                           int64_t plane, int64_t ldkv, int64_t batch, int64_t beam, int64_t seq,
                           int64_t heads, int64_t head_dim, float scale, const float* mask,

@@ -69,6 +69,9 @@ SIGNATURES = {
                             P], I32),
     "fq_beam_state_init": ([BeamStateC, I64, I64, I64, P], I32),
     "fq_step_advance": ([P, P], I32),
+    "fq_gemm_x3h_slabs": ([P, P, I64, P, P, I64, P, I64, I64, I64, I64, P, P], I32),
+    "fq_cross_attention_xh_slabs": ([P, I64, I64, I64, P, P, P, I64, I64, I64, I64, I64, I64,
+                                     I64, F32, P, P, P, P, I64, P, P], I32),
     "fq_encoder_attention_xh": ([P, I64, I64, I64, I64, I64, F32, P, P, P, P, I64, P, P], I32),
     "fq_sample_step": ([P, I64, P, P, I64, P, I64, I64, F64, I64, I64, I64, P, I64, P, P, P,
                         I64, I64, P, P, P, P, P, P, P, P], I32),
@@ -178,6 +181,23 @@ def call(name: str, *args) -> int:
     if rc < 0:
         msg = lib.fq_last_error().decode("utf-8", "replace")
         raise _ERRORS.get(rc, EngineError)(f"{name}: {msg}")
+    return rc
+
+
+def lib_call_rc(name: str, *args) -> int:
+    """Like :func:`call` for an entry point whose "unsupported shape" status
+    is a routing answer (the caller falls back): returns the status instead
+    of raising, counts a launch only on success."""
+    global _prepared
+    lib = load()
+    if not _prepared:
+        rc = lib.fq_prepare()
+        if rc < 0:
+            raise ExtensionError(f"fq_prepare: {lib.fq_last_error().decode()}")
+        _prepared = True
+    rc = getattr(lib, name)(*args)
+    if rc >= 0:
+        _launches[0] += 1
     return rc
 
 

@@ -1770,7 +1770,11 @@ __global__ void __launch_bounds__(32) cross_attention_xh(
     const float* __restrict__ cq, int64_t ldcq, const h16* __restrict__ ck,
     const h16* __restrict__ cv, int64_t plane, int64_t ldkv, int beam, int seq, float scale,
     const float* __restrict__ mask, float* __restrict__ out, h16* __restrict__ out_hi,
-    h16* __restrict__ out_lo, int64_t ldo, int* d_bad) {
+    h16* __restrict__ out_lo, int64_t ldo, int* d_bad, int nslab = 0, int64_t qslab = 0,
+    const float* __restrict__ qbias = nullptr) {
+  // nslab > 0: cq holds the query GEMM's nslab split-K slabs (stride qslab
+  // floats) summed here in split order, then + qbias -- the additions of the
+  // split-K GEMM's DSMEM epilogue, so the query bits are the same.
   // HD = 64: 128-byte rows with the 16-byte chunks XOR-swizzled by row (no
   // padding: 12 instead of 13.5 KB of ring per warp at NS = 3); other head
   // dims keep a 16-byte row pad against ldmatrix bank conflicts
@@ -1822,11 +1826,47 @@ __global__ void __launch_bounds__(32) cross_attention_xh(
     const bool ok = g < beam;
     const float* qp = cq + ((int64_t)b * beam + (ok ? g : 0)) * ldcq + h * HD;
 #pragma unroll
+    // this lane's 2 KT query element pairs: every load issued before any add
+    float2 qv[KT][2];
+#pragma unroll
+    for (int kk = 0; kk < KT; ++kk)
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh)
+        qv[kk][hh] = ok ? *reinterpret_cast<const float2*>(qp + 16 * kk + 2 * t4 + 8 * hh)
+                        : make_float2(0.f, 0.f);
+    if (nslab > 0 && ok) {
+      float2 sv[3][KT][2], bv[KT][2];  // slabs 1..3 (nslab <= 4 on this path) and bias
+#pragma unroll
+      for (int sl = 0; sl < 3; ++sl)
+#pragma unroll
+        for (int kk = 0; kk < KT; ++kk)
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh)
+            sv[sl][kk][hh] = sl + 1 < nslab ? *reinterpret_cast<const float2*>(
+                                                  qp + (sl + 1) * qslab + 16 * kk + 2 * t4 + 8 * hh)
+                                            : make_float2(0.f, 0.f);
+#pragma unroll
+      for (int kk = 0; kk < KT; ++kk)
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh)
+          bv[kk][hh] = *reinterpret_cast<const float2*>(qbias + h * HD + 16 * kk + 2 * t4 + 8 * hh);
+#pragma unroll
+      for (int kk = 0; kk < KT; ++kk)
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          float2 v = qv[kk][hh];
+#pragma unroll
+          for (int sl = 0; sl < 3; ++sl)
+            if (sl + 1 < nslab) { v.x += sv[sl][kk][hh].x; v.y += sv[sl][kk][hh].y; }
+          v.x = fadd_rn(v.x, bv[kk][hh].x);
+          v.y = fadd_rn(v.y, bv[kk][hh].y);
+          qv[kk][hh] = v;
+        }
+    }
+#pragma unroll
     for (int kk = 0; kk < KT; ++kk) {
-      const float2 x0 = ok ? *reinterpret_cast<const float2*>(qp + 16 * kk + 2 * t4) : make_float2(0.f, 0.f);
-      const float2 x1 = ok ? *reinterpret_cast<const float2*>(qp + 16 * kk + 2 * t4 + 8) : make_float2(0.f, 0.f);
-      split_xh2(x0.x, x0.y, qh[kk][0], ql[kk][0]);
-      split_xh2(x1.x, x1.y, qh[kk][1], ql[kk][1]);
+      split_xh2(qv[kk][0].x, qv[kk][0].y, qh[kk][0], ql[kk][0]);
+      split_xh2(qv[kk][1].x, qv[kk][1].y, qh[kk][1], ql[kk][1]);
     }
   }
   // ---- pass 1: scores ----
@@ -2332,11 +2372,11 @@ int fq_decoder_self_attention_xh(const float* sqkv, int64_t ldq, void* kcache, v
   return launch_status("fq_decoder_self_attention_xh");
 }
 
-int fq_cross_attention_xh(const float* cq, int64_t ldcq, const void* ck, const void* cv,
-                          int64_t plane, int64_t ldkv, int64_t batch, int64_t beam, int64_t seq,
-                          int64_t heads, int64_t head_dim, float scale, const float* mask,
-                          float* out, void* out_hi, void* out_lo, int64_t ldo, int* d_bad,
-                          fq_stream_t stream) {
+static int cross_xh_launch(const float* cq, int64_t ldcq, const void* ck, const void* cv,
+                           int64_t plane, int64_t ldkv, int64_t batch, int64_t beam, int64_t seq,
+                           int64_t heads, int64_t head_dim, float scale, const float* mask,
+                           float* out, void* out_hi, void* out_lo, int64_t ldo, int* d_bad,
+                           int nslab, int64_t qslab, const float* qbias, fq_stream_t stream) {
   FQ_CHECK_ARG(cq && ck && cv && (out || out_hi) && (!out_hi == !out_lo) && batch > 0 &&
                    beam > 0 && beam <= 8 && seq > 0 && seq <= 128 && heads > 0 &&
                    (head_dim == 16 || head_dim == 32 || head_dim == 64 || head_dim == 128) &&
@@ -2359,7 +2399,7 @@ int fq_cross_attention_xh(const float* cq, int64_t ldcq, const void* ck, const v
                           : cross_attention_xh<HD, NT, 3>,                                    \
                 grid, 32, smem, as_stream(stream), 1u, cq, ldcq,                              \
                 (const h16*)ck, (const h16*)cv, plane, ldkv, (int)beam, (int)seq, scale, mask, \
-                out, (h16*)out_hi, (h16*)out_lo, ldo, d_bad)
+                out, (h16*)out_hi, (h16*)out_lo, ldo, d_bad, nslab, qslab, qbias)
 #define FQ_CROSS_XHH(HD)                                                                      \
   if (nt == 1) FQ_CROSS_XH(HD, 1);                                                            \
   else if (nt == 2) FQ_CROSS_XH(HD, 2);                                                       \
@@ -2373,6 +2413,29 @@ int fq_cross_attention_xh(const float* cq, int64_t ldcq, const void* ck, const v
 #undef FQ_CROSS_XHH
 #undef FQ_CROSS_XH
   return launch_status("fq_cross_attention_xh");
+}
+
+int fq_cross_attention_xh(const float* cq, int64_t ldcq, const void* ck, const void* cv,
+                          int64_t plane, int64_t ldkv, int64_t batch, int64_t beam, int64_t seq,
+                          int64_t heads, int64_t head_dim, float scale, const float* mask,
+                          float* out, void* out_hi, void* out_lo, int64_t ldo, int* d_bad,
+                          fq_stream_t stream) {
+  return cross_xh_launch(cq, ldcq, ck, cv, plane, ldkv, batch, beam, seq, heads, head_dim, scale,
+                         mask, out, out_hi, out_lo, ldo, d_bad, 0, 0, nullptr, stream);
+}
+
+int fq_cross_attention_xh_slabs(const float* q_slabs, int64_t nslab, int64_t ldq,
+                                int64_t slab_stride, const float* q_bias, const void* ck,
+                                const void* cv, int64_t plane, int64_t ldkv, int64_t batch,
+                                int64_t beam, int64_t seq, int64_t heads, int64_t head_dim,
+                                float scale, const float* mask, float* out, void* out_hi,
+                                void* out_lo, int64_t ldo, int* d_bad, fq_stream_t stream) {
+  FQ_CHECK_ARG(q_slabs && q_bias && nslab >= 1 && nslab <= 4 && slab_stride % 2 == 0 &&
+                   ((uintptr_t)q_bias & 7) == 0,
+               FQ_ERR_DIMENSION, "fq_cross_attention_xh_slabs: bad slabs");
+  return cross_xh_launch(q_slabs, ldq, ck, cv, plane, ldkv, batch, beam, seq, heads, head_dim,
+                         scale, mask, out, out_hi, out_lo, ldo, d_bad, (int)nslab, slab_stride,
+                         q_bias, stream);
 }
 
 int fq_cross_attention_slabs(const float* q_slabs, int nslab, int64_t ldq, const float* q_bias,

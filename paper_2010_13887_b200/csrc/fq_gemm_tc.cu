@@ -2424,6 +2424,30 @@ extern "C" int fq_gemm_x3h_pair(const void* a, const void* a_lo, int64_t lda, co
                                                tc::HarsEpi{}, b_lo, a_lo);
 }
 
+// The exact-mode GEMM as its split-K partial slabs only ([S][M][N] fp32 in ws,
+// slab s = K slice s; the consumer sums them in slice order, e.g. the exact
+// cross-attention's query load): for the shapes whose numerics are K/4
+// slices (N <= 1024, K >= 1024); *nslab receives S. FQ_ERR_UNSUPPORTED otherwise.
+extern "C" int fq_gemm_x3h_slabs(const void* a, const void* a_lo, int64_t lda, const void* b,
+                                 const void* b_lo, int64_t ldb, void* ws, int64_t ws_bytes,
+                                 int64_t M, int64_t N, int64_t K, int32_t* nslab,
+                                 fq_stream_t stream) {
+  FQ_CHECK_ARG(ws && nslab && M > 0 && N > 0 && K > 0, FQ_ERR_DIMENSION,
+               "fq_gemm_x3h_slabs: bad args");
+  int rc = check_xh(a, a_lo, lda, b, b_lo, ldb, M, N, K);
+  if (rc != FQ_OK) return rc;
+  const XhPlan p = plan_xh(M, N, K);
+  FQ_CHECK_ARG(p.split > 1 && ws_bytes >= (int64_t)p.split * M * N * (int64_t)sizeof(float) &&
+                   ((uintptr_t)ws & 15) == 0 && M % 32 == 0 && N % 32 == 0,
+               FQ_ERR_UNSUPPORTED, "fq_gemm_x3h_slabs: not a split-K slice shape");
+  tc::Epi ep{ws, N, 0, 0, nullptr, nullptr, 0, 0, g_gemm_dbg};
+  ep.chunk_kb = p.chunk_kb;
+  *nslab = p.split;
+  return tc::launch_splitk<128, 3, false, true, tc::OP_X3H>(a, lda, b, ldb, ep, M, N, K, p.split,
+                                                            as_stream(stream), tc::LnEpi{}, b_lo,
+                                                            a_lo);
+}
+
 extern "C" int fq_gemm_x3h_ln(const void* a, const void* a_lo, int64_t lda, const void* b,
                               const void* b_lo, int64_t ldb, const float* bias, const float* res,
                               int64_t ldr, const float* gamma, const float* beta, double eps,

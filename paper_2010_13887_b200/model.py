@@ -898,16 +898,36 @@ class DecoderStep:
         ctr.count_fused("decoder_self_attention", R * d * 16)
         _lin_ln(dw, self.sctx, self.sctx16, lw["w_so"], lw["b_so"], x, lw["ln1_g"], lw["ln1_b"],
                 c.ln_eps, self.snorm, self.snorm16, self.ln_ws, counters=ctr, timers=tm)
-        _lin(dw, self.snorm, self.snorm16, lw["w_cq"], self.cq, bias=lw["b_cq"], counters=ctr,
-             timers=tm)
         cr = self.cross  # [2, n, 2*L*d] pair planes
         ld = cr.stride(1)
         ch, cl = self.cctx16
-        _abi.call("fq_cross_attention_xh", self.cq.data_ptr(), self.cq.stride(0),
-                  cr[0, :, 2 * i * d:].data_ptr(), cr[0, :, (2 * i + 1) * d:].data_ptr(),
-                  cr.stride(0), ld, self.batch, self.beam, self.enc_seq, h, hd, scale,
-                  _abi.ptr(self.mask), None, ch.data_ptr(), cl.data_ptr(), ch.stride(0),
-                  self.bad.data_ptr(), stream)
+        # the cross query GEMM as its split-K slabs (in the LN workspace, free
+        # between LN1 and the cross-out GEMM), summed + biased by the
+        # cross-attention's query load: no DSMEM reduction, same bits
+        nsl = ctypes.c_int32(0)
+        qh, ql = self.snorm16
+        w_cq = lw["w_cq"]
+        rc = -1
+        if self.ln_ws is not None:
+            rc = _abi.lib_call_rc("fq_gemm_x3h_slabs", qh.data_ptr(), ql.data_ptr(), qh.stride(0),
+                                  w_cq.hi.data_ptr(), w_cq.lo.data_ptr(), w_cq.hi.stride(0),
+                                  self.ln_ws.data_ptr(), self.ln_ws.numel() * 4, R, d, d,
+                                  ctypes.addressof(nsl), stream)
+        if rc == 0:
+            ctr.count_gemm(R * d * 4 + d * d * 4 + R * d * 4)
+            _abi.call("fq_cross_attention_xh_slabs", self.ln_ws.data_ptr(), nsl.value, d, R * d,
+                      lw["b_cq"].data_ptr(), cr[0, :, 2 * i * d:].data_ptr(),
+                      cr[0, :, (2 * i + 1) * d:].data_ptr(), cr.stride(0), ld, self.batch,
+                      self.beam, self.enc_seq, h, hd, scale, _abi.ptr(self.mask), None,
+                      ch.data_ptr(), cl.data_ptr(), ch.stride(0), self.bad.data_ptr(), stream)
+        else:
+            _lin(dw, self.snorm, self.snorm16, w_cq, self.cq, bias=lw["b_cq"], counters=ctr,
+                 timers=tm)
+            _abi.call("fq_cross_attention_xh", self.cq.data_ptr(), self.cq.stride(0),
+                      cr[0, :, 2 * i * d:].data_ptr(), cr[0, :, (2 * i + 1) * d:].data_ptr(),
+                      cr.stride(0), ld, self.batch, self.beam, self.enc_seq, h, hd, scale,
+                      _abi.ptr(self.mask), None, ch.data_ptr(), cl.data_ptr(), ch.stride(0),
+                      self.bad.data_ptr(), stream)
         ctr.count_fused("cross_attention", R * d * 16)
         _lin_ln(dw, self.cctx, self.cctx16, lw["w_co"], lw["b_co"], self.snorm, lw["ln2_g"],
                 lw["ln2_b"], c.ln_eps, self.cnorm, self.cnorm16, self.ln_ws, counters=ctr,

@@ -325,3 +325,54 @@ def test_encoder_attention_xh(T, S):
            A.stream_handle())
     T.cuda.synchronize()
     assert int(bad.item()) == S * H
+
+
+def test_cross_attention_xh_slab_query_bit_identical(T):
+    """Exact cross-attention with the query as the split-K slabs of its GEMM
+    (fq_gemm_x3h_slabs + fq_cross_attention_xh_slabs: slabs summed in order +
+    bias in the query load) == the DSMEM-reduced query GEMM + the plain kernel,
+    bit for bit (C2 decode shape: 512 rows, d = 1024, 16 heads x 64)."""
+    import ctypes
+    from paper_2010_13887_b200.model import XHWeight
+    from paper_2010_13887_b200.tensor import split_pair
+    A = _abi()
+    g = T.Generator(device="cuda").manual_seed(17)
+    B, K, S, H, hd = 128, 4, 37, 16, 64
+    R, d = B * K, H * hd
+    x = T.randn(R, d, device="cuda", generator=g)
+    xh, xl = split_pair(x)
+    w = XHWeight.from_kn(T.randn(d, d, device="cuda", generator=g) * 0.03, transpose=False)
+    bias = T.randn(d, device="cuda", generator=g) * 0.1
+    kv = T.randn(B * S, 2 * d, device="cuda", generator=g)
+    kvh, kvl = split_pair(kv)
+    planes = T.stack([kvh, kvl]).contiguous()  # [2, B*S, 2d]
+    mask = T.zeros(B, S, device="cuda")
+    mask[3, 20:] = -math.inf
+    scale = float(np.float32(1 / math.sqrt(hd)))
+    q = T.empty(R, d, device="cuda")
+    A.call("fq_gemm_x3h", xh.data_ptr(), xl.data_ptr(), d, w.hi.data_ptr(), w.lo.data_ptr(), d,
+           q.data_ptr(), d, R, d, d, 0, bias.data_ptr(), None, 0, 0, A.stream_handle())
+    outs = []
+    for slabs in (False, True):
+        oh = T.empty(R, d, device="cuda", dtype=T.float16)
+        ol = T.empty_like(oh)
+        bad = T.zeros(1, dtype=T.int32, device="cuda")
+        args = (planes[0, :, :d].data_ptr(), planes[0, :, d:].data_ptr(), planes.stride(0),
+                planes.stride(1), B, K, S, H, hd, scale, mask.data_ptr(), None, oh.data_ptr(),
+                ol.data_ptr(), d, bad.data_ptr(), A.stream_handle())
+        if slabs:
+            ws = T.empty(4 * R * d, device="cuda")
+            n = ctypes.c_int32(0)
+            assert A.lib_call_rc("fq_gemm_x3h_slabs", xh.data_ptr(), xl.data_ptr(), d,
+                                 w.hi.data_ptr(), w.lo.data_ptr(), d, ws.data_ptr(),
+                                 ws.numel() * 4, R, d, d, ctypes.addressof(n),
+                                 A.stream_handle()) == 0
+            assert n.value == 4
+            A.call("fq_cross_attention_xh_slabs", ws.data_ptr(), n.value, d, R * d,
+                   bias.data_ptr(), *args)
+        else:
+            A.call("fq_cross_attention_xh", q.data_ptr(), d, *args)
+        T.cuda.synchronize()
+        assert int(bad.item()) == 0
+        outs.append((oh, ol))
+    assert T.equal(outs[0][0], outs[1][0]) and T.equal(outs[0][1], outs[1][1])
