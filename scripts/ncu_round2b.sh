@@ -33,7 +33,7 @@ cap encgemm "tc_gemm_kernel" 1
 cap selfattn "decoder_self_attention" 190
 cap crossattn "cross_attention" 190
 cap ln "layer_norm_slabs_row128" 540
-cap harsstep "hars_step_kernel" 30
+cap harsstep "hars_step_item_kernel" 30
 cap encattn "encoder_attention" 3
 cap logits16 "tc_gemm_kernel<.int.224" 30 fp16
 cap merge16 "hars_merge_step" 32 fp16
