@@ -186,8 +186,9 @@ def call(name: str, *args) -> int:
 
 def lib_call_rc(name: str, *args) -> int:
     """Like :func:`call` for an entry point whose "unsupported shape" status
-    is a routing answer (the caller falls back): returns the status instead
-    of raising, counts a launch only on success."""
+    (FQ_ERR_UNSUPPORTED) is a routing answer (the caller falls back): returns
+    that status instead of raising (any other error raises), counts a launch
+    only on success."""
     global _prepared
     lib = load()
     if not _prepared:
@@ -198,6 +199,9 @@ def lib_call_rc(name: str, *args) -> int:
     rc = getattr(lib, name)(*args)
     if rc >= 0:
         _launches[0] += 1
+    elif rc != -6:  # only FQ_ERR_UNSUPPORTED is a routing answer
+        msg = lib.fq_last_error().decode("utf-8", "replace")
+        raise _ERRORS.get(rc, EngineError)(f"{name}: {msg}")
     return rc
 
 
