@@ -1926,6 +1926,13 @@ static int hars_num_sms() {
 // fq_retrieve use the same rule, so their logsumexp bits agree.
 static int row_cluster(int64_t rows) {
   if (kSwSplit != 1) return kSwSplit;
+  static int forced = -1;  // FQ_ROW_C=1|2|4|8 (A/B runs)
+  if (forced < 0) {
+    const char* e = getenv("FQ_ROW_C");
+    forced = e ? atoi(e) : 0;
+    if (forced != 1 && forced != 2 && forced != 4 && forced != 8) forced = 0;
+  }
+  if (forced) return forced;
   int C = 1;
   while (C < 8 && rows * C * 2 <= 4 * (int64_t)hars_num_sms()) C *= 2;
   return C;
