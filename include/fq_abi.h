@@ -389,6 +389,18 @@ int fq_hars_merge_step(fq_beam_state st, int64_t batch, int64_t beam, int64_t vo
 int fq_beam_state_init(fq_beam_state st, int64_t batch, int64_t beam, int64_t max_len,
                        fq_stream_t stream);
 
+/* HOST helper (no device work): BeamState.finalize (decode.py:173-183) for a
+ * whole batch from the host copy of an fq_beam_state (all pointers HOST
+ * arrays): finished list + non-empty live prefixes not already finished
+ * (score cum / len**alpha), stably sorted by (-score, sequence), the first
+ * `keep` per item into out_tok [batch][keep][max_len], out_len, out_score,
+ * out_n [batch]. */
+int fq_finalize_beams(const int32_t* live, const int32_t* step, const int32_t* prefix,
+                      const double* cum, const int32_t* fin_count, const int32_t* fin_tok,
+                      const int32_t* fin_len, const double* fin_score, int64_t batch, int64_t K,
+                      int64_t max_len, double alpha, int64_t keep, int32_t* out_tok,
+                      int32_t* out_len, double* out_score, int32_t* out_n);
+
 /* *d_cur += 1 (KVCache.end_step, model.py:508-512). */
 int fq_step_advance(int32_t* d_cur, fq_stream_t stream);
 

@@ -69,6 +69,7 @@ SIGNATURES = {
                             P], I32),
     "fq_beam_state_init": ([BeamStateC, I64, I64, I64, P], I32),
     "fq_step_advance": ([P, P], I32),
+    "fq_finalize_beams": ([P, P, P, P, P, P, P, P, I64, I64, I64, F64, I64, P, P, P, P], I32),
     "fq_gemm_x3h_slabs": ([P, P, I64, P, P, I64, P, I64, I64, I64, I64, P, P], I32),
     "fq_cross_attention_xh_slabs": ([P, I64, I64, I64, P, P, P, I64, I64, I64, I64, I64, I64,
                                      I64, F32, P, P, P, P, I64, P, P], I32),
@@ -111,7 +112,7 @@ _lib = None
 _lock = threading.Lock()
 _prepared = False
 _NO_PREPARE = {"fq_abi_version", "fq_last_error", "fq_num_sms", "fq_prepare", "fq_gemm_plan",
-               "fq_set_pdl"}
+               "fq_set_pdl", "fq_finalize_beams"}
 _launches = [0]
 
 

@@ -172,3 +172,80 @@ int fq_split_f16(const float* src, int64_t lds, int64_t rows, int64_t cols, int 
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Host helper (no device work): BeamState.finalize (decode.py:173-183) for a
+// whole batch straight from the device beam state's host copy, so generate
+// returns hypotheses without building per-item BeamState objects. Per item:
+// the finished list (kept sorted by the device) then every non-empty live
+// prefix not already finished, scored cum / len**alpha (alpha != 0: the same
+// C pow as Python's float pow), stably sorted by (-score, sequence) and cut to
+// K. All pointers are HOST arrays of the fq_beam_state layout.
+// ---------------------------------------------------------------------------
+#include <math.h>
+#include <string.h>
+#include <vector>
+
+namespace {
+struct FinHyp {
+  const int32_t* tok;
+  int len;
+  double score;
+};
+bool fin_less(const FinHyp& a, const FinHyp& b) {  // key (-score, seq), Python order
+  if (a.score != b.score) return a.score > b.score;
+  const int n = a.len < b.len ? a.len : b.len;
+  for (int i = 0; i < n; ++i)
+    if (a.tok[i] != b.tok[i]) return a.tok[i] < b.tok[i];
+  return a.len < b.len;
+}
+}  // namespace
+
+extern "C" int fq_finalize_beams(const int32_t* live, const int32_t* step, const int32_t* prefix,
+                                 const double* cum, const int32_t* fin_count,
+                                 const int32_t* fin_tok, const int32_t* fin_len,
+                                 const double* fin_score, int64_t batch, int64_t K,
+                                 int64_t max_len, double alpha, int64_t keep, int32_t* out_tok,
+                                 int32_t* out_len, double* out_score, int32_t* out_n) {
+  if (!live || !step || !prefix || !cum || !fin_count || !fin_tok || !fin_len || !fin_score ||
+      !out_tok || !out_len || !out_score || !out_n || batch < 0 || K < 1 || max_len < 1 ||
+      keep < 1)
+    return FQ_ERR_DIMENSION;
+  std::vector<FinHyp> h;
+  h.reserve(2 * K);
+  for (int64_t b = 0; b < batch; ++b) {
+    h.clear();
+    const int nf = fin_count[b], nl = live[b], st = step[b];
+    for (int i = 0; i < nf && i < K; ++i)
+      h.push_back({fin_tok + (b * K + i) * max_len, fin_len[b * K + i], fin_score[b * K + i]});
+    const size_t nfin = h.size();
+    for (int i = 0; i < nl && i < K; ++i) {
+      const int32_t* p = prefix + (b * K + i) * max_len;
+      if (st <= 0) continue;  // empty prefix
+      bool dup = false;
+      for (size_t f = 0; f < nfin && !dup; ++f)
+        dup = h[f].len == st && memcmp(h[f].tok, p, (size_t)st * sizeof(int32_t)) == 0;
+      if (dup) continue;
+      const double c = cum[b * K + i];
+      h.push_back({p, st, alpha != 0.0 ? c / pow((double)st, alpha) : c});
+    }
+    // stable insertion sort (<= 2K entries)
+    for (size_t i = 1; i < h.size(); ++i) {
+      FinHyp x = h[i];
+      size_t j = i;
+      while (j > 0 && fin_less(x, h[j - 1])) {
+        h[j] = h[j - 1];
+        --j;
+      }
+      h[j] = x;
+    }
+    const int n = (int)(h.size() < (size_t)keep ? h.size() : (size_t)keep);
+    out_n[b] = n;
+    for (int i = 0; i < n; ++i) {
+      memcpy(out_tok + (b * keep + i) * max_len, h[i].tok, (size_t)h[i].len * sizeof(int32_t));
+      out_len[b * keep + i] = h[i].len;
+      out_score[b * keep + i] = h[i].score;
+    }
+  }
+  return FQ_OK;
+}

@@ -300,6 +300,33 @@ class DeviceBeamState:
 
     error_flags = None  # set by Session.generate: checked when the host reads the state
 
+    def finalize_batch(self, config: DecodeConfig) -> list:
+        """[state.finalize(config) for state in host_items()] in one native pass
+        over the host copy (fq_finalize_beams): (tokens, score) lists per item."""
+        from . import _abi
+        check_error_flags(self.error_flags)
+        h = self._to_host()
+        B, K, S = self.batch, self.beam, self.max_len
+        keep = config.effective_beam_size
+        ot = np.zeros((B, keep, S), np.int32)
+        ol = np.zeros((B, keep), np.int32)
+        osc = np.zeros((B, keep), np.float64)
+        on = np.zeros(B, np.int32)
+        arrs = [np.ascontiguousarray(h[n]) for n in ("live", "step", "prefix", "cum", "fin_count",
+                                                      "fin_tok", "fin_len", "fin_score")]
+        _abi.call("fq_finalize_beams", *[_np_ptr(a) for a in arrs], B, K, S,
+                  float(config.length_penalty), keep, _np_ptr(ot), _np_ptr(ol), _np_ptr(osc),
+                  _np_ptr(on))
+        # only the used tokens to Python, in one call: ragged (b, i) order
+        flat = ot[np.arange(S)[None, None, :] < ol[:, :, None]].tolist()
+        offs = np.concatenate([[0], np.cumsum(ol.ravel())]).tolist()
+        ll, sl, nl = ol.tolist(), osc.tolist(), on.tolist()
+        out = []
+        for b in range(B):
+            base = b * keep
+            out.append([(flat[offs[base + i]:offs[base + i + 1]], sl[b][i]) for i in range(nl[b])])
+        return out
+
     def host_items(self) -> list:
         check_error_flags(self.error_flags)
         h = self._to_host()
@@ -319,6 +346,10 @@ class DeviceBeamState:
                                  parents=par[b, :nl].tolist(), last_tokens=last,
                                  chosen_tokens=list(last)))
         return out
+
+
+def _np_ptr(a: np.ndarray) -> int:
+    return a.ctypes.data
 
 
 def length_penalty_table(alpha: float, max_len: int, device, out=None):

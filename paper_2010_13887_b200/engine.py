@@ -388,6 +388,9 @@ class Session:
                               "ovf": [g["ovf"] for g in groups if "ovf" in g]}
         if return_device_state:
             return result
+        if isinstance(result, D.DeviceBeamState):  # finalize natively from the host copy
+            return [[Hypothesis(tokens=s, score=sc) for s, sc in item]
+                    for item in result.finalize_batch(cfg)]
         states = result.host_items()
         return [[Hypothesis(tokens=s, score=sc) for s, sc in state.finalize(cfg)]
                 for state in states]

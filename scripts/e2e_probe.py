@@ -37,5 +37,10 @@ b, _ = t(lambda: sess.generate(src_pin, dc))
 c, _ = t(lambda: sess.generate(src_dev, dc))
 d, items = t(lambda: st.host_items())
 e, _ = t(lambda: [s.finalize(dc) for s in items])
+f_, _ = t(lambda: st.finalize_batch(dc))
+import paper_2010_13887_b200.decode as D
+g_, _ = t(lambda: st._to_host())
+h_, _ = t(lambda: D.check_error_flags(st.error_flags))
+print(f"finalize_batch {f_:.2f} ms | _to_host {g_:.2f} | error flags {h_:.2f}")
 print(f"device-state generate {a:.2f} ms | host-in generate {b:.2f} | device-in host-out {c:.2f} "
       f"| host_items {d:.2f} | finalize {e:.2f}")

@@ -147,3 +147,52 @@ def test_plan_errors():
         P.build_plan([])
     with pytest.raises(P.PlanError):
         P.build_plan([P.IntermediateSpec("a", 10, 3, 1)])
+
+
+def test_finalize_beams_host_helper_equals_beamstate_finalize():
+    """fq_finalize_beams (host helper, no GPU) == BeamState.finalize
+    (decode.py:173-183) over random batched states: finished lists with score
+    ties (sequence order decides), live prefixes duplicating a finished one,
+    length penalties, empty prefixes and partially finished items."""
+    import paper_2010_13887_b200 as P
+    from paper_2010_13887_b200 import _abi
+    rng = np.random.default_rng(7)
+    for trial in range(200):
+        B, K, S = int(rng.integers(1, 6)), int(rng.integers(1, 6)), int(rng.integers(2, 9))
+        alpha = float(rng.choice([0.0, 0.6, 1.0]))
+        live = rng.integers(0, K + 1, B).astype(np.int32)
+        step = rng.integers(0, S, B).astype(np.int32)
+        prefix = rng.integers(0, 4, (B, K, S)).astype(np.int32)
+        cum = np.round(rng.normal(size=(B, K)), 1)
+        fc = rng.integers(0, K + 1, B).astype(np.int32)
+        ft = rng.integers(0, 4, (B, K, S)).astype(np.int32)
+        fl = rng.integers(1, S + 1, (B, K)).astype(np.int32)
+        fs = np.round(rng.normal(size=(B, K)), 1)
+        states = []
+        for b in range(B):
+            fin = [(ft[b, i, :fl[b, i]].tolist(), float(fs[b, i])) for i in range(fc[b])]
+            if fc[b] and live[b] and step[b]:  # a live prefix equal to a finished sequence
+                ft[b, 0, :step[b]] = prefix[b, 0, :step[b]]
+                fl[b, 0] = step[b]
+                fin[0] = (prefix[b, 0, :step[b]].tolist(), fin[0][1])
+            fin.sort(key=lambda h: (-h[1], h[0]))  # the device keeps it sorted
+            for i, (sq, sc) in enumerate(fin):
+                ft[b, i, :len(sq)] = sq
+                fl[b, i] = len(sq)
+                fs[b, i] = sc
+            states.append(P.BeamState(prefixes=[prefix[b, i, :step[b]].tolist()
+                                                for i in range(live[b])],
+                                      cum_log_prob=cum[b, :live[b]].tolist(), finished=fin,
+                                      step=int(step[b])))
+        cfg = P.DecodeConfig(beam_size=K, length_penalty=alpha)
+        ot = np.zeros((B, K, S), np.int32)
+        ol = np.zeros((B, K), np.int32)
+        osc = np.zeros((B, K))
+        on = np.zeros(B, np.int32)
+        arrs = [np.ascontiguousarray(a) for a in (live, step, prefix, cum, fc, ft, fl, fs)]
+        assert _abi.call("fq_finalize_beams", *[a.ctypes.data for a in arrs], B, K, S, alpha, K,
+                         ot.ctypes.data, ol.ctypes.data, osc.ctypes.data, on.ctypes.data) == 0
+        for b in range(B):
+            want = states[b].finalize(cfg)
+            got = [(ot[b, i, :ol[b, i]].tolist(), float(osc[b, i])) for i in range(on[b])]
+            assert got == want, (trial, b, got, want)
