@@ -550,18 +550,19 @@ def test_retrieve_split_and_per_row_paths_agree(P, O, rows, V, split, monkeypatc
         assert abs(lse[b] - orr.logsumexp_full[0]) <= 1e-7 * abs(orr.logsumexp_full[0]) + 1e-7
 
 
-@pytest.mark.parametrize("split,B", [("1", 6), ("0", 6), ("0", 80)])
-def test_fused_hars_step_equals_separate_launches(P, split, B, monkeypatch):
+@pytest.mark.parametrize("split,B,K", [("1", 6, 4), ("0", 6, 4), ("0", 80, 4), ("0", 40, 8),
+                                       ("0", 20, 16)])
+def test_fused_hars_step_equals_separate_launches(P, split, B, K, monkeypatch):
     """fq_hars_step (groups + stage 1 + stage 2 + advance + next embedding in
     one launch) reproduces fq_hars_groups + fq_retrieve + fq_hars_select +
     fq_step_advance step for step, including EOS picks and a length penalty
     (the stage-1 layouts: "1" balanced split; "0" rows over CTA clusters at
     24 rows, and at 320 rows one CTA per row with the per-item cluster
-    hand-over of stage 2)."""
+    hand-over of stage 2, clusters of 4 and 8; beam 16 on the row kernel)."""
     import torch
     monkeypatch.setenv("FQ_HARS_SPLIT", split)
     from paper_2010_13887_b200 import _abi, decode as D
-    K, V, S, d, eos = 4, 32000, 16, 64, 7
+    V, S, d, eos = 32000, 16, 64, 7
     R = B * K
     g = torch.Generator(device="cuda").manual_seed(0)
     lp = D.length_penalty_table(0.6, S, "cuda")
