@@ -401,6 +401,12 @@ class Session:
         set per (batch, max_steps) shape, allocated on first use)."""
         key = (batch, max_steps)
         b = self._sample_buffers.get(key)
+        if b is None and len(self._sample_buffers) >= 4:  # bounded: drop the oldest shape
+            old = next(iter(self._sample_buffers))
+            del self._sample_buffers[old]
+            for gk in [gk for gk in self._graphs if gk[0] == "sample" and gk[1] == old[0]
+                       and gk[3] == old[1]]:
+                del self._graphs[gk]  # its graph points at the dropped buffers
         if b is None:
             dev = torch.device("cuda", torch.cuda.current_device())
             i32 = dict(dtype=torch.int32, device=dev)
