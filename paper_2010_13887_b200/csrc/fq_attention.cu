@@ -1785,7 +1785,6 @@ __global__ void __launch_bounds__(32) cross_attention_xh(
   constexpr int NP = NT * 16;
   constexpr int KT = HD / 16;
   __shared__ __align__(128) uint8_t ring[NS][2][16 * RS];
-  __shared__ float Ps[8][NP + 4];
   const int b = blockIdx.x, h = blockIdx.y, lane = threadIdx.x;
   const int g = lane >> 2, t4 = lane & 3;
   // the cross K/V planes are written once per request, before the decode
@@ -1945,15 +1944,13 @@ __global__ void __launch_bounds__(32) cross_attention_xh(
     l1 += __shfl_xor_sync(0xffffffffu, l1, o);
   }
   const double inv0 = l0 > 0.0 ? 1.0 / l0 : 0.0, inv1 = l1 > 0.0 ? 1.0 / l1 : 0.0;
+  // p = fp32(e / sum), kept in registers in the score layout (lane (g, t4):
+  // positions 16m + g (+8), beams 2t4, 2t4 + 1); pass 2 gathers its P^T
+  // fragments by shuffles (no smem: more warps resident per SM)
 #pragma unroll
-  for (int m = 0; m < NT; ++m) {
+  for (int m = 0; m < NT; ++m)
 #pragma unroll
-    for (int hh = 0; hh < 2; ++hh) {
-      const int p = 16 * m + g + 8 * hh;
-      Ps[2 * t4][p] = (float)((double)e[m][2 * hh] * inv0);
-      Ps[2 * t4 + 1][p] = (float)((double)e[m][2 * hh + 1] * inv1);
-    }
-  }
+    for (int c = 0; c < 4; ++c) e[m][c] = (float)((double)e[m][c] * ((c & 1) ? inv1 : inv0));
   if (d_bad && g == 0) {
     if (2 * t4 < beam && !(l0 > 0.0)) atomicAdd(d_bad, 1);
     if (2 * t4 + 1 < beam && !(l1 > 0.0)) atomicAdd(d_bad, 1);
@@ -1976,8 +1973,23 @@ __global__ void __launch_bounds__(32) cross_attention_xh(
       const uint8_t* Vh = &ring[st][0][0];
       const uint8_t* Vl = &ring[st][1][0];
       uint32_t bh0, bl0, bh1, bl1;
-      split_xh2(Ps[g][16 * kk + 2 * t4], Ps[g][16 * kk + 2 * t4 + 1], bh0, bl0);
-      split_xh2(Ps[g][16 * kk + 2 * t4 + 8], Ps[g][16 * kk + 2 * t4 + 9], bh1, bl1);
+      {
+        // P[beam g][16kk + 2t4 + j (+8)] lives in lane (2t4 + j, g >> 1), element
+        // (g & 1) (+2 for the upper 8 positions)
+        float pv[2][2];
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const int src = (2 * t4 + j) * 4 + (g >> 1);
+          const float v0 = __shfl_sync(0xffffffffu, e[kk][0], src);
+          const float v1 = __shfl_sync(0xffffffffu, e[kk][1], src);
+          const float v2 = __shfl_sync(0xffffffffu, e[kk][2], src);
+          const float v3 = __shfl_sync(0xffffffffu, e[kk][3], src);
+          pv[0][j] = (g & 1) ? v1 : v0;
+          pv[1][j] = (g & 1) ? v3 : v2;
+        }
+        split_xh2(pv[0][0], pv[0][1], bh0, bl0);
+        split_xh2(pv[1][0], pv[1][1], bh1, bl1);
+      }
 #pragma unroll
       for (int m = 0; m < KT; ++m) {
         uint32_t ah[4], al[4];
