@@ -1039,7 +1039,10 @@ __global__ void __launch_bounds__(32 * kCrossWarps) cross_attention_tma(
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tv)));
   }
   __syncwarp();
-  pdl_enter();
+  // the cross K/V buffer is written once per request, before the decode step
+  // graph: its boxes stream in before the grid-dependency wait (only the
+  // query comes from the preceding GEMM)
+  pdl_launch_dependents();
   if (lane == 0) {
     bar_expect(&bar, 2 * NP * 128);
     asm volatile(
@@ -1053,6 +1056,7 @@ __global__ void __launch_bounds__(32 * kCrossWarps) cross_attention_tma(
         "l"(reinterpret_cast<uint64_t>(&tv)), "r"(h * HD), "r"(b * seq), "r"(sm_u32(&bar))
         : "memory");
   }
+  pdl_wait();
   uint32_t qh[HD / 16][2], ql[HD / 16][2];
   {
     const bool ok = g < beam;

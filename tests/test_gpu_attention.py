@@ -221,6 +221,39 @@ def test_cross_attention_stream_kernel(T, H, hd, beam):
     assert _rel(out16[:n].float(), want[:n]) <= 1e-2
 
 
+@pytest.mark.parametrize("beam,S", [(1, 1), (4, 64), (3, 37), (8, 17), (5, 64)])
+def test_cross_attention_fp16_ctx(T, beam, S):
+    """The fp16 mode's cross-attention (fp16 K/V, fp16 context only -- the
+    engine's half_mode call; cross_attention_xh<..., PAIR=false>) vs float64,
+    with a partly and a fully masked item (the latter counted in d_bad)."""
+    A = _abi()
+    g = T.Generator(device="cuda").manual_seed(beam * 100 + S)
+    B, H, hd, L = 4, 16, 64, 2
+    d = H * hd
+    ld = 2 * L * d
+    cq = T.randn(B * beam, d, device="cuda", generator=g)
+    packed = T.randn(B * S, ld, device="cuda", generator=g).to(T.float16)
+    mask = T.zeros(B, S, device="cuda")
+    mask[1, (S + 1) // 2:] = -math.inf
+    mask[3, :] = -math.inf
+    scale = float(np.float32(1 / math.sqrt(hd)))
+    ck, cv = packed[:, 2 * d:], packed[:, 3 * d:]
+    out16 = T.full((B * beam, d), float("nan"), device="cuda", dtype=T.float16)
+    bad = T.zeros(1, dtype=T.int32, device="cuda")
+    A.call("fq_cross_attention", cq.data_ptr(), d, ck.data_ptr(), cv.data_ptr(), 1, ld, B, beam,
+           S, H, hd, scale, mask.data_ptr(), None, out16.data_ptr(), d, 0, bad.data_ptr(),
+           A.stream_handle())
+    T.cuda.synchronize()
+    assert int(bad.item()) == beam * H
+    K = ck[:, :d].double().view(B, S, H, hd).permute(0, 2, 1, 3)
+    V = cv[:, :d].double().view(B, S, H, hd).permute(0, 2, 1, 3)
+    Q = cq.double().view(B, beam, H, hd).permute(0, 2, 1, 3)
+    P = _softmax_ref(T, (Q @ K.transpose(-1, -2)) * scale, mask.double()[:, None, None, :])
+    want = (P @ V).permute(0, 2, 1, 3).reshape(B * beam, d)
+    n = 3 * beam  # items 0..2
+    assert _rel(out16[:n].float(), want[:n]) <= 2e-3
+
+
 @pytest.mark.parametrize("S,hd,exact", [(64, 64, 1), (64, 64, 0), (17, 128, 1), (1, 64, 1),
                                         (64, 32, 0)])
 def test_encoder_attention_tiled(T, S, hd, exact):
