@@ -496,6 +496,19 @@ int fq_decoder_self_attention_xh(const float* sqkv, int64_t ldq, void* kcache, v
                                  int64_t rows, int64_t heads, int64_t head_dim, int64_t max_len,
                                  float scale, float* out, void* out_hi, void* out_lo,
                                  int64_t ldo, fq_stream_t stream);
+/* The same decoder self-attention, one warp per (item, head) with the beams
+ * (rows item*beam .. item*beam + beam-1, beam <= 8, head_dim 64) as the MMA's
+ * query columns: each distinct history slot the item's beams share (via hist)
+ * is read once. Scores and probabilities equal fq_decoder_self_attention_xh's
+ * bit for bit; the context may differ in the last fp32 bit (the P.V terms are
+ * grouped by shared slot, not by position). Opt-in in the engine
+ * (FQ_SELF_ITEMS=1): fewer bytes, but slower at C2 than the per-row kernel. */
+int fq_decoder_self_attention_xh_items(const float* sqkv, int64_t ldq, void* kcache,
+                                       void* vcache, int64_t plane, const int32_t* hist,
+                                       const int32_t* d_cur, int64_t items, int64_t beam,
+                                       int64_t heads, int64_t head_dim, int64_t max_len,
+                                       float scale, float* out, void* out_hi, void* out_lo,
+                                       int64_t ldo, fq_stream_t stream);
 /* Exact-mode encoder self-attention on 3xFP16 warp MMAs (head_dim 64, seq <=
  * 64; model.py:329-336, kernels.py:106-139 softmax): ctx written as the
  * out-projection GEMM's fp16 pair (out_hi, out_lo) and optionally fp32 `out`. */

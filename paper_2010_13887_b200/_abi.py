@@ -97,6 +97,8 @@ SIGNATURES = {
                         I64, I64, P], I32),
     "fq_decoder_self_attention_xh": ([P, I64, P, P, I64, P, P, I64, I64, I64, I64, F32, P, P, P,
                                       I64, P], I32),
+    "fq_decoder_self_attention_xh_items": ([P, I64, P, P, I64, P, P, I64, I64, I64, I64, I64, F32,
+                                            P, P, P, I64, P], I32),
     "fq_cross_attention_xh": ([P, I64, P, P, I64, I64, I64, I64, I64, I64, I64, F32, P, P, P, P,
                                I64, P, P], I32),
     "fq_split_f16": ([P, I64, I64, I64, I32, P, P, I64, P], I32),

@@ -1760,6 +1760,296 @@ __global__ void __launch_bounds__(32) decoder_self_attention_xh(
   }
 }
 
+// Exact-mode decoder self-attention, one CTA of W warps per (item, head) with
+// the beams as the MMA's query columns (head_dim 64, beam 2..8). The beams of
+// an item share most of their K/V history (the history table points their
+// positions at the same physical slots: ~40-55% distinct slots at C2), so
+// each distinct slot (position t, physical row) streams through a ring ONCE
+// and is scored against every beam's query. The slot list is split
+// round-robin over the warps in 16-slot chunks (each warp its own cp.async
+// ring, its K chunks then its V chunks); a beam's softmax runs over ITS
+// positions 0..cur gathered in position order (the per-row kernel's
+// warp_softmax_xh, so p is identical), and O^T = V^T . P^T with P = 0 where a
+// beam does not use the slot, the warps' partial sums added in warp order.
+// Scores and p match decoder_self_attention_xh bit for bit; the context only
+// differs by the grouping of the P.V terms. Measured at C2 (B200): 0.4x the
+// DRAM bytes of the per-row kernel, yet 65.0 vs 63.3 ms per request at the
+// best setting (W = 2, NS = 3; W = 4: 66.6): the kernel is bound by its
+// dependent chunk chains, not by bytes, so it stays opt-in. Dynamic smem: sc[Dpad][beam]
+// (scores, then p), tmp[W][max_len + 16], off[Dmax] (element offset of each
+// distinct slot), idx[beam][max_len] (int16: beam j's slot at position t).
+template <int W, int NS>
+__global__ void __launch_bounds__(32 * W) self_attention_items_xh(
+    const float* __restrict__ sqkv, int64_t ldq, h16* __restrict__ kc, h16* __restrict__ vc,
+    int64_t plane, const int32_t* __restrict__ hist, const int32_t* __restrict__ d_cur,
+    int rows, int beam, int heads, int max_len, float scale, float* __restrict__ out,
+    h16* __restrict__ out_hi, h16* __restrict__ out_lo, int64_t ldo) {
+  constexpr int HD = 64, KT = 4, CPR = 8, MB = 8;
+  auto soff = [](int r, int byte) {
+    return r * 128 + ((((byte >> 4) ^ (r & 7)) << 4) | (byte & 15));
+  };
+  __shared__ __align__(128) uint8_t rings[W][NS][2][16 * 128];
+  __shared__ int s_d;
+  extern __shared__ __align__(16) float dyn[];
+  const int dmax = beam * max_len;
+  const int dpad = (dmax + 15) & ~15;
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float* sc = dyn;                                                     // [dpad][beam]
+  float* tmp = sc + (size_t)dpad * beam + wid * (max_len + 16);        // [W][max_len + 16]
+  int* off = reinterpret_cast<int*>(sc + (size_t)dpad * beam + W * (max_len + 16));  // [dmax]
+  int16_t* idx = reinterpret_cast<int16_t*>(off + dmax);               // [beam][max_len]
+  auto ring = rings[wid];
+  pdl_enter();
+  const int b = blockIdx.x, h = blockIdx.y;
+  const int g = lane >> 2, t4 = lane & 3;
+  const int d = heads * HD;
+  const int cur = *d_cur;
+  const int r0 = b * beam;
+  // this step's k, v of every beam as pairs (each warp keeps them for its ring)
+  uint32_t knh[MB], knl[MB], vnh[MB], vnl[MB];
+#pragma unroll
+  for (int j = 0; j < MB; ++j) {
+    knh[j] = knl[j] = vnh[j] = vnl[j] = 0u;
+    if (j < beam) {
+      const float* rp = sqkv + (int64_t)(r0 + j) * ldq + h * HD + 2 * lane;
+      const float2 kn = *reinterpret_cast<const float2*>(rp + d);
+      const float2 vn = *reinterpret_cast<const float2*>(rp + 2 * d);
+      split_xh2(kn.x, kn.y, knh[j], knl[j]);
+      split_xh2(vn.x, vn.y, vnh[j], vnl[j]);
+    }
+  }
+  if (wid == 0) {
+    // ---- distinct (position, physical row) slots of the item, position order ----
+    int D = 0;
+    for (int t0 = 0; t0 < cur; t0 += 32) {
+      const int t = t0 + lane;
+      int src[MB];
+      unsigned first = 0;
+#pragma unroll
+      for (int j = 0; j < MB; ++j) {
+        src[j] = -1;
+        if (j < beam && t < cur) src[j] = hist[(int64_t)(r0 + j) * max_len + t];
+      }
+#pragma unroll
+      for (int j = 0; j < MB; ++j) {
+        bool f = j < beam && t < cur;
+#pragma unroll
+        for (int k = 0; k < j; ++k) f = f && src[k] != src[j];
+        first |= f ? 1u << j : 0u;
+      }
+      const int n = __popc(first);
+      int incl = n;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      const int u0 = D + incl - n;
+      if (t < cur) {
+#pragma unroll
+        for (int j = 0; j < MB; ++j) {
+          if (j < beam) {
+            int k0 = j;  // the first beam holding the same slot
+#pragma unroll
+            for (int k = MB - 1; k >= 0; --k)
+              if (k < j && src[k] == src[j]) k0 = k;
+            const int u = u0 + __popc(first & ((1u << k0) - 1u));
+            if (k0 == j) off[u] = (t * rows + src[j]) * d + h * HD;
+            idx[j * max_len + t] = (int16_t)u;
+          }
+        }
+      }
+      D += __shfl_sync(0xffffffffu, incl, 31);
+    }
+    if (lane < beam) idx[lane * max_len + cur] = (int16_t)(D + lane);
+    if (lane == 0) s_d = D;
+    // this step's slots (cur, r0 + j): written once, read by later steps
+#pragma unroll
+    for (int j = 0; j < MB; ++j) {
+      if (j < beam) {
+        const int64_t slot = ((int64_t)cur * rows + r0 + j) * d + h * HD + 2 * lane;
+        *reinterpret_cast<uint32_t*>(kc + slot) = knh[j];
+        *reinterpret_cast<uint32_t*>(kc + plane + slot) = knl[j];
+        *reinterpret_cast<uint32_t*>(vc + slot) = vnh[j];
+        *reinterpret_cast<uint32_t*>(vc + plane + slot) = vnl[j];
+      }
+    }
+  }
+  // Q^T fragments: lane (g, t4) holds beam g, dims 16k + {2t4, 2t4+1, 2t4+8, 2t4+9}
+  uint32_t qh[KT][2], ql[KT][2];
+  {
+    const bool ok = g < beam;
+    const float* qp = sqkv + (int64_t)(r0 + (ok ? g : 0)) * ldq + h * HD;
+#pragma unroll
+    for (int kk = 0; kk < KT; ++kk) {
+      const float2 x0 = ok ? *reinterpret_cast<const float2*>(qp + 16 * kk + 2 * t4)
+                           : make_float2(0.f, 0.f);
+      const float2 x1 = ok ? *reinterpret_cast<const float2*>(qp + 16 * kk + 2 * t4 + 8)
+                           : make_float2(0.f, 0.f);
+      split_xh2(x0.x, x0.y, qh[kk][0], ql[kk][0]);
+      split_xh2(x1.x, x1.y, qh[kk][1], ql[kk][1]);
+    }
+  }
+  __syncthreads();
+  const int dprev = s_d;  // slots dprev + j: this step's k, v of beam j (registers)
+  const int D = dprev + beam;
+  const int nchunk = (D + 15) / 16;
+  const int nmine = nchunk > wid ? (nchunk - wid + W - 1) / W : 0;  // chunks wid, wid + W, ...
+  auto issue = [&](const h16* src, int c, int st) {
+    for (int x = lane; x < 16 * CPR; x += 32) {
+      const int rr = x / CPR, ch = x % CPR;
+      const int u = 16 * c + rr;
+      uint8_t* dh = &ring[st][0][0] + soff(rr, ch * 16);
+      uint8_t* dl = &ring[st][1][0] + soff(rr, ch * 16);
+      if (u < dprev) {
+        const h16* p = src + off[u] + ch * 8;
+        cp16(sm_u32(dh), p);
+        cp16(sm_u32(dl), p + plane);
+      } else if (u >= D) {  // padding slots: zeros (p = 0, never NaN)
+        *reinterpret_cast<uint4*>(dh) = make_uint4(0, 0, 0, 0);
+        *reinterpret_cast<uint4*>(dl) = make_uint4(0, 0, 0, 0);
+      }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  auto put_cur = [&](int c, int st, const uint32_t* hi, const uint32_t* lo) {
+#pragma unroll
+    for (int j = 0; j < MB; ++j) {
+      const int u = dprev + j;
+      if (j < beam && u / 16 == c) {
+        *reinterpret_cast<uint32_t*>(&ring[st][0][0] + soff(u % 16, lane * 4)) = hi[j];
+        *reinterpret_cast<uint32_t*>(&ring[st][1][0] + soff(u % 16, lane * 4)) = lo[j];
+      }
+    }
+  };
+  // this warp's chunk sequence: K of chunks wid + W i, then V of the same
+  auto issue_g = [&](int gi) {
+    if (gi < nmine) issue(kc, wid + W * gi, gi % NS);
+    else if (gi < 2 * nmine) issue(vc, wid + W * (gi - nmine), gi % NS);
+    else asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+#pragma unroll
+  for (int c = 0; c < NS - 1; ++c) issue_g(c);
+  const int lrow = (lane & 7) + ((lane >> 3) & 1) * 8, lcol = (lane >> 4) * 8;
+  // ---- pass 1: S^T[16 slots x 8 beams] = K . Q^T per chunk ----
+  for (int i = 0; i < nmine; ++i) {
+    const int c = wid + W * i, st = i % NS;
+    asm volatile("cp.async.wait_group %0;" ::"n"(NS - 2) : "memory");
+    put_cur(c, st, knh, knl);
+    __syncwarp();
+    const uint8_t* Kh = &ring[st][0][0];
+    const uint8_t* Kl = &ring[st][1][0];
+    float big[4] = {0.f, 0.f, 0.f, 0.f}, sml[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int kk = 0; kk < KT; ++kk) {
+      uint32_t ah[4], al[4];
+      ldsm_x4(ah, Kh + soff(lrow, (16 * kk + lcol) * 2));
+      ldsm_x4(al, Kl + soff(lrow, (16 * kk + lcol) * 2));
+      mma_f16_16816(big, ah, qh[kk][0], qh[kk][1]);
+      mma_f16_16816(sml, ah, ql[kk][0], ql[kk][1]);
+      mma_f16_16816(sml, al, qh[kk][0], qh[kk][1]);
+    }
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int u = 16 * c + g + 8 * (e >> 1), j = 2 * t4 + (e & 1);
+      if (j < beam) sc[u * beam + j] = fmul_rn(fadd_rn(big[e], sml[e] * kXhInv), scale);
+    }
+    __syncwarp();  // stage st consumed
+    issue_g(i + NS - 1);
+  }
+  __syncthreads();
+  // ---- per beam: exact softmax over its positions 0..cur, in position order ----
+  const int npos = cur + 1;
+  for (int j = wid; j < beam; j += W) {
+    const int16_t* ij = idx + j * max_len;
+    for (int t = lane; t < npos; t += 32) tmp[t] = sc[ij[t] * beam + j];
+    __syncwarp();
+    warp_softmax_xh(tmp, npos);
+    for (int u = lane; u < 16 * nchunk; u += 32) sc[u * beam + j] = 0.0f;
+    __syncwarp();
+    for (int t = lane; t < npos; t += 32) sc[ij[t] * beam + j] = tmp[t];
+  }
+  __syncthreads();
+  // ---- pass 2: O^T[HD x 8 beams] += V^T . P^T over this warp's chunks ----
+  float ob[KT][4], os[KT][4];
+#pragma unroll
+  for (int m = 0; m < KT; ++m)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) ob[m][e] = os[m][e] = 0.0f;
+  const int mi = lane >> 3;
+  const int vrow = (lane & 7) + ((mi >> 1) & 1) * 8, vcol = (mi & 1) * 8;
+  for (int i = 0; i < nmine; ++i) {
+    const int c = wid + W * i, st = (nmine + i) % NS;
+    asm volatile("cp.async.wait_group %0;" ::"n"(NS - 2) : "memory");
+    put_cur(c, st, vnh, vnl);
+    __syncwarp();
+    const uint8_t* Vh = &ring[st][0][0];
+    const uint8_t* Vl = &ring[st][1][0];
+    uint32_t bh0, bl0, bh1, bl1;
+    {
+      // P^T[slot 16c + 2t4 (+1, +8, +9)][beam g]
+      const bool ok = g < beam;
+      const float* pp = sc + (16 * c + 2 * t4) * beam + g;
+      split_xh2(ok ? pp[0] : 0.f, ok ? pp[beam] : 0.f, bh0, bl0);
+      split_xh2(ok ? pp[8 * beam] : 0.f, ok ? pp[9 * beam] : 0.f, bh1, bl1);
+    }
+#pragma unroll
+    for (int m = 0; m < KT; ++m) {
+      uint32_t ah[4], al[4];
+      ldsm_x4_t(ah, Vh + soff(vrow, (16 * m + vcol) * 2));
+      ldsm_x4_t(al, Vl + soff(vrow, (16 * m + vcol) * 2));
+      mma_f16_16816(ob[m], ah, bh0, bh1);
+      mma_f16_16816(os[m], ah, bl0, bl1);
+      mma_f16_16816(os[m], al, bh0, bh1);
+    }
+    __syncwarp();
+    issue_g(nmine + i + NS - 1);
+  }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+  if (W > 1) {  // partial sums of warps 1.. through their (drained) rings, added in warp order
+    float* red = reinterpret_cast<float*>(&ring[0][0][0]);  // 32 lanes x 32 floats = 4 KB
+    if (wid > 0) {
+#pragma unroll
+      for (int m = 0; m < KT; ++m)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          red[(m * 4 + e) * 32 + lane] = ob[m][e];
+          red[(16 + m * 4 + e) * 32 + lane] = os[m][e];
+        }
+    }
+    __syncthreads();
+    if (wid > 0) return;
+#pragma unroll
+    for (int w = 1; w < W; ++w) {
+      const float* rw = reinterpret_cast<const float*>(&rings[w][0][0][0]);
+#pragma unroll
+      for (int m = 0; m < KT; ++m)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          ob[m][e] += rw[(m * 4 + e) * 32 + lane];
+          os[m][e] += rw[(16 + m * 4 + e) * 32 + lane];
+        }
+    }
+  }
+  // ---- store: lane holds dims {16m + g, +8} x beams {2t4, 2t4+1} ----
+#pragma unroll
+  for (int jj = 0; jj < 2; ++jj) {
+    const int j = 2 * t4 + jj;
+    if (j >= beam) continue;
+    const int64_t o = (int64_t)(r0 + j) * ldo + h * HD;
+#pragma unroll
+    for (int m = 0; m < KT; ++m) {
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh) {
+        const int dd = 16 * m + g + 8 * hh;
+        const float v = fadd_rn(ob[m][2 * hh + jj], os[m][2 * hh + jj] * kXhInv);
+        if (out) out[o + dd] = v;
+        if (out_hi) split_xh(v, out_hi[o + dd], out_lo[o + dd]);
+      }
+    }
+  }
+}
+
 // Exact-mode cross-attention (3xFP16 warp MMAs), warp per (item, head), beams
 // as the MMA's 8 query columns. The item's K then V head slices (fp16 pair
 // planes of the cross-K/V buffer, [2][items * seq][ldkv]) stream through a
@@ -2191,7 +2481,12 @@ int attention_xh_prepare() {
 #define FQ_XH_OPT(HD)                                                                           \
   cudaFuncSetAttribute(decoder_self_attention_xh<HD, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sz) || \
       cudaFuncSetAttribute(decoder_self_attention_xh<HD, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, sz)
-  if (FQ_XH_OPT(16) || FQ_XH_OPT(32) || FQ_XH_OPT(64) || FQ_XH_OPT(128)) {
+  if (FQ_XH_OPT(16) || FQ_XH_OPT(32) || FQ_XH_OPT(64) || FQ_XH_OPT(128) ||
+      cudaFuncSetAttribute(self_attention_items_xh<1, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sz) ||
+      cudaFuncSetAttribute(self_attention_items_xh<1, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, sz) ||
+      cudaFuncSetAttribute(self_attention_items_xh<2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sz) ||
+      cudaFuncSetAttribute(self_attention_items_xh<2, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, sz) ||
+      cudaFuncSetAttribute(self_attention_items_xh<4, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sz)) {
     set_error("fq_prepare: cannot opt in to large shared memory (exact attention)");
     return FQ_ERR_CUDA;
   }
@@ -2386,6 +2681,42 @@ int fq_decoder_self_attention_xh(const float* sqkv, int64_t ldq, void* kcache, v
   else FQ_SELF_XH(128);
 #undef FQ_SELF_XH
   return launch_status("fq_decoder_self_attention_xh");
+}
+
+int fq_decoder_self_attention_xh_items(const float* sqkv, int64_t ldq, void* kcache,
+                                       void* vcache, int64_t plane, const int32_t* hist,
+                                       const int32_t* d_cur, int64_t items, int64_t beam,
+                                       int64_t heads, int64_t head_dim, int64_t max_len,
+                                       float scale, float* out, void* out_hi, void* out_lo,
+                                       int64_t ldo, fq_stream_t stream) {
+  FQ_CHECK_ARG(sqkv && kcache && vcache && hist && d_cur && (out || out_hi) &&
+                   (!out_hi == !out_lo) && items > 0 && beam >= 1 && beam <= 8 && heads > 0 &&
+                   max_len > 0 && head_dim == 64 && ldq % 2 == 0 && ((uintptr_t)sqkv & 7) == 0 &&
+                   plane % 8 == 0 && ((uintptr_t)kcache & 15) == 0 &&
+                   ((uintptr_t)vcache & 15) == 0,
+               FQ_ERR_DIMENSION, "fq_decoder_self_attention_xh_items: bad args");
+  FQ_CHECK_ARG(plane < (1LL << 31) && beam * max_len <= 32767, FQ_ERR_CAPACITY,
+               "fq_decoder_self_attention_xh_items: cache too large");
+  const int64_t dmax = beam * max_len, dpad = (dmax + 15) & ~15LL;
+  static int ns = -1, nw = -1;  // ring depth / warps per CTA (FQ_XH_ITEMS_STAGES, _WARPS: A/B)
+  if (ns < 0) {
+    const char* e = getenv("FQ_XH_ITEMS_STAGES");
+    ns = (e && e[0] == '2') ? 2 : 3;
+    e = getenv("FQ_XH_ITEMS_WARPS");
+    nw = e ? atoi(e) : 2;
+    if (nw != 1 && nw != 4) nw = 2;
+  }
+  const size_t smem = (size_t)(dpad * beam + nw * (max_len + 16) + dmax) * 4 + (size_t)dmax * 2;
+  FQ_CHECK_ARG(smem <= 160 * 1024, FQ_ERR_CAPACITY,
+               "decoder self-attention (items): beam x max_len too large");
+  const dim3 grid((unsigned)items, (unsigned)heads);
+  auto kern = nw == 1   ? (ns == 3 ? self_attention_items_xh<1, 3> : self_attention_items_xh<1, 2>)
+              : nw == 2 ? (ns == 3 ? self_attention_items_xh<2, 3> : self_attention_items_xh<2, 2>)
+                        : self_attention_items_xh<4, 2>;  // (48 KB static smem cap)
+  launch_kernel(kern, grid, 32 * nw, smem, as_stream(stream), 1u, sqkv, ldq, (h16*)kcache, (h16*)vcache, plane, hist,
+                d_cur, (int)(items * beam), (int)beam, (int)heads, (int)max_len, scale, out,
+                (h16*)out_hi, (h16*)out_lo, ldo);
+  return launch_status("fq_decoder_self_attention_xh_items");
 }
 
 static int cross_xh_launch(const float* cq, int64_t ldcq, const void* ck, const void* cv,

@@ -38,6 +38,12 @@ from .ops import attention_scale
 from .tensor import (ACT_IDS, OpCounters, Timers, as_device, gemm, gemm_x3, gemm_xh,
                      global_counters, split_pair)
 
+# FQ_SELF_ITEMS=1: the exact-mode decoder self-attention per (item, head) over
+# the history slots the beams share (read once). Opt-in: at C2 it reads 0.4x
+# the bytes but runs 2.7% slower per request than the per-row kernel (fewer,
+# longer dependent chunk chains; scripts/self_items_ab.sh)
+_SELF_ITEMS = os.environ.get("FQ_SELF_ITEMS", "0") == "1"
+
 F32 = np.float32
 I64 = np.int64
 PRECISIONS = ("fp32", "fp16")
@@ -891,10 +897,17 @@ class DecoderStep:
         R, d, h, hd = self.rows, c.d_model, c.num_heads, c.head_dim
         k, v = self.cache._k[i], self.cache._v[i]
         sh, sl = self.sctx16
-        _abi.call("fq_decoder_self_attention_xh", self.sqkv.data_ptr(), self.sqkv.stride(0),
-                  k.data_ptr(), v.data_ptr(), self.cache.plane, self.cache.hist.data_ptr(),
-                  self.cache.d_cur.data_ptr(), R, h, hd, c.max_seq_len, scale, None,
-                  sh.data_ptr(), sl.data_ptr(), sh.stride(0), stream)
+        if self.beam > 1 and hd == 64 and _SELF_ITEMS:  # beams share history slots
+            _abi.call("fq_decoder_self_attention_xh_items", self.sqkv.data_ptr(),
+                      self.sqkv.stride(0), k.data_ptr(), v.data_ptr(), self.cache.plane,
+                      self.cache.hist.data_ptr(), self.cache.d_cur.data_ptr(), self.batch,
+                      self.beam, h, hd, c.max_seq_len, scale, None, sh.data_ptr(), sl.data_ptr(),
+                      sh.stride(0), stream)
+        else:
+            _abi.call("fq_decoder_self_attention_xh", self.sqkv.data_ptr(), self.sqkv.stride(0),
+                      k.data_ptr(), v.data_ptr(), self.cache.plane, self.cache.hist.data_ptr(),
+                      self.cache.d_cur.data_ptr(), R, h, hd, c.max_seq_len, scale, None,
+                      sh.data_ptr(), sl.data_ptr(), sh.stride(0), stream)
         ctr.count_fused("decoder_self_attention", R * d * 16)
         _lin_ln(dw, self.sctx, self.sctx16, lw["w_so"], lw["b_so"], x, lw["ln1_g"], lw["ln1_b"],
                 c.ln_eps, self.snorm, self.snorm16, self.ln_ws, counters=ctr, timers=tm)

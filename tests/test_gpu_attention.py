@@ -409,3 +409,60 @@ def test_cross_attention_xh_slab_query_bit_identical(T):
         assert int(bad.item()) == 0
         outs.append((oh, ol))
     assert T.equal(outs[0][0], outs[1][0]) and T.equal(outs[0][1], outs[1][1])
+
+
+@pytest.mark.parametrize("beam,cur,S", [(4, 13, 64), (4, 0, 64), (4, 63, 64), (2, 16, 32),
+                                        (8, 31, 40), (3, 15, 20), (4, 100, 128)])
+def test_self_attention_items_xh(T, beam, cur, S):
+    """The exact self-attention per (item, head) over the distinct history
+    slots of the item's beams vs the per-row kernel on the same pair cache:
+    the same slot writes, contexts within the last fp32 bits (only the
+    grouping of the P.V terms differs), both vs float64."""
+    A = _abi()
+    g = T.Generator(device="cuda").manual_seed(beam * 1000 + cur)
+    items, H, hd = 5, 4, 64
+    rows, d = items * beam, H * hd
+    kv = T.randn(2, S, rows, d, device="cuda", generator=g)
+
+    def pair(x):
+        hi = x.half()
+        return T.stack([hi, ((x - hi.float()) * 2048).half()])
+
+    kc, vc = pair(kv[0]), pair(kv[1])  # [2 (hi, lo), S, rows, d]
+    hist = T.empty(rows, S, dtype=T.int32, device="cuda")
+    share = T.randint(0, 3, (items, S), generator=g, device="cuda")
+    for r in range(rows):
+        it = r // beam
+        own = T.randint(it * beam, (it + 1) * beam, (S,), generator=g, device="cuda")
+        # mostly shared (one row for all beams), some positions diverging
+        hist[r] = T.where(share[it] > 0, it * beam + share[it] % beam, own).int()
+    sqkv = T.randn(rows, 3 * d, device="cuda", generator=g)
+    d_cur = T.tensor([cur], dtype=T.int32, device="cuda")
+    scale = float(np.float32(1 / math.sqrt(hd)))
+    plane = S * rows * d
+    outs = []
+    for fn in ("fq_decoder_self_attention_xh", "fq_decoder_self_attention_xh_items"):
+        k2, v2 = kc.clone(), vc.clone()
+        out = T.empty(rows, d, device="cuda")
+        oh = T.empty(rows, d, device="cuda", dtype=T.float16)
+        ol = T.empty_like(oh)
+        shape = (rows,) if fn.endswith("_xh") else (items, beam)
+        A.call(fn, sqkv.data_ptr(), 3 * d, k2.data_ptr(), v2.data_ptr(), plane, hist.data_ptr(),
+               d_cur.data_ptr(), *shape, H, hd, S, scale, out.data_ptr(), oh.data_ptr(),
+               ol.data_ptr(), d, A.stream_handle())
+        T.cuda.synchronize()
+        outs.append((out, oh, ol, k2, v2))
+    (o0, h0, l0, k0, v0), (o1, h1, l1, k1, v1) = outs
+    assert T.equal(k0, k1) and T.equal(v0, v1)  # this step's slots, written once
+    assert _rel(o1, o0.double()) <= 1e-6
+    assert T.equal(h1, o1.half())
+    kd = (k1[0].double() + k1[1].double() / 2048)
+    vd = (v1[0].double() + v1[1].double() / 2048)
+    ar = T.arange(cur + 1, device="cuda")
+    for r in range(rows):
+        idx = T.cat([hist[r, :cur].long(), T.tensor([r], device="cuda")])
+        Kr, Vr = kd[ar, idx].view(cur + 1, H, hd), vd[ar, idx].view(cur + 1, H, hd)
+        q = sqkv[r, :d].double().view(H, hd)
+        p = T.softmax(T.einsum("the,he->ht", Kr, q) * scale, dim=1)
+        want = T.einsum("ht,the->he", p, Vr).reshape(d)
+        assert _rel(o1[r], want) <= 1e-5, r
