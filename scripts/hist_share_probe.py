@@ -21,8 +21,6 @@ for s in (8, 16, 32, 48, 63):
     hist = sess._buffers.get("dec.cache.hist", (512, 64), torch.int32).cpu().numpy()
     cur = int(sess._buffers.get("dec.cache.cur", (1,), torch.int32).item())
     h = hist[:, :cur].reshape(128, 4, cur)
-    distinct = sum(len(set(zip(np.repeat(np.arange(cur), 1), h[i, j]))) for i in range(128)
-                   for j in range(1))  # placeholder
     tot = 0
     for i in range(128):
         tot += sum(len(set(h[i, :, t].tolist())) for t in range(cur))
