@@ -398,6 +398,14 @@ __device__ __forceinline__ void mma_commit_mc(uint64_t* bar, uint16_t mask) {
       : "memory");
 }
 
+// End of a TMA-store epilogue: the bulk stores complete (smem read, global
+// writes performed) before the CTA moves on or exits. (Waiting only for the
+// smem reads, .read, measured neutral at C2: the dependent grid waits for
+// this grid's completion either way.)
+__device__ __forceinline__ void tma_store_drain() {
+  asm volatile("cp.async.bulk.wait_group %0;" ::"n"(0) : "memory");
+}
+
 // Per-CTA phase stamps for scripts/xh_cta_anatomy.py: compiled in only with
 // -DFQ_GEMM_STAMPS (scripts/build_variant.sh), off the product path.
 __device__ __forceinline__ void dbg_stamp(unsigned long long* dbg, int slot) {
@@ -972,9 +980,8 @@ __global__ void __launch_bounds__(threads_of<OP>(), 1)
       }
     }
   }
-  if constexpr (!HS) {  // TMA stores complete (smem read, writes performed) before exit
-    if (ep.tstore && warp >= 2 && warp < 6 && lane == 0)
-      asm volatile("cp.async.bulk.wait_group %0;" ::"n"(0) : "memory");
+  if constexpr (!HS) {  // TMA stores complete before exit
+    if (ep.tstore && warp >= 2 && warp < 6 && lane == 0) tma_store_drain();
   }
   if (threadIdx.x == 64) dbg_stamp(ep.dbg, 5);  // epilogue done
   __syncwarp();
@@ -1095,6 +1102,7 @@ __global__ void __launch_bounds__(threads_of<OP>(), 1)
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = tmem_base_sh;
+  if (threadIdx.x == 0) dbg_stamp(ep.dbg, 1);
 
   if (warp == 0) {
     if (lane == 0) {  // ---- TMA producer: this CTA's K slice ----
@@ -1140,6 +1148,7 @@ __global__ void __launch_bounds__(threads_of<OP>(), 1)
             const int s = it % STAGES;
             if constexpr (X3) mbar_wait(&conv_bar[s], (it / STAGES) & 1);
             else mbar_wait(&full_bar[s], (it / STAGES) & 1);
+            if (it == 0) dbg_stamp(ep.dbg, 2);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             const uint32_t a_base = smem_u32(smem + s * STAGE_BYTES);
             const uint32_t b_base = a_base + B_OFF;
@@ -1153,6 +1162,7 @@ __global__ void __launch_bounds__(threads_of<OP>(), 1)
           }
           mma_commit(&xfull_bar[slot]);
         }
+        dbg_stamp(ep.dbg, 7);  // every MMA issued
       } else {
         for (int kb = kb0, it = 0; kb < kb1; ++kb, ++it) {
           const int s = it % STAGES;
@@ -1206,6 +1216,7 @@ __global__ void __launch_bounds__(threads_of<OP>(), 1)
       mbar_wait(&tfull_bar, 0);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     }
+    if (threadIdx.x == 64) dbg_stamp(ep.dbg, 4);  // the slice's chunks summed
     auto acc_chunk = [&](float (&v)[32], const int cc) {
       if constexpr (XS) {
 #pragma unroll
@@ -1234,7 +1245,7 @@ __global__ void __launch_bounds__(threads_of<OP>(), 1)
           if (lane == 0 && m0 + q * 32 < M)  // M % 32 == 0: whole boxes inside the slab
             tma_store_2d(&tma_c, box, n0 + cc, rank * M + m0 + q * 32);
         }
-        if (lane == 0) asm volatile("cp.async.bulk.wait_group %0;" ::"n"(0) : "memory");
+        if (lane == 0) tma_store_drain();
         __syncwarp();
       }
     }
@@ -1264,6 +1275,7 @@ __global__ void __launch_bounds__(threads_of<OP>(), 1)
       }
     }
   }
+  if (threadIdx.x == 64) dbg_stamp(ep.dbg, 5);  // epilogue stores issued
   if constexpr (SLAB) {
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
@@ -1820,7 +1832,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
-    if (lane == 0) asm volatile("cp.async.bulk.wait_group %0;" ::"n"(0) : "memory");
+    if (lane == 0) tma_store_drain();
   }
   __syncwarp();
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");

@@ -27,7 +27,15 @@ for sh in shapes.split(","):
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     dbg = torch.zeros(8 * 4096, dtype=torch.int64, device="cuda")
 
+    slab_ws = torch.empty(8 * M * N, device="cuda")
+    nsl = ctypes.c_int32(0)
+
     def run(w):
+        if os.environ.get("SLABS"):  # the decode N = 1024 GEMMs: split-K slabs, no reduction
+            _abi.call("fq_gemm_x3h_slabs", a[0].data_ptr(), a[1].data_ptr(), K, w.hi.data_ptr(),
+                      w.lo.data_ptr(), K, slab_ws.data_ptr(), slab_ws.numel() * 4, M, N, K,
+                      ctypes.addressof(nsl), _abi.stream_handle())
+            return
         _abi.call("fq_gemm_x3h", a[0].data_ptr(), a[1].data_ptr(), K, w.hi.data_ptr(),
                   w.lo.data_ptr(), K, c.data_ptr(), N, M, N, K, 0, bias.data_ptr(), None, 0, 1,
                   _abi.stream_handle())
