@@ -1757,13 +1757,26 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else {  // ---- epilogue: warps 2..5, this CTA's 128 rows ----
-    pdl_wait();
     const int q = warp & 3;
     uint8_t* box = boxes + (warp - 2) * 4096;
+    // the tile's bias (a constant) staged in shared memory while the MMAs run:
+    // the first tile's before the grid-dependency wait, so the epilogue's adds
+    // do not wait on a global round trip
+    __shared__ __align__(16) float s_bias[BN];
+    const int et = threadIdx.x - 64;  // 0..127
+    auto stage_bias = [&](int n0) {
+      if (!ep.bias) return;
+      asm volatile("bar.sync 1, 128;" ::: "memory");  // previous tile's reads done
+      if (et < BN) s_bias[et] = __ldg(ep.bias + n0 + et);
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+    };
+    if (pid < ngroups) stage_bias((pid / mt) * BN);
+    pdl_wait();
     int gc = 0;
     for (int g = pid; g < ngroups; g += npairs) {
       const int m0 = (g % mt) * 2 * BM + (int)rank * BM, n0 = (g / mt) * BN;
       const int rbase = m0 + q * 32;
+      if (g != pid) stage_bias(n0);
       float racc[BN];
       for (int kb0 = 0; kb0 < num_kb; kb0 += CH, ++gc) {
         const int slot = gc & 1;
@@ -1790,7 +1803,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (ep.bias) {
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
-            const float4 b = __ldg(reinterpret_cast<const float4*>(ep.bias + col0 + 4 * i));
+            const float4 b = *reinterpret_cast<const float4*>(s_bias + j * 32 + 4 * i);
             v[4 * i] = fadd_rn(v[4 * i], b.x);
             v[4 * i + 1] = fadd_rn(v[4 * i + 1], b.y);
             v[4 * i + 2] = fadd_rn(v[4 * i + 2], b.z);
