@@ -389,15 +389,18 @@ def test_xh_gemm_matches_f64(P, M, N, K):
 
 
 @pytest.mark.parametrize("act", ["none", "relu", "gelu"])
-def test_xh_gemm_epilogue_bits_vs_separate_ops(P, act):
-    """Fused bias / act / residual epilogue == the GEMM then fq_bias_residual_act."""
+@pytest.mark.parametrize("M,N,K,with_res", [(384, 1536, 512, True), (512, 4096, 1024, False),
+                                            (512, 3072, 1024, False), (4096, 3072, 1024, False)])
+def test_xh_gemm_epilogue_bits_vs_separate_ops(P, act, M, N, K, with_res):
+    """Fused bias / act / residual epilogue == the GEMM then fq_bias_residual_act
+    (without a residual: the CTA-pair kernels of the decode FFN1 / QKV shapes,
+    whose bias is staged in shared memory, one and several tiles per CTA)."""
     import torch
-    M, N, K = 384, 1536, 512
-    g = torch.Generator(device="cuda").manual_seed(11)
+    g = torch.Generator(device="cuda").manual_seed(11 + M + N)
     a = torch.randn(M, K, device="cuda", generator=g)
     b = torch.randn(N, K, device="cuda", generator=g) * 0.05
     bias = torch.randn(N, device="cuda", generator=g)
-    res = torch.randn(M, N, device="cuda", generator=g)
+    res = torch.randn(M, N, device="cuda", generator=g) if with_res else None
     fused = torch.empty(M, N, device="cuda")
     _xh(a, b, fused, bias=bias, residual=res, activation=act)
     plain = torch.empty(M, N, device="cuda")
