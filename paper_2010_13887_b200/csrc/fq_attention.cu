@@ -2112,6 +2112,17 @@ __global__ void __launch_bounds__(32) cross_attention_xh(
   };
 #pragma unroll
   for (int c = 0; c < NS - 1; ++c) issue_g(c);
+  // the padding mask is written with the cross K/V (once per request): this
+  // lane's mask values (positions 16m + g, + 8) also before the wait
+  const float* mk = mask ? mask + (int64_t)b * seq : nullptr;
+  float mvr[NT][2];
+#pragma unroll
+  for (int m = 0; m < NT; ++m)
+#pragma unroll
+    for (int hh = 0; hh < 2; ++hh) {
+      const int p = 16 * m + g + 8 * hh;
+      mvr[m][hh] = (mk && p < seq) ? mk[p] : 0.0f;
+    }
   pdl_wait();
   // Q^T fragments: lane (g, t4) holds beam g, dims 16k + {2t4, 2t4+1, 2t4+8, 2t4+9}
   uint32_t qh[KT][2], ql[KT][2];
@@ -2191,7 +2202,6 @@ __global__ void __launch_bounds__(32) cross_attention_xh(
     }
   }
   // ---- exact softmax per beam column (lane: columns 2t4, 2t4+1) ----
-  const float* mk = mask ? mask + (int64_t)b * seq : nullptr;
   float mx0 = -INFINITY, mx1 = -INFINITY;
 #pragma unroll
   for (int m = 0; m < NT; ++m) {
@@ -2203,7 +2213,7 @@ __global__ void __launch_bounds__(32) cross_attention_xh(
         t0 = fmul_rn(sc[m][2 * hh], scale);
         t1 = fmul_rn(sc[m][2 * hh + 1], scale);
         if (mk) {
-          const float mv = mk[p];
+          const float mv = mvr[m][hh];
           t0 = fadd_rn(t0, mv);
           t1 = fadd_rn(t1, mv);
         }
