@@ -1604,10 +1604,31 @@ __global__ void __launch_bounds__(32) decoder_self_attention_xh(
   const int r = blockIdx.x, h = blockIdx.y, lane = threadIdx.x;
   const int g = lane >> 2, t4 = lane & 3;
   const int d = heads * HD;
+  // this row's q, k, v first: they do not depend on the position, so their
+  // round trip overlaps the d_cur -> history-table chain below
+  const float* rowp = sqkv + (int64_t)r * ldq + h * HD;
+  float2 kn[KE], vn[KE];
+#pragma unroll
+  for (int i = 0; i < KE; ++i) {
+    const int e = 2 * lane + 64 * i;
+    kn[i] = vn[i] = make_float2(0.f, 0.f);
+    if (e < HD) {
+      kn[i] = *reinterpret_cast<const float2*>(rowp + d + e);
+      vn[i] = *reinterpret_cast<const float2*>(rowp + 2 * d + e);
+    }
+  }
+  float2 qx[KT][2];
+#pragma unroll
+  for (int kk = 0; kk < KT; ++kk) {
+    qx[kk][0] = qx[kk][1] = make_float2(0.f, 0.f);
+    if (g == 0) {
+      qx[kk][0] = *reinterpret_cast<const float2*>(rowp + 16 * kk + 2 * t4);
+      qx[kk][1] = *reinterpret_cast<const float2*>(rowp + 16 * kk + 2 * t4 + 8);
+    }
+  }
   const int cur = *d_cur;
   for (int t = lane; t < cur; t += 32)
     off_s[t] = (t * rows + hist[(int64_t)r * max_len + t]) * d + h * HD;
-  const float* rowp = sqkv + (int64_t)r * ldq + h * HD;
   // this step's k, v as pairs -> cache slot (cur, r); kept for the ring
   uint32_t knh[KE], knl[KE], vnh[KE], vnl[KE];
   {
@@ -1616,10 +1637,8 @@ __global__ void __launch_bounds__(32) decoder_self_attention_xh(
     for (int i = 0; i < KE; ++i) {
       const int e = 2 * lane + 64 * i;
       if (e < HD) {
-        const float2 kn = *reinterpret_cast<const float2*>(rowp + d + e);
-        const float2 vn = *reinterpret_cast<const float2*>(rowp + 2 * d + e);
-        split_xh2(kn.x, kn.y, knh[i], knl[i]);
-        split_xh2(vn.x, vn.y, vnh[i], vnl[i]);
+        split_xh2(kn[i].x, kn[i].y, knh[i], knl[i]);
+        split_xh2(vn[i].x, vn[i].y, vnh[i], vnl[i]);
         *reinterpret_cast<uint32_t*>(kc + slot + e) = knh[i];
         *reinterpret_cast<uint32_t*>(kc + plane + slot + e) = knl[i];
         *reinterpret_cast<uint32_t*>(vc + slot + e) = vnh[i];
@@ -1631,13 +1650,8 @@ __global__ void __launch_bounds__(32) decoder_self_attention_xh(
   uint32_t qh[KT][2], ql[KT][2];
 #pragma unroll
   for (int kk = 0; kk < KT; ++kk) {
-    float2 x0 = make_float2(0.f, 0.f), x1 = x0;
-    if (g == 0) {
-      x0 = *reinterpret_cast<const float2*>(rowp + 16 * kk + 2 * t4);
-      x1 = *reinterpret_cast<const float2*>(rowp + 16 * kk + 2 * t4 + 8);
-    }
-    split_xh2(x0.x, x0.y, qh[kk][0], ql[kk][0]);
-    split_xh2(x1.x, x1.y, qh[kk][1], ql[kk][1]);
+    split_xh2(qx[kk][0].x, qx[kk][0].y, qh[kk][0], ql[kk][0]);
+    split_xh2(qx[kk][1].x, qx[kk][1].y, qh[kk][1], ql[kk][1]);
   }
   __syncwarp();
   const int npos = cur + 1, nchunk = (npos + 15) / 16;
